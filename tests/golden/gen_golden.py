@@ -1,0 +1,88 @@
+"""Generate golden vectors from the UNMODIFIED reference package.
+
+Run in the build container (where the reference is mounted read-only):
+
+    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/gen_golden.py
+
+Writes ``tests/golden/<case>.npz`` with the reference's topology arrays,
+switch bits, residual R(u), tangent J(u)du, mixed gradient q(u) and
+homogeneous dq(du) for each case in ``tests/cases.py``, plus Newton-GMRES
+histories for the solve cases.  The reference never runs on the GPU box;
+these committed files are what pins the oracle there.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent.parent))
+sys.path.insert(0, str(HERE.parent))
+
+from ldgkit import master as R_master  # noqa: E402
+from ldgkit import mesh as R_mesh  # noqa: E402
+from ldgkit import model as R_model  # noqa: E402
+from ldgkit.disc import LdgSystem, SolverState  # noqa: E402
+from ldgkit.driver import _steady_fns, build_pde_block_jacobi  # noqa: E402
+from ldgkit.solver import NewtonOptions  # noqa: E402
+from ldgkit.timeint import solve_steady  # noqa: E402
+
+from cases import ACCEPT_FLAGS, CASES, SOLVE_CASES, build_case, seeded_state  # noqa: E402
+
+
+def topo_arrays(sys_):
+    t = sys_.topology
+    return dict(elem_l=t.elem_l, face_l=t.face_l, elem_r=t.elem_r, face_r=t.face_r,
+                translation=t.translation, elem_b=t.elem_b, face_b=t.face_b,
+                tag_b=t.tag_b, n_true_interior=np.array(t.n_true_interior),
+                switch=sys_.fi_switch, connectivity=sys_.mesh.connectivity)
+
+
+def gen_case(name, spec):
+    model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
+    s = LdgSystem(model, mesh, topo, master)
+    ne, nb, ncu = s.n_elements, s.n_nodes, s.ncu
+    u = seeded_state(ne, nb, ncu, 1)
+    du = seeded_state(ne, nb, ncu, 0)
+    st = SolverState(u=u, q=None, w=None, t=0.0)
+    R = s.residual(st)[0]
+    J = s.residual_tangent(st, du)[0]
+    out = dict(u=u, du=du, R=R, Jdu=J, **topo_arrays(s))
+    if s.kind == "D":
+        out["q"] = s.compute_mixed(u, 0.0)
+        out["dq"] = s.compute_mixed(du, 0.0, homogeneous=True)
+    out["node_x"] = s.disc.node_x
+    out["fi_h"] = s.disc.fi_h
+    out["mass_inv0"] = s.disc.mass_inv[0]
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, ne * nb * ncu, "dofs", float(np.abs(R).max()), float(np.abs(J).max()))
+
+
+def gen_solve(name, spec):
+    model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
+    s = LdgSystem(model, mesh, topo, master)
+    st = s.interpolate_initial()
+    f = ACCEPT_FLAGS
+    opts = NewtonOptions(abs_tol=f["abs_tol"], rel_tol=f["rel_tol"], max_iter=20,
+                         forcing=f["forcing"], gmres_restart=f["restart"],
+                         gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent")
+    pre = None
+    if spec["precond"] == "block_jacobi":
+        rf, tf = _steady_fns(s)
+        pre = build_pde_block_jacobi(s, rf, tf, s.pack(st.u), "tangent")
+    out_state, stats = solve_steady(s, st, opts, precond=pre)
+    np.savez_compressed(HERE / f"solve_{name}.npz", u=out_state.u,
+                        newton_iters=np.array(stats.newton_iters),
+                        gmres_iters=np.array(stats.gmres_iters),
+                        residual_norms=np.array(stats.residual_norms))
+    print("solve", name, stats.newton_iters, stats.gmres_iters)
+
+
+if __name__ == "__main__":
+    for n, sp in CASES.items():
+        gen_case(n, sp)
+    for n, sp in SOLVE_CASES.items():
+        gen_solve(n, sp)

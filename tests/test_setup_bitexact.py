@@ -1,0 +1,67 @@
+"""Setup layer (reference element, mesh, face topology) is bit-exact with
+the reference: against committed golden arrays everywhere, and against the
+live reference package when it is importable (build container)."""
+
+import sys
+
+import numpy as np
+import pytest
+
+from cases import CASES, GOLDEN, b200_setup, build_case
+from conftest import REFERENCE_SRC, reference_available
+
+TOPO = ("elem_l", "face_l", "elem_r", "face_r", "translation", "elem_b",
+        "face_b", "tag_b")
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_topology_matches_golden(name):
+    g = np.load(GOLDEN / f"{name}.npz")
+    model, mesh, topo, master = build_case(CASES[name], *b200_setup())
+    assert np.array_equal(mesh.connectivity, g["connectivity"])
+    for k in TOPO:
+        assert np.array_equal(getattr(topo, k), g[k]), k
+    assert topo.n_true_interior == int(g["n_true_interior"])
+
+
+needs_ref = pytest.mark.skipif(not reference_available(),
+                               reason="reference package not mounted")
+
+
+@needs_ref
+@pytest.mark.parametrize("kind,p", [(k, p) for k in ("line", "tri", "quad", "tet", "hex")
+                                    for p in (1, 2, 3, 5)])
+def test_master_bitexact_vs_reference(kind, p):
+    sys.path.insert(0, REFERENCE_SRC)
+    from ldgkit import master as RM
+    from paper_2205_07824_b200 import refelem
+    a, b = RM.build_master(kind, p), refelem.build_master(kind, p)
+    for nm in ("nodes", "quad_pts", "quad_wts", "phi", "dphi", "vandermonde_inv"):
+        assert np.array_equal(getattr(a, nm), getattr(b, nm)), nm
+    for fa, fb in zip(a.faces, b.faces):
+        assert np.array_equal(fa.phi, fb.phi)
+        assert np.array_equal(fa.xi, fb.xi)
+
+
+@needs_ref
+@pytest.mark.parametrize("kind,counts,per", [
+    ("hex", [3, 2, 4], None), ("tet", [2, 3, 2], None), ("quad", [5, 3], None),
+    ("tri", [4, 4], None), ("hex", [3, 3, 3], 3), ("tet", [2, 2, 2], 3),
+    ("tri", [3, 4], 2), ("quad", [4, 2], 2)])
+def test_mesh_topology_bitexact_vs_reference(kind, counts, per):
+    sys.path.insert(0, REFERENCE_SRC)
+    from ldgkit import mesh as RM
+    from cases import BOX_PERIODIC
+    from paper_2205_07824_b200 import meshgen
+    nd = len(counts)
+    spec = BOX_PERIODIC[per] if per else None
+    for pg in (1, 2):
+        m1 = RM.generate_structured([(0, 1)] * nd, counts, kind, p_geom=pg)
+        m2 = meshgen.generate_structured([(0, 1)] * nd, counts, kind, p_geom=pg)
+        for nm in ("vertices", "connectivity", "ho_nodes", "boundary_faces"):
+            assert np.array_equal(getattr(m1, nm), getattr(m2, nm)), nm
+        t1 = RM.build_face_topology(m1, spec)
+        t2 = meshgen.build_face_topology(m2, spec)
+        for k in TOPO:
+            assert np.array_equal(getattr(t1, k), getattr(t2, k)), k
+        assert np.array_equal(np.array(t1.perm), np.array(t2.perm))
