@@ -1,0 +1,306 @@
+"""Benchmark: LDG tangent matvec GDOF/s (3D Poisson, hex p=3, ~10M DOFs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A "step" is one Jacobian-vector product J(u) du of the config-3 system
+(BASELINE.json configs[2]: 3D Poisson on a structured hex box mesh, p=3,
+n=54 -> 10,077,696 DOFs) -- the matvec GMRES applies every iteration.
+
+* ``value``: device-resident throughput (inputs already in HBM), CUDA events
+  on the launching stream, max over ranks.  Inputs+outputs (du 81 MB, dq
+  242 MB, dR 81 MB) exceed the 126 MB L2, so no flush is needed.
+* ``e2e``: the same metric through the public drop-in call
+  ``LdgSystem.residual_tangent(state, du)`` with du in pinned host memory and
+  the result returned in host memory, copies inside the timed region.
+* ``roofline``: the dominant kernel (the flux pass) against measured HBM
+  bandwidth with its algorithmic bytes; ``matvec_roofline``: the whole
+  matvec at SURVEY 8(d)'s 72 B/DOF.
+* ``cpu_baseline``: the oracle (restatement of the reference numpy path) on
+  a bounded sample, rank 0 only.
+* ``--impl reference``: that reference CPU implementation timed on this
+  host, same metric and unit.
+
+Multi-GPU (torchrun, N>1): round-1 runs independent replicas (weak scaling,
+each rank its own 10M-DOF system); see DESIGN.md for the partitioned path.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+N_ELEM = 54          # 54^3 hexes x 64 nodes = 10,077,696 DOFs
+P = 3
+CPU_SAMPLE_N = 10    # 10^3 hexes x 64 nodes = 64,000 DOFs
+MODEL = ROOT / "tests" / "golden" / "poisson3d.model"
+METRIC = "DG matvec GDOF/s (3D, p=3)"
+BYTES_FLUX = 40      # flux pass: du 8 + dq 24 read, dR 8 written (per DOF)
+BYTES_MIXED = 32     # mixed pass: du 8 read, dq 24 written
+BYTES_MATVEC = 72    # 8 (3 + 2 nd)
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def build_problem(n, p=P):
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    m = model.load_model(str(MODEL))
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [n] * 3, "hex")
+    topo = meshgen.build_face_topology(mesh)
+    master = refelem.build_master("hex", p)
+    return m, mesh, topo, master
+
+
+def cpu_oracle_times(n, reps):
+    """Oracle residual_tangent on n^3 hexes: per-call seconds, DOFs."""
+    from oracle import make_oracle
+    m, mesh, topo, master = build_problem(n)
+    o = make_oracle(m, mesh, topo, master)
+    ne, nb = mesh.connectivity.shape[0], master.n_nodes
+    u = np.random.default_rng(1).normal(size=(ne, nb, 1))
+    du = np.random.default_rng(0).normal(size=(ne, nb, 1))
+    o.residual_tangent(u, du)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        o.residual_tangent(u, du)
+        ts.append(time.perf_counter() - t0)
+    return ts, ne * nb
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.p, self.out = index, None, ""
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is None:
+            return
+        self.p.terminate()
+        try:
+            self.out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+
+    def summary(self):
+        rows = [[x.strip() for x in r.split(",")] for r in self.out.strip().splitlines()
+                if r.count(",") >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4)
+                          if r[4 + k].lower() in ("active", "1")})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def run_reference(args, rank):
+    """The reference CPU path (oracle port of ldgkit's numpy implementation)."""
+    if rank != 0:
+        return
+    ts, ndof = cpu_oracle_times(CPU_SAMPLE_N, max(args.steps, 1))
+    med = float(np.median(ts))
+    v = ndof / med / 1e9
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "GDOF/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"3D Poisson hex p=3 tangent matvec; bounded sample "
+                               f"n={CPU_SAMPLE_N} ({ndof} DOFs) of config 3"},
+        "cpu_baseline": {"value": v, "unit": "GDOF/s", "cores": 1, "kind": "port",
+                         "sample": f"{ndof}-DOF hex p=3 Poisson tangent, median of "
+                                   f"{len(ts)} calls (numpy c_einsum path: 1 core)"},
+        "e2e": {"value": v, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_b200(args, rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2205_07824_b200 import _lib as L
+    from paper_2205_07824_b200.system import LdgSystem, SolverState
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    m, mesh, topo, master = build_problem(args.n)
+    t0 = time.time()
+    s = LdgSystem(m, mesh, topo, master)
+    setup_s = time.time() - t0
+    ne, nb, ndof = s.n_elements, s.n_nodes, s.n_dofs
+    gen = torch.Generator(device=dev).manual_seed(rank)
+    du = torch.randn((ne, nb, 1), dtype=torch.float64, device=dev, generator=gen)
+    dq = torch.empty((ne, nb, 1, 3), dtype=torch.float64, device=dev)
+    dR = torch.empty_like(du)
+    stream = torch.cuda.current_stream()
+    lib, h = s.lib, s._h
+
+    def launch_mixed():
+        L.check(lib.ldg_compute_mixed(h, L.ptr(du), None, L.ptr(dq), L.stream_ptr()), "mixed")
+
+    def launch_flux():
+        # flux pass with no boundary/source data: bitwise the tangent's pass B
+        L.check(lib.ldg_residual(h, L.ptr(du), L.ptr(dq), None, None, L.ptr(dR),
+                                 L.stream_ptr()), "flux")
+
+    for _ in range(args.warmup):
+        s.tangent_dev(du, out=dR, dq_scratch=dq)
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            s.tangent_dev(du, out=dR, dq_scratch=dq)
+        end.record(stream)
+        torch.cuda.synchronize()
+        # per-kernel split, same stream, events between the two launches
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)]
+              for _ in range(args.steps)]
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            launch_mixed()
+            ev[k][1].record(stream)
+            launch_flux()
+            ev[k][2].record(stream)
+        torch.cuda.synchronize()
+    mixed_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    flux_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    t_ms = start.elapsed_time(end) / args.steps
+    tmax = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    t_ms = float(tmax.item())
+
+    # e2e through the public drop-in call with pinned host buffers
+    du_host = du.cpu().pin_memory()
+    st = SolverState(u=du_host, q=None, w=None, t=0.0)
+    for _ in range(2):
+        s.residual_tangent(st, du_host)
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    for _ in range(args.steps):
+        out, _, _ = s.residual_tangent(st, du_host)
+    eb.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = ea.elapsed_time(eb) / args.steps
+    wall_e2e = (time.perf_counter() - e0) / args.steps * 1e3
+    assert out.device.type == "cpu"
+    emax = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(emax, op=dist.ReduceOp.MAX)
+    e2e_ms = float(emax.item())
+
+    if rank != 0:
+        return
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"
+    fl = float(np.median(flux_ms))
+    mx = float(np.median(mixed_ms))
+    gdofs = world * ndof / (t_ms * 1e-3) / 1e9
+    ach_flux = BYTES_FLUX * ndof / (fl * 1e-3) / 1e9
+    ach_mixed = BYTES_MIXED * ndof / (mx * 1e-3) / 1e9
+    ach_mv = BYTES_MATVEC * ndof / (t_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": gdofs, "unit": "GDOF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded normal du)",
+        "config": {"workload": "config 3: 3D Poisson (tests/golden/poisson3d.model) on "
+                               f"structured hex box n={args.n}, p=3, tangent J(u)du",
+                   "dofs_per_gpu": ndof, "elements_per_gpu": ne,
+                   "l2": "inputs larger than L2 (du 81 MB + dq 242 MB + dR 81 MB)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "setup_s": round(setup_s, 2)},
+        "e2e": {"value": world * ndof / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
+                "h2d_bytes_per_step": ndof * 8, "d2h_bytes_per_step": ndof * 8,
+                "ms_per_step": e2e_ms, "wall_ms_per_step": wall_e2e,
+                "call": "LdgSystem.residual_tangent(state, du) with pinned torch CPU du"},
+        "roofline": {"bound": "hbm", "kernel": "flux_kernel<4,3,1> (pass B)",
+                     "achieved": ach_flux, "peak": hbm, "unit": "GB/s",
+                     "frac": ach_flux / hbm, "traffic": None,
+                     "algorithmic_bytes_per_dof": BYTES_FLUX, "ms": fl,
+                     "peak_source": peak_src},
+        "mixed_roofline": {"kernel": "mixed_kernel<4,3,1> (pass A)", "achieved": ach_mixed,
+                           "frac": ach_mixed / hbm, "algorithmic_bytes_per_dof": BYTES_MIXED,
+                           "ms": mx},
+        "matvec_roofline": {"achieved": ach_mv, "peak": hbm, "unit": "GB/s",
+                            "frac": ach_mv / hbm, "algorithmic_bytes_per_dof": BYTES_MATVEC,
+                            "target_60pct_gdofs": 0.6 * hbm / BYTES_MATVEC},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        ts, nd_cpu = cpu_oracle_times(CPU_SAMPLE_N, 3)
+        v = nd_cpu / float(np.median(ts)) / 1e9
+        line["cpu_baseline"] = {"value": v, "unit": "GDOF/s", "cores": 1, "kind": "port",
+                                "sample": f"{nd_cpu}-DOF hex p=3 Poisson tangent (n="
+                                          f"{CPU_SAMPLE_N}), median of 3 after 1 warm-up"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_ELEM)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    run_b200(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * ldgb200.h -- C ABI of the B200 LDG hot path (libldgb200.so).
+ *
+ * The reference (ldgkit) is pure Python; its "FFI" for this path is the duck
+ * typed LdgSystem / solver interface.  Each entry point below replaces one
+ * reference call (file:line under /root/reference/pkg/src/ldgkit/):
+ *
+ *   ldg_compute_mixed        LdgSystem.compute_mixed          disc.py:436-490
+ *   ldg_residual             LdgSystem.residual               disc.py:588-653
+ *   ldg_residual_tangent     LdgSystem.residual_tangent       disc.py:591-593
+ *   ldg_mass_apply           LdgSystem.mass_apply (const m)   disc.py:897-925
+ *   ldg_mass_inv_apply       MassPreconditioner.apply         driver.py:99-106
+ *   ldg_dot / ldg_nrm2 / ldg_axpy / ldg_scal / ldg_copy
+ *                            numpy dot/norm/axpy in gmres     solver.py:98-145
+ *   ldg_mgs_step             MGS dot+axpy pair                solver.py:130-138
+ *   ldg_cgs_dots / ldg_cgs_update  block Gram-Schmidt (fast mode)
+ *   ldg_combine              x += Z^T y                       solver.py:163-164
+ *   ldg_bj_probe_vector      coloured unit probe              solver.py:327-330
+ *   ldg_bj_extract           mats[b][:,k] = col[blocks[b]]    solver.py:331-334
+ *   ldg_bj_invert            lu_factor (+1e-12 shift rule)    solver.py:335-345
+ *   ldg_bj_apply             BlockJacobiPreconditioner.apply  solver.py:296-300
+ *
+ * Conventions: every double* / int* argument is DEVICE memory owned by the
+ * caller (PyTorch tensors on the host side); the handle owns only the
+ * immutable connectivity / geometry tables uploaded by ldg_create.  All work
+ * is enqueued on `stream` (a cudaStream_t passed as void*).  Return codes:
+ * 0 success, 1 non-finite output (first bad element via ldg_last_bad_element),
+ * 2 invalid argument / unsupported configuration, >=3 CUDA error.
+ */
+#ifndef LDGB200_H
+#define LDGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LDG_MAX_N1 9
+#define LDG_MAX_NCU 5
+
+/* element-face info bits (LdgTables.finfo) */
+#define LDG_FACE_INTERIOR 0
+#define LDG_FACE_DIRICHLET 1
+#define LDG_FACE_NEUMANN 2
+#define LDG_FACE_KIND_MASK 3
+#define LDG_FACE_SIDE_RIGHT 4   /* this element is the right side of the face */
+#define LDG_FACE_SWITCH 8       /* face switch bit (disc.py:287) */
+#define LDG_FACE_MAP_SHIFT 8    /* bits 8..23: neighbour node map id */
+
+/* Host-side description of a tensor-product (quad/hex) kind-D system with a
+ * flux that is linear in (u, q) with constant coefficients.  Pointers are
+ * HOST memory; ldg_create copies them to the device. */
+typedef struct LdgTables {
+  int32_t nd;            /* 2 or 3 */
+  int32_t n1;            /* nodes per direction, p+1 */
+  int32_t ncu;           /* state components */
+  int32_t ne;            /* elements */
+  int32_t n_maps;        /* distinct neighbour node maps */
+  int32_t trace_centered;   /* numflux.trace == 'centered'      */
+  int32_t grad_centered;    /* numflux.grad_trace == 'centered' */
+  int32_t flux_uses_u;      /* any Au coefficient nonzero        */
+  const double* geo;     /* (ne, 1 + nd*nd): detJ, invjt[d][r]            */
+  const int32_t* fnbr;   /* (ne, 2*nd): neighbour element / boundary row  */
+  const int32_t* finfo;  /* (ne, 2*nd): LDG_FACE_* bits                   */
+  const double* ftau;    /* (ne, 2*nd): penalty tau on this face          */
+  const int32_t* nmap;   /* (n_maps, n1^(nd-1)): own face node -> nbr node */
+  double d1[LDG_MAX_N1 * LDG_MAX_N1];  /* GLL collocation derivative D[i][m]  */
+  double m1[LDG_MAX_N1 * LDG_MAX_N1];  /* 1D mass   M[a][b] = int l_a l_b      */
+  double s1[LDG_MAX_N1 * LDG_MAX_N1];  /* 1D stiff. S[a][b] = int l'_a l_b     */
+  double clo[LDG_MAX_N1];              /* M^-1 e_0                           */
+  double chi[LDG_MAX_N1];              /* M^-1 e_{n1-1}                      */
+  double au[LDG_MAX_NCU * 3 * LDG_MAX_NCU];       /* f_cd += au[c][d][k] u_k  */
+  double aq[LDG_MAX_NCU * 3 * LDG_MAX_NCU * 3];   /* f_cd += aq[c][d][k][e] q_ke */
+  double mass_coef[LDG_MAX_NCU];       /* constant mass m_c (disc.py:902-906) */
+} LdgTables;
+
+typedef struct LdgHandle LdgHandle;
+
+int ldg_create(const LdgTables* host, LdgHandle** out);
+int ldg_destroy(LdgHandle* h);
+int64_t ldg_last_bad_element(LdgHandle* h);
+const char* ldg_last_error(void);
+int ldg_version(void);
+
+/* q = M^-1 [ -int grad(u) phi + oint (u - u^) n phi ]   (disc.py:436-490)
+ * gproj: (n_bfaces, n1^(nd-1), ncu) projected Dirichlet data, or NULL for
+ * the homogeneous linearisation.  q layout (ne, nb, ncu, nd). */
+int ldg_compute_mixed(LdgHandle* h, const double* u, const double* gproj,
+                      double* q, void* stream);
+
+/* R(u) (disc.py:595-653): q must be compute_mixed(u) with the same gproj;
+ * bsrc (ne, nb, ncu) = -int s(x,t) phi or NULL; gproj Dirichlet/Neumann
+ * projected data. */
+int ldg_residual(LdgHandle* h, const double* u, const double* q,
+                 const double* gproj, const double* bsrc, double* R,
+                 void* stream);
+
+/* dR = J(u) du with the reference linearisation (disc.py:591-604, frozen
+ * tau): computes dq = compute_mixed(du, homogeneous) into dq_scratch and
+ * then the flux pass.  Linear constant-coefficient fluxes do not read the
+ * base state. */
+int ldg_residual_tangent(LdgHandle* h, const double* du, double* dq_scratch,
+                         double* dR, void* stream);
+
+/* constant-mass operator and its block inverse (element mass M_e =
+ * detJ * M1 (x) M1 (x) M1) */
+int ldg_mass_apply(LdgHandle* h, const double* v, double scale, double* out,
+                   void* stream);
+int ldg_mass_inv_apply(LdgHandle* h, const double* v, double* out, void* stream);
+
+/* ---- Krylov vector primitives (deterministic fixed-order reductions) ---- */
+/* scratch: >= ldg_reduce_scratch_doubles() doubles; result written to out[0] */
+int64_t ldg_reduce_scratch_doubles(void);
+int ldg_dot(int64_t n, const double* x, const double* y, double* scratch,
+            double* out, void* stream);
+int ldg_nrm2(int64_t n, const double* x, double* scratch, double* out,
+             void* stream);
+/* y = a*x + y with a = sign * (*a_dev) (device scalar) or a_host if a_dev NULL */
+int ldg_axpy(int64_t n, double a_host, const double* a_dev, double sign,
+             const double* x, double* y, void* stream);
+/* y = x * (1 / *den_dev)  (reference: V[k+1] = w / H[k+1,k]) */
+int ldg_div_scalar(int64_t n, const double* x, const double* den_dev, double* y,
+                   void* stream);
+/* fused MGS step: w -= h_in * Vi ; h_out = <Vnext, w> (Vnext may be NULL) */
+int ldg_mgs_step(int64_t n, const double* vi, const double* h_in, double* w,
+                 const double* vnext, double* scratch, double* h_out,
+                 void* stream);
+/* h[i] = <V_i, w> for i < k (V rows of length n, row stride ldv) */
+int ldg_cgs_dots(int64_t n, int k, const double* V, int64_t ldv, const double* w,
+                 double* scratch, double* h, void* stream);
+/* w -= sum_i h[i] V_i ; nrm_out = ||w|| */
+int ldg_cgs_update(int64_t n, int k, const double* V, int64_t ldv,
+                   const double* h, double* w, double* scratch, double* nrm_out,
+                   void* stream);
+/* x += sum_i y[i] Z_i  (y device) */
+int ldg_combine(int64_t n, int k, const double* Z, int64_t ldz, const double* y,
+                double* x, void* stream);
+
+/* ---- block-Jacobi ---- */
+int ldg_bj_probe_vector(int64_t nblk, int bs, const int32_t* members,
+                        int64_t n_members, int k, double* v, void* stream);
+int ldg_bj_extract(int bs, const int32_t* members, int64_t n_members, int k,
+                   const double* col, double* mats, void* stream);
+/* mats (nblk, bs, bs) row-major -> inv_t (nblk, bs, bs) holding inverse^T;
+ * shifted (nblk) int flags: 1 where the 1e-12 shift rule fired. */
+int ldg_bj_invert(int64_t nblk, int bs, const double* mats, double* inv_t,
+                  int32_t* shifted, void* stream);
+int ldg_bj_apply(int64_t nblk, int bs, const double* inv_t, const double* r,
+                 double* z, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LDGB200_H */

@@ -1,0 +1,235 @@
+// Element block-Jacobi preconditioner (solver.py:291-346, driver.py:119-142).
+//
+// Build = coloured unit probes through the tangent operator (host loop over
+// colours x block directions, each a device matvec) + ldg_bj_extract, then
+// ldg_bj_invert: one CTA per element block runs Gauss-Jordan with partial
+// pivoting in shared memory.  Its pivots are exactly the LU pivots of
+// scipy.linalg.lu_factor, so the reference's regularisation rule
+// (|pivot| < 1e-14 max(1, max|A|) or non-finite -> A + 1e-12 I,
+// solver.py:336-345) is applied to the same test.  The explicit inverse is
+// stored transposed so the apply (a batched GEMV, HBM-bound on the block
+// matrices) reads it fully coalesced.
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ldgb200.h"
+
+namespace {
+
+constexpr int kInvThreads = 256;
+constexpr int kMaxSmemBs = 160;          // in-shared-memory inversion limit
+
+__global__ void probe_kernel(int bs, const int32_t* __restrict__ members,
+                             int64_t nm, int k, double* __restrict__ v) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nm) v[(int64_t)members[t] * bs + k] = 1.0;
+}
+
+__global__ void extract_kernel(int bs, const int32_t* __restrict__ members,
+                               int64_t nm, int k, const double* __restrict__ col,
+                               double* __restrict__ mats) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nm * bs) return;
+  const int64_t b = members[t / bs];
+  const int row = (int)(t % bs);
+  mats[(b * bs + row) * bs + k] = col[b * bs + row];
+}
+
+__device__ double block_max_abs(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double r = threadIdx.x < kInvThreads / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if (threadIdx.x == 0) red[0] = r;
+  }
+  __syncthreads();
+  const double out = red[0];
+  __syncthreads();
+  return out;
+}
+
+// In-place Gauss-Jordan with partial pivoting; returns false if a pivot
+// fails the reference threshold.
+__device__ bool gauss_jordan(double* A, int bs, int* perm, double thr,
+                             double* red, int* ipiv) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int c = 0; c < bs; ++c) {
+    // pivot search over rows c..bs-1 (first max, like LAPACK idamax)
+    if (threadIdx.x < 32) {
+      double best = -1.0;
+      int br = c;
+      for (int r = c + threadIdx.x; r < bs; r += 32) {
+        const double a = fabs(A[r * bs + c]);
+        if (a > best) { best = a; br = r; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+        if (ob > best || (ob == best && orr < br)) { best = ob; br = orr; }
+      }
+      if (threadIdx.x == 0) *ipiv = br;
+    }
+    __syncthreads();
+    const int p = *ipiv;
+    if (threadIdx.x == 0) perm[c] = p;
+    if (p != c)
+      for (int k = threadIdx.x; k < bs; k += kInvThreads) {
+        const double t = A[c * bs + k];
+        A[c * bs + k] = A[p * bs + k];
+        A[p * bs + k] = t;
+      }
+    __syncthreads();
+    const double piv = A[c * bs + c];
+    if (threadIdx.x == 0 && (!(fabs(piv) >= thr) || !isfinite(piv))) bad = 1;
+    const double inv = 1.0 / piv;
+    __syncthreads();
+    for (int k = threadIdx.x; k < bs; k += kInvThreads)
+      A[c * bs + k] = (k == c) ? inv : A[c * bs + k] * inv;
+    __syncthreads();
+    for (int t = threadIdx.x; t < bs * bs; t += kInvThreads) {
+      const int r = t / bs, k = t % bs;
+      if (r == c) continue;
+      const double f = A[r * bs + c];
+      if (k == c) continue;
+      A[r * bs + k] = fma(-f, A[c * bs + k], A[r * bs + k]);
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < bs; r += kInvThreads)
+      if (r != c) A[r * bs + c] = -A[r * bs + c] * inv;
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges, last first
+  for (int c = bs - 1; c >= 0; --c) {
+    const int p = perm[c];
+    if (p != c)
+      for (int r = threadIdx.x; r < bs; r += kInvThreads) {
+        const double t = A[r * bs + c];
+        A[r * bs + c] = A[r * bs + p];
+        A[r * bs + p] = t;
+      }
+    __syncthreads();
+  }
+  return bad == 0;
+}
+
+__global__ void __launch_bounds__(kInvThreads)
+invert_kernel(int bs, const double* __restrict__ mats, double* __restrict__ inv_t,
+              int32_t* __restrict__ shifted) {
+  extern __shared__ double A[];
+  __shared__ double red[kInvThreads / 32];
+  __shared__ int perm[kMaxSmemBs];
+  __shared__ int ipiv;
+  const int64_t b = blockIdx.x;
+  const double* M = mats + b * bs * bs;
+  double amax = 0.0;
+  for (int t = threadIdx.x; t < bs * bs; t += kInvThreads) {
+    A[t] = M[t];
+    amax = fmax(amax, fabs(A[t]));
+  }
+  amax = block_max_abs(amax, red);
+  const double thr = 1e-14 * fmax(1.0, amax);
+  bool ok = gauss_jordan(A, bs, perm, thr, red, &ipiv);
+  if (!ok) {
+    // solver.py:343: A + 1e-12 I, factor without further checks
+    for (int t = threadIdx.x; t < bs * bs; t += kInvThreads)
+      A[t] = M[t] + ((t / bs) == (t % bs) ? 1e-12 : 0.0);
+    __syncthreads();
+    gauss_jordan(A, bs, perm, 0.0, red, &ipiv);
+  }
+  if (threadIdx.x == 0 && shifted) shifted[b] = ok ? 0 : 1;
+  double* O = inv_t + b * bs * bs;
+  for (int t = threadIdx.x; t < bs * bs; t += kInvThreads) {
+    const int r = t / bs, c = t % bs;
+    O[c * bs + r] = A[t];
+  }
+}
+
+// z_b = inv_b r_b with inv stored transposed: thread i reads column i of
+// inv_t rows (coalesced), r_b from shared memory.
+__global__ void __launch_bounds__(256)
+bj_apply_kernel(int64_t nblk, int bs, const double* __restrict__ inv_t,
+                const double* __restrict__ r, double* __restrict__ z) {
+  extern __shared__ double rs[];
+  const int per = blockDim.x / bs;                 // blocks per CTA
+  const int slot = threadIdx.x / bs, i = threadIdx.x % bs;
+  const int64_t b = (int64_t)blockIdx.x * per + slot;
+  const bool active = slot < per && b < nblk;
+  if (active) rs[slot * bs + i] = r[b * bs + i];
+  __syncthreads();
+  if (!active) return;
+  const double* It = inv_t + b * bs * bs;
+  double acc = 0.0;
+  for (int j = 0; j < bs; ++j) acc = fma(__ldg(It + (int64_t)j * bs + i), rs[slot * bs + j], acc);
+  z[b * bs + i] = acc;
+}
+
+// large blocks: one CTA per block, threads stride rows
+__global__ void __launch_bounds__(256)
+bj_apply_big_kernel(int bs, const double* __restrict__ inv_t,
+                    const double* __restrict__ r, double* __restrict__ z) {
+  extern __shared__ double rs[];
+  const int64_t b = blockIdx.x;
+  for (int j = threadIdx.x; j < bs; j += blockDim.x) rs[j] = r[b * bs + j];
+  __syncthreads();
+  const double* It = inv_t + b * bs * bs;
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < bs; ++j) acc = fma(__ldg(It + (int64_t)j * bs + i), rs[j], acc);
+    z[b * bs + i] = acc;
+  }
+}
+
+inline int rc() { return cudaGetLastError() == cudaSuccess ? 0 : 3; }
+
+}  // namespace
+
+extern "C" {
+
+int ldg_bj_probe_vector(int64_t nblk, int bs, const int32_t* members, int64_t nm,
+                        int k, double* v, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(v, 0, (size_t)nblk * bs * sizeof(double), s) != cudaSuccess) return 3;
+  if (nm > 0) probe_kernel<<<(unsigned)((nm + 255) / 256), 256, 0, s>>>(bs, members, nm, k, v);
+  return rc();
+}
+
+int ldg_bj_extract(int bs, const int32_t* members, int64_t nm, int k,
+                   const double* col, double* mats, void* stream) {
+  const int64_t n = nm * bs;
+  if (n > 0)
+    extract_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        bs, members, nm, k, col, mats);
+  return rc();
+}
+
+int ldg_bj_invert(int64_t nblk, int bs, const double* mats, double* inv_t,
+                  int32_t* shifted, void* stream) {
+  if (bs > kMaxSmemBs) return 2;
+  const size_t sm = (size_t)bs * bs * sizeof(double);
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (nblk > 0)
+    invert_kernel<<<(unsigned)nblk, kInvThreads, sm, (cudaStream_t)stream>>>(bs, mats, inv_t,
+                                                                             shifted);
+  return rc();
+}
+
+int ldg_bj_apply(int64_t nblk, int bs, const double* inv_t, const double* r, double* z,
+                 void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nblk <= 0) return 0;
+  if (bs <= 256) {
+    const int per = 256 / bs;
+    const unsigned grid = (unsigned)((nblk + per - 1) / per);
+    bj_apply_kernel<<<grid, per * bs, per * bs * sizeof(double), s>>>(nblk, bs, inv_t, r, z);
+  } else {
+    bj_apply_big_kernel<<<(unsigned)nblk, 256, bs * sizeof(double), s>>>(bs, inv_t, r, z);
+  }
+  return rc();
+}
+
+}  // extern "C"

@@ -1,0 +1,240 @@
+// Krylov vector primitives for the device GMRES (solver.py:79-174).
+//
+// All reductions are deterministic: a fixed grid of kRedBlocks blocks
+// grid-strides the vector, reduces in a fixed warp-shuffle tree, writes one
+// partial per block, and the last block to finish (atomic ticket) sums the
+// partials in index order.  Results are bitwise reproducible run to run.
+// Fused variants cut HBM passes: the MGS step does w -= h_i V_i and the next
+// dot <V_{i+1}, w> in one sweep (3 reads + 1 write instead of 5 passes).
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ldgb200.h"
+
+namespace {
+
+constexpr int kRedBlocks = 1184;      // 8 x 148 SMs
+constexpr int kThreads = 256;
+constexpr int kMaxK = 8;              // dots per sweep in the multi-dot kernel
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block sum in fixed order; result valid in thread 0
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = l < (kThreads / 32) ? sh[l] : 0.0;
+    r = warp_sum(r);
+  }
+  __syncthreads();
+  return r;
+}
+
+// last-block finalisation: partials[0..nparts) summed in order into *out
+// (scaled by sqrt if want_sqrt); ticket lives at scratch tail.
+__device__ __forceinline__ void finish(double* partials, unsigned int* ticket,
+                                       int nvals, double* out, bool want_sqrt,
+                                       double* sh) {
+  __shared__ bool last;
+  __threadfence();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int v = 0; v < nvals; ++v) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads)
+      s += partials[(size_t)v * gridDim.x + b];
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) out[v] = want_sqrt ? sqrt(s) : s;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+__global__ void __launch_bounds__(kThreads)
+dot_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+           double* partials, unsigned int* ticket, double* out, int want_sqrt) {
+  __shared__ double sh[kThreads / 32];
+  double s = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
+    s = fma(x[i], y[i], s);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  finish(partials, ticket, 1, out, want_sqrt, sh);
+}
+
+__global__ void __launch_bounds__(kThreads)
+axpy_kernel(int64_t n, double a_host, const double* __restrict__ a_dev, double sign,
+            const double* __restrict__ x, double* __restrict__ y) {
+  const double a = a_dev ? sign * (*a_dev) : a_host;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+__global__ void __launch_bounds__(kThreads)
+div_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ den,
+           double* __restrict__ y) {
+  const double d = *den;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
+    y[i] = x[i] / d;
+}
+
+// w -= h_in * vi ; partial <vnext, w>
+__global__ void __launch_bounds__(kThreads)
+mgs_kernel(int64_t n, const double* __restrict__ vi, const double* __restrict__ h_in,
+           double* __restrict__ w, const double* __restrict__ vnext,
+           double* partials, unsigned int* ticket, double* h_out) {
+  __shared__ double sh[kThreads / 32];
+  const double h = h_in ? *h_in : 0.0;
+  double s = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    double wv = w[i];
+    if (vi) {
+      wv = wv - h * vi[i];        // reference: w = w - H[i,k] * V[i]
+      w[i] = wv;
+    }
+    if (vnext) s = fma(vnext[i], wv, s);
+  }
+  if (!vnext) return;
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  finish(partials, ticket, 1, h_out, false, sh);
+}
+
+// up to kMaxK dots <V_i, w> per sweep
+__global__ void __launch_bounds__(kThreads)
+multidot_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
+                const double* __restrict__ w, double* partials,
+                unsigned int* ticket, double* h) {
+  __shared__ double sh[kThreads / 32];
+  double acc[kMaxK];
+#pragma unroll
+  for (int r = 0; r < kMaxK; ++r) acc[r] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const double wv = w[i];
+#pragma unroll
+    for (int r = 0; r < kMaxK; ++r)
+      if (r < k) acc[r] = fma(V[(int64_t)r * ldv + i], wv, acc[r]);
+  }
+  for (int r = 0; r < k; ++r) {
+    const double s = block_sum(acc[r], sh);
+    if (threadIdx.x == 0) partials[(size_t)r * gridDim.x + blockIdx.x] = s;
+  }
+  finish(partials, ticket, k, h, false, sh);
+}
+
+// w -= sum_i h[i] V_i (i < k), optional ||w||
+__global__ void __launch_bounds__(kThreads)
+update_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
+              const double* __restrict__ hcoef, double sign, double* __restrict__ w,
+              double* partials, unsigned int* ticket, double* nrm) {
+  extern __shared__ double hs[];
+  __shared__ double sh[kThreads / 32];
+  for (int r = threadIdx.x; r < k; r += kThreads) hs[r] = hcoef[r];
+  __syncthreads();
+  double s = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    double acc = 0.0;
+    for (int r = 0; r < k; ++r) acc = fma(hs[r], V[(int64_t)r * ldv + i], acc);
+    const double wv = fma(sign, acc, w[i]);
+    w[i] = wv;
+    s = fma(wv, wv, s);
+  }
+  if (!nrm) return;
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  finish(partials, ticket, 1, nrm, true, sh);
+}
+
+inline unsigned int* ticket_of(double* scratch) {
+  return reinterpret_cast<unsigned int*>(scratch + (size_t)kRedBlocks * kMaxK);
+}
+
+inline int grid_for(int64_t n) {
+  int64_t g = (n + kThreads - 1) / kThreads;
+  return (int)(g < kRedBlocks ? (g < 1 ? 1 : g) : kRedBlocks);
+}
+
+inline int rc() { return cudaGetLastError() == cudaSuccess ? 0 : 3; }
+
+}  // namespace
+
+extern "C" {
+
+int64_t ldg_reduce_scratch_doubles(void) { return (int64_t)kRedBlocks * kMaxK + 8; }
+
+// NOTE: reductions always launch the full kRedBlocks grid so partial counts
+// (and therefore rounding) do not depend on n.
+int ldg_dot(int64_t n, const double* x, const double* y, double* scratch,
+            double* out, void* stream) {
+  dot_kernel<<<kRedBlocks, kThreads, 0, (cudaStream_t)stream>>>(
+      n, x, y, scratch, ticket_of(scratch), out, 0);
+  return rc();
+}
+
+int ldg_nrm2(int64_t n, const double* x, double* scratch, double* out, void* stream) {
+  dot_kernel<<<kRedBlocks, kThreads, 0, (cudaStream_t)stream>>>(
+      n, x, x, scratch, ticket_of(scratch), out, 1);
+  return rc();
+}
+
+int ldg_axpy(int64_t n, double a_host, const double* a_dev, double sign,
+             const double* x, double* y, void* stream) {
+  axpy_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, a_host, a_dev,
+                                                                  sign, x, y);
+  return rc();
+}
+
+int ldg_div_scalar(int64_t n, const double* x, const double* den, double* y,
+                   void* stream) {
+  div_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, den, y);
+  return rc();
+}
+
+int ldg_mgs_step(int64_t n, const double* vi, const double* h_in, double* w,
+                 const double* vnext, double* scratch, double* h_out, void* stream) {
+  mgs_kernel<<<kRedBlocks, kThreads, 0, (cudaStream_t)stream>>>(
+      n, vi, h_in, w, vnext, scratch, ticket_of(scratch), h_out);
+  return rc();
+}
+
+int ldg_cgs_dots(int64_t n, int k, const double* V, int64_t ldv, const double* w,
+                 double* scratch, double* h, void* stream) {
+  for (int r0 = 0; r0 < k; r0 += kMaxK) {
+    const int kk = k - r0 < kMaxK ? k - r0 : kMaxK;
+    multidot_kernel<<<kRedBlocks, kThreads, 0, (cudaStream_t)stream>>>(
+        n, kk, V + (int64_t)r0 * ldv, ldv, w, scratch, ticket_of(scratch), h + r0);
+    if (rc()) return 3;
+  }
+  return 0;
+}
+
+int ldg_cgs_update(int64_t n, int k, const double* V, int64_t ldv, const double* h,
+                   double* w, double* scratch, double* nrm_out, void* stream) {
+  update_kernel<<<kRedBlocks, kThreads, k * sizeof(double), (cudaStream_t)stream>>>(
+      n, k, V, ldv, h, -1.0, w, scratch, ticket_of(scratch), nrm_out);
+  return rc();
+}
+
+int ldg_combine(int64_t n, int k, const double* Z, int64_t ldz, const double* y,
+                double* x, void* stream) {
+  update_kernel<<<grid_for(n), kThreads, k * sizeof(double), (cudaStream_t)stream>>>(
+      n, k, Z, ldz, y, 1.0, x, nullptr, nullptr, nullptr);
+  return rc();
+}
+
+}  // extern "C"

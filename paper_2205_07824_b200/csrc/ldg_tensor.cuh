@@ -1,0 +1,51 @@
+// Shared definitions for the tensor-product (quad/hex) LDG kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ldgb200.h"
+
+namespace ldg {
+
+// Operator data passed by value (__grid_constant__) to every launch.  The
+// 1D tables are tiny and read uniformly across a warp, so they live in the
+// kernel parameter bank (constant cache), which DFMA can consume directly.
+struct TensorParams {
+  int ne, nd, n1, ncu;
+  int trace_centered, grad_centered, flux_uses_u;
+  int pad_;
+  const double* geo;      // (ne, 1+nd*nd)
+  const int32_t* fnbr;    // (ne, 2nd)
+  const int32_t* finfo;   // (ne, 2nd)
+  const double* ftau;     // (ne, 2nd)
+  const int32_t* nmap;    // (n_maps, n1^(nd-1))
+  unsigned long long* bad;  // first non-finite element (atomicMin)
+  double d1[LDG_MAX_N1 * LDG_MAX_N1];
+  double m1[LDG_MAX_N1 * LDG_MAX_N1];
+  double s1[LDG_MAX_N1 * LDG_MAX_N1];
+  double m1inv[LDG_MAX_N1 * LDG_MAX_N1];
+  double clo[LDG_MAX_N1];
+  double chi[LDG_MAX_N1];
+  double au[LDG_MAX_NCU * 3 * LDG_MAX_NCU];
+  double aq[LDG_MAX_NCU * 3 * LDG_MAX_NCU * 3];
+  double mass_coef[LDG_MAX_NCU];
+};
+
+// hex local faces (master.py:43-44): z-, z+, y-, y+, x-, x+
+// quad local faces: y-, x+, y+, x-
+__host__ __device__ constexpr int face_axis(int nd, int lf) {
+  return nd == 3 ? (lf < 2 ? 2 : (lf < 4 ? 1 : 0))
+                 : ((lf == 0 || lf == 2) ? 1 : 0);
+}
+__host__ __device__ constexpr int face_side(int nd, int lf) {
+  return nd == 3 ? (lf & 1) : (lf == 1 || lf == 2 ? 1 : 0);
+}
+
+int launch_mixed(const TensorParams& P, const double* u, const double* gproj,
+                 double* q, cudaStream_t s);
+int launch_flux(const TensorParams& P, bool tangent, const double* u,
+                const double* q, const double* gproj, const double* bsrc,
+                double* R, cudaStream_t s);
+int launch_mass(const TensorParams& P, bool inverse, const double* v,
+                double scale, double* out, cudaStream_t s);
+
+}  // namespace ldg

@@ -1,0 +1,345 @@
+"""Drop-in ``LdgSystem`` whose residual / tangent / mixed-gradient / mass
+operators run as hand-written sm_100a CUDA kernels.
+
+Mirrors ``ldgkit.disc.LdgSystem`` (disc.py:257-948): same constructor
+(model, mesh, topology, master), same methods and return conventions
+(tuples of block arrays; a new array per call), same error types and
+messages (``DiscError``, ``KernelNanError("<label> kernel produced
+non-finite values (first at element N)")``).  numpy inputs give numpy
+outputs (host<->device copies included); torch CUDA tensors stay on the
+device, which is how the device solver (``solver.py``) drives it.
+
+There is no CPU path: constructing a system without the native library or
+without a GPU raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .tables import DiscError, KernelNanError, TensorTables
+
+__all__ = ["LdgSystem", "SolverState", "DiscError", "KernelNanError"]
+
+
+@dataclass
+class SolverState:
+    """disc.py:45-66."""
+
+    u: object
+    q: object
+    w: object
+    t: float
+
+    def copy(self):
+        c = (lambda a: None if a is None else a.clone() if hasattr(a, "clone") else a.copy())
+        return SolverState(c(self.u), c(self.q), c(self.w), self.t)
+
+    def all_finite(self):
+        import torch
+        ok = True
+        for a in (self.u, self.q, self.w):
+            if a is None:
+                continue
+            ok = ok and bool(torch.isfinite(a).all()) if hasattr(a, "is_cuda") \
+                else ok and bool(np.isfinite(a).all())
+        return ok
+
+
+class _Disc:
+    """Host-side geometry views read by reference callers
+    (driver.py:102, diagnostics.py:43-63): computed lazily from the affine
+    tables, never used by the kernels."""
+
+    def __init__(self, tab):
+        self._t = tab
+
+    @property
+    def node_x(self):
+        return self._t.node_coords()
+
+    @property
+    def wdetj(self):
+        return self._t.detj[:, None] * self._t.master.quad_wts[None, :]
+
+    @property
+    def xq(self):
+        t = self._t
+        return t.x0[:, None, :] + np.einsum("edr,qr->eqd", t.J, t.master.quad_pts)
+
+    @property
+    def detj(self):
+        return np.repeat(self._t.detj[:, None], self._t.master.quad_pts.shape[0], axis=1)
+
+    @property
+    def mass_inv(self):
+        t = self._t
+        mi = t.m1inv
+        k = np.kron(np.kron(mi, mi), mi) if t.nd == 3 else np.kron(mi, mi)
+        return k[None, :, :] / t.detj[:, None, None]
+
+    @property
+    def fi_h(self):
+        return self._t.fi_h
+
+    @property
+    def fb_h(self):
+        return self._t.fb_h
+
+
+class LdgSystem:
+    """The semi-discrete LDG operator on the B200 (tensor quad/hex, kind D,
+    flux linear in (u, q))."""
+
+    def __init__(self, model, mesh, topology, master, device=None):
+        import torch
+        self.model, self.mesh, self.topology, self.master = model, mesh, topology, master
+        self.kind = model.kind
+        self.ncu, self.nd, self.nw = model.ncu, model.nd, model.nw
+        if model.nd != mesh.nd:
+            raise DiscError(f"model nd={model.nd} but mesh nd={mesh.nd}")
+        self.tab = TensorTables(model, mesh, topology, master)
+        self.lib = _lib.load()
+        self.device = torch.device(device if device is not None else "cuda")
+        self.fi_switch = self.tab.switch
+        self.beta_hat = np.ones(mesh.nd) / np.sqrt(mesh.nd)
+        self.bc_groups = self.tab.bc_groups
+        self.disc = _Disc(self.tab)
+        self._create_handle()
+        self._bdata = {}
+        self._src = {}
+        self._scratch = {}
+
+    # -- native handle -------------------------------------------------------------
+    def _create_handle(self):
+        t = self.tab
+        T = _lib.LdgTables()
+        T.nd, T.n1, T.ncu, T.ne = t.nd, t.n1, t.ncu, t.ne
+        T.n_maps = t.nmap.shape[0]
+        T.trace_centered = int(self.model.numflux.trace == "centered")
+        T.grad_centered = int(self.model.numflux.grad_trace == "centered")
+        T.flux_uses_u = int(t.flux_uses_u)
+        self._keep = []
+
+        def arr(a, dt):
+            a, p = _lib.as_c(a, dt)
+            self._keep.append(a)
+            return p
+
+        T.geo = arr(t.geo, np.float64)
+        T.fnbr = arr(t.fnbr, np.int32)
+        T.finfo = arr(t.finfo, np.int32)
+        T.ftau = arr(t.ftau, np.float64)
+        T.nmap = arr(t.nmap, np.int32)
+        n1 = t.n1
+        for name in ("d1", "m1", "s1"):
+            dst = getattr(T, name)
+            src = np.ascontiguousarray(getattr(t, name)).ravel()
+            for k in range(n1 * n1):
+                dst[k] = src[k]
+        for k in range(n1):
+            T.clo[k] = t.clo[k]
+            T.chi[k] = t.chi[k]
+        for k, v in enumerate(t.au.ravel()):
+            T.au[k] = v
+        for k, v in enumerate(t.aq.ravel()):
+            T.aq[k] = v
+        for k, v in enumerate(t.mass_coef):
+            T.mass_coef[k] = v
+        h = C.c_void_p()
+        _lib.check(self.lib.ldg_create(C.byref(T), C.byref(h)), "ldg_create")
+        self._keep = None
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and getattr(self, "lib", None) is not None:
+            try:
+                self.lib.ldg_destroy(h)
+            except Exception:
+                pass
+
+    # -- shapes and packing (disc.py:310-355) ----------------------------------------
+    @property
+    def n_elements(self):
+        return self.tab.ne
+
+    @property
+    def n_nodes(self):
+        return self.master.n_nodes
+
+    def block_shapes(self):
+        return [("u", (self.n_elements, self.n_nodes, self.ncu))]
+
+    @property
+    def n_dofs(self):
+        return self.n_elements * self.n_nodes * self.ncu
+
+    def pack(self, u, q=None, w=None):
+        return u.reshape(-1) if hasattr(u, "is_cuda") else np.ravel(u)
+
+    def unpack(self, vec):
+        return vec[: self.n_dofs].reshape(self.block_shapes()[0][1]), None, None
+
+    def state_from_vector(self, vec, t):
+        u, q, w = self.unpack(vec)
+        return SolverState(u=u, q=q, w=w, t=t)
+
+    # -- device helpers ----------------------------------------------------------------
+    def _dev(self, a):
+        """-> (device tensor, origin) with origin 'cuda', 'torch' (host
+        torch tensor, returned as host torch) or 'numpy'."""
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda:
+                return a.to(self.device, torch.float64).contiguous(), "cuda"
+            pinned = a.is_pinned()
+            return a.to(self.device, torch.float64, non_blocking=pinned).contiguous(), "torch"
+        return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64),
+                               device=self.device), "numpy"
+
+    def _empty(self, shape):
+        import torch
+        return torch.empty(shape, dtype=torch.float64, device=self.device)
+
+    def boundary_data(self, t):
+        """Projected Dirichlet/Neumann data at time t (device, cached)."""
+        import torch
+        key = float(t)
+        if key not in self._bdata:
+            if len(self._bdata) > 4:
+                self._bdata.clear()
+            g = self.tab.boundary_projection(key)
+            self._bdata[key] = torch.as_tensor(g, device=self.device) if g.size else None
+        return self._bdata[key]
+
+    def source_data(self, t):
+        import torch
+        key = float(t)
+        if key not in self._src:
+            if len(self._src) > 2:
+                self._src.clear()
+            b = self.tab.source_load(key)
+            self._src[key] = None if b is None else torch.as_tensor(b, device=self.device)
+        return self._src[key]
+
+    def _stream(self):
+        return _lib.stream_ptr()
+
+    def _check_nan(self, label):
+        bad = int(self.lib.ldg_last_bad_element(self._h))
+        if bad >= 0:
+            raise KernelNanError(f"{label} kernel produced non-finite values "
+                                 f"(first at element {bad})")
+
+    # -- device operators (torch in / torch out, no host sync) ---------------------------
+    def mixed_dev(self, u, t=0.0, homogeneous=False, out=None):
+        q = out if out is not None else self._empty((self.n_elements, self.n_nodes,
+                                                     self.ncu, self.nd))
+        g = None if homogeneous else self.boundary_data(t)
+        _lib.check(self.lib.ldg_compute_mixed(self._h, _lib.ptr(u), _lib.ptr(g),
+                                              _lib.ptr(q), self._stream()),
+                   "ldg_compute_mixed")
+        return q
+
+    def residual_dev(self, u, t=0.0, out=None, q_scratch=None):
+        q = self.mixed_dev(u, t, out=q_scratch)
+        R = out if out is not None else self._empty(u.shape)
+        _lib.check(self.lib.ldg_residual(
+            self._h, _lib.ptr(u), _lib.ptr(q), _lib.ptr(self.boundary_data(t)),
+            _lib.ptr(self.source_data(t)), _lib.ptr(R), self._stream()), "ldg_residual")
+        return R
+
+    def tangent_dev(self, du, out=None, dq_scratch=None):
+        dq = dq_scratch if dq_scratch is not None else self._empty(
+            (self.n_elements, self.n_nodes, self.ncu, self.nd))
+        R = out if out is not None else self._empty(du.shape)
+        _lib.check(self.lib.ldg_residual_tangent(self._h, _lib.ptr(du), _lib.ptr(dq),
+                                                 _lib.ptr(R), self._stream()),
+                   "ldg_residual_tangent")
+        return R
+
+    def mass_apply_dev(self, v, scale=1.0, out=None):
+        if not self.tab.mass_const:
+            raise DiscError("state-dependent mass is not supported on the B200 path")
+        o = out if out is not None else self._empty(v.shape)
+        _lib.check(self.lib.ldg_mass_apply(self._h, _lib.ptr(v), float(scale), _lib.ptr(o),
+                                           self._stream()), "ldg_mass_apply")
+        return o
+
+    def mass_inv_dev(self, v, out=None):
+        o = out if out is not None else self._empty(v.shape)
+        _lib.check(self.lib.ldg_mass_inv_apply(self._h, _lib.ptr(v), _lib.ptr(o),
+                                               self._stream()), "ldg_mass_inv_apply")
+        return o
+
+    # -- reference-shaped API ------------------------------------------------------------------
+    def _ret(self, x, origin):
+        import torch
+        if origin == "cuda":
+            return x
+        if origin == "torch":
+            out = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+            out.copy_(x, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return out
+        return x.cpu().numpy()
+
+    def compute_mixed(self, u, t, homogeneous=False):
+        """disc.py:436-449."""
+        ud, dev = self._dev(u)
+        q = self.mixed_dev(ud.reshape(self.n_elements, self.n_nodes, self.ncu), t, homogeneous)
+        if dev != "cuda":
+            self._check_nan("mixed")
+        return self._ret(q, dev)
+
+    def residual(self, state):
+        """disc.py:588-589 -> (Ru, None, None)."""
+        ud, dev = self._dev(state.u)
+        R = self.residual_dev(ud.reshape(self.n_elements, self.n_nodes, self.ncu), state.t)
+        if dev != "cuda":
+            self._check_nan("flux")
+        return self._ret(R, dev), None, None
+
+    def residual_tangent(self, state, du, dq=None, dw=None):
+        """disc.py:591-593 (reference linearisation; the base state enters
+        only through nonlinear fluxes, which this path rejects at setup)."""
+        dd, dev = self._dev(du)
+        R = self.tangent_dev(dd.reshape(self.n_elements, self.n_nodes, self.ncu))
+        if dev != "cuda":
+            self._check_nan("flux")
+        return self._ret(R, dev), None, None
+
+    def mass_apply(self, state, vu, vq=None, vw=None):
+        """disc.py:897-925 (constant mass)."""
+        vd, dev = self._dev(vu)
+        return self._ret(self.mass_apply_dev(vd.reshape(self.n_elements, self.n_nodes,
+                                                        self.ncu)), dev), None, None
+
+    def mass_tangent_extra(self, state, y_u, du, dq=None, dw=None):
+        """disc.py:927-931: zero for constant mass."""
+        if self.tab.mass_const:
+            return None
+        raise DiscError("state-dependent mass is not supported on the B200 path")
+
+    def interpolate_initial(self):
+        """disc.py:420-432 (host evaluation of the init plan at the nodes)."""
+        from .expr import evaluate
+        x = self.disc.node_x
+        b = {"t": 0.0, **self.model.mu_bindings()}
+        for k in range(self.nd):
+            b[f"x{k + 1}"] = x[..., k].ravel()
+        v = evaluate(self.model.init_plan(), b)
+        if not np.isfinite(v).all():
+            col = int(np.argwhere(~np.isfinite(v))[0][1])
+            raise KernelNanError("initial kernel produced non-finite values "
+                                 f"(first at element {col // self.n_nodes})")
+        B = self.n_elements * self.n_nodes
+        if v.shape[1] != B:
+            v = np.broadcast_to(v, (v.shape[0], B))
+        u = np.moveaxis(v.reshape((v.shape[0], self.n_elements, self.n_nodes)), 0, -1)
+        return SolverState(u=np.ascontiguousarray(u[..., : self.ncu]), q=None, w=None, t=0.0)

@@ -1,0 +1,555 @@
+"""Host table builder: (model, mesh, topology, master) -> device tables.
+
+Replaces the reference's dense per-quadrature-point ``Discretization``
+(disc.py:74-239, ~1.9 KB/DOF at hex p=3) with what the B200 kernels read:
+
+* per element: detJ and invJ^T (affine elements, 80 B);
+* per element-face: neighbour element (or boundary row), an info word
+  (interior/dirichlet/neumann, left/right side, the reference's switch bit,
+  the neighbour node-map id) and the penalty tau;
+* a handful of neighbour node maps (own face node -> neighbour volume node,
+  found by matching physical node coordinates, periodic shift applied);
+* 1D GLL operators D1, M1, S1 and the lift columns M1^-1 e_0, M1^-1 e_p;
+* flux coefficients of a flux that is linear in (u, q).
+
+The switch bits are computed with the reference's own floating-point
+pipeline (disc.py:139-180, 285-287) because on simplices and on faces with
+n . beta_hat = 0 they are decided by rounding; the tests pin them against the
+reference bit for bit.  Everything else is exact-arithmetic geometry.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import refelem
+from .expr import evaluate
+from .refelem import FACES, face_map
+
+# local face -> (normal axis, high side) for the tensor kinds
+FACE_AXIS = {"quad": [(1, 0), (0, 1), (1, 1), (0, 0)],
+             "hex": [(2, 0), (2, 1), (1, 0), (1, 1), (0, 0), (0, 1)]}
+
+
+class DiscError(ValueError):
+    pass
+
+
+class KernelNanError(DiscError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# plan analysis
+# ---------------------------------------------------------------------------
+
+
+def affine_form(plan, mu, variables):
+    """Symbolic affine forms of a plan's outputs in `variables` with
+    constant coefficients (mu substituted).  Returns a list of
+    (coeffs: dict var->float, const: float) or None if any output is not
+    affine with constant coefficients."""
+    forms = []
+    for ins in plan.instructions:
+        tag = ins[0]
+        f = None
+        if tag == "const":
+            f = ({}, float(ins[1]))
+        elif tag == "sym":
+            s = ins[1]
+            if s in variables:
+                f = ({s: 1.0}, 0.0)
+            elif s in mu:
+                f = ({}, float(mu[s]))
+        elif tag == "neg":
+            a = forms[ins[1]]
+            if a is not None:
+                f = ({k: -v for k, v in a[0].items()}, -a[1])
+        elif tag in ("add", "sub"):
+            a, b = forms[ins[1]], forms[ins[2]]
+            if a is not None and b is not None:
+                s = 1.0 if tag == "add" else -1.0
+                co = dict(a[0])
+                for k, v in b[0].items():
+                    co[k] = co.get(k, 0.0) + s * v
+                f = (co, a[1] + s * b[1])
+        elif tag == "mul":
+            a, b = forms[ins[1]], forms[ins[2]]
+            if a is not None and b is not None:
+                if not a[0]:
+                    f = ({k: a[1] * v for k, v in b[0].items()}, a[1] * b[1])
+                elif not b[0]:
+                    f = ({k: b[1] * v for k, v in a[0].items()}, a[1] * b[1])
+        elif tag == "div":
+            a, b = forms[ins[1]], forms[ins[2]]
+            if a is not None and b is not None and not b[0] and b[1] != 0.0:
+                f = ({k: v / b[1] for k, v in a[0].items()}, a[1] / b[1])
+        elif tag in ("call", "pow"):
+            args = ins[2] if tag == "call" else (ins[1], ins[2])
+            fa = [forms[x] for x in args]
+            if all(x is not None and not x[0] for x in fa):
+                vals = [np.array([x[1]]) for x in fa]
+                from .expr import _binop, _fn
+                with np.errstate(all="ignore"):
+                    v = _fn(ins[1], vals) if tag == "call" else _binop("pow", *vals)
+                f = ({}, float(v[0]))
+        forms.append(f)
+    out = []
+    for r in plan.outputs:
+        if forms[r] is None:
+            return None
+        out.append(forms[r])
+    return out
+
+
+def uses_any(plan, prefixes):
+    return any(s.startswith(prefixes) for s in
+               {i[1] for i in plan.instructions if i[0] == "sym"})
+
+
+def plan_is_zero(plan):
+    return all(plan.instructions[r] == ("const", 0.0) for r in plan.outputs)
+
+
+# ---------------------------------------------------------------------------
+# reference-faithful switch bits (disc.py:139-180, 285-287)
+# ---------------------------------------------------------------------------
+
+
+def reference_switch(mesh, topo, master, geom, chunk=1 << 16):
+    nd = mesh.nd
+    nfi = topo.elem_l.shape[0]
+    nqf = master.faces[0].weights.shape[0]
+    nbar = np.zeros((nfi, nd))
+    for lf in range(master.n_faces):
+        sel = np.nonzero(topo.face_l == lf)[0]
+        if sel.size == 0:
+            continue
+        gd = geom.eval_basis_grad(master.faces[lf].xi)
+        _, T = face_map(mesh.elem_kind, lf)
+        for c0 in range(0, sel.size, chunk):
+            s = sel[c0:c0 + chunk]
+            ho = mesh.ho_nodes[topo.elem_l[s]]
+            if nd == 1:
+                raise DiscError("1D meshes are not supported by the B200 path")
+            tang = np.einsum("qgd,sd,kgc->kqcs", gd, T, ho)
+            if nd == 2:
+                t = tang[:, :, :, 0]
+                nv = np.stack([t[:, :, 1], -t[:, :, 0]], axis=-1)
+            else:
+                nv = np.cross(tang[:, :, :, 0], tang[:, :, :, 1])
+            mag = np.linalg.norm(nv, axis=-1)
+            n = np.zeros((s.size, nqf, nd))
+            n[:] = nv / mag[:, :, None]
+            nbar[s] = n.mean(axis=1)
+    beta = np.ones(nd) / np.sqrt(nd)
+    return (nbar @ beta) > 0.0
+
+
+def _reference_switch_subset(mesh, master, geom, elems, lfs):
+    """reference_switch restricted to the given (left element, face) list."""
+    nd = mesh.nd
+    nqf = master.faces[0].weights.shape[0]
+    out = np.zeros(elems.size, dtype=bool)
+    nbar = np.zeros((elems.size, nd))
+    for lf in np.unique(lfs):
+        sel = np.nonzero(lfs == lf)[0]
+        gd = geom.eval_basis_grad(master.faces[lf].xi)
+        _, T = face_map(mesh.elem_kind, lf)
+        ho = mesh.ho_nodes[elems[sel]]
+        tang = np.einsum("qgd,sd,kgc->kqcs", gd, T, ho)
+        if nd == 2:
+            t = tang[:, :, :, 0]
+            nv = np.stack([t[:, :, 1], -t[:, :, 0]], axis=-1)
+        else:
+            nv = np.cross(tang[:, :, :, 0], tang[:, :, :, 1])
+        mag = np.linalg.norm(nv, axis=-1)
+        n = np.zeros((sel.size, nqf, nd))
+        n[:] = nv / mag[:, :, None]
+        nbar[sel] = n.mean(axis=1)
+    beta = np.ones(nd) / np.sqrt(nd)
+    out[:] = (nbar @ beta) > 0.0
+    return out
+
+
+# ---------------------------------------------------------------------------
+# table builder
+# ---------------------------------------------------------------------------
+
+
+class TensorTables:
+    """Host arrays for the tensor-product (quad/hex) kernels."""
+
+    def __init__(self, model, mesh, topo, master):
+        self.model, self.mesh, self.topo, self.master = model, mesh, topo, master
+        kind = master.kind
+        if kind != mesh.elem_kind:
+            raise DiscError("master element kind does not match the mesh")
+        if kind not in ("quad", "hex"):
+            raise DiscError(f"B200 tensor path needs quad/hex elements, got {kind}")
+        if model.kind != "D":
+            raise DiscError(f"B200 path supports diffusion (kind D) models, got {model.kind}")
+        if model.nw > 0 or model.numflux.uhat is not None or model.numflux.fhat is not None:
+            raise DiscError("ODE blocks and u^/f^ overrides are not supported on the B200 path")
+        self.nd, self.p, self.ncu = mesh.nd, master.p, model.ncu
+        self.n1 = master.p + 1
+        if self.n1 > 7 or self.ncu > 3:
+            raise DiscError("tensor path supports p <= 6 and ncu <= 3")
+        if master.quad_degree < 2 * master.p:
+            raise DiscError("tensor path needs quadrature degree >= 2p (exact mass/stiffness)")
+        self.nf = 2 * self.nd
+        self.nfn = self.n1 ** (self.nd - 1)
+        self.ne = mesh.connectivity.shape[0]
+        self._check_gll()
+        self._operators()
+        self._geometry()
+        self._flux_coefficients()
+        self._faces()
+
+    # -- reference element -----------------------------------------------------
+    def _check_gll(self):
+        m = self.master
+        x1 = refelem.gauss_lobatto(m.p)
+        if m.nodes1d is None or np.max(np.abs(m.nodes1d - x1)) > 1e-13:
+            raise DiscError("tensor path needs GLL solution nodes")
+        L = m.phi1d
+        if self.nd == 3:
+            kron = np.einsum("zk,yj,xi->zyxkji", L, L, L).reshape(m.phi.shape)
+        else:
+            kron = np.einsum("yj,xi->yxji", L, L).reshape(m.phi.shape)
+        if np.max(np.abs(kron - m.phi)) > 1e-12:
+            raise DiscError("master basis is not the tensor GLL basis")
+
+    def _operators(self):
+        m = self.master
+        n1 = self.n1
+        L, dL = m.phi1d, m.dphi1d
+        w = m.quad1d[1]
+        basis = refelem.TensorLegendreBasis(1, m.p)
+        V = basis.eval(m.nodes1d[:, None])
+        Vd = basis.grad(m.nodes1d[:, None])[:, :, 0]
+        self.d1 = Vd @ np.linalg.inv(V)                       # D[i][m] = l'_m(x_i)
+        self.m1 = np.einsum("q,qa,qb->ab", w, L, L)
+        self.s1 = np.einsum("q,qa,qb->ab", w, dL, L)          # S[a][b] = int l'_a l_b
+        mi = np.linalg.inv(self.m1)
+        self.clo = mi[:, 0].copy()
+        self.chi = mi[:, n1 - 1].copy()
+        self.m1inv = mi
+
+    def _geometry(self):
+        mesh, nd = self.mesh, self.nd
+        geom = refelem.build_geom_master(mesh.elem_kind, mesh.p_geom)
+        self.geom_master = geom
+        corners = refelem.VERTS[mesh.elem_kind]
+        gd = geom.eval_basis_grad(corners)                    # (nv, ng, nd)
+        J = np.einsum("egd,vgr->evdr", mesh.ho_nodes, gd)
+        scale = max(mesh.diameter(), 1.0)
+        if np.max(np.abs(J - J[:, :1])) > 1e-11 * scale:
+            raise DiscError("B200 tensor path needs affine elements (curved or "
+                            "non-parallelepiped elements are not supported yet)")
+        J = J[:, 0]
+        self.detj = np.linalg.det(J)
+        if np.any(self.detj <= 0):
+            bad = int(np.argmax(self.detj <= 0))
+            raise DiscError(f"nonpositive Jacobian in element {bad}")
+        self.invjt = np.linalg.inv(J).transpose(0, 2, 1)
+        self.x0 = np.einsum("egd,g->ed", mesh.ho_nodes,
+                            geom.eval_basis(np.zeros((1, nd)))[0])  # image of xi = 0
+        self.J = J
+        self.geo = np.concatenate([self.detj[:, None], self.invjt.reshape(self.ne, -1)], axis=1)
+        m = self.master
+        self.elem_vol = self.detj * m.quad_wts.sum()
+
+    def node_coords(self, elems=None, nodes=None):
+        """Physical coordinates of solution nodes (affine map)."""
+        m = self.master
+        xi = m.nodes if nodes is None else m.nodes[nodes]
+        e = slice(None) if elems is None else elems
+        return self.x0[e][:, None, :] + np.einsum("edr,nr->end", self.J[e], xi)
+
+    def _flux_coefficients(self):
+        model, nd, ncu = self.model, self.nd, self.ncu
+        mu = model.mu_bindings()
+        var = [f"u{i + 1}" for i in range(ncu)] + \
+            [f"q{i + 1}_{j + 1}" for i in range(ncu) for j in range(nd)]
+        forms = affine_form(model.flux_plan(), mu, set(var))
+        if forms is None:
+            raise DiscError("B200 path needs a flux linear in (u, q) with constant "
+                            "coefficients (nonlinear fluxes are not supported yet)")
+        if any(abs(c) > 0 for _, c in forms):
+            raise DiscError("flux has a state-independent part; not supported")
+        self.au = np.zeros((5, 3, 5))
+        self.aq = np.zeros((5, 3, 5, 3))
+        for c in range(ncu):
+            for d in range(nd):
+                co = forms[c * nd + d][0]
+                for k in range(ncu):
+                    self.au[c, d, k] = co.get(f"u{k + 1}", 0.0)
+                    for e in range(nd):
+                        self.aq[c, d, k, e] = co.get(f"q{k + 1}_{e + 1}", 0.0)
+        self.flux_uses_u = bool(np.any(self.au != 0))
+        if uses_any(model.source_plan(), ("u", "q", "w")):
+            raise DiscError("state-dependent sources are not supported on the B200 path yet")
+        self.source_zero = plan_is_zero(model.source_plan())
+        mp = model.mass_plan()
+        mforms = affine_form(mp, mu, set())
+        self.mass_const = mforms is not None
+        self.mass_coef = np.zeros(5)
+        if mforms is not None:
+            for c in range(ncu):
+                self.mass_coef[c] = mforms[c][1]
+        ws = model.wavespeed_plan()
+        if ws is not None and uses_any(ws, ("u", "q", "w", "x")):
+            raise DiscError("wavespeed depending on the state or x is not supported yet")
+
+    # -- faces -------------------------------------------------------------------
+    def face_node_vol(self, lf):
+        """Volume node index of each face node t (increasing volume order)."""
+        n1, nd = self.n1, self.nd
+        ax, hi = FACE_AXIS[self.master.kind][lf]
+        io = n1 - 1 if hi else 0
+        t = np.arange(self.nfn)
+        if nd == 2:
+            return io + n1 * t if ax == 0 else t + n1 * io
+        a, b = t % n1, t // n1
+        if ax == 0:
+            return io + n1 * a + n1 * n1 * b
+        if ax == 1:
+            return a + n1 * io + n1 * n1 * b
+        return a + n1 * b + n1 * n1 * io
+
+    def face_normal_area(self, elems, lf):
+        """Outward unit normal and |t1 x t2| of local face lf (affine)."""
+        _, T = face_map(self.master.kind, lf)
+        tn = np.cross(T[0], T[1]) if self.nd == 3 else np.array([T[0][1], -T[0][0]])
+        v = np.einsum("edr,r->ed", self.invjt[elems], tn)
+        ln = np.linalg.norm(v, axis=1)
+        return v / ln[:, None], self.detj[elems] * ln
+
+    def _faces(self):
+        topo, model, mesh = self.topo, self.model, self.mesh
+        ne, nf, nfn = self.ne, self.nf, self.nfn
+        fnbr = np.full((ne, nf), -1, dtype=np.int32)
+        finfo = np.full((ne, nf), -1, dtype=np.int32)
+        ftau = np.zeros((ne, nf))
+        nfi = topo.elem_l.shape[0]
+        el, fl, er, fr = (np.asarray(a, dtype=np.int64) for a in
+                          (topo.elem_l, topo.face_l, topo.elem_r, topo.face_r))
+        # switch bits, the reference way
+        self.switch = self._switch_bits(el, fl)
+        # penalty
+        tau = float(model.numflux.tau)
+        over_h = model.numflux.tau_over_h
+        over_h = True if over_h is None else bool(over_h)      # kind D default
+        fw = self.master.faces[0].weights.sum()
+        ws = model.wavespeed_plan()
+        mu = model.mu_bindings()
+
+        def lam(normals):
+            if ws is None or normals.shape[0] == 0:
+                return 0.0
+            b = {"t": 0.0, **mu}
+            for k in range(self.nd):
+                b[f"n{k + 1}"] = normals[:, k]
+            return evaluate(ws, b)[0]
+
+        n_l = np.zeros((nfi, self.nd))
+        area = np.zeros(nfi)
+        for lf in range(nf):
+            sel = np.nonzero(fl == lf)[0]
+            if sel.size:
+                n_l[sel], sj = self.face_normal_area(el[sel], lf)
+                area[sel] = sj * fw
+        fi_h = 0.5 * (self.elem_vol[el] + self.elem_vol[er]) / np.maximum(area, 1e-300)
+        tau_i = (tau / fi_h if over_h else np.full(nfi, tau)) + lam(n_l)
+        self.fi_h = fi_h
+        # neighbour node maps
+        maps, mapid_l, mapid_r = self._node_maps(el, fl, er, fr)
+        self.nmap = maps
+        sw = self.switch.astype(np.int32)
+        fnbr[el, fl] = er
+        fnbr[er, fr] = el
+        finfo[el, fl] = 0 | (sw << 3) | (mapid_l << 8)
+        finfo[er, fr] = 0 | 4 | (sw << 3) | (mapid_r << 8)
+        ftau[el, fl] = tau_i
+        ftau[er, fr] = tau_i
+        # boundary faces
+        eb, fb, tb = (np.asarray(a, dtype=np.int64) for a in
+                      (topo.elem_b, topo.face_b, topo.tag_b))
+        self.bc_groups = []
+        for tag in (np.unique(tb) if tb.size else []):
+            tag = int(tag)
+            if tag not in model.bcs:
+                raise DiscError(f"mesh boundary tag {tag} has no [bc] entry")
+            bc = model.bcs[tag]
+            if bc.type == "periodic":
+                raise DiscError(f"tag {tag} is periodic in the model but was not "
+                                "paired in the mesh topology")
+            if bc.type not in ("dirichlet", "neumann"):
+                raise DiscError(f"boundary type {bc.type!r} is not supported on the B200 path")
+            self.bc_groups.append((tag, bc, np.nonzero(tb == tag)[0]))
+        kinds = np.zeros(eb.size, dtype=np.int32)
+        for tag, bc, idx in self.bc_groups:
+            kinds[idx] = 1 if bc.type == "dirichlet" else 2
+        nb_ = np.zeros((eb.size, self.nd))
+        area_b = np.zeros(eb.size)
+        for lf in range(nf):
+            sel = np.nonzero(fb == lf)[0]
+            if sel.size:
+                nb_[sel], sj = self.face_normal_area(eb[sel], lf)
+                area_b[sel] = sj * fw
+        fb_h = self.elem_vol[eb] / np.maximum(area_b, 1e-300)
+        tau_b = (tau / fb_h if over_h else np.full(eb.size, tau)) + lam(nb_)
+        self.fb_h = fb_h
+        fnbr[eb, fb] = np.arange(eb.size, dtype=np.int32)
+        finfo[eb, fb] = kinds
+        ftau[eb, fb] = tau_b
+        if np.any(finfo < 0):
+            e = int(np.argwhere(finfo < 0)[0][0])
+            raise DiscError(f"element {e} has an unclassified face")
+        self.fnbr, self.finfo, self.ftau = fnbr, finfo, ftau
+        self.n_boundary = eb.size
+        self.eb, self.fb = eb, fb
+
+    def _switch_bits(self, el, fl):
+        """n_bar . beta_hat > 0 (disc.py:285-287).  Faces whose affine normal
+        is clearly off the n.beta = 0 plane take the sign directly; near-tie
+        faces are recomputed with the reference pipeline so rounding decides
+        them exactly as it does in the reference."""
+        nfi = el.size
+        if nfi == 0:
+            return np.zeros(0, dtype=bool)
+        n = np.zeros((nfi, self.nd))
+        for lf in range(self.nf):
+            sel = np.nonzero(fl == lf)[0]
+            if sel.size:
+                n[sel], _ = self.face_normal_area(el[sel], lf)
+        d = n @ (np.ones(self.nd) / np.sqrt(self.nd))
+        sw = d > 0.0
+        near = np.abs(d) < 1e-8
+        if near.any():
+            idx = np.nonzero(near)[0]
+            sw[idx] = _reference_switch_subset(self.mesh, self.master, self.geom_master,
+                                               el[idx], fl[idx])
+        return sw
+
+    def _node_maps(self, el, fl, er, fr, chunk=1 << 15):
+        """Own face node t -> neighbour volume node, both sides; returns
+        (unique maps, map id of the left side, map id of the right side).
+
+        Per (face_l, face_r) class a candidate permutation is found by
+        nearest-node matching on one face and verified on all faces of the
+        class at once; faces it does not fit (other orientations) go round
+        again, so structured meshes cost one vectorised check per class."""
+        nfi, nfn = el.size, self.nfn
+        if nfi == 0:
+            return np.zeros((1, nfn), dtype=np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32)
+        perm_lr = np.zeros((nfi, nfn), dtype=np.int64)   # left t -> right t'
+        tr = np.asarray(self.topo.translation, dtype=float)
+        if tr.shape[0] != nfi:
+            tr = np.zeros((nfi, self.nd))
+        tol2 = (1e-9 * max(self.mesh.diameter(), 1.0)) ** 2
+        for a in range(self.nf):
+            va = self.face_node_vol(a)
+            for b in range(self.nf):
+                rem = np.nonzero((fl == a) & (fr == b))[0]
+                vb = self.face_node_vol(b)
+                while rem.size:
+                    f0 = rem[:1]
+                    xl = self.node_coords(el[f0], va) + tr[f0][:, None, :]
+                    xr = self.node_coords(er[f0], vb)
+                    d2 = np.sum((xl[:, :, None, :] - xr[:, None, :, :]) ** 2, axis=3)
+                    p = np.argmin(d2[0], axis=1)
+                    if d2[0][np.arange(nfn), p].max() > tol2 or \
+                            np.unique(p).size != nfn:
+                        raise DiscError("non-conforming face nodes (hanging or "
+                                        "misaligned faces are not supported)")
+                    ok = np.zeros(rem.size, dtype=bool)
+                    for c0 in range(0, rem.size, chunk):
+                        s_ = rem[c0:c0 + chunk]
+                        xl = self.node_coords(el[s_], va) + tr[s_][:, None, :]
+                        xr = self.node_coords(er[s_], vb[p])
+                        ok[c0:c0 + chunk] = np.sum((xl - xr) ** 2, axis=2).max(axis=1) <= tol2
+                    perm_lr[rem[ok]] = p
+                    rem = rem[~ok]
+        vol = np.stack([self.face_node_vol(a) for a in range(self.nf)])   # (nf, nfn)
+        map_l = vol[fr[:, None], perm_lr]                   # left t -> right vol node
+        inv = np.argsort(perm_lr, axis=1)                   # right t' -> left t
+        map_r = vol[fl[:, None], inv]
+        # distinct maps via a hash of (class, permutation) rows
+        allm = np.concatenate([map_l, map_r], axis=0)
+        key = allm @ (np.int64(self.n1 ** self.nd + 1) ** np.arange(nfn, dtype=np.int64) %
+                      np.int64(2 ** 61 - 1))
+        _, first, ids = np.unique(key, return_index=True, return_inverse=True)
+        uniq = allm[first]
+        if not np.array_equal(uniq[ids], allm):
+            raise DiscError("face node map hashing collided")
+        ids = ids.reshape(-1).astype(np.int32)
+        if uniq.shape[0] >= (1 << 16):
+            raise DiscError("too many distinct face orientations")
+        return uniq.astype(np.int32), ids[:nfi], ids[nfi:]
+
+    # -- time-dependent data ---------------------------------------------------------
+    def boundary_projection(self, t):
+        """(n_bfaces, nfn, ncu) L2 projection of Dirichlet / Neumann data onto
+        the face nodes: the face quadrature of any trace against it equals the
+        reference's quadrature of the raw data (disc.py:559-563, 775-782)."""
+        nb_ = self.n_boundary
+        out = np.zeros((nb_, self.nfn, self.ncu))
+        if nb_ == 0:
+            return out
+        m, geom, model = self.master, self.geom_master, self.model
+        mu = model.mu_bindings()
+        w = m.faces[0].weights
+        for tag, bc, idx in self.bc_groups:
+            plan = model.bc_plan(tag)
+            for lf in range(self.nf):
+                s = idx[self.fb[idx] == lf]
+                if s.size == 0:
+                    continue
+                face = m.faces[lf]
+                xq = np.einsum("qg,kgd->kqd", geom.eval_basis(face.xi),
+                               self.mesh.ho_nodes[self.eb[s]])
+                n, _ = self.face_normal_area(self.eb[s], lf)
+                b = {"t": float(t), **mu}
+                for k in range(self.nd):
+                    b[f"x{k + 1}"] = xq[..., k].ravel()
+                    b[f"n{k + 1}"] = np.repeat(n[:, k], xq.shape[1])
+                g = evaluate(plan, b)                       # (ncu, B)
+                if g.shape[1] != xq.shape[0] * xq.shape[1]:
+                    g = np.broadcast_to(g, (g.shape[0], xq.shape[0] * xq.shape[1]))
+                if not np.isfinite(g).all():
+                    col = int(np.argwhere(~np.isfinite(g))[0][1])
+                    raise KernelNanError(f"bc tag {tag} kernel produced non-finite "
+                                         f"values (first at element {col // xq.shape[1]})")
+                g = g.reshape(self.ncu, s.size, -1).transpose(1, 2, 0)   # (k, nqf, ncu)
+                Phi = face.phi[:, self.face_node_vol(lf)]              # (nqf, nfn)
+                Mf = Phi.T @ (w[:, None] * Phi)
+                P = np.linalg.solve(Mf, Phi.T * w[None, :])            # (nfn, nqf)
+                out[s] = np.einsum("tq,kqc->ktc", P, g)
+        return out
+
+    def source_load(self, t):
+        """(ne, nb, ncu) = -int s(x, t) phi (disc.py:621-629), or None."""
+        if self.source_zero:
+            return None
+        m, model = self.master, self.model
+        b = {"t": float(t), **model.mu_bindings()}
+        out = np.empty((self.ne, m.n_nodes, self.ncu))
+        step = 1 << 15
+        for c0 in range(0, self.ne, step):
+            e = np.arange(c0, min(self.ne, c0 + step))
+            xq = self.x0[e][:, None, :] + np.einsum("edr,qr->eqd", self.J[e], m.quad_pts)
+            for k in range(self.nd):
+                b[f"x{k + 1}"] = xq[..., k].ravel()
+            s = evaluate(model.source_plan(), b)
+            if s.shape[1] != xq.shape[0] * xq.shape[1]:
+                s = np.broadcast_to(s, (s.shape[0], xq.shape[0] * xq.shape[1]))
+            if not np.isfinite(s).all():
+                col = int(np.argwhere(~np.isfinite(s))[0][1])
+                raise KernelNanError("source kernel produced non-finite values "
+                                     f"(first at element {c0 + col // xq.shape[1]})")
+            s = s.reshape(self.ncu, e.size, -1)                       # (c, e, q)
+            wd = self.detj[e][:, None] * m.quad_wts[None, :]
+            out[e] = -np.einsum("eq,ceq,qa->eac", wd, s, m.phi)
+        return out

@@ -1,0 +1,109 @@
+"""B200 kernels vs the reference (golden vectors) and vs the oracle.
+
+Bar (BASELINE.json north_star): residual vectors agree to 1e-12 relative
+L2 in fp64; connectivity and switch bits bit-exact."""
+
+import numpy as np
+import pytest
+
+from cases import CASES, GOLDEN, b200_setup, build_case
+
+pytestmark = pytest.mark.gpu
+TENSOR = sorted(n for n, s in CASES.items() if s["kind"] in ("quad", "hex"))
+TOL = 1e-12
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def system_for(name):
+    from paper_2205_07824_b200.system import LdgSystem
+    return LdgSystem(*build_case(CASES[name], *b200_setup()))
+
+
+@pytest.mark.parametrize("name", TENSOR)
+def test_residual_tangent_mixed_vs_reference_golden(name):
+    from paper_2205_07824_b200.system import SolverState
+    g = np.load(GOLDEN / f"{name}.npz")
+    s = system_for(name)
+    assert np.array_equal(s.fi_switch, g["switch"])
+    st = SolverState(u=g["u"], q=None, w=None, t=0.0)
+    R, _, _ = s.residual(st)
+    J, _, _ = s.residual_tangent(st, g["du"])
+    assert isinstance(R, np.ndarray) and R.shape == g["R"].shape
+    assert rel(R, g["R"]) < TOL
+    assert rel(J, g["Jdu"]) < TOL
+    assert rel(s.compute_mixed(g["u"], 0.0), g["q"]) < TOL
+    assert rel(s.compute_mixed(g["du"], 0.0, homogeneous=True), g["dq"]) < TOL
+
+
+@pytest.mark.parametrize("kind,counts,p", [("hex", [7, 6, 5], 3), ("hex", [5, 4, 6], 1),
+                                          ("hex", [4, 4, 3], 4), ("hex", [3, 3, 4], 5),
+                                          ("quad", [13, 9], 3), ("quad", [6, 7], 6)])
+def test_vs_oracle_poisson_larger(kind, counts, p):
+    from oracle import make_oracle
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem, SolverState
+    nd = len(counts)
+    m = model.load_model(str(GOLDEN / f"poisson{nd}d.model"))
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * nd, counts, kind)
+    topo = meshgen.build_face_topology(mesh)
+    master = refelem.build_master(kind, p)
+    s = LdgSystem(m, mesh, topo, master)
+    o = make_oracle(m, mesh, topo, master)
+    rng = np.random.default_rng(7)
+    u = rng.normal(size=(s.n_elements, s.n_nodes, 1))
+    du = rng.normal(size=u.shape)
+    st = SolverState(u=u, q=None, w=None, t=0.0)
+    assert rel(s.residual(st)[0], o.residual(u)) < TOL
+    assert rel(s.residual_tangent(st, du)[0], o.residual_tangent(u, du)) < TOL
+
+
+def test_convdiff_periodic_p1_to_p5_vs_oracle():
+    from cases import BOX_PERIODIC
+    from oracle import make_oracle
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem, SolverState
+    m = model.builtin_model("convection_diffusion", nd=3, mu=[1.0, 1.0, 1.0, 1.0])
+    m.bcs = {}
+    for p, n in ((1, 6), (2, 5), (3, 4), (4, 3), (5, 3)):
+        mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [n] * 3, "hex")
+        topo = meshgen.build_face_topology(mesh, BOX_PERIODIC[3])
+        master = refelem.build_master("hex", p)
+        s = LdgSystem(m, mesh, topo, master)
+        o = make_oracle(m, mesh, topo, master)
+        rng = np.random.default_rng(p)
+        u = rng.normal(size=(s.n_elements, s.n_nodes, 1))
+        st = SolverState(u=u, q=None, w=None, t=0.0)
+        assert rel(s.residual_tangent(st, u)[0], o.residual_tangent(u, u)) < TOL, p
+
+
+def test_device_path_is_deterministic_and_linear_at_scale():
+    """Size-independent properties at a config-3-like size: bitwise
+    run-to-run reproducibility and linearity of the tangent."""
+    import torch
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem
+    m = model.load_model(str(GOLDEN / "poisson3d.model"))
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [24] * 3, "hex")
+    s = LdgSystem(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("hex", 3))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    shape = (s.n_elements, s.n_nodes, 1)
+    a = torch.randn(shape, dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn(shape, dtype=torch.float64, device="cuda", generator=g)
+    Ja, Ja2 = s.tangent_dev(a), s.tangent_dev(a)
+    assert torch.equal(Ja, Ja2)
+    Jb = s.tangent_dev(b)
+    Jab = s.tangent_dev(1.5 * a - 0.25 * b)
+    err = torch.linalg.norm(Jab - (1.5 * Ja - 0.25 * Jb)) / torch.linalg.norm(Jab)
+    assert float(err) < 1e-13
+
+
+def test_nan_reported_with_element():
+    from paper_2205_07824_b200.system import KernelNanError, SolverState
+    s = system_for("poisson3d_hex_p2")
+    u = np.zeros((s.n_elements, s.n_nodes, 1))
+    u[5, 3, 0] = np.nan
+    with pytest.raises(KernelNanError, match="non-finite values"):
+        s.residual(SolverState(u=u, q=None, w=None, t=0.0))
