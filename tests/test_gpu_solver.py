@@ -1,0 +1,111 @@
+"""Device Newton-GMRES / block-Jacobi vs the reference (golden solve
+histories) and the oracle solver.  Bar: converged solutions within 1e-10
+relative L2, Newton/GMRES iteration counts within +-1."""
+
+import numpy as np
+import pytest
+
+from cases import ACCEPT_FLAGS, GOLDEN, SOLVE_CASES, b200_setup, build_case
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def test_gmres_matches_oracle_on_dense_operator():
+    import torch
+    from oracle.solver_oracle import gmres as ogmres
+    from paper_2205_07824_b200.solver import gmres
+    rng = np.random.default_rng(0)
+    for trial in range(5):
+        n = 60
+        A = rng.normal(size=(n, n))
+        A += np.diag(np.abs(A).sum(axis=1) + 1.0)      # test_solver.py:45-57
+        b = rng.normal(size=n)
+        Ad = torch.as_tensor(A, device="cuda")
+        res = gmres(lambda v: Ad @ v, b, rel_tol=1e-10, restart=20, max_iter=200)
+        xo, conv, its, hist, _ = ogmres(lambda v: A @ v, b, None, 1e-10, 20, 200)
+        assert res.converged and conv
+        assert abs(res.iterations - its) <= 1
+        assert rel(res.x, np.linalg.solve(A, b)) < 1e-8
+        k = min(len(hist), len(res.residual_norms))
+        np.testing.assert_allclose(res.residual_norms[:k], hist[:k], rtol=1e-6)
+
+
+def test_gmres_reference_edge_cases():
+    import torch
+    from paper_2205_07824_b200.solver import SolverError, gmres
+    I = lambda v: v.clone()  # noqa: E731
+    r = gmres(I, np.arange(1.0, 9.0))
+    assert r.converged and r.iterations == 1
+    r = gmres(I, np.zeros(3))
+    assert r.converged and r.iterations == 0
+    with pytest.raises(SolverError):
+        gmres(I, np.ones(2), rel_tol=2.0)
+    with pytest.raises(SolverError):
+        gmres(lambda v: v * float("nan"), np.ones(4))
+    del torch
+
+
+@pytest.mark.parametrize("name", sorted(SOLVE_CASES))
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+def test_steady_solve_matches_reference(name, orth):
+    from paper_2205_07824_b200.driver import run_steady
+    from paper_2205_07824_b200.system import LdgSystem
+    spec = SOLVE_CASES[name]
+    g = np.load(GOLDEN / f"solve_{name}.npz")
+    s = LdgSystem(*build_case(spec, *b200_setup()))
+    f = ACCEPT_FLAGS
+    st, stats, _ = run_steady(s, precond=spec["precond"], abs_tol=f["abs_tol"],
+                              rel_tol=f["rel_tol"], forcing=f["forcing"],
+                              restart=f["restart"], gmres_max_iter=f["gmres_max_iter"],
+                              orth=orth)
+    assert stats.converged
+    assert stats.newton_iters == int(g["newton_iters"])
+    assert abs(stats.total_gmres_iters - int(np.sum(g["gmres_iters"]))) <= 1, \
+        (stats.gmres_iters, g["gmres_iters"])
+    assert rel(st.u.cpu().numpy(), g["u"]) < 1e-10
+
+
+def test_block_jacobi_blocks_match_oracle():
+    import torch
+    from cases import CASES
+    from oracle import make_oracle
+    from oracle.solver_oracle import (block_jacobi_blocks, distance2_coloring,
+                                      element_neighbors)
+    from paper_2205_07824_b200.driver import _steady_fns, build_pde_block_jacobi
+    from paper_2205_07824_b200.system import LdgSystem
+    parts = build_case(CASES["poisson2d_quad_p3"], *b200_setup())
+    s = LdgSystem(*parts)
+    o = make_oracle(*parts)
+    ne, bs = s.n_elements, s.n_nodes
+    colors = distance2_coloring(element_neighbors(parts[2], ne))
+    mats = block_jacobi_blocks(lambda x, v: o.residual_tangent(
+        x.reshape(ne, bs, 1), v.reshape(ne, bs, 1)).ravel(), np.zeros(ne * bs), ne, bs, colors)
+    rf, tf = _steady_fns(s)
+    M = build_pde_block_jacobi(s, rf, tf, torch.zeros(ne * bs, device="cuda"))
+    r = np.random.default_rng(3).normal(size=ne * bs)
+    z = M.apply(torch.as_tensor(r, device="cuda")).cpu().numpy()
+    want = np.concatenate([np.linalg.solve(mats[b], r[b * bs:(b + 1) * bs]) for b in range(ne)])
+    assert rel(z, want) < 1e-11
+    assert int(M.shifted.sum()) == 0
+
+
+def test_block_jacobi_shift_rule_on_singular_block():
+    import torch
+    from paper_2205_07824_b200.solver import build_block_jacobi
+    # operator with an exactly singular first block: R(u) = A u blockwise
+    bs, nb = 4, 3
+    A = np.stack([np.eye(bs) for _ in range(nb)])
+    A[0, 1, 1] = 0.0
+    Ad = torch.as_tensor(A, device="cuda")
+
+    def tan(x, v):
+        return torch.einsum("bij,bj->bi", Ad, v.reshape(nb, bs)).reshape(-1)
+
+    M = build_block_jacobi(tan, torch.zeros(nb * bs, device="cuda"), nb, bs, np.zeros(nb, int))
+    assert M.shifted.cpu().tolist() == [1, 0, 0]
+    z = M.apply(torch.ones(nb * bs, dtype=torch.float64, device="cuda")).cpu().numpy()
+    assert abs(z[1] - 1e12) / 1e12 < 1e-6 and abs(z[5] - 1.0) < 1e-14
