@@ -89,19 +89,34 @@ int ldg_version(void);
 int ldg_compute_mixed(LdgHandle* h, const double* u, const double* gproj,
                       double* q, void* stream);
 
-/* R(u) (disc.py:595-653): q must be compute_mixed(u) with the same gproj;
- * bsrc (ne, nb, ncu) = -int s(x,t) phi or NULL; gproj Dirichlet/Neumann
- * projected data. */
-int ldg_residual(LdgHandle* h, const double* u, const double* q,
-                 const double* gproj, const double* bsrc, double* R,
-                 void* stream);
+/* Device scratch (doubles) the residual / tangent calls need: the face
+ * export buffer of the fused operator, ne * 2nd * n1^(nd-1) * ncu. */
+int64_t ldg_scratch_doubles(LdgHandle* h);
 
-/* dR = J(u) du with the reference linearisation (disc.py:591-604, frozen
- * tau): computes dq = compute_mixed(du, homogeneous) into dq_scratch and
- * then the flux pass.  Linear constant-coefficient fluxes do not read the
- * base state. */
-int ldg_residual_tangent(LdgHandle* h, const double* du, double* dq_scratch,
+/* R(u) (disc.py:588-653) by the fused two-pass operator (ldg_fused.cu):
+ * the mixed gradient never leaves the SM.  gproj: projected Dirichlet /
+ * Neumann data (n_bfaces, n1^(nd-1), ncu) or NULL for zero data; bsrc
+ * (ne, nb, ncu) = -int s(x,t) phi or NULL. */
+int ldg_residual(LdgHandle* h, const double* u, const double* gproj,
+                 const double* bsrc, double* scratch, double* R, void* stream);
+
+/* dR = J(u) du with the reference linearisation (disc.py:591-604: frozen
+ * tau, homogeneous Dirichlet lift, zero Neumann tangent).  Fluxes linear in
+ * (u, q) with constant coefficients do not read the base state. */
+int ldg_residual_tangent(LdgHandle* h, const double* du, double* scratch,
                          double* dR, void* stream);
+
+/* One pass of the fused operator (1 = element pass, 2 = face completion),
+ * for per-kernel timing; ldg_residual(_tangent) = pass 1 then pass 2. */
+int ldg_operator_pass(LdgHandle* h, int pass, int tangent, const double* u,
+                      const double* gproj, const double* bsrc, double* scratch,
+                      double* R, void* stream);
+
+/* Unfused reference structure, kept for comparison: flux pass from a
+ * precomputed q = compute_mixed(u) (72 B/DOF of HBM traffic at nd = 3). */
+int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
+                        const double* q, const double* gproj,
+                        const double* bsrc, double* R, void* stream);
 
 /* constant-mass operator and its block inverse (element mass M_e =
  * detJ * M1 (x) M1 (x) M1) */

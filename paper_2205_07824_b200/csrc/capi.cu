@@ -131,21 +131,43 @@ int ldg_compute_mixed(LdgHandle* h, const double* u, const double* gproj,
   return rc ? fail(rc, "compute_mixed launch", cudaGetLastError()) : 0;
 }
 
-int ldg_residual(LdgHandle* h, const double* u, const double* q,
-                 const double* gproj, const double* bsrc, double* R,
-                 void* stream) {
-  if (!h || !u || !q || !R) return fail(2, "null argument");
-  int rc = ldg::launch_flux(h->P, false, u, q, gproj, bsrc, R, (cudaStream_t)stream);
+int64_t ldg_scratch_doubles(LdgHandle* h) {
+  if (!h) return -1;
+  const int64_t nf = 2 * h->P.nd;
+  int64_t nfn = h->P.nd == 3 ? (int64_t)h->P.n1 * h->P.n1 : h->P.n1;
+  return (int64_t)h->P.ne * nf * nfn * h->P.ncu;
+}
+
+int ldg_residual(LdgHandle* h, const double* u, const double* gproj,
+                 const double* bsrc, double* scratch, double* R, void* stream) {
+  if (!h || !u || !R || !scratch) return fail(2, "null argument");
+  int rc = ldg::launch_fused(h->P, false, u, gproj, bsrc, R, scratch, (cudaStream_t)stream);
   return rc ? fail(rc, "residual launch", cudaGetLastError()) : 0;
 }
 
-int ldg_residual_tangent(LdgHandle* h, const double* du, double* dq,
+int ldg_residual_tangent(LdgHandle* h, const double* du, double* scratch,
                          double* dR, void* stream) {
-  if (!h || !du || !dq || !dR) return fail(2, "null argument");
-  cudaStream_t s = (cudaStream_t)stream;
-  int rc = ldg::launch_mixed(h->P, du, nullptr, dq, s);
-  if (!rc) rc = ldg::launch_flux(h->P, true, du, dq, nullptr, nullptr, dR, s);
+  if (!h || !du || !scratch || !dR) return fail(2, "null argument");
+  int rc = ldg::launch_fused(h->P, true, du, nullptr, nullptr, dR, scratch,
+                             (cudaStream_t)stream);
   return rc ? fail(rc, "residual_tangent launch", cudaGetLastError()) : 0;
+}
+
+int ldg_operator_pass(LdgHandle* h, int pass, int tangent, const double* u,
+                      const double* gproj, const double* bsrc, double* scratch,
+                      double* R, void* stream) {
+  if (!h || !u || !R || !scratch || pass < 1 || pass > 2) return fail(2, "bad argument");
+  int rc = ldg::launch_fused_pass(h->P, pass, tangent != 0, u, gproj, bsrc, R, scratch,
+                                  (cudaStream_t)stream);
+  return rc ? fail(rc, "operator pass launch", cudaGetLastError()) : 0;
+}
+
+int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
+                        const double* q, const double* gproj,
+                        const double* bsrc, double* R, void* stream) {
+  if (!h || !u || !q || !R) return fail(2, "null argument");
+  int rc = ldg::launch_flux(h->P, tangent != 0, u, q, gproj, bsrc, R, (cudaStream_t)stream);
+  return rc ? fail(rc, "flux launch", cudaGetLastError()) : 0;
 }
 
 int ldg_mass_apply(LdgHandle* h, const double* v, double scale, double* out,

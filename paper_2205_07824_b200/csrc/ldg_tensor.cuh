@@ -45,6 +45,12 @@ int launch_mixed(const TensorParams& P, const double* u, const double* gproj,
 int launch_flux(const TensorParams& P, bool tangent, const double* u,
                 const double* q, const double* gproj, const double* bsrc,
                 double* R, cudaStream_t s);
+int launch_fused(const TensorParams& P, bool tangent, const double* u,
+                 const double* gproj, const double* bsrc, double* R, double* X,
+                 cudaStream_t s);
+int launch_fused_pass(const TensorParams& P, int pass, bool tangent, const double* u,
+                      const double* gproj, const double* bsrc, double* R, double* X,
+                      cudaStream_t s);
 int launch_mass(const TensorParams& P, bool inverse, const double* v,
                 double scale, double* out, cudaStream_t s);
 

@@ -246,21 +246,39 @@ class LdgSystem:
                    "ldg_compute_mixed")
         return q
 
-    def residual_dev(self, u, t=0.0, out=None, q_scratch=None):
-        q = self.mixed_dev(u, t, out=q_scratch)
+    def scratch(self):
+        """Face-export scratch of the fused operator (device, cached)."""
+        if "x" not in self._scratch:
+            n = int(self.lib.ldg_scratch_doubles(self._h))
+            self._scratch["x"] = self._empty((max(n, 1),))
+        return self._scratch["x"]
+
+    def residual_dev(self, u, t=0.0, out=None, scratch=None):
         R = out if out is not None else self._empty(u.shape)
+        x = scratch if scratch is not None else self.scratch()
         _lib.check(self.lib.ldg_residual(
-            self._h, _lib.ptr(u), _lib.ptr(q), _lib.ptr(self.boundary_data(t)),
-            _lib.ptr(self.source_data(t)), _lib.ptr(R), self._stream()), "ldg_residual")
+            self._h, _lib.ptr(u), _lib.ptr(self.boundary_data(t)),
+            _lib.ptr(self.source_data(t)), _lib.ptr(x), _lib.ptr(R), self._stream()),
+            "ldg_residual")
         return R
 
-    def tangent_dev(self, du, out=None, dq_scratch=None):
-        dq = dq_scratch if dq_scratch is not None else self._empty(
-            (self.n_elements, self.n_nodes, self.ncu, self.nd))
+    def tangent_dev(self, du, out=None, scratch=None):
         R = out if out is not None else self._empty(du.shape)
-        _lib.check(self.lib.ldg_residual_tangent(self._h, _lib.ptr(du), _lib.ptr(dq),
+        x = scratch if scratch is not None else self.scratch()
+        _lib.check(self.lib.ldg_residual_tangent(self._h, _lib.ptr(du), _lib.ptr(x),
                                                  _lib.ptr(R), self._stream()),
                    "ldg_residual_tangent")
+        return R
+
+    def flux_from_mixed_dev(self, u, q, tangent, t=0.0, out=None):
+        """The unfused two-kernel structure (mixed -> flux), for comparison."""
+        R = out if out is not None else self._empty(u.shape)
+        g = None if tangent else self.boundary_data(t)
+        b = None if tangent else self.source_data(t)
+        _lib.check(self.lib.ldg_flux_from_mixed(self._h, int(bool(tangent)), _lib.ptr(u),
+                                                _lib.ptr(q), _lib.ptr(g), _lib.ptr(b),
+                                                _lib.ptr(R), self._stream()),
+                   "ldg_flux_from_mixed")
         return R
 
     def mass_apply_dev(self, v, scale=1.0, out=None):

@@ -369,8 +369,8 @@ class TensorTables:
         sw = self.switch.astype(np.int32)
         fnbr[el, fl] = er
         fnbr[er, fr] = el
-        finfo[el, fl] = 0 | (sw << 3) | (mapid_l << 8)
-        finfo[er, fr] = 0 | 4 | (sw << 3) | (mapid_r << 8)
+        finfo[el, fl] = 0 | (sw << 3) | (fr.astype(np.int32) << 4) | (mapid_l << 8)
+        finfo[er, fr] = 0 | 4 | (sw << 3) | (fl.astype(np.int32) << 4) | (mapid_r << 8)
         ftau[el, fl] = tau_i
         ftau[er, fr] = tau_i
         # boundary faces

@@ -72,7 +72,7 @@ def mixed(tab, u, gproj=None):
     return q
 
 
-def flux(tab, u, q, tangent, gproj=None, bsrc=None):
+def flux(tab, u, q, tangent, gproj=None, bsrc=None, split=False):
     nd, n1 = tab.nd, tab.n1
     ne, nb, ncu = u.shape
     au, aq = tab.au[:ncu, :nd, :ncu], tab.aq[:ncu, :nd, :ncu, :nd]
@@ -111,6 +111,10 @@ def flux(tab, u, q, tangent, gproj=None, bsrc=None):
             qr = np.where(right[..., None], qo[it], qn)
             uh = 0.5 * (ul + ur) if cen else np.where(sw, ul, ur)
             qh = 0.5 * (ql + qr) if gcen else np.where(sw[..., None], qr, ql)
+            if split:
+                # pass 1 keeps only this side's share of q^
+                mine = (sw == right)[..., None]
+                qh = 0.5 * qo[it] if gcen else np.where(mine, qo[it], 0.0)
             pen = np.where(right, -1.0, 1.0) * tau[it][:, None, None] * (ul - uh)
             ff = np.einsum("cdk,etk->etcd", au, uh) + np.einsum("cdkx,etkx->etcd", aq, qh)
             fa = np.einsum("etcd,ed->etc", ff, ij[it][:, :, ax])
@@ -136,4 +140,54 @@ def flux(tab, u, q, tangent, gproj=None, bsrc=None):
         R[:, vol[lf]] += x[:, vol[lf]]
     if not tangent and bsrc is not None:
         R += bsrc
+    return R
+
+
+
+def fused(tab, u, tangent, gproj=None, bsrc=None):
+    """Emulate ldg_fused.cu: pass 1 = flux with only the own share of q^,
+    exports X = sJ n.(Aq q); pass 2 adds -w X_nbr through the
+    neighbour-local-face bits and node maps, lifted by (M1 (x) M1)."""
+    nd, n1, nfn = tab.nd, tab.n1, tab.nfn
+    ne, nb, ncu = u.shape
+    q = mixed(tab, u, None if tangent else gproj)
+    R = flux(tab, u, q, tangent, gproj, bsrc, split=True)
+    aq = tab.aq[:ncu, :nd, :ncu, :nd]
+    vol = _vol_nodes(tab)
+    ax_side = _axis_side(tab)
+    gcen = tab.model.numflux.grad_trace == "centered"
+    X = np.zeros((ne, tab.nf, nfn, ncu))
+    for lf in range(tab.nf):
+        ax, hi = ax_side[lf]
+        f = np.einsum("cdkx,etkx->etcd", aq, q[:, vol[lf]])
+        X[:, lf] = (1.0 if hi else -1.0) * tab.detj[:, None, None] * \
+            np.einsum("etcd,ed->etc", f, tab.invjt[:, :, ax])
+    for lf in range(tab.nf):
+        info, nbr = tab.finfo[:, lf], tab.fnbr[:, lf]
+        it = np.nonzero((info & 3) == 0)[0]
+        if it.size == 0:
+            continue
+        right = (info[it] & 4) > 0
+        sw = (info[it] & 8) > 0
+        act = np.ones(it.size, bool) if gcen else (sw != right)
+        it = it[act]
+        if it.size == 0:
+            continue
+        nlf = (info[it] >> 4) & 7
+        nn = tab.nmap[info[it] >> 8]
+        tn = np.full(nn.shape, -1)
+        for b in range(tab.nf):
+            inv = np.full(nb, -1)
+            inv[vol[b]] = np.arange(nfn)
+            sel = nlf == b
+            tn[sel] = inv[nn[sel]]
+        assert np.all(tn >= 0)
+        w = 0.5 if gcen else 1.0
+        full = np.zeros((it.size, nb, ncu))
+        full[:, vol[lf]] = -w * X[nbr[it][:, None], nlf[:, None], tn]
+        x = full
+        for a in range(nd):
+            if a != ax_side[lf][0]:
+                x = _apply1d(tab.m1, x, a, nd, n1)
+        R[it[:, None], vol[lf][None, :]] += x[:, vol[lf]]
     return R

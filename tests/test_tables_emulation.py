@@ -28,6 +28,9 @@ def test_tensor_algebra_matches_reference(name):
     assert rel(emu.flux(tab, g["u"], q, False, gp, bs), g["R"]) < 1e-13
     assert rel(emu.flux(tab, g["du"], dq, True), g["Jdu"]) < 1e-13
     assert rel(tab.fi_h, g["fi_h"]) < 1e-13
+    # the fused two-pass split (ldg_fused.cu) reproduces the same operator
+    assert rel(emu.fused(tab, g["u"], False, gp, bs), g["R"]) < 1e-13
+    assert rel(emu.fused(tab, g["du"], True), g["Jdu"]) < 1e-13
 
 
 @pytest.mark.parametrize("name", ["poisson2d_tri_p2", "poisson3d_tet_p2"])
