@@ -181,7 +181,7 @@ class _Workspace:
             self.V = torch.empty((m + 1, n), dtype=torch.float64, device=device)
             self.Z = torch.empty((m, n), dtype=torch.float64, device=device)
             self.w = torch.empty(n, dtype=torch.float64, device=device)
-            self.H = torch.zeros((m + 2, m + 1), dtype=torch.float64, device=device)
+            self.H = torch.zeros((m + 1, m + 2), dtype=torch.float64, device=device)  # row k = column k of H
             self.c = torch.zeros(m + 2, dtype=torch.float64, device=device)
             self.nrm = torch.zeros(4, dtype=torch.float64, device=device)
             self.key = (m, n, str(device))
@@ -240,7 +240,7 @@ def gmres(op, rhs, precond=None, rel_tol=1e-8, restart=30, max_iter=200, x0=None
             Z[k].copy_(z)
             w.copy_(apply_op(Z[k]))
             ops.nrm2(w, nr[0:1])
-            col = Hd[:, k]
+            col = Hd[k]                     # contiguous: device kernels index it linearly
             if orth == "cgs2":
                 ops.cgs_dots(V, k + 1, w, col)
                 ops.cgs_update(V, k + 1, col, w, nr[1:2])
