@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 #include "ldg_tensor.cuh"
 
 namespace {
@@ -37,6 +38,7 @@ struct LdgHandle {
   int32_t* finfo = nullptr;
   double* ftau = nullptr;
   int32_t* nmap = nullptr;
+  double* frec = nullptr;
   unsigned long long* bad = nullptr;
 };
 
@@ -61,6 +63,16 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   rc |= upload(&h->finfo, t->finfo, ne * nf, "finfo");
   rc |= upload(&h->ftau, t->ftau, ne * nf, "ftau");
   rc |= upload(&h->nmap, t->nmap, (size_t)t->n_maps * nfn, "nmap");
+  {
+    // packed 16-byte face records {double tau; int32 nbr; int32 info}
+    std::vector<double> rec(ne * nf * 2);
+    for (size_t x = 0; x < ne * nf; ++x) {
+      rec[2 * x] = t->ftau[x];
+      int32_t pair[2] = {t->fnbr[x], t->finfo[x]};
+      memcpy(&rec[2 * x + 1], pair, sizeof(pair));
+    }
+    rc |= upload(&h->frec, rec.data(), rec.size(), "frec");
+  }
   cudaError_t e = cudaMalloc(&h->bad, sizeof(unsigned long long));
   if (e != cudaSuccess) rc |= fail(3, "bad flag", e);
   else cudaMemset(h->bad, 0xff, sizeof(unsigned long long));
@@ -74,7 +86,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   P.grad_centered = t->grad_centered;
   P.flux_uses_u = t->flux_uses_u;
   P.geo = h->geo; P.fnbr = h->fnbr; P.finfo = h->finfo; P.ftau = h->ftau;
-  P.nmap = h->nmap; P.bad = h->bad;
+  P.nmap = h->nmap; P.bad = h->bad; P.frec = h->frec;
   const int n1 = t->n1;
   // tables arrive with row stride n1 packed at the front of each array
   memcpy(P.d1, t->d1, sizeof(P.d1));
@@ -112,7 +124,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
 int ldg_destroy(LdgHandle* h) {
   if (!h) return 0;
   cudaFree(h->geo); cudaFree(h->fnbr); cudaFree(h->finfo); cudaFree(h->ftau);
-  cudaFree(h->nmap); cudaFree(h->bad);
+  cudaFree(h->nmap); cudaFree(h->frec); cudaFree(h->bad);
   delete h;
   return 0;
 }

@@ -76,32 +76,53 @@ __device__ __forceinline__ void bad_if(const TensorParams& P, int e, double v) {
 // --------------------------------------------------------------------------
 //
 // Thread roles per element (lt in [0, TPE)):
-//   column owner  (hex: (i,j), quad: i)   owns the k (quad: j) node column
-//   y-pencil owner (hex only: (i,k))      owns nodes (i, 0..N1-1, k)
-//   row owner     (hex: (j,k), quad: j)   owns nodes (0..N1-1, j, k) (contiguous)
-//   face-node     (t = lt on every face)
+//   column owner   (hex (i,j) / quad i)  owns the node column along k (quad j)
+//   y-pencil owner (hex (i,k))           owns nodes (i, 0..N1-1, k)
+//   row owner      (hex (j,k) / quad j)  owns nodes (0..N1-1, j, k)
+//   face-node      (t = lt on every face)
 // Every 1D contraction is done by the owner of the pencil along its axis, so
-// all operator indices are compile-time (constant-bank DFMA operands) and
-// each shared-memory value loaded feeds N1 FMAs.
+// operator indices are compile-time (constant-bank DFMA operands) and each
+// value loaded from shared memory feeds N1 FMAs.  Hex volume planes use a
+// rotation swizzle, sw(i,j,k) = (i+k)%N1 + N1 (j+k)%N1 + N1^2 k, which makes
+// column, row, y-pencil and face-node accesses bank-conflict free at N1 = 4.
 //
 // q is never formed: with h_s = -d_s u + sum_{faces f with axis s} lift_f,
-// q = invjt h, and the flux density in reference directions is
+// q = invjt h and the flux density in reference directions is
 //   F_{c,r} = Cu[c][r][k] u_k + C[c][r][k][s] h_{k,s},
-//   C = detJ invjt^T Aq invjt,  Cu = detJ invjt^T Au     (per element).
-// The face export sJ n.(Aq q) equals sgn * F^q_{c,axis} at the face node.
+//   C = detJ invjt^T Aq invjt,  Cu = detJ invjt^T Au     (per element),
+// and the face export sJ n.(Aq q) is sgn * F^q_{c,axis} at the face node.
+// The lifts are added by the pencil owner along the face normal, so each
+// jump is read once per pencil instead of once per node.
+
+struct __align__(16) FaceRec {
+  double tau;
+  int32_t nbr;
+  int32_t info;
+};
+
+template <int N1>
+__device__ __forceinline__ int swz(int i, int j, int k) {
+  int a = i + k, b = j + k;
+  a -= a >= N1 ? N1 : 0;
+  b -= b >= N1 ? N1 : 0;
+  return a + N1 * b + N1 * N1 * k;
+}
 
 template <int N1, int ND, int NCU>
 struct P1Smem {
   static constexpr int NF = ND == 3 ? N1 * N1 : N1;
   static constexpr int NB = ND == 3 ? N1 * N1 * N1 : N1 * N1;
+  static constexpr int NBP = ND == 3 ? NB : NB + 4;          // quad: slot padding
   static constexpr int NFACE = 2 * ND;
   static constexpr int NC = NCU * ND * NCU * ND + NCU * ND * NCU;   // C then Cu
-  static constexpr int GSZ = (ND - 1) * NCU * NB;                   // gx (,gy) planes
-  static constexpr int EXT = 6 * N1 * N1;                           // face-slab pencils
-  static constexpr int WORK = GSZ > EXT ? GSZ : EXT;
-  static constexpr int FSZ = NCU * ND * NB;                         // F^q, then stages
-  static constexpr int FSZ2 = FSZ > ND * NB ? FSZ : ND * NB;
-  static constexpr int PER = NCU * NB + WORK + FSZ2 + 2 * NFACE * NF * NCU + NC;
+  static constexpr int FACEV = NFACE * NF * NCU;
+  // region R1: h planes (ND-1 per component), later 3 stage planes
+  static constexpr int R1 = (ND - 1) * NCU * NBP > 3 * NBP ? (ND - 1) * NCU * NBP : 3 * NBP;
+  static constexpr int EXT = ND == 3 ? 6 * N1 * N1 : 2 * N1;  // face-slab pencils
+  static constexpr int SJ = FACEV > EXT ? FACEV : EXT;       // jumps, later pencils
+  static constexpr int SF = FACEV > NBP ? FACEV : NBP;       // face F^q, later B23
+  static constexpr int SU = NCU * NBP > NBP ? NCU * NBP : NBP;
+  static constexpr int PER = SU + R1 + SJ + FACEV + SF + NC;
   static constexpr int TPE = NF;
   static constexpr int EPB_T = (kFBlock / TPE) > 0 ? (kFBlock / TPE) : 1;
   static constexpr int EPB_S = kFSmemDoubles / PER > 0 ? kFSmemDoubles / PER : 1;
@@ -110,27 +131,39 @@ struct P1Smem {
 
 template <int N1, int ND, int NCU, bool TANGENT>
 __global__ void __launch_bounds__(kFBlock)
-fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ u,
-             const double* __restrict__ gproj, const double* __restrict__ bsrc,
-             double* __restrict__ R, double* __restrict__ X) {
+fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+             const double* __restrict__ u, const double* __restrict__ gproj,
+             const double* __restrict__ bsrc, double* __restrict__ R,
+             double* __restrict__ X) {
   using S = P1Smem<N1, ND, NCU>;
-  constexpr int NB = S::NB, NF = S::NF, TPE = S::TPE, EPB = S::EPB, NFACE = S::NFACE;
-  constexpr int NC = S::NC, CQ = NCU * ND * NCU * ND;
-  __shared__ double su[EPB][NCU][NB];
-  __shared__ double swork[EPB][S::WORK];       // gx/gy planes, then face-slab pencils
-  __shared__ double sF[EPB][S::FSZ2];          // F^q planes, then stage planes
-  __shared__ double sj[EPB][NFACE][NF][NCU];   // jumps u - u^
-  __shared__ double sfh[EPB][NFACE][NF][NCU];  // sJ f^ (own share)
-  __shared__ double sC[EPB][NC];
+  constexpr int NB = S::NB, NBP = S::NBP, NF = S::NF, TPE = S::TPE, EPB = S::EPB;
+  constexpr int NFACE = S::NFACE, NC = S::NC, CQ = NCU * ND * NCU * ND;
+  __shared__ __align__(16) double s_u[EPB][S::SU];      // u planes; later B1 plane
+  __shared__ __align__(16) double s_r1[EPB][S::R1];     // h planes; later stage planes
+  __shared__ __align__(16) double s_j[EPB][S::SJ];      // jumps; later face-slab pencils
+  __shared__ __align__(16) double s_fh[EPB][S::FACEV];  // sJ f^ (own share)
+  __shared__ __align__(16) double s_f[EPB][S::SF];      // face F^q; later B23 plane
+  __shared__ double s_c[EPB][NC];
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
   const int e = blockIdx.x * EPB + slot;
   const bool active = slot < EPB && e < P.ne;
-  const int ta = lt % N1, tb = ND == 3 ? lt / N1 : 0;   // (i,j) | (i,k) | (j,k) ; quad: i | j
-  const int i = ta, j = tb;                              // column owner coordinates
+  const int ta = lt % N1, tb = ND == 3 ? lt / N1 : 0;
+  const int i = ta, j = tb;
+  double* su = s_u[slot];
+  double* sj = s_j[slot];
+  double* sfh = s_fh[slot];
+  double* sff = s_f[slot];
+  double* sr = s_r1[slot];
+  // volume-plane index (hex: swizzled)
+  auto vix = [](int a, int b, int k) {
+    return ND == 3 ? swz<N1>(a, b, k) : a + N1 * k;
+  };
+  auto fix = [](int lf, int t, int c) { return (lf * NF + t) * NCU + c; };
 
-  // ---- A: column of u, element geometry
+  // ---- A: u column, geometry, face records, C coefficients
   double uc[NCU][N1];
   double detj = 1.0, ij[ND][ND];
+  FaceRec fr[NFACE];
   if (active) {
     const double* ue = u + (size_t)e * NB * NCU;
 #pragma unroll
@@ -139,7 +172,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
         uc[c][k] = __ldg(ue + node * NCU + c);
-        su[slot][c][node] = uc[c][k];
+        su[c * NBP + vix(i, j, k)] = uc[c][k];
       }
     }
     const double* g = P.geo + (size_t)e * (1 + ND * ND);
@@ -148,9 +181,14 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
     for (int d = 0; d < ND; ++d)
 #pragma unroll
       for (int r = 0; r < ND; ++r) ij[d][r] = __ldg(g + 1 + d * ND + r);
-    // C[c][r][k][s] = detJ sum_{d,e} invjt[d][r] aq[c][d][k][e] invjt[e][s];
-    // Cu[c][r][k] = detJ sum_d invjt[d][r] au[c][d][k]
-    // (dynamic r_/s_ indices read invjt from global/L1, keeping ij in registers)
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(frec + (size_t)e * NFACE + lf));
+      fr[lf].tau = v.x;
+      const int2 w = *reinterpret_cast<const int2*>(&v.y);
+      fr[lf].nbr = w.x;
+      fr[lf].info = w.y;
+    }
     const double* gij = g + 1;
     for (int x = lt; x < NC; x += TPE) {
       double v = 0.0;
@@ -170,36 +208,36 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
         for (int d = 0; d < ND; ++d)
           v = fma(__ldg(gij + d * ND + r_), P.au[(c_ * 3 + d) * LDG_MAX_NCU + k_], v);
       }
-      sC[slot][x] = detj * v;
+      s_c[slot][x] = detj * v;
     }
   }
   __syncthreads();
 
   // ---- B: face node lt of every face: jumps and the u part of sJ f^
-  int info[NFACE];
+  double gl[NCU][N1];       // d/dk of the column (registers)
   if (active) {
 #pragma unroll
     for (int lf = 0; lf < NFACE; ++lf) {
-      info[lf] = __ldg(P.finfo + e * NFACE + lf);
-      const int nbr = __ldg(P.fnbr + e * NFACE + lf);
-      const int kind = info[lf] & LDG_FACE_KIND_MASK;
+      const int info = fr[lf].info, nbr = fr[lf].nbr;
+      const int kind = info & LDG_FACE_KIND_MASK;
       const int ax = face_axis(ND, lf);
       const double sgn = face_side(ND, lf) ? 1.0 : -1.0;
       const int vn = fvol<N1, ND>(lf, lt);
+      const int vs = ND == 3 ? swz<N1>(vn % N1, (vn / N1) % N1, vn / (N1 * N1)) : vn;
       double len2 = 0.0;
 #pragma unroll
       for (int d = 0; d < ND; ++d) len2 = fma(ij[d][ax], ij[d][ax], len2);
       const double sjac = detj * sqrt(len2);
-      const double tau = __ldg(P.ftau + e * NFACE + lf);
+      const double tau = fr[lf].tau;
       double uo[NCU], uh[NCU], fh[NCU], jmp[NCU];
 #pragma unroll
-      for (int c = 0; c < NCU; ++c) uo[c] = su[slot][c][vn];
+      for (int c = 0; c < NCU; ++c) uo[c] = su[c * NBP + vs];
       if (kind == LDG_FACE_INTERIOR) {
-        const bool right = info[lf] & LDG_FACE_SIDE_RIGHT;
-        const bool sw = info[lf] & LDG_FACE_SWITCH;
+        const bool right = info & LDG_FACE_SIDE_RIGHT;
+        const bool sw = info & LDG_FACE_SWITCH;
         double un[NCU];
         if (P.trace_centered || (sw == right) || !sw) {
-          const int nn = __ldg(P.nmap + (info[lf] >> LDG_FACE_MAP_SHIFT) * NF + lt);
+          const int nn = __ldg(P.nmap + (info >> LDG_FACE_MAP_SHIFT) * NF + lt);
 #pragma unroll
           for (int c = 0; c < NCU; ++c) un[c] = __ldg(u + ((size_t)nbr * NB + nn) * NCU + c);
         } else {
@@ -230,25 +268,20 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
         }
       }
       if (P.flux_uses_u && kind != LDG_FACE_NEUMANN) {
-        // sJ n.(Au u^) = sgn * Cu[c][ax][k] u^_k
 #pragma unroll
         for (int c = 0; c < NCU; ++c) {
           double a = 0.0;
 #pragma unroll
-          for (int kk = 0; kk < NCU; ++kk) a = fma(sC[slot][CQ + (c * ND + ax) * NCU + kk], uh[kk], a);
+          for (int kk = 0; kk < NCU; ++kk) a = fma(s_c[slot][CQ + (c * ND + ax) * NCU + kk], uh[kk], a);
           fh[c] = fma(sgn, a, fh[c]);
         }
       }
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
-        sj[slot][lf][lt][c] = jmp[c];
-        sfh[slot][lf][lt][c] = fh[c];
+        sj[fix(lf, lt, c)] = jmp[c];
+        sfh[fix(lf, lt, c)] = fh[c];
       }
     }
-  }
-  // ---- C: gradient pencils (owner of the pencil along each axis)
-  double gl[NCU][N1];       // gradient along the column axis (registers)
-  if (active) {
 #pragma unroll
     for (int c = 0; c < NCU; ++c)
 #pragma unroll
@@ -259,64 +292,61 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
         gl[c][k] = a;
       }
   }
-  __syncthreads();          // su complete (B wrote only sj/sfh/sC)
+  __syncthreads();
+
+  // ---- C: h pencils along x (row owner) and y (y-pencil owner), lifts folded in
   if (active) {
+    // quad faces: 0 y-, 1 x+, 2 y+, 3 x-; hex: 0 z-, 1 z+, 2 y-, 3 y+, 4 x-, 5 x+
+    constexpr int XLO = ND == 3 ? 4 : 3, XHI = ND == 3 ? 5 : 1;
 #pragma unroll
     for (int c = 0; c < NCU; ++c) {
-      // row owner: x derivative of the row (0..N1-1, tb-coords)
       double row[N1];
 #pragma unroll
-      for (int m = 0; m < N1; ++m)
-        row[m] = su[slot][c][ND == 3 ? m + N1 * ta + N1 * N1 * tb : m + N1 * ta];
+      for (int m = 0; m < N1; ++m) row[m] = su[c * NBP + (ND == 3 ? vix(m, ta, tb) : m + N1 * ta)];
+      const int t = ND == 3 ? ta + N1 * tb : ta;
+      const double jl = sj[fix(XLO, t, c)], jh = sj[fix(XHI, t, c)];
 #pragma unroll
       for (int a = 0; a < N1; ++a) {
         double v = 0.0;
 #pragma unroll
         for (int m = 0; m < N1; ++m) v = fma(P.d1[a * N1 + m], row[m], v);
-        swork[slot][c * NB + (ND == 3 ? a + N1 * ta + N1 * N1 * tb : a + N1 * ta)] = v;
+        sr[c * NBP + (ND == 3 ? vix(a, ta, tb) : a + N1 * ta)] = -v - P.clo[a] * jl + P.chi[a] * jh;
       }
       if (ND == 3) {
-        // y-pencil owner (i,k) = (ta, tb)
         double col[N1];
 #pragma unroll
-        for (int m = 0; m < N1; ++m) col[m] = su[slot][c][ta + N1 * m + N1 * N1 * tb];
+        for (int m = 0; m < N1; ++m) col[m] = su[c * NBP + vix(ta, m, tb)];
+        const double yl = sj[fix(2, ta + N1 * tb, c)], yh = sj[fix(3, ta + N1 * tb, c)];
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
           double v = 0.0;
 #pragma unroll
           for (int m = 0; m < N1; ++m) v = fma(P.d1[a * N1 + m], col[m], v);
-          swork[slot][(NCU + c) * NB + ta + N1 * a + N1 * N1 * tb] = v;
+          sr[(NCU + c) * NBP + vix(ta, a, tb)] = -v - P.clo[a] * yl + P.chi[a] * yh;
         }
       }
     }
   }
   __syncthreads();
 
-  // ---- D: h = -grad u + lifted jumps, F = Cu u + C h at the column's nodes
+  // ---- D: F = Cu u + C h at the column's nodes; F^q at face nodes
   double F[NCU][ND][N1];
   if (active) {
-    const double cli = P.clo[i], chi_i = P.chi[i];
-    const double clj = ND == 3 ? P.clo[j] : 0.0, chj = ND == 3 ? P.chi[j] : 0.0;
+    constexpr int ZLO = ND == 3 ? 0 : 0, ZHI = ND == 3 ? 1 : 2;   // column-axis faces
+    double zl[NCU], zh[NCU];
+#pragma unroll
+    for (int c = 0; c < NCU; ++c) {
+      zl[c] = sj[fix(ZLO, ND == 3 ? i + N1 * j : i, c)];
+      zh[c] = sj[fix(ZHI, ND == 3 ? i + N1 * j : i, c)];
+    }
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
-      const int node = ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k;
       double h[NCU][ND];
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
-        if (ND == 3) {
-          // faces: 0 z-, 1 z+, 2 y-, 3 y+, 4 x-, 5 x+
-          h[c][0] = -swork[slot][c * NB + node] - cli * sj[slot][4][j + N1 * k][c]
-                    + chi_i * sj[slot][5][j + N1 * k][c];
-          h[c][1] = -swork[slot][(NCU + c) * NB + node] - clj * sj[slot][2][i + N1 * k][c]
-                    + chj * sj[slot][3][i + N1 * k][c];
-          h[c][2] = -gl[c][k] - P.clo[k] * sj[slot][0][i + N1 * j][c]
-                    + P.chi[k] * sj[slot][1][i + N1 * j][c];
-        } else {
-          // quad faces: 0 y-, 1 x+, 2 y+, 3 x-
-          h[c][0] = -swork[slot][c * NB + node] - cli * sj[slot][3][k][c]
-                    + chi_i * sj[slot][1][k][c];
-          h[c][ND - 1] = -gl[c][k] - P.clo[k] * sj[slot][0][i][c] + P.chi[k] * sj[slot][2][i][c];
-        }
+        h[c][0] = sr[c * NBP + vix(i, j, k)];
+        if (ND == 3) h[c][1] = sr[(NCU + c) * NBP + vix(i, j, k)];
+        h[c][ND - 1] = -gl[c][k] - P.clo[k] * zl[c] + P.chi[k] * zh[c];
       }
 #pragma unroll
       for (int c = 0; c < NCU; ++c)
@@ -327,15 +357,28 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
           for (int kk = 0; kk < NCU; ++kk)
 #pragma unroll
             for (int s_ = 0; s_ < ND; ++s_)
-              fq = fma(sC[slot][((c * ND + r) * NCU + kk) * ND + s_], h[kk][s_], fq);
-          sF[slot][(c * ND + r) * NB + node] = fq;
+              fq = fma(s_c[slot][((c * ND + r) * NCU + kk) * ND + s_], h[kk][s_], fq);
           double fu = 0.0;
           if (P.flux_uses_u) {
 #pragma unroll
             for (int kk = 0; kk < NCU; ++kk)
-              fu = fma(sC[slot][CQ + (c * ND + r) * NCU + kk], uc[kk][k], fu);
+              fu = fma(s_c[slot][CQ + (c * ND + r) * NCU + kk], uc[kk][k], fu);
           }
           F[c][r][k] = fq + fu;
+          // F^q of the face-normal component at this column's face nodes
+          if (ND == 3) {
+            if (r == 2 && k == 0) sff[fix(0, i + N1 * j, c)] = fq;
+            if (r == 2 && k == N1 - 1) sff[fix(1, i + N1 * j, c)] = fq;
+            if (r == 1 && j == 0) sff[fix(2, i + N1 * k, c)] = fq;
+            if (r == 1 && j == N1 - 1) sff[fix(3, i + N1 * k, c)] = fq;
+            if (r == 0 && i == 0) sff[fix(4, j + N1 * k, c)] = fq;
+            if (r == 0 && i == N1 - 1) sff[fix(5, j + N1 * k, c)] = fq;
+          } else {
+            if (r == 1 && k == 0) sff[fix(0, i, c)] = fq;
+            if (r == 1 && k == N1 - 1) sff[fix(2, i, c)] = fq;
+            if (r == 0 && i == 0) sff[fix(3, k, c)] = fq;
+            if (r == 0 && i == N1 - 1) sff[fix(1, k, c)] = fq;
+          }
         }
     }
   }
@@ -345,25 +388,24 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
   if (active) {
 #pragma unroll
     for (int lf = 0; lf < NFACE; ++lf) {
-      const int kind = info[lf] & LDG_FACE_KIND_MASK;
+      const int info = fr[lf].info;
+      const int kind = info & LDG_FACE_KIND_MASK;
       if (kind == LDG_FACE_NEUMANN) continue;
       double w_own = 1.0;
       bool exp_ = false;
       if (kind == LDG_FACE_INTERIOR) {
-        const bool right = info[lf] & LDG_FACE_SIDE_RIGHT;
-        const bool sw = info[lf] & LDG_FACE_SWITCH;
+        const bool right = info & LDG_FACE_SIDE_RIGHT;
+        const bool sw = info & LDG_FACE_SWITCH;
         const bool mine = sw == right;
         w_own = P.grad_centered ? 0.5 : (mine ? 1.0 : 0.0);
         exp_ = P.grad_centered || mine;
       }
       if (w_own == 0.0 && !exp_) continue;
-      const int ax = face_axis(ND, lf);
       const double sgn = face_side(ND, lf) ? 1.0 : -1.0;
-      const int vn = fvol<N1, ND>(lf, lt);
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
-        const double xf = sgn * sF[slot][(c * ND + ax) * NB + vn];
-        sfh[slot][lf][lt][c] = fma(w_own, xf, sfh[slot][lf][lt][c]);
+        const double xf = sgn * sff[fix(lf, lt, c)];
+        sfh[fix(lf, lt, c)] = fma(w_own, xf, sfh[fix(lf, lt, c)]);
         if (exp_) X[(((size_t)e * NFACE + lf) * NF + lt) * NCU + c] = xf;
       }
     }
@@ -372,8 +414,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
 
   // ---- F..H: R = -sum_r K_r F_r + face terms, sum factorised by pencils
   double* Re = R + (size_t)(active ? e : 0) * NB * NCU;
-  double* sP = sF[slot];         // stage planes
-  double* sX = swork[slot];      // face-slab pencils
+  double* sX = sj;             // face-slab pencils (jumps are dead)
 #pragma unroll
   for (int c = 0; c < NCU; ++c) {
     if (ND == 3) {
@@ -388,20 +429,20 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
             a2 = fma(P.m1[k * N1 + m], F[c][1][m], a2);
             a3 = fma(P.s1[k * N1 + m], F[c][2][m], a3);
           }
-          if (k == 0) a3 -= sfh[slot][0][i + N1 * j][c];
-          if (k == N1 - 1) a3 -= sfh[slot][1][i + N1 * j][c];
-          const int node = i + N1 * j + N1 * N1 * k;
-          sP[node] = a1;
-          sP[NB + node] = a2;
-          sP[2 * NB + node] = a3;
+          if (k == 0) a3 -= sfh[fix(0, i + N1 * j, c)];
+          if (k == N1 - 1) a3 -= sfh[fix(1, i + N1 * j, c)];
+          const int v = vix(i, j, k);
+          sr[v] = a1;
+          sr[NBP + v] = a2;
+          sr[2 * NBP + v] = a3;
         }
-        // face slabs along z: p = (type x|y, side, idx), out[k] = M_z fh
+        // face-slab pencils along z: p = (type x|y, side, idx): out[k] = M fh
         for (int p = lt; p < 4 * N1; p += TPE) {
           const int type = p / (2 * N1), side = (p / N1) & 1, idx = p % N1;
           const int lf = type == 0 ? 4 + side : 2 + side;
           double v[N1];
 #pragma unroll
-          for (int n = 0; n < N1; ++n) v[n] = sfh[slot][lf][idx + N1 * n][c];
+          for (int n = 0; n < N1; ++n) v[n] = sfh[fix(lf, idx + N1 * n, c)];
 #pragma unroll
           for (int k = 0; k < N1; ++k) {
             double a = 0.0;
@@ -412,17 +453,18 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
         }
       }
       __syncthreads();
-      double B1[N1], B23[N1];
       if (active) {
-        // y stage (pencil owner (i,k) = (ta,tb))
+        // y stage (pencil owner (i,k) = (ta,tb)); B1 -> su plane, B23 -> sff plane
         double a1[N1], a2[N1], a3[N1];
 #pragma unroll
         for (int m = 0; m < N1; ++m) {
-          const int node = ta + N1 * m + N1 * N1 * tb;
-          a1[m] = sP[node];
-          a2[m] = sP[NB + node];
-          a3[m] = sP[2 * NB + node];
+          const int v = vix(ta, m, tb);
+          a1[m] = sr[v];
+          a2[m] = sr[NBP + v];
+          a3[m] = sr[2 * NBP + v];
         }
+        const double yl = sX[((1 * 2 + 0) * N1 + ta) * N1 + tb];
+        const double yh = sX[((1 * 2 + 1) * N1 + ta) * N1 + tb];
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
           double b1 = 0.0, b2 = 0.0;
@@ -432,19 +474,11 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
             b2 = fma(P.s1[a * N1 + m], a2[m], b2);
             b2 = fma(P.m1[a * N1 + m], a3[m], b2);
           }
-          B1[a] = b1;
-          B23[a] = b2;
-        }
-        B23[0] -= sX[((1 * 2 + 0) * N1 + ta) * N1 + tb];
-        B23[N1 - 1] -= sX[((1 * 2 + 1) * N1 + ta) * N1 + tb];
-      }
-      __syncthreads();
-      if (active) {
-#pragma unroll
-        for (int a = 0; a < N1; ++a) {
-          const int node = ta + N1 * a + N1 * N1 * tb;
-          sP[node] = B1[a];
-          sP[NB + node] = B23[a];
+          if (a == 0) b2 -= yl;
+          if (a == N1 - 1) b2 -= yh;
+          const int v = vix(ta, a, tb);
+          su[v] = b1;
+          sff[v] = b2;
         }
         // x-face slabs along y: Bx[side][j][k] = sum_m M[j][m] Ax[side][m][k]
         for (int p = lt; p < 2 * N1; p += TPE) {
@@ -463,14 +497,17 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
       }
       __syncthreads();
       if (active) {
-        // x stage (row owner (j,k) = (ta,tb)): contiguous row
+        // x stage (row owner (j,k) = (ta,tb))
         double b1[N1], b23[N1];
 #pragma unroll
         for (int m = 0; m < N1; ++m) {
-          const int node = m + N1 * ta + N1 * N1 * tb;
-          b1[m] = sP[node];
-          b23[m] = sP[NB + node];
+          const int v = vix(m, ta, tb);
+          b1[m] = su[v];
+          b23[m] = sff[v];
         }
+        const double xl = sX[4 * N1 * N1 + (0 * N1 + ta) * N1 + tb];
+        const double xh = sX[4 * N1 * N1 + (1 * N1 + ta) * N1 + tb];
+        double out[N1];
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
           double r = 0.0;
@@ -479,16 +516,20 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
             r = fma(P.s1[a * N1 + m], b1[m], r);
             r = fma(P.m1[a * N1 + m], b23[m], r);
           }
-          double out = -r;
-          if (a == 0) out += sX[4 * N1 * N1 + (0 * N1 + ta) * N1 + tb];
-          if (a == N1 - 1) out += sX[4 * N1 * N1 + (1 * N1 + ta) * N1 + tb];
+          out[a] = -r;
+        }
+        out[0] += xl;
+        out[N1 - 1] += xh;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
           const int node = a + N1 * ta + N1 * N1 * tb;
-          if (!TANGENT && bsrc) out += __ldg(bsrc + ((size_t)e * NB + node) * NCU + c);
-          bad_if(P, e, out);
-          Re[node * NCU + c] = out;
+          double o = out[a];
+          if (!TANGENT && bsrc) o += __ldg(bsrc + ((size_t)e * NB + node) * NCU + c);
+          bad_if(P, e, o);
+          Re[node * NCU + c] = o;
         }
       }
-      __syncthreads();
+      if (NCU > 1) __syncthreads();
     } else {
       if (active) {
         // y stage (column owner i): A1 = M F_x, A2 = S F_y - y faces
@@ -500,17 +541,16 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
             a1 = fma(P.m1[k * N1 + m], F[c][0][m], a1);
             a2 = fma(P.s1[k * N1 + m], F[c][ND - 1][m], a2);
           }
-          if (k == 0) a2 -= sfh[slot][0][i][c];
-          if (k == N1 - 1) a2 -= sfh[slot][2][i][c];
-          sP[i + N1 * k] = a1;
-          sP[NB + i + N1 * k] = a2;
+          if (k == 0) a2 -= sfh[fix(0, i, c)];
+          if (k == N1 - 1) a2 -= sfh[fix(2, i, c)];
+          sr[i + N1 * k] = a1;
+          sr[NBP + i + N1 * k] = a2;
         }
-        // x-face slabs along y: Ax[side][k] = sum_n M[k][n] fh[x side][n]
         for (int p = lt; p < 2; p += TPE) {
           const int lf = p == 0 ? 3 : 1;
           double v[N1];
 #pragma unroll
-          for (int n = 0; n < N1; ++n) v[n] = sfh[slot][lf][n][c];
+          for (int n = 0; n < N1; ++n) v[n] = sfh[fix(lf, n, c)];
 #pragma unroll
           for (int k = 0; k < N1; ++k) {
             double a = 0.0;
@@ -522,12 +562,11 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
       }
       __syncthreads();
       if (active) {
-        // x stage (row owner j = ta)
         double a1[N1], a2[N1];
 #pragma unroll
         for (int m = 0; m < N1; ++m) {
-          a1[m] = sP[m + N1 * ta];
-          a2[m] = sP[NB + m + N1 * ta];
+          a1[m] = sr[m + N1 * ta];
+          a2[m] = sr[NBP + m + N1 * ta];
         }
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
@@ -537,13 +576,13 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
             r = fma(P.s1[a * N1 + m], a1[m], r);
             r = fma(P.m1[a * N1 + m], a2[m], r);
           }
-          double out = -r;
-          if (a == 0) out += sX[0 * N1 + ta];
-          if (a == N1 - 1) out += sX[1 * N1 + ta];
+          double o = -r;
+          if (a == 0) o += sX[0 * N1 + ta];
+          if (a == N1 - 1) o += sX[1 * N1 + ta];
           const int node = a + N1 * ta;
-          if (!TANGENT && bsrc) out += __ldg(bsrc + ((size_t)e * NB + node) * NCU + c);
-          bad_if(P, e, out);
-          Re[node * NCU + c] = out;
+          if (!TANGENT && bsrc) o += __ldg(bsrc + ((size_t)e * NB + node) * NCU + c);
+          bad_if(P, e, o);
+          Re[node * NCU + c] = o;
         }
       }
       __syncthreads();
@@ -554,6 +593,11 @@ fused_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ 
 // --------------------------------------------------------------------------
 // pass 2: neighbour share of f(., q^) on faces whose q^ comes from across
 // --------------------------------------------------------------------------
+//
+// Each column owner adds, for its nodes, the (M1 (x) M1)-lifted neighbour
+// exports of every completion face containing them (sum factorised: the
+// in-face row is contracted with the thread's M1 row, the column direction
+// with compile-time M1 entries), then read-modify-writes its R column.
 
 template <int N1, int ND, int NCU>
 struct P2Smem {
@@ -566,85 +610,112 @@ struct P2Smem {
 
 template <int N1, int ND, int NCU>
 __global__ void __launch_bounds__(kFBlock)
-complete_kernel(const __grid_constant__ TensorParams P, const double* __restrict__ X,
-                double* __restrict__ R) {
+complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+                const double* __restrict__ X, double* __restrict__ R) {
   using S = P2Smem<N1, ND, NCU>;
   constexpr int NB = S::NB, NF = S::NF, TPE = S::TPE, EPB = S::EPB, NFACE = S::NFACE;
-  __shared__ double sv[EPB][NF][NCU];
-  __shared__ double sacc[EPB][NCU][NB];
+  __shared__ double sv[EPB][NFACE][NF][NCU];
+  __shared__ int sact[EPB];
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
   const int e = blockIdx.x * EPB + slot;
   const bool active = slot < EPB && e < P.ne;
-  const int a = lt % N1, b = ND == 3 ? lt / N1 : 0;
-  // this thread's rows of M1 for the (M1 (x) M1) face lift
-  double Ma[N1], Mb[N1];
-#pragma unroll
-  for (int m = 0; m < N1; ++m) {
-    Ma[m] = P.m1[a * N1 + m];
-    Mb[m] = ND == 3 ? P.m1[b * N1 + m] : 0.0;
-  }
-  bool any = false;
+  const int i = lt % N1, j = ND == 3 ? lt / N1 : 0;
+  int mask = 0;
   if (active) {
 #pragma unroll
-    for (int c = 0; c < NCU; ++c)
+    for (int lf = 0; lf < NFACE; ++lf) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(frec + (size_t)e * NFACE + lf));
+      const int2 w = *reinterpret_cast<const int2*>(&v.y);
+      const int info = w.y;
+      if ((info & LDG_FACE_KIND_MASK) != LDG_FACE_INTERIOR) continue;
+      const bool right = info & LDG_FACE_SIDE_RIGHT;
+      const bool sw = info & LDG_FACE_SWITCH;
+      if (!(P.grad_centered || (sw != right))) continue;
+      mask |= 1 << lf;
+      const double wgt = P.grad_centered ? -0.5 : -1.0;
+      const int nlf = (info >> 4) & 7;
+      const int nv = __ldg(P.nmap + (info >> LDG_FACE_MAP_SHIFT) * NF + lt);
+      const int tn = vol_to_face<N1, ND>(face_axis(ND, nlf), nv);
 #pragma unroll
-      for (int k = 0; k < N1; ++k)
-        sacc[slot][c][ND == 3 ? a + N1 * b + N1 * N1 * k : a + N1 * k] = 0.0;
-  }
-  for (int lf = 0; lf < NFACE; ++lf) {
-    int info = 0;
-    bool act = false;
-    double w = 0.0;
-    if (active) {
-      info = __ldg(P.finfo + e * NFACE + lf);
-      if ((info & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR) {
-        const bool right = info & LDG_FACE_SIDE_RIGHT;
-        const bool sw = info & LDG_FACE_SWITCH;
-        act = P.grad_centered || (sw != right);
-        w = P.grad_centered ? 0.5 : 1.0;
-      }
-      if (act) {
-        const int nbr = __ldg(P.fnbr + e * NFACE + lf);
-        const int nlf = (info >> 4) & 7;
-        const int nv = __ldg(P.nmap + (info >> LDG_FACE_MAP_SHIFT) * NF + lt);
-        const int tn = vol_to_face<N1, ND>(face_axis(ND, nlf), nv);
-#pragma unroll
-        for (int c = 0; c < NCU; ++c)
-          sv[slot][lt][c] = -w * __ldg(X + (((size_t)nbr * NFACE + nlf) * NF + tn) * NCU + c);
-      }
+      for (int c = 0; c < NCU; ++c)
+        sv[slot][lf][lt][c] = wgt * __ldg(X + (((size_t)w.x * NFACE + nlf) * NF + tn) * NCU + c);
     }
-    any = any || act;
-    __syncthreads();
-    if (act) {
-      const int vn = fvol<N1, ND>(lf, lt);
-#pragma unroll
-      for (int c = 0; c < NCU; ++c) {
-        double acc = 0.0;
-        if (ND == 3) {
-#pragma unroll
-          for (int bb = 0; bb < N1; ++bb) {
-            double s_ = 0.0;
-#pragma unroll
-            for (int aa = 0; aa < N1; ++aa) s_ = fma(Ma[aa], sv[slot][aa + N1 * bb][c], s_);
-            acc = fma(Mb[bb], s_, acc);
-          }
-        } else {
-#pragma unroll
-          for (int aa = 0; aa < N1; ++aa) acc = fma(Ma[aa], sv[slot][aa][c], acc);
-        }
-        sacc[slot][c][vn] += acc;
-      }
-    }
-    __syncthreads();
   }
-  if (!active || !any) return;
+  __syncthreads();
+  if (!active || mask == 0) return;
   double* Re = R + (size_t)e * NB * NCU;
 #pragma unroll
-  for (int k = 0; k < N1; ++k) {
-    const int node = ND == 3 ? a + N1 * b + N1 * N1 * k : a + N1 * k;
+  for (int c = 0; c < NCU; ++c) {
+    double acc[N1];
 #pragma unroll
-    for (int c = 0; c < NCU; ++c) {
-      const double out = Re[node * NCU + c] + sacc[slot][c][node];
+    for (int k = 0; k < N1; ++k) acc[k] = 0.0;
+    if (ND == 3) {
+      // z faces (node (i,j,0|N1-1)): sum_{aa,bb} M[i][aa] M[j][bb] sv[aa + N1 bb]
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int lf = side;
+        if (!(mask & (1 << lf))) continue;
+        double s_ = 0.0;
+#pragma unroll
+        for (int bb = 0; bb < N1; ++bb) {
+          double r = 0.0;
+#pragma unroll
+          for (int aa = 0; aa < N1; ++aa) r = fma(P.m1[i * N1 + aa], sv[slot][lf][aa + N1 * bb][c], r);
+          s_ = fma(P.m1[j * N1 + bb], r, s_);
+        }
+        acc[side ? N1 - 1 : 0] += s_;
+      }
+      // x faces (i = 0 | N1-1, face coords (j,k)); y faces (j = 0 | N1-1, (i,k))
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int lf = q < 2 ? 4 + q : 2 + (q - 2);
+        const bool onface = q < 2 ? (i == (q ? N1 - 1 : 0)) : (j == (q == 3 ? N1 - 1 : 0));
+        if (!(mask & (1 << lf)) || !onface) continue;
+        const int row = q < 2 ? j : i;          // in-face coordinate owned by the thread
+        double w[N1];                           // w[bb] = sum_aa M[row][aa] sv[aa + N1 bb]
+#pragma unroll
+        for (int bb = 0; bb < N1; ++bb) {
+          double r = 0.0;
+#pragma unroll
+          for (int aa = 0; aa < N1; ++aa) r = fma(P.m1[row * N1 + aa], sv[slot][lf][aa + N1 * bb][c], r);
+          w[bb] = r;
+        }
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          double r = 0.0;
+#pragma unroll
+          for (int bb = 0; bb < N1; ++bb) r = fma(P.m1[k * N1 + bb], w[bb], r);
+          acc[k] += r;
+        }
+      }
+    } else {
+      // quad: y faces (node (i, 0|N1-1)): sum_aa M[i][aa] sv[aa]; x faces (i = 0|N1-1)
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int lf = side ? 2 : 0;
+        if (!(mask & (1 << lf))) continue;
+        double s_ = 0.0;
+#pragma unroll
+        for (int aa = 0; aa < N1; ++aa) s_ = fma(P.m1[i * N1 + aa], sv[slot][lf][aa][c], s_);
+        acc[side ? N1 - 1 : 0] += s_;
+      }
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int lf = side ? 1 : 3;
+        if (!(mask & (1 << lf)) || i != (side ? N1 - 1 : 0)) continue;
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          double r = 0.0;
+#pragma unroll
+          for (int aa = 0; aa < N1; ++aa) r = fma(P.m1[k * N1 + aa], sv[slot][lf][aa][c], r);
+          acc[k] += r;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      const int node = ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k;
+      const double out = Re[node * NCU + c] + acc[k];
       bad_if(P, e, out);
       Re[node * NCU + c] = out;
     }
@@ -665,11 +736,14 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
   const int grid2 = (P.ne + S2::EPB - 1) / S2::EPB;
   if (grid <= 0) return 0;
   if (pass & 1) {
-    if (tangent) fused_kernel<N1, ND, NCU, true><<<grid, kFBlock, 0, s>>>(P, u, gproj, bsrc, R, X);
-    else fused_kernel<N1, ND, NCU, false><<<grid, kFBlock, 0, s>>>(P, u, gproj, bsrc, R, X);
+    const FaceRec* fr = reinterpret_cast<const FaceRec*>(P.frec);
+    if (tangent) fused_kernel<N1, ND, NCU, true><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
+    else fused_kernel<N1, ND, NCU, false><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
     if (cudaGetLastError() != cudaSuccess) return 3;
   }
-  if (pass & 2) complete_kernel<N1, ND, NCU><<<grid2, kFBlock, 0, s>>>(P, X, R);
+  if (pass & 2)
+    complete_kernel<N1, ND, NCU><<<grid2, kFBlock, 0, s>>>(
+        P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
