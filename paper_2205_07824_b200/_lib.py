@@ -12,7 +12,10 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libldgb200.so"
+import os
+
+LIB_PATH = Path(os.environ.get("LDGB200_LIB",
+                             Path(__file__).resolve().parent / "lib" / "libldgb200.so"))
 MAX_N1 = 9
 MAX_NCU = 5
 

@@ -37,19 +37,20 @@ def needs_build():
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, out=None, defines=()):
+    lib = Path(out) if out else LIB
+    if not force and out is None and not needs_build():
         return LIB
-    LIB.parent.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                     "--expt-relaxed-constexpr", "-I", str(ROOT / "include"),
-                    "-I", str(CSRC)]
+                    "-I", str(CSRC)] + [f"-D{d}" for d in defines]
     if verbose:
         flags += ["-Xptxas", "-v"]
     procs = []
     for src in SOURCES:
-        obj = LIB.parent / (Path(src).stem + ".o")
+        obj = lib.parent / (Path(src).stem + ".o")
         objs.append(obj)
         cmd = [nvcc(), *flags, "-c", str(CSRC / src), "-o", str(obj)]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE,
@@ -60,13 +61,13 @@ def build(force=False, verbose=False):
             sys.stdout.write(out)
         if p.returncode:
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "shared", *map(str, objs), "-o", str(tmp)]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         o.unlink(missing_ok=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

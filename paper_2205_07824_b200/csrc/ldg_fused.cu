@@ -30,6 +30,9 @@ namespace ldg {
 namespace {
 
 constexpr int kFBlock = 128;
+#ifndef LDG_P1_MINBLOCKS
+#define LDG_P1_MINBLOCKS 1
+#endif
 constexpr int kFSmemDoubles = 6144;   // 48 KB static
 
 template <int N1, int ND, int NCU>
@@ -130,7 +133,7 @@ struct P1Smem {
 };
 
 template <int N1, int ND, int NCU, bool TANGENT>
-__global__ void __launch_bounds__(kFBlock)
+__global__ void __launch_bounds__(kFBlock, LDG_P1_MINBLOCKS)
 fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
              const double* __restrict__ u, const double* __restrict__ gproj,
              const double* __restrict__ bsrc, double* __restrict__ R,
@@ -159,6 +162,20 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     return ND == 3 ? swz<N1>(a, b, k) : a + N1 * k;
   };
   auto fix = [](int lf, int t, int c) { return (lf * NF + t) * NCU + c; };
+  // per-thread shared-plane offsets of the three pencils and the face nodes,
+  // computed once (integer work stays out of the contraction loops)
+  int cidx[N1], ridx[N1], yidx[N1], fvs[NFACE];
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    cidx[k] = vix(i, j, k);
+    ridx[k] = ND == 3 ? vix(k, ta, tb) : k + N1 * ta;
+    yidx[k] = ND == 3 ? vix(ta, k, tb) : 0;
+  }
+#pragma unroll
+  for (int lf = 0; lf < NFACE; ++lf) {
+    const int vn = fvol<N1, ND>(lf, lt);
+    fvs[lf] = ND == 3 ? swz<N1>(vn % N1, (vn / N1) % N1, vn / (N1 * N1)) : vn;
+  }
 
   // ---- A: u column, geometry, face records, C coefficients
   double uc[NCU][N1];
@@ -172,7 +189,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
         uc[c][k] = __ldg(ue + node * NCU + c);
-        su[c * NBP + vix(i, j, k)] = uc[c][k];
+        su[c * NBP + cidx[k]] = uc[c][k];
       }
     }
     const double* g = P.geo + (size_t)e * (1 + ND * ND);
@@ -222,8 +239,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       const int kind = info & LDG_FACE_KIND_MASK;
       const int ax = face_axis(ND, lf);
       const double sgn = face_side(ND, lf) ? 1.0 : -1.0;
-      const int vn = fvol<N1, ND>(lf, lt);
-      const int vs = ND == 3 ? swz<N1>(vn % N1, (vn / N1) % N1, vn / (N1 * N1)) : vn;
+      const int vs = fvs[lf];
       double len2 = 0.0;
 #pragma unroll
       for (int d = 0; d < ND; ++d) len2 = fma(ij[d][ax], ij[d][ax], len2);
@@ -302,7 +318,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     for (int c = 0; c < NCU; ++c) {
       double row[N1];
 #pragma unroll
-      for (int m = 0; m < N1; ++m) row[m] = su[c * NBP + (ND == 3 ? vix(m, ta, tb) : m + N1 * ta)];
+      for (int m = 0; m < N1; ++m) row[m] = su[c * NBP + ridx[m]];
       const int t = ND == 3 ? ta + N1 * tb : ta;
       const double jl = sj[fix(XLO, t, c)], jh = sj[fix(XHI, t, c)];
 #pragma unroll
@@ -310,19 +326,19 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         double v = 0.0;
 #pragma unroll
         for (int m = 0; m < N1; ++m) v = fma(P.d1[a * N1 + m], row[m], v);
-        sr[c * NBP + (ND == 3 ? vix(a, ta, tb) : a + N1 * ta)] = -v - P.clo[a] * jl + P.chi[a] * jh;
+        sr[c * NBP + ridx[a]] = -v - P.clo[a] * jl + P.chi[a] * jh;
       }
       if (ND == 3) {
         double col[N1];
 #pragma unroll
-        for (int m = 0; m < N1; ++m) col[m] = su[c * NBP + vix(ta, m, tb)];
+        for (int m = 0; m < N1; ++m) col[m] = su[c * NBP + yidx[m]];
         const double yl = sj[fix(2, ta + N1 * tb, c)], yh = sj[fix(3, ta + N1 * tb, c)];
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
           double v = 0.0;
 #pragma unroll
           for (int m = 0; m < N1; ++m) v = fma(P.d1[a * N1 + m], col[m], v);
-          sr[(NCU + c) * NBP + vix(ta, a, tb)] = -v - P.clo[a] * yl + P.chi[a] * yh;
+          sr[(NCU + c) * NBP + yidx[a]] = -v - P.clo[a] * yl + P.chi[a] * yh;
         }
       }
     }
@@ -344,8 +360,8 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       double h[NCU][ND];
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
-        h[c][0] = sr[c * NBP + vix(i, j, k)];
-        if (ND == 3) h[c][1] = sr[(NCU + c) * NBP + vix(i, j, k)];
+        h[c][0] = sr[c * NBP + cidx[k]];
+        if (ND == 3) h[c][1] = sr[(NCU + c) * NBP + cidx[k]];
         h[c][ND - 1] = -gl[c][k] - P.clo[k] * zl[c] + P.chi[k] * zh[c];
       }
 #pragma unroll
@@ -431,7 +447,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
           }
           if (k == 0) a3 -= sfh[fix(0, i + N1 * j, c)];
           if (k == N1 - 1) a3 -= sfh[fix(1, i + N1 * j, c)];
-          const int v = vix(i, j, k);
+          const int v = cidx[k];
           sr[v] = a1;
           sr[NBP + v] = a2;
           sr[2 * NBP + v] = a3;
@@ -458,7 +474,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         double a1[N1], a2[N1], a3[N1];
 #pragma unroll
         for (int m = 0; m < N1; ++m) {
-          const int v = vix(ta, m, tb);
+          const int v = yidx[m];
           a1[m] = sr[v];
           a2[m] = sr[NBP + v];
           a3[m] = sr[2 * NBP + v];
@@ -476,7 +492,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
           }
           if (a == 0) b2 -= yl;
           if (a == N1 - 1) b2 -= yh;
-          const int v = vix(ta, a, tb);
+          const int v = yidx[a];
           su[v] = b1;
           sff[v] = b2;
         }
@@ -501,7 +517,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         double b1[N1], b23[N1];
 #pragma unroll
         for (int m = 0; m < N1; ++m) {
-          const int v = vix(m, ta, tb);
+          const int v = ridx[m];
           b1[m] = su[v];
           b23[m] = sff[v];
         }
@@ -620,6 +636,13 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
   const int e = blockIdx.x * EPB + slot;
   const bool active = slot < EPB && e < P.ne;
   const int i = lt % N1, j = ND == 3 ? lt / N1 : 0;
+  // this thread's M1 rows (i for the first in-face index, j for the second)
+  double Mi[N1], Mj[N1];
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    Mi[m] = P.m1[i * N1 + m];
+    Mj[m] = P.m1[j * N1 + m];
+  }
   int mask = 0;
   if (active) {
 #pragma unroll
@@ -660,8 +683,8 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
         for (int bb = 0; bb < N1; ++bb) {
           double r = 0.0;
 #pragma unroll
-          for (int aa = 0; aa < N1; ++aa) r = fma(P.m1[i * N1 + aa], sv[slot][lf][aa + N1 * bb][c], r);
-          s_ = fma(P.m1[j * N1 + bb], r, s_);
+          for (int aa = 0; aa < N1; ++aa) r = fma(Mi[aa], sv[slot][lf][aa + N1 * bb][c], r);
+          s_ = fma(Mj[bb], r, s_);
         }
         acc[side ? N1 - 1 : 0] += s_;
       }
@@ -671,13 +694,13 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
         const int lf = q < 2 ? 4 + q : 2 + (q - 2);
         const bool onface = q < 2 ? (i == (q ? N1 - 1 : 0)) : (j == (q == 3 ? N1 - 1 : 0));
         if (!(mask & (1 << lf)) || !onface) continue;
-        const int row = q < 2 ? j : i;          // in-face coordinate owned by the thread
         double w[N1];                           // w[bb] = sum_aa M[row][aa] sv[aa + N1 bb]
 #pragma unroll
         for (int bb = 0; bb < N1; ++bb) {
           double r = 0.0;
 #pragma unroll
-          for (int aa = 0; aa < N1; ++aa) r = fma(P.m1[row * N1 + aa], sv[slot][lf][aa + N1 * bb][c], r);
+          for (int aa = 0; aa < N1; ++aa)
+            r = fma(q < 2 ? Mj[aa] : Mi[aa], sv[slot][lf][aa + N1 * bb][c], r);
           w[bb] = r;
         }
 #pragma unroll
@@ -696,7 +719,7 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
         if (!(mask & (1 << lf))) continue;
         double s_ = 0.0;
 #pragma unroll
-        for (int aa = 0; aa < N1; ++aa) s_ = fma(P.m1[i * N1 + aa], sv[slot][lf][aa][c], s_);
+        for (int aa = 0; aa < N1; ++aa) s_ = fma(Mi[aa], sv[slot][lf][aa][c], s_);
         acc[side ? N1 - 1 : 0] += s_;
       }
 #pragma unroll
