@@ -85,6 +85,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   P.trace_centered = t->trace_centered;
   P.grad_centered = t->grad_centered;
   P.flux_uses_u = t->flux_uses_u;
+  P.n_maps = t->n_maps;
   P.geo = h->geo; P.fnbr = h->fnbr; P.finfo = h->finfo; P.ftau = h->ftau;
   P.nmap = h->nmap; P.bad = h->bad; P.frec = h->frec;
   const int n1 = t->n1;

@@ -30,9 +30,7 @@ namespace ldg {
 namespace {
 
 constexpr int kFBlock = 128;
-#ifndef LDG_P1_MINBLOCKS
-#define LDG_P1_MINBLOCKS 1
-#endif
+
 constexpr int kFSmemDoubles = 6144;   // 48 KB static
 
 template <int N1, int ND, int NCU>
@@ -105,7 +103,8 @@ struct __align__(16) FaceRec {
 
 template <int N1>
 __device__ __forceinline__ int swz(int i, int j, int k) {
-  int a = i + k, b = j + k;
+  if ((N1 & (N1 - 1)) == 0) return (i ^ k) + N1 * (j ^ k) + N1 * N1 * k;   // XOR swizzle
+  int a = i + k, b = j + k;                                                  // rotation
   a -= a >= N1 ? N1 : 0;
   b -= b >= N1 ? N1 : 0;
   return a + N1 * b + N1 * N1 * k;
@@ -130,10 +129,16 @@ struct P1Smem {
   static constexpr int EPB_T = (kFBlock / TPE) > 0 ? (kFBlock / TPE) : 1;
   static constexpr int EPB_S = kFSmemDoubles / PER > 0 ? kFSmemDoubles / PER : 1;
   static constexpr int EPB = EPB_T < EPB_S ? EPB_T : EPB_S;
+  // blocks per SM the shared memory allows; registers are capped to match
+  static constexpr int SMEM_BLOCKS = (227 * 1024) / (EPB * PER * 8 + 1024);
+  // (only where the register budget fits without spills: hex, ncu = 1, p <= 3)
+  static constexpr int MINB = (ND == 3 && NCU == 1 && N1 <= 4)
+                                  ? (SMEM_BLOCKS < 1 ? 1 : (SMEM_BLOCKS > 8 ? 8 : SMEM_BLOCKS))
+                                  : 1;
 };
 
 template <int N1, int ND, int NCU, bool TANGENT>
-__global__ void __launch_bounds__(kFBlock, LDG_P1_MINBLOCKS)
+__global__ void __launch_bounds__(kFBlock, P1Smem<N1, ND, NCU>::MINB)
 fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
              const double* __restrict__ u, const double* __restrict__ gproj,
              const double* __restrict__ bsrc, double* __restrict__ R,
@@ -147,6 +152,11 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   __shared__ __align__(16) double s_fh[EPB][S::FACEV];  // sJ f^ (own share)
   __shared__ __align__(16) double s_f[EPB][S::SF];      // face F^q; later B23 plane
   __shared__ double s_c[EPB][NC];
+  constexpr int kMaxMaps = 16;
+  __shared__ int s_map[kMaxMaps * NF];
+  const bool map_in_smem = P.n_maps <= kMaxMaps;
+  if (map_in_smem)
+    for (int x = threadIdx.x; x < P.n_maps * NF; x += blockDim.x) s_map[x] = __ldg(P.nmap + x);
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
   const int e = blockIdx.x * EPB + slot;
   const bool active = slot < EPB && e < P.ne;
@@ -162,20 +172,9 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     return ND == 3 ? swz<N1>(a, b, k) : a + N1 * k;
   };
   auto fix = [](int lf, int t, int c) { return (lf * NF + t) * NCU + c; };
-  // per-thread shared-plane offsets of the three pencils and the face nodes,
-  // computed once (integer work stays out of the contraction loops)
-  int cidx[N1], ridx[N1], yidx[N1], fvs[NFACE];
-#pragma unroll
-  for (int k = 0; k < N1; ++k) {
-    cidx[k] = vix(i, j, k);
-    ridx[k] = ND == 3 ? vix(k, ta, tb) : k + N1 * ta;
-    yidx[k] = ND == 3 ? vix(ta, k, tb) : 0;
-  }
-#pragma unroll
-  for (int lf = 0; lf < NFACE; ++lf) {
-    const int vn = fvol<N1, ND>(lf, lt);
-    fvs[lf] = ND == 3 ? swz<N1>(vn % N1, (vn / N1) % N1, vn / (N1 * N1)) : vn;
-  }
+  auto cidx = [&](int k) { return vix(i, j, k); };
+  auto ridx = [&](int m) { return ND == 3 ? vix(m, ta, tb) : m + N1 * ta; };
+  auto yidx = [&](int m) { return ND == 3 ? vix(ta, m, tb) : 0; };
 
   // ---- A: u column, geometry, face records, C coefficients
   double uc[NCU][N1];
@@ -189,7 +188,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
         uc[c][k] = __ldg(ue + node * NCU + c);
-        su[c * NBP + cidx[k]] = uc[c][k];
+        su[c * NBP + cidx(k)] = uc[c][k];
       }
     }
     const double* g = P.geo + (size_t)e * (1 + ND * ND);
@@ -231,15 +230,39 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   __syncthreads();
 
   // ---- B: face node lt of every face: jumps and the u part of sJ f^
-  double gl[NCU][N1];       // d/dk of the column (registers)
+  // all neighbour / boundary-data gathers are issued first (one latency)
+  double ext[NFACE][NCU];
   if (active) {
 #pragma unroll
     for (int lf = 0; lf < NFACE; ++lf) {
       const int info = fr[lf].info, nbr = fr[lf].nbr;
       const int kind = info & LDG_FACE_KIND_MASK;
+      const bool right = info & LDG_FACE_SIDE_RIGHT;
+      const bool sw = info & LDG_FACE_SWITCH;
+      const double* src = nullptr;
+      if (kind == LDG_FACE_INTERIOR) {
+        if (P.trace_centered || (sw == right) || !sw) {
+          const int mid = info >> LDG_FACE_MAP_SHIFT;
+          const int nn = map_in_smem ? s_map[mid * NF + lt] : __ldg(P.nmap + mid * NF + lt);
+          src = u + ((size_t)nbr * NB + nn) * NCU;
+        }
+      } else if (!TANGENT && gproj) {
+        src = gproj + ((size_t)nbr * NF + lt) * NCU;
+      }
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) ext[lf][c] = src ? __ldg(src + c) : 0.0;
+    }
+  }
+  double gl[NCU][N1];       // d/dk of the column (registers)
+  if (active) {
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf) {
+      const int info = fr[lf].info;
+      const int kind = info & LDG_FACE_KIND_MASK;
       const int ax = face_axis(ND, lf);
       const double sgn = face_side(ND, lf) ? 1.0 : -1.0;
-      const int vs = fvs[lf];
+      const int vn_ = fvol<N1, ND>(lf, lt);
+      const int vs = ND == 3 ? swz<N1>(vn_ % N1, (vn_ / N1) % N1, vn_ / (N1 * N1)) : vn_;
       double len2 = 0.0;
 #pragma unroll
       for (int d = 0; d < ND; ++d) len2 = fma(ij[d][ax], ij[d][ax], len2);
@@ -252,14 +275,9 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         const bool right = info & LDG_FACE_SIDE_RIGHT;
         const bool sw = info & LDG_FACE_SWITCH;
         double un[NCU];
-        if (P.trace_centered || (sw == right) || !sw) {
-          const int nn = __ldg(P.nmap + (info >> LDG_FACE_MAP_SHIFT) * NF + lt);
+        const bool got = P.trace_centered || (sw == right) || !sw;
 #pragma unroll
-          for (int c = 0; c < NCU; ++c) un[c] = __ldg(u + ((size_t)nbr * NB + nn) * NCU + c);
-        } else {
-#pragma unroll
-          for (int c = 0; c < NCU; ++c) un[c] = uo[c];
-        }
+        for (int c = 0; c < NCU; ++c) un[c] = got ? ext[lf][c] : uo[c];
 #pragma unroll
         for (int c = 0; c < NCU; ++c) {
           const double ul = right ? un[c] : uo[c], ur = right ? uo[c] : un[c];
@@ -270,7 +288,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       } else if (kind == LDG_FACE_DIRICHLET) {
 #pragma unroll
         for (int c = 0; c < NCU; ++c) {
-          uh[c] = (!TANGENT && gproj) ? __ldg(gproj + ((size_t)nbr * NF + lt) * NCU + c) : 0.0;
+          uh[c] = ext[lf][c];
           jmp[c] = uo[c] - uh[c];
           fh[c] = sjac * tau * jmp[c];
         }
@@ -279,8 +297,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         for (int c = 0; c < NCU; ++c) {
           uh[c] = uo[c];
           jmp[c] = 0.0;
-          fh[c] = (!TANGENT && gproj) ? sjac * __ldg(gproj + ((size_t)nbr * NF + lt) * NCU + c)
-                                      : 0.0;
+          fh[c] = sjac * ext[lf][c];
         }
       }
       if (P.flux_uses_u && kind != LDG_FACE_NEUMANN) {
@@ -318,7 +335,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     for (int c = 0; c < NCU; ++c) {
       double row[N1];
 #pragma unroll
-      for (int m = 0; m < N1; ++m) row[m] = su[c * NBP + ridx[m]];
+      for (int m = 0; m < N1; ++m) row[m] = su[c * NBP + ridx(m)];
       const int t = ND == 3 ? ta + N1 * tb : ta;
       const double jl = sj[fix(XLO, t, c)], jh = sj[fix(XHI, t, c)];
 #pragma unroll
@@ -326,19 +343,19 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         double v = 0.0;
 #pragma unroll
         for (int m = 0; m < N1; ++m) v = fma(P.d1[a * N1 + m], row[m], v);
-        sr[c * NBP + ridx[a]] = -v - P.clo[a] * jl + P.chi[a] * jh;
+        sr[c * NBP + ridx(a)] = -v - P.clo[a] * jl + P.chi[a] * jh;
       }
       if (ND == 3) {
         double col[N1];
 #pragma unroll
-        for (int m = 0; m < N1; ++m) col[m] = su[c * NBP + yidx[m]];
+        for (int m = 0; m < N1; ++m) col[m] = su[c * NBP + yidx(m)];
         const double yl = sj[fix(2, ta + N1 * tb, c)], yh = sj[fix(3, ta + N1 * tb, c)];
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
           double v = 0.0;
 #pragma unroll
           for (int m = 0; m < N1; ++m) v = fma(P.d1[a * N1 + m], col[m], v);
-          sr[(NCU + c) * NBP + yidx[a]] = -v - P.clo[a] * yl + P.chi[a] * yh;
+          sr[(NCU + c) * NBP + yidx(a)] = -v - P.clo[a] * yl + P.chi[a] * yh;
         }
       }
     }
@@ -360,8 +377,8 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       double h[NCU][ND];
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
-        h[c][0] = sr[c * NBP + cidx[k]];
-        if (ND == 3) h[c][1] = sr[(NCU + c) * NBP + cidx[k]];
+        h[c][0] = sr[c * NBP + cidx(k)];
+        if (ND == 3) h[c][1] = sr[(NCU + c) * NBP + cidx(k)];
         h[c][ND - 1] = -gl[c][k] - P.clo[k] * zl[c] + P.chi[k] * zh[c];
       }
 #pragma unroll
@@ -447,7 +464,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
           }
           if (k == 0) a3 -= sfh[fix(0, i + N1 * j, c)];
           if (k == N1 - 1) a3 -= sfh[fix(1, i + N1 * j, c)];
-          const int v = cidx[k];
+          const int v = cidx(k);
           sr[v] = a1;
           sr[NBP + v] = a2;
           sr[2 * NBP + v] = a3;
@@ -474,7 +491,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         double a1[N1], a2[N1], a3[N1];
 #pragma unroll
         for (int m = 0; m < N1; ++m) {
-          const int v = yidx[m];
+          const int v = yidx(m);
           a1[m] = sr[v];
           a2[m] = sr[NBP + v];
           a3[m] = sr[2 * NBP + v];
@@ -492,7 +509,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
           }
           if (a == 0) b2 -= yl;
           if (a == N1 - 1) b2 -= yh;
-          const int v = yidx[a];
+          const int v = yidx(a);
           su[v] = b1;
           sff[v] = b2;
         }
@@ -517,7 +534,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         double b1[N1], b23[N1];
 #pragma unroll
         for (int m = 0; m < N1; ++m) {
-          const int v = ridx[m];
+          const int v = ridx(m);
           b1[m] = su[v];
           b23[m] = sff[v];
         }

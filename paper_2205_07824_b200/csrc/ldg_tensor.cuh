@@ -12,7 +12,7 @@ namespace ldg {
 struct TensorParams {
   int ne, nd, n1, ncu;
   int trace_centered, grad_centered, flux_uses_u;
-  int pad_;
+  int n_maps;
   const double* geo;      // (ne, 1+nd*nd)
   const int32_t* fnbr;    // (ne, 2nd)
   const int32_t* finfo;   // (ne, 2nd)
