@@ -47,6 +47,13 @@ extern "C" {
 #define LDG_FACE_SIDE_RIGHT 4   /* this element is the right side of the face */
 #define LDG_FACE_SWITCH 8       /* face switch bit (disc.py:287) */
 #define LDG_FACE_MAP_SHIFT 8    /* bits 8..23: neighbour node map id */
+/* bits 4..6: the neighbour's local face.  Bits 24..28 are derived flags
+ * ldg_create adds from the trace rules (callers pass them as zero). */
+#define LDG_FL_UNBR (1 << 24)      /* u^ or the penalty reads the neighbour */
+#define LDG_FL_EXPORT (1 << 25)    /* neighbour takes (part of) q^ from this side */
+#define LDG_FL_QOWN (1 << 26)      /* q^ = this side's q */
+#define LDG_FL_QHALF (1 << 27)     /* q^ centered: half from each side */
+#define LDG_FL_COMPLETE (1 << 28)  /* pass 2 adds the neighbour share */
 
 /* Host-side description of a tensor-product (quad/hex) kind-D system with a
  * flux that is linear in (u, q) with constant coefficients.  Pointers are

@@ -2,6 +2,7 @@
 // See include/ldgb200.h for the reference interface each one replaces.
 
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -39,6 +40,8 @@ struct LdgHandle {
   double* ftau = nullptr;
   int32_t* nmap = nullptr;
   double* frec = nullptr;
+  double* kco = nullptr;
+  int kstride = 0;
   unsigned long long* bad = nullptr;
 };
 
@@ -64,14 +67,68 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   rc |= upload(&h->ftau, t->ftau, ne * nf, "ftau");
   rc |= upload(&h->nmap, t->nmap, (size_t)t->n_maps * nfn, "nmap");
   {
-    // packed 16-byte face records {double tau; int32 nbr; int32 info}
+    // Derived per-element / per-face data of the fused kernels (ldg_fused.cu):
+    //  * coefficient block [C | Cu | sJ(axis)] with
+    //    C[c][r][k][s] = detJ sum_{d,e} invjt[d][r] aq[c][d][k][e] invjt[e][s],
+    //    Cu[c][r][k]   = detJ sum_d invjt[d][r] au[c][d][k],
+    //    sJ(axis)      = detJ |invjt[:, axis]|  (|t1 x t2| of an affine face);
+    //  * face records {sJ*tau, nbr, info | flags}.
+    const int nd = t->nd, ncu = t->ncu;
+    const int cq = ncu * nd * ncu * nd, cu = ncu * nd * ncu;
+    const int kst = ((cq + cu + nd) + 1) & ~1;
+    std::vector<double> kco((size_t)ne * kst, 0.0);
     std::vector<double> rec(ne * nf * 2);
-    for (size_t x = 0; x < ne * nf; ++x) {
-      rec[2 * x] = t->ftau[x];
-      int32_t pair[2] = {t->fnbr[x], t->finfo[x]};
-      memcpy(&rec[2 * x + 1], pair, sizeof(pair));
+    auto axis_of = [&](int lf) {
+      return nd == 3 ? (lf < 2 ? 2 : (lf < 4 ? 1 : 0)) : ((lf == 0 || lf == 2) ? 1 : 0);
+    };
+    for (size_t e = 0; e < ne; ++e) {
+      const double* g = t->geo + e * (1 + nd * nd);
+      const double dj = g[0];
+      const double* ij = g + 1;                   // ij[d*nd + r] = invjt[d][r]
+      double* kb = kco.data() + e * kst;
+      for (int c = 0; c < ncu; ++c)
+        for (int r = 0; r < nd; ++r)
+          for (int k = 0; k < ncu; ++k)
+            for (int s2 = 0; s2 < nd; ++s2) {
+              double v = 0.0;
+              for (int d = 0; d < nd; ++d)
+                for (int ee = 0; ee < nd; ++ee)
+                  v += ij[d * nd + r] * t->aq[((c * 3 + d) * LDG_MAX_NCU + k) * 3 + ee] *
+                       ij[ee * nd + s2];
+              kb[((c * nd + r) * ncu + k) * nd + s2] = dj * v;
+            }
+      for (int c = 0; c < ncu; ++c)
+        for (int r = 0; r < nd; ++r)
+          for (int k = 0; k < ncu; ++k) {
+            double v = 0.0;
+            for (int d = 0; d < nd; ++d) v += ij[d * nd + r] * t->au[(c * 3 + d) * LDG_MAX_NCU + k];
+            kb[cq + (c * nd + r) * ncu + k] = dj * v;
+          }
+      for (int a = 0; a < nd; ++a) {
+        double l2 = 0.0;
+        for (int d = 0; d < nd; ++d) l2 += ij[d * nd + a] * ij[d * nd + a];
+        kb[cq + cu + a] = dj * sqrt(l2);
+      }
+      for (size_t lf = 0; lf < nf; ++lf) {
+        const size_t x = e * nf + lf;
+        int32_t info = t->finfo[x] & 0x00ffffff;
+        if ((info & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR) {
+          const bool right = info & LDG_FACE_SIDE_RIGHT, sw = info & LDG_FACE_SWITCH;
+          const bool tc = t->trace_centered, gc = t->grad_centered;
+          if (tc || (sw == right) || !sw) info |= LDG_FL_UNBR;
+          if (gc || (sw == right)) info |= LDG_FL_EXPORT;
+          if (!gc && (sw == right)) info |= LDG_FL_QOWN;
+          if (gc) info |= LDG_FL_QHALF;
+          if (gc || (sw != right)) info |= LDG_FL_COMPLETE;
+        }
+        rec[2 * x] = t->ftau[x] * kb[cq + cu + axis_of((int)lf)];
+        int32_t pair[2] = {t->fnbr[x], info};
+        memcpy(&rec[2 * x + 1], pair, sizeof(pair));
+      }
     }
     rc |= upload(&h->frec, rec.data(), rec.size(), "frec");
+    rc |= upload(&h->kco, kco.data(), kco.size(), "kco");
+    h->kstride = kst;
   }
   cudaError_t e = cudaMalloc(&h->bad, sizeof(unsigned long long));
   if (e != cudaSuccess) rc |= fail(3, "bad flag", e);
@@ -87,7 +144,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   P.flux_uses_u = t->flux_uses_u;
   P.n_maps = t->n_maps;
   P.geo = h->geo; P.fnbr = h->fnbr; P.finfo = h->finfo; P.ftau = h->ftau;
-  P.nmap = h->nmap; P.bad = h->bad; P.frec = h->frec;
+  P.nmap = h->nmap; P.bad = h->bad; P.frec = h->frec; P.kco = h->kco; P.kstride = h->kstride;
   const int n1 = t->n1;
   // tables arrive with row stride n1 packed at the front of each array
   memcpy(P.d1, t->d1, sizeof(P.d1));
@@ -125,7 +182,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
 int ldg_destroy(LdgHandle* h) {
   if (!h) return 0;
   cudaFree(h->geo); cudaFree(h->fnbr); cudaFree(h->finfo); cudaFree(h->ftau);
-  cudaFree(h->nmap); cudaFree(h->frec); cudaFree(h->bad);
+  cudaFree(h->nmap); cudaFree(h->frec); cudaFree(h->kco); cudaFree(h->bad);
   delete h;
   return 0;
 }

@@ -124,13 +124,16 @@ struct P1Smem {
   static constexpr int SJ = FACEV > EXT ? FACEV : EXT;       // jumps, later pencils
   static constexpr int SF = FACEV > NBP ? FACEV : NBP;       // face F^q, later B23
   static constexpr int SU = NCU * NBP > NBP ? NCU * NBP : NBP;
-  static constexpr int PER = SU + R1 + SJ + FACEV + SF + NC;
+  static constexpr int PER = SU + R1 + SJ + FACEV + SF + NC + ND;
+  static constexpr int MAXMAPS = NF <= 16 ? 16 : 8;          // node maps cached per block
   static constexpr int TPE = NF;
   static constexpr int EPB_T = (kFBlock / TPE) > 0 ? (kFBlock / TPE) : 1;
-  static constexpr int EPB_S = kFSmemDoubles / PER > 0 ? kFSmemDoubles / PER : 1;
+  static constexpr int EPB_S = (kFSmemDoubles - (NF <= 16 ? 16 : 8) * NF / 2) / PER > 0
+                                  ? (kFSmemDoubles - (NF <= 16 ? 16 : 8) * NF / 2) / PER : 1;
   static constexpr int EPB = EPB_T < EPB_S ? EPB_T : EPB_S;
   // blocks per SM the shared memory allows; registers are capped to match
-  static constexpr int SMEM_BLOCKS = (227 * 1024) / (EPB * PER * 8 + 1024);
+  static constexpr int SMEM_BLOCKS = (227 * 1024) / (EPB * PER * 8 + MAXMAPS * NF * 4 + 1024);
+  static constexpr int EPB_S2 = (kFSmemDoubles - MAXMAPS * NF / 2) / PER;
   // (only where the register budget fits without spills: hex, ncu = 1, p <= 3)
   static constexpr int MINB = (ND == 3 && NCU == 1 && N1 <= 4)
                                   ? (SMEM_BLOCKS < 1 ? 1 : (SMEM_BLOCKS > 8 ? 8 : SMEM_BLOCKS))
@@ -151,9 +154,10 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   __shared__ __align__(16) double s_j[EPB][S::SJ];      // jumps; later face-slab pencils
   __shared__ __align__(16) double s_fh[EPB][S::FACEV];  // sJ f^ (own share)
   __shared__ __align__(16) double s_f[EPB][S::SF];      // face F^q; later B23 plane
-  __shared__ double s_c[EPB][NC];
-  constexpr int kMaxMaps = 16;
+  constexpr int kMaxMaps = S::MAXMAPS;
   __shared__ int s_map[kMaxMaps * NF];
+  constexpr int KSZ = NC + ND;             // C, Cu, sJ per face axis
+  __shared__ double s_k[EPB][KSZ];
   const bool map_in_smem = P.n_maps <= kMaxMaps;
   if (map_in_smem)
     for (int x = threadIdx.x; x < P.n_maps * NF; x += blockDim.x) s_map[x] = __ldg(P.nmap + x);
@@ -176,9 +180,10 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   auto ridx = [&](int m) { return ND == 3 ? vix(m, ta, tb) : m + N1 * ta; };
   auto yidx = [&](int m) { return ND == 3 ? vix(ta, m, tb) : 0; };
 
-  // ---- A: u column, geometry, face records, C coefficients
+  // ---- A: u column, element coefficient block, face records (all loads
+  // issued before any use)
   double uc[NCU][N1];
-  double detj = 1.0, ij[ND][ND];
+  const double* kc = s_k[slot];            // element coefficient block (shared)
   FaceRec fr[NFACE];
   if (active) {
     const double* ue = u + (size_t)e * NB * NCU;
@@ -186,46 +191,22 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     for (int k = 0; k < N1; ++k) {
       const int node = ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k;
 #pragma unroll
-      for (int c = 0; c < NCU; ++c) {
-        uc[c][k] = __ldg(ue + node * NCU + c);
-        su[c * NBP + cidx(k)] = uc[c][k];
-      }
+      for (int c = 0; c < NCU; ++c) uc[c][k] = __ldg(ue + node * NCU + c);
     }
-    const double* g = P.geo + (size_t)e * (1 + ND * ND);
-    detj = __ldg(g);
-#pragma unroll
-    for (int d = 0; d < ND; ++d)
-#pragma unroll
-      for (int r = 0; r < ND; ++r) ij[d][r] = __ldg(g + 1 + d * ND + r);
+    const double* kb = P.kco + (size_t)e * P.kstride;
+    for (int x = lt; x < KSZ; x += TPE) s_k[slot][x] = __ldg(kb + x);
 #pragma unroll
     for (int lf = 0; lf < NFACE; ++lf) {
       const double2 v = __ldg(reinterpret_cast<const double2*>(frec + (size_t)e * NFACE + lf));
-      fr[lf].tau = v.x;
+      fr[lf].tau = v.x;                    // sJ * tau on this face
       const int2 w = *reinterpret_cast<const int2*>(&v.y);
       fr[lf].nbr = w.x;
       fr[lf].info = w.y;
     }
-    const double* gij = g + 1;
-    for (int x = lt; x < NC; x += TPE) {
-      double v = 0.0;
-      if (x < CQ) {
-        const int s_ = x % ND, k_ = (x / ND) % NCU, r_ = (x / (ND * NCU)) % ND,
-                  c_ = x / (ND * NCU * ND);
 #pragma unroll
-        for (int d = 0; d < ND; ++d)
+    for (int k = 0; k < N1; ++k)
 #pragma unroll
-          for (int ee = 0; ee < ND; ++ee)
-            v = fma(__ldg(gij + d * ND + r_) * P.aq[((c_ * 3 + d) * LDG_MAX_NCU + k_) * 3 + ee],
-                    __ldg(gij + ee * ND + s_), v);
-      } else {
-        const int y = x - CQ;
-        const int k_ = y % NCU, r_ = (y / NCU) % ND, c_ = y / (NCU * ND);
-#pragma unroll
-        for (int d = 0; d < ND; ++d)
-          v = fma(__ldg(gij + d * ND + r_), P.au[(c_ * 3 + d) * LDG_MAX_NCU + k_], v);
-      }
-      s_c[slot][x] = detj * v;
-    }
+      for (int c = 0; c < NCU; ++c) su[c * NBP + cidx(k)] = uc[c][k];
   }
   __syncthreads();
 
@@ -241,8 +222,8 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       const bool sw = info & LDG_FACE_SWITCH;
       const double* src = nullptr;
       if (kind == LDG_FACE_INTERIOR) {
-        if (P.trace_centered || (sw == right) || !sw) {
-          const int mid = info >> LDG_FACE_MAP_SHIFT;
+        if (info & LDG_FL_UNBR) {
+          const int mid = (info >> LDG_FACE_MAP_SHIFT) & 0xffff;
           const int nn = map_in_smem ? s_map[mid * NF + lt] : __ldg(P.nmap + mid * NF + lt);
           src = u + ((size_t)nbr * NB + nn) * NCU;
         }
@@ -263,11 +244,8 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       const double sgn = face_side(ND, lf) ? 1.0 : -1.0;
       const int vn_ = fvol<N1, ND>(lf, lt);
       const int vs = ND == 3 ? swz<N1>(vn_ % N1, (vn_ / N1) % N1, vn_ / (N1 * N1)) : vn_;
-      double len2 = 0.0;
-#pragma unroll
-      for (int d = 0; d < ND; ++d) len2 = fma(ij[d][ax], ij[d][ax], len2);
-      const double sjac = detj * sqrt(len2);
-      const double tau = fr[lf].tau;
+      const double sjac = kc[NC + ax];       // |t1 x t2| of the (affine) face
+      const double stau = fr[lf].tau;        // sJ * tau
       double uo[NCU], uh[NCU], fh[NCU], jmp[NCU];
 #pragma unroll
       for (int c = 0; c < NCU; ++c) uo[c] = su[c * NBP + vs];
@@ -275,7 +253,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         const bool right = info & LDG_FACE_SIDE_RIGHT;
         const bool sw = info & LDG_FACE_SWITCH;
         double un[NCU];
-        const bool got = P.trace_centered || (sw == right) || !sw;
+        const bool got = info & LDG_FL_UNBR;
 #pragma unroll
         for (int c = 0; c < NCU; ++c) un[c] = got ? ext[lf][c] : uo[c];
 #pragma unroll
@@ -283,14 +261,14 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
           const double ul = right ? un[c] : uo[c], ur = right ? uo[c] : un[c];
           uh[c] = P.trace_centered ? 0.5 * (ul + ur) : (sw ? ul : ur);
           jmp[c] = uo[c] - uh[c];
-          fh[c] = sjac * (right ? -tau : tau) * (ul - uh[c]);   // frozen tau (disc.py:694-698)
+          fh[c] = (right ? -stau : stau) * (ul - uh[c]);   // frozen tau (disc.py:694-698)
         }
       } else if (kind == LDG_FACE_DIRICHLET) {
 #pragma unroll
         for (int c = 0; c < NCU; ++c) {
           uh[c] = ext[lf][c];
           jmp[c] = uo[c] - uh[c];
-          fh[c] = sjac * tau * jmp[c];
+          fh[c] = stau * jmp[c];
         }
       } else {
 #pragma unroll
@@ -305,7 +283,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         for (int c = 0; c < NCU; ++c) {
           double a = 0.0;
 #pragma unroll
-          for (int kk = 0; kk < NCU; ++kk) a = fma(s_c[slot][CQ + (c * ND + ax) * NCU + kk], uh[kk], a);
+          for (int kk = 0; kk < NCU; ++kk) a = fma(kc[CQ + (c * ND + ax) * NCU + kk], uh[kk], a);
           fh[c] = fma(sgn, a, fh[c]);
         }
       }
@@ -365,6 +343,9 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   // ---- D: F = Cu u + C h at the column's nodes; F^q at face nodes
   double F[NCU][ND][N1];
   if (active) {
+    double cr[NC];
+#pragma unroll
+    for (int x = 0; x < NC; ++x) cr[x] = kc[x];
     constexpr int ZLO = ND == 3 ? 0 : 0, ZHI = ND == 3 ? 1 : 2;   // column-axis faces
     double zl[NCU], zh[NCU];
 #pragma unroll
@@ -390,12 +371,12 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
           for (int kk = 0; kk < NCU; ++kk)
 #pragma unroll
             for (int s_ = 0; s_ < ND; ++s_)
-              fq = fma(s_c[slot][((c * ND + r) * NCU + kk) * ND + s_], h[kk][s_], fq);
+              fq = fma(cr[((c * ND + r) * NCU + kk) * ND + s_], h[kk][s_], fq);
           double fu = 0.0;
           if (P.flux_uses_u) {
 #pragma unroll
             for (int kk = 0; kk < NCU; ++kk)
-              fu = fma(s_c[slot][CQ + (c * ND + r) * NCU + kk], uc[kk][k], fu);
+              fu = fma(cr[CQ + (c * ND + r) * NCU + kk], uc[kk][k], fu);
           }
           F[c][r][k] = fq + fu;
           // F^q of the face-normal component at this column's face nodes
@@ -424,15 +405,10 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       const int info = fr[lf].info;
       const int kind = info & LDG_FACE_KIND_MASK;
       if (kind == LDG_FACE_NEUMANN) continue;
-      double w_own = 1.0;
-      bool exp_ = false;
-      if (kind == LDG_FACE_INTERIOR) {
-        const bool right = info & LDG_FACE_SIDE_RIGHT;
-        const bool sw = info & LDG_FACE_SWITCH;
-        const bool mine = sw == right;
-        w_own = P.grad_centered ? 0.5 : (mine ? 1.0 : 0.0);
-        exp_ = P.grad_centered || mine;
-      }
+      // flags precomputed at ldg_create (q^ = own / half / neighbour, export)
+      const bool exp_ = info & LDG_FL_EXPORT;
+      const double w_own = kind != LDG_FACE_INTERIOR ? 1.0
+                           : ((info & LDG_FL_QOWN) ? 1.0 : ((info & LDG_FL_QHALF) ? 0.5 : 0.0));
       if (w_own == 0.0 && !exp_) continue;
       const double sgn = face_side(ND, lf) ? 1.0 : -1.0;
 #pragma unroll
@@ -660,21 +636,43 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
     Mi[m] = P.m1[i * N1 + m];
     Mj[m] = P.m1[j * N1 + m];
   }
-  int mask = 0;
+  constexpr int kMaxMaps = 16;
+  __shared__ int s_map[kMaxMaps * NF];
+  const bool map_in_smem = P.n_maps <= kMaxMaps;
+  if (map_in_smem)
+    for (int x = threadIdx.x; x < P.n_maps * NF; x += blockDim.x) s_map[x] = __ldg(P.nmap + x);
+  // R column loads are independent of the exports: issue them first
+  double rcol[NCU][N1];
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c)
+        rcol[c][k] = R[((size_t)e * NB + (ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k)) * NCU + c];
+  }
+  int info_[NFACE], nbr_[NFACE];
   if (active) {
 #pragma unroll
     for (int lf = 0; lf < NFACE; ++lf) {
       const double2 v = __ldg(reinterpret_cast<const double2*>(frec + (size_t)e * NFACE + lf));
       const int2 w = *reinterpret_cast<const int2*>(&v.y);
-      const int info = w.y;
-      if ((info & LDG_FACE_KIND_MASK) != LDG_FACE_INTERIOR) continue;
-      const bool right = info & LDG_FACE_SIDE_RIGHT;
-      const bool sw = info & LDG_FACE_SWITCH;
-      if (!(P.grad_centered || (sw != right))) continue;
+      nbr_[lf] = w.x;
+      info_[lf] = w.y;
+    }
+  }
+  __syncthreads();
+  int mask = 0;
+  if (active) {
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf) {
+      const int info = info_[lf];
+      if (!(info & LDG_FL_COMPLETE)) continue;
       mask |= 1 << lf;
       const double wgt = P.grad_centered ? -0.5 : -1.0;
       const int nlf = (info >> 4) & 7;
-      const int nv = __ldg(P.nmap + (info >> LDG_FACE_MAP_SHIFT) * NF + lt);
+      const int mid = (info >> LDG_FACE_MAP_SHIFT) & 0xffff;
+      const int nv = map_in_smem ? s_map[mid * NF + lt] : __ldg(P.nmap + mid * NF + lt);
+      const int2 w = make_int2(nbr_[lf], info);
       const int tn = vol_to_face<N1, ND>(face_axis(ND, nlf), nv);
 #pragma unroll
       for (int c = 0; c < NCU; ++c)
@@ -755,7 +753,7 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
       const int node = ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k;
-      const double out = Re[node * NCU + c] + acc[k];
+      const double out = rcol[c][k] + acc[k];
       bad_if(P, e, out);
       Re[node * NCU + c] = out;
     }

@@ -18,7 +18,10 @@ struct TensorParams {
   const int32_t* finfo;   // (ne, 2nd)
   const double* ftau;     // (ne, 2nd)
   const int32_t* nmap;    // (n_maps, n1^(nd-1))
-  const void* frec;       // (ne, 2nd) packed {tau, nbr, info} records (16 B)
+  const void* frec;       // (ne, 2nd) packed {sJ*tau, nbr, info|flags} records (16 B)
+  const double* kco;      // (ne, kstride): C, Cu, sJ per face axis (fused kernels)
+  int kstride;
+  int pad2_;
   unsigned long long* bad;  // first non-finite element (atomicMin)
   double d1[LDG_MAX_N1 * LDG_MAX_N1];
   double m1[LDG_MAX_N1 * LDG_MAX_N1];

@@ -1,0 +1,198 @@
+"""Element-partitioned multi-GPU layer.
+
+One process per GPU.  Each rank owns a contiguous range of global elements
+(x-slabs on the structured meshes, whose elements are numbered x-outermost,
+mesh.py:156-163); the global face tables are built once (bit-exact with the
+reference) and sliced, so connectivity, switch bits and gather indices of
+every partition are the global ones.  Per operator application two halo
+steps exchange ghost-element data over NCCL (gloo on CPU in the tests):
+
+  1. before pass 1: the state of the ghost elements (neighbours owned by
+     other ranks) -- the u^ / penalty gathers read their face nodes;
+  2. between pass 1 and pass 2: the ghost elements' face exports
+     X = sJ n.(Aq q), which carry the neighbour share of f(., q^).
+
+Krylov reductions are allreduced sums of per-rank partials
+(:class:`DistVecOps`).  Ranks are on one node: NCCL runs over NVLink 5 /
+NVSwitch.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .tables import DiscError
+
+
+def element_ranges(ne, nranks):
+    """Balanced contiguous element ranges [e0, e1) per rank."""
+    base, rem = divmod(ne, nranks)
+    starts = np.cumsum([0] + [base + (1 if r < rem else 0) for r in range(nranks)])
+    return [(int(starts[r]), int(starts[r + 1])) for r in range(nranks)]
+
+
+class PartitionPlan:
+    """Local numbering, sliced tables and halo lists of one rank."""
+
+    def __init__(self, tab, nranks, rank):
+        self.nranks, self.rank = nranks, rank
+        ne = tab.ne
+        self.ranges = element_ranges(ne, nranks)
+        e0, e1 = self.ranges[rank]
+        self.e0, self.e1 = e0, e1
+        self.ne_loc = e1 - e0
+        owner = np.zeros(ne, dtype=np.int64)
+        for r, (a, b) in enumerate(self.ranges):
+            owner[a:b] = r
+        self.owner = owner
+        fnbr = tab.fnbr[e0:e1].astype(np.int64)
+        finfo = tab.finfo[e0:e1]
+        interior = (finfo & 3) == 0
+        nbrs = np.where(interior, fnbr, -1)
+        ext = np.unique(nbrs[(nbrs >= 0) & ((nbrs < e0) | (nbrs >= e1))])
+        self.ghosts = ext                                 # global ids, sorted
+        self.n_ghost = ext.size
+        g2l = {int(g): self.ne_loc + k for k, g in enumerate(ext.tolist())}
+        loc = np.where(interior & (nbrs >= e0) & (nbrs < e1), nbrs - e0, -1)
+        ghost_mask = interior & ((nbrs < e0) | (nbrs >= e1))
+        if ghost_mask.any():
+            loc[ghost_mask] = np.searchsorted(ext, nbrs[ghost_mask]) + self.ne_loc
+        # boundary rows referenced by owned elements -> local rows
+        bmask = ~interior
+        brows = np.unique(fnbr[bmask]) if bmask.any() else np.zeros(0, np.int64)
+        self.brows = brows
+        if bmask.any():
+            loc[bmask] = np.searchsorted(brows, fnbr[bmask])
+        self.fnbr = loc.astype(np.int32)
+        self.finfo = finfo.copy()
+        self.ftau = tab.ftau[e0:e1].copy()
+        self.geo = tab.geo[e0:e1].copy()
+        del g2l
+        # halo lists: what I send to q = my owned elements adjacent to q's range
+        self.recv = {}
+        self.send = {}
+        for q in range(nranks):
+            if q == rank:
+                continue
+            mine = self.ghosts[owner[self.ghosts] == q]
+            if mine.size:
+                self.recv[q] = (np.searchsorted(self.ghosts, mine) + self.ne_loc).astype(np.int64)
+            adj = (owner[np.where(nbrs >= 0, nbrs, 0)] == q) & (nbrs >= 0)
+            rows = np.nonzero(adj.any(axis=1))[0]
+            if rows.size:
+                self.send[q] = rows.astype(np.int64)          # local owned rows, sorted
+        if np.any(self.fnbr < 0):
+            raise DiscError("partition left an unresolved neighbour")
+
+
+class LocalTables:
+    """TensorTables interface over one partition (rows sliced, neighbours
+    renumbered to [owned | ghosts])."""
+
+    def __init__(self, tab, plan):
+        self._g, self.plan = tab, plan
+        for k in ("nd", "n1", "ncu", "nf", "nfn", "p", "nmap", "d1", "m1", "s1", "clo", "chi",
+                  "m1inv", "au", "aq", "flux_uses_u", "mass_coef", "mass_const", "source_zero",
+                  "model", "master", "mesh", "topo", "bc_groups"):
+            setattr(self, k, getattr(tab, k))
+        e0, e1 = plan.e0, plan.e1
+        self.ne = plan.ne_loc
+        self.geo, self.fnbr, self.finfo, self.ftau = plan.geo, plan.fnbr, plan.finfo, plan.ftau
+        self.detj, self.invjt = tab.detj[e0:e1], tab.invjt[e0:e1]
+        self.J, self.x0 = tab.J[e0:e1], tab.x0[e0:e1]
+        self.elem_vol = tab.elem_vol[e0:e1]
+        self.switch = tab.switch          # global face bits (for reference)
+        self.fi_h, self.fb_h = tab.fi_h, tab.fb_h
+
+    def node_coords(self, elems=None, nodes=None):
+        e = np.arange(self.plan.e0, self.plan.e1) if elems is None else \
+            np.asarray(elems) + self.plan.e0
+        return self._g.node_coords(e, nodes)
+
+    def face_node_vol(self, lf):
+        return self._g.face_node_vol(lf)
+
+    def boundary_projection(self, t):
+        g = self._g.boundary_projection(t)
+        return g[self.plan.brows] if g.size else g
+
+    def source_load(self, t):
+        b = self._g.source_load(t)
+        return None if b is None else b[self.plan.e0:self.plan.e1]
+
+
+class HaloExchanger:
+    """Ghost-row exchange of an (n_owned + n_ghost, width) array with
+    torch.distributed point-to-point ops (NCCL on GPU, gloo on CPU)."""
+
+    def __init__(self, plan, group=None):
+        self.plan, self.group = plan, group
+
+    def exchange(self, arr):
+        import torch
+        import torch.distributed as dist
+        ops, recv_bufs = [], []
+        flat = arr.reshape(arr.shape[0], -1)
+        for q, rows in sorted(self.plan.send.items()):
+            idx = torch.as_tensor(rows, device=arr.device)
+            buf = flat.index_select(0, idx).contiguous()
+            ops.append(dist.P2POp(dist.isend, buf, q, group=self.group))
+        for q, rows in sorted(self.plan.recv.items()):
+            buf = torch.empty((rows.size, flat.shape[1]), dtype=arr.dtype, device=arr.device)
+            recv_bufs.append((rows, buf))
+            ops.append(dist.P2POp(dist.irecv, buf, q, group=self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        for rows, buf in recv_bufs:
+            flat.index_copy_(0, torch.as_tensor(rows, device=arr.device), buf)
+        return arr
+
+
+class DistVecOps:
+    """VecOps with every reduction allreduced over the process group (sum
+    of per-rank partials; norms from allreduced squares)."""
+
+    def __init__(self, base, group=None):
+        self.b, self.group = base, group
+
+    def _ar(self, t):
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def dot(self, x, y, out):
+        self.b.dot(x, y, out)
+        self._ar(out)
+
+    def nrm2(self, x, out):
+        self.b.dot(x, x, out)
+        self._ar(out)
+        out.sqrt_()
+
+    def norm(self, x):
+        out = x.new_zeros(1)
+        self.nrm2(x, out)
+        return float(out.item())
+
+    def axpy(self, *a, **k):
+        return self.b.axpy(*a, **k)
+
+    def div(self, *a, **k):
+        return self.b.div(*a, **k)
+
+    def mgs_step(self, vi, h_in, w, vnext, h_out):
+        self.b.mgs_step(vi, h_in, w, vnext, h_out)
+        if vnext is not None:
+            self._ar(h_out)
+
+    def cgs_dots(self, V, k, w, h):
+        self.b.cgs_dots(V, k, w, h)
+        self._ar(h[:k])
+
+    def cgs_update(self, V, k, h, w, nrm_out):
+        self.b.cgs_update(V, k, h, w, None)
+        self.nrm2(w, nrm_out)
+
+    def combine(self, *a, **k):
+        return self.b.combine(*a, **k)
