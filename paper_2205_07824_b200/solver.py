@@ -156,8 +156,10 @@ def vecops(device):
 
 
 def _as_device(v, device=None):
+    """Flat float64 tensor; torch tensors keep their device (the product
+    passes CUDA tensors), numpy arrays go to the GPU."""
     import torch
-    if isinstance(v, torch.Tensor) and v.is_cuda:
+    if isinstance(v, torch.Tensor):
         return v.reshape(-1).to(torch.float64).contiguous(), True
     dev = device or torch.device("cuda")
     return torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64).ravel(),
@@ -192,14 +194,15 @@ _WS = _Workspace()
 
 
 def gmres(op, rhs, precond=None, rel_tol=1e-8, restart=30, max_iter=200, x0=None,
-          orth="mgs"):
+          orth="mgs", ops=None):
     """Right-preconditioned restarted GMRES (solver.py:79-174) on device
-    vectors.  numpy rhs -> numpy x; CUDA tensor rhs -> CUDA tensor x."""
+    vectors.  numpy rhs -> numpy x; CUDA tensor rhs -> CUDA tensor x.
+    `ops` overrides the vector-kernel backend (e.g. parallel.DistVecOps)."""
     import torch
     b, on_dev = _as_device(rhs)
     n = b.numel()
     dev = b.device
-    ops = vecops(dev)
+    ops = ops or vecops(dev)
     if not (0.0 < rel_tol < 1.0):
         raise SolverError("gmres: rel_tol must be in (0, 1)")
     M = precond or IdentityPreconditioner()
@@ -355,14 +358,14 @@ def jacobian_vector(residual_fn, base, v, mode="fd", base_residual=None, tangent
 
 
 def newton_solve(residual_fn, x0, options=None, precond=None, tangent_fn=None,
-                 callback=None):
+                 callback=None, ops=None):
     """Inexact Newton with right-preconditioned GMRES (solver.py:220-283);
     x0 may be numpy (returns numpy) or a CUDA tensor."""
     import torch
     opts = options or NewtonOptions()
     x, on_dev = _as_device(x0)
     x = x.clone()
-    ops = vecops(x.device)
+    ops = ops or vecops(x.device)
     stats = SolveStats()
     R = residual_fn(x)
     rnorm = ops.norm(R)
@@ -380,7 +383,7 @@ def newton_solve(residual_fn, x0, options=None, precond=None, tangent_fn=None,
         eta = opts.forcing if opts.forcing is not None else min(0.1, np.sqrt(rnorm))
         eta = min(max(eta, 1e-14), 0.9)
         lin = gmres(op, -R, precond=M, rel_tol=eta, restart=opts.gmres_restart,
-                    max_iter=opts.gmres_max_iter, orth=opts.orth)
+                    max_iter=opts.gmres_max_iter, orth=opts.orth, ops=ops)
         stats.gmres_iters.append(lin.iterations)
         d = lin.x
         step, accepted = 1.0, False

@@ -27,10 +27,13 @@ def _apply1d(op, x, axis, nd, n1):
 
 
 def mixed(tab, u, gproj=None):
+    """u may carry ghost rows after the tab.ne owned rows (partitions)."""
     nd, n1, nfn = tab.nd, tab.n1, tab.nfn
-    ne, nb, ncu = u.shape
+    ne = tab.ne
+    _, nb, ncu = u.shape
     ij = tab.invjt
-    g = np.stack([_apply1d(tab.d1, u, r, nd, n1) for r in range(nd)], axis=-1)  # (e,a,c,r)
+    uo_all = u[:ne]
+    g = np.stack([_apply1d(tab.d1, uo_all, r, nd, n1) for r in range(nd)], axis=-1)
     q = -np.einsum("edr,eacr->eacd", ij, g)
     vol = _vol_nodes(tab)
     ax_side = _axis_side(tab)
@@ -38,13 +41,13 @@ def mixed(tab, u, gproj=None):
         info = tab.finfo[:, lf]
         nbr = tab.fnbr[:, lf]
         kind = info & 3
-        own = u[:, vol[lf], :]                                 # (e, t, c)
+        own = u[:ne, vol[lf], :]                               # (e, t, c)
         jump = np.zeros_like(own)
         it = kind == 0
         right = (info & 4) > 0
         sw = (info & 8) > 0
         cen = tab.model.numflux.trace == "centered"
-        own_hat = (~cen) & (sw != right)
+        own_hat = (not cen) & (sw != right)
         mid = info >> 8
         need = it & ~own_hat
         e_idx = np.nonzero(need)[0]
@@ -74,10 +77,11 @@ def mixed(tab, u, gproj=None):
 
 def flux(tab, u, q, tangent, gproj=None, bsrc=None, split=False):
     nd, n1 = tab.nd, tab.n1
-    ne, nb, ncu = u.shape
+    ne = tab.ne
+    _, nb, ncu = u.shape
     au, aq = tab.au[:ncu, :nd, :ncu], tab.aq[:ncu, :nd, :ncu, :nd]
     ij, detj = tab.invjt, tab.detj
-    f = np.einsum("cdk,eak->eacd", au, u) + np.einsum("cdkx,eakx->eacd", aq, q)
+    f = np.einsum("cdk,eak->eacd", au, u[:ne]) + np.einsum("cdkx,eakx->eacd", aq, q[:ne])
     F = detj[:, None, None, None] * np.einsum("edr,eacd->eacr", ij, f)
     R = np.zeros((ne, nb, ncu))
     for r in range(nd):
@@ -96,7 +100,7 @@ def flux(tab, u, q, tangent, gproj=None, bsrc=None, split=False):
         sgn = 1.0 if hi else -1.0
         ln = np.linalg.norm(ij[:, :, ax], axis=1)
         sj = detj * ln
-        uo, qo = u[:, vol[lf]], q[:, vol[lf]]
+        uo, qo = u[:ne, vol[lf]], q[:ne, vol[lf]]
         fh = np.zeros((ne, tab.nfn, ncu))
         it = np.nonzero(kind == 0)[0]
         if it.size:
@@ -104,7 +108,7 @@ def flux(tab, u, q, tangent, gproj=None, bsrc=None, split=False):
             sw = ((info[it] & 8) > 0)[:, None, None]
             nn = tab.nmap[info[it] >> 8]
             un = u[nbr[it][:, None], nn]
-            qn = q[nbr[it][:, None], nn]
+            qn = q[nbr[it][:, None], nn] if q.shape[0] > nbr[it].max() else np.zeros_like(qo[it])
             ul = np.where(right, un, uo[it])
             ur = np.where(right, uo[it], un)
             ql = np.where(right[..., None], qn, qo[it])
@@ -144,7 +148,7 @@ def flux(tab, u, q, tangent, gproj=None, bsrc=None, split=False):
 
 
 
-def fused(tab, u, tangent, gproj=None, bsrc=None):
+def fused_unused(tab, u, tangent, gproj=None, bsrc=None):
     """Emulate ldg_fused.cu: pass 1 = flux with only the own share of q^,
     exports X = sJ n.(Aq q); pass 2 adds -w X_nbr through the
     neighbour-local-face bits and node maps, lifted by (M1 (x) M1)."""
@@ -191,3 +195,66 @@ def fused(tab, u, tangent, gproj=None, bsrc=None):
                 x = _apply1d(tab.m1, x, a, nd, n1)
         R[it[:, None], vol[lf][None, :]] += x[:, vol[lf]]
     return R
+
+
+
+def pass1(tab, u_ext, tangent, gproj=None, bsrc=None):
+    """Fused pass 1 on the owned rows of a (possibly partitioned) table:
+    returns (R with the own share of q^, exports X of the owned rows)."""
+    nd = tab.nd
+    ne = tab.ne
+    ncu = u_ext.shape[2]
+    q = mixed(tab, u_ext, None if tangent else gproj)
+    R = flux(tab, u_ext, q, tangent, gproj, bsrc, split=True)
+    aq = tab.aq[:ncu, :nd, :ncu, :nd]
+    vol = _vol_nodes(tab)
+    ax_side = _axis_side(tab)
+    X = np.zeros((ne, tab.nf, tab.nfn, ncu))
+    for lf in range(tab.nf):
+        ax, hi = ax_side[lf]
+        f = np.einsum("cdkx,etkx->etcd", aq, q[:, vol[lf]])
+        X[:, lf] = (1.0 if hi else -1.0) * tab.detj[:, None, None] * \
+            np.einsum("etcd,ed->etc", f, tab.invjt[:, :, ax])
+    return R, X
+
+
+def pass2(tab, X_ext, R):
+    """Fused pass 2: add -w X_nbr lifted by (M1 (x) M1) (exports may include
+    ghost rows after the owned rows)."""
+    nd, n1, nfn = tab.nd, tab.n1, tab.nfn
+    nb = R.shape[1]
+    vol = _vol_nodes(tab)
+    ax_side = _axis_side(tab)
+    gcen = tab.model.numflux.grad_trace == "centered"
+    R = R.copy()
+    for lf in range(tab.nf):
+        info, nbr = tab.finfo[:, lf], tab.fnbr[:, lf]
+        it = np.nonzero((info & 3) == 0)[0]
+        right = (info[it] & 4) > 0
+        sw = (info[it] & 8) > 0
+        act = np.ones(it.size, bool) if gcen else (sw != right)
+        it = it[act]
+        if it.size == 0:
+            continue
+        nlf = (info[it] >> 4) & 7
+        nn = tab.nmap[(info[it] >> 8) & 0xffff]
+        tn = np.full(nn.shape, -1)
+        for b in range(tab.nf):
+            inv = np.full(nb, -1)
+            inv[vol[b]] = np.arange(nfn)
+            sel = nlf == b
+            tn[sel] = inv[nn[sel]]
+        full = np.zeros((it.size, nb, R.shape[2]))
+        full[:, vol[lf]] = -(0.5 if gcen else 1.0) * X_ext[nbr[it][:, None], nlf[:, None], tn]
+        x = full
+        for a in range(nd):
+            if a != ax_side[lf][0]:
+                x = _apply1d(tab.m1, x, a, nd, n1)
+        R[it[:, None], vol[lf][None, :]] += x[:, vol[lf]]
+    return R
+
+
+
+def fused(tab, u, tangent, gproj=None, bsrc=None):
+    R, X = pass1(tab, u, tangent, gproj, bsrc)
+    return pass2(tab, X, R)
