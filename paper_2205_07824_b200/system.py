@@ -95,14 +95,16 @@ class LdgSystem:
     """The semi-discrete LDG operator on the B200 (tensor quad/hex, kind D,
     flux linear in (u, q))."""
 
-    def __init__(self, model, mesh, topology, master, device=None):
+    def __init__(self, model, mesh, topology, master, device=None, tables=None):
+        """`tables` (internal): prebuilt host tables, e.g. one partition's
+        ``parallel.LocalTables``; default builds them from the setup objects."""
         import torch
         self.model, self.mesh, self.topology, self.master = model, mesh, topology, master
         self.kind = model.kind
         self.ncu, self.nd, self.nw = model.ncu, model.nd, model.nw
         if model.nd != mesh.nd:
             raise DiscError(f"model nd={model.nd} but mesh nd={mesh.nd}")
-        self.tab = TensorTables(model, mesh, topology, master)
+        self.tab = tables if tables is not None else TensorTables(model, mesh, topology, master)
         self.lib = _lib.load()
         self.device = torch.device(device if device is not None else "cuda")
         self.fi_switch = self.tab.switch
@@ -246,12 +248,27 @@ class LdgSystem:
                    "ldg_compute_mixed")
         return q
 
-    def scratch(self):
-        """Face-export scratch of the fused operator (device, cached)."""
-        if "x" not in self._scratch:
-            n = int(self.lib.ldg_scratch_doubles(self._h))
-            self._scratch["x"] = self._empty((max(n, 1),))
-        return self._scratch["x"]
+    def scratch(self, rows=None):
+        """Face-export scratch of the fused operator (device, cached); with
+        `rows` > n_elements the buffer also holds ghost-element rows."""
+        rows = self.n_elements if rows is None else rows
+        key = ("x", rows)
+        if key not in self._scratch:
+            per = int(self.lib.ldg_scratch_doubles(self._h)) // max(self.n_elements, 1)
+            self._scratch[key] = self._empty((max(rows * per, 1),))
+        return self._scratch[key]
+
+    def operator_pass(self, which, u, tangent, t=0.0, scratch=None, out=None):
+        """One pass of the fused operator (1: element pass, 2: completion);
+        the partitioned layer exchanges halos between them."""
+        R = out if out is not None else self._empty((self.n_elements, self.n_nodes, self.ncu))
+        x = scratch if scratch is not None else self.scratch()
+        g = None if tangent else self.boundary_data(t)
+        b = None if tangent else self.source_data(t)
+        _lib.check(self.lib.ldg_operator_pass(self._h, which, int(bool(tangent)), _lib.ptr(u),
+                                              _lib.ptr(g), _lib.ptr(b), _lib.ptr(x), _lib.ptr(R),
+                                              self._stream()), "ldg_operator_pass")
+        return R
 
     def residual_dev(self, u, t=0.0, out=None, scratch=None):
         R = out if out is not None else self._empty(u.shape)
