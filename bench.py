@@ -20,8 +20,9 @@ n=54 -> 10,077,696 DOFs) -- the matvec GMRES applies every iteration.
 * ``--impl reference``: that reference CPU implementation timed on this
   host, same metric and unit.
 
-Multi-GPU (torchrun, N>1): round-1 runs independent replicas (weak scaling,
-each rank its own 10M-DOF system); see DESIGN.md for the partitioned path.
+Multi-GPU (torchrun, N>1): weak scaling on an N-slab box ((54 N) x 54 x 54
+hexes); each rank owns one 10M-DOF x-slab, exchanges ghost-element halos
+over NCCL twice per matvec (parallel.PartitionedLdgSystem).
 """
 
 from __future__ import annotations
@@ -57,10 +58,13 @@ def peaks():
         return {}
 
 
-def build_problem(n, p=P):
+def build_problem(n, p=P, nx_mult=1):
+    """Config-3 problem; with nx_mult = N the box is N unit cubes long in x
+    (N x-slabs of n^3 elements: weak scaling, one slab per rank)."""
     from paper_2205_07824_b200 import meshgen, model, refelem
     m = model.load_model(str(MODEL))
-    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [n] * 3, "hex")
+    mesh = meshgen.generate_structured([(0.0, float(nx_mult)), (0.0, 1.0), (0.0, 1.0)],
+                                       [n * nx_mult, n, n], "hex")
     topo = meshgen.build_face_topology(mesh)
     master = refelem.build_master("hex", p)
     return m, mesh, topo, master
@@ -151,26 +155,37 @@ def run_b200(args, rank, world):
     import torch.distributed as dist
     from paper_2205_07824_b200 import _lib as L
     from paper_2205_07824_b200.system import LdgSystem, SolverState
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
-    m, mesh, topo, master = build_problem(args.n)
+    m, mesh, topo, master = build_problem(args.n, nx_mult=world)
     t0 = time.time()
-    s = LdgSystem(m, mesh, topo, master)
+    if world == 1:
+        s = LdgSystem(m, mesh, topo, master)
+        core = s
+    else:
+        # element-partitioned: this rank owns one x-slab, NCCL halos
+        from paper_2205_07824_b200.parallel import PartitionedLdgSystem
+        s = PartitionedLdgSystem(m, mesh, topo, master, world, rank, device=dev)
+        core = s.sys
     setup_s = time.time() - t0
     ne, nb, ndof = s.n_elements, s.n_nodes, s.n_dofs
     gen = torch.Generator(device=dev).manual_seed(rank)
     du = torch.randn((ne, nb, 1), dtype=torch.float64, device=dev, generator=gen)
     dR = torch.empty_like(du)
-    X = s.scratch()
+    X = core.scratch() if world == 1 else s.X
+    u_in = du if world == 1 else s.u_ext
     dq = torch.empty((ne, nb, 1, 3), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
-    lib, h = s.lib, s._h
+    lib, h = core.lib, core._h
 
     def step():
-        s.tangent_dev(du, out=dR, scratch=X)
+        if world == 1:
+            s.tangent_dev(du, out=dR, scratch=X)
+        else:
+            s.tangent_dev(du, out=dR)
 
     def launch_pass(k):
-        L.check(lib.ldg_operator_pass(h, k, 1, L.ptr(du), None, None, L.ptr(X), L.ptr(dR),
+        L.check(lib.ldg_operator_pass(h, k, 1, L.ptr(u_in), None, None, L.ptr(X), L.ptr(dR),
                                       L.stream_ptr()), "operator pass")
 
     for _ in range(args.warmup):
@@ -207,9 +222,11 @@ def run_b200(args, rank, world):
                for _ in range(args.steps)]
         for k in range(args.steps):
             ev2[k][0].record(stream)
-            s.mixed_dev(du, homogeneous=True, out=dq)
+            if world == 1:
+                core.mixed_dev(du, homogeneous=True, out=dq)
             ev2[k][1].record(stream)
-            s.flux_from_mixed_dev(du, dq, True, out=dR)
+            if world == 1:
+                core.flux_from_mixed_dev(du, dq, True, out=dR)
             ev2[k][2].record(stream)
         torch.cuda.synchronize()
     p1_ms = [e[0].elapsed_time(e[1]) for e in ev]
@@ -222,7 +239,7 @@ def run_b200(args, rank, world):
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     t_ms = float(tmax.item())
     # algorithmic bytes of the fused passes from the face tables
-    tab = s.tab
+    tab = core.tab
     info = tab.finfo
     interior = (info & 3) == 0
     right = (info & 4) > 0
@@ -236,15 +253,30 @@ def run_b200(args, rank, world):
 
     # e2e through the public drop-in call with pinned host buffers
     du_host = du.cpu().pin_memory()
-    st = SolverState(u=du_host, q=None, w=None, t=0.0)
-    for _ in range(2):
-        s.residual_tangent(st, du_host)
-    torch.cuda.synchronize()
-    e0 = time.perf_counter()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world == 1:
+        st = SolverState(u=du_host, q=None, w=None, t=0.0)
+
+        def e2e_step():
+            return s.residual_tangent(st, du_host)[0]
+    else:
+        out_host = torch.empty(du_host.shape, dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            d = du_host.to(dev, non_blocking=True)
+            r = s.tangent_dev(d)
+            out_host.copy_(r, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return out_host
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = time.perf_counter()
     ea.record(stream)
     for _ in range(args.steps):
-        out, _, _ = s.residual_tangent(st, du_host)
+        out = e2e_step()
     eb.record(stream)
     torch.cuda.synchronize()
     e2e_ms = ea.elapsed_time(eb) / args.steps
@@ -276,7 +308,8 @@ def run_b200(args, rank, world):
                                f"structured hex box n={args.n}, p=3, tangent J(u)du",
                    "dofs_per_gpu": ndof, "elements_per_gpu": ne,
                    "l2": "L2 flushed (256 MB write) between timed steps; per-step CUDA events",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"element-partitioned x{world} (x-slabs, NCCL halos)"
+                                   if world > 1 else "single GPU"),
                    "setup_s": round(setup_s, 2)},
         "e2e": {"value": world * ndof / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
                 "h2d_bytes_per_step": ndof * 8, "d2h_bytes_per_step": ndof * 8,
@@ -296,7 +329,7 @@ def run_b200(args, rank, world):
                             "target_60pct_gdofs": 0.6 * hbm / BYTES_MATVEC,
                             "fused_bytes_per_dof": (bytes_p1 + bytes_p2) / ndof,
                             "fused_frac": ach_fused / hbm},
-        "unfused_reference_structure": {
+        "unfused_reference_structure": None if world > 1 else {
             "ms_per_step": float(np.median(unf_ms)), "mixed_ms": float(np.median(unf_mixed)),
             "gdofs": ndof / (float(np.median(unf_ms)) * 1e-3) / 1e9},
         "gpu_launches": 2 * args.steps,
@@ -329,8 +362,9 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+        # LDG_DIST_BACKEND=gloo lets several ranks share one GPU (testing only)
+        dist.init_process_group(os.environ.get("LDG_DIST_BACKEND", "nccl"))
     run_b200(args, rank, world)
     if world > 1:
         import torch.distributed as dist

@@ -663,21 +663,29 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
   __syncthreads();
   int mask = 0;
   if (active) {
+    // addresses first, then every gather issued back to back (one latency)
+    const double* src[NFACE];
 #pragma unroll
     for (int lf = 0; lf < NFACE; ++lf) {
       const int info = info_[lf];
-      if (!(info & LDG_FL_COMPLETE)) continue;
-      mask |= 1 << lf;
-      const double wgt = P.grad_centered ? -0.5 : -1.0;
+      const bool act = info & LDG_FL_COMPLETE;
+      mask |= act ? (1 << lf) : 0;
       const int nlf = (info >> 4) & 7;
-      const int mid = (info >> LDG_FACE_MAP_SHIFT) & 0xffff;
+      const int mid = act ? (info >> LDG_FACE_MAP_SHIFT) & 0xffff : 0;
       const int nv = map_in_smem ? s_map[mid * NF + lt] : __ldg(P.nmap + mid * NF + lt);
-      const int2 w = make_int2(nbr_[lf], info);
       const int tn = vol_to_face<N1, ND>(face_axis(ND, nlf), nv);
-#pragma unroll
-      for (int c = 0; c < NCU; ++c)
-        sv[slot][lf][lt][c] = wgt * __ldg(X + (((size_t)w.x * NFACE + nlf) * NF + tn) * NCU + c);
+      src[lf] = act ? X + (((size_t)nbr_[lf] * NFACE + nlf) * NF + tn) * NCU : nullptr;
     }
+    double xv[NFACE][NCU];
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) xv[lf][c] = src[lf] ? __ldg(src[lf] + c) : 0.0;
+    const double wgt = P.grad_centered ? -0.5 : -1.0;
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) sv[slot][lf][lt][c] = wgt * xv[lf][c];
   }
   __syncthreads();
   if (!active || mask == 0) return;
