@@ -350,7 +350,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_ELEM)
+    ap.add_argument("--elems", dest="n", type=int, default=N_ELEM,
+                    help="hexes per direction per rank (default 54 -> 10,077,696 DOFs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -66,6 +66,17 @@ __device__ __forceinline__ int vol_to_face(int ax, int v) {
   return ax == 0 ? j + N1 * k : (ax == 1 ? i + N1 * k : i + N1 * j);
 }
 
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void bad_if(const TensorParams& P, int e, double v) {
   if (!isfinite(v)) atomicMin(P.bad, (unsigned long long)e);
 }
@@ -154,13 +165,8 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   __shared__ __align__(16) double s_j[EPB][S::SJ];      // jumps; later face-slab pencils
   __shared__ __align__(16) double s_fh[EPB][S::FACEV];  // sJ f^ (own share)
   __shared__ __align__(16) double s_f[EPB][S::SF];      // face F^q; later B23 plane
-  constexpr int kMaxMaps = S::MAXMAPS;
-  __shared__ int s_map[kMaxMaps * NF];
   constexpr int KSZ = NC + ND;             // C, Cu, sJ per face axis
-  __shared__ double s_k[EPB][KSZ];
-  const bool map_in_smem = P.n_maps <= kMaxMaps;
-  if (map_in_smem)
-    for (int x = threadIdx.x; x < P.n_maps * NF; x += blockDim.x) s_map[x] = __ldg(P.nmap + x);
+  __shared__ __align__(16) double s_k[EPB][KSZ];
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
   const int e = blockIdx.x * EPB + slot;
   const bool active = slot < EPB && e < P.ne;
@@ -180,21 +186,25 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   auto ridx = [&](int m) { return ND == 3 ? vix(m, ta, tb) : m + N1 * ta; };
   auto yidx = [&](int m) { return ND == 3 ? vix(ta, m, tb) : 0; };
 
-  // ---- A: u column, element coefficient block, face records (all loads
-  // issued before any use)
+  // ---- A: u column and the element coefficient block stream into shared
+  // memory with cp.async (no register staging); the face records come into
+  // registers and the neighbour / boundary-data gathers they address are
+  // issued right away, so all of the element's global latency overlaps.
   double uc[NCU][N1];
   const double* kc = s_k[slot];            // element coefficient block (shared)
   FaceRec fr[NFACE];
+  double ext[NFACE][NCU];
   if (active) {
     const double* ue = u + (size_t)e * NB * NCU;
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
       const int node = ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k;
 #pragma unroll
-      for (int c = 0; c < NCU; ++c) uc[c][k] = __ldg(ue + node * NCU + c);
+      for (int c = 0; c < NCU; ++c) cp_async8(su + c * NBP + cidx(k), ue + node * NCU + c);
     }
     const double* kb = P.kco + (size_t)e * P.kstride;
-    for (int x = lt; x < KSZ; x += TPE) s_k[slot][x] = __ldg(kb + x);
+    for (int x = lt; x < KSZ; x += TPE) cp_async8(s_k[slot] + x, kb + x);
+    cp_async_commit();
 #pragma unroll
     for (int lf = 0; lf < NFACE; ++lf) {
       const double2 v = __ldg(reinterpret_cast<const double2*>(frec + (size_t)e * NFACE + lf));
@@ -203,37 +213,36 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       fr[lf].nbr = w.x;
       fr[lf].info = w.y;
     }
-#pragma unroll
-    for (int k = 0; k < N1; ++k)
-#pragma unroll
-      for (int c = 0; c < NCU; ++c) su[c * NBP + cidx(k)] = uc[c][k];
-  }
-  __syncthreads();
-
-  // ---- B: face node lt of every face: jumps and the u part of sJ f^
-  // all neighbour / boundary-data gathers are issued first (one latency)
-  double ext[NFACE][NCU];
-  if (active) {
+    const double* src[NFACE];
 #pragma unroll
     for (int lf = 0; lf < NFACE; ++lf) {
       const int info = fr[lf].info, nbr = fr[lf].nbr;
       const int kind = info & LDG_FACE_KIND_MASK;
-      const bool right = info & LDG_FACE_SIDE_RIGHT;
-      const bool sw = info & LDG_FACE_SWITCH;
-      const double* src = nullptr;
+      src[lf] = nullptr;
       if (kind == LDG_FACE_INTERIOR) {
         if (info & LDG_FL_UNBR) {
           const int mid = (info >> LDG_FACE_MAP_SHIFT) & 0xffff;
-          const int nn = map_in_smem ? s_map[mid * NF + lt] : __ldg(P.nmap + mid * NF + lt);
-          src = u + ((size_t)nbr * NB + nn) * NCU;
+          src[lf] = u + ((size_t)nbr * NB + __ldg(P.nmap + mid * NF + lt)) * NCU;
         }
       } else if (!TANGENT && gproj) {
-        src = gproj + ((size_t)nbr * NF + lt) * NCU;
+        src[lf] = gproj + ((size_t)nbr * NF + lt) * NCU;
       }
-#pragma unroll
-      for (int c = 0; c < NCU; ++c) ext[lf][c] = src ? __ldg(src + c) : 0.0;
     }
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) ext[lf][c] = src[lf] ? __ldg(src[lf] + c) : 0.0;
   }
+  cp_async_wait_all();
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) uc[c][k] = su[c * NBP + cidx(k)];
+  }
+
+  // ---- B: face node lt of every face: jumps and the u part of sJ f^
   double gl[NCU][N1];       // d/dk of the column (registers)
   if (active) {
 #pragma unroll
