@@ -128,6 +128,47 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def run_solve(system, orth="cgs2"):
+    """Newton-GMRES time to solution on the bench system with the
+    reference acceptance flags (test_acceptance.py:69-81), block-Jacobi."""
+    import torch
+    from paper_2205_07824_b200.driver import run_steady
+    torch.cuda.synchronize()
+    st, stats, tm = run_steady(system, precond="block_jacobi", orth=orth)
+    torch.cuda.synchronize()
+    xq = system.disc.xq
+    w = system.disc.wdetj
+    uq = np.einsum("qa,ea->eq", system.master.phi, st.u.reshape(system.n_elements, -1).cpu().numpy())
+    ex = np.sin(np.pi * xq[..., 0]) * np.sin(np.pi * xq[..., 1]) * np.sin(np.pi * xq[..., 2])
+    err = float(np.sqrt(np.sum(w * (uq - ex) ** 2) / np.sum(w * ex ** 2)))
+    return {"orth": orth, "precond_build_s": tm["precond_build_s"], "solve_s": tm["solve_s"],
+            "time_to_solution_s": tm["precond_build_s"] + tm["solve_s"],
+            "newton_iters": stats.newton_iters, "gmres_iters": stats.total_gmres_iters,
+            "final_residual": stats.final_residual, "error_u": err}
+
+
+def cpu_solve(n):
+    """Oracle (reference numpy path) steady solve on n^3 hexes, same flags."""
+    from oracle import make_oracle
+    from oracle.solver_oracle import (block_jacobi_blocks, block_jacobi_factor,
+                                      distance2_coloring, element_neighbors, newton_solve)
+    m, mesh, topo, master = build_problem(n)
+    o = make_oracle(m, mesh, topo, master)
+    ne, nb = mesh.connectivity.shape[0], master.n_nodes
+    tan = lambda x, v: o.residual_tangent(x.reshape(ne, nb, 1), v.reshape(ne, nb, 1)).ravel()  # noqa: E731
+    t0 = time.perf_counter()
+    colors = distance2_coloring(element_neighbors(topo, ne))
+    M = block_jacobi_factor(block_jacobi_blocks(tan, np.zeros(ne * nb), ne, nb, colors))
+    t1 = time.perf_counter()
+    x, st = newton_solve(lambda x: o.residual(x.reshape(ne, nb, 1)).ravel(), tan, np.zeros(ne * nb),
+                         abs_tol=1e-11, rel_tol=3e-8, forcing=1e-8, restart=250,
+                         gmres_max_iter=6000, precond=M)
+    t2 = time.perf_counter()
+    return {"dofs": ne * nb, "precond_build_s": t1 - t0, "solve_s": t2 - t1,
+            "time_to_solution_s": t2 - t0, "newton_iters": st["newton_iters"],
+            "gmres_iters": int(sum(st["gmres_iters"])), "cores": 1}
+
+
 def run_reference(args, rank):
     """The reference CPU path (oracle port of ldgkit's numpy implementation)."""
     if rank != 0:
@@ -234,7 +275,8 @@ def run_b200(args, rank, world):
     unf_ms = [e[0].elapsed_time(e[2]) for e in ev2]
     unf_mixed = [e[0].elapsed_time(e[1]) for e in ev2]
     t_ms = float(np.sum([e[0].elapsed_time(e[1]) for e in st_ev])) / args.steps
-    tmax = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+    tmax = torch.tensor([t_ms], dtype=torch.float64,
+                        device=dev if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     t_ms = float(tmax.item())
@@ -282,7 +324,8 @@ def run_b200(args, rank, world):
     e2e_ms = ea.elapsed_time(eb) / args.steps
     wall_e2e = (time.perf_counter() - e0) / args.steps * 1e3
     assert out.device.type == "cpu"
-    emax = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    emax = torch.tensor([e2e_ms], dtype=torch.float64,
+                        device=dev if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(emax, op=dist.ReduceOp.MAX)
     e2e_ms = float(emax.item())
@@ -335,6 +378,12 @@ def run_b200(args, rank, world):
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_solve:
+        line["solve"] = {"metric": "Newton-GMRES time to solution (s), config 3, block-Jacobi, "
+                                   "acceptance flags", "dofs": ndof,
+                         "gpu": run_solve(s, "cgs2")}
+        if not args.no_cpu_baseline:
+            line["solve"]["cpu_oracle_small"] = {"n": 3, **cpu_solve(3)}
     if not args.no_cpu_baseline:
         ts, nd_cpu = cpu_oracle_times(CPU_SAMPLE_N, 3)
         v = nd_cpu / float(np.median(ts)) / 1e9
@@ -353,6 +402,8 @@ def main():
     ap.add_argument("--elems", dest="n", type=int, default=N_ELEM,
                     help="hexes per direction per rank (default 54 -> 10,077,696 DOFs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true",
+                    help="skip the Newton-GMRES time-to-solution measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -54,6 +54,7 @@ extern "C" {
 #define LDG_FL_QOWN (1 << 26)      /* q^ = this side's q */
 #define LDG_FL_QHALF (1 << 27)     /* q^ centered: half from each side */
 #define LDG_FL_COMPLETE (1 << 28)  /* pass 2 adds the neighbour share */
+#define LDG_FL_ALPHA_SHIFT 29      /* bits 29..30: jump coefficient 0 | 1 | 1/2 */
 
 /* Host-side description of a tensor-product (quad/hex) kind-D system with a
  * flux that is linear in (u, q) with constant coefficients.  Pointers are

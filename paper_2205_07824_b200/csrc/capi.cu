@@ -112,16 +112,34 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
       for (size_t lf = 0; lf < nf; ++lf) {
         const size_t x = e * nf + lf;
         int32_t info = t->finfo[x] & 0x00ffffff;
-        if ((info & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR) {
+        const int kind = info & LDG_FACE_KIND_MASK;
+        const double sj = kb[cq + cu + axis_of((int)lf)];
+        // coefficient form of the trace rules (disc.py:492-574, 657-821):
+        // jump = alpha d and sJ sigma tau (u_L - u^) = beta sJ tau d with
+        // d = u_own - u_other; alpha, beta in {0, 1, 1/2}
+        int acode = 0;
+        double beta = 0.0;
+        if (kind == LDG_FACE_INTERIOR) {
           const bool right = info & LDG_FACE_SIDE_RIGHT, sw = info & LDG_FACE_SWITCH;
           const bool tc = t->trace_centered, gc = t->grad_centered;
-          if (tc || (sw == right) || !sw) info |= LDG_FL_UNBR;
+          if (tc) { acode = 2; beta = 0.5; }
+          else {
+            acode = (sw == right) ? 1 : 0;      // u^ = the neighbour's trace
+            beta = sw ? 0.0 : 1.0;              // penalty vanishes on switch faces
+          }
+          if (acode != 0 || beta != 0.0) info |= LDG_FL_UNBR;
           if (gc || (sw == right)) info |= LDG_FL_EXPORT;
           if (!gc && (sw == right)) info |= LDG_FL_QOWN;
           if (gc) info |= LDG_FL_QHALF;
           if (gc || (sw != right)) info |= LDG_FL_COMPLETE;
+          rec[2 * x] = beta * sj * t->ftau[x];
+        } else if (kind == LDG_FACE_DIRICHLET) {
+          acode = 1;
+          rec[2 * x] = sj * t->ftau[x];
+        } else {
+          rec[2 * x] = sj;                      // Neumann: + sJ g
         }
-        rec[2 * x] = t->ftau[x] * kb[cq + cu + axis_of((int)lf)];
+        info |= acode << LDG_FL_ALPHA_SHIFT;
         int32_t pair[2] = {t->fnbr[x], info};
         memcpy(&rec[2 * x + 1], pair, sizeof(pair));
       }

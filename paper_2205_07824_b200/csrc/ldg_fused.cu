@@ -251,41 +251,25 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       const int kind = info & LDG_FACE_KIND_MASK;
       const int ax = face_axis(ND, lf);
       const double sgn = face_side(ND, lf) ? 1.0 : -1.0;
+      (void)ax;
       const int vn_ = fvol<N1, ND>(lf, lt);
       const int vs = ND == 3 ? swz<N1>(vn_ % N1, (vn_ / N1) % N1, vn_ / (N1 * N1)) : vn_;
-      const double sjac = kc[NC + ax];       // |t1 x t2| of the (affine) face
-      const double stau = fr[lf].tau;        // sJ * tau
-      double uo[NCU], uh[NCU], fh[NCU], jmp[NCU];
+      // coefficient form (ldg_create): with d = u_own - u_other (u_other =
+      // neighbour trace, Dirichlet g, or 0), every rule of disc.py:492-574 and
+      // :657-821 is jump = alpha d, sJ * sigma * tau (u_L - u^) = rec.tau * d;
+      // Neumann faces carry rec.tau = sJ and add sJ g.
+      const double rt = fr[lf].tau;
+      const int acode = (info >> LDG_FL_ALPHA_SHIFT) & 3;
+      const double alpha = acode == 1 ? 1.0 : (acode == 2 ? 0.5 : 0.0);
+      const bool neu = kind == LDG_FACE_NEUMANN;
+      double uh[NCU], fh[NCU], jmp[NCU];
 #pragma unroll
-      for (int c = 0; c < NCU; ++c) uo[c] = su[c * NBP + vs];
-      if (kind == LDG_FACE_INTERIOR) {
-        const bool right = info & LDG_FACE_SIDE_RIGHT;
-        const bool sw = info & LDG_FACE_SWITCH;
-        double un[NCU];
-        const bool got = info & LDG_FL_UNBR;
-#pragma unroll
-        for (int c = 0; c < NCU; ++c) un[c] = got ? ext[lf][c] : uo[c];
-#pragma unroll
-        for (int c = 0; c < NCU; ++c) {
-          const double ul = right ? un[c] : uo[c], ur = right ? uo[c] : un[c];
-          uh[c] = P.trace_centered ? 0.5 * (ul + ur) : (sw ? ul : ur);
-          jmp[c] = uo[c] - uh[c];
-          fh[c] = (right ? -stau : stau) * (ul - uh[c]);   // frozen tau (disc.py:694-698)
-        }
-      } else if (kind == LDG_FACE_DIRICHLET) {
-#pragma unroll
-        for (int c = 0; c < NCU; ++c) {
-          uh[c] = ext[lf][c];
-          jmp[c] = uo[c] - uh[c];
-          fh[c] = stau * jmp[c];
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < NCU; ++c) {
-          uh[c] = uo[c];
-          jmp[c] = 0.0;
-          fh[c] = sjac * ext[lf][c];
-        }
+      for (int c = 0; c < NCU; ++c) {
+        const double uo = su[c * NBP + vs];
+        const double d = uo - ext[lf][c];
+        jmp[c] = alpha * d;
+        uh[c] = uo - jmp[c];
+        fh[c] = rt * (neu ? ext[lf][c] : d);
       }
       if (P.flux_uses_u && kind != LDG_FACE_NEUMANN) {
 #pragma unroll
@@ -633,7 +617,6 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
   using S = P2Smem<N1, ND, NCU>;
   constexpr int NB = S::NB, NF = S::NF, TPE = S::TPE, EPB = S::EPB, NFACE = S::NFACE;
   __shared__ double sv[EPB][NFACE][NF][NCU];
-  __shared__ int sact[EPB];
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
   const int e = blockIdx.x * EPB + slot;
   const bool active = slot < EPB && e < P.ne;

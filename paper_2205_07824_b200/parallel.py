@@ -131,21 +131,27 @@ class HaloExchanger:
     def exchange(self, arr):
         import torch
         import torch.distributed as dist
+        # gloo moves host memory only: stage device buffers through the host
+        # (testing several ranks on one GPU); NCCL sends device buffers directly
+        stage = arr.is_cuda and dist.get_backend(self.group) == "gloo"
         ops, recv_bufs = [], []
         flat = arr.reshape(arr.shape[0], -1)
         for q, rows in sorted(self.plan.send.items()):
             idx = torch.as_tensor(rows, device=arr.device)
             buf = flat.index_select(0, idx).contiguous()
+            if stage:
+                buf = buf.cpu()
             ops.append(dist.P2POp(dist.isend, buf, q, group=self.group))
         for q, rows in sorted(self.plan.recv.items()):
-            buf = torch.empty((rows.size, flat.shape[1]), dtype=arr.dtype, device=arr.device)
+            buf = torch.empty((rows.size, flat.shape[1]), dtype=arr.dtype,
+                              device="cpu" if stage else arr.device)
             recv_bufs.append((rows, buf))
             ops.append(dist.P2POp(dist.irecv, buf, q, group=self.group))
         if ops:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
         for rows, buf in recv_bufs:
-            flat.index_copy_(0, torch.as_tensor(rows, device=arr.device), buf)
+            flat.index_copy_(0, torch.as_tensor(rows, device=arr.device), buf.to(arr.device))
         return arr
 
 
@@ -158,7 +164,12 @@ class DistVecOps:
 
     def _ar(self, t):
         import torch.distributed as dist
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        if t.is_cuda and dist.get_backend(self.group) == "gloo":
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 
     def dot(self, x, y, out):
