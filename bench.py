@@ -357,7 +357,9 @@ def run_b200(args, rank, world):
         "e2e": {"value": world * ndof / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
                 "h2d_bytes_per_step": ndof * 8, "d2h_bytes_per_step": ndof * 8,
                 "ms_per_step": e2e_ms, "wall_ms_per_step": wall_e2e,
-                "call": "LdgSystem.residual_tangent(state, du) with pinned torch CPU du"},
+                "call": ("LdgSystem.residual_tangent(state, du) with pinned torch CPU du"
+                         if world == 1 else
+                         "PartitionedLdgSystem.tangent_dev on the H2D copy of pinned du, D2H of R")},
         "roofline": {"bound": "hbm", "kernel": "fused_kernel<4,3,1,tangent> (pass 1)",
                      "achieved": ach_p1, "peak": hbm, "unit": "GB/s",
                      "frac": ach_p1 / hbm, "traffic": None,

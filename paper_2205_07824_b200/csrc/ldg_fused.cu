@@ -616,7 +616,8 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
                 const double* __restrict__ X, double* __restrict__ R) {
   using S = P2Smem<N1, ND, NCU>;
   constexpr int NB = S::NB, NF = S::NF, TPE = S::TPE, EPB = S::EPB, NFACE = S::NFACE;
-  __shared__ double sv[EPB][NFACE][NF][NCU];
+  __shared__ double sv[EPB][NFACE][NF][NCU];    // neighbour exports, then lifted values
+  __shared__ double sw2[EPB][NFACE][NF][NCU];   // first-direction partial lift
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
   const int e = blockIdx.x * EPB + slot;
   const bool active = slot < EPB && e < P.ne;
@@ -680,7 +681,47 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
       for (int c = 0; c < NCU; ++c) sv[slot][lf][lt][c] = wgt * xv[lf][c];
   }
   __syncthreads();
+  // lift every completion face by (M1 (x) M1), sum factorised with all of the
+  // element's threads busy: w[a][b] = sum_a' M[a][a'] v[a'][b], then
+  // out[a][b] = sum_b' M[b][b'] w[a][b'] (thread = face node (a, b))
+  if (active) {
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf) {
+      if (!(mask & (1 << lf))) continue;
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) {
+        double w = 0.0;
+        if (ND == 3) {
+#pragma unroll
+          for (int aa = 0; aa < N1; ++aa) w = fma(Mi[aa], sv[slot][lf][aa + N1 * j][c], w);
+        } else {
+#pragma unroll
+          for (int aa = 0; aa < N1; ++aa) w = fma(Mi[aa], sv[slot][lf][aa][c], w);
+        }
+        sw2[slot][lf][lt][c] = w;
+      }
+    }
+  }
+  __syncthreads();
+  if (active && ND == 3) {
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf) {
+      if (!(mask & (1 << lf))) continue;
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) {
+        double o = 0.0;
+#pragma unroll
+        for (int bb = 0; bb < N1; ++bb) o = fma(Mj[bb], sw2[slot][lf][i + N1 * bb][c], o);
+        sv[slot][lf][lt][c] = o;          // lifted value at face node (i, j)
+      }
+    }
+  }
+  __syncthreads();
   if (!active || mask == 0) return;
+  // gather the lifted face values onto this thread's column and RMW R
+  auto fval = [&](int lf, int t, int c) {
+    return ND == 3 ? sv[slot][lf][t][c] : sw2[slot][lf][t][c];
+  };
   double* Re = R + (size_t)e * NB * NCU;
 #pragma unroll
   for (int c = 0; c < NCU; ++c) {
@@ -688,66 +729,25 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
 #pragma unroll
     for (int k = 0; k < N1; ++k) acc[k] = 0.0;
     if (ND == 3) {
-      // z faces (node (i,j,0|N1-1)): sum_{aa,bb} M[i][aa] M[j][bb] sv[aa + N1 bb]
+      // faces 0 z-, 1 z+ (node (i,j,0|N1-1)), 2 y-, 3 y+ (j = 0|N1-1, coords (i,k)),
+      // 4 x-, 5 x+ (i = 0|N1-1, coords (j,k))
+      if (mask & 1) acc[0] += fval(0, i + N1 * j, c);
+      if (mask & 2) acc[N1 - 1] += fval(1, i + N1 * j, c);
 #pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int lf = side;
-        if (!(mask & (1 << lf))) continue;
-        double s_ = 0.0;
-#pragma unroll
-        for (int bb = 0; bb < N1; ++bb) {
-          double r = 0.0;
-#pragma unroll
-          for (int aa = 0; aa < N1; ++aa) r = fma(Mi[aa], sv[slot][lf][aa + N1 * bb][c], r);
-          s_ = fma(Mj[bb], r, s_);
-        }
-        acc[side ? N1 - 1 : 0] += s_;
-      }
-      // x faces (i = 0 | N1-1, face coords (j,k)); y faces (j = 0 | N1-1, (i,k))
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int lf = q < 2 ? 4 + q : 2 + (q - 2);
-        const bool onface = q < 2 ? (i == (q ? N1 - 1 : 0)) : (j == (q == 3 ? N1 - 1 : 0));
-        if (!(mask & (1 << lf)) || !onface) continue;
-        double w[N1];                           // w[bb] = sum_aa M[row][aa] sv[aa + N1 bb]
-#pragma unroll
-        for (int bb = 0; bb < N1; ++bb) {
-          double r = 0.0;
-#pragma unroll
-          for (int aa = 0; aa < N1; ++aa)
-            r = fma(q < 2 ? Mj[aa] : Mi[aa], sv[slot][lf][aa + N1 * bb][c], r);
-          w[bb] = r;
-        }
-#pragma unroll
-        for (int k = 0; k < N1; ++k) {
-          double r = 0.0;
-#pragma unroll
-          for (int bb = 0; bb < N1; ++bb) r = fma(P.m1[k * N1 + bb], w[bb], r);
-          acc[k] += r;
-        }
+      for (int k = 0; k < N1; ++k) {
+        if ((mask & 4) && j == 0) acc[k] += fval(2, i + N1 * k, c);
+        if ((mask & 8) && j == N1 - 1) acc[k] += fval(3, i + N1 * k, c);
+        if ((mask & 16) && i == 0) acc[k] += fval(4, j + N1 * k, c);
+        if ((mask & 32) && i == N1 - 1) acc[k] += fval(5, j + N1 * k, c);
       }
     } else {
-      // quad: y faces (node (i, 0|N1-1)): sum_aa M[i][aa] sv[aa]; x faces (i = 0|N1-1)
+      // quad faces 0 y-, 2 y+ (node (i, 0|N1-1)), 3 x-, 1 x+ (i = 0|N1-1, coord k)
+      if (mask & 1) acc[0] += fval(0, i, c);
+      if (mask & 4) acc[N1 - 1] += fval(2, i, c);
 #pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int lf = side ? 2 : 0;
-        if (!(mask & (1 << lf))) continue;
-        double s_ = 0.0;
-#pragma unroll
-        for (int aa = 0; aa < N1; ++aa) s_ = fma(Mi[aa], sv[slot][lf][aa][c], s_);
-        acc[side ? N1 - 1 : 0] += s_;
-      }
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int lf = side ? 1 : 3;
-        if (!(mask & (1 << lf)) || i != (side ? N1 - 1 : 0)) continue;
-#pragma unroll
-        for (int k = 0; k < N1; ++k) {
-          double r = 0.0;
-#pragma unroll
-          for (int aa = 0; aa < N1; ++aa) r = fma(P.m1[k * N1 + aa], sv[slot][lf][aa][c], r);
-          acc[k] += r;
-        }
+      for (int k = 0; k < N1; ++k) {
+        if ((mask & 8) && i == 0) acc[k] += fval(3, k, c);
+        if ((mask & 2) && i == N1 - 1) acc[k] += fval(1, k, c);
       }
     }
 #pragma unroll
