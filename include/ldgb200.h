@@ -83,9 +83,34 @@ typedef struct LdgTables {
   double mass_coef[LDG_MAX_NCU];       /* constant mass m_c (disc.py:902-906) */
 } LdgTables;
 
+/* Host-side description of a simplex (tri / tet) kind-D system for the
+ * dense-tabulation kernels (csrc/ldg_dense.cu).  Pointers are HOST memory. */
+typedef struct LdgDenseTables {
+  int32_t nd, nb, nqf, nface, nperm, ncu, ne;
+  int32_t trace_centered, grad_centered, flux_uses_u;
+  const double* geo;      /* (ne, 1 + nd*nd)                                 */
+  const double* fnorm;    /* (ne, nface, nd) outward unit face normals        */
+  const double* fsj;      /* (ne, nface) |t1 x t2| of each (affine) face      */
+  const int32_t* fnbr;    /* (ne, nface) neighbour element / boundary row     */
+  const int32_t* finfo;   /* (ne, nface) kind|side|switch|nbr face<<4|orient<<8 */
+  const double* ftau;     /* (ne, nface) penalty                              */
+  const double* dr;       /* (nd, nb, nb) collocation derivative matrices     */
+  const double* kr;       /* (nd, nb, nb) int d_r phi_a phi_b                 */
+  const double* lift;     /* (nface, nb, nqf) M_ref^-1 Phi^T W                */
+  const double* fluxop;   /* (nface, nb, nqf) Phi^T W                         */
+  const double* phif;     /* (nface, nqf, nb) own face traces                 */
+  const double* phio;     /* (nface, nperm, nqf, nb) neighbour traces         */
+  double au[LDG_MAX_NCU * 3 * LDG_MAX_NCU];
+  double aq[LDG_MAX_NCU * 3 * LDG_MAX_NCU * 3];
+} LdgDenseTables;
+
 typedef struct LdgHandle LdgHandle;
 
 int ldg_create(const LdgTables* host, LdgHandle** out);
+/* Simplex systems: same entry points below (compute_mixed, residual,
+ * residual_tangent); boundary data are values at face quadrature points,
+ * (n_bfaces, nqf, ncu); scratch holds q, ne*nb*ncu*nd doubles. */
+int ldg_create_dense(const LdgDenseTables* host, LdgHandle** out);
 int ldg_destroy(LdgHandle* h);
 int64_t ldg_last_bad_element(LdgHandle* h);
 const char* ldg_last_error(void);

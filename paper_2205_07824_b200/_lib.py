@@ -47,12 +47,26 @@ class LdgTables(C.Structure):
     ]
 
 
+class LdgDenseTables(C.Structure):
+    _fields_ = [
+        ("nd", C.c_int32), ("nb", C.c_int32), ("nqf", C.c_int32), ("nface", C.c_int32),
+        ("nperm", C.c_int32), ("ncu", C.c_int32), ("ne", C.c_int32),
+        ("trace_centered", C.c_int32), ("grad_centered", C.c_int32), ("flux_uses_u", C.c_int32),
+        ("geo", C.c_void_p), ("fnorm", C.c_void_p), ("fsj", C.c_void_p), ("fnbr", C.c_void_p),
+        ("finfo", C.c_void_p), ("ftau", C.c_void_p), ("dr", C.c_void_p), ("kr", C.c_void_p),
+        ("lift", C.c_void_p), ("fluxop", C.c_void_p), ("phif", C.c_void_p), ("phio", C.c_void_p),
+        ("au", C.c_double * (MAX_NCU * 3 * MAX_NCU)),
+        ("aq", C.c_double * (MAX_NCU * 3 * MAX_NCU * 3)),
+    ]
+
+
 _lib = None
 
 _SIGS = {
     "ldg_version": ([], C.c_int),
     "ldg_last_error": ([], C.c_char_p),
     "ldg_create": ([C.POINTER(LdgTables), C.POINTER(C.c_void_p)], C.c_int),
+    "ldg_create_dense": ([C.POINTER(LdgDenseTables), C.POINTER(C.c_void_p)], C.c_int),
     "ldg_destroy": ([C.c_void_p], C.c_int),
     "ldg_last_bad_element": ([C.c_void_p], C.c_int64),
     "ldg_compute_mixed": ([C.c_void_p] * 5, C.c_int),

@@ -17,7 +17,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "lib" / "libldgb200.so"
-SOURCES = ["capi.cu", "ldg_tensor.cu", "ldg_fused.cu", "krylov.cu", "bjacobi.cu"]
+SOURCES = ["capi.cu", "ldg_tensor.cu", "ldg_fused.cu", "ldg_dense.cu", "krylov.cu",
+           "bjacobi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include "ldg_dense.cuh"
 #include "ldg_tensor.cuh"
 
 namespace {
@@ -33,6 +34,9 @@ int upload(T** dst, const T* src, size_t n, const char* what) {
 }  // namespace
 
 struct LdgHandle {
+  int dense = 0;                 // 0: tensor (quad/hex), 1: dense (tri/tet)
+  ldg::DenseParams D;
+  std::vector<void*> dense_bufs;
   ldg::TensorParams P;
   double* geo = nullptr;
   int32_t* fnbr = nullptr;
@@ -199,9 +203,62 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
 
 int ldg_destroy(LdgHandle* h) {
   if (!h) return 0;
+  for (void* p : h->dense_bufs) cudaFree(p);
   cudaFree(h->geo); cudaFree(h->fnbr); cudaFree(h->finfo); cudaFree(h->ftau);
   cudaFree(h->nmap); cudaFree(h->frec); cudaFree(h->kco); cudaFree(h->bad);
   delete h;
+  return 0;
+}
+
+int ldg_create_dense(const LdgDenseTables* t, LdgHandle** out) {
+  if (!t || !out) return fail(2, "null argument");
+  if (t->nd < 2 || t->nd > 3 || t->ncu < 1 || t->ncu > LDG_MAX_NCU || t->ne < 0)
+    return fail(2, "unsupported dense configuration");
+  LdgHandle* h = new LdgHandle();
+  h->dense = 1;
+  memset(&h->D, 0, sizeof(h->D));
+  memset(&h->P, 0, sizeof(h->P));
+  ldg::DenseParams& D = h->D;
+  D.ne = t->ne; D.nd = t->nd; D.nb = t->nb; D.nqf = t->nqf; D.nface = t->nface;
+  D.nperm = t->nperm; D.ncu = t->ncu; D.trace_centered = t->trace_centered;
+  D.grad_centered = t->grad_centered; D.flux_uses_u = t->flux_uses_u;
+  const size_t ne = t->ne, nf = t->nface, nb = t->nb, nq = t->nqf, nd = t->nd;
+  int rc = 0;
+  auto up = [&](const double* src, size_t n, const double** dst, const char* what) {
+    double* d = nullptr;
+    rc |= upload(&d, src, n, what);
+    h->dense_bufs.push_back(d);
+    *dst = d;
+  };
+  auto upi = [&](const int32_t* src, size_t n, const int32_t** dst, const char* what) {
+    int32_t* d = nullptr;
+    rc |= upload(&d, src, n, what);
+    h->dense_bufs.push_back(d);
+    *dst = d;
+  };
+  up(t->geo, ne * (1 + nd * nd), &D.geo, "geo");
+  up(t->fnorm, ne * nf * nd, &D.fnorm, "fnorm");
+  up(t->fsj, ne * nf, &D.fsj, "fsj");
+  upi(t->fnbr, ne * nf, &D.fnbr, "fnbr");
+  upi(t->finfo, ne * nf, &D.finfo, "finfo");
+  up(t->ftau, ne * nf, &D.ftau, "ftau");
+  up(t->dr, nd * nb * nb, &D.dr, "dr");
+  up(t->kr, nd * nb * nb, &D.kr, "kr");
+  up(t->lift, nf * nb * nq, &D.lift, "lift");
+  up(t->fluxop, nf * nb * nq, &D.fluxop, "fluxop");
+  up(t->phif, nf * nq * nb, &D.phif, "phif");
+  up(t->phio, nf * (size_t)t->nperm * nq * nb, &D.phio, "phio");
+  cudaError_t e = cudaMalloc(&h->bad, sizeof(unsigned long long));
+  if (e != cudaSuccess) rc |= fail(3, "bad flag", e);
+  else cudaMemset(h->bad, 0xff, sizeof(unsigned long long));
+  if (rc) {
+    ldg_destroy(h);
+    return 3;
+  }
+  D.bad = h->bad;
+  memcpy(D.au, t->au, sizeof(D.au));
+  memcpy(D.aq, t->aq, sizeof(D.aq));
+  *out = h;
   return 0;
 }
 
@@ -215,12 +272,17 @@ int64_t ldg_last_bad_element(LdgHandle* h) {
 int ldg_compute_mixed(LdgHandle* h, const double* u, const double* gproj,
                       double* q, void* stream) {
   if (!h || !u || !q) return fail(2, "null argument");
+  if (h->dense) {
+    int rc = ldg::launch_dense(h->D, 0, u, gproj, nullptr, q, nullptr, (cudaStream_t)stream);
+    return rc ? fail(rc, "dense compute_mixed launch", cudaGetLastError()) : 0;
+  }
   int rc = ldg::launch_mixed(h->P, u, gproj, q, (cudaStream_t)stream);
   return rc ? fail(rc, "compute_mixed launch", cudaGetLastError()) : 0;
 }
 
 int64_t ldg_scratch_doubles(LdgHandle* h) {
   if (!h) return -1;
+  if (h->dense) return (int64_t)h->D.ne * h->D.nb * h->D.ncu * h->D.nd;
   const int64_t nf = 2 * h->P.nd;
   int64_t nfn = h->P.nd == 3 ? (int64_t)h->P.n1 * h->P.n1 : h->P.n1;
   return (int64_t)h->P.ne * nf * nfn * h->P.ncu;
@@ -229,6 +291,10 @@ int64_t ldg_scratch_doubles(LdgHandle* h) {
 int ldg_residual(LdgHandle* h, const double* u, const double* gproj,
                  const double* bsrc, double* scratch, double* R, void* stream) {
   if (!h || !u || !R || !scratch) return fail(2, "null argument");
+  if (h->dense) {
+    int rc = ldg::launch_dense(h->D, 1, u, gproj, bsrc, scratch, R, (cudaStream_t)stream);
+    return rc ? fail(rc, "dense residual launch", cudaGetLastError()) : 0;
+  }
   int rc = ldg::launch_fused(h->P, false, u, gproj, bsrc, R, scratch, (cudaStream_t)stream);
   return rc ? fail(rc, "residual launch", cudaGetLastError()) : 0;
 }
@@ -236,6 +302,10 @@ int ldg_residual(LdgHandle* h, const double* u, const double* gproj,
 int ldg_residual_tangent(LdgHandle* h, const double* du, double* scratch,
                          double* dR, void* stream) {
   if (!h || !du || !scratch || !dR) return fail(2, "null argument");
+  if (h->dense) {
+    int rc = ldg::launch_dense(h->D, 2, du, nullptr, nullptr, scratch, dR, (cudaStream_t)stream);
+    return rc ? fail(rc, "dense tangent launch", cudaGetLastError()) : 0;
+  }
   int rc = ldg::launch_fused(h->P, true, du, nullptr, nullptr, dR, scratch,
                              (cudaStream_t)stream);
   return rc ? fail(rc, "residual_tangent launch", cudaGetLastError()) : 0;
@@ -245,6 +315,7 @@ int ldg_operator_pass(LdgHandle* h, int pass, int tangent, const double* u,
                       const double* gproj, const double* bsrc, double* scratch,
                       double* R, void* stream) {
   if (!h || !u || !R || !scratch || pass < 1 || pass > 2) return fail(2, "bad argument");
+  if (h->dense) return fail(2, "not available for simplex systems");
   int rc = ldg::launch_fused_pass(h->P, pass, tangent != 0, u, gproj, bsrc, R, scratch,
                                   (cudaStream_t)stream);
   return rc ? fail(rc, "operator pass launch", cudaGetLastError()) : 0;
@@ -254,6 +325,7 @@ int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
                         const double* q, const double* gproj,
                         const double* bsrc, double* R, void* stream) {
   if (!h || !u || !q || !R) return fail(2, "null argument");
+  if (h->dense) return fail(2, "not available for simplex systems");
   int rc = ldg::launch_flux(h->P, tangent != 0, u, q, gproj, bsrc, R, (cudaStream_t)stream);
   return rc ? fail(rc, "flux launch", cudaGetLastError()) : 0;
 }
@@ -261,12 +333,14 @@ int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
 int ldg_mass_apply(LdgHandle* h, const double* v, double scale, double* out,
                    void* stream) {
   if (!h || !v || !out) return fail(2, "null argument");
+  if (h->dense) return fail(2, "not available for simplex systems");
   int rc = ldg::launch_mass(h->P, false, v, scale, out, (cudaStream_t)stream);
   return rc ? fail(rc, "mass launch", cudaGetLastError()) : 0;
 }
 
 int ldg_mass_inv_apply(LdgHandle* h, const double* v, double* out, void* stream) {
   if (!h || !v || !out) return fail(2, "null argument");
+  if (h->dense) return fail(2, "not available for simplex systems");
   int rc = ldg::launch_mass(h->P, true, v, 1.0, out, (cudaStream_t)stream);
   return rc ? fail(rc, "mass inverse launch", cudaGetLastError()) : 0;
 }

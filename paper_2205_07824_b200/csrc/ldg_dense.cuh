@@ -1,0 +1,33 @@
+// Shared definitions for the dense (simplex) LDG kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ldgb200.h"
+
+namespace ldg {
+
+struct DenseParams {
+  int ne, nd, nb, nqf, nface, nperm, ncu;
+  int trace_centered, grad_centered, flux_uses_u;
+  const double* geo;      // (ne, 1+nd*nd)
+  const double* fnorm;    // (ne, nface, nd) outward unit normals
+  const double* fsj;      // (ne, nface) |t1 x t2|
+  const int32_t* fnbr;
+  const int32_t* finfo;   // bits: kind | side | switch | nbr face << 4 | orientation << 8
+  const double* ftau;
+  const double* dr;       // (nd, nb, nb)   collocation derivatives
+  const double* kr;       // (nd, nb, nb)   int d_r phi_a phi_b
+  const double* lift;     // (nface, nb, nqf)  M_ref^-1 Phi^T W
+  const double* fluxop;   // (nface, nb, nqf)  Phi^T W
+  const double* phif;     // (nface, nqf, nb)  own traces
+  const double* phio;     // (nface, nperm, nqf, nb) neighbour traces by orientation
+  unsigned long long* bad;
+  double au[LDG_MAX_NCU * 3 * LDG_MAX_NCU];
+  double aq[LDG_MAX_NCU * 3 * LDG_MAX_NCU * 3];
+};
+
+// what: 0 mixed (q = compute_mixed(u, gval)), 1 residual, 2 tangent
+int launch_dense(const DenseParams& P, int what, const double* u, const double* gval,
+                 const double* bsrc, double* q, double* R, cudaStream_t s);
+
+}  // namespace ldg

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .tables import DiscError, KernelNanError, TensorTables
+from .tables import DenseTables, DiscError, KernelNanError, TensorTables
 
 __all__ = ["LdgSystem", "SolverState", "DiscError", "KernelNanError"]
 
@@ -78,6 +78,8 @@ class _Disc:
     @property
     def mass_inv(self):
         t = self._t
+        if hasattr(t, "minv"):                      # simplex: M_e = detJ M_ref
+            return t.minv[None, :, :] / t.detj[:, None, None]
         mi = t.m1inv
         k = np.kron(np.kron(mi, mi), mi) if t.nd == 3 else np.kron(mi, mi)
         return k[None, :, :] / t.detj[:, None, None]
@@ -104,7 +106,13 @@ class LdgSystem:
         self.ncu, self.nd, self.nw = model.ncu, model.nd, model.nw
         if model.nd != mesh.nd:
             raise DiscError(f"model nd={model.nd} but mesh nd={mesh.nd}")
-        self.tab = tables if tables is not None else TensorTables(model, mesh, topology, master)
+        self.dense = master.kind in ("tri", "tet")
+        if tables is not None:
+            self.tab = tables
+        elif self.dense:
+            self.tab = DenseTables(model, mesh, topology, master)
+        else:
+            self.tab = TensorTables(model, mesh, topology, master)
         self.lib = _lib.load()
         self.device = torch.device(device if device is not None else "cuda")
         self.fi_switch = self.tab.switch
@@ -117,7 +125,44 @@ class LdgSystem:
         self._scratch = {}
 
     # -- native handle -------------------------------------------------------------
+    def _create_dense_handle(self):
+        t = self.tab
+        T = _lib.LdgDenseTables()
+        T.nd, T.nb, T.nqf, T.nface = t.nd, t.nb, t.nqf, t.nf
+        T.nperm, T.ncu, T.ne = len(t.perms), t.ncu, t.ne
+        T.trace_centered = int(self.model.numflux.trace == "centered")
+        T.grad_centered = int(self.model.numflux.grad_trace == "centered")
+        T.flux_uses_u = int(t.flux_uses_u)
+        keep = []
+
+        def arr(a, dt):
+            a, p = _lib.as_c(a, dt)
+            keep.append(a)
+            return p
+
+        T.geo = arr(t.geo, np.float64)
+        T.fnorm = arr(t.fnorm, np.float64)
+        T.fsj = arr(t.fsj, np.float64)
+        T.fnbr = arr(t.fnbr, np.int32)
+        T.finfo = arr(t.finfo, np.int32)
+        T.ftau = arr(t.ftau, np.float64)
+        T.dr = arr(t.dr, np.float64)
+        T.kr = arr(t.kr, np.float64)
+        T.lift = arr(t.lift, np.float64)
+        T.fluxop = arr(t.fluxop, np.float64)
+        T.phif = arr(t.phif, np.float64)
+        T.phio = arr(t.phio, np.float64)
+        for k, v in enumerate(t.au.ravel()):
+            T.au[k] = v
+        for k, v in enumerate(t.aq.ravel()):
+            T.aq[k] = v
+        h = C.c_void_p()
+        _lib.check(self.lib.ldg_create_dense(C.byref(T), C.byref(h)), "ldg_create_dense")
+        self._h = h
+
     def _create_handle(self):
+        if self.dense:
+            return self._create_dense_handle()
         t = self.tab
         T = _lib.LdgTables()
         T.nd, T.n1, T.ncu, T.ne = t.nd, t.n1, t.ncu, t.ne
@@ -215,7 +260,8 @@ class LdgSystem:
         if key not in self._bdata:
             if len(self._bdata) > 4:
                 self._bdata.clear()
-            g = self.tab.boundary_projection(key)
+            g = self.tab.boundary_values(key) if self.dense else \
+                self.tab.boundary_projection(key)
             self._bdata[key] = torch.as_tensor(g, device=self.device) if g.size else None
         return self._bdata[key]
 

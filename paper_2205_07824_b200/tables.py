@@ -553,3 +553,225 @@ class TensorTables:
             wd = self.detj[e][:, None] * m.quad_wts[None, :]
             out[e] = -np.einsum("eq,ceq,qa->eac", wd, s, m.phi)
         return out
+
+
+# ---------------------------------------------------------------------------
+# dense (simplex) tables
+# ---------------------------------------------------------------------------
+
+
+def _face_vertex_perms(kind):
+    import itertools
+    nv = 2 if kind == "tri" else 3
+    return [list(p) for p in itertools.permutations(range(nv))]
+
+
+class DenseTables:
+    """Host arrays for the dense-tabulation kernels (tri / tet): the
+    reference's quadrature-point formulation (disc.py:436-821) with
+    per-element affine geometry and orientation-indexed right traces
+    instead of the reference's per-face Newton-inverted tabulations
+    (disc.py:182-225; they agree to ~1e-15)."""
+
+    def __init__(self, model, mesh, topo, master):
+        self.model, self.mesh, self.topo, self.master = model, mesh, topo, master
+        kind = master.kind
+        if kind != mesh.elem_kind:
+            raise DiscError("master element kind does not match the mesh")
+        if kind not in ("tri", "tet"):
+            raise DiscError(f"dense path is for simplices, got {kind}")
+        if model.kind != "D":
+            raise DiscError(f"B200 path supports diffusion (kind D) models, got {model.kind}")
+        if model.nw > 0 or model.numflux.uhat is not None or model.numflux.fhat is not None:
+            raise DiscError("ODE blocks and u^/f^ overrides are not supported on the B200 path")
+        if master.quad_degree < 2 * master.p:
+            raise DiscError("dense path needs quadrature degree >= 2p")
+        self.kind = kind
+        self.nd, self.p, self.ncu = mesh.nd, master.p, model.ncu
+        self.nb = master.n_nodes
+        self.nf = master.n_faces
+        self.nqf = master.faces[0].weights.shape[0]
+        self.ne = mesh.connectivity.shape[0]
+        if self.ncu > 3:
+            raise DiscError("dense path supports ncu <= 3")
+        TensorTables._flux_coefficients(self)
+        self._geometry()
+        self._operators()
+        self._faces()
+
+    # reuse the affine geometry and face-geometry helpers of the tensor tables
+    _geometry = TensorTables._geometry
+    node_coords = TensorTables.node_coords
+    face_normal_area = TensorTables.face_normal_area
+    _switch_bits = TensorTables._switch_bits
+
+    def _operators(self):
+        m = self.master
+        nd = self.nd
+        dn = m.eval_basis_grad(m.nodes)                       # (a, b, r) = d phi_b / d xi_r (x_a)
+        self.dr = np.ascontiguousarray(dn.transpose(2, 0, 1))  # (r, a, b)
+        w = m.quad_wts
+        self.kr = np.einsum("q,qar,qb->rab", w, m.dphi, m.phi)
+        Mref = np.einsum("q,qa,qb->ab", w, m.phi, m.phi)
+        self.minv = np.linalg.inv(Mref)
+        self.lift = np.stack([self.minv @ (f.phi.T * f.weights[None, :]) for f in m.faces])
+        self.fluxop = np.stack([f.phi.T * f.weights[None, :] for f in m.faces])
+        self.phif = np.stack([f.phi for f in m.faces])       # own traces (nf, nqf, nb)
+        # neighbour traces per (local face, vertex permutation of the face)
+        perms = _face_vertex_perms(self.kind)
+        self.perms = perms
+        sigma = m.faces[0].sigma
+        po = np.zeros((self.nf, len(perms), self.nqf, self.nb))
+        self.perm_pts = np.zeros((self.nf, len(perms), self.nqf, nd))
+        for lf in range(self.nf):
+            v = refelem.VERTS[self.kind][list(refelem.FACES[self.kind][lf])]
+            for o, pi in enumerate(perms):
+                vp = v[pi]
+                xi = vp[0][None, :] + sigma @ (vp[1:] - vp[0])
+                self.perm_pts[lf, o] = xi
+                po[lf, o] = m.eval_basis(xi)
+        self.phio = po
+        self.face_area_ref = np.array([m.faces[lf].weights.sum() for lf in range(self.nf)])
+
+    def _faces(self):
+        topo, model, mesh, m = self.topo, self.model, self.mesh, self.master
+        ne, nf = self.ne, self.nf
+        el, fl, er, fr = (np.asarray(a, dtype=np.int64) for a in
+                          (topo.elem_l, topo.face_l, topo.elem_r, topo.face_r))
+        nfi = el.size
+        self.switch = self._switch_bits(el, fl)
+        fnbr = np.full((ne, nf), -1, dtype=np.int32)
+        finfo = np.full((ne, nf), -1, dtype=np.int32)
+        ftau = np.zeros((ne, nf))
+        tau = float(model.numflux.tau)
+        over_h = True if model.numflux.tau_over_h is None else bool(model.numflux.tau_over_h)
+        ws = model.wavespeed_plan()
+        mu = model.mu_bindings()
+
+        def lam(normals):
+            if ws is None or normals.shape[0] == 0:
+                return 0.0
+            b = {"t": 0.0, **mu}
+            for k in range(self.nd):
+                b[f"n{k + 1}"] = normals[:, k]
+            return evaluate(ws, b)[0]
+
+        n_l = np.zeros((nfi, self.nd))
+        area = np.zeros(nfi)
+        for lf in range(nf):
+            sel = np.nonzero(fl == lf)[0]
+            if sel.size:
+                n_l[sel], sj = self.face_normal_area(el[sel], lf)
+                area[sel] = sj * m.faces[lf].weights.sum()
+        fi_h = 0.5 * (self.elem_vol[el] + self.elem_vol[er]) / np.maximum(area, 1e-300)
+        tau_i = (tau / fi_h if over_h else np.full(nfi, tau)) + lam(n_l)
+        self.fi_h = fi_h
+        # orientation: which vertex permutation of the neighbour's face lands
+        # on this side's face quadrature points (periodic shift applied)
+        tr = np.asarray(topo.translation, dtype=float)
+        if tr.shape[0] != nfi:
+            tr = np.zeros((nfi, self.nd))
+        o_l = self._orient(el, fl, er, fr, tr)
+        o_r = self._orient(er, fr, el, fl, -tr)
+        sw = self.switch.astype(np.int32)
+        fnbr[el, fl] = er
+        fnbr[er, fr] = el
+        finfo[el, fl] = (sw << 3) | (fr.astype(np.int32) << 4) | (o_l << 8)
+        finfo[er, fr] = 4 | (sw << 3) | (fl.astype(np.int32) << 4) | (o_r << 8)
+        ftau[el, fl] = tau_i
+        ftau[er, fr] = tau_i
+        eb, fb, tb = (np.asarray(a, dtype=np.int64) for a in
+                      (topo.elem_b, topo.face_b, topo.tag_b))
+        self.bc_groups = []
+        for tag in (np.unique(tb) if tb.size else []):
+            tag = int(tag)
+            if tag not in model.bcs:
+                raise DiscError(f"mesh boundary tag {tag} has no [bc] entry")
+            bc = model.bcs[tag]
+            if bc.type not in ("dirichlet", "neumann"):
+                raise DiscError(f"boundary type {bc.type!r} is not supported on the B200 path")
+            self.bc_groups.append((tag, bc, np.nonzero(tb == tag)[0]))
+        kinds = np.zeros(eb.size, dtype=np.int32)
+        for tag, bc, idx in self.bc_groups:
+            kinds[idx] = 1 if bc.type == "dirichlet" else 2
+        nb_ = np.zeros((eb.size, self.nd))
+        area_b = np.zeros(eb.size)
+        for lf in range(nf):
+            sel = np.nonzero(fb == lf)[0]
+            if sel.size:
+                nb_[sel], sj = self.face_normal_area(eb[sel], lf)
+                area_b[sel] = sj * m.faces[lf].weights.sum()
+        fb_h = self.elem_vol[eb] / np.maximum(area_b, 1e-300)
+        tau_b = (tau / fb_h if over_h else np.full(eb.size, tau)) + lam(nb_)
+        self.fb_h = fb_h
+        fnbr[eb, fb] = np.arange(eb.size, dtype=np.int32)
+        finfo[eb, fb] = kinds
+        ftau[eb, fb] = tau_b
+        if np.any(finfo < 0):
+            raise DiscError("element with an unclassified face")
+        self.fnbr, self.finfo, self.ftau = fnbr, finfo, ftau
+        self.n_boundary = eb.size
+        self.eb, self.fb = eb, fb
+        # per element-face outward normal and |t1 x t2|
+        self.fnorm = np.zeros((ne, nf, self.nd))
+        self.fsj = np.zeros((ne, nf))
+        for lf in range(nf):
+            n, sj = self.face_normal_area(np.arange(ne), lf)
+            self.fnorm[:, lf] = n
+            self.fsj[:, lf] = sj
+
+    def face_points(self, elems, lf, pts=None):
+        """Physical coordinates of face-lf quadrature points of elements."""
+        xi = self.master.faces[lf].xi if pts is None else pts
+        return self.x0[elems][:, None, :] + np.einsum("edr,qr->eqd", self.J[elems], xi)
+
+    def _orient(self, ea, fa, eb, fbb, shift, chunk=1 << 15):
+        n = ea.size
+        out = np.full(n, -1, dtype=np.int32)
+        scale2 = (1e-9 * max(self.mesh.diameter(), 1.0)) ** 2
+        for a in range(self.nf):
+            for b in range(self.nf):
+                sel = np.nonzero((fa == a) & (fb_ == b))[0] if False else \
+                    np.nonzero((fa == a) & (fbb == b))[0]
+                for c0 in range(0, sel.size, chunk):
+                    s = sel[c0:c0 + chunk]
+                    x = self.face_points(ea[s], a) + shift[s][:, None, :]
+                    for o in range(len(self.perms)):
+                        todo = out[s] < 0
+                        if not todo.any():
+                            break
+                        y = self.face_points(eb[s], b, self.perm_pts[b, o])
+                        ok = np.sum((x - y) ** 2, axis=2).max(axis=1) <= scale2
+                        out[s[ok & todo]] = o
+        if np.any(out < 0):
+            raise DiscError("could not orient a face (non-conforming mesh?)")
+        return out
+
+    def boundary_values(self, t):
+        """(n_bfaces, nqf, ncu) Dirichlet / Neumann data at the face
+        quadrature points (disc.py:559-563, 775-782)."""
+        out = np.zeros((self.n_boundary, self.nqf, self.ncu))
+        model = self.model
+        for tag, bc, idx in self.bc_groups:
+            plan = model.bc_plan(tag)
+            for lf in range(self.nf):
+                s = idx[self.fb[idx] == lf]
+                if s.size == 0:
+                    continue
+                xq = self.face_points(self.eb[s], lf)
+                n, _ = self.face_normal_area(self.eb[s], lf)
+                b = {"t": float(t), **model.mu_bindings()}
+                for k in range(self.nd):
+                    b[f"x{k + 1}"] = xq[..., k].ravel()
+                    b[f"n{k + 1}"] = np.repeat(n[:, k], xq.shape[1])
+                g = evaluate(plan, b)
+                if g.shape[1] != xq.shape[0] * xq.shape[1]:
+                    g = np.broadcast_to(g, (g.shape[0], xq.shape[0] * xq.shape[1]))
+                if not np.isfinite(g).all():
+                    col = int(np.argwhere(~np.isfinite(g))[0][1])
+                    raise KernelNanError(f"bc tag {tag} kernel produced non-finite values "
+                                         f"(first at element {col // xq.shape[1]})")
+                out[s] = g.reshape(self.ncu, s.size, -1).transpose(1, 2, 0)
+        return out
+
+    source_load = TensorTables.source_load

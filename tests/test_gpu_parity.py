@@ -9,7 +9,7 @@ import pytest
 from cases import CASES, GOLDEN, b200_setup, build_case
 
 pytestmark = pytest.mark.gpu
-TENSOR = sorted(n for n, s in CASES.items() if s["kind"] in ("quad", "hex"))
+TENSOR = sorted(CASES)            # every case: tensor (quad/hex) and dense (tri/tet) paths
 TOL = 1e-12
 
 
@@ -40,7 +40,9 @@ def test_residual_tangent_mixed_vs_reference_golden(name):
 
 @pytest.mark.parametrize("kind,counts,p", [("hex", [7, 6, 5], 3), ("hex", [5, 4, 6], 1),
                                           ("hex", [4, 4, 3], 4), ("hex", [3, 3, 4], 5),
-                                          ("quad", [13, 9], 3), ("quad", [6, 7], 6)])
+                                          ("quad", [13, 9], 3), ("quad", [6, 7], 6),
+                                          ("tri", [7, 6], 3), ("tri", [5, 5], 4),
+                                          ("tet", [4, 3, 3], 3), ("tet", [3, 3, 3], 1)])
 def test_vs_oracle_poisson_larger(kind, counts, p):
     from oracle import make_oracle
     from paper_2205_07824_b200 import meshgen, model, refelem

@@ -109,3 +109,18 @@ def test_block_jacobi_shift_rule_on_singular_block():
     assert M.shifted.cpu().tolist() == [1, 0, 0]
     z = M.apply(torch.ones(nb * bs, dtype=torch.float64, device="cuda")).cpu().numpy()
     assert abs(z[1] - 1e12) / 1e12 < 1e-6 and abs(z[5] - 1.0) < 1e-14
+
+
+@pytest.mark.parametrize("precond,want", [("identity", 88), ("block_jacobi", 60)])
+def test_criterion7_known_answer_tri(precond, want):
+    """Published reference answer (pkg/test_output.txt:269, recipe
+    test_acceptance.py:299-324): poisson2d tri n=4 p=2, GMRES iterations
+    identity 88 / block_jacobi 60, one Newton step."""
+    from paper_2205_07824_b200.driver import run_steady
+    from paper_2205_07824_b200.system import LdgSystem
+    spec = dict(model=("file", "poisson2d.model"), kind="tri", counts=[4, 4], p=2)
+    s = LdgSystem(*build_case(spec, *b200_setup()))
+    _, stats, _ = run_steady(s, precond=precond, abs_tol=1e-10, rel_tol=3e-7, forcing=1e-7,
+                             restart=400, gmres_max_iter=4000)
+    assert stats.newton_iters == 1
+    assert abs(stats.total_gmres_iters - want) <= 1, stats.gmres_iters

@@ -59,3 +59,17 @@ def test_node_maps_config3_structure():
     tab = TensorTables(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("hex", 3))
     assert tab.nmap.shape == (6, 16)
     assert tab.switch.all()
+
+
+@pytest.mark.parametrize("name", ["poisson2d_tri_p2", "poisson3d_tet_p2"])
+def test_dense_algebra_matches_reference(name):
+    import dense_emulation as de
+    from paper_2205_07824_b200.tables import DenseTables
+    g = np.load(GOLDEN / f"{name}.npz")
+    t = DenseTables(*build_case(CASES[name], *b200_setup()))
+    assert np.array_equal(t.switch, g["switch"])
+    gv, bs = t.boundary_values(0.0), t.source_load(0.0)
+    q, dq = de.mixed(t, g["u"], gv), de.mixed(t, g["du"])
+    assert rel(q, g["q"]) < 1e-13 and rel(dq, g["dq"]) < 1e-13
+    assert rel(de.flux(t, g["u"], q, False, gv, bs), g["R"]) < 1e-13
+    assert rel(de.flux(t, g["du"], dq, True), g["Jdu"]) < 1e-13
