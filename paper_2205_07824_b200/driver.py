@@ -126,3 +126,138 @@ def run_steady(system, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8, forc
         raise DriverError(f"steady Newton solve did not converge "
                           f"(residual {stats.final_residual:.3e})")
     return out, stats, {"init_s": t1 - t0, "precond_build_s": t2 - t1, "solve_s": t3 - t2}
+
+
+# ---------------------------------------------------------------------------
+# DIRK time integration (timeint.py:33-207) on device vectors
+# ---------------------------------------------------------------------------
+
+
+class ButcherTableau:
+    def __init__(self, A, b, c, order):
+        self.A, self.b, self.c = (np.asarray(x, dtype=float) for x in (A, b, c))
+        self.order = order
+
+    @property
+    def stages(self):
+        return self.b.shape[0]
+
+    @property
+    def is_stiffly_accurate(self):
+        return bool(np.allclose(self.A[-1], self.b, atol=1e-14))
+
+
+def _alexander_gamma():
+    """Root of x^3 - 3x^2 + 3x/2 - 1/6 in (1/6, 1/2) (timeint.py:73-85)."""
+    x = 0.43
+    for _ in range(60):
+        f = x ** 3 - 3 * x ** 2 + 1.5 * x - 1 / 6
+        step = f / (3 * x ** 2 - 6 * x + 1.5)
+        x -= step
+        if abs(step) < 1e-16:
+            break
+    if not (1 / 6 < x < 1 / 2):
+        raise TimeIntError("SDIRK3 gamma iteration left (1/6, 1/2)")
+    return x
+
+
+def dirk_tableau(stages, order):
+    """(1,1) implicit Euler, (2,2) L-stable SDIRK, (3,3) Alexander, (3,4)
+    Crouzeix (timeint.py:88-112)."""
+    if (stages, order) == (1, 1):
+        return ButcherTableau([[1.0]], [1.0], [1.0], 1)
+    if (stages, order) == (2, 2):
+        g = 1.0 - 1.0 / np.sqrt(2.0)
+        return ButcherTableau([[g, 0.0], [1.0 - g, g]], [1.0 - g, g], [g, 1.0], 2)
+    if (stages, order) == (3, 3):
+        g = _alexander_gamma()
+        b1 = -1.5 * g ** 2 + 4.0 * g - 0.25
+        b2 = 1.5 * g ** 2 - 5.0 * g + 1.25
+        return ButcherTableau([[g, 0.0, 0.0], [(1.0 - g) / 2.0, g, 0.0], [b1, b2, g]],
+                              [b1, b2, g], [g, (1.0 + g) / 2.0, 1.0], 3)
+    if (stages, order) == (3, 4):
+        g = 0.5 + np.cos(np.pi / 18.0) / np.sqrt(3.0)
+        d = 1.0 / (6.0 * (2.0 * g - 1.0) ** 2)
+        return ButcherTableau([[g, 0.0, 0.0], [0.5 - g, g, 0.0], [2.0 * g, 1.0 - 4.0 * g, g]],
+                              [d, 1.0 - 2.0 * d, d], [g, 0.5, 1.0 - g], 4)
+    raise TimeIntError(f"unsupported DIRK pair (stages={stages}, order={order}); "
+                       "supported: (1,1),(2,2),(3,3),(3,4)")
+
+
+class StepStats:
+    def __init__(self):
+        self.stage_stats = []
+
+    @property
+    def newton_iters(self):
+        return sum(s.newton_iters for s in self.stage_stats)
+
+    @property
+    def gmres_iters(self):
+        return sum(s.total_gmres_iters for s in self.stage_stats)
+
+    @property
+    def final_residual(self):
+        return max((s.final_residual for s in self.stage_stats), default=0.0)
+
+
+class StageSolveError(TimeIntError):
+    def __init__(self, stage, stats):
+        super().__init__(f"nonlinear solve failed at stage {stage} "
+                         f"(residual {stats.final_residual:.3e})")
+        self.stage, self.stats = stage, stats
+
+
+def _stage_functions(system, Yk, a_dt, t_stage):
+    """N(U) = M (U - U_k)/(a dt) + R(U, t_i) and its tangent (constant mass,
+    timeint.py:132-165)."""
+    shape = (system.n_elements, system.n_nodes, system.ncu)
+    inv = 1.0 / a_dt
+
+    def stage_residual(Y):
+        M = system.mass_apply_dev((Y - Yk).reshape(shape), scale=inv)
+        return (M + system.residual_dev(Y.reshape(shape), t_stage)).reshape(-1)
+
+    def stage_tangent(Y, V):
+        M = system.mass_apply_dev(V.reshape(shape), scale=inv)
+        return (M + system.tangent_dev(V.reshape(shape))).reshape(-1)
+
+    return stage_residual, stage_tangent
+
+
+def advance_step(system, state, dt, tableau, newton_options=None, precond=None, callback=None):
+    """One DIRK step (timeint.py:168-207); state.u numpy or CUDA tensor."""
+    import torch
+    from .system import SolverState
+    if dt <= 0:
+        raise TimeIntError("dt must be positive")
+    opts = newton_options or NewtonOptions()
+    u = state.u if isinstance(state.u, torch.Tensor) else torch.as_tensor(
+        np.ascontiguousarray(state.u, dtype=np.float64), device=system.device)
+    Y0 = u.reshape(-1).to(system.device).clone()
+    K, stats, Ylast = [], StepStats(), None
+    for i in range(tableau.stages):
+        Yk = Y0.clone()
+        for j in range(i):
+            Yk += dt * tableau.A[i, j] * K[j]
+        a_dt = tableau.A[i, i] * dt
+        t_stage = state.t + tableau.c[i] * dt
+        res_fn, tan_fn = _stage_functions(system, Yk, a_dt, t_stage)
+        guess = Yk + a_dt * K[-1] if K else Yk.clone()
+        Yi, st = newton_solve(res_fn, guess, opts, precond=precond, tangent_fn=tan_fn,
+                              callback=callback)
+        stats.stage_stats.append(st)
+        if not st.converged:
+            raise StageSolveError(i, st)
+        K.append((Yi - Yk) / a_dt)
+        Ylast = Yi
+    if tableau.is_stiffly_accurate:
+        Ynew = Ylast
+    else:
+        Ynew = Y0.clone()
+        for bi, Ki in zip(tableau.b, K):
+            Ynew += dt * bi * Ki
+    if not bool(torch.isfinite(Ynew).all()):
+        raise TimeIntError("non-finite state after time step")
+    shape = (system.n_elements, system.n_nodes, system.ncu)
+    return SolverState(u=Ynew.reshape(shape), q=None, w=None, t=state.t + dt), stats

@@ -83,6 +83,9 @@ def build_case(spec, model_mod, mesh_mod, master_mod):
     if "bcs" in spec:
         model.bcs = {t: model_mod.BoundaryCondition(type=ty, data=list(d))
                      for t, (ty, d) in spec["bcs"].items()}
+    if "init" in spec:
+        model.init = {"u1": spec["init"]}
+        model._plans = {}
     if "numflux" in spec:
         for k, v in spec["numflux"].items():
             setattr(model.numflux, k, v)
@@ -104,3 +107,18 @@ def seeded_state(ne, nb, ncu, seed):
 def b200_setup():
     from paper_2205_07824_b200 import meshgen, model, refelem
     return model, meshgen, refelem
+
+
+# transient (DIRK) cases: reference advance_step (timeint.py:168-207)
+TRANSIENT_CASES = {
+    "convdiff2d_quad_p3_dirk22": dict(
+        model=("builtin", "convection_diffusion", 2, [1.0, 0.5, 0.05]), kind="quad",
+        counts=[6, 6], p=3, periodic=2, init="sin(2*pi*x1)*sin(2*pi*x2)",
+        stages=2, order=2, dt=0.02, steps=3, precond="mass"),
+    "convdiff3d_hex_p2_dirk11": dict(
+        model=("builtin", "convection_diffusion", 3, [0.6, -0.3, 0.4, 0.05]), kind="hex",
+        counts=[4, 4, 4], p=2, periodic=3, init="cos(2*pi*x1)*sin(2*pi*x3)",
+        stages=1, order=1, dt=0.01, steps=2, precond="mass"),
+}
+
+TRANSIENT_FLAGS = dict(abs_tol=1e-10, rel_tol=1e-9, forcing=None, restart=60, gmres_max_iter=600)

@@ -30,7 +30,8 @@ from ldgkit.driver import _steady_fns, build_pde_block_jacobi  # noqa: E402
 from ldgkit.solver import NewtonOptions  # noqa: E402
 from ldgkit.timeint import solve_steady  # noqa: E402
 
-from cases import ACCEPT_FLAGS, CASES, SOLVE_CASES, build_case, seeded_state  # noqa: E402
+from cases import (ACCEPT_FLAGS, CASES, SOLVE_CASES, TRANSIENT_CASES,  # noqa: E402
+                   TRANSIENT_FLAGS, build_case, seeded_state)
 
 
 def topo_arrays(sys_):
@@ -81,8 +82,37 @@ def gen_solve(name, spec):
     print("solve", name, stats.newton_iters, stats.gmres_iters)
 
 
+def gen_transient(name, spec):
+    from ldgkit.driver import MassPreconditioner
+    from ldgkit.timeint import advance_step, dirk_tableau
+    model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
+    s = LdgSystem(model, mesh, topo, master)
+    st = s.interpolate_initial()
+    f = TRANSIENT_FLAGS
+    opts = NewtonOptions(abs_tol=f["abs_tol"], rel_tol=f["rel_tol"], max_iter=20,
+                         forcing=f["forcing"], gmres_restart=f["restart"],
+                         gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent")
+    tab = dirk_tableau(spec["stages"], spec["order"])
+    M = MassPreconditioner(s)
+    newton, gm = [], []
+    u0 = st.u.copy()
+    for _ in range(spec["steps"]):
+        st, stats = advance_step(s, st, spec["dt"], tab, opts, precond=M)
+        newton.append(stats.newton_iters)
+        gm.append(stats.gmres_iters)
+    np.savez_compressed(HERE / f"transient_{name}.npz", u0=u0, u=st.u, t=np.array(st.t),
+                        newton=np.array(newton), gmres=np.array(gm))
+    print("transient", name, newton, gm, float(np.abs(st.u).max()))
+
+
 if __name__ == "__main__":
+    if "--transient-only" in sys.argv:
+        for n, sp in TRANSIENT_CASES.items():
+            gen_transient(n, sp)
+        sys.exit(0)
     for n, sp in CASES.items():
         gen_case(n, sp)
     for n, sp in SOLVE_CASES.items():
         gen_solve(n, sp)
+    for n, sp in TRANSIENT_CASES.items():
+        gen_transient(n, sp)

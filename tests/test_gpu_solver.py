@@ -124,3 +124,33 @@ def test_criterion7_known_answer_tri(precond, want):
                              restart=400, gmres_max_iter=4000)
     assert stats.newton_iters == 1
     assert abs(stats.total_gmres_iters - want) <= 1, stats.gmres_iters
+
+
+@pytest.mark.parametrize("name", ["convdiff2d_quad_p3_dirk22", "convdiff3d_hex_p2_dirk11"])
+def test_dirk_transient_matches_reference(name):
+    """Device advance_step (timeint.py:168-207) with the mass preconditioner
+    vs the reference's own transient run (golden)."""
+    from cases import TRANSIENT_CASES, TRANSIENT_FLAGS
+    from paper_2205_07824_b200.driver import MassPreconditioner, advance_step, dirk_tableau
+    from paper_2205_07824_b200.solver import NewtonOptions
+    from paper_2205_07824_b200.system import LdgSystem
+    spec = TRANSIENT_CASES[name]
+    g = np.load(GOLDEN / f"transient_{name}.npz")
+    s = LdgSystem(*build_case(spec, *b200_setup()))
+    st = s.interpolate_initial()
+    assert rel(st.u, g["u0"]) < 1e-13
+    f = TRANSIENT_FLAGS
+    opts = NewtonOptions(abs_tol=f["abs_tol"], rel_tol=f["rel_tol"], max_iter=20,
+                         forcing=f["forcing"], gmres_restart=f["restart"],
+                         gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent")
+    tab = dirk_tableau(spec["stages"], spec["order"])
+    M = MassPreconditioner(s)
+    newton, gm = [], []
+    for _ in range(spec["steps"]):
+        st, stats = advance_step(s, st, spec["dt"], tab, opts, precond=M)
+        newton.append(stats.newton_iters)
+        gm.append(stats.gmres_iters)
+    assert abs(st.t - float(g["t"])) < 1e-14
+    assert newton == g["newton"].tolist()
+    assert all(abs(a - b) <= 1 + 0.02 * b for a, b in zip(gm, g["gmres"].tolist())), (gm, g["gmres"])
+    assert rel(st.u.cpu().numpy(), g["u"]) < 1e-9
