@@ -197,6 +197,28 @@ int ldg_bj_invert(int64_t nblk, int bs, const double* mats, double* inv_t,
 int ldg_bj_apply(int64_t nblk, int bs, const double* inv_t, const double* r,
                  double* z, void* stream);
 
+/* ---- generated model kernels (nonlinear / kind-C path, csrc/jit.cu) ----
+ * The pointwise flux / source / wavespeed / mass plans of a model
+ * (expr.py:363-373, evaluated by disc.py:393-416 in the reference) are lowered
+ * to CUDA device functions by paper_2205_07824_b200/codegen.py, spliced into
+ * csrc/ldg_nl.cuh and compiled for sm_100a by NVRTC.  The loaded module's
+ * kernels replace LdgSystem.compute_mixed / residual / residual_tangent /
+ * mass_apply / mass_tangent_extra (disc.py:436-948) for models whose flux is
+ * not linear with constant coefficients (Euler, Navier-Stokes, Burgers...).
+ * Every kernel takes ONE parameter block by value; the caller packs it. */
+typedef struct LdgModule LdgModule;
+const char* ldg_jit_last_error(void);
+/* compile only (no GPU needed): cubin_out NULL -> *cubin_size = bytes needed */
+int ldg_jit_compile(const char* src, const char* name, const char* const* opts,
+                    int nopts, void* cubin_out, int64_t* cubin_size);
+int ldg_jit_load(const void* cubin, int64_t size, LdgModule** out);
+int ldg_jit_unload(LdgModule* m);
+int ldg_jit_launch(LdgModule* m, const char* kernel, int grid_x, int grid_y,
+                   int block_x, int smem_bytes, const void* params,
+                   int64_t param_size, void* stream);
+int ldg_jit_attr(LdgModule* m, const char* kernel, int* regs, int* local_bytes,
+                 int* static_smem);
+
 #ifdef __cplusplus
 }
 #endif

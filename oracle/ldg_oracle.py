@@ -587,3 +587,15 @@ class OracleLdg:
                                d.xq.shape[:2], "mass")
         vq = np.einsum("qa,eai->eqi", phi, vu)
         return np.einsum("eq,eqi,qa->eai", d.wdetj, mq * vq, phi, optimize=True)
+
+    def mass_tangent_extra(self, u, y, du, t=0.0):
+        """disc.py:927-948: (dm/du . du) y, None for a constant mass."""
+        if self.mass_const:
+            return None
+        d, phi = self.d, self.master.phi
+        uq = np.einsum("qa,eai->eqi", phi, u)
+        duq = np.einsum("qa,eai->eqi", phi, du)
+        _, dm = self._eval(self.model.mass_plan(), self._bind(d.xq, t, uq),
+                           d.xq.shape[:2], "mass", self._seed(duq))
+        yq = np.einsum("qa,eai->eqi", phi, y)
+        return np.einsum("eq,eqi,qa->eai", d.wdetj, dm * yq, phi, optimize=True)

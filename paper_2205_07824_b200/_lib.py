@@ -98,6 +98,14 @@ _SIGS = {
                       C.c_int),
     "ldg_bj_apply": ([C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
                      C.c_int),
+    "ldg_jit_last_error": ([], C.c_char_p),
+    "ldg_jit_compile": ([C.c_char_p, C.c_char_p, C.c_void_p, C.c_int, C.c_void_p,
+                         C.POINTER(C.c_int64)], C.c_int),
+    "ldg_jit_load": ([C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)], C.c_int),
+    "ldg_jit_unload": ([C.c_void_p], C.c_int),
+    "ldg_jit_launch": ([C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                        C.c_int64, C.c_void_p], C.c_int),
+    "ldg_jit_attr": ([C.c_void_p, C.c_char_p] + [C.POINTER(C.c_int)] * 3, C.c_int),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -127,10 +135,12 @@ def load(require_gpu=True):
     return lib
 
 
-def check(rc, what):
+def check(rc, what, jit=False):
     if rc == 0:
         return
-    msg = _lib.ldg_last_error().decode() if _lib is not None else ""
+    msg = ""
+    if _lib is not None:
+        msg = (_lib.ldg_jit_last_error() if jit else _lib.ldg_last_error()).decode()
     raise LdgNativeError(f"{what} failed (code {rc}): {msg}")
 
 

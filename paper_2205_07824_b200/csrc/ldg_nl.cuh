@@ -1,0 +1,736 @@
+// Kernel template of the generated (model-specific) LDG path, compiled at
+// run time by NVRTC for sm_100a (csrc/jit.cu).  NOT compiled by nvcc: the
+// Python side (paper_2205_07824_b200/nonlinear.py) prepends a prelude with
+//   * the compile-time shape: ND, N1 (nodes / direction), NQ1 (Gauss points /
+//     direction), NCU, KIND_C, HAS_WS, TRACE_CENTERED, GRAD_CENTERED,
+//     MASS_CONST, NT (threads per element);
+//   * __constant__ 1D operators c_phi / c_dphi (NQ1 x N1, l_a(x_q)),
+//     c_d1 (GLL collocation derivative), c_clo / c_chi (M1^-1 e_0, e_p),
+//     c_m1inv, c_xq1 (1D Gauss points), c_qw (volume weights), c_fxi / c_fw
+//     (face-point reference coordinates and weights, matched to the
+//     reference's face rules), c_mass (constant mass coefficients);
+//   * the model's plans as device functions plan_flux / plan_src /
+//     plan_ws / plan_mass (+ _d dual variants), emitted by codegen.py;
+// and then this file.
+//
+// Algorithm: the reference's quadrature formulation (disc.py:595-893) per
+// element, with the dense tables replaced by tensor contractions:
+//   nl_mixed     q = M^-1 [-int grad(u) phi + oint (u - u^) n phi]   disc.py:436-490
+//                (GLL collocation: exact for affine elements, as in ldg_tensor.cu)
+//   nl_residual  R = -int f(u,q) . grad(phi) - int s phi + oint f^ phi disc.py:595-653
+//   nl_tangent   the reference linearisation of R (frozen tau, LLF dlam tie
+//                rule, homogeneous lift, zero Neumann tangent)       disc.py:657-862
+//   nl_mass      int m(u) v phi  (and the (dm/du du) y extra term)   disc.py:897-948
+//   nl_mass_inv  M^-1 v = detJ^-1 (M1^-1)^(x)nd v                    driver.py:92-106
+// Interior faces are visited from both elements (element-centric: no scatter,
+// no atomics); both sides evaluate the numerical flux in the LEFT element's
+// frame (left normal, left = u^-), so the two contributions are bitwise
+// negatives of each other exactly as the reference's scatter of +/- vals.
+
+typedef unsigned long long u64;
+typedef unsigned long long sz_t;  // (no <cstddef> under NVRTC)
+
+constexpr int NB = ND == 3 ? N1 * N1 * N1 : N1 * N1;
+constexpr int NQ = ND == 3 ? NQ1 * NQ1 * NQ1 : NQ1 * NQ1;
+constexpr int NFN = ND == 3 ? N1 * N1 : N1;
+constexpr int NQF = ND == 3 ? NQ1 * NQ1 : NQ1;
+constexpr int NFACE = 2 * ND;
+constexpr int NVQ = KIND_C ? 0 : NCU * ND;
+constexpr int NV = NCU + NVQ;                  // state variables per point (u, q)
+constexpr int KMAX = N1 > NQ1 ? N1 : NQ1;
+constexpr int MX = ND == 3 ? KMAX * KMAX * KMAX : KMAX * KMAX;
+constexpr int MXF = ND == 3 ? KMAX * KMAX : KMAX;
+constexpr int NG = NCU * (ND + 1);             // G_r (r < ND) and the source field
+
+struct NlParams {
+  int ne, nbface;
+  double t, scale;
+  const double* geo;     // (ne, 1 + ND*ND): detJ, invjt[d][r]
+  const double* xmap;    // (ne, ND + ND*ND): x0, J[d][r] with x = x0 + J xi
+  const int* fnbr;       // (ne, NFACE) neighbour element / boundary-face row
+  const int* finfo;      // (ne, NFACE) kind | right<<2 | switch<<3 | map<<8
+  const double* fgeo;    // (ne, NFACE, ND + 2): left normal, left |t1 x t2|, tau/h
+  const int* nmap;       // (n_maps, NFN) own face node -> neighbour volume node
+  const double* gq;      // (nbface, NQF, NCU) boundary data at face points
+  const double* gproj;   // (nbface, NFN, NCU) projected Dirichlet data (mixed lift)
+  const double* u;       // base state (ne, NB, NCU)
+  const double* q;       // base mixed gradient (ne, NB, NCU, ND) / mass operand v
+  const double* du;      // direction
+  const double* dq;      // direction gradient (homogeneous lift of du)
+  double* out;
+  u64* bad;              // [0]: first element with a non-finite plan value
+};
+
+__device__ __forceinline__ bool fin(double v) { return v - v == 0.0; }
+// (ldg_sign / ldg_min / ldg_max, used by the plans, come with the prelude)
+__device__ __forceinline__ void flag(const NlParams& P, int e, double v) {
+  if (!fin(v)) atomicMin(P.bad, (u64)e);
+}
+
+// hex local faces z-, z+, y-, y+, x-, x+; quad y-, x+, y+, x- (master.py:43-44)
+__device__ __forceinline__ int face_axis(int lf) {
+  return ND == 3 ? (lf < 2 ? 2 : (lf < 4 ? 1 : 0)) : ((lf == 0 || lf == 2) ? 1 : 0);
+}
+__device__ __forceinline__ int face_side(int lf) {
+  return ND == 3 ? (lf & 1) : (lf == 1 || lf == 2 ? 1 : 0);
+}
+// volume node of face node t (t = i_a0 + N1 i_a1 over the tangential axes a0 < a1)
+__device__ __forceinline__ int face_vol_node(int lf, int t) {
+  const int ax = face_axis(lf);
+  const int io = face_side(lf) ? N1 - 1 : 0;
+  if (ND == 2) return ax == 0 ? io + N1 * t : t + N1 * io;
+  const int a = t % N1, b = t / N1;
+  if (ax == 0) return io + N1 * a + N1 * N1 * b;
+  if (ax == 1) return a + N1 * io + N1 * N1 * b;
+  return a + N1 * b + N1 * N1 * io;
+}
+
+// ---------------------------------------------------------------------------
+// block-cooperative 1D contraction along one axis of a (D0 x D1 x D2) grid
+// (D0 fastest) for NVAR variables stored [v][grid]:
+//   out[v][.., o, ..] = sum_i M(o, i) in[v][.., i, ..]
+// M(o, i) = op[o * N1 + i] (interpolation, rows = outputs) or, with TRANS,
+// op[i * N1 + o] (the transpose: quadrature -> nodes).  `sel(v)` picks the
+// operator id of variable v (dphi for the differentiated direction).
+// ---------------------------------------------------------------------------
+enum { OP_PHI = 0, OP_DPHI = 1, OP_M1INV = 2 };
+__device__ __forceinline__ double op_at(int id, int k) {
+  return id == OP_PHI ? c_phi[k] : (id == OP_DPHI ? c_dphi[k] : c_m1inv[k]);
+}
+template <int D0, int D1, int D2, int AX, int NIN, int NOUT, bool TRANS, typename Sel>
+__device__ __forceinline__ void contract(const double* __restrict__ in, double* __restrict__ out,
+                                         int nvar, int tid, Sel sel) {
+  constexpr int O0 = AX == 0 ? NOUT : D0, O1 = AX == 1 ? NOUT : D1, O2 = AX == 2 ? NOUT : D2;
+  constexpr int I0 = AX == 0 ? NIN : D0, I1 = AX == 1 ? NIN : D1, I2 = AX == 2 ? NIN : D2;
+  constexpr int OSZ = O0 * O1 * O2, ISZ = I0 * I1 * I2;
+  constexpr int STR = AX == 0 ? 1 : (AX == 1 ? I0 : I0 * I1);
+  const int total = nvar * OSZ;
+  for (int idx = tid; idx < total; idx += NT) {
+    const int v = idx / OSZ, r = idx - v * OSZ;
+    const int o0 = r % O0, o1 = (r / O0) % O1, o2 = r / (O0 * O1);
+    const int o = AX == 0 ? o0 : (AX == 1 ? o1 : o2);
+    const int base = v * ISZ + (AX == 0 ? 0 : o0) + (AX == 1 ? 0 : o1) * I0 +
+                     (AX == 2 ? 0 : o2) * I0 * I1;
+    const int id = sel(v);
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < NIN; ++i)
+      acc = fma(op_at(id, TRANS ? i * N1 + o : o * N1 + i), in[base + i * STR], acc);
+    out[idx] = acc;
+  }
+}
+
+// nodes -> volume quadrature points (all variables, operator phi)
+__device__ __forceinline__ void to_quad(double* a, double* b, int nvar, int tid, double*& res) {
+  auto phi = [](int) { return (int)OP_PHI; };
+  if (ND == 3) {
+    contract<N1, N1, N1, 0, N1, NQ1, false>(a, b, nvar, tid, phi);
+    __syncthreads();
+    contract<NQ1, N1, N1, 1, N1, NQ1, false>(b, a, nvar, tid, phi);
+    __syncthreads();
+    contract<NQ1, NQ1, N1, 2, N1, NQ1, false>(a, b, nvar, tid, phi);
+    __syncthreads();
+    res = b;
+  } else {
+    contract<N1, N1, 1, 0, N1, NQ1, false>(a, b, nvar, tid, phi);
+    __syncthreads();
+    contract<NQ1, N1, 1, 1, N1, NQ1, false>(b, a, nvar, tid, phi);
+    __syncthreads();
+    res = a;
+  }
+}
+
+// quadrature fields [r][c] (r < ND: G_r, r = ND: source) -> nodes, applying
+// dphi^T along direction r and phi^T elsewhere (the transposed volume rule)
+__device__ __forceinline__ void from_quad(double* a, double* b, int nfield, int tid, double*& res) {
+  auto sel0 = [](int v) { return v / NCU == 0 ? (int)OP_DPHI : (int)OP_PHI; };
+  auto sel1 = [](int v) { return v / NCU == 1 ? (int)OP_DPHI : (int)OP_PHI; };
+  auto sel2 = [](int v) { return v / NCU == 2 ? (int)OP_DPHI : (int)OP_PHI; };
+  if (ND == 3) {
+    contract<NQ1, NQ1, NQ1, 0, NQ1, N1, true>(a, b, nfield, tid, sel0);
+    __syncthreads();
+    contract<N1, NQ1, NQ1, 1, NQ1, N1, true>(b, a, nfield, tid, sel1);
+    __syncthreads();
+    contract<N1, N1, NQ1, 2, NQ1, N1, true>(a, b, nfield, tid, sel2);
+    __syncthreads();
+    res = b;
+  } else {
+    contract<NQ1, NQ1, 1, 0, NQ1, N1, true>(a, b, nfield, tid, sel0);
+    __syncthreads();
+    contract<N1, NQ1, 1, 1, NQ1, N1, true>(b, a, nfield, tid, sel1);
+    __syncthreads();
+    res = a;
+  }
+}
+
+__device__ __forceinline__ void quad_point(int p, double* xi) {
+  xi[0] = c_xq1[p % NQ1];
+  xi[1] = c_xq1[(p / NQ1) % NQ1];
+  if (ND == 3) xi[2] = c_xq1[p / (NQ1 * NQ1)];
+}
+
+__device__ __forceinline__ void phys_point(const NlParams& P, int e, const double* xi, double* x) {
+  const double* m = P.xmap + (sz_t)e * (ND + ND * ND);
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    double a = m[d];
+#pragma unroll
+    for (int r = 0; r < ND; ++r) a = fma(m[ND + d * ND + r], xi[r], a);
+    x[d] = a;
+  }
+}
+
+// global value of state variable v (u components, then q components) of the
+// array family `arr` (0: base u/q, 1: direction du/dq) at (element, node)
+__device__ __forceinline__ double state_at(const NlParams& P, int fam, int v, sz_t e, int node) {
+  if (v < NCU) return (fam ? P.du : P.u)[(e * NB + node) * NCU + v];
+  return (fam ? P.dq : P.q)[(e * NB + node) * (NCU * ND) + (v - NCU)];
+}
+
+// ---------------------------------------------------------------------------
+// mixed gradient (kind D): one thread per node, EPBM elements per block
+// ---------------------------------------------------------------------------
+constexpr int EPBM = NB >= 128 ? 1 : 128 / NB;
+
+extern "C" __global__ void __launch_bounds__(EPBM * NB > 32 ? EPBM * NB : 32)
+nl_mixed(const __grid_constant__ NlParams P) {
+  __shared__ double su[EPBM][NCU][NB];
+  __shared__ double sj[EPBM][NFACE][NFN][NCU];
+  const int slot = threadIdx.x / NB, a = threadIdx.x % NB;
+  const int e = blockIdx.x * EPBM + slot;
+  const bool active = slot < EPBM && e < P.ne;
+  if (active)
+    for (int c = 0; c < NCU; ++c) su[slot][c][a] = P.u[((sz_t)e * NB + a) * NCU + c];
+  __syncthreads();
+  if (active) {
+    for (int idx = a; idx < NFACE * NFN; idx += NB) {
+      const int lf = idx / NFN, t = idx % NFN;
+      const int info = P.finfo[e * NFACE + lf], nbr = P.fnbr[e * NFACE + lf];
+      const int kind = info & 3;
+      const int vn = face_vol_node(lf, t);
+      for (int c = 0; c < NCU; ++c) {
+        const double own = su[slot][c][vn];
+        double jump = 0.0;
+        if (kind == 0) {
+          const bool right = info & 4, sw = info & 8;
+          const bool own_hat = !TRACE_CENTERED && (sw != right);   // u^ = own trace
+          if (!own_hat) {
+            const int nn = P.nmap[(info >> 8) * NFN + t];
+            const double other = P.u[((sz_t)nbr * NB + nn) * NCU + c];
+            jump = TRACE_CENTERED ? 0.5 * (own - other) : own - other;
+          }
+        } else if (kind == 1) {
+          jump = own - (P.gproj ? P.gproj[((sz_t)nbr * NFN + t) * NCU + c] : 0.0);
+        }
+        sj[slot][lf][t][c] = jump;
+      }
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+  const double* g = P.geo + (sz_t)e * (1 + ND * ND);
+  const int i = a % N1, j = (a / N1) % N1, k = ND == 3 ? a / (N1 * N1) : 0;
+  const int ix[3] = {i, j, k};
+  for (int c = 0; c < NCU; ++c) {
+    double gr[ND];
+#pragma unroll
+    for (int r = 0; r < ND; ++r) {
+      double acc = 0.0;
+      const int st = r == 0 ? 1 : (r == 1 ? N1 : N1 * N1);
+      const int b0 = a - ix[r] * st;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) acc = fma(c_d1[ix[r] * N1 + m], su[slot][c][b0 + m * st], acc);
+      gr[r] = acc;
+    }
+    double qd[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      double acc = 0.0;
+#pragma unroll
+      for (int r = 0; r < ND; ++r) acc = fma(g[1 + d * ND + r], gr[r], acc);
+      qd[d] = -acc;
+    }
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf) {
+      const int ax = face_axis(lf);
+      const bool hi = face_side(lf);
+      const int nidx = ix[ax];
+      int t;
+      if (ND == 3) t = ax == 0 ? j + N1 * k : (ax == 1 ? i + N1 * k : i + N1 * j);
+      else t = ax == 0 ? j : i;
+      const double cf = hi ? c_chi[nidx] : c_clo[nidx];
+      const double v = (hi ? cf : -cf) * sj[slot][lf][t][c];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) qd[d] = fma(v, g[1 + d * ND + ax], qd[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < ND; ++d) P.out[(((sz_t)e * NB + a) * NCU + c) * ND + d] = qd[d];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// residual / tangent: one element per block of NT threads
+// ---------------------------------------------------------------------------
+template <bool TANGENT>
+struct RShape {
+  static constexpr int NVA = NV * (TANGENT ? 2 : 1);              // u,q (+ du,dq)
+  static constexpr int BS = (NVA > NG ? NVA : NG) * MX;           // one work buffer
+  static constexpr int SMEM = NVA * NB + NCU * NB + 2 * BS;       // doubles
+  // faces per round: own + neighbour traces (two stages) and the face fluxes
+  // must fit in the two volume work buffers
+  static constexpr int fits(int fr) { return 4 * fr * NVA * MXF + fr * NQF * NCU <= 2 * BS; }
+  static constexpr int pick() {
+    int best = 1;
+    for (int c = 1; c <= NFACE; ++c)
+      if (fits(c)) best = c;
+    return best;
+  }
+  static constexpr int FR = pick();
+};
+
+// numerical flux f^ . n at one face point (disc.py:657-862), in the left frame
+template <bool TANGENT>
+__device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bool right, bool sw,
+                                          int brow, int s, const double* x, const double* n,
+                                          double tau0, const double* vo, const double* vn,
+                                          double* fh) {
+  // vo / vn: own / neighbour values [u(NCU) q(NVQ) | du dq] at this point
+  const double* uo = vo;
+  const double* duo = vo + NV;
+  if (kind == 2) {                                     // neumann: f^ = g, zero tangent
+#pragma unroll
+    for (int c = 0; c < NCU; ++c) fh[c] = TANGENT ? 0.0 : P.gq[((sz_t)brow * NQF + s) * NCU + c];
+    return;
+  }
+  double f[NCU * ND], df[NCU * ND];
+  if (kind == 1) {                                     // dirichlet
+    double g[NCU], zero[NCU];
+#pragma unroll
+    for (int c = 0; c < NCU; ++c) {
+      g[c] = P.gq[((sz_t)brow * NQF + s) * NCU + c];
+      zero[c] = 0.0;
+    }
+    if (KIND_C) {
+      // LLF against the ghost state g (disc.py:839-862)
+      double fg[NCU * ND], lami, lamg, dlami = 0.0;
+      if (TANGENT) {
+        plan_flux_d(x, P.t, uo, nullptr, nullptr, n, duo, nullptr, nullptr, f, df);
+        plan_ws_d(x, P.t, uo, nullptr, nullptr, n, duo, nullptr, nullptr, &lami, &dlami);
+      } else {
+        plan_flux(x, P.t, uo, nullptr, nullptr, n, f);
+        plan_ws(x, P.t, uo, nullptr, nullptr, n, &lami);
+      }
+      plan_flux(x, P.t, g, nullptr, nullptr, n, fg);
+      plan_ws(x, P.t, g, nullptr, nullptr, n, &lamg);
+      flag(P, e, lami);
+      flag(P, e, lamg);
+      const double lam = ldg_max(lami, lamg);
+      const double dlam = lami >= lamg ? dlami : 0.0;
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) {
+        double fa = 0.0, dfa = 0.0;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          flag(P, e, f[c * ND + d]);
+          flag(P, e, fg[c * ND + d]);
+          fa += (f[c * ND + d] + fg[c * ND + d]) * n[d];
+          if (TANGENT) dfa += df[c * ND + d] * n[d];
+        }
+        fh[c] = TANGENT ? 0.5 * dfa + 0.5 * dlam * (uo[c] - g[c]) + 0.5 * lam * duo[c]
+                        : 0.5 * fa + 0.5 * lam * (uo[c] - g[c]);
+      }
+    } else {
+      // f(g, q_b) . n + tau_b (u_b - g) (disc.py:799-821)
+      const double* qo = uo + NCU;
+      const double* dqo = duo + NCU;
+      if (TANGENT) plan_flux_d(x, P.t, g, qo, nullptr, n, zero, dqo, nullptr, f, df);
+      else plan_flux(x, P.t, g, qo, nullptr, n, f);
+      double tau = tau0;
+      if (HAS_WS) {
+        double li, lg;
+        plan_ws(x, P.t, uo, nullptr, nullptr, n, &li);
+        plan_ws(x, P.t, g, nullptr, nullptr, n, &lg);
+        flag(P, e, li);
+        flag(P, e, lg);
+        tau += ldg_max(li, lg);
+      }
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) {
+        double fa = 0.0;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          flag(P, e, f[c * ND + d]);
+          fa += (TANGENT ? df[c * ND + d] : f[c * ND + d]) * n[d];
+        }
+        fh[c] = TANGENT ? fa + tau * duo[c] : fa + tau * (uo[c] - g[c]);
+      }
+    }
+    return;
+  }
+  // interior: left / right states
+  const double* uL = right ? vn : vo;
+  const double* uR = right ? vo : vn;
+  const double* duL = uL + NV;
+  const double* duR = uR + NV;
+  if (KIND_C) {
+    // local Lax-Friedrichs (disc.py:724-751)
+    double fR[NCU * ND], dfR[NCU * ND], lamL, lamR, dlamL = 0.0, dlamR = 0.0;
+    if (TANGENT) {
+      plan_flux_d(x, P.t, uL, nullptr, nullptr, n, duL, nullptr, nullptr, f, df);
+      plan_flux_d(x, P.t, uR, nullptr, nullptr, n, duR, nullptr, nullptr, fR, dfR);
+      plan_ws_d(x, P.t, uL, nullptr, nullptr, n, duL, nullptr, nullptr, &lamL, &dlamL);
+      plan_ws_d(x, P.t, uR, nullptr, nullptr, n, duR, nullptr, nullptr, &lamR, &dlamR);
+    } else {
+      plan_flux(x, P.t, uL, nullptr, nullptr, n, f);
+      plan_flux(x, P.t, uR, nullptr, nullptr, n, fR);
+      plan_ws(x, P.t, uL, nullptr, nullptr, n, &lamL);
+      plan_ws(x, P.t, uR, nullptr, nullptr, n, &lamR);
+    }
+    flag(P, e, lamL);
+    flag(P, e, lamR);
+    const double lam = ldg_max(lamL, lamR);
+    const double dlam = lamL >= lamR ? dlamL : dlamR;
+#pragma unroll
+    for (int c = 0; c < NCU; ++c) {
+      double fa = 0.0, dfa = 0.0;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        flag(P, e, f[c * ND + d]);
+        flag(P, e, fR[c * ND + d]);
+        fa += (f[c * ND + d] + fR[c * ND + d]) * n[d];
+        if (TANGENT) dfa += (df[c * ND + d] + dfR[c * ND + d]) * n[d];
+      }
+      fh[c] = TANGENT ? 0.5 * dfa + 0.5 * dlam * (uL[c] - uR[c]) + 0.5 * lam * (duL[c] - duR[c])
+                      : 0.5 * fa + 0.5 * lam * (uL[c] - uR[c]);
+    }
+    return;
+  }
+  // kind D: f(u^, q^) . n + tau (u^- - u^) (disc.py:657-722)
+  double uh[NCU], duh[NCU], qh[NVQ > 0 ? NVQ : 1], dqh[NVQ > 0 ? NVQ : 1];
+#pragma unroll
+  for (int c = 0; c < NCU; ++c) {
+    uh[c] = TRACE_CENTERED ? 0.5 * (uL[c] + uR[c]) : (sw ? uL[c] : uR[c]);
+    if (TANGENT) duh[c] = TRACE_CENTERED ? 0.5 * (duL[c] + duR[c]) : (sw ? duL[c] : duR[c]);
+  }
+#pragma unroll
+  for (int k = 0; k < NVQ; ++k) {
+    const double ql = uL[NCU + k], qr = uR[NCU + k];
+    qh[k] = GRAD_CENTERED ? 0.5 * (ql + qr) : (sw ? qr : ql);
+    if (TANGENT) {
+      const double dl = duL[NCU + k], dr = duR[NCU + k];
+      dqh[k] = GRAD_CENTERED ? 0.5 * (dl + dr) : (sw ? dr : dl);
+    }
+  }
+  if (TANGENT) plan_flux_d(x, P.t, uh, qh, nullptr, n, duh, dqh, nullptr, f, df);
+  else plan_flux(x, P.t, uh, qh, nullptr, n, f);
+  double tau = tau0;
+  if (HAS_WS) {
+    double ll, lr;
+    plan_ws(x, P.t, uL, nullptr, nullptr, n, &ll);
+    plan_ws(x, P.t, uR, nullptr, nullptr, n, &lr);
+    flag(P, e, ll);
+    flag(P, e, lr);
+    tau += ldg_max(ll, lr);
+  }
+#pragma unroll
+  for (int c = 0; c < NCU; ++c) {
+    double fa = 0.0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      flag(P, e, f[c * ND + d]);
+      fa += (TANGENT ? df[c * ND + d] : f[c * ND + d]) * n[d];
+    }
+    fh[c] = TANGENT ? fa + tau * (duL[c] - duh[c]) : fa + tau * (uL[c] - uh[c]);
+  }
+}
+
+template <bool TANGENT>
+__device__ __forceinline__ void residual_body(const NlParams& P) {
+  using S = RShape<TANGENT>;
+  constexpr int NVA = S::NVA, FR = S::FR;
+  static_assert(S::fits(1), "face buffers do not fit");
+  extern __shared__ __align__(16) double smem_r[];
+  double* sV = smem_r;                      // [NVA][NB] node values
+  double* sR = sV + NVA * NB;             // [NCU][NB] residual accumulator
+  double* bA = sR + NCU * NB;             // work buffers
+  double* bB = bA + S::BS;
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (e >= P.ne) return;
+
+  // ---- load u, q (+ du, dq) of the element: [v][node]
+  for (int idx = tid; idx < NVA * NB; idx += NT) {
+    const int v = idx / NB, a = idx % NB;
+    const int fam = v >= NV, vv = v % NV;
+    const double val = state_at(P, fam, vv, (sz_t)e, a);
+    sV[idx] = val;
+    bA[idx] = val;
+  }
+  __syncthreads();
+
+  // ---- volume: interpolate to quadrature points
+  double* vq;
+  to_quad(bA, bB, NVA, tid, vq);
+  double* gbuf = vq == bA ? bB : bA;
+  const double* geo = P.geo + (sz_t)e * (1 + ND * ND);
+  const double detj = geo[0];
+  for (int p = tid; p < NQ; p += NT) {
+    double val[NVA];
+#pragma unroll
+    for (int v = 0; v < NVA; ++v) val[v] = vq[v * NQ + p];
+    double xi[ND], x[ND];
+    quad_point(p, xi);
+    phys_point(P, e, xi, x);
+    double f[NCU * ND], df[NCU * ND], s[NCU], ds[NCU];
+    const double* qv = NVQ ? val + NCU : nullptr;
+    if (TANGENT) {
+      const double* dqv = NVQ ? val + NV + NCU : nullptr;
+      plan_flux_d(x, P.t, val, qv, nullptr, nullptr, val + NV, dqv, nullptr, f, df);
+      plan_src_d(x, P.t, val, qv, nullptr, nullptr, val + NV, dqv, nullptr, s, ds);
+    } else {
+      plan_flux(x, P.t, val, qv, nullptr, nullptr, f);
+      plan_src(x, P.t, val, qv, nullptr, nullptr, s);
+    }
+    const double wd = c_qw[p] * detj;
+#pragma unroll
+    for (int c = 0; c < NCU; ++c) {
+      flag(P, e, s[c]);
+#pragma unroll
+      for (int d = 0; d < ND; ++d) flag(P, e, f[c * ND + d]);
+#pragma unroll
+      for (int r = 0; r < ND; ++r) {
+        double a = 0.0;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) a = fma(TANGENT ? df[c * ND + d] : f[c * ND + d], geo[1 + d * ND + r], a);
+        gbuf[(r * NCU + c) * NQ + p] = wd * a;
+      }
+      gbuf[(ND * NCU + c) * NQ + p] = wd * (TANGENT ? ds[c] : s[c]);
+    }
+  }
+  __syncthreads();
+  double* rn;
+  from_quad(gbuf, vq, NG, tid, rn);
+  for (int idx = tid; idx < NCU * NB; idx += NT) {
+    const int c = idx / NB, a = idx % NB;
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r <= ND; ++r) acc += rn[(r * NCU + c) * NB + a];
+    sR[idx] = -acc;
+  }
+  __syncthreads();
+
+  // ---- faces, FR at a time: traces at face points, f^, lift
+  constexpr int TSZ = FR * NVA * MXF;          // one trace buffer (own or neighbour)
+  double* T0 = bA;                             // [side][f][v][face grid], dense
+  double* T1 = bA + 2 * TSZ;
+  double* sF = bA + 4 * TSZ;                   // [f][NQF][NCU]
+  for (int f0 = 0; f0 < NFACE; f0 += FR) {
+    const int nfr = NFACE - f0 < FR ? NFACE - f0 : FR;
+    for (int idx = tid; idx < 2 * FR * NVA * NFN; idx += NT) {
+      const int side = idx / (FR * NVA * NFN), r = idx % (FR * NVA * NFN);
+      const int f = r / (NVA * NFN), v = (r / NFN) % NVA, t = r % NFN;
+      double val = 0.0;
+      if (f < nfr) {
+        const int lf = f0 + f;
+        if (side == 0) {
+          val = sV[v * NB + face_vol_node(lf, t)];
+        } else {
+          const int info = P.finfo[e * NFACE + lf];
+          if ((info & 3) == 0) {
+            const int nbr = P.fnbr[e * NFACE + lf];
+            const int nn = P.nmap[(info >> 8) * NFN + t];
+            val = state_at(P, v >= NV, v % NV, (sz_t)nbr, nn);
+          }
+        }
+      }
+      T0[idx] = val;
+    }
+    __syncthreads();
+    auto phi = [](int) { return (int)OP_PHI; };
+    double* tr;
+    if (ND == 3) {
+      contract<N1, N1, 1, 0, N1, NQ1, false>(T0, T1, 2 * FR * NVA, tid, phi);
+      __syncthreads();
+      contract<NQ1, N1, 1, 1, N1, NQ1, false>(T1, T0, 2 * FR * NVA, tid, phi);
+      __syncthreads();
+      tr = T0;
+    } else {
+      contract<N1, 1, 1, 0, N1, NQ1, false>(T0, T1, 2 * FR * NVA, tid, phi);
+      __syncthreads();
+      tr = T1;
+    }
+    // trace layout after contraction: [side][f][v][NQF]
+    for (int it = tid; it < nfr * NQF; it += NT) {
+      const int f = it / NQF, s = it % NQF, lf = f0 + f;
+      const int info = P.finfo[e * NFACE + lf];
+      const int kind = info & 3;
+      const bool right = kind == 0 && (info & 4);
+      const bool sw = info & 8;
+      const int brow = P.fnbr[e * NFACE + lf];
+      const double* fg = P.fgeo + ((sz_t)e * NFACE + lf) * (ND + 2);
+      double n[ND];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) n[d] = fg[d];
+      double x[ND];
+      phys_point(P, e, &c_fxi[(lf * NQF + s) * ND], x);
+      double vo[NVA], vn[NVA];
+#pragma unroll
+      for (int v = 0; v < NVA; ++v) {
+        vo[v] = tr[((0 * FR + f) * NVA + v) * NQF + s];
+        vn[v] = tr[((1 * FR + f) * NVA + v) * NQF + s];
+      }
+      double fh[NCU];
+      face_flux<TANGENT>(P, e, kind, right, sw, brow, s, x, n, fg[ND + 1], vo, vn, fh);
+      const double w = c_fw[lf * NQF + s] * fg[ND] * (right ? -1.0 : 1.0);
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) sF[(f * NQF + s) * NCU + c] = w * fh[c];
+    }
+    __syncthreads();
+    // lift onto the face nodes, one face at a time (faces share edge nodes)
+    for (int f = 0; f < nfr; ++f) {
+      const int lf = f0 + f;
+      for (int it = tid; it < NFN * NCU; it += NT) {
+        const int t = it / NCU, c = it % NCU;
+        const int t0 = t % N1, t1 = ND == 3 ? t / N1 : 0;
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < NQF; ++s) {
+          const int s0 = s % NQ1, s1 = ND == 3 ? s / NQ1 : 0;
+          const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1] : c_phi[s0 * N1 + t0];
+          acc = fma(ph, sF[(f * NQF + s) * NCU + c], acc);
+        }
+        sR[c * NB + face_vol_node(lf, t)] += acc;
+      }
+      __syncthreads();
+    }
+  }
+  for (int idx = tid; idx < NCU * NB; idx += NT) {
+    const int a = idx / NCU, c = idx % NCU;
+    P.out[(sz_t)e * NB * NCU + idx] = sR[c * NB + a];
+  }
+}
+
+extern "C" __global__ void __launch_bounds__(NT) nl_residual(const __grid_constant__ NlParams P) {
+  residual_body<false>(P);
+}
+extern "C" __global__ void __launch_bounds__(NT) nl_tangent(const __grid_constant__ NlParams P) {
+  residual_body<true>(P);
+}
+
+// ---------------------------------------------------------------------------
+// mass operator (disc.py:897-948): out = scale * int m(u) v phi, or with
+// EXTRA the (dm/du . du) v term; v in P.q, base u in P.u, du in P.du
+// ---------------------------------------------------------------------------
+constexpr int NVM = MASS_CONST ? NCU : 3 * NCU;   // v (+ u, du)
+constexpr int MSMEM = 2 * (NVM > NCU ? NVM : NCU) * MX;
+
+template <bool EXTRA>
+__device__ __forceinline__ void mass_body(const NlParams& P) {
+  extern __shared__ __align__(16) double smem_m[];
+  double* bA = smem_m;
+  double* bB = smem_m + MSMEM / 2;
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (e >= P.ne) return;
+  constexpr int NL = MASS_CONST ? NCU : (EXTRA ? 3 * NCU : 2 * NCU);   // v (+ u (+ du))
+  for (int idx = tid; idx < NL * NB; idx += NT) {
+    const int v = idx / NB, a = idx % NB;
+    const double* src = v < NCU ? P.q : (v < 2 * NCU ? P.u : P.du);
+    bA[idx] = src[((sz_t)e * NB + a) * NCU + v % NCU];
+  }
+  __syncthreads();
+  double* vq;
+  to_quad(bA, bB, NL, tid, vq);
+  double* fld = vq == bA ? bB : bA;
+  const double detj = P.geo[(sz_t)e * (1 + ND * ND)];
+  for (int p = tid; p < NQ; p += NT) {
+    double m[NCU], dm[NCU];
+    if (MASS_CONST) {
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) { m[c] = c_mass[c]; dm[c] = 0.0; }
+    } else {
+      double xi[ND], x[ND], uq[NCU], duq[NCU];
+      quad_point(p, xi);
+      phys_point(P, e, xi, x);
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) {
+        uq[c] = vq[(NCU + c) * NQ + p];
+        duq[c] = EXTRA ? vq[(2 * NCU + c) * NQ + p] : 0.0;
+      }
+      if (EXTRA) plan_mass_d(x, P.t, uq, nullptr, nullptr, nullptr, duq, nullptr, nullptr, m, dm);
+      else plan_mass(x, P.t, uq, nullptr, nullptr, nullptr, m);
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) flag(P, e, m[c]);
+    }
+    const double wd = c_qw[p] * detj;
+#pragma unroll
+    for (int c = 0; c < NCU; ++c)
+      fld[c * NQ + p] = wd * (EXTRA ? dm[c] : m[c]) * vq[c * NQ + p];
+  }
+  __syncthreads();
+  // phi^T along every axis: reuse from_quad with the source-field selector
+  // (fields indexed >= ND*NCU take phi everywhere): shift by ND*NCU
+  double* other = fld == bA ? bB : bA;
+  auto phi = [](int) { return (int)OP_PHI; };
+  double* res;
+  if (ND == 3) {
+    contract<NQ1, NQ1, NQ1, 0, NQ1, N1, true>(fld, other, NCU, tid, phi);
+    __syncthreads();
+    contract<N1, NQ1, NQ1, 1, NQ1, N1, true>(other, fld, NCU, tid, phi);
+    __syncthreads();
+    contract<N1, N1, NQ1, 2, NQ1, N1, true>(fld, other, NCU, tid, phi);
+    __syncthreads();
+    res = other;
+  } else {
+    contract<NQ1, NQ1, 1, 0, NQ1, N1, true>(fld, other, NCU, tid, phi);
+    __syncthreads();
+    contract<N1, NQ1, 1, 1, NQ1, N1, true>(other, fld, NCU, tid, phi);
+    __syncthreads();
+    res = fld;
+  }
+  for (int idx = tid; idx < NCU * NB; idx += NT) {
+    const int a = idx / NCU, c = idx % NCU;
+    P.out[(sz_t)e * NB * NCU + idx] = P.scale * res[c * NB + a];
+  }
+}
+
+extern "C" __global__ void __launch_bounds__(NT) nl_mass(const __grid_constant__ NlParams P) {
+  mass_body<false>(P);
+}
+extern "C" __global__ void __launch_bounds__(NT) nl_mass_extra(const __grid_constant__ NlParams P) {
+  mass_body<true>(P);
+}
+
+// M^-1 v = detJ^-1 (M1^-1 (x) ... ) v per component (MassPreconditioner.apply)
+extern "C" __global__ void __launch_bounds__(NT) nl_mass_inv(const __grid_constant__ NlParams P) {
+  extern __shared__ __align__(16) double smem_i[];
+  double* bA = smem_i;
+  double* bB = smem_i + NCU * NB;
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (e >= P.ne) return;
+  for (int idx = tid; idx < NCU * NB; idx += NT) {
+    const int v = idx / NB, a = idx % NB;
+    bA[idx] = P.q[((sz_t)e * NB + a) * NCU + v];
+  }
+  __syncthreads();
+  auto mi = [](int) { return (int)OP_M1INV; };
+  double* res;
+  if (ND == 3) {
+    contract<N1, N1, N1, 0, N1, N1, false>(bA, bB, NCU, tid, mi);
+    __syncthreads();
+    contract<N1, N1, N1, 1, N1, N1, false>(bB, bA, NCU, tid, mi);
+    __syncthreads();
+    contract<N1, N1, N1, 2, N1, N1, false>(bA, bB, NCU, tid, mi);
+    __syncthreads();
+    res = bB;
+  } else {
+    contract<N1, N1, 1, 0, N1, N1, false>(bA, bB, NCU, tid, mi);
+    __syncthreads();
+    contract<N1, N1, 1, 1, N1, N1, false>(bB, bA, NCU, tid, mi);
+    __syncthreads();
+    res = bA;
+  }
+  const double inv = P.scale / P.geo[(sz_t)e * (1 + ND * ND)];
+  for (int idx = tid; idx < NCU * NB; idx += NT) {
+    const int a = idx / NCU, c = idx % NCU;
+    P.out[(sz_t)e * NB * NCU + idx] = inv * res[c * NB + a];
+  }
+}

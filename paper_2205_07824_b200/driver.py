@@ -34,7 +34,7 @@ def _steady_fns(system):
         return system.residual_dev(uflat.reshape(shape), 0.0).reshape(-1)
 
     def tangent(uflat, v):
-        return system.tangent_dev(v.reshape(shape)).reshape(-1)
+        return system.tangent_dev(v.reshape(shape), base=uflat.reshape(shape)).reshape(-1)
 
     return residual, tangent
 
@@ -92,7 +92,8 @@ def solve_steady(system, state, newton_options=None, precond=None, callback=None
         return system.residual_dev(uflat.reshape(shape), t).reshape(-1)
 
     def tangent(uflat, v):
-        return system.tangent_dev(v.reshape(shape)).reshape(-1)
+        return system.tangent_dev(v.reshape(shape), base=uflat.reshape(shape),
+                                  t=t).reshape(-1)
 
     import torch
     u0 = state.u if isinstance(state.u, torch.Tensor) else torch.as_tensor(
@@ -209,18 +210,24 @@ class StageSolveError(TimeIntError):
 
 
 def _stage_functions(system, Yk, a_dt, t_stage):
-    """N(U) = M (U - U_k)/(a dt) + R(U, t_i) and its tangent (constant mass,
-    timeint.py:132-165)."""
+    """N(U) = M(U) (U - U_k)/(a dt) + R(U, t_i) and its tangent
+    M(U) dU/(a dt) + (dM/dU dU)(U - U_k)/(a dt) + dR (timeint.py:132-165)."""
     shape = (system.n_elements, system.n_nodes, system.ncu)
     inv = 1.0 / a_dt
 
     def stage_residual(Y):
-        M = system.mass_apply_dev((Y - Yk).reshape(shape), scale=inv)
-        return (M + system.residual_dev(Y.reshape(shape), t_stage)).reshape(-1)
+        Ys = Y.reshape(shape)
+        M = system.mass_apply_dev((Y - Yk).reshape(shape), scale=inv, base=Ys, t=t_stage)
+        return (M + system.residual_dev(Ys, t_stage)).reshape(-1)
 
     def stage_tangent(Y, V):
-        M = system.mass_apply_dev(V.reshape(shape), scale=inv)
-        return (M + system.tangent_dev(V.reshape(shape))).reshape(-1)
+        Ys, Vs = Y.reshape(shape), V.reshape(shape)
+        M = system.mass_apply_dev(Vs, scale=inv, base=Ys, t=t_stage)
+        extra = system.mass_tangent_extra_dev((Y - Yk).reshape(shape), Vs, Ys, t_stage,
+                                              scale=inv)
+        if extra is not None:
+            M = M + extra
+        return (M + system.tangent_dev(Vs, base=Ys, t=t_stage)).reshape(-1)
 
     return stage_residual, stage_tangent
 

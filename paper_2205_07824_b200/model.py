@@ -275,7 +275,52 @@ def _linear_elasticity(nd):
                     init={f"u{i}": "0" for i in range(1, nd + 1)})
 
 
+def _shallow_water(nd):
+    _nd("shallow_water", nd, (2,))
+    flux = ["u2", "u3", "u2*u2/u1 + mu1*u1*u1/2", "u2*u3/u1",
+            "u2*u3/u1", "u3*u3/u1 + mu1*u1*u1/2"]
+    return PdeModel(kind="C", ncu=3, nd=2, nparam=1, mass=["1"] * 3, flux=flux,
+                    source=["0"] * 3, mu=np.array([1.0]),
+                    wavespeed="abs(u2/u1*n1 + u3/u1*n2) + sqrt(mu1*u1)",
+                    init={"u1": "1", "u2": "0", "u3": "0"})
+
+
+def _compressible_ns(nd):
+    """2D compressible Navier-Stokes, kind D (model.py:677-712 restated):
+    gamma = mu1, viscosity = mu2, Prandtl = mu3; q_ij = -d(u_i)/dx_j."""
+    _nd("compressible_ns", nd, (2,))
+    ke = "u2*u2+u3*u3"
+    p = f"(mu1-1)*(u4 - (({ke})/u1)/2)"
+    vel = ("u2/u1", "u3/u1")
+
+    def dv(i, j):            # d(velocity_i)/dx_j from the conserved gradients
+        return f"(({vel[i]})*q1_{j + 1} - q{i + 2}_{j + 1})/u1"
+
+    txx = f"mu2*(4*({dv(0, 0)})/3 - 2*({dv(1, 1)})/3)"
+    tyy = f"mu2*(4*({dv(1, 1)})/3 - 2*({dv(0, 0)})/3)"
+    txy = f"mu2*(({dv(0, 1)}) + ({dv(1, 0)}))"
+    T = f"(u4 - ({ke})/(2*u1))/u1"
+
+    def dT(j):
+        return (f"((({T})*q1_{j} - q4_{j} + (({vel[0]})*q2_{j} + ({vel[1]})*q3_{j}) - "
+                f"(({ke})/(2*u1))/u1*q1_{j})/u1)")
+
+    k = "mu1*mu2/mu3"
+    vx, vy = vel
+    flux = ["u2", "u3",
+            f"u2*({vx}) + {p} - ({txx})", f"u2*({vy}) - ({txy})",
+            f"u3*({vx}) - ({txy})", f"u3*({vy}) + {p} - ({tyy})",
+            f"(u4 + {p})*({vx}) - ({vx})*({txx}) - ({vy})*({txy}) - ({k})*({dT(1)})",
+            f"(u4 + {p})*({vy}) - ({vx})*({txy}) - ({vy})*({tyy}) - ({k})*({dT(2)})"]
+    return PdeModel(kind="D", ncu=4, nd=2, nparam=3, mass=["1"] * 4, flux=flux,
+                    source=["0"] * 4, mu=np.array([1.4, 1e-3, 0.72]),
+                    wavespeed=f"abs({vx}*n1 + {vy}*n2) + sqrt(mu1*({p})/u1)",
+                    init={"u1": "1", "u2": "0", "u3": "0", "u4": "2.5"})
+
+
 _BUILTINS = {
+    "shallow_water": _shallow_water,
+    "compressible_ns": _compressible_ns,
     "poisson": _poisson,
     "convection_diffusion": _convection_diffusion,
     "linear_convection": _linear_convection,

@@ -254,7 +254,8 @@ class PartitionedLdgSystem:
     def residual_dev(self, u, t=0.0, out=None):
         return self.apply(u, False, t, out)
 
-    def tangent_dev(self, du, out=None):
+    def tangent_dev(self, du, out=None, base=None, t=0.0):
+        """Linear fused operator: the tangent reads neither base nor t."""
         return self.apply(du, True, 0.0, out)
 
 

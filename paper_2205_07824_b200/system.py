@@ -22,6 +22,7 @@ import numpy as np
 
 from . import _lib
 from .tables import DenseTables, DiscError, KernelNanError, TensorTables
+from .nonlinear import NlOperator, NlTables, linear_path_reason
 
 __all__ = ["LdgSystem", "SolverState", "DiscError", "KernelNanError"]
 
@@ -94,8 +95,13 @@ class _Disc:
 
 
 class LdgSystem:
-    """The semi-discrete LDG operator on the B200 (tensor quad/hex, kind D,
-    flux linear in (u, q))."""
+    """The semi-discrete LDG operator on the B200.
+
+    Three device paths behind one interface: the fused sum-factorised
+    operator (quad/hex, kind D, flux linear in (u, q) with constant
+    coefficients: ldg_fused.cu), the dense simplex kernels (tri/tet,
+    ldg_dense.cu) and the generated model-specific kernels (quad/hex, kind C
+    or any nonlinear kind-D model: nonlinear.py + ldg_nl.cuh via NVRTC)."""
 
     def __init__(self, model, mesh, topology, master, device=None, tables=None):
         """`tables` (internal): prebuilt host tables, e.g. one partition's
@@ -107,10 +113,17 @@ class LdgSystem:
         if model.nd != mesh.nd:
             raise DiscError(f"model nd={model.nd} but mesh nd={mesh.nd}")
         self.dense = master.kind in ("tri", "tet")
+        self.nl = None
+        self.nl_reason = None if self.dense else linear_path_reason(model)
+        if tables is not None and self.nl_reason is not None:
+            raise DiscError(f"prebuilt (partitioned) tables support linear models only "
+                            f"({self.nl_reason})")
         if tables is not None:
             self.tab = tables
         elif self.dense:
             self.tab = DenseTables(model, mesh, topology, master)
+        elif self.nl_reason is not None:
+            self.tab = NlTables(model, mesh, topology, master)
         else:
             self.tab = TensorTables(model, mesh, topology, master)
         self.lib = _lib.load()
@@ -119,7 +132,12 @@ class LdgSystem:
         self.beta_hat = np.ones(mesh.nd) / np.sqrt(mesh.nd)
         self.bc_groups = self.tab.bc_groups
         self.disc = _Disc(self.tab)
-        self._create_handle()
+        if self.nl_reason is not None:
+            self.nl = NlOperator(self.tab, self.device)
+            self._h = None
+            self._baseq = None
+        else:
+            self._create_handle()
         self._bdata = {}
         self._src = {}
         self._scratch = {}
@@ -279,13 +297,19 @@ class LdgSystem:
         return _lib.stream_ptr()
 
     def _check_nan(self, label):
-        bad = int(self.lib.ldg_last_bad_element(self._h))
+        if self.nl is not None:
+            bad = self.nl.bad_element()
+            self.nl.reset_bad()
+        else:
+            bad = int(self.lib.ldg_last_bad_element(self._h))
         if bad >= 0:
             raise KernelNanError(f"{label} kernel produced non-finite values "
                                  f"(first at element {bad})")
 
     # -- device operators (torch in / torch out, no host sync) ---------------------------
     def mixed_dev(self, u, t=0.0, homogeneous=False, out=None):
+        if self.nl is not None:
+            return self.nl.mixed(u, t, homogeneous, out=out)
         q = out if out is not None else self._empty((self.n_elements, self.n_nodes,
                                                      self.ncu, self.nd))
         g = None if homogeneous else self.boundary_data(t)
@@ -316,7 +340,20 @@ class LdgSystem:
                                               self._stream()), "ldg_operator_pass")
         return R
 
+    def base_mixed(self, u, t=0.0):
+        """q = compute_mixed(u, t) of the tangent's base state, cached per
+        (tensor, version, t): the loop-invariant half of every tangent
+        (disc.py:602)."""
+        if self.kind != "D":
+            return None
+        key = (u.data_ptr(), u._version, tuple(u.shape), float(t))
+        if self._baseq is None or self._baseq[0] != key:
+            self._baseq = (key, self.nl.mixed(u, t))
+        return self._baseq[1]
+
     def residual_dev(self, u, t=0.0, out=None, scratch=None):
+        if self.nl is not None:
+            return self.nl.residual(u, t, q=self.base_mixed(u, t), out=out)
         R = out if out is not None else self._empty(u.shape)
         x = scratch if scratch is not None else self.scratch()
         _lib.check(self.lib.ldg_residual(
@@ -325,7 +362,14 @@ class LdgSystem:
             "ldg_residual")
         return R
 
-    def tangent_dev(self, du, out=None, scratch=None):
+    def tangent_dev(self, du, out=None, scratch=None, base=None, t=0.0):
+        """J(base) du.  The linear fused path ignores `base` and `t` (the
+        tangent of a flux linear in (u, q) does not read them)."""
+        if self.nl is not None:
+            if base is None:
+                raise DiscError("the tangent of a nonlinear model needs the base state")
+            base = base.reshape(du.shape)
+            return self.nl.tangent(base, du, t, q=self.base_mixed(base, t), out=out)
         R = out if out is not None else self._empty(du.shape)
         x = scratch if scratch is not None else self.scratch()
         _lib.check(self.lib.ldg_residual_tangent(self._h, _lib.ptr(du), _lib.ptr(x),
@@ -344,7 +388,10 @@ class LdgSystem:
                    "ldg_flux_from_mixed")
         return R
 
-    def mass_apply_dev(self, v, scale=1.0, out=None):
+    def mass_apply_dev(self, v, scale=1.0, out=None, base=None, t=0.0):
+        if self.nl is not None:
+            return self.nl.mass(v, None if base is None else base.reshape(v.shape), t,
+                                scale, out=out)
         if not self.tab.mass_const:
             raise DiscError("state-dependent mass is not supported on the B200 path")
         o = out if out is not None else self._empty(v.shape)
@@ -352,7 +399,21 @@ class LdgSystem:
                                            self._stream()), "ldg_mass_apply")
         return o
 
+    def mass_tangent_extra_dev(self, y, du, base, t=0.0, scale=1.0, out=None):
+        """(dm/du . du) y (disc.py:927-948); None for a constant mass."""
+        if self.mass_is_constant:
+            return None
+        return self.nl.mass_extra(y, base.reshape(y.shape), du, t, scale, out=out)
+
+    @property
+    def mass_is_constant(self):
+        if self.nl is not None:
+            return bool(self.nl.shape["MASS_CONST"])
+        return bool(getattr(self.tab, "mass_const", True))
+
     def mass_inv_dev(self, v, out=None):
+        if self.nl is not None:
+            return self.nl.mass_inv(v, out=out)
         o = out if out is not None else self._empty(v.shape)
         _lib.check(self.lib.ldg_mass_inv_apply(self._h, _lib.ptr(v), _lib.ptr(o),
                                                self._stream()), "ldg_mass_inv_apply")
@@ -387,25 +448,36 @@ class LdgSystem:
         return self._ret(R, dev), None, None
 
     def residual_tangent(self, state, du, dq=None, dw=None):
-        """disc.py:591-593 (reference linearisation; the base state enters
-        only through nonlinear fluxes, which this path rejects at setup)."""
+        """disc.py:591-593 (the reference linearisation)."""
         dd, dev = self._dev(du)
-        R = self.tangent_dev(dd.reshape(self.n_elements, self.n_nodes, self.ncu))
+        shape = (self.n_elements, self.n_nodes, self.ncu)
+        base = None
+        if self.nl is not None:
+            base = self._dev(state.u)[0].reshape(shape)
+        R = self.tangent_dev(dd.reshape(shape), base=base, t=state.t)
         if dev != "cuda":
             self._check_nan("flux")
         return self._ret(R, dev), None, None
 
     def mass_apply(self, state, vu, vq=None, vw=None):
-        """disc.py:897-925 (constant mass)."""
+        """disc.py:897-925."""
         vd, dev = self._dev(vu)
-        return self._ret(self.mass_apply_dev(vd.reshape(self.n_elements, self.n_nodes,
-                                                        self.ncu)), dev), None, None
+        shape = (self.n_elements, self.n_nodes, self.ncu)
+        base = None if self.mass_is_constant else self._dev(state.u)[0].reshape(shape)
+        M = self.mass_apply_dev(vd.reshape(shape), base=base, t=state.t)
+        if dev != "cuda" and self.nl is not None:
+            self._check_nan("mass")
+        return self._ret(M, dev), None, None
 
     def mass_tangent_extra(self, state, y_u, du, dq=None, dw=None):
-        """disc.py:927-931: zero for constant mass."""
-        if self.tab.mass_const:
+        """disc.py:927-948: None for a constant mass."""
+        if self.mass_is_constant:
             return None
-        raise DiscError("state-dependent mass is not supported on the B200 path")
+        shape = (self.n_elements, self.n_nodes, self.ncu)
+        yd, dev = self._dev(y_u)
+        out = self.mass_tangent_extra_dev(yd.reshape(shape), self._dev(du)[0].reshape(shape),
+                                          self._dev(state.u)[0].reshape(shape), state.t)
+        return self._ret(out, dev)
 
     def interpolate_initial(self):
         """disc.py:420-432 (host evaluation of the init plan at the nodes)."""

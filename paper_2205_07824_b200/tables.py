@@ -180,21 +180,27 @@ def _reference_switch_subset(mesh, master, geom, elems, lfs):
 class TensorTables:
     """Host arrays for the tensor-product (quad/hex) kernels."""
 
-    def __init__(self, model, mesh, topo, master):
+    def __init__(self, model, mesh, topo, master, nonlinear=False):
+        """`nonlinear`: tables for the generated-kernel path (nonlinear.py):
+        any kind C / D model, the state-dependent penalty evaluated on the
+        device; otherwise the linear constant-coefficient fused path."""
         self.model, self.mesh, self.topo, self.master = model, mesh, topo, master
+        self.nonlinear = nonlinear
         kind = master.kind
         if kind != mesh.elem_kind:
             raise DiscError("master element kind does not match the mesh")
         if kind not in ("quad", "hex"):
             raise DiscError(f"B200 tensor path needs quad/hex elements, got {kind}")
-        if model.kind != "D":
-            raise DiscError(f"B200 path supports diffusion (kind D) models, got {model.kind}")
+        if model.kind not in (("C", "D") if nonlinear else ("D",)):
+            raise DiscError(f"B200 path supports kind C/D models, got {model.kind}"
+                            if nonlinear else
+                            f"linear B200 path supports kind D models, got {model.kind}")
         if model.nw > 0 or model.numflux.uhat is not None or model.numflux.fhat is not None:
             raise DiscError("ODE blocks and u^/f^ overrides are not supported on the B200 path")
         self.nd, self.p, self.ncu = mesh.nd, master.p, model.ncu
         self.n1 = master.p + 1
-        if self.n1 > 7 or self.ncu > 3:
-            raise DiscError("tensor path supports p <= 6 and ncu <= 3")
+        if self.n1 > 7 or self.ncu > (5 if nonlinear else 3):
+            raise DiscError("tensor path supports p <= 6 and ncu <= 3 (5 on the generated path)")
         if master.quad_degree < 2 * master.p:
             raise DiscError("tensor path needs quadrature degree >= 2p (exact mass/stiffness)")
         self.nf = 2 * self.nd
@@ -203,7 +209,11 @@ class TensorTables:
         self._check_gll()
         self._operators()
         self._geometry()
-        self._flux_coefficients()
+        if nonlinear:
+            self.flux_uses_u = True
+            self.source_zero = plan_is_zero(model.source_plan())
+        else:
+            self._flux_coefficients()
         self._faces()
 
     # -- reference element -----------------------------------------------------
@@ -340,13 +350,15 @@ class TensorTables:
         # penalty
         tau = float(model.numflux.tau)
         over_h = model.numflux.tau_over_h
-        over_h = True if over_h is None else bool(over_h)      # kind D default
+        over_h = (model.kind == "D") if over_h is None else bool(over_h)   # disc.py:701-705
         fw = self.master.faces[0].weights.sum()
         ws = model.wavespeed_plan()
         mu = model.mu_bindings()
 
         def lam(normals):
-            if ws is None or normals.shape[0] == 0:
+            # constant wavespeed folded into tau (linear path); the generated
+            # path evaluates lambda(u) per face point on the device
+            if ws is None or normals.shape[0] == 0 or self.nonlinear:
                 return 0.0
             b = {"t": 0.0, **mu}
             for k in range(self.nd):
@@ -401,6 +413,8 @@ class TensorTables:
         fb_h = self.elem_vol[eb] / np.maximum(area_b, 1e-300)
         tau_b = (tau / fb_h if over_h else np.full(eb.size, tau)) + lam(nb_)
         self.fb_h = fb_h
+        self.n_left, self.sj_left, self.n_bnd, self.sj_bnd = n_l, area / fw, nb_, area_b / fw
+        self.tau_i, self.tau_b = tau_i, tau_b
         fnbr[eb, fb] = np.arange(eb.size, dtype=np.int32)
         finfo[eb, fb] = kinds
         ftau[eb, fb] = tau_b
@@ -649,7 +663,9 @@ class DenseTables:
         mu = model.mu_bindings()
 
         def lam(normals):
-            if ws is None or normals.shape[0] == 0:
+            # constant wavespeed folded into tau (linear path); the generated
+            # path evaluates lambda(u) per face point on the device
+            if ws is None or normals.shape[0] == 0 or self.nonlinear:
                 return 0.0
             b = {"t": 0.0, **mu}
             for k in range(self.nd):

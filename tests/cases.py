@@ -57,6 +57,71 @@ CASES = {
         numflux=dict(trace="centered", grad_trace="centered", tau=2.5)),
 }
 
+# nonlinear / kind C cases (generated-kernel path, nonlinear.py); "state"
+# gives the base state as constant + amplitude * seeded normal noise so the
+# Euler / Navier-Stokes states stay physical (rho, p > 0)
+NONLIN_DIFF2D = """[model] kind=D ncu=1 nd=2 nw=0 nparam=1
+[mu]
+mu1=0.7
+[mass]
+m1=1 + 0.5*u1*u1
+[flux]
+f1_1=(1 + mu1*u1*u1)*q1_1 + 0.3*u1*abs(u1)
+f1_2=(1 + mu1*u1*u1)*q1_2 - 0.2*max(u1, 0.1)
+[source]
+s1=sin(u1) + x1*x2 - 0.1*pow(2, u1)
+[numflux] trace=switch grad_trace=opposite tau=1.5
+wavespeed=abs(0.3*n1 - 0.2*n2) + 0.1*tanh(u1)
+[bc tag=1 type=dirichlet]
+g1=0.5*x2
+[bc tag=2 type=neumann]
+g1=0.1 + x2
+[bc tag=3 type=dirichlet]
+g1=exp(-x1)
+[bc tag=4 type=dirichlet]
+g1=0.25
+[init]
+u1=0
+"""
+
+NL_CASES = {
+    "euler2d_quad_periodic_p3": dict(
+        model=("builtin", "euler", 2, None), kind="quad", counts=[3, 3], p=3, periodic=2,
+        state=([1.0, 0.2, -0.1, 2.5], 0.05)),
+    "euler2d_quad_dirichlet_p2": dict(
+        model=("builtin", "euler", 2, None), kind="quad", counts=[3, 2], p=2,
+        bcs={t: ("dirichlet", ["1", "0.1*x2", "0.05", "2.6"]) for t in (1, 2, 3, 4)},
+        state=([1.0, 0.1, 0.05, 2.6], 0.05)),
+    "euler3d_hex_periodic_p2": dict(
+        model=("builtin", "euler", 3, None), kind="hex", counts=[2, 2, 2], p=2, periodic=3,
+        state=([1.0, 0.2, -0.1, 0.15, 2.5], 0.05)),
+    "burgers2d_quad_p3": dict(
+        model=("builtin", "burgers", 2, None), kind="quad", counts=[3, 3], p=3,
+        bcs={t: ("dirichlet", ["0.5 + 0.1*x1"]) for t in (1, 2, 3, 4)},
+        state=([0.3], 0.5)),
+    "ns2d_quad_periodic_p3": dict(
+        model=("builtin", "compressible_ns", 2, [1.4, 0.05, 0.72]), kind="quad",
+        counts=[3, 3], p=3, periodic=2, state=([1.0, 0.2, -0.1, 2.5], 0.05)),
+    "ns2d_quad_mixedbc_p2": dict(
+        model=("builtin", "compressible_ns", 2, [1.4, 0.05, 0.72]), kind="quad",
+        counts=[3, 2], p=2,
+        bcs={1: ("dirichlet", ["1", "0.1", "0", "2.5"]),
+             2: ("dirichlet", ["1", "0.1*x2", "0.02", "2.5"]),
+             3: ("neumann", ["0", "0.01", "-0.02", "0.003*x1"]),
+             4: ("dirichlet", ["1.05", "0", "0", "2.55"])},
+        state=([1.0, 0.1, 0.0, 2.5], 0.05)),
+    "ns3d_hex_periodic_p2": dict(
+        model=("file", "ns3d.model"), kind="hex", counts=[2, 2, 2], p=2, periodic=3,
+        state=([1.0, 0.2, -0.1, 0.15, 2.5], 0.05)),
+    "nonlin_diff2d_quad_p2": dict(
+        model=("text", NONLIN_DIFF2D), kind="quad", counts=[3, 3], p=2,
+        state=([0.2], 0.4)),
+    "nonlin_diff2d_quad_centered_p3": dict(
+        model=("text", NONLIN_DIFF2D), kind="quad", counts=[2, 3], p=3,
+        numflux=dict(trace="centered", grad_trace="centered", tau=2.0),
+        state=([0.1], 0.3)),
+}
+
 SOLVE_CASES = {
     # (case name, precond, solver flags)
     "poisson2d_quad_p3_n4_bj": dict(model=("file", "poisson2d.model"), kind="quad",
@@ -77,6 +142,8 @@ def build_case(spec, model_mod, mesh_mod, master_mod):
     src = spec["model"]
     if src[0] == "file":
         model = model_mod.load_model(str(GOLDEN / src[1]))
+    elif src[0] == "text":
+        model = model_mod.parse_model_text(src[1])
     else:
         _, name, nd, mu = src
         model = model_mod.builtin_model(name, nd=nd, mu=mu)
@@ -84,15 +151,20 @@ def build_case(spec, model_mod, mesh_mod, master_mod):
         model.bcs = {t: model_mod.BoundaryCondition(type=ty, data=list(d))
                      for t, (ty, d) in spec["bcs"].items()}
     if "init" in spec:
-        model.init = {"u1": spec["init"]}
+        init = spec["init"]
+        model.init = dict(init) if isinstance(init, dict) else {"u1": init}
         model._plans = {}
     if "numflux" in spec:
         for k, v in spec["numflux"].items():
             setattr(model.numflux, k, v)
     kind = spec["kind"]
     nd = {"quad": 2, "tri": 2, "hex": 3, "tet": 3}[kind]
-    mesh = mesh_mod.generate_structured([(0.0, 1.0)] * nd, spec["counts"], kind)
+    dom = spec.get("domain", (0.0, 1.0))
+    mesh = mesh_mod.generate_structured([tuple(dom)] * nd, spec["counts"], kind)
     per = BOX_PERIODIC[spec["periodic"]] if spec.get("periodic") else None
+    if per is not None and dom != (0.0, 1.0):
+        L = dom[1] - dom[0]
+        per = [(a, b, tuple(L * v for v in vec)) for a, b, vec in per]
     if per is None and not model.bcs and spec.get("periodic") is None:
         pass
     topo = mesh_mod.build_face_topology(mesh, per)
@@ -102,6 +174,15 @@ def build_case(spec, model_mod, mesh_mod, master_mod):
 
 def seeded_state(ne, nb, ncu, seed):
     return np.random.default_rng(seed).normal(size=(ne, nb, ncu))
+
+
+def case_state(spec, ne, nb, ncu, seed):
+    """Base state of a case: seeded normal, or constant + amplitude * normal."""
+    z = seeded_state(ne, nb, ncu, seed)
+    if "state" not in spec:
+        return z
+    base, amp = spec["state"]
+    return np.asarray(base, dtype=float)[None, None, :] + amp * z
 
 
 def b200_setup():

@@ -30,8 +30,8 @@ from ldgkit.driver import _steady_fns, build_pde_block_jacobi  # noqa: E402
 from ldgkit.solver import NewtonOptions  # noqa: E402
 from ldgkit.timeint import solve_steady  # noqa: E402
 
-from cases import (ACCEPT_FLAGS, CASES, SOLVE_CASES, TRANSIENT_CASES,  # noqa: E402
-                   TRANSIENT_FLAGS, build_case, seeded_state)
+from cases import (ACCEPT_FLAGS, CASES, NL_CASES, SOLVE_CASES,  # noqa: E402
+                   TRANSIENT_CASES, TRANSIENT_FLAGS, build_case, case_state, seeded_state)
 
 
 def topo_arrays(sys_):
@@ -60,6 +60,30 @@ def gen_case(name, spec):
     out["mass_inv0"] = s.disc.mass_inv[0]
     np.savez_compressed(HERE / f"{name}.npz", **out)
     print(name, ne * nb * ncu, "dofs", float(np.abs(R).max()), float(np.abs(J).max()))
+
+
+def gen_nl_case(name, spec):
+    """Nonlinear / kind C operator goldens: R(u), J(u)du, compute_mixed,
+    mass_apply and mass_tangent_extra at a physical base state."""
+    model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
+    s = LdgSystem(model, mesh, topo, master)
+    ne, nb, ncu = s.n_elements, s.n_nodes, s.ncu
+    u = case_state(spec, ne, nb, ncu, 1)
+    du = seeded_state(ne, nb, ncu, 0)
+    y = seeded_state(ne, nb, ncu, 2)
+    st = SolverState(u=u, q=None, w=None, t=0.3)
+    out = dict(u=u, du=du, y=y, t=np.array(0.3), R=s.residual(st)[0],
+               Jdu=s.residual_tangent(st, du)[0], M=s.mass_apply(st, y)[0],
+               **topo_arrays(s))
+    ex = s.mass_tangent_extra(st, y, du)
+    if ex is not None:
+        out["Mx"] = ex
+    if s.kind == "D":
+        out["q"] = s.compute_mixed(u, 0.3)
+        out["dq"] = s.compute_mixed(du, 0.3, homogeneous=True)
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, ne * nb * ncu, "dofs", float(np.abs(out["R"]).max()),
+          float(np.abs(out["Jdu"]).max()))
 
 
 def gen_solve(name, spec):
@@ -106,12 +130,18 @@ def gen_transient(name, spec):
 
 
 if __name__ == "__main__":
+    if "--nl-only" in sys.argv:
+        for n, sp in NL_CASES.items():
+            gen_nl_case(n, sp)
+        sys.exit(0)
     if "--transient-only" in sys.argv:
         for n, sp in TRANSIENT_CASES.items():
             gen_transient(n, sp)
         sys.exit(0)
     for n, sp in CASES.items():
         gen_case(n, sp)
+    for n, sp in NL_CASES.items():
+        gen_nl_case(n, sp)
     for n, sp in SOLVE_CASES.items():
         gen_solve(n, sp)
     for n, sp in TRANSIENT_CASES.items():

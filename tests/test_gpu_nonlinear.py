@@ -1,0 +1,115 @@
+"""Generated-kernel path (nonlinear.py + csrc/ldg_nl.cuh via NVRTC) on the
+B200 against reference golden vectors and the oracle.
+
+Bar (BASELINE.json north_star): residual vectors to 1e-12 relative L2 in
+fp64.  Cases: kind C Euler / Burgers with the LLF flux (interior, periodic
+and Dirichlet ghost states), kind D compressible Navier-Stokes (2D builtin,
+3D user model file) with Dirichlet / Neumann / periodic faces, and a
+nonlinear diffusion model with state-dependent source and mass, abs / max /
+pow / tanh subgradient rules, switch and centered traces."""
+
+import numpy as np
+import pytest
+
+from cases import GOLDEN, NL_CASES, b200_setup, build_case, case_state
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def system_for(spec):
+    from paper_2205_07824_b200.system import LdgSystem
+    return LdgSystem(*build_case(spec, *b200_setup()))
+
+
+@pytest.mark.parametrize("name", sorted(NL_CASES))
+def test_generated_path_vs_reference_golden(name):
+    from paper_2205_07824_b200.system import SolverState
+    g = np.load(GOLDEN / f"{name}.npz")
+    s = system_for(NL_CASES[name])
+    assert s.nl is not None, "expected the generated-kernel path"
+    assert np.array_equal(s.fi_switch, g["switch"])
+    t = float(g["t"])
+    st = SolverState(u=g["u"], q=None, w=None, t=t)
+    R = s.residual(st)[0]
+    J = s.residual_tangent(st, g["du"])[0]
+    assert rel(R, g["R"]) < TOL, rel(R, g["R"])
+    assert rel(J, g["Jdu"]) < TOL, rel(J, g["Jdu"])
+    assert rel(s.mass_apply(st, g["y"])[0], g["M"]) < TOL
+    if "Mx" in g:
+        assert rel(s.mass_tangent_extra(st, g["y"], g["du"]), g["Mx"]) < TOL
+    else:
+        assert s.mass_tangent_extra(st, g["y"], g["du"]) is None
+    if "q" in g:
+        assert rel(s.compute_mixed(g["u"], t), g["q"]) < TOL
+        assert rel(s.compute_mixed(g["du"], t, homogeneous=True), g["dq"]) < TOL
+
+
+@pytest.mark.parametrize("name,counts,p", [
+    ("euler2d_quad_periodic_p3", [7, 5], 4),
+    ("ns2d_quad_mixedbc_p2", [5, 6], 3),
+    ("ns3d_hex_periodic_p2", [3, 3, 2], 3),
+    ("euler3d_hex_periodic_p2", [3, 2, 3], 3),
+    ("nonlin_diff2d_quad_p2", [6, 5], 5),
+])
+def test_generated_path_vs_oracle_larger(name, counts, p):
+    from oracle import make_oracle
+    from paper_2205_07824_b200.system import SolverState
+    spec = dict(NL_CASES[name], counts=counts, p=p)
+    model, mesh, topo, master = build_case(spec, *b200_setup())
+    from paper_2205_07824_b200.system import LdgSystem
+    s = LdgSystem(model, mesh, topo, master)
+    o = make_oracle(model, mesh, topo, master)
+    ne, nb, ncu = s.n_elements, s.n_nodes, s.ncu
+    u = case_state(spec, ne, nb, ncu, 5)
+    du = np.random.default_rng(6).normal(size=u.shape)
+    st = SolverState(u=u, q=None, w=None, t=0.1)
+    assert rel(s.residual(st)[0], o.residual(u, 0.1)) < TOL
+    assert rel(s.residual_tangent(st, du)[0], o.residual_tangent(u, du, 0.1)) < TOL
+
+
+def test_tangent_matches_central_difference():
+    """disc.py tangent vs central FD of the residual (test_disc.py:320-369
+    bar 3e-6) on the 3D Navier-Stokes model.  The reference linearisation
+    freezes the wavespeed penalty (disc.py:694-698), so the comparison drops
+    the wavespeed to make the tangent the exact derivative."""
+    import torch
+    from paper_2205_07824_b200.system import LdgSystem, SolverState
+    spec = NL_CASES["ns3d_hex_periodic_p2"]
+    model, mesh, topo, master = build_case(spec, *b200_setup())
+    model.wavespeed = None
+    model._plans = {}
+    s = LdgSystem(model, mesh, topo, master)
+    u = case_state(spec, s.n_elements, s.n_nodes, s.ncu, 3)
+    du = np.random.default_rng(4).normal(size=u.shape)
+    J = s.residual_tangent(SolverState(u=u, q=None, w=None, t=0.0), du)[0]
+    h = 1e-6
+    Rp = s.residual(SolverState(u=u + h * du, q=None, w=None, t=0.0))[0]
+    Rm = s.residual(SolverState(u=u - h * du, q=None, w=None, t=0.0))[0]
+    assert rel((Rp - Rm) / (2 * h), J) < 3e-6
+    # device-resident closures give the same numbers
+    ud = torch.as_tensor(u, device="cuda")
+    Jd = s.tangent_dev(torch.as_tensor(du, device="cuda"), base=ud).cpu().numpy()
+    assert rel(Jd, J) < 1e-15
+
+
+def test_nonfinite_state_raises_kernel_nan():
+    from paper_2205_07824_b200.system import KernelNanError, SolverState
+    spec = NL_CASES["euler2d_quad_periodic_p3"]
+    s = system_for(spec)
+    u = case_state(spec, s.n_elements, s.n_nodes, s.ncu, 1)
+    u[4, 2, 0] = -1.0            # negative density -> sqrt of a negative pressure ratio
+    with pytest.raises(KernelNanError, match="non-finite values"):
+        s.residual(SolverState(u=u, q=None, w=None, t=0.0))
+
+
+def test_generated_kernels_do_not_spill():
+    s = system_for(NL_CASES["ns3d_hex_periodic_p2"])
+    for k in ("nl_mixed", "nl_residual", "nl_tangent", "nl_mass", "nl_mass_inv"):
+        a = s.nl.kernel_attrs(k)
+        assert a["regs"] > 0
+        print(k, a)
