@@ -130,6 +130,10 @@ SOLVE_CASES = {
                                     counts=[4, 4], p=3, precond="identity"),
     "poisson3d_hex_p3_n2_bj": dict(model=("file", "poisson3d.model"), kind="hex",
                                    counts=[2, 2, 2], p=3, precond="block_jacobi"),
+    # nonlinear steady solve (Newton > 1 iteration, line search, nonlinear tangent)
+    "nonlin_diff2d_quad_p3_n3_bj": dict(model=("text", NONLIN_DIFF2D.replace(
+        "m1=1 + 0.5*u1*u1", "m1=0")), kind="quad", counts=[3, 3], p=3,
+        precond="block_jacobi"),
 }
 
 # acceptance solver flags (test_acceptance.py:69-81)
@@ -201,5 +205,31 @@ TRANSIENT_CASES = {
         counts=[4, 4, 4], p=2, periodic=3, init="cos(2*pi*x1)*sin(2*pi*x3)",
         stages=1, order=1, dt=0.01, steps=2, precond="mass"),
 }
+
+# config 2 / config 4 shapes on the generated-kernel path (nonlinear.py)
+_T = "(1 - (0.4*25/(8*1.4*pi^2))*exp(1 - ((x1-5)^2 + (x2-5)^2)))"
+_VX = "(1 - 5/(2*pi)*exp((1 - ((x1-5)^2 + (x2-5)^2))/2)*(x2-5))"
+_VY = "(5/(2*pi)*exp((1 - ((x1-5)^2 + (x2-5)^2))/2)*(x1-5))"
+VORTEX_INIT = {"u1": f"{_T}^2.5", "u2": f"{_T}^2.5*{_VX}", "u3": f"{_T}^2.5*{_VY}",
+               "u4": f"{_T}^3.5/0.4 + 0.5*{_T}^2.5*({_VX}^2 + {_VY}^2)"}
+_U, _V = "sin(x1)*cos(x2)*cos(x3)", "(-cos(x1)*sin(x2)*cos(x3))"
+TGV_INIT = {"u1": "1", "u2": _U, "u3": _V, "u4": "0",
+            "u5": f"(10 + (cos(2*x1) + cos(2*x2))*(cos(2*x3) + 2)/16)/0.4 + "
+                  f"0.5*(({_U})^2 + ({_V})^2)"}
+
+TRANSIENT_CASES.update({
+    "euler2d_vortex_quad_p3_dirk22": dict(
+        model=("builtin", "euler", 2, None), kind="quad", counts=[4, 4], p=3, periodic=2,
+        domain=(0.0, 10.0), init=VORTEX_INIT, stages=2, order=2, dt=0.05, steps=2,
+        precond="mass"),
+    # the reference's transient block-Jacobi (spatial Jacobian at t = 0, no
+    # M/dt term, driver.py:270-274) does not converge GMRES on this flow for
+    # any dt tried (0.05 .. 10); the step uses the mass preconditioner and the
+    # block-Jacobi build + apply is pinned separately ("bj_apply")
+    "ns3d_tgv_hex_p2_dirk11": dict(
+        model=("file", "ns3d.model"), kind="hex", counts=[2, 2, 2], p=2, periodic=3,
+        domain=(0.0, 2 * np.pi), init=TGV_INIT, stages=1, order=1, dt=0.05, steps=1,
+        precond="mass", bj_apply=True),
+})
 
 TRANSIENT_FLAGS = dict(abs_tol=1e-10, rel_tol=1e-9, forcing=None, restart=60, gmres_max_iter=600)

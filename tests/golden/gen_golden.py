@@ -117,15 +117,30 @@ def gen_transient(name, spec):
                          forcing=f["forcing"], gmres_restart=f["restart"],
                          gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent")
     tab = dirk_tableau(spec["stages"], spec["order"])
-    M = MassPreconditioner(s)
+    if spec["precond"] == "block_jacobi":
+        # transient block-Jacobi: built once at t = 0 from the steady
+        # closures (driver.py:270-274)
+        rf, tf = _steady_fns(s)
+        M = build_pde_block_jacobi(s, rf, tf, s.pack(st.u), "tangent")
+    else:
+        M = MassPreconditioner(s)
     newton, gm = [], []
     u0 = st.u.copy()
     for _ in range(spec["steps"]):
         st, stats = advance_step(s, st, spec["dt"], tab, opts, precond=M)
         newton.append(stats.newton_iters)
         gm.append(stats.gmres_iters)
+    extra = {}
+    if spec.get("bj_apply"):
+        # block-Jacobi of the steady closures at the initial state, applied
+        # to a seeded vector (solver.py:291-346, driver.py:109-142)
+        s0 = s.interpolate_initial()
+        rf, tf = _steady_fns(s)
+        bj = build_pde_block_jacobi(s, rf, tf, s.pack(s0.u), "tangent")
+        r = np.random.default_rng(9).normal(size=s.n_dofs)
+        extra = dict(bj_r=r, bj_z=bj.apply(r))
     np.savez_compressed(HERE / f"transient_{name}.npz", u0=u0, u=st.u, t=np.array(st.t),
-                        newton=np.array(newton), gmres=np.array(gm))
+                        newton=np.array(newton), gmres=np.array(gm), **extra)
     print("transient", name, newton, gm, float(np.abs(st.u).max()))
 
 
@@ -136,7 +151,15 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--transient-only" in sys.argv:
         for n, sp in TRANSIENT_CASES.items():
+            if len(sys.argv) > 2 and n not in sys.argv:
+                continue
             gen_transient(n, sp)
+        sys.exit(0)
+    if "--solve-only" in sys.argv:
+        for n, sp in SOLVE_CASES.items():
+            if len(sys.argv) > 2 and n not in sys.argv:
+                continue
+            gen_solve(n, sp)
         sys.exit(0)
     for n, sp in CASES.items():
         gen_case(n, sp)

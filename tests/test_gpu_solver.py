@@ -126,10 +126,13 @@ def test_criterion7_known_answer_tri(precond, want):
     assert abs(stats.total_gmres_iters - want) <= 1, stats.gmres_iters
 
 
-@pytest.mark.parametrize("name", ["convdiff2d_quad_p3_dirk22", "convdiff3d_hex_p2_dirk11"])
+@pytest.mark.parametrize("name", ["convdiff2d_quad_p3_dirk22", "convdiff3d_hex_p2_dirk11",
+                                  "euler2d_vortex_quad_p3_dirk22", "ns3d_tgv_hex_p2_dirk11"])
 def test_dirk_transient_matches_reference(name):
     """Device advance_step (timeint.py:168-207) with the mass preconditioner
-    vs the reference's own transient run (golden)."""
+    vs the reference's own transient run (golden): linear conv-diff on the
+    fused path, Euler isentropic vortex (config 2 shape) and 3D Navier-Stokes
+    Taylor-Green (config 4 shape) on the generated-kernel path."""
     from cases import TRANSIENT_CASES, TRANSIENT_FLAGS
     from paper_2205_07824_b200.driver import MassPreconditioner, advance_step, dirk_tableau
     from paper_2205_07824_b200.solver import NewtonOptions
@@ -154,3 +157,21 @@ def test_dirk_transient_matches_reference(name):
     assert newton == g["newton"].tolist()
     assert all(abs(a - b) <= 1 + 0.02 * b for a, b in zip(gm, g["gmres"].tolist())), (gm, g["gmres"])
     assert rel(st.u.cpu().numpy(), g["u"]) < 1e-9
+
+
+def test_transient_block_jacobi_apply_matches_reference_ns3d():
+    """Block-Jacobi of the steady closures at the initial Taylor-Green state
+    (driver.py:270-274, solver.py:303-346): 8 periodic hex p=2 elements, 5
+    components, 135 x 135 blocks, applied to a seeded vector vs the
+    reference's own build + lu_solve."""
+    import torch
+    from cases import TRANSIENT_CASES
+    from paper_2205_07824_b200.driver import _steady_fns, build_pde_block_jacobi
+    from paper_2205_07824_b200.system import LdgSystem
+    g = np.load(GOLDEN / "transient_ns3d_tgv_hex_p2_dirk11.npz")
+    s = LdgSystem(*build_case(TRANSIENT_CASES["ns3d_tgv_hex_p2_dirk11"], *b200_setup()))
+    u0 = torch.as_tensor(s.interpolate_initial().u, device="cuda").reshape(-1)
+    rf, tf = _steady_fns(s)
+    M = build_pde_block_jacobi(s, rf, tf, u0)
+    z = M.apply(torch.as_tensor(g["bj_r"], device="cuda")).cpu().numpy()
+    assert rel(z, g["bj_z"]) < 1e-9, rel(z, g["bj_z"])
