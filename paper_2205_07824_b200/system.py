@@ -346,9 +346,12 @@ class LdgSystem:
         (disc.py:602)."""
         if self.kind != "D":
             return None
+        # the cache holds the base tensor itself, so its storage cannot be
+        # recycled by the allocator for another state with the same address;
+        # views of one storage share the version counter
         key = (u.data_ptr(), u._version, tuple(u.shape), float(t))
         if self._baseq is None or self._baseq[0] != key:
-            self._baseq = (key, self.nl.mixed(u, t))
+            self._baseq = (key, self.nl.mixed(u, t), u)
         return self._baseq[1]
 
     def residual_dev(self, u, t=0.0, out=None, scratch=None):
