@@ -3,6 +3,7 @@
 
 #include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -167,6 +168,10 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   P.n_maps = t->n_maps;
   P.geo = h->geo; P.fnbr = h->fnbr; P.finfo = h->finfo; P.ftau = h->ftau;
   P.nmap = h->nmap; P.bad = h->bad; P.frec = h->frec; P.kco = h->kco; P.kstride = h->kstride;
+  {
+    const char* v = getenv("LDG_PASS1_VARIANT");    // "pencil" forces the v9 kernel (A/B timing)
+    P.variant = (v && strcmp(v, "pencil") == 0) ? 1 : 0;
+  }
   const int n1 = t->n1;
   // tables arrive with row stride n1 packed at the front of each array
   memcpy(P.d1, t->d1, sizeof(P.d1));

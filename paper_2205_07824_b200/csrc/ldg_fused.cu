@@ -593,6 +593,436 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
 }
 
 // --------------------------------------------------------------------------
+// pass 1, plane mapping (hex, ncu = 1, p = 3): the shared-memory-lean variant
+// --------------------------------------------------------------------------
+//
+// The pencil kernel above moves every 1D contraction to the owner of the
+// pencil along its axis, which costs a shared-memory transpose per stage
+// (~25 KB of shared traffic per element; ncu: L1 92% busy, HBM 22%).  Here
+// thread k of an element (4 consecutive lanes) owns the z-plane k (16 nodes,
+// registers): x and y contractions, the x/y face work and the flux
+// combination are all in registers, and only two exchanges cross planes:
+//   1. u planes (+ the z-face jumps) for d/dz and the z lifts,
+//   2. the in-plane partial volume terms T1 = -(S_x M_y F_x + M_x S_y F_y)
+//      + x/y face lifts, T2 = -M_x M_y F_z, contracted along z:
+//      R_k = sum_m M[k][m] T1_m + S[k][m] T2_m  (+ z-face lifts on k = 0, 3).
+// A warp owns 8 consecutive elements (4 KB of u, 4 KB of R): u and the
+// neighbour face values arrive by cp.async straight into shared memory
+// (coalesced 256 B rows; no register staging, no dependence stalls until
+// first use) and R leaves through shared memory as coalesced rows.  The four
+// threads of an element sit in one warp, so exchanges use __syncwarp only.
+// Outputs and arithmetic identities are those of fused_kernel.
+
+namespace {
+constexpr int kPlaneBlock = 128;
+constexpr int kPlaneEpb = kPlaneBlock / 4;
+constexpr int kPS = 17;                      // padded plane stride (doubles)
+constexpr int kES = 5;                       // padded stride of a thread's 4 face values
+// per-element shared region (doubles):
+//   [0, 68)    u planes (stride 17), later T1, later the R staging
+//   [68, 108)  z-face jumps  [face][row j][i] (row stride 5)
+//   [108, 148) z-face fluxes [face][row j][i]
+//   [148, 216) T2 planes (stride 17)
+//   [216, 232) the element's coefficient block C | Cu (cp.async)
+// The thread-private x/y face fluxes live in the thread's own u-plane slot
+// between the u exchange and the T1 store.
+// element stride = 4 (mod 16) doubles so the 8 elements of a warp spread
+// over the banks
+constexpr int kOffJ = 4 * kPS, kOffF = kOffJ + 40, kOffE = kOffF + 40, kOffC = kOffE + 4 * kPS;
+constexpr int kPlanePer = 244;
+static_assert(kOffC + 16 <= kPlanePer, "layout");
+static_assert(kPlanePer % 16 == 4, "element stride must be 4 mod 16 doubles");
+constexpr int kPlaneMaps = 16;               // node maps cached in shared memory
+}  // namespace
+
+// a[k * 4 + m] for a lane-dependent k without dynamically indexing the
+// parameter bank (which would copy the parameter block to local memory)
+__device__ __forceinline__ double sel4(const double* a, int k, int m) {
+  const double v0 = a[m], v1 = a[4 + m], v2 = a[8 + m], v3 = a[12 + m];
+  return k == 0 ? v0 : (k == 1 ? v1 : (k == 2 ? v2 : v3));
+}
+__device__ __forceinline__ double sel1(const double* a, int k) {
+  return k == 0 ? a[0] : (k == 1 ? a[1] : (k == 2 ? a[2] : a[3]));
+}
+
+#ifndef LDG_PLANE_MINB
+#define LDG_PLANE_MINB 3          // 3 blocks (12 warps) per SM: <= 168 registers
+#endif
+
+template <bool TANGENT, bool HAS_CU>
+__global__ void __launch_bounds__(kPlaneBlock, LDG_PLANE_MINB)
+plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+             const double* __restrict__ u, const double* __restrict__ gproj,
+             const double* __restrict__ bsrc, double* __restrict__ R,
+             double* __restrict__ X) {
+  constexpr int N1 = 4, NP = 16, NB = 64;
+  extern __shared__ __align__(16) double psm[];
+  __shared__ int s_map[kPlaneMaps * NP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = threadIdx.x >> 2, k = threadIdx.x & 3;
+  const int e = blockIdx.x * kPlaneEpb + slot;
+  const int e_w = blockIdx.x * kPlaneEpb + warp * 8;       // first element of the warp
+  const bool active = e < P.ne;
+  double* sEl = psm + slot * kPlanePer;
+  double* sU = sEl;
+  double* sJZ = sEl + kOffJ;
+  double* sFZ = sEl + kOffF;
+  double* sT2 = sEl + kOffE;
+  double* sC = sEl + kOffC;
+  double* sXY = sU + k * kPS;                              // this thread's slot
+  double* sW = psm + warp * 8 * kPlanePer;                 // the warp's 8 elements
+
+  const bool map_smem = P.n_maps <= kPlaneMaps;
+  if (map_smem)
+    for (int x = threadIdx.x; x < P.n_maps * NP; x += kPlaneBlock) s_map[x] = __ldg(P.nmap + x);
+
+  // ---- A: u rows (coalesced, cp.async), records, coefficients, gathers
+  {
+    const int nval = min(8, P.ne - e_w) * NB;              // doubles of this warp
+    const double* ub = u + (size_t)e_w * NB;
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+      const int d = lane + 32 * x;                         // element d/64, plane, node
+      if (d < nval)
+        cp_async8(sW + (d >> 6) * kPlanePer + ((d >> 4) & 3) * kPS + (d & 15), ub + d);
+    }
+  }
+  double tau[6];
+  int info[6];
+  double ext[6][N1];                                       // neighbour / boundary face values
+  __syncthreads();                                         // s_map ready (uniform)
+  if (active) {
+    int nbr[6];
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(frec + (size_t)e * 6 + lf));
+      tau[lf] = v.x;
+      const int2 w = *reinterpret_cast<const int2*>(&v.y);
+      nbr[lf] = w.x;
+      info[lf] = w.y;
+    }
+    const double* kb = P.kco + (size_t)e * P.kstride;
+#pragma unroll
+    for (int x = 0; x < 3; ++x) cp_async8(sC + 3 * k + x, kb + 3 * k + x);   // C (9) + Cu (3)
+    // face node t of this thread's 4 values: x faces (j,k) -> j + 4k; y faces
+    // (i,k) -> i + 4k; z faces, row j = k: (i,k) -> i + 4k.  A run of 4
+    // consecutive, 32-B aligned neighbour nodes is fetched with 2 x 16 B loads.
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf) {
+      const int kind = info[lf] & LDG_FACE_KIND_MASK;
+#pragma unroll
+      for (int a = 0; a < N1; ++a) ext[lf][a] = 0.0;
+      if (kind == LDG_FACE_INTERIOR) {
+        if (info[lf] & LDG_FL_UNBR) {
+          const int mid = (info[lf] >> LDG_FACE_MAP_SHIFT) & 0xffff;
+          const double* base = u + (size_t)nbr[lf] * NB;
+          int nn[N1];
+#pragma unroll
+          for (int a = 0; a < N1; ++a)
+            nn[a] = map_smem ? s_map[mid * NP + a + 4 * k] : __ldg(P.nmap + mid * NP + a + 4 * k);
+          if (nn[1] == nn[0] + 1 && nn[2] == nn[0] + 2 && nn[3] == nn[0] + 3 && (nn[0] & 3) == 0) {
+            const double2* b2 = reinterpret_cast<const double2*>(base + nn[0]);
+            const double2 v0 = __ldg(b2), v1 = __ldg(b2 + 1);
+            ext[lf][0] = v0.x; ext[lf][1] = v0.y; ext[lf][2] = v1.x; ext[lf][3] = v1.y;
+          } else {
+#pragma unroll
+            for (int a = 0; a < N1; ++a) ext[lf][a] = __ldg(base + nn[a]);
+          }
+        }
+      } else if (!TANGENT && gproj) {
+        const double2* b2 = reinterpret_cast<const double2*>(gproj + (size_t)nbr[lf] * NP + 4 * k);
+        const double2 v0 = __ldg(b2), v1 = __ldg(b2 + 1);
+        ext[lf][0] = v0.x; ext[lf][1] = v0.y; ext[lf][2] = v1.x; ext[lf][3] = v1.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf) {
+      tau[lf] = 0.0;
+      info[lf] = LDG_FACE_NEUMANN;
+#pragma unroll
+      for (int a = 0; a < N1; ++a) ext[lf][a] = 0.0;
+    }
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncwarp();
+  // idle lanes (past the last element) run on with zero data so that every
+  // __syncwarp() below is reached by the whole warp
+
+  // ---- B: d/dz from all four planes; z-face jumps / own-data flux, row j = k
+  double up[NP], hz[NP];
+#pragma unroll
+  for (int n = 0; n < NP; ++n) {
+    up[n] = sU[k * kPS + n];
+    hz[n] = 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    const double dkm = sel4(P.d1, k, m);
+#pragma unroll
+    for (int n = 0; n < NP; ++n) hz[n] = fma(dkm, sU[m * kPS + n], hz[n]);
+  }
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {                 // faces 0 (z-, plane 0), 1 (z+, plane 3)
+    const int kind = info[f] & LDG_FACE_KIND_MASK;
+    const int acode = (info[f] >> LDG_FL_ALPHA_SHIFT) & 3;
+    const double alpha = acode == 1 ? 1.0 : (acode == 2 ? 0.5 : 0.0);
+    const bool neu = kind == LDG_FACE_NEUMANN;
+    const double sgn = f ? 1.0 : -1.0;
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      const double uo = sU[(f ? 3 : 0) * kPS + i + 4 * k];
+      const double ex = ext[f][i];
+      const double d = uo - ex;
+      const double jmp = alpha * d;
+      double fh = tau[f] * (neu ? ex : d);
+      if (HAS_CU && !neu) fh = fma(sgn * sC[11], uo - jmp, fh);
+      sJZ[f * 20 + k * kES + i] = jmp;
+      sFZ[f * 20 + k * kES + i] = fh;
+    }
+  }
+  __syncwarp();
+  double h[3][NP];                               // h_x, h_y, h_z of the plane
+  {
+    const double clk = sel1(P.clo, k), chk = sel1(P.chi, k);
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+      h[2][n] = -hz[n] - clk * sJZ[(n >> 2) * kES + (n & 3)] + chk * sJZ[20 + (n >> 2) * kES + (n & 3)];
+  }
+  // ---- C: x / y faces at this plane and the in-plane gradients; the
+  // own-data face fluxes go to the thread's (now dead) u-plane slot
+  // sXY[(s * 2 + ax) * 4 + a]; the jumps are recomputed where they are lifted
+  double alx[2], aly[2];                         // jump coefficients of the x / y faces
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+      const int lf = ax == 0 ? 4 + s : 2 + s;
+      const int kind = info[lf] & LDG_FACE_KIND_MASK;
+      const int acode = (info[lf] >> LDG_FL_ALPHA_SHIFT) & 3;
+      const double alpha = acode == 1 ? 1.0 : (acode == 2 ? 0.5 : 0.0);
+      if (ax == 0) alx[s] = alpha;
+      else aly[s] = alpha;
+      const bool neu = kind == LDG_FACE_NEUMANN;
+      const double sgn = s ? 1.0 : -1.0;
+#pragma unroll
+      for (int a = 0; a < N1; ++a) {
+        // x face: node (s ? 3 : 0, a, k); y face: node (a, s ? 3 : 0, k)
+        const double uo = ax == 0 ? up[(s ? 3 : 0) + 4 * a] : up[a + 4 * (s ? 3 : 0)];
+        const double ex = ext[lf][a];
+        const double d = uo - ex;
+        double fh = tau[lf] * (neu ? ex : d);
+        if (HAS_CU && !neu) fh = fma(sgn * sC[9 + ax], uo - alpha * d, fh);
+        sXY[(s * 2 + ax) * 4 + a] = fh;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < N1; ++j) {
+    const double jxl = alx[0] * (up[4 * j] - ext[4][j]);
+    const double jxh = alx[1] * (up[3 + 4 * j] - ext[5][j]);
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double vx = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) vx = fma(P.d1[i * N1 + m], up[m + 4 * j], vx);
+      h[0][i + 4 * j] = -vx - P.clo[i] * jxl + P.chi[i] * jxh;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N1; ++i) {
+    const double jyl = aly[0] * (up[i] - ext[2][i]);
+    const double jyh = aly[1] * (up[i + 12] - ext[3][i]);
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {
+      double vy = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) vy = fma(P.d1[j * N1 + m], up[i + 4 * m], vy);
+      h[1][i + 4 * j] = -vy - P.clo[j] * jyl + P.chi[j] * jyh;
+    }
+  }
+
+  // ---- D: flux density F^q = C h (in place), face exports and the q^ own
+  // share of the face fluxes, then F = F^q + Cu u
+#pragma unroll
+  for (int n = 0; n < NP; ++n) {
+    const double h0 = h[0][n], h1 = h[1][n], h2 = h[2][n];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) h[r][n] = fma(sC[3 * r], h0, fma(sC[3 * r + 1], h1, sC[3 * r + 2] * h2));
+  }
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+      const int lf = ax == 0 ? 4 + s : 2 + s;
+      const int kind = info[lf] & LDG_FACE_KIND_MASK;
+      if (kind == LDG_FACE_NEUMANN) continue;
+      const bool exp_ = (info[lf] & LDG_FL_EXPORT) && active;
+      const double w_own = kind != LDG_FACE_INTERIOR ? 1.0
+                           : ((info[lf] & LDG_FL_QOWN) ? 1.0 : ((info[lf] & LDG_FL_QHALF) ? 0.5 : 0.0));
+      const double sgn = s ? 1.0 : -1.0;
+      double xv[N1];
+#pragma unroll
+      for (int a = 0; a < N1; ++a) {
+        const int n = ax == 0 ? (s ? 3 : 0) + 4 * a : a + 4 * (s ? 3 : 0);
+        xv[a] = sgn * h[ax][n];
+        sXY[(s * 2 + ax) * 4 + a] = fma(w_own, xv[a], sXY[(s * 2 + ax) * 4 + a]);
+      }
+      if (exp_) {
+        double2* xp = reinterpret_cast<double2*>(X + ((size_t)e * 6 + lf) * NP + 4 * k);
+        xp[0] = make_double2(xv[0], xv[1]);
+        xp[1] = make_double2(xv[2], xv[3]);
+      }
+    }
+  if (k == 0 || k == 3) {                        // z face of this plane
+    const int f = k == 3;
+    const int inf = f ? info[1] : info[0];
+    const int kind = inf & LDG_FACE_KIND_MASK;
+    if (kind != LDG_FACE_NEUMANN) {
+      const bool exp_ = (inf & LDG_FL_EXPORT) && active;
+      const double w_own = kind != LDG_FACE_INTERIOR ? 1.0
+                           : ((inf & LDG_FL_QOWN) ? 1.0 : ((inf & LDG_FL_QHALF) ? 0.5 : 0.0));
+      const double sgn = f ? 1.0 : -1.0;
+      double2* xp = reinterpret_cast<double2*>(X + ((size_t)e * 6 + f) * NP);
+#pragma unroll
+      for (int n = 0; n < NP; n += 2) {
+        const double x0 = sgn * h[2][n], x1 = sgn * h[2][n + 1];
+        double* z0 = sFZ + f * 20 + (n >> 2) * kES + (n & 3);
+        z0[0] = fma(w_own, x0, z0[0]);
+        z0[1] = fma(w_own, x1, z0[1]);
+        if (exp_) xp[n / 2] = make_double2(x0, x1);
+      }
+    }
+  }
+  if (HAS_CU) {
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) h[r][n] = fma(sC[9 + r], up[n], h[r][n]);
+  }
+
+  // ---- E: in-plane volume partials and x / y lifts, in place; T2 goes to
+  // shared memory as soon as it is formed (its region is not read before)
+  {
+    double (&F)[3][NP] = h;
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {               // M_y F_z, M_y F_x, S_y F_y along column i
+      double a1[N1], b1[N1], c1[N1];
+#pragma unroll
+      for (int j = 0; j < N1; ++j) {
+        double x1 = 0.0, x2 = 0.0, x3 = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          x1 = fma(P.m1[j * N1 + m], F[0][i + 4 * m], x1);
+          x2 = fma(P.s1[j * N1 + m], F[1][i + 4 * m], x2);
+          x3 = fma(P.m1[j * N1 + m], F[2][i + 4 * m], x3);
+        }
+        a1[j] = x1;
+        b1[j] = x2;
+        c1[j] = x3;
+      }
+#pragma unroll
+      for (int j = 0; j < N1; ++j) {
+        F[0][i + 4 * j] = a1[j];
+        F[1][i + 4 * j] = b1[j];
+        F[2][i + 4 * j] = c1[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {               // along x, row j
+      double g1[N1];
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double x1 = 0.0, x2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          x1 = fma(P.s1[i * N1 + m], F[0][m + 4 * j], x1);
+          x1 = fma(P.m1[i * N1 + m], F[1][m + 4 * j], x1);
+          x2 = fma(P.m1[i * N1 + m], F[2][m + 4 * j], x2);
+        }
+        g1[i] = x1;
+        sT2[k * kPS + i + 4 * j] = -x2;          // T2 = -M_x M_y F_z
+      }
+#pragma unroll
+      for (int i = 0; i < N1; ++i) F[0][i + 4 * j] = -g1[i];
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int a = 0; a < N1; ++a) {
+        double lx = 0.0, ly = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          lx = fma(P.m1[a * N1 + m], sXY[(s * 2 + 0) * 4 + m], lx);
+          ly = fma(P.m1[a * N1 + m], sXY[(s * 2 + 1) * 4 + m], ly);
+        }
+        F[0][(s ? 3 : 0) + 4 * a] += lx;
+        F[0][a + 4 * (s ? 3 : 0)] += ly;
+      }
+  }
+  // T1 over the u planes (dead since the jump exchange above)
+#pragma unroll
+  for (int n = 0; n < NP; ++n) sU[k * kPS + n] = h[0][n];
+  __syncwarp();
+  // ---- F: z contraction, z-face lifts, source; R rows out through shared
+  double out[NP];
+#pragma unroll
+  for (int n = 0; n < NP; ++n) out[n] = 0.0;
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    const double mk = sel4(P.m1, k, m), sk = sel4(P.s1, k, m);
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+      out[n] = fma(mk, sU[m * kPS + n], fma(sk, sT2[m * kPS + n], out[n]));
+  }
+  if (k == 0 || k == 3) {
+    const int f = k == 3;
+    double w[NP];                                // (M_x (x) M_y) fh_z
+#pragma unroll
+    for (int j = 0; j < N1; ++j)
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) a = fma(P.m1[i * N1 + m], sFZ[f * 20 + j * kES + m], a);
+        w[i + 4 * j] = a;
+      }
+#pragma unroll
+    for (int j = 0; j < N1; ++j)
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) a = fma(P.m1[j * N1 + m], w[i + 4 * m], a);
+        out[i + 4 * j] += a;
+      }
+  }
+  if (active) {
+#pragma unroll
+    for (int n = 0; n < NP; ++n) bad_if(P, e, out[n]);
+  }
+  __syncwarp();                                  // T1 / T2 reads done
+#pragma unroll
+  for (int n = 0; n < NP; ++n) sU[k * kPS + n] = out[n];
+  __syncwarp();
+  {
+    const int nval = min(8, P.ne - e_w) * NB;
+    double* rb = R + (size_t)e_w * NB;
+    const double* sb = (!TANGENT && bsrc) ? bsrc + (size_t)e_w * NB : nullptr;
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+      const int d = lane + 32 * x;
+      if (d < nval) {
+        double v = sW[(d >> 6) * kPlanePer + ((d >> 4) & 3) * kPS + (d & 15)];
+        if (sb) v += __ldg(sb + d);
+        rb[d] = v;
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // pass 2: neighbour share of f(., q^) on faces whose q^ comes from across
 // --------------------------------------------------------------------------
 //
@@ -775,7 +1205,26 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
   if (grid <= 0) return 0;
   if (pass & 1) {
     const FaceRec* fr = reinterpret_cast<const FaceRec*>(P.frec);
-    if (tangent) fused_kernel<N1, ND, NCU, true><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
+    if (N1 == 4 && ND == 3 && NCU == 1 && P.variant == 0) {
+      const int gp = (P.ne + kPlaneEpb - 1) / kPlaneEpb;
+      const int smem = kPlaneEpb * kPlanePer * (int)sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(plane_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+      }
+      if (P.flux_uses_u) {
+        if (tangent) plane_kernel<true, true><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X);
+        else plane_kernel<false, true><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X);
+      } else {
+        if (tangent) plane_kernel<true, false><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X);
+        else plane_kernel<false, false><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X);
+      }
+      if (cudaGetLastError() != cudaSuccess) return 3;
+    } else if (tangent) fused_kernel<N1, ND, NCU, true><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
     else fused_kernel<N1, ND, NCU, false><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
     if (cudaGetLastError() != cudaSuccess) return 3;
   }

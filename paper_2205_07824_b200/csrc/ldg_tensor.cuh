@@ -21,7 +21,7 @@ struct TensorParams {
   const void* frec;       // (ne, 2nd) packed {sJ*tau, nbr, info|flags} records (16 B)
   const double* kco;      // (ne, kstride): C, Cu, sJ per face axis (fused kernels)
   int kstride;
-  int pad2_;
+  int variant;           // pass-1 kernel: 0 auto (plane kernel where it applies), 1 pencil kernel
   unsigned long long* bad;  // first non-finite element (atomicMin)
   double d1[LDG_MAX_N1 * LDG_MAX_N1];
   double m1[LDG_MAX_N1 * LDG_MAX_N1];
