@@ -57,6 +57,7 @@ int ldg_version(void) { return 1; }
 const char* ldg_last_error(void) { return g_err.c_str(); }
 
 int ldg_create(const LdgTables* t, LdgHandle** out) {
+  std::vector<double> h_rec_host;   // face records, kept on the host for the chunk schedule
   if (!t || !out) return fail(2, "null argument");
   if (t->nd < 2 || t->nd > 3 || t->n1 < 2 || t->n1 > LDG_MAX_N1 || t->ncu < 1 ||
       t->ncu > LDG_MAX_NCU || t->ne < 0)
@@ -150,6 +151,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
       }
     }
     rc |= upload(&h->frec, rec.data(), rec.size(), "frec");
+    h_rec_host.swap(rec);
     rc |= upload(&h->kco, kco.data(), kco.size(), "kco");
     h->kstride = kst;
   }
@@ -171,6 +173,39 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   {
     const char* v = getenv("LDG_PASS1_VARIANT");    // "pencil" forces the v9 kernel (A/B timing)
     P.variant = (v && strcmp(v, "pencil") == 0) ? 1 : 0;
+  }
+  P.e0 = 0;
+  P.e1 = t->ne;
+  {
+    // chunk-interleaved schedule of the fused operator (ldg_fused.cu run_fused):
+    // chunk_dep[c] = last chunk whose exports pass 2 of chunk c reads
+    int nch = 1;                       // measured: chunking loses (launch tails outweigh L2 reuse)
+    if (const char* v = getenv("LDG_CHUNKS")) nch = atoi(v);
+    nch = nch < 1 ? 1 : (nch > ldg::LDG_MAX_CHUNKS ? ldg::LDG_MAX_CHUNKS : nch);
+    const int ne = t->ne, nf = 2 * t->nd;
+    P.nchunk = nch;
+    for (int c = 0; c <= nch; ++c) {
+      long long b = (long long)ne * c / nch;
+      b = (b + 31) / 32 * 32;
+      P.chunk_start[c] = c == nch ? ne : (int)(b < ne ? b : ne);
+    }
+    std::vector<int> dep(nch, 0);
+    int c = 0;
+    for (int e = 0; e < ne; ++e) {
+      while (e >= P.chunk_start[c + 1]) ++c;
+      dep[c] = dep[c] > c ? dep[c] : c;
+      for (int lf = 0; lf < nf; ++lf) {
+        int32_t pair[2];
+        memcpy(pair, &h_rec_host[(size_t)(e * nf + lf) * 2 + 1], sizeof(pair));
+        const int info = pair[1];
+        if ((info & LDG_FACE_KIND_MASK) != LDG_FACE_INTERIOR || !(info & LDG_FL_COMPLETE)) continue;
+        const int nb = pair[0];
+        int cn = 0;
+        while (nb >= P.chunk_start[cn + 1]) ++cn;
+        dep[c] = dep[c] > cn ? dep[c] : cn;
+      }
+    }
+    for (int k = 0; k < nch; ++k) P.chunk_dep[k] = dep[k];
   }
   const int n1 = t->n1;
   // tables arrive with row stride n1 packed at the front of each array

@@ -168,8 +168,8 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   constexpr int KSZ = NC + ND;             // C, Cu, sJ per face axis
   __shared__ __align__(16) double s_k[EPB][KSZ];
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
-  const int e = blockIdx.x * EPB + slot;
-  const bool active = slot < EPB && e < P.ne;
+  const int e = P.e0 + blockIdx.x * EPB + slot;
+  const bool active = slot < EPB && e < P.e1;
   const int ta = lt % N1, tb = ND == 3 ? lt / N1 : 0;
   const int i = ta, j = tb;
   double* su = s_u[slot];
@@ -660,9 +660,9 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   __shared__ int s_map[kPlaneMaps * NP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = threadIdx.x >> 2, k = threadIdx.x & 3;
-  const int e = blockIdx.x * kPlaneEpb + slot;
-  const int e_w = blockIdx.x * kPlaneEpb + warp * 8;       // first element of the warp
-  const bool active = e < P.ne;
+  const int e = P.e0 + blockIdx.x * kPlaneEpb + slot;
+  const int e_w = P.e0 + blockIdx.x * kPlaneEpb + warp * 8;   // first element of the warp
+  const bool active = e < P.e1;
   double* sEl = psm + slot * kPlanePer;
   double* sU = sEl;
   double* sJZ = sEl + kOffJ;
@@ -678,7 +678,7 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
 
   // ---- A: u rows (coalesced, cp.async), records, coefficients, gathers
   {
-    const int nval = min(8, P.ne - e_w) * NB;              // doubles of this warp
+    const int nval = min(8, P.e1 - e_w) * NB;              // doubles of this warp
     const double* ub = u + (size_t)e_w * NB;
 #pragma unroll
     for (int x = 0; x < 16; ++x) {
@@ -1007,7 +1007,7 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   for (int n = 0; n < NP; ++n) sU[k * kPS + n] = out[n];
   __syncwarp();
   {
-    const int nval = min(8, P.ne - e_w) * NB;
+    const int nval = min(8, P.e1 - e_w) * NB;
     double* rb = R + (size_t)e_w * NB;
     const double* sb = (!TANGENT && bsrc) ? bsrc + (size_t)e_w * NB : nullptr;
 #pragma unroll
@@ -1049,8 +1049,10 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
   __shared__ double sv[EPB][NFACE][NF][NCU];    // neighbour exports, then lifted values
   __shared__ double sw2[EPB][NFACE][NF][NCU];   // first-direction partial lift
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
-  const int e = blockIdx.x * EPB + slot;
-  const bool active = slot < EPB && e < P.ne;
+  // blocks run in reverse element order: pass 1 finished with the last
+  // elements, whose R rows and exports are still resident in L2
+  const int e = P.e0 + (gridDim.x - 1 - blockIdx.x) * EPB + slot;
+  const bool active = slot < EPB && e < P.e1;
   const int i = lt % N1, j = ND == 3 ? lt / N1 : 0;
   // this thread's M1 rows (i for the first in-face index, j for the second)
   double Mi[N1], Mj[N1];
@@ -1200,13 +1202,14 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
                     cudaStream_t s) {
   using S1 = P1Smem<N1, ND, NCU>;
   using S2 = P2Smem<N1, ND, NCU>;
-  const int grid = (P.ne + S1::EPB - 1) / S1::EPB;
-  const int grid2 = (P.ne + S2::EPB - 1) / S2::EPB;
+  const int nel = P.e1 - P.e0;
+  const int grid = (nel + S1::EPB - 1) / S1::EPB;
+  const int grid2 = (nel + S2::EPB - 1) / S2::EPB;
   if (grid <= 0) return 0;
   if (pass & 1) {
     const FaceRec* fr = reinterpret_cast<const FaceRec*>(P.frec);
     if (N1 == 4 && ND == 3 && NCU == 1 && P.variant == 0) {
-      const int gp = (P.ne + kPlaneEpb - 1) / kPlaneEpb;
+      const int gp = (nel + kPlaneEpb - 1) / kPlaneEpb;
       const int smem = kPlaneEpb * kPlanePer * (int)sizeof(double);
       static bool attr = false;
       if (!attr) {
@@ -1234,11 +1237,48 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+// Full operator.  With P.nchunk > 1 the element range is cut into chunks and
+// the two passes interleave, P1(0) P1(1) P2(0) P1(2) P2(1) ...: pass 2 of a
+// chunk runs as soon as pass 1 of every chunk it reads exports from is done
+// (chunk_dep, computed from the face table at ldg_create), while that
+// chunk's R rows and exports are still resident in L2, so pass 2 costs L2
+// rather than HBM traffic.
 template <int N1, int ND, int NCU>
 static int run_fused(const TensorParams& P, bool tangent, const double* u,
                      const double* gproj, const double* bsrc, double* R, double* X,
                      cudaStream_t s) {
-  return run_pass<N1, ND, NCU>(P, 3, tangent, u, gproj, bsrc, R, X, s);
+  if (P.nchunk <= 1) return run_pass<N1, ND, NCU>(P, 3, tangent, u, gproj, bsrc, R, X, s);
+  // pass 2 chunks go to a side stream so they overlap the next pass-1 chunk
+  // (fork / join with events: also valid under CUDA graph capture)
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t ev[LDG_MAX_CHUNKS + 2];
+  if (!side) {
+    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) return 3;
+    for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  }
+  cudaEventRecord(ev[LDG_MAX_CHUNKS + 1], s);
+  cudaStreamWaitEvent(side, ev[LDG_MAX_CHUNKS + 1], 0);       // fork
+  TensorParams Q = P;
+  for (int c = 0; c < P.nchunk; ++c) {
+    Q.e0 = P.chunk_start[c];
+    Q.e1 = P.chunk_start[c + 1];
+    if (int rc = run_pass<N1, ND, NCU>(Q, 1, tangent, u, gproj, bsrc, R, X, s)) return rc;
+    cudaEventRecord(ev[c], s);
+    bool waited = false;
+    for (int d = 0; d < P.nchunk; ++d) {
+      if (P.chunk_dep[d] != c) continue;
+      if (!waited) {
+        cudaStreamWaitEvent(side, ev[c], 0);
+        waited = true;
+      }
+      Q.e0 = P.chunk_start[d];
+      Q.e1 = P.chunk_start[d + 1];
+      if (int rc = run_pass<N1, ND, NCU>(Q, 2, tangent, u, gproj, bsrc, R, X, side)) return rc;
+    }
+  }
+  cudaEventRecord(ev[LDG_MAX_CHUNKS], side);
+  cudaStreamWaitEvent(s, ev[LDG_MAX_CHUNKS], 0);               // join
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 #define LDG_FDISPATCH(FN, ...)                                                  \

@@ -6,6 +6,8 @@
 
 namespace ldg {
 
+constexpr int LDG_MAX_CHUNKS = 16;
+
 // Operator data passed by value (__grid_constant__) to every launch.  The
 // 1D tables are tiny and read uniformly across a warp, so they live in the
 // kernel parameter bank (constant cache), which DFMA can consume directly.
@@ -22,6 +24,10 @@ struct TensorParams {
   const double* kco;      // (ne, kstride): C, Cu, sJ per face axis (fused kernels)
   int kstride;
   int variant;           // pass-1 kernel: 0 auto (plane kernel where it applies), 1 pencil kernel
+  int e0, e1;            // element range of this launch (chunked schedules)
+  int nchunk;            // > 1: residual / tangent run chunk-interleaved (L2-resident pass 2)
+  int chunk_start[LDG_MAX_CHUNKS + 1];
+  int chunk_dep[LDG_MAX_CHUNKS];   // last chunk whose pass 1 pass 2 of this chunk reads
   unsigned long long* bad;  // first non-finite element (atomicMin)
   double d1[LDG_MAX_N1 * LDG_MAX_N1];
   double m1[LDG_MAX_N1 * LDG_MAX_N1];
