@@ -23,6 +23,7 @@
 // Mapping: one thread per node column ((i,j) with the k column in registers
 // for hex, i with the j column for quads) = one thread per face node.
 
+#include <algorithm>
 #include "ldg_tensor.cuh"
 
 namespace ldg {
@@ -69,6 +70,13 @@ __device__ __forceinline__ int vol_to_face(int ax, int v) {
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_group1() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -618,19 +626,20 @@ constexpr int kPlaneBlock = 128;
 constexpr int kPlaneEpb = kPlaneBlock / 4;
 constexpr int kPS = 17;                      // padded plane stride (doubles)
 constexpr int kES = 5;                       // padded stride of a thread's 4 face values
-// per-element shared region (doubles):
-//   [0, 68)    u planes (stride 17), later T1, later the R staging
-//   [68, 108)  z-face jumps  [face][row j][i] (row stride 5)
-//   [108, 148) z-face fluxes [face][row j][i]
-//   [148, 216) T2 planes (stride 17)
-//   [216, 232) the element's coefficient block C | Cu (cp.async)
-// The thread-private x/y face fluxes live in the thread's own u-plane slot
-// between the u exchange and the T1 store.
+// per-element shared region (doubles), two input buffers + work space:
+//   in buffer b at b * 96:  [0, 68) u planes (stride 17), later T1 and the R
+//                           staging; [68, 84) coefficient block C | Cu;
+//                           [84, 96) the six face records (16 B each)
+//   [192, 232) z-face jumps  [face][row j][i] (row stride 5)
+//   [232, 272) z-face fluxes [face][row j][i]
+//   [272, 340) T2 planes (stride 17)
 // element stride = 4 (mod 16) doubles so the 8 elements of a warp spread
-// over the banks
-constexpr int kOffJ = 4 * kPS, kOffF = kOffJ + 40, kOffE = kOffF + 40, kOffC = kOffE + 4 * kPS;
-constexpr int kPlanePer = 244;
-static_assert(kOffC + 16 <= kPlanePer, "layout");
+// over the banks.  The thread-private x/y face fluxes live in the thread's
+// own u-plane slot between the u exchange and the T1 store.
+constexpr int kInSz = 96, kInC = 4 * kPS, kInF = kInC + 16;
+constexpr int kOffJ = 2 * kInSz, kOffF = kOffJ + 40, kOffE = kOffF + 40;
+constexpr int kPlanePer = kOffE + 4 * kPS;   // 340
+static_assert(kInF + 12 <= kInSz, "layout");
 static_assert(kPlanePer % 16 == 4, "element stride must be 4 mod 16 doubles");
 constexpr int kPlaneMaps = 16;               // node maps cached in shared memory
 }  // namespace
@@ -646,7 +655,7 @@ __device__ __forceinline__ double sel1(const double* a, int k) {
 }
 
 #ifndef LDG_PLANE_MINB
-#define LDG_PLANE_MINB 3          // 3 blocks (12 warps) per SM: <= 168 registers
+#define LDG_PLANE_MINB 2          // 2 persistent blocks per SM (shared-memory bound)
 #endif
 
 template <bool TANGENT, bool HAS_CU>
@@ -660,95 +669,124 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   __shared__ int s_map[kPlaneMaps * NP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = threadIdx.x >> 2, k = threadIdx.x & 3;
-  const int e = P.e0 + blockIdx.x * kPlaneEpb + slot;
-  const int e_w = P.e0 + blockIdx.x * kPlaneEpb + warp * 8;   // first element of the warp
-  const bool active = e < P.e1;
-  double* sEl = psm + slot * kPlanePer;
-  double* sU = sEl;
-  double* sJZ = sEl + kOffJ;
-  double* sFZ = sEl + kOffF;
-  double* sT2 = sEl + kOffE;
-  double* sC = sEl + kOffC;
-  double* sXY = sU + k * kPS;                              // this thread's slot
-  double* sW = psm + warp * 8 * kPlanePer;                 // the warp's 8 elements
-
+  const int ls = lane >> 2;                                // element slot within the warp
   const bool map_smem = P.n_maps <= kPlaneMaps;
   if (map_smem)
     for (int x = threadIdx.x; x < P.n_maps * NP; x += kPlaneBlock) s_map[x] = __ldg(P.nmap + x);
+  __syncthreads();
+  double* sWarp = psm + warp * 8 * kPlanePer;              // the warp's 8 element regions
+  double* sEl = sWarp + ls * kPlanePer;
+  double* sJZ = sEl + kOffJ;
+  double* sFZ = sEl + kOffF;
+  double* sT2 = sEl + kOffE;
+  const int nel = P.e1 - P.e0;
+  const int ngroups = (nel + 7) >> 3;
+  const int stride = gridDim.x * (kPlaneBlock / 32);
+  int g = blockIdx.x * (kPlaneBlock / 32) + warp;
 
-  // ---- A: u rows (coalesced, cp.async), records, coefficients, gathers
-  {
-    const int nval = min(8, P.e1 - e_w) * NB;              // doubles of this warp
-    const double* ub = u + (size_t)e_w * NB;
+  // prefetch of one group of 8 elements into input buffer `buf`: u rows
+  // (coalesced 8 B copies into the padded planes), the coefficient blocks and
+  // the face records (16 B copies); one cp.async group per call
+  auto prefetch = [&](int gg, int buf) {
+    if (gg < ngroups) {
+      const int e_w = P.e0 + gg * 8;
+      const int ne_w = min(8, P.e1 - e_w);
+      const double* ub = u + (size_t)e_w * NB;
+      double* dst = sWarp + buf * kInSz;
 #pragma unroll
-    for (int x = 0; x < 16; ++x) {
-      const int d = lane + 32 * x;                         // element d/64, plane, node
-      if (d < nval)
-        cp_async8(sW + (d >> 6) * kPlanePer + ((d >> 4) & 3) * kPS + (d & 15), ub + d);
-    }
-  }
-  double tau[6];
-  int info[6];
-  double ext[6][N1];                                       // neighbour / boundary face values
-  __syncthreads();                                         // s_map ready (uniform)
-  if (active) {
-    int nbr[6];
+      for (int x = 0; x < 16; ++x) {
+        const int d = lane + 32 * x;                       // element d/64, plane, node
+        if (d < ne_w * NB)
+          cp_async8(dst + (d >> 6) * kPlanePer + ((d >> 4) & 3) * kPS + (d & 15), ub + d);
+      }
+      const double* kb = P.kco + (size_t)e_w * P.kstride;
 #pragma unroll
-    for (int lf = 0; lf < 6; ++lf) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(frec + (size_t)e * 6 + lf));
-      tau[lf] = v.x;
-      const int2 w = *reinterpret_cast<const int2*>(&v.y);
-      nbr[lf] = w.x;
-      info[lf] = w.y;
-    }
-    const double* kb = P.kco + (size_t)e * P.kstride;
+      for (int x = 0; x < 2; ++x) {                        // 8 elements x 8 chunks of 16 B
+        const int c = lane + 32 * x, el = c >> 3, part = c & 7;
+        if (el < ne_w && 2 * part < P.kstride)
+          cp_async16(dst + el * kPlanePer + kInC + 2 * part, kb + (size_t)el * P.kstride + 2 * part);
+      }
+      const double* fb = reinterpret_cast<const double*>(frec + (size_t)e_w * 6);
 #pragma unroll
-    for (int x = 0; x < 3; ++x) cp_async8(sC + 3 * k + x, kb + 3 * k + x);   // C (9) + Cu (3)
-    // face node t of this thread's 4 values: x faces (j,k) -> j + 4k; y faces
-    // (i,k) -> i + 4k; z faces, row j = k: (i,k) -> i + 4k.  A run of 4
-    // consecutive, 32-B aligned neighbour nodes is fetched with 2 x 16 B loads.
-#pragma unroll
-    for (int lf = 0; lf < 6; ++lf) {
-      const int kind = info[lf] & LDG_FACE_KIND_MASK;
-#pragma unroll
-      for (int a = 0; a < N1; ++a) ext[lf][a] = 0.0;
-      if (kind == LDG_FACE_INTERIOR) {
-        if (info[lf] & LDG_FL_UNBR) {
-          const int mid = (info[lf] >> LDG_FACE_MAP_SHIFT) & 0xffff;
-          const double* base = u + (size_t)nbr[lf] * NB;
-          int nn[N1];
-#pragma unroll
-          for (int a = 0; a < N1; ++a)
-            nn[a] = map_smem ? s_map[mid * NP + a + 4 * k] : __ldg(P.nmap + mid * NP + a + 4 * k);
-          if (nn[1] == nn[0] + 1 && nn[2] == nn[0] + 2 && nn[3] == nn[0] + 3 && (nn[0] & 3) == 0) {
-            const double2* b2 = reinterpret_cast<const double2*>(base + nn[0]);
-            const double2 v0 = __ldg(b2), v1 = __ldg(b2 + 1);
-            ext[lf][0] = v0.x; ext[lf][1] = v0.y; ext[lf][2] = v1.x; ext[lf][3] = v1.y;
-          } else {
-#pragma unroll
-            for (int a = 0; a < N1; ++a) ext[lf][a] = __ldg(base + nn[a]);
-          }
-        }
-      } else if (!TANGENT && gproj) {
-        const double2* b2 = reinterpret_cast<const double2*>(gproj + (size_t)nbr[lf] * NP + 4 * k);
-        const double2 v0 = __ldg(b2), v1 = __ldg(b2 + 1);
-        ext[lf][0] = v0.x; ext[lf][1] = v0.y; ext[lf][2] = v1.x; ext[lf][3] = v1.y;
+      for (int x = 0; x < 2; ++x) {                        // 8 elements x 6 records of 16 B
+        const int c = lane + 32 * x, el = c / 6, part = c % 6;
+        if (c < 48 && el < ne_w) cp_async16(dst + el * kPlanePer + kInF + 2 * part, fb + 2 * c);
       }
     }
-  } else {
+    cp_async_commit();
+  };
+
+  prefetch(g, 0);
+  for (int it = 0; g < ngroups; g += stride, ++it) {
+    const int cur = it & 1;
+    prefetch(g + stride, cur ^ 1);
+    cp_async_wait_group1();                                // this group's data landed
+    __syncwarp();
+    const int e = P.e0 + g * 8 + ls;
+    const int e_w = P.e0 + g * 8;
+    const bool active = e < P.e1;
+    double* sIn = sEl + cur * kInSz;
+    double* sU = sIn;
+    double* sC = sIn + kInC;
+    double* sXY = sU + k * kPS;                            // this thread's slot
+    double* sW = sWarp + cur * kInSz;                      // staging rows of this buffer
+
+    // ---- A: records and gathers
+    double tau[6];
+    int info[6];
+    double ext[6][N1];                                     // neighbour / boundary face values
+    if (active) {
+      int nbr[6];
 #pragma unroll
-    for (int lf = 0; lf < 6; ++lf) {
-      tau[lf] = 0.0;
-      info[lf] = LDG_FACE_NEUMANN;
+      for (int lf = 0; lf < 6; ++lf) {
+        const double* r = sIn + kInF + 2 * lf;
+        tau[lf] = r[0];
+        const int2 w = *reinterpret_cast<const int2*>(r + 1);
+        nbr[lf] = w.x;
+        info[lf] = w.y;
+      }
+      // face node t of this thread's 4 values: x faces (j,k) -> j + 4k; y faces
+      // (i,k) -> i + 4k; z faces, row j = k: (i,k) -> i + 4k.  A run of 4
+      // consecutive, 32-B aligned neighbour nodes is fetched with 2 x 16 B loads.
 #pragma unroll
-      for (int a = 0; a < N1; ++a) ext[lf][a] = 0.0;
+      for (int lf = 0; lf < 6; ++lf) {
+        const int kind = info[lf] & LDG_FACE_KIND_MASK;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) ext[lf][a] = 0.0;
+        if (kind == LDG_FACE_INTERIOR) {
+          if (info[lf] & LDG_FL_UNBR) {
+            const int mid = (info[lf] >> LDG_FACE_MAP_SHIFT) & 0xffff;
+            const double* base = u + (size_t)nbr[lf] * NB;
+            int nn[N1];
+#pragma unroll
+            for (int a = 0; a < N1; ++a)
+              nn[a] = map_smem ? s_map[mid * NP + a + 4 * k] : __ldg(P.nmap + mid * NP + a + 4 * k);
+            if (nn[1] == nn[0] + 1 && nn[2] == nn[0] + 2 && nn[3] == nn[0] + 3 && (nn[0] & 3) == 0) {
+              const double2* b2 = reinterpret_cast<const double2*>(base + nn[0]);
+              const double2 v0 = __ldg(b2), v1 = __ldg(b2 + 1);
+              ext[lf][0] = v0.x; ext[lf][1] = v0.y; ext[lf][2] = v1.x; ext[lf][3] = v1.y;
+            } else {
+#pragma unroll
+              for (int a = 0; a < N1; ++a) ext[lf][a] = __ldg(base + nn[a]);
+            }
+          }
+        } else if (!TANGENT && gproj) {
+          const double2* b2 = reinterpret_cast<const double2*>(gproj + (size_t)nbr[lf] * NP + 4 * k);
+          const double2 v0 = __ldg(b2), v1 = __ldg(b2 + 1);
+          ext[lf][0] = v0.x; ext[lf][1] = v0.y; ext[lf][2] = v1.x; ext[lf][3] = v1.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int lf = 0; lf < 6; ++lf) {
+        tau[lf] = 0.0;
+        info[lf] = LDG_FACE_NEUMANN;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) ext[lf][a] = 0.0;
+      }
     }
-  }
-  cp_async_commit();
-  cp_async_wait_all();
-  __syncwarp();
-  // idle lanes (past the last element) run on with zero data so that every
-  // __syncwarp() below is reached by the whole warp
+    // idle lanes (past the last element) run on with zero data so that every
+    // __syncwarp() below is reached by the whole warp
 
   // ---- B: d/dz from all four planes; z-face jumps / own-data flux, row j = k
   double up[NP], hz[NP];
@@ -1020,6 +1058,8 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       }
     }
   }
+  __syncwarp();                                  // this buffer is refilled two groups on
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -1209,7 +1249,10 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
   if (pass & 1) {
     const FaceRec* fr = reinterpret_cast<const FaceRec*>(P.frec);
     if (N1 == 4 && ND == 3 && NCU == 1 && P.variant == 0) {
-      const int gp = (nel + kPlaneEpb - 1) / kPlaneEpb;
+      static int nsm = 0;
+      if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+      const int groups = (nel + 7) / 8;
+      const int gp = std::max(1, std::min((groups + 3) / 4, nsm * LDG_PLANE_MINB));
       const int smem = kPlaneEpb * kPlanePer * (int)sizeof(double);
       static bool attr = false;
       if (!attr) {
@@ -1231,9 +1274,10 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
     else fused_kernel<N1, ND, NCU, false><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
     if (cudaGetLastError() != cudaSuccess) return 3;
   }
-  if (pass & 2)
+  if (pass & 2) {
     complete_kernel<N1, ND, NCU><<<grid2, kFBlock, 0, s>>>(
-        P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
+          P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
