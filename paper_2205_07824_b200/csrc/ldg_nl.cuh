@@ -274,18 +274,13 @@ nl_mixed(const __grid_constant__ NlParams P) {
 template <bool TANGENT>
 struct RShape {
   static constexpr int NVA = NV * (TANGENT ? 2 : 1);              // u,q (+ du,dq)
-  static constexpr int BS = (NVA > NG ? NVA : NG) * MX;           // one work buffer
-  static constexpr int SMEM = NVA * NB + NCU * NB + 2 * BS;       // doubles
-  // faces per round: own + neighbour traces (two stages) and the face fluxes
-  // must fit in the two volume work buffers
-  static constexpr int fits(int fr) { return 4 * fr * NVA * MXF + fr * NQF * NCU <= 2 * BS; }
-  static constexpr int pick() {
-    int best = 1;
-    for (int c = 1; c <= NFACE; ++c)
-      if (fits(c)) best = c;
-    return best;
-  }
-  static constexpr int FR = pick();
+  static constexpr int BS = (NVA > NG ? NVA : NG) * MX;           // one volume work buffer
+  // face phase: traces of every face at its Gauss points, own and neighbour
+  // side [side][face][v][NQF], one face's staging pair, and the face fluxes
+  static constexpr int TR = NFACE * NVA * NQF;
+  static constexpr int FACE = 2 * TR + 4 * NVA * MXF + NFACE * NQF * NCU;
+  static constexpr int WORK = 2 * BS > FACE ? 2 * BS : FACE;
+  static constexpr int SMEM = NVA * NB + NCU * NB + WORK;         // doubles
 };
 
 // numerical flux f^ . n at one face point (disc.py:657-862), in the left frame
@@ -447,8 +442,7 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
 template <bool TANGENT>
 __device__ __forceinline__ void residual_body(const NlParams& P) {
   using S = RShape<TANGENT>;
-  constexpr int NVA = S::NVA, FR = S::FR;
-  static_assert(S::fits(1), "face buffers do not fit");
+  constexpr int NVA = S::NVA;
   extern __shared__ __align__(16) double smem_r[];
   double* sV = smem_r;                      // [NVA][NB] node values
   double* sR = sV + NVA * NB;             // [NCU][NB] residual accumulator
@@ -518,91 +512,92 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
   }
   __syncthreads();
 
-  // ---- faces, FR at a time: traces at face points, f^, lift
-  constexpr int TSZ = FR * NVA * MXF;          // one trace buffer (own or neighbour)
-  double* T0 = bA;                             // [side][f][v][face grid], dense
-  double* T1 = bA + 2 * TSZ;
-  double* sF = bA + 4 * TSZ;                   // [f][NQF][NCU]
-  for (int f0 = 0; f0 < NFACE; f0 += FR) {
-    const int nfr = NFACE - f0 < FR ? NFACE - f0 : FR;
-    for (int idx = tid; idx < 2 * FR * NVA * NFN; idx += NT) {
-      const int side = idx / (FR * NVA * NFN), r = idx % (FR * NVA * NFN);
-      const int f = r / (NVA * NFN), v = (r / NFN) % NVA, t = r % NFN;
+  // ---- faces: traces of all faces at their Gauss points (one face's own and
+  // neighbour staging at a time), then every face point's f^ at once, then
+  // the lift with each (node, component) owned by one thread
+  double* TRc = bA;                            // [side][face][v][NQF]
+  double* ST0 = bA + 2 * S::TR;                // staging [side][v][face grid]
+  double* ST1 = ST0 + 2 * NVA * MXF;
+  double* sF = ST1 + 2 * NVA * MXF;            // [face][NQF][NCU]
+  auto phi = [](int) { return (int)OP_PHI; };
+  for (int lf = 0; lf < NFACE; ++lf) {
+    const int info = P.finfo[e * NFACE + lf];
+    const bool interior = (info & 3) == 0;
+    const int nbr = P.fnbr[e * NFACE + lf];
+    for (int idx = tid; idx < 2 * NVA * NFN; idx += NT) {
+      const int side = idx / (NVA * NFN), v = (idx / NFN) % NVA, t = idx % NFN;
       double val = 0.0;
-      if (f < nfr) {
-        const int lf = f0 + f;
-        if (side == 0) {
-          val = sV[v * NB + face_vol_node(lf, t)];
-        } else {
-          const int info = P.finfo[e * NFACE + lf];
-          if ((info & 3) == 0) {
-            const int nbr = P.fnbr[e * NFACE + lf];
-            const int nn = P.nmap[(info >> 8) * NFN + t];
-            val = state_at(P, v >= NV, v % NV, (sz_t)nbr, nn);
-          }
-        }
-      }
-      T0[idx] = val;
+      if (side == 0) val = sV[v * NB + face_vol_node(lf, t)];
+      else if (interior) val = state_at(P, v >= NV, v % NV, (sz_t)nbr, P.nmap[(info >> 8) * NFN + t]);
+      ST0[idx] = val;
     }
     __syncthreads();
-    auto phi = [](int) { return (int)OP_PHI; };
-    double* tr;
+    const double* tr;
     if (ND == 3) {
-      contract<N1, N1, 1, 0, N1, NQ1, false>(T0, T1, 2 * FR * NVA, tid, phi);
+      contract<N1, N1, 1, 0, N1, NQ1, false>(ST0, ST1, 2 * NVA, tid, phi);
       __syncthreads();
-      contract<NQ1, N1, 1, 1, N1, NQ1, false>(T1, T0, 2 * FR * NVA, tid, phi);
+      contract<NQ1, N1, 1, 1, N1, NQ1, false>(ST1, ST0, 2 * NVA, tid, phi);
       __syncthreads();
-      tr = T0;
+      tr = ST0;
     } else {
-      contract<N1, 1, 1, 0, N1, NQ1, false>(T0, T1, 2 * FR * NVA, tid, phi);
+      contract<N1, 1, 1, 0, N1, NQ1, false>(ST0, ST1, 2 * NVA, tid, phi);
       __syncthreads();
-      tr = T1;
+      tr = ST1;
     }
-    // trace layout after contraction: [side][f][v][NQF]
-    for (int it = tid; it < nfr * NQF; it += NT) {
-      const int f = it / NQF, s = it % NQF, lf = f0 + f;
-      const int info = P.finfo[e * NFACE + lf];
-      const int kind = info & 3;
-      const bool right = kind == 0 && (info & 4);
-      const bool sw = info & 8;
-      const int brow = P.fnbr[e * NFACE + lf];
-      const double* fg = P.fgeo + ((sz_t)e * NFACE + lf) * (ND + 2);
-      double n[ND];
-#pragma unroll
-      for (int d = 0; d < ND; ++d) n[d] = fg[d];
-      double x[ND];
-      phys_point(P, e, &c_fxi[(lf * NQF + s) * ND], x);
-      double vo[NVA], vn[NVA];
-#pragma unroll
-      for (int v = 0; v < NVA; ++v) {
-        vo[v] = tr[((0 * FR + f) * NVA + v) * NQF + s];
-        vn[v] = tr[((1 * FR + f) * NVA + v) * NQF + s];
-      }
-      double fh[NCU];
-      face_flux<TANGENT>(P, e, kind, right, sw, brow, s, x, n, fg[ND + 1], vo, vn, fh);
-      const double w = c_fw[lf * NQF + s] * fg[ND] * (right ? -1.0 : 1.0);
-#pragma unroll
-      for (int c = 0; c < NCU; ++c) sF[(f * NQF + s) * NCU + c] = w * fh[c];
+    for (int idx = tid; idx < 2 * NVA * NQF; idx += NT) {
+      const int side = idx / (NVA * NQF), r = idx % (NVA * NQF);
+      TRc[(side * NFACE + lf) * NVA * NQF + r] = tr[idx];
     }
     __syncthreads();
-    // lift onto the face nodes, one face at a time (faces share edge nodes)
-    for (int f = 0; f < nfr; ++f) {
-      const int lf = f0 + f;
-      for (int it = tid; it < NFN * NCU; it += NT) {
-        const int t = it / NCU, c = it % NCU;
-        const int t0 = t % N1, t1 = ND == 3 ? t / N1 : 0;
-        double acc = 0.0;
-#pragma unroll
-        for (int s = 0; s < NQF; ++s) {
-          const int s0 = s % NQ1, s1 = ND == 3 ? s / NQ1 : 0;
-          const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1] : c_phi[s0 * N1 + t0];
-          acc = fma(ph, sF[(f * NQF + s) * NCU + c], acc);
-        }
-        sR[c * NB + face_vol_node(lf, t)] += acc;
-      }
-      __syncthreads();
-    }
   }
+  for (int it = tid; it < NFACE * NQF; it += NT) {
+    const int lf = it / NQF, s = it % NQF;
+    const int info = P.finfo[e * NFACE + lf];
+    const int kind = info & 3;
+    const bool right = kind == 0 && (info & 4);
+    const bool sw = info & 8;
+    const int brow = P.fnbr[e * NFACE + lf];
+    const double* fg = P.fgeo + ((sz_t)e * NFACE + lf) * (ND + 2);
+    double n[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) n[d] = fg[d];
+    double x[ND];
+    phys_point(P, e, &c_fxi[(lf * NQF + s) * ND], x);
+    double vo[NVA], vn[NVA];
+#pragma unroll
+    for (int v = 0; v < NVA; ++v) {
+      vo[v] = TRc[((0 * NFACE + lf) * NVA + v) * NQF + s];
+      vn[v] = TRc[((1 * NFACE + lf) * NVA + v) * NQF + s];
+    }
+    double fh[NCU];
+    face_flux<TANGENT>(P, e, kind, right, sw, brow, s, x, n, fg[ND + 1], vo, vn, fh);
+    const double w = c_fw[lf * NQF + s] * fg[ND] * (right ? -1.0 : 1.0);
+#pragma unroll
+    for (int c = 0; c < NCU; ++c) sF[(lf * NQF + s) * NCU + c] = w * fh[c];
+  }
+  __syncthreads();
+  // lift: thread owns (volume node, component) and sums the faces through it
+  for (int it = tid; it < NB * NCU; it += NT) {
+    const int a = it / NCU, c = it % NCU;
+    const int ia[3] = {a % N1, (a / N1) % N1, ND == 3 ? a / (N1 * N1) : 0};
+    double acc = 0.0;
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf) {
+      const int ax = face_axis(lf);
+      if (ia[ax] != (face_side(lf) ? N1 - 1 : 0)) continue;
+      // face-node coordinates (t0, t1) over the tangential axes, ascending
+      const int t0 = ia[ax == 0 ? 1 : 0];
+      const int t1 = ND == 3 ? ia[ax == 2 ? 1 : 2] : 0;
+#pragma unroll
+      for (int s = 0; s < NQF; ++s) {
+        const int s0 = s % NQ1, s1 = ND == 3 ? s / NQ1 : 0;
+        const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1] : c_phi[s0 * N1 + t0];
+        acc = fma(ph, sF[(lf * NQF + s) * NCU + c], acc);
+      }
+    }
+    sR[c * NB + a] += acc;
+  }
+  __syncthreads();
   for (int idx = tid; idx < NCU * NB; idx += NT) {
     const int a = idx / NCU, c = idx % NCU;
     P.out[(sz_t)e * NB * NCU + idx] = sR[c * NB + a];

@@ -201,7 +201,11 @@ def generate_source(tab):
     kmax = max(n1, nq1)
     mx, mxf = kmax ** nd, kmax ** (nd - 1)
     nq, nb = nq1 ** nd, n1 ** nd
+    # threads per element: the quadrature points rounded to warps; 3D elements
+    # get at least 128 (contractions and face work have more parallelism)
     nt = min(256, ((max(nq, nb) + 31) // 32) * 32)
+    if nd == 3:
+        nt = max(nt, 128)
     ng = ncu * (nd + 1)
     defs = dict(ND=nd, N1=n1, NQ1=nq1, NCU=ncu, KIND_C=int(model.kind == "C"),
                 HAS_WS=int(ws is not None), TRACE_CENTERED=int(model.numflux.trace == "centered"),
@@ -284,9 +288,12 @@ class NlOperator:
         s = self.shape
         nv, nb, mx, ng, ncu = s["NV"], s["NB"], s["MX"], s["NG"], tab.ncu
         self.smem = {}
+        nd, nqf, mxf = tab.nd, tab.nq1 ** (tab.nd - 1), s["MXF"]
         for name, tan in (("nl_residual", False), ("nl_tangent", True)):
             nva = nv * (2 if tan else 1)
-            self.smem[name] = 8 * (nva * nb + ncu * nb + 2 * max(nva, ng) * mx)
+            face = 2 * (2 * nd) * nva * nqf + 4 * nva * mxf + 2 * nd * nqf * ncu
+            work = max(2 * max(nva, ng) * mx, face)
+            self.smem[name] = 8 * (nva * nb + ncu * nb + work)
         nvm = ncu if s["MASS_CONST"] else 3 * ncu
         self.smem["nl_mass"] = self.smem["nl_mass_extra"] = 8 * 2 * max(nvm, ncu) * mx
         self.smem["nl_mass_inv"] = 8 * 2 * ncu * nb
