@@ -169,6 +169,38 @@ def cpu_solve(n):
             "gmres_iters": int(sum(st["gmres_iters"])), "cores": 1}
 
 
+def load_traffic():
+    """DRAM bytes per launch of the two fused kernels from the committed ncu
+    --set full capture (profiles/traffic.json, written by
+    tools_ncu_traffic.py from the same bench command): dram__bytes_read.sum +
+    dram__bytes_write.sum.  Absent file -> null."""
+    try:
+        return json.loads((ROOT / "profiles" / "traffic.json").read_text())
+    except Exception:
+        return {}
+
+
+def nonlinear_lines(hbm):
+    """Configs 4 and 2 on the generated-kernel path (scripts/nl_bench.py):
+    3D compressible Navier-Stokes hex p=3 n=32 (10.5M DOFs) and 2D Euler quad
+    p=4 n=256 (6.6M DOFs) residual / tangent GDOF/s with the SURVEY 8(d)
+    byte counts (104 / 24 B/DOF)."""
+    sys.path.insert(0, str(ROOT / "scripts"))
+    import nl_bench
+    from cases import TRANSIENT_CASES
+    out = {}
+    ns = dict(TRANSIENT_CASES["ns3d_tgv_hex_p2_dirk11"], counts=[32] * 3, p=3,
+              state=([1.0, 0.2, -0.1, 0.15, 25.0], 0.05))
+    eu = dict(TRANSIENT_CASES["euler2d_vortex_quad_p3_dirk22"], counts=[256] * 2, p=4,
+              state=([1.0, 0.2, -0.1, 2.5], 0.05))
+    for name, spec in (("config4_ns3d_hex_p3_n32", ns), ("config2_euler2d_quad_p4_n256", eu)):
+        _, r = nl_bench.run(name, spec, 10, hbm)
+        out[name] = {k: r[k] for k in ("dofs", "tangent_gdofs", "residual_gdofs", "tangent_ms",
+                                       "residual_ms", "tangent_bytes_per_dof",
+                                       "tangent_frac_hbm")}
+    return out
+
+
 def run_reference(args, rank):
     """The reference CPU path (oracle port of ldgkit's numpy implementation)."""
     if rank != 0:
@@ -280,6 +312,11 @@ def run_b200(args, rank, world):
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     t_ms = float(tmax.item())
+    traffic = load_traffic()
+    p1_name = ("plane_kernel<tangent> (pass 1, z-plane mapping, persistent)"
+               if (core.tab.n1 == 4 and core.tab.nd == 3 and core.ncu == 1
+                   and os.environ.get("LDG_PASS1_VARIANT", "") != "pencil")
+               else "fused_kernel<tangent> (pass 1, pencil mapping)")
     # algorithmic bytes of the fused passes from the face tables
     tab = core.tab
     info = tab.finfo
@@ -360,14 +397,15 @@ def run_b200(args, rank, world):
                 "call": ("LdgSystem.residual_tangent(state, du) with pinned torch CPU du"
                          if world == 1 else
                          "PartitionedLdgSystem.tangent_dev on the H2D copy of pinned du, D2H of R")},
-        "roofline": {"bound": "hbm", "kernel": "fused_kernel<4,3,1,tangent> (pass 1)",
+        "roofline": {"bound": "hbm", "kernel": p1_name,
                      "achieved": ach_p1, "peak": hbm, "unit": "GB/s",
-                     "frac": ach_p1 / hbm, "traffic": None,
+                     "frac": ach_p1 / hbm, "traffic": traffic.get("pass1"),
+                     "traffic_source": traffic.get("source"),
                      "algorithmic_bytes_per_dof": bytes_p1 / ndof, "ms": p1,
                      "peak_source": peak_src},
         "pass2_roofline": {"kernel": "complete_kernel<4,3,1> (pass 2)", "achieved": ach_p2,
                            "frac": ach_p2 / hbm, "algorithmic_bytes_per_dof": bytes_p2 / ndof,
-                           "ms": p2},
+                           "traffic": traffic.get("pass2"), "ms": p2},
         "matvec_roofline": {"achieved": ach_mv, "peak": hbm, "unit": "GB/s",
                             "frac": ach_mv / hbm, "algorithmic_bytes_per_dof": BYTES_MATVEC,
                             "note": "SURVEY 8(d) two-pass accounting (q through HBM)",
@@ -380,6 +418,8 @@ def run_b200(args, rank, world):
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_nonlinear:
+        line["nonlinear"] = nonlinear_lines(hbm)
     if world == 1 and not args.no_solve:
         line["solve"] = {"metric": "Newton-GMRES time to solution (s), config 3, block-Jacobi, "
                                    "acceptance flags", "dofs": ndof,
@@ -406,6 +446,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true",
                     help="skip the Newton-GMRES time-to-solution measurement")
+    ap.add_argument("--no-nonlinear", action="store_true",
+                    help="skip the generated-kernel (configs 2 / 4) throughput lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", 1))

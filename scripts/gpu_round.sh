@@ -1,0 +1,13 @@
+#!/bin/bash
+# One GPU session: full bench line, launch list, ncu --set full of the two
+# fused kernels (run under gpurun; outputs in gpurun_out/)
+set -u
+timeout 600 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
+tail -c 600 gpurun_out/bench_full.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-solve \
+  --no-cpu-baseline --no-nonlinear > /dev/null 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on \
+  -k regex:"plane_kernel|complete_kernel" -s 6 -c 2 -o gpurun_out/prof_bench \
+  python bench.py --steps 2 --warmup 3 --no-solve --no-cpu-baseline --no-nonlinear > /dev/null 2>&1
+ls -la gpurun_out | tail -5

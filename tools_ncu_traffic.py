@@ -1,0 +1,34 @@
+"""Write profiles/traffic.json: DRAM bytes per launch of the fused pass-1 /
+pass-2 kernels from an ncu --set full report of the bench command.
+
+    python tools_ncu_traffic.py gpurun_out/prof_bench.ncu-rep [source-note]
+"""
+import csv
+import json
+import subprocess
+import sys
+
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+hdr, units = rows[0], rows[1]
+idx = {h: i for i, h in enumerate(hdr)}
+res = {"source": sys.argv[2] if len(sys.argv) > 2 else rep}
+
+
+def mb(r, k):
+    v = float(r[idx[k]].replace(",", ""))
+    u = units[idx[k]]
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+
+
+for r in rows[2:]:
+    name = r[idx["Kernel Name"]]
+    b = mb(r, "dram__bytes_read.sum") + mb(r, "dram__bytes_write.sum")
+    key = "pass1" if ("plane_kernel" in name or "fused_kernel" in name) else (
+        "pass2" if "complete_kernel" in name else name[:40])
+    res.setdefault(key, b)
+    res.setdefault(key + "_kernel", name[:80])
+json.dump(res, open("profiles/traffic.json", "w"), indent=1)
+print(json.dumps(res))
