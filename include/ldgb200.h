@@ -55,6 +55,7 @@ extern "C" {
 #define LDG_FL_QHALF (1 << 27)     /* q^ centered: half from each side */
 #define LDG_FL_COMPLETE (1 << 28)  /* pass 2 adds the neighbour share */
 #define LDG_FL_ALPHA_SHIFT 29      /* bits 29..30: jump coefficient 0 | 1 | 1/2 */
+#define LDG_FL_XIDENT (1u << 31)   /* the neighbour's face-node order equals this face's */
 
 /* Host-side description of a tensor-product (quad/hex) kind-D system with a
  * flux that is linear in (u, q) with constant coefficients.  Pointers are
@@ -125,6 +126,12 @@ int ldg_compute_mixed(LdgHandle* h, const double* u, const double* gproj,
 /* Device scratch (doubles) the residual / tangent calls need: the face
  * export buffer of the fused operator, ne * 2nd * n1^(nd-1) * ncu. */
 int64_t ldg_scratch_doubles(LdgHandle* h);
+
+/* Where pass 1 writes the face exports: 1 (default) into the consuming
+ * neighbour's own (element, face) slots in its face-node order, so pass 2
+ * reads its slots without a gather; 0 into the producer's slots (the
+ * partitioned layer exchanges producer rows between ranks). */
+int ldg_set_export_layout(LdgHandle* h, int consumer);
 
 /* R(u) (disc.py:588-653) by the fused two-pass operator (ldg_fused.cu):
  * the mixed gradient never leaves the SM.  gproj: projected Dirichlet /

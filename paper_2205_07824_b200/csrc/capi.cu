@@ -135,6 +135,22 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
           }
           if (acode != 0 || beta != 0.0) info |= LDG_FL_UNBR;
           if (gc || (sw == right)) info |= LDG_FL_EXPORT;
+          {
+            // consumer-slot exports need the neighbour's face-node order; flag
+            // the (structured-mesh) case where it is this face's own order
+            const int nlf = (info >> 4) & 7, mid = (info >> LDG_FACE_MAP_SHIFT) & 0xffff;
+            const int n1 = t->n1, nfn_ = nd == 3 ? n1 * n1 : n1;
+            const int nax = axis_of(nlf);
+            bool ident = true;
+            for (int tt = 0; tt < nfn_ && ident; ++tt) {
+              const int v = t->nmap[(size_t)mid * nfn_ + tt];
+              const int i = v % n1, j = (v / n1) % n1, k = v / (n1 * n1);
+              const int tn = nd == 3 ? (nax == 0 ? j + n1 * k : (nax == 1 ? i + n1 * k : i + n1 * j))
+                                     : (nax == 0 ? v / n1 : v % n1);
+              ident = tn == tt;
+            }
+            if (ident) info = (int32_t)((uint32_t)info | LDG_FL_XIDENT);
+          }
           if (!gc && (sw == right)) info |= LDG_FL_QOWN;
           if (gc) info |= LDG_FL_QHALF;
           if (gc || (sw != right)) info |= LDG_FL_COMPLETE;
@@ -176,6 +192,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   }
   P.e0 = 0;
   P.e1 = t->ne;
+  P.x_consumer = 1;
   {
     // chunk-interleaved schedule of the fused operator (ldg_fused.cu run_fused):
     // chunk_dep[c] = last chunk whose exports pass 2 of chunk c reads
@@ -299,6 +316,12 @@ int ldg_create_dense(const LdgDenseTables* t, LdgHandle** out) {
   memcpy(D.au, t->au, sizeof(D.au));
   memcpy(D.aq, t->aq, sizeof(D.aq));
   *out = h;
+  return 0;
+}
+
+int ldg_set_export_layout(LdgHandle* h, int consumer) {
+  if (!h || h->dense) return fail(2, "export layout applies to tensor handles");
+  h->P.x_consumer = consumer ? 1 : 0;
   return 0;
 }
 

@@ -416,7 +416,20 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       for (int c = 0; c < NCU; ++c) {
         const double xf = sgn * sff[fix(lf, lt, c)];
         sfh[fix(lf, lt, c)] = fma(w_own, xf, sfh[fix(lf, lt, c)]);
-        if (exp_) X[(((size_t)e * NFACE + lf) * NF + lt) * NCU + c] = xf;
+        if (exp_) {
+          size_t xo;
+          if (P.x_consumer) {      // the neighbour's slot, in its face-node order
+            const int nlf = (info >> 4) & 7;
+            const int mid = (info >> LDG_FACE_MAP_SHIFT) & 0xffff;
+            const int tn = ((unsigned)info & LDG_FL_XIDENT) ? lt
+                : vol_to_face<N1, ND>(face_axis(ND, nlf), __ldg(P.nmap + mid * NF + lt));
+            const int nbr = __ldg(&frec[(size_t)e * NFACE + lf].nbr);   // (re-read: keeps it out of registers)
+            xo = (((size_t)nbr * NFACE + nlf) * NF + tn) * NCU + c;
+          } else {
+            xo = (((size_t)e * NFACE + lf) * NF + lt) * NCU + c;
+          }
+          X[xo] = xf;
+        }
       }
     }
   }
@@ -908,9 +921,37 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         sXY[(s * 2 + ax) * 4 + a] = fma(w_own, xv[a], sXY[(s * 2 + ax) * 4 + a]);
       }
       if (exp_) {
-        double2* xp = reinterpret_cast<double2*>(X + ((size_t)e * 6 + lf) * NP + 4 * k);
-        xp[0] = make_double2(xv[0], xv[1]);
-        xp[1] = make_double2(xv[2], xv[3]);
+        if (P.x_consumer && ((unsigned)info[lf] & LDG_FL_XIDENT)) {   // same node order
+          const int nbr = reinterpret_cast<const int2*>(sIn + kInF + 2 * lf + 1)->x;
+          double2* xp = reinterpret_cast<double2*>(X + ((size_t)nbr * 6 + ((info[lf] >> 4) & 7)) * NP + 4 * k);
+          xp[0] = make_double2(xv[0], xv[1]);
+          xp[1] = make_double2(xv[2], xv[3]);
+        } else if (P.x_consumer) {  // the neighbour's slot, in its face-node order
+          const int inf = info[lf];
+          const int nlf = (inf >> 4) & 7, mid = (inf >> LDG_FACE_MAP_SHIFT) & 0xffff;
+          const int nbr = reinterpret_cast<const int2*>(sIn + kInF + 2 * lf + 1)->x;
+          double* xb = X + ((size_t)nbr * 6 + nlf) * NP;
+          const int nax = face_axis(3, nlf);
+          int tn[N1];
+#pragma unroll
+          for (int a = 0; a < N1; ++a) {
+            const int t = a + 4 * k;
+            const int nv = map_smem ? s_map[mid * NP + t] : __ldg(P.nmap + mid * NP + t);
+            tn[a] = vol_to_face<N1, 3>(nax, nv);
+          }
+          if (tn[1] == tn[0] + 1 && tn[2] == tn[0] + 2 && tn[3] == tn[0] + 3 && (tn[0] & 1) == 0) {
+            double2* xp = reinterpret_cast<double2*>(xb + tn[0]);   // aligned run of 4
+            xp[0] = make_double2(xv[0], xv[1]);
+            xp[1] = make_double2(xv[2], xv[3]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < N1; ++a) xb[tn[a]] = xv[a];
+          }
+        } else {
+          double2* xp = reinterpret_cast<double2*>(X + ((size_t)e * 6 + lf) * NP + 4 * k);
+          xp[0] = make_double2(xv[0], xv[1]);
+          xp[1] = make_double2(xv[2], xv[3]);
+        }
       }
     }
   if (k == 0 || k == 3) {                        // z face of this plane
@@ -923,13 +964,38 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
                            : ((inf & LDG_FL_QOWN) ? 1.0 : ((inf & LDG_FL_QHALF) ? 0.5 : 0.0));
       const double sgn = f ? 1.0 : -1.0;
       double2* xp = reinterpret_cast<double2*>(X + ((size_t)e * 6 + f) * NP);
+      double* xb = nullptr;
+      int mid = 0, nax = 0;
+      if (exp_ && P.x_consumer) {
+        const int nlf = (inf >> 4) & 7;
+        const double* nb2 = sIn + kInF + 2 * f + 1;
+        const size_t row = ((size_t)reinterpret_cast<const int2*>(nb2)->x * 6 + nlf) * NP;
+        if ((unsigned)inf & LDG_FL_XIDENT) {
+          xp = reinterpret_cast<double2*>(X + row);       // same node order: plain rows
+        } else {
+          mid = (inf >> LDG_FACE_MAP_SHIFT) & 0xffff;
+          nax = face_axis(3, nlf);
+          xb = X + row;
+        }
+      }
 #pragma unroll
       for (int n = 0; n < NP; n += 2) {
         const double x0 = sgn * h[2][n], x1 = sgn * h[2][n + 1];
+        if (xb) {
+          const int v0 = map_smem ? s_map[mid * NP + n] : __ldg(P.nmap + mid * NP + n);
+          const int v1 = map_smem ? s_map[mid * NP + n + 1] : __ldg(P.nmap + mid * NP + n + 1);
+          const int t0 = vol_to_face<N1, 3>(nax, v0), t1 = vol_to_face<N1, 3>(nax, v1);
+          if (t1 == t0 + 1 && (t0 & 1) == 0) {
+            *reinterpret_cast<double2*>(xb + t0) = make_double2(x0, x1);
+          } else {
+            xb[t0] = x0;
+            xb[t1] = x1;
+          }
+        }
         double* z0 = sFZ + f * 20 + (n >> 2) * kES + (n & 3);
         z0[0] = fma(w_own, x0, z0[0]);
         z0[1] = fma(w_own, x1, z0[1]);
-        if (exp_) xp[n / 2] = make_double2(x0, x1);
+        if (exp_ && !xb) xp[n / 2] = make_double2(x0, x1);
       }
     }
   }
@@ -1135,6 +1201,10 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
       const int info = info_[lf];
       const bool act = info & LDG_FL_COMPLETE;
       mask |= act ? (1 << lf) : 0;
+      if (P.x_consumer) {                 // the exporter wrote into this element's slot
+        src[lf] = act ? X + (((size_t)e * NFACE + lf) * NF + lt) * NCU : nullptr;
+        continue;
+      }
       const int nlf = (info >> 4) & 7;
       const int mid = act ? (info >> LDG_FACE_MAP_SHIFT) & 0xffff : 0;
       const int nv = map_in_smem ? s_map[mid * NF + lt] : __ldg(P.nmap + mid * NF + lt);

@@ -25,6 +25,7 @@ struct TensorParams {
   int kstride;
   int variant;           // pass-1 kernel: 0 auto (plane kernel where it applies), 1 pencil kernel
   int e0, e1;            // element range of this launch (chunked schedules)
+  int x_consumer;        // 1: exports land in the consuming neighbour's slots (pass 2 reads its own)
   int nchunk;            // > 1: residual / tangent run chunk-interleaved (L2-resident pass 2)
   int chunk_start[LDG_MAX_CHUNKS + 1];
   int chunk_dep[LDG_MAX_CHUNKS];   // last chunk whose pass 1 pass 2 of this chunk reads

@@ -227,6 +227,10 @@ class PartitionedLdgSystem:
         self.plan = PartitionPlan(gtab, nranks, rank)
         self.local = LocalTables(gtab, self.plan)
         self.sys = LdgSystem(model, mesh, topology, master, device=device, tables=self.local)
+        # exports stay in the producer's rows: those rows are what the halo
+        # exchange ships to the ranks holding the element as a ghost
+        from . import _lib as L
+        L.check(self.sys.lib.ldg_set_export_layout(self.sys._h, 0), "ldg_set_export_layout")
         self.exchanger = exchanger if exchanger is not None else HaloExchanger(self.plan)
         p = self.plan
         self.n_elements, self.n_nodes, self.ncu = p.ne_loc, master.n_nodes, model.ncu
