@@ -347,8 +347,8 @@ def run_b200(args, rank, world):
             out_host.copy_(r, non_blocking=True)
             torch.cuda.current_stream().synchronize()
             return out_host
-    for _ in range(2):
-        e2e_step()
+    for _ in range(max(args.warmup, 3)):     # same pattern as the timed loop (the caller
+        out = e2e_step()                      # holds the previous result)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -152,6 +152,22 @@ int ldg_operator_pass(LdgHandle* h, int pass, int tangent, const double* u,
                       const double* gproj, const double* bsrc, double* scratch,
                       double* R, void* stream);
 
+/* The same pass over elements [e0, e1) only (chunk-pipelined host calls:
+ * H2D of later chunks and D2H of finished ones overlap the kernels). */
+int ldg_operator_pass_range(LdgHandle* h, int pass, int tangent, const double* u,
+                            const double* gproj, const double* bsrc, double* scratch,
+                            double* R, int e0, int e1, void* stream);
+
+/* LdgSystem.residual / residual_tangent (disc.py:588-593) on HOST data:
+ * v_host, out_host pinned (ne, nb, ncu).  Chunk-pipelined (chunk bounds
+ * `starts` (nchunk + 1), per chunk the last chunk holding a face neighbour
+ * `dep`): H2D, the two fused passes and D2H overlap.  Blocks until out_host
+ * is written.  tangent = 0 evaluates R(v) with gproj / bsrc. */
+int ldg_apply_host(LdgHandle* h, int tangent, const double* v_host, double* out_host,
+                   double* v_dev, double* R_dev, double* scratch, const double* gproj,
+                   const double* bsrc, int nchunk, const int32_t* starts,
+                   const int32_t* dep, void* stream);
+
 /* Unfused reference structure, kept for comparison: flux pass from a
  * precomputed q = compute_mixed(u) (72 B/DOF of HBM traffic at nd = 3). */
 int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,

@@ -75,6 +75,11 @@ _SIGS = {
     "ldg_residual": ([C.c_void_p] * 7, C.c_int),
     "ldg_residual_tangent": ([C.c_void_p] * 5, C.c_int),
     "ldg_operator_pass": ([C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 6, C.c_int),
+    "ldg_operator_pass_range": ([C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 5
+                                + [C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "ldg_apply_host": ([C.c_void_p, C.c_int] + [C.c_void_p] * 7 + [C.c_int, C.c_void_p,
+                                                                 C.c_void_p, C.c_void_p],
+                       C.c_int),
     "ldg_flux_from_mixed": ([C.c_void_p, C.c_int] + [C.c_void_p] * 6, C.c_int),
     "ldg_mass_apply": ([C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_mass_inv_apply": ([C.c_void_p] * 4, C.c_int),

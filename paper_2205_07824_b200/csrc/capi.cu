@@ -48,6 +48,10 @@ struct LdgHandle {
   double* kco = nullptr;
   int kstride = 0;
   unsigned long long* bad = nullptr;
+  // host-pipeline resources (ldg_apply_host): copy streams, chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_p2;
+  cudaEvent_t ev_start = nullptr;
 };
 
 extern "C" {
@@ -263,6 +267,11 @@ int ldg_destroy(LdgHandle* h) {
   for (void* p : h->dense_bufs) cudaFree(p);
   cudaFree(h->geo); cudaFree(h->fnbr); cudaFree(h->finfo); cudaFree(h->ftau);
   cudaFree(h->nmap); cudaFree(h->frec); cudaFree(h->kco); cudaFree(h->bad);
+  for (auto e : h->ev_in) cudaEventDestroy(e);
+  for (auto e : h->ev_p2) cudaEventDestroy(e);
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
+  if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_out) cudaStreamDestroy(h->s_out);
   delete h;
   return 0;
 }
@@ -382,6 +391,98 @@ int ldg_operator_pass(LdgHandle* h, int pass, int tangent, const double* u,
   int rc = ldg::launch_fused_pass(h->P, pass, tangent != 0, u, gproj, bsrc, R, scratch,
                                   (cudaStream_t)stream);
   return rc ? fail(rc, "operator pass launch", cudaGetLastError()) : 0;
+}
+
+int ldg_operator_pass_range(LdgHandle* h, int pass, int tangent, const double* u,
+                            const double* gproj, const double* bsrc, double* scratch,
+                            double* R, int e0, int e1, void* stream) {
+  if (!h || !u || !R || !scratch || pass < 1 || pass > 2) return fail(2, "bad argument");
+  if (h->dense) return fail(2, "not available for simplex systems");
+  if (e0 < 0 || e1 > h->P.ne || e0 > e1) return fail(2, "element range out of bounds");
+  if (e0 == e1) return 0;
+  ldg::TensorParams Q = h->P;
+  Q.e0 = e0;
+  Q.e1 = e1;
+  int rc = ldg::launch_fused_pass(Q, pass, tangent != 0, u, gproj, bsrc, R, scratch,
+                                  (cudaStream_t)stream);
+  return rc ? fail(rc, "operator pass launch", cudaGetLastError()) : 0;
+}
+
+// Host-resident operator call, chunk pipelined: H2D of the chunks on one copy
+// stream, the two fused passes per chunk on `stream` once the rows of every
+// neighbour chunk have arrived (chunk_dep), D2H of each finished chunk on a
+// second copy stream, so PCIe in both directions overlaps the kernels and each
+// other.  v_host / out_host: pinned host (ne, nb, ncu); v_dev / R_dev /
+// scratch: device work buffers.  Returns when out_host holds the result.
+int ldg_apply_host(LdgHandle* h, int tangent, const double* v_host, double* out_host,
+                   double* v_dev, double* R_dev, double* scratch, const double* gproj,
+                   const double* bsrc, int nchunk, const int32_t* starts,
+                   const int32_t* dep, void* stream) {
+  if (!h || !v_host || !out_host || !v_dev || !R_dev || !scratch || nchunk < 1 || !starts || !dep)
+    return fail(2, "bad argument");
+  if (h->dense) return fail(2, "not available for simplex systems");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h->s_in) {
+    cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
+  }
+  while ((int)h->ev_in.size() < nchunk) {
+    cudaEvent_t a, b;
+    cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+    h->ev_in.push_back(a);
+    h->ev_p2.push_back(b);
+  }
+  const size_t row = (size_t)(h->P.nd == 3 ? h->P.n1 * h->P.n1 * h->P.n1 : h->P.n1 * h->P.n1) *
+                     h->P.ncu;
+  cudaEventRecord(h->ev_start, s);
+  cudaStreamWaitEvent(h->s_in, h->ev_start, 0);
+  for (int c = 0; c < nchunk; ++c) {
+    const size_t a = (size_t)starts[c] * row, n = (size_t)(starts[c + 1] - starts[c]) * row;
+    cudaMemcpyAsync(v_dev + a, v_host + a, n * sizeof(double), cudaMemcpyHostToDevice, h->s_in);
+    cudaEventRecord(h->ev_in[c], h->s_in);
+  }
+  std::vector<char> done(nchunk, 0);
+  for (int c = 0; c < nchunk; ++c) {
+    cudaStreamWaitEvent(s, h->ev_in[dep[c]], 0);
+    ldg::TensorParams Q = h->P;
+    Q.e0 = starts[c];
+    Q.e1 = starts[c + 1];
+    int rc = ldg::launch_fused_pass(Q, 1, tangent != 0, v_dev, gproj, bsrc, R_dev, scratch, s);
+    if (rc) return fail(rc, "pass 1 launch", cudaGetLastError());
+    for (int d = 0; d < nchunk; ++d) {
+      if (done[d] || dep[d] > c) continue;
+      Q.e0 = starts[d];
+      Q.e1 = starts[d + 1];
+      rc = ldg::launch_fused_pass(Q, 2, tangent != 0, v_dev, gproj, bsrc, R_dev, scratch, s);
+      if (rc) return fail(rc, "pass 2 launch", cudaGetLastError());
+      cudaEventRecord(h->ev_p2[d], s);
+      cudaStreamWaitEvent(h->s_out, h->ev_p2[d], 0);
+      const size_t a = (size_t)starts[d] * row, n = (size_t)(starts[d + 1] - starts[d]) * row;
+      cudaMemcpyAsync(out_host + a, R_dev + a, n * sizeof(double), cudaMemcpyDeviceToHost,
+                      h->s_out);
+      done[d] = 1;
+    }
+  }
+  if (getenv("LDG_PIPE_DEBUG")) {       // timeline of the copies and kernels
+    cudaEvent_t t1, t2, t3;
+    cudaEventCreate(&t1); cudaEventCreate(&t2); cudaEventCreate(&t3);
+    cudaEventRecord(t1, h->s_in);
+    cudaEventRecord(t2, s);
+    cudaEventRecord(t3, h->s_out);
+    cudaStreamSynchronize(h->s_out);
+    cudaStreamSynchronize(h->s_in);
+    cudaStreamSynchronize(s);
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, t1, t3);
+    cudaEventElapsedTime(&b, t2, t3);
+    fprintf(stderr, "pipe: D2H end - H2D end %.3f ms, D2H end - compute end %.3f ms\n", a, b);
+    cudaEventDestroy(t1); cudaEventDestroy(t2); cudaEventDestroy(t3);
+  }
+  cudaError_t e = cudaStreamSynchronize(h->s_out);
+  if (e != cudaSuccess) return fail(3, "host pipeline", e);
+  return 0;
 }
 
 int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,

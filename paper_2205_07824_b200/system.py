@@ -422,6 +422,70 @@ class LdgSystem:
                                                self._stream()), "ldg_mass_inv_apply")
         return o
 
+    # -- chunk-pipelined host calls (fused path) --------------------------------------------
+    PIPE_CHUNKS = int(__import__('os').environ.get('LDG_PIPE_CHUNKS', 16))
+
+    def _pipe_plan(self):
+        """Element chunks and, per chunk, the last chunk holding a face
+        neighbour of one of its elements: pass 1 of a chunk needs the input
+        rows up to that chunk, pass 2 the exports of pass 1 up to it."""
+        if getattr(self, "_pipe", None) is None:
+            ne = self.n_elements
+            C_ = max(1, min(self.PIPE_CHUNKS, ne // 1024))
+            starts = [(ne * c // C_ + 31) // 32 * 32 for c in range(C_)] + [ne]
+            starts = [min(x, ne) for x in starts]
+            chunk_of = np.searchsorted(np.asarray(starts[1:]), np.arange(ne), side="right")
+            nbr = np.where((self.tab.finfo & 3) == 0, self.tab.fnbr, -1)
+            far = np.where(nbr >= 0, chunk_of[np.clip(nbr, 0, ne - 1)], 0).max(axis=1)
+            dep = np.maximum(np.maximum.reduceat(far, starts[:-1]) if ne else [], np.arange(C_))
+            self._pipe = (starts, [int(d) for d in dep])
+        return self._pipe
+
+    def _pinned_out(self, shape):
+        """A pinned host result buffer.  Every call returns a new array as far
+        as the caller can tell (disc.py returns fresh arrays): a pooled buffer
+        is reused only once the pool holds its last reference, which avoids a
+        cudaHostAlloc (~60 ms for 80 MB) per call in a solver loop."""
+        import sys
+        import torch
+        pool = self._scratch.setdefault(("pinned_out", shape), [])
+        for buf in pool:
+            if sys.getrefcount(buf) <= 3:        # the pool list, `buf`, the argument
+                return buf
+        buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        if len(pool) < 4:
+            pool.append(buf)
+        return buf
+
+    def _host_pipeline(self, v, tangent, t):
+        """J v or R(v) for a CPU torch tensor v through ldg_apply_host: H2D of
+        the chunks on a copy stream, the two fused passes per chunk as soon as
+        their neighbour rows have arrived, D2H of each finished chunk on a
+        second copy stream (PCIe in both directions overlaps the kernels and
+        each other)."""
+        import torch
+        starts, dep = self._pipe_plan()
+        shape = (self.n_elements, self.n_nodes, self.ncu)
+        vh = v.reshape(shape)
+        if not vh.is_pinned():
+            vh = vh.pin_memory()
+        vh = vh.contiguous()
+        key = ("pipe", shape)
+        if key not in self._scratch:
+            self._scratch[key] = (self._empty(shape), self._empty(shape),
+                                  np.asarray(starts, dtype=np.int32),
+                                  np.asarray(dep, dtype=np.int32))
+        vd, R, st_, dp_ = self._scratch[key]
+        out = self._pinned_out(tuple(v.shape))     # returned as is (no view)
+        g = None if tangent else self.boundary_data(t)
+        b = None if tangent else self.source_data(t)
+        _lib.check(self.lib.ldg_apply_host(
+            self._h, int(bool(tangent)), C.c_void_p(vh.data_ptr()), C.c_void_p(out.data_ptr()),
+            _lib.ptr(vd), _lib.ptr(R), _lib.ptr(self.scratch()), _lib.ptr(g), _lib.ptr(b),
+            len(dep), st_.ctypes.data_as(C.c_void_p), dp_.ctypes.data_as(C.c_void_p),
+            self._stream()), "ldg_apply_host")
+        return out
+
     # -- reference-shaped API ------------------------------------------------------------------
     def _ret(self, x, origin):
         import torch
@@ -442,8 +506,17 @@ class LdgSystem:
             self._check_nan("mixed")
         return self._ret(q, dev)
 
+    def _pipelined(self, x):
+        import torch
+        return (isinstance(x, torch.Tensor) and not x.is_cuda and self.nl is None
+                and not self.dense and getattr(self, "_h", None) is not None)
+
     def residual(self, state):
         """disc.py:588-589 -> (Ru, None, None)."""
+        if self._pipelined(state.u):
+            R = self._host_pipeline(state.u, False, state.t)
+            self._check_nan("flux")
+            return R, None, None
         ud, dev = self._dev(state.u)
         R = self.residual_dev(ud.reshape(self.n_elements, self.n_nodes, self.ncu), state.t)
         if dev != "cuda":
@@ -452,6 +525,10 @@ class LdgSystem:
 
     def residual_tangent(self, state, du, dq=None, dw=None):
         """disc.py:591-593 (the reference linearisation)."""
+        if self._pipelined(du):
+            R = self._host_pipeline(du, True, state.t)
+            self._check_nan("flux")
+            return R, None, None
         dd, dev = self._dev(du)
         shape = (self.n_elements, self.n_nodes, self.ncu)
         base = None

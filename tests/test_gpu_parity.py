@@ -130,3 +130,29 @@ def test_partitioned_native_operator_single_gpu(name, nparts):
         Rs = bus.apply_all(us, tangent)
         R = np.concatenate([r.cpu().numpy() for r in Rs])
         assert rel(R, g[want]) < TOL, (key, rel(R, g[want]))
+
+
+def test_host_pipeline_matches_device_and_never_aliases():
+    """Pinned-CPU torch inputs run the chunk-pipelined ldg_apply_host (H2D,
+    passes and D2H overlapped): bitwise equal to the device path, and a result
+    the caller still holds is never reused for a later call."""
+    import torch
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem, SolverState
+    m = model.load_model(str(GOLDEN / "poisson3d.model"))
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [20, 18, 16], "hex")
+    s = LdgSystem(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("hex", 3))
+    assert len(s._pipe_plan()[1]) > 1
+    shape = (s.n_elements, s.n_nodes, 1)
+    a = torch.randn(shape, dtype=torch.float64).pin_memory()
+    b = torch.randn(shape, dtype=torch.float64).pin_memory()
+    st = SolverState(u=a, q=None, w=None, t=0.0)
+    Ja = s.residual_tangent(st, a)[0]
+    Ja_copy = Ja.clone()
+    Jb = s.residual_tangent(st, b)[0]
+    Jc = s.residual_tangent(st, a)[0]
+    assert Ja.data_ptr() != Jb.data_ptr() and Jc.data_ptr() not in (Ja.data_ptr(), Jb.data_ptr())
+    assert torch.equal(Ja, Ja_copy) and torch.equal(Jc, Ja)
+    assert torch.equal(Jb, s.tangent_dev(b.cuda()).cpu())
+    Ra = s.residual(st)[0]
+    assert torch.equal(Ra, s.residual_dev(a.cuda()).cpu())
