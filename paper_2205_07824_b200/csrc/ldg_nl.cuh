@@ -2,15 +2,17 @@
 // run time by NVRTC for sm_100a (csrc/jit.cu).  NOT compiled by nvcc: the
 // Python side (paper_2205_07824_b200/nonlinear.py) prepends a prelude with
 //   * the compile-time shape: ND, N1 (nodes / direction), NQ1 (Gauss points /
-//     direction), NCU, KIND_C, HAS_WS, TRACE_CENTERED, GRAD_CENTERED,
-//     MASS_CONST, NT (threads per element);
+//     direction), NCU, NW (ODE states), KIND_C, KIND_W, HAS_WS,
+//     TRACE_CENTERED, GRAD_CENTERED, MASS_CONST, NT (threads per element),
+//     ODE_ALPHA / ODE_BETA;
 //   * __constant__ 1D operators c_phi / c_dphi (NQ1 x N1, l_a(x_q)),
 //     c_d1 (GLL collocation derivative), c_clo / c_chi (M1^-1 e_0, e_p),
 //     c_m1inv, c_xq1 (1D Gauss points), c_qw (volume weights), c_fxi / c_fw
 //     (face-point reference coordinates and weights, matched to the
 //     reference's face rules), c_mass (constant mass coefficients);
 //   * the model's plans as device functions plan_flux / plan_src /
-//     plan_ws / plan_mass (+ _d dual variants), emitted by codegen.py;
+//     plan_ws / plan_mass / plan_sw (+ _d dual variants), emitted by codegen.py;
+//   * c_xn: reference coordinates of the solution nodes (ODE collocation);
 // and then this file.
 //
 // Algorithm: the reference's quadrature formulation (disc.py:595-893) per
@@ -36,7 +38,8 @@ constexpr int NFN = ND == 3 ? N1 * N1 : N1;
 constexpr int NQF = ND == 3 ? NQ1 * NQ1 : NQ1;
 constexpr int NFACE = 2 * ND;
 constexpr int NVQ = KIND_C ? 0 : NCU * ND;
-constexpr int NV = NCU + NVQ;                  // state variables per point (u, q)
+constexpr int NV = NCU + NVQ + NW;             // state variables per point (u, q, w)
+constexpr int OW = NCU + NVQ;                  // offset of w within a point's variables
 constexpr int KMAX = N1 > NQ1 ? N1 : NQ1;
 constexpr int MX = ND == 3 ? KMAX * KMAX * KMAX : KMAX * KMAX;
 constexpr int MXF = ND == 3 ? KMAX * KMAX : KMAX;
@@ -57,6 +60,8 @@ struct NlParams {
   const double* q;       // base mixed gradient (ne, NB, NCU, ND) / mass operand v
   const double* du;      // direction
   const double* dq;      // direction gradient (homogeneous lift of du)
+  const double* w;       // ODE states (ne, NB, NW)
+  const double* dw;
   double* out;
   u64* bad;              // [0]: first element with a non-finite plan value
 };
@@ -184,7 +189,8 @@ __device__ __forceinline__ void phys_point(const NlParams& P, int e, const doubl
 // array family `arr` (0: base u/q, 1: direction du/dq) at (element, node)
 __device__ __forceinline__ double state_at(const NlParams& P, int fam, int v, sz_t e, int node) {
   if (v < NCU) return (fam ? P.du : P.u)[(e * NB + node) * NCU + v];
-  return (fam ? P.dq : P.q)[(e * NB + node) * (NCU * ND) + (v - NCU)];
+  if (v < OW) return (fam ? P.dq : P.q)[(e * NB + node) * (NCU * ND) + (v - NCU)];
+  return (fam ? P.dw : P.w)[(e * NB + node) * (NW > 0 ? NW : 1) + (v - OW)];
 }
 
 // ---------------------------------------------------------------------------
@@ -221,6 +227,17 @@ nl_mixed(const __grid_constant__ NlParams P) {
           }
         } else if (kind == 1) {
           jump = own - (P.gproj ? P.gproj[((sz_t)nbr * NFN + t) * NCU + c] : 0.0);
+        } else if (kind == 3) {
+          // absorbing (kind W): u^ = (u + c q.n)/2 with the state gradient P.q
+          // (its direction dq in the tangent: the form is linear), c the
+          // state-independent wavespeed (disc.py:566-572)
+          const double* fg = P.fgeo + ((sz_t)e * NFACE + lf) * (ND + 2);
+          double wsc;
+          plan_ws(nullptr, P.t, nullptr, nullptr, nullptr, fg, &wsc);
+          double qn = 0.0;
+#pragma unroll
+          for (int d = 0; d < ND; ++d) qn += P.q[(((sz_t)e * NB + vn) * NCU + c) * ND + d] * fg[d];
+          jump = own - 0.5 * (own + wsc * qn);
         }
         sj[slot][lf][t][c] = jump;
       }
@@ -283,18 +300,50 @@ struct RShape {
   static constexpr int SMEM = NVA * NB + NCU * NB + WORK;         // doubles
 };
 
-// numerical flux f^ . n at one face point (disc.py:657-862), in the left frame
+// numerical flux f^ . n at one face point (disc.py:657-862), in the left frame.
+// ODE states bind as w^ = (w- + w+)/2 for kind D / W, the left trace for the
+// LLF flux and w_b on boundaries, with a zero tangent at faces (the reference
+// seeds only u^ and q^ there, disc.py:690-691, 735-736, 808-810).
 template <bool TANGENT>
 __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bool right, bool sw,
                                           int brow, int s, const double* x, const double* n,
                                           double tau0, const double* vo, const double* vn,
                                           double* fh) {
-  // vo / vn: own / neighbour values [u(NCU) q(NVQ) | du dq] at this point
+  // vo / vn: own / neighbour values [u(NCU) q(NVQ) w(NW) | du dq dw] at this point
   const double* uo = vo;
   const double* duo = vo + NV;
+  double wf[NW > 0 ? NW : 1], zw[NW > 0 ? NW : 1];
+#pragma unroll
+  for (int k = 0; k < (NW > 0 ? NW : 1); ++k) {
+    zw[k] = 0.0;
+    wf[k] = 0.0;
+    if (NW > 0) {
+      const double wo = vo[OW + k], wn = vn[OW + k];
+      const double wl = right ? wn : wo, wr = right ? wo : wn;
+      wf[k] = kind != 0 ? wo : (KIND_C ? wl : 0.5 * (wl + wr));
+    }
+  }
+  const double* wp = NW > 0 ? wf : nullptr;
+  const double* dwp = NW > 0 ? zw : nullptr;
   if (kind == 2) {                                     // neumann: f^ = g, zero tangent
 #pragma unroll
     for (int c = 0; c < NCU; ++c) fh[c] = TANGENT ? 0.0 : P.gq[((sz_t)brow * NQF + s) * NCU + c];
+    return;
+  }
+  if (kind == 3) {                                     // absorbing: c u^ (disc.py:783-794)
+    double c;
+    plan_ws(x, P.t, uo, nullptr, nullptr, n, &c);
+    flag(P, e, c);
+#pragma unroll
+    for (int i = 0; i < NCU; ++i) {
+      double qn = 0.0, dqn = 0.0;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        qn += uo[NCU + i * ND + d] * n[d];
+        if (TANGENT) dqn += duo[NCU + i * ND + d] * n[d];
+      }
+      fh[i] = TANGENT ? c * (0.5 * (duo[i] + c * dqn)) : c * (0.5 * (uo[i] + c * qn));
+    }
     return;
   }
   double f[NCU * ND], df[NCU * ND];
@@ -309,13 +358,13 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
       // LLF against the ghost state g (disc.py:839-862)
       double fg[NCU * ND], lami, lamg, dlami = 0.0;
       if (TANGENT) {
-        plan_flux_d(x, P.t, uo, nullptr, nullptr, n, duo, nullptr, nullptr, f, df);
+        plan_flux_d(x, P.t, uo, nullptr, wp, n, duo, nullptr, dwp, f, df);
         plan_ws_d(x, P.t, uo, nullptr, nullptr, n, duo, nullptr, nullptr, &lami, &dlami);
       } else {
-        plan_flux(x, P.t, uo, nullptr, nullptr, n, f);
+        plan_flux(x, P.t, uo, nullptr, wp, n, f);
         plan_ws(x, P.t, uo, nullptr, nullptr, n, &lami);
       }
-      plan_flux(x, P.t, g, nullptr, nullptr, n, fg);
+      plan_flux(x, P.t, g, nullptr, wp, n, fg);
       plan_ws(x, P.t, g, nullptr, nullptr, n, &lamg);
       flag(P, e, lami);
       flag(P, e, lamg);
@@ -338,8 +387,8 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
       // f(g, q_b) . n + tau_b (u_b - g) (disc.py:799-821)
       const double* qo = uo + NCU;
       const double* dqo = duo + NCU;
-      if (TANGENT) plan_flux_d(x, P.t, g, qo, nullptr, n, zero, dqo, nullptr, f, df);
-      else plan_flux(x, P.t, g, qo, nullptr, n, f);
+      if (TANGENT) plan_flux_d(x, P.t, g, qo, wp, n, zero, dqo, dwp, f, df);
+      else plan_flux(x, P.t, g, qo, wp, n, f);
       double tau = tau0;
       if (HAS_WS) {
         double li, lg;
@@ -371,13 +420,13 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
     // local Lax-Friedrichs (disc.py:724-751)
     double fR[NCU * ND], dfR[NCU * ND], lamL, lamR, dlamL = 0.0, dlamR = 0.0;
     if (TANGENT) {
-      plan_flux_d(x, P.t, uL, nullptr, nullptr, n, duL, nullptr, nullptr, f, df);
-      plan_flux_d(x, P.t, uR, nullptr, nullptr, n, duR, nullptr, nullptr, fR, dfR);
+      plan_flux_d(x, P.t, uL, nullptr, wp, n, duL, nullptr, dwp, f, df);
+      plan_flux_d(x, P.t, uR, nullptr, wp, n, duR, nullptr, dwp, fR, dfR);
       plan_ws_d(x, P.t, uL, nullptr, nullptr, n, duL, nullptr, nullptr, &lamL, &dlamL);
       plan_ws_d(x, P.t, uR, nullptr, nullptr, n, duR, nullptr, nullptr, &lamR, &dlamR);
     } else {
-      plan_flux(x, P.t, uL, nullptr, nullptr, n, f);
-      plan_flux(x, P.t, uR, nullptr, nullptr, n, fR);
+      plan_flux(x, P.t, uL, nullptr, wp, n, f);
+      plan_flux(x, P.t, uR, nullptr, wp, n, fR);
       plan_ws(x, P.t, uL, nullptr, nullptr, n, &lamL);
       plan_ws(x, P.t, uR, nullptr, nullptr, n, &lamR);
     }
@@ -400,7 +449,7 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
     }
     return;
   }
-  // kind D: f(u^, q^) . n + tau (u^- - u^) (disc.py:657-722)
+  // kind D / W: f(u^, q^, w^) . n + tau (u^- - u^) (disc.py:657-722)
   double uh[NCU], duh[NCU], qh[NVQ > 0 ? NVQ : 1], dqh[NVQ > 0 ? NVQ : 1];
 #pragma unroll
   for (int c = 0; c < NCU; ++c) {
@@ -416,8 +465,8 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
       dqh[k] = GRAD_CENTERED ? 0.5 * (dl + dr) : (sw ? dr : dl);
     }
   }
-  if (TANGENT) plan_flux_d(x, P.t, uh, qh, nullptr, n, duh, dqh, nullptr, f, df);
-  else plan_flux(x, P.t, uh, qh, nullptr, n, f);
+  if (TANGENT) plan_flux_d(x, P.t, uh, qh, wp, n, duh, dqh, dwp, f, df);
+  else plan_flux(x, P.t, uh, qh, wp, n, f);
   double tau = tau0;
   if (HAS_WS) {
     double ll, lr;
@@ -476,13 +525,15 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
     phys_point(P, e, xi, x);
     double f[NCU * ND], df[NCU * ND], s[NCU], ds[NCU];
     const double* qv = NVQ ? val + NCU : nullptr;
+    const double* wv = NW ? val + OW : nullptr;
     if (TANGENT) {
       const double* dqv = NVQ ? val + NV + NCU : nullptr;
-      plan_flux_d(x, P.t, val, qv, nullptr, nullptr, val + NV, dqv, nullptr, f, df);
-      plan_src_d(x, P.t, val, qv, nullptr, nullptr, val + NV, dqv, nullptr, s, ds);
+      const double* dwv = NW ? val + NV + OW : nullptr;
+      plan_flux_d(x, P.t, val, qv, wv, nullptr, val + NV, dqv, dwv, f, df);
+      plan_src_d(x, P.t, val, qv, wv, nullptr, val + NV, dqv, dwv, s, ds);
     } else {
-      plan_flux(x, P.t, val, qv, nullptr, nullptr, f);
-      plan_src(x, P.t, val, qv, nullptr, nullptr, s);
+      plan_flux(x, P.t, val, qv, wv, nullptr, f);
+      plan_src(x, P.t, val, qv, wv, nullptr, s);
     }
     const double wd = c_qw[p] * detj;
 #pragma unroll
@@ -727,5 +778,121 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mass_inv(const __grid_consta
   for (int idx = tid; idx < NCU * NB; idx += NT) {
     const int a = idx / NCU, c = idx % NCU;
     P.out[(sz_t)e * NB * NCU + idx] = inv * res[c * NB + a];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plain element mass on the (ncu, nd) gradient block: out = scale * M v,
+// M_ab = int phi_a phi_b (disc.py:919-921, Mq = mass @ vq; with scale = -1
+// and v = the lifted gradient it forms the wave gradient residual Rq)
+// ---------------------------------------------------------------------------
+constexpr int NQC = NCU * ND;
+extern "C" __global__ void __launch_bounds__(NT) nl_mass_q(const __grid_constant__ NlParams P) {
+  extern __shared__ __align__(16) double smem_q[];
+  double* bA = smem_q;
+  double* bB = smem_q + NQC * MX;
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (e >= P.ne) return;
+  for (int idx = tid; idx < NQC * NB; idx += NT) {
+    const int v = idx / NB, a = idx % NB;
+    bA[idx] = P.q[((sz_t)e * NB + a) * NQC + v];
+  }
+  __syncthreads();
+  double* vq;
+  to_quad(bA, bB, NQC, tid, vq);
+  double* fld = vq == bA ? bB : bA;
+  const double detj = P.geo[(sz_t)e * (1 + ND * ND)];
+  for (int idx = tid; idx < NQC * NQ; idx += NT) fld[idx] = c_qw[idx % NQ] * detj * vq[idx];
+  __syncthreads();
+  double* other = fld == bA ? bB : bA;
+  auto phi = [](int) { return (int)OP_PHI; };
+  double* res;
+  if (ND == 3) {
+    contract<NQ1, NQ1, NQ1, 0, NQ1, N1, true>(fld, other, NQC, tid, phi);
+    __syncthreads();
+    contract<N1, NQ1, NQ1, 1, NQ1, N1, true>(other, fld, NQC, tid, phi);
+    __syncthreads();
+    contract<N1, N1, NQ1, 2, NQ1, N1, true>(fld, other, NQC, tid, phi);
+    __syncthreads();
+    res = other;
+  } else {
+    contract<NQ1, NQ1, 1, 0, NQ1, N1, true>(fld, other, NQC, tid, phi);
+    __syncthreads();
+    contract<N1, NQ1, 1, 1, NQ1, N1, true>(other, fld, NQC, tid, phi);
+    __syncthreads();
+    res = fld;
+  }
+  for (int idx = tid; idx < NQC * NB; idx += NT) {
+    const int a = idx / NQC, v = idx % NQC;
+    P.out[(sz_t)e * NB * NQC + idx] = P.scale * res[v * NB + a];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pointwise ODE block, collocated at the solution nodes (disc.py:876-893):
+// Rw = beta w - s_w(x, t, u, q, w), tangent beta dw - ds_w
+// ---------------------------------------------------------------------------
+template <bool TANGENT>
+__device__ __forceinline__ void ode_body(const NlParams& P) {
+  const sz_t idx = (sz_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (NW == 0 || idx >= (sz_t)P.ne * NB) return;
+  const int e = (int)(idx / NB), a = (int)(idx % NB);
+  double x[ND];
+  phys_point(P, e, &c_xn[a * ND], x);
+  double val[2 * (NV > 0 ? NV : 1)];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    val[v] = state_at(P, 0, v, (sz_t)e, a);
+    val[NV + v] = TANGENT ? state_at(P, 1, v, (sz_t)e, a) : 0.0;
+  }
+  const double* qv = NVQ ? val + NCU : nullptr;
+  const double* dqv = NVQ ? val + NV + NCU : nullptr;
+  double sw[NW > 0 ? NW : 1], dsw[NW > 0 ? NW : 1];
+  if (TANGENT) plan_sw_d(x, P.t, val, qv, val + OW, nullptr, val + NV, dqv, val + NV + OW, sw, dsw);
+  else plan_sw(x, P.t, val, qv, val + OW, nullptr, sw);
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    flag(P, e, sw[k]);
+    P.out[idx * NW + k] = TANGENT ? ODE_BETA * val[NV + OW + k] - dsw[k]
+                                  : ODE_BETA * val[OW + k] - sw[k];
+  }
+}
+
+extern "C" __global__ void nl_ode(const __grid_constant__ NlParams P) { ode_body<false>(P); }
+extern "C" __global__ void nl_ode_tangent(const __grid_constant__ NlParams P) { ode_body<true>(P); }
+
+// M^-1 on the (ncu, nd) gradient block (MassPreconditioner, driver.py:99-106)
+extern "C" __global__ void __launch_bounds__(NT) nl_mass_inv_q(const __grid_constant__ NlParams P) {
+  extern __shared__ __align__(16) double smem_iq[];
+  double* bA = smem_iq;
+  double* bB = smem_iq + NQC * NB;
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (e >= P.ne) return;
+  for (int idx = tid; idx < NQC * NB; idx += NT) {
+    const int v = idx / NB, a = idx % NB;
+    bA[idx] = P.q[((sz_t)e * NB + a) * NQC + v];
+  }
+  __syncthreads();
+  auto mi = [](int) { return (int)OP_M1INV; };
+  double* res;
+  if (ND == 3) {
+    contract<N1, N1, N1, 0, N1, N1, false>(bA, bB, NQC, tid, mi);
+    __syncthreads();
+    contract<N1, N1, N1, 1, N1, N1, false>(bB, bA, NQC, tid, mi);
+    __syncthreads();
+    contract<N1, N1, N1, 2, N1, N1, false>(bA, bB, NQC, tid, mi);
+    __syncthreads();
+    res = bB;
+  } else {
+    contract<N1, N1, 1, 0, N1, N1, false>(bA, bB, NQC, tid, mi);
+    __syncthreads();
+    contract<N1, N1, 1, 1, N1, N1, false>(bB, bA, NQC, tid, mi);
+    __syncthreads();
+    res = bA;
+  }
+  const double inv = P.scale / P.geo[(sz_t)e * (1 + ND * ND)];
+  for (int idx = tid; idx < NQC * NB; idx += NT) {
+    const int a = idx / NQC, v = idx % NQC;
+    P.out[(sz_t)e * NB * NQC + idx] = inv * res[v * NB + a];
   }
 }

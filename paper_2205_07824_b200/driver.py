@@ -27,7 +27,11 @@ class TimeIntError(RuntimeError):
 
 
 def _steady_fns(system):
-    """Flat device closures R(u) and J(u) v at t = 0 (driver.py:224-234)."""
+    """Flat device closures R(u) and J(u) v at t = 0 (driver.py:224-234);
+    packed (u | q | w) vectors for kind W / ODE systems."""
+    if getattr(system, "multi_block", False):
+        return (lambda Y: system.residual_packed_dev(Y, 0.0),
+                lambda Y, V: system.tangent_packed_dev(V, Y, 0.0))
     shape = (system.n_elements, system.n_nodes, system.ncu)
 
     def residual(uflat):
@@ -47,6 +51,8 @@ class MassPreconditioner:
 
     def apply(self, r):
         s = self.system
+        if getattr(s, "multi_block", False):
+            return s.mass_inv_packed_dev(r)
         return s.mass_inv_dev(r.reshape(s.n_elements, s.n_nodes, s.ncu)).reshape(-1)
 
 
@@ -56,6 +62,9 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
     (driver.py:119-125)."""
     if jv_mode != "tangent":
         raise DriverError("the B200 block-Jacobi build probes the tangent operator")
+    if getattr(system, "multi_block", False):
+        raise DriverError("block-Jacobi on packed (u, q, w) systems is not supported on the "
+                          "B200 path; use the mass preconditioner")
     if colors is None:
         colors = distance2_coloring(element_neighbor_sets(system.topology, system.n_elements))
     return build_block_jacobi(tangent_fn, state_vec, system.n_elements,
@@ -96,6 +105,18 @@ def solve_steady(system, state, newton_options=None, precond=None, callback=None
                                   t=t).reshape(-1)
 
     import torch
+    if getattr(system, "multi_block", False):
+        def dev(a):
+            return None if a is None else torch.as_tensor(
+                a if isinstance(a, torch.Tensor) else np.ascontiguousarray(a, dtype=np.float64),
+                device=system.device)
+        x0 = system.pack(dev(state.u), dev(state.q), dev(state.w))
+        x, stats = newton_solve(lambda Y: system.residual_packed_dev(Y, t), x0, opts,
+                                precond=precond,
+                                tangent_fn=lambda Y, V: system.tangent_packed_dev(V, Y, t),
+                                callback=callback)
+        u, q, w = system.unpack(x)
+        return SolverState(u=u, q=q, w=w, t=t), stats
     u0 = state.u if isinstance(state.u, torch.Tensor) else torch.as_tensor(
         np.ascontiguousarray(state.u, dtype=np.float64), device=system.device)
     x, stats = newton_solve(residual, u0.reshape(-1).cuda(), opts, precond=precond,
@@ -214,6 +235,19 @@ def _stage_functions(system, Yk, a_dt, t_stage):
     M(U) dU/(a dt) + (dM/dU dU)(U - U_k)/(a dt) + dR (timeint.py:132-165)."""
     shape = (system.n_elements, system.n_nodes, system.ncu)
     inv = 1.0 / a_dt
+    if getattr(system, "multi_block", False):
+        def stage_residual_p(Y):
+            return system.mass_packed_dev(Y - Yk, Y, t_stage, inv) + \
+                system.residual_packed_dev(Y, t_stage)
+
+        def stage_tangent_p(Y, V):
+            M = system.mass_packed_dev(V, Y, t_stage, inv)
+            extra = system.mass_extra_packed_dev(Y - Yk, V, Y, t_stage, inv)
+            if extra is not None:
+                M = M + extra
+            return M + system.tangent_packed_dev(V, Y, t_stage)
+
+        return stage_residual_p, stage_tangent_p
 
     def stage_residual(Y):
         Ys = Y.reshape(shape)
@@ -239,9 +273,15 @@ def advance_step(system, state, dt, tableau, newton_options=None, precond=None, 
     if dt <= 0:
         raise TimeIntError("dt must be positive")
     opts = newton_options or NewtonOptions()
-    u = state.u if isinstance(state.u, torch.Tensor) else torch.as_tensor(
-        np.ascontiguousarray(state.u, dtype=np.float64), device=system.device)
-    Y0 = u.reshape(-1).to(system.device).clone()
+
+    def dev(a):
+        return None if a is None else (a if isinstance(a, torch.Tensor) else torch.as_tensor(
+            np.ascontiguousarray(a, dtype=np.float64))).to(system.device)
+
+    if getattr(system, "multi_block", False):
+        Y0 = system.pack(dev(state.u), dev(state.q), dev(state.w)).clone()
+    else:
+        Y0 = dev(state.u).reshape(-1).clone()
     K, stats, Ylast = [], StepStats(), None
     for i in range(tableau.stages):
         Yk = Y0.clone()
@@ -266,5 +306,8 @@ def advance_step(system, state, dt, tableau, newton_options=None, precond=None, 
             Ynew += dt * bi * Ki
     if not bool(torch.isfinite(Ynew).all()):
         raise TimeIntError("non-finite state after time step")
+    if getattr(system, "multi_block", False):
+        u, q, w = system.unpack(Ynew)
+        return SolverState(u=u, q=q, w=w, t=state.t + dt), stats
     shape = (system.n_elements, system.n_nodes, system.ncu)
     return SolverState(u=Ynew.reshape(shape), q=None, w=None, t=state.t + dt), stats

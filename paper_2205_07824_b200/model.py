@@ -318,7 +318,20 @@ def _compressible_ns(nd):
                     init={"u1": "1", "u2": "0", "u3": "0", "u4": "2.5"})
 
 
+def _wave(nd):
+    """Scalar wave equation, kind W (model.py:715-727 restated): du/dt +
+    c^2 div(q) = 0, dq/dt + grad(u) = 0, displacement dw/dt = u; c = mu1."""
+    nd = _nd("wave", nd, (1, 2, 3))
+    init = {"u1": "0", "w1": "0"}
+    init.update({f"q1_{j + 1}": "0" for j in range(nd)})
+    return PdeModel(kind="W", ncu=1, nd=nd, nw=1, nparam=1, mass=["1"],
+                    flux=[f"mu1*mu1*q1_{j + 1}" for j in range(nd)], source=["0"],
+                    ode=OdeSpec(alpha=1.0, beta=0.0, sw=["u1"]), mu=np.array([1.0]),
+                    wavespeed="mu1", init=init)
+
+
 _BUILTINS = {
+    "wave": _wave,
     "shallow_water": _shallow_water,
     "compressible_ns": _compressible_ns,
     "poisson": _poisson,

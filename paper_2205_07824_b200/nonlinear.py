@@ -45,7 +45,7 @@ class NlParams(C.Structure):
     _fields_ = [("ne", C.c_int32), ("nbface", C.c_int32), ("t", C.c_double),
                 ("scale", C.c_double)] + [(k, C.c_void_p) for k in (
                     "geo", "xmap", "fnbr", "finfo", "fgeo", "nmap", "gq", "gproj",
-                    "u", "q", "du", "dq", "out", "bad")]
+                    "u", "q", "du", "dq", "w", "dw", "out", "bad")]
 
 
 def linear_path_reason(model):
@@ -53,6 +53,8 @@ def linear_path_reason(model):
     else why the generated path is needed."""
     if model.kind != "D":
         return f"kind {model.kind}"
+    if model.nw > 0:
+        return "pointwise ODE block"
     if model.ncu > 3:
         return "ncu > 3"
     mu = model.mu_bindings()
@@ -149,6 +151,8 @@ class NlTables(TensorTables):
         out = np.zeros((nbf, nqf, self.ncu))
         mu = self.model.mu_bindings()
         for tag, bc, idx in self.bc_groups:
+            if bc.type == "absorbing":
+                continue
             plan = self.model.bc_plan(tag)
             for lf in range(self.nf):
                 s = idx[self.fb[idx] == lf]
@@ -187,17 +191,21 @@ def generate_source(tab):
         raise DiscError("kind C models need a wavespeed for the LLF flux")
     if ws is not None and (codegen.uses(ws, "q") or codegen.uses(ws, "w")):
         raise DiscError("wavespeed plans may read x, t, u, n only")
-    if any(codegen.uses(p, "w") for p in (flux, src, mass)):
-        raise DiscError("ODE states are not supported on the generated path")
-    if codegen.uses(mass, "q"):
-        raise DiscError("the mass may not read q (kind D states carry none)")
+    if codegen.uses(mass, "q") or codegen.uses(mass, "w"):
+        raise DiscError("the mass may read x, t, u only on the generated path")
+    absorbing = any(bc.type == "absorbing" for _, bc, _ in tab.bc_groups)
+    if absorbing and (ws is None or codegen.uses(ws, "u") or codegen.uses(ws, "x")):
+        raise DiscError("absorbing boundaries need a wavespeed independent of u and x "
+                        "(the gradient lift takes u^ at the face nodes)")
+    nw = model.nw
+    sw = model.sw_plan() if nw > 0 else None
     if tab.periodic and (codegen.uses(flux, "x") or (ws is not None and codegen.uses(ws, "x"))):
         raise DiscError("face plans reading x on periodic meshes are not supported")
     mforms = affine_form(mass, mu, set())
     mass_const = mforms is not None
     n1, nq1 = tab.n1, tab.nq1
     nvq = 0 if model.kind == "C" else ncu * nd
-    nv = ncu + nvq
+    nv = ncu + nvq + nw
     kmax = max(n1, nq1)
     mx, mxf = kmax ** nd, kmax ** (nd - 1)
     nq, nb = nq1 ** nd, n1 ** nd
@@ -207,7 +215,11 @@ def generate_source(tab):
     if nd == 3:
         nt = max(nt, 128)
     ng = ncu * (nd + 1)
-    defs = dict(ND=nd, N1=n1, NQ1=nq1, NCU=ncu, KIND_C=int(model.kind == "C"),
+    ode = model.ode
+    defs = dict(ND=nd, N1=n1, NQ1=nq1, NCU=ncu, NW=nw, KIND_C=int(model.kind == "C"),
+                KIND_W=int(model.kind == "W"),
+                ODE_ALPHA=codegen.literal(ode.alpha if ode is not None else 1.0),
+                ODE_BETA=codegen.literal(ode.beta if ode is not None else 0.0),
                 HAS_WS=int(ws is not None), TRACE_CENTERED=int(model.numflux.trace == "centered"),
                 GRAD_CENTERED=int(model.numflux.grad_trace == "centered"),
                 MASS_CONST=int(mass_const), NT=nt)
@@ -218,7 +230,7 @@ def generate_source(tab):
         mc[:] = [f[1] for f in mforms]
     consts = dict(c_phi=m.phi1d, c_dphi=m.dphi1d, c_d1=tab.d1, c_clo=tab.clo, c_chi=tab.chi,
                   c_m1inv=tab.m1inv, c_xq1=m.quad1d[0], c_qw=m.quad_wts, c_fxi=tab.fxi,
-                  c_fw=tab.fw, c_mass=mc)
+                  c_fw=tab.fw, c_mass=mc, c_xn=m.nodes)
     for k, v in consts.items():
         lines.append(f"__constant__ double {k}[{np.size(v)}] = {_arr(v, k)};")
     lines.append(codegen.DEVICE_HELPERS)
@@ -229,6 +241,7 @@ def generate_source(tab):
     else:
         lines.append(codegen.emit_plan(_ZeroPlan(1), "plan_ws", nd, mu))
     lines.append(codegen.emit_plan(mass, "plan_mass", nd, mu))
+    lines.append(codegen.emit_plan(sw if sw is not None else _ZeroPlan(1), "plan_sw", nd, mu))
     src_text = "\n".join(lines) + "\n" + TEMPLATE.read_text()
     shapes = dict(defs, NB=nb, NQ=nq, NV=nv, MX=mx, MXF=mxf, NG=ng)
     return src_text, shapes
@@ -297,6 +310,8 @@ class NlOperator:
         nvm = ncu if s["MASS_CONST"] else 3 * ncu
         self.smem["nl_mass"] = self.smem["nl_mass_extra"] = 8 * 2 * max(nvm, ncu) * mx
         self.smem["nl_mass_inv"] = 8 * 2 * ncu * nb
+        self.smem["nl_mass_q"] = 8 * 2 * ncu * tab.nd * mx
+        self.smem["nl_mass_inv_q"] = 8 * 2 * ncu * tab.nd * nb
 
     def __del__(self):
         h = getattr(self, "_mod", None)
@@ -348,33 +363,71 @@ class NlOperator:
         return torch.empty(shape, dtype=torch.float64, device=self.device)
 
     # -- operators -------------------------------------------------------------
-    def mixed(self, u, t=0.0, homogeneous=False, out=None):
+    def mixed(self, u, t=0.0, homogeneous=False, out=None, state_q=None):
+        """M^-1 (lifted gradient form) of u; `state_q` (kind W) is the state
+        gradient absorbing boundaries take u^ from."""
         tab = self.tab
         q = out if out is not None else self._empty((tab.ne, self.shape["NB"], tab.ncu, tab.nd))
-        P = self._params(t, u=u, out=q, gproj=None if homogeneous else self.gproj(t))
+        P = self._params(t, u=u, q=state_q, out=q,
+                         gproj=None if homogeneous else self.gproj(t))
         nb = self.shape["NB"]
         epb = 1 if nb >= 128 else 128 // nb
         self._launch("nl_mixed", (tab.ne + epb - 1) // epb, epb * nb, P)
         return q
 
-    def residual(self, u, t=0.0, q=None, out=None):
+    def residual(self, u, t=0.0, q=None, w=None, out=None):
+        """Ru; q is the state gradient (kind W) or the mixed gradient (kind D,
+        computed when not given); w the ODE states."""
         R = out if out is not None else self._empty(u.shape)
         if self.tab.model.kind == "D" and q is None:
             q = self.mixed(u, t)
-        P = self._params(t, u=u, q=q, out=R, gq=self.gq(t))
+        P = self._params(t, u=u, q=q, w=w, out=R, gq=self.gq(t))
         self._launch("nl_residual", self.tab.ne, self.shape["NT"], P)
         return R
 
-    def tangent(self, u, du, t=0.0, q=None, out=None):
+    def tangent(self, u, du, t=0.0, q=None, w=None, dq=None, dw=None, out=None):
+        """dRu (the reference linearisation); kind D derives dq from du by
+        the homogeneous lift, kind W takes the state direction dq."""
         R = out if out is not None else self._empty(du.shape)
-        dq = None
         if self.tab.model.kind == "D":
             if q is None:
                 q = self.mixed(u, t)
             dq = self.mixed(du, t, homogeneous=True)
-        P = self._params(t, u=u, q=q, du=du, dq=dq, out=R, gq=self.gq(t))
+        P = self._params(t, u=u, q=q, du=du, dq=dq, w=w, dw=dw, out=R, gq=self.gq(t))
         self._launch("nl_tangent", self.tab.ne, self.shape["NT"], P)
         return R
+
+    def gradient_residual(self, u, q, t=0.0, tangent=False, out=None):
+        """Kind W gradient equation, Rq = -(lifted gradient form)
+        (disc.py:866-874): the lift of (u, q) -- or of the direction (du, dq)
+        with homogeneous Dirichlet data -- times the element mass."""
+        tab = self.tab
+        qt = self.mixed(u, t, homogeneous=tangent, state_q=q)
+        o = out if out is not None else self._empty(qt.shape)
+        P = self._params(t, -1.0, q=qt, out=o)
+        self._launch("nl_mass_q", tab.ne, self.shape["NT"], P)
+        return o
+
+    def mass_q(self, v, scale=1.0, out=None):
+        o = out if out is not None else self._empty(v.shape)
+        P = self._params(0.0, scale, q=v, out=o)
+        self._launch("nl_mass_q", self.tab.ne, self.shape["NT"], P)
+        return o
+
+    def mass_inv_q(self, v, out=None):
+        o = out if out is not None else self._empty(v.shape)
+        P = self._params(0.0, 1.0, q=v, out=o)
+        self._launch("nl_mass_inv_q", self.tab.ne, self.shape["NT"], P)
+        return o
+
+    def ode(self, u, q, w, t=0.0, du=None, dq=None, dw=None, out=None):
+        """Rw = beta w - s_w (or its tangent when du is given), at the nodes."""
+        tab = self.tab
+        o = out if out is not None else self._empty(w.shape)
+        P = self._params(t, u=u, q=q, w=w, du=du, dq=dq, dw=dw, out=o)
+        n = tab.ne * self.shape["NB"]
+        self._launch("nl_ode_tangent" if du is not None else "nl_ode", (n + 127) // 128, 128, P)
+        return o
 
     def mass(self, v, u=None, t=0.0, scale=1.0, out=None):
         o = out if out is not None else self._empty(v.shape)

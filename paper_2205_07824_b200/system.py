@@ -238,17 +238,49 @@ class LdgSystem:
         return self.master.n_nodes
 
     def block_shapes(self):
-        return [("u", (self.n_elements, self.n_nodes, self.ncu))]
+        """disc.py:320-326: u, then q for kind W, then w for ODE blocks."""
+        ne, nb = self.n_elements, self.n_nodes
+        shapes = [("u", (ne, nb, self.ncu))]
+        if self.kind == "W":
+            shapes.append(("q", (ne, nb, self.ncu, self.nd)))
+        if self.nw > 0:
+            shapes.append(("w", (ne, nb, self.nw)))
+        return shapes
+
+    @property
+    def multi_block(self):
+        """True when the packed state carries q (kind W) or w (ODE) blocks."""
+        return self.kind == "W" or self.nw > 0
 
     @property
     def n_dofs(self):
-        return self.n_elements * self.n_nodes * self.ncu
+        return sum(int(np.prod(s)) for _, s in self.block_shapes())
 
     def pack(self, u, q=None, w=None):
-        return u.reshape(-1) if hasattr(u, "is_cuda") else np.ravel(u)
+        """disc.py:333-339 (numpy or torch)."""
+        parts = [u]
+        if self.kind == "W":
+            parts.append(q)
+        if self.nw > 0:
+            parts.append(w)
+        if hasattr(u, "is_cuda"):
+            import torch
+            if len(parts) == 1:
+                return u.reshape(-1)
+            return torch.cat([p.reshape(-1) for p in parts])
+        return np.concatenate([np.ravel(p) for p in parts])
 
     def unpack(self, vec):
-        return vec[: self.n_dofs].reshape(self.block_shapes()[0][1]), None, None
+        """disc.py:341-351: views of the packed blocks."""
+        out, k = [], 0
+        for _, shape in self.block_shapes():
+            n = int(np.prod(shape))
+            out.append(vec[k:k + n].reshape(shape))
+            k += n
+        u = out[0]
+        q = out[1] if self.kind == "W" else None
+        w = out[-1] if self.nw > 0 else None
+        return u, q, w
 
     def state_from_vector(self, vec, t):
         u, q, w = self.unpack(vec)
@@ -500,6 +532,8 @@ class LdgSystem:
 
     def compute_mixed(self, u, t, homogeneous=False):
         """disc.py:436-449."""
+        if self.kind != "D":
+            raise DiscError("compute_mixed applies to diffusion models")
         ud, dev = self._dev(u)
         q = self.mixed_dev(ud.reshape(self.n_elements, self.n_nodes, self.ncu), t, homogeneous)
         if dev != "cuda":
@@ -511,8 +545,27 @@ class LdgSystem:
         return (isinstance(x, torch.Tensor) and not x.is_cuda and self.nl is None
                 and not self.dense and getattr(self, "_h", None) is not None)
 
+    def _packed_host(self, fn, state, *vecs):
+        """Run a packed device operator on reference-shaped blocks; returns
+        the (u, q, w) blocks like the reference."""
+        blocks = [self._dev(b)[0] if b is not None else None for b in
+                  (state.u, state.q, state.w)]
+        dev = self._dev(state.u)[1]
+        Y = self._cat([b for b in blocks if b is not None])
+        args = []
+        for v in vecs:
+            vb = [self._dev(b)[0] if b is not None else None for b in v]
+            args.append(self._cat([b for b in vb if b is not None]))
+        out = fn(*args, Y)
+        self._check_nan("flux")
+        u, q, w = self.unpack(out)
+        return (self._ret(u, dev), None if q is None else self._ret(q, dev),
+                None if w is None else self._ret(w, dev))
+
     def residual(self, state):
-        """disc.py:588-589 -> (Ru, None, None)."""
+        """disc.py:588-589 -> (Ru, Rq, Rw)."""
+        if self.nl is not None and self.multi_block:
+            return self._packed_host(lambda Y: self.residual_packed_dev(Y, state.t), state)
         if self._pipelined(state.u):
             R = self._host_pipeline(state.u, False, state.t)
             self._check_nan("flux")
@@ -525,6 +578,9 @@ class LdgSystem:
 
     def residual_tangent(self, state, du, dq=None, dw=None):
         """disc.py:591-593 (the reference linearisation)."""
+        if self.nl is not None and self.multi_block:
+            return self._packed_host(lambda V, Y: self.tangent_packed_dev(V, Y, state.t),
+                                     state, (du, dq, dw))
         if self._pipelined(du):
             R = self._host_pipeline(du, True, state.t)
             self._check_nan("flux")
@@ -541,6 +597,9 @@ class LdgSystem:
 
     def mass_apply(self, state, vu, vq=None, vw=None):
         """disc.py:897-925."""
+        if self.nl is not None and self.multi_block:
+            return self._packed_host(lambda V, Y: self.mass_packed_dev(V, Y, state.t),
+                                     state, (vu, vq, vw))
         vd, dev = self._dev(vu)
         shape = (self.n_elements, self.n_nodes, self.ncu)
         base = None if self.mass_is_constant else self._dev(state.u)[0].reshape(shape)
@@ -559,6 +618,64 @@ class LdgSystem:
                                           self._dev(state.u)[0].reshape(shape), state.t)
         return self._ret(out, dev)
 
+    # -- packed multi-block operators (kind W / ODE blocks; generated path) ------------------
+    def _blocks_dev(self, Y):
+        return self.unpack(Y)
+
+    def _cat(self, parts):
+        import torch
+        return torch.cat([p.reshape(-1) for p in parts if p is not None])
+
+    def residual_packed_dev(self, Y, t=0.0):
+        """[Ru | Rq | Rw] of a packed device state (disc.py:595-653, 866-893)."""
+        u, q, w = self._blocks_dev(Y)
+        qq = self.base_mixed(u, t) if self.kind == "D" else q
+        Ru = self.nl.residual(u, t, q=qq, w=w)
+        Rq = self.nl.gradient_residual(u, q, t) if self.kind == "W" else None
+        Rw = self.nl.ode(u, qq, w, t) if self.nw > 0 else None
+        return self._cat([Ru, Rq, Rw])
+
+    def tangent_packed_dev(self, V, Y, t=0.0):
+        """The reference linearisation on packed vectors."""
+        u, q, w = self._blocks_dev(Y)
+        du, dq, dw = self._blocks_dev(V)
+        qq, dqq = q, dq
+        if self.kind == "D":
+            qq = self.base_mixed(u, t)
+            dqq = self.nl.mixed(du, t, homogeneous=True) if self.nw > 0 else None
+        dRu = self.nl.tangent(u, du, t, q=qq, w=w, dq=dq, dw=dw)
+        dRq = self.nl.gradient_residual(du, dq, t, tangent=True) if self.kind == "W" else None
+        dRw = self.nl.ode(u, qq, w, t, du=du, dq=dqq, dw=dw) if self.nw > 0 else None
+        return self._cat([dRu, dRq, dRw])
+
+    def mass_packed_dev(self, V, Y, t=0.0, scale=1.0):
+        """[M(u) vu | M vq | alpha vw] (disc.py:897-925)."""
+        u, _, _ = self._blocks_dev(Y)
+        vu, vq, vw = self._blocks_dev(V)
+        Mu = self.nl.mass(vu, u, t, scale)
+        Mq = self.nl.mass_q(vq, scale) if self.kind == "W" else None
+        Mw = (scale * self.model.ode.alpha) * vw if self.nw > 0 else None
+        return self._cat([Mu, Mq, Mw])
+
+    def mass_extra_packed_dev(self, Yd, V, Y, t=0.0, scale=1.0):
+        """(dm/du du) y on the u block, zero elsewhere (disc.py:927-948)."""
+        import torch
+        if self.mass_is_constant:
+            return None
+        u, _, _ = self._blocks_dev(Y)
+        du, _, _ = self._blocks_dev(V)
+        yu, _, _ = self._blocks_dev(Yd)
+        out = torch.zeros_like(V)
+        out[: u.numel()].copy_(self.nl.mass_extra(yu, u, du, t, scale).reshape(-1))
+        return out
+
+    def mass_inv_packed_dev(self, V):
+        """MassPreconditioner.apply on packed vectors (driver.py:99-106)."""
+        vu, vq, vw = self._blocks_dev(V)
+        return self._cat([self.nl.mass_inv(vu),
+                          self.nl.mass_inv_q(vq) if self.kind == "W" else None,
+                          vw / self.model.ode.alpha if self.nw > 0 else None])
+
     def interpolate_initial(self):
         """disc.py:420-432 (host evaluation of the init plan at the nodes)."""
         from .expr import evaluate
@@ -574,5 +691,14 @@ class LdgSystem:
         B = self.n_elements * self.n_nodes
         if v.shape[1] != B:
             v = np.broadcast_to(v, (v.shape[0], B))
-        u = np.moveaxis(v.reshape((v.shape[0], self.n_elements, self.n_nodes)), 0, -1)
-        return SolverState(u=np.ascontiguousarray(u[..., : self.ncu]), q=None, w=None, t=0.0)
+        vals = np.moveaxis(v.reshape((v.shape[0], self.n_elements, self.n_nodes)), 0, -1)
+        k = self.ncu
+        u = np.ascontiguousarray(vals[..., :k])
+        q = w = None
+        if self.kind == "W":
+            q = np.ascontiguousarray(vals[..., k:k + self.ncu * self.nd]).reshape(
+                self.n_elements, self.n_nodes, self.ncu, self.nd)
+            k += self.ncu * self.nd
+        if self.nw > 0:
+            w = np.ascontiguousarray(vals[..., k:k + self.nw])
+        return SolverState(u=u, q=q, w=w, t=0.0)

@@ -191,12 +191,14 @@ class TensorTables:
             raise DiscError("master element kind does not match the mesh")
         if kind not in ("quad", "hex"):
             raise DiscError(f"B200 tensor path needs quad/hex elements, got {kind}")
-        if model.kind not in (("C", "D") if nonlinear else ("D",)):
-            raise DiscError(f"B200 path supports kind C/D models, got {model.kind}"
+        if model.kind not in (("C", "D", "W") if nonlinear else ("D",)):
+            raise DiscError(f"B200 path supports kind C/D/W models, got {model.kind}"
                             if nonlinear else
                             f"linear B200 path supports kind D models, got {model.kind}")
-        if model.nw > 0 or model.numflux.uhat is not None or model.numflux.fhat is not None:
-            raise DiscError("ODE blocks and u^/f^ overrides are not supported on the B200 path")
+        if (model.nw > 0 and not nonlinear) or model.numflux.uhat is not None or \
+                model.numflux.fhat is not None:
+            raise DiscError("u^/f^ overrides are not supported on the B200 path (ODE blocks "
+                            "run on the generated path)")
         self.nd, self.p, self.ncu = mesh.nd, master.p, model.ncu
         self.n1 = master.p + 1
         if self.n1 > 7 or self.ncu > (5 if nonlinear else 3):
@@ -397,12 +399,15 @@ class TensorTables:
             if bc.type == "periodic":
                 raise DiscError(f"tag {tag} is periodic in the model but was not "
                                 "paired in the mesh topology")
-            if bc.type not in ("dirichlet", "neumann"):
+            if bc.type == "absorbing" and model.kind != "W":
+                raise DiscError("absorbing boundaries require a wave model")   # disc.py:300-301
+            if bc.type not in ("dirichlet", "neumann") and not (
+                    self.nonlinear and bc.type == "absorbing"):
                 raise DiscError(f"boundary type {bc.type!r} is not supported on the B200 path")
             self.bc_groups.append((tag, bc, np.nonzero(tb == tag)[0]))
         kinds = np.zeros(eb.size, dtype=np.int32)
         for tag, bc, idx in self.bc_groups:
-            kinds[idx] = 1 if bc.type == "dirichlet" else 2
+            kinds[idx] = {"dirichlet": 1, "neumann": 2, "absorbing": 3}[bc.type]
         nb_ = np.zeros((eb.size, self.nd))
         area_b = np.zeros(eb.size)
         for lf in range(nf):
@@ -516,6 +521,8 @@ class TensorTables:
         mu = model.mu_bindings()
         w = m.faces[0].weights
         for tag, bc, idx in self.bc_groups:
+            if bc.type == "absorbing":
+                continue
             plan = model.bc_plan(tag)
             for lf in range(self.nf):
                 s = idx[self.fb[idx] == lf]
@@ -704,12 +711,15 @@ class DenseTables:
             if tag not in model.bcs:
                 raise DiscError(f"mesh boundary tag {tag} has no [bc] entry")
             bc = model.bcs[tag]
-            if bc.type not in ("dirichlet", "neumann"):
+            if bc.type == "absorbing" and model.kind != "W":
+                raise DiscError("absorbing boundaries require a wave model")   # disc.py:300-301
+            if bc.type not in ("dirichlet", "neumann") and not (
+                    self.nonlinear and bc.type == "absorbing"):
                 raise DiscError(f"boundary type {bc.type!r} is not supported on the B200 path")
             self.bc_groups.append((tag, bc, np.nonzero(tb == tag)[0]))
         kinds = np.zeros(eb.size, dtype=np.int32)
         for tag, bc, idx in self.bc_groups:
-            kinds[idx] = 1 if bc.type == "dirichlet" else 2
+            kinds[idx] = {"dirichlet": 1, "neumann": 2, "absorbing": 3}[bc.type]
         nb_ = np.zeros((eb.size, self.nd))
         area_b = np.zeros(eb.size)
         for lf in range(nf):
@@ -769,6 +779,8 @@ class DenseTables:
         out = np.zeros((self.n_boundary, self.nqf, self.ncu))
         model = self.model
         for tag, bc, idx in self.bc_groups:
+            if bc.type == "absorbing":
+                continue
             plan = model.bc_plan(tag)
             for lf in range(self.nf):
                 s = idx[self.fb[idx] == lf]

@@ -122,6 +122,45 @@ NL_CASES = {
         state=([0.1], 0.3)),
 }
 
+REACT_ODE = """[model] kind=D ncu=1 nd=2 nw=1 nparam=1
+[mu]
+mu1=0.4
+[mass]
+m1=1
+[flux]
+f1_1=(1 + 0.1*w1)*q1_1
+f1_2=q1_2 + mu1*u1
+[source]
+s1=w1 - u1*u1
+[ode] alpha=1.5 beta=0.5
+sw1=u1*u1 + 0.1*q1_1 - sin(w1)
+[numflux] trace=switch grad_trace=opposite tau=1
+[bc tag=1 type=dirichlet]
+g1=0.2
+[bc tag=2 type=dirichlet]
+g1=x2
+[bc tag=3 type=neumann]
+g1=0.05
+[bc tag=4 type=dirichlet]
+g1=0
+[init]
+u1=0
+w1=0
+"""
+
+MB_CASES = {
+    # kind W (wave, q and w are states) with Dirichlet + absorbing faces
+    "wave2d_quad_absorbing_p3": dict(
+        model=("builtin", "wave", 2, [1.3]), kind="quad", counts=[3, 3], p=3,
+        bcs={1: ("dirichlet", ["0.1*x2"]), 2: ("absorbing", []), 3: ("dirichlet", ["0"]),
+             4: ("absorbing", [])}),
+    "wave3d_hex_periodic_p2": dict(
+        model=("builtin", "wave", 3, [0.8]), kind="hex", counts=[2, 2, 2], p=2, periodic=3),
+    # kind D with a pointwise ODE block coupled both ways
+    "reactode2d_quad_p2": dict(model=("text", REACT_ODE), kind="quad", counts=[3, 3], p=2,
+                               state=([0.3], 0.3)),
+}
+
 SOLVE_CASES = {
     # (case name, precond, solver flags)
     "poisson2d_quad_p3_n4_bj": dict(model=("file", "poisson2d.model"), kind="quad",
@@ -230,6 +269,15 @@ TRANSIENT_CASES.update({
         model=("file", "ns3d.model"), kind="hex", counts=[2, 2, 2], p=2, periodic=3,
         domain=(0.0, 2 * np.pi), init=TGV_INIT, stages=1, order=1, dt=0.05, steps=1,
         precond="mass", bj_apply=True),
+})
+
+TRANSIENT_CASES.update({
+    "wave2d_quad_p3_dirk22": dict(
+        model=("builtin", "wave", 2, [1.0]), kind="quad", counts=[4, 4], p=3,
+        bcs={1: ("dirichlet", ["0"]), 2: ("absorbing", []), 3: ("dirichlet", ["0"]),
+             4: ("absorbing", [])},
+        init={"u1": "sin(pi*x1)*sin(pi*x2)", "q1_1": "0", "q1_2": "0", "w1": "0"},
+        stages=2, order=2, dt=0.02, steps=2, precond="mass"),
 })
 
 TRANSIENT_FLAGS = dict(abs_tol=1e-10, rel_tol=1e-9, forcing=None, restart=60, gmres_max_iter=600)

@@ -30,7 +30,7 @@ from ldgkit.driver import _steady_fns, build_pde_block_jacobi  # noqa: E402
 from ldgkit.solver import NewtonOptions  # noqa: E402
 from ldgkit.timeint import solve_steady  # noqa: E402
 
-from cases import (ACCEPT_FLAGS, CASES, NL_CASES, SOLVE_CASES,  # noqa: E402
+from cases import (ACCEPT_FLAGS, CASES, MB_CASES, NL_CASES, SOLVE_CASES,  # noqa: E402
                    TRANSIENT_CASES, TRANSIENT_FLAGS, build_case, case_state, seeded_state)
 
 
@@ -86,6 +86,40 @@ def gen_nl_case(name, spec):
           float(np.abs(out["Jdu"]).max()))
 
 
+def mb_states(s, spec):
+    """Seeded packed-block states (u, q for kind W, w) and directions."""
+    ne, nb = s.n_elements, s.n_nodes
+    u = case_state(spec, ne, nb, s.ncu, 1)
+    du = seeded_state(ne, nb, s.ncu, 0)
+    q = dq = w = dw = None
+    if s.kind == "W":
+        q = np.random.default_rng(11).normal(size=(ne, nb, s.ncu, s.nd))
+        dq = np.random.default_rng(12).normal(size=(ne, nb, s.ncu, s.nd))
+    if s.nw > 0:
+        w = 0.5 * np.random.default_rng(13).normal(size=(ne, nb, s.nw))
+        dw = np.random.default_rng(14).normal(size=(ne, nb, s.nw))
+    return u, q, w, du, dq, dw
+
+
+def gen_mb_case(name, spec):
+    """Packed multi-block operator goldens (kind W / ODE blocks)."""
+    model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
+    s = LdgSystem(model, mesh, topo, master)
+    u, q, w, du, dq, dw = mb_states(s, spec)
+    st = SolverState(u=u, q=q, w=w, t=0.2)
+    out = dict(u=u, du=du, t=np.array(0.2), **topo_arrays(s))
+    for k, v in (("q", q), ("dq", dq), ("w", w), ("dw", dw)):
+        if v is not None:
+            out[k] = v
+    for tag, blocks in (("R", s.residual(st)), ("J", s.residual_tangent(st, du, dq, dw)),
+                        ("M", s.mass_apply(st, du, dq, dw))):
+        for bname, b in zip("uqw", blocks):
+            if b is not None:
+                out[f"{tag}{bname}"] = b
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, s.n_dofs, "dofs", sorted(k for k in out if k[0] in "RJM"))
+
+
 def gen_solve(name, spec):
     model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
     s = LdgSystem(model, mesh, topo, master)
@@ -117,6 +151,7 @@ def gen_transient(name, spec):
                          forcing=f["forcing"], gmres_restart=f["restart"],
                          gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent")
     tab = dirk_tableau(spec["stages"], spec["order"])
+    extra = {}
     if spec["precond"] == "block_jacobi":
         # transient block-Jacobi: built once at t = 0 from the steady
         # closures (driver.py:270-274)
@@ -130,7 +165,8 @@ def gen_transient(name, spec):
         st, stats = advance_step(s, st, spec["dt"], tab, opts, precond=M)
         newton.append(stats.newton_iters)
         gm.append(stats.gmres_iters)
-    extra = {}
+    if st.q is not None or st.w is not None:
+        extra.update({k: v for k, v in (("q", st.q), ("w", st.w)) if v is not None})
     if spec.get("bj_apply"):
         # block-Jacobi of the steady closures at the initial state, applied
         # to a seeded vector (solver.py:291-346, driver.py:109-142)
@@ -138,7 +174,7 @@ def gen_transient(name, spec):
         rf, tf = _steady_fns(s)
         bj = build_pde_block_jacobi(s, rf, tf, s.pack(s0.u), "tangent")
         r = np.random.default_rng(9).normal(size=s.n_dofs)
-        extra = dict(bj_r=r, bj_z=bj.apply(r))
+        extra.update(bj_r=r, bj_z=bj.apply(r))
     np.savez_compressed(HERE / f"transient_{name}.npz", u0=u0, u=st.u, t=np.array(st.t),
                         newton=np.array(newton), gmres=np.array(gm), **extra)
     print("transient", name, newton, gm, float(np.abs(st.u).max()))
@@ -148,6 +184,10 @@ if __name__ == "__main__":
     if "--nl-only" in sys.argv:
         for n, sp in NL_CASES.items():
             gen_nl_case(n, sp)
+        sys.exit(0)
+    if "--mb-only" in sys.argv:
+        for n, sp in MB_CASES.items():
+            gen_mb_case(n, sp)
         sys.exit(0)
     if "--transient-only" in sys.argv:
         for n, sp in TRANSIENT_CASES.items():
@@ -165,6 +205,8 @@ if __name__ == "__main__":
         gen_case(n, sp)
     for n, sp in NL_CASES.items():
         gen_nl_case(n, sp)
+    for n, sp in MB_CASES.items():
+        gen_mb_case(n, sp)
     for n, sp in SOLVE_CASES.items():
         gen_solve(n, sp)
     for n, sp in TRANSIENT_CASES.items():

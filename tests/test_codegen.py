@@ -7,7 +7,7 @@ import math
 import numpy as np
 import pytest
 
-from cases import NL_CASES, b200_setup, build_case
+from cases import MB_CASES, NL_CASES, b200_setup, build_case
 
 
 def test_literals_are_exact():
@@ -48,10 +48,11 @@ def test_nonlinear_tables_and_routing(name):
 
 
 @pytest.mark.parametrize("name", ["euler2d_quad_dirichlet_p2", "ns3d_hex_periodic_p2",
-                                  "nonlin_diff2d_quad_p2"])
+                                  "nonlin_diff2d_quad_p2", "wave2d_quad_absorbing_p3",
+                                  "reactode2d_quad_p2"])
 def test_nvrtc_compiles_generated_source(name):
     from paper_2205_07824_b200.nonlinear import NlTables, compile_source, generate_source
-    model, mesh, topo, master = build_case(NL_CASES[name], *b200_setup())
+    model, mesh, topo, master = build_case({**NL_CASES, **MB_CASES}[name], *b200_setup())
     src, _ = generate_source(NlTables(model, mesh, topo, master))
     cubin = compile_source(src)
     assert cubin[:4] == b"\x7fELF" and len(cubin) > 10000

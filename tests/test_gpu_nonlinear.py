@@ -113,3 +113,28 @@ def test_generated_kernels_do_not_spill():
         a = s.nl.kernel_attrs(k)
         assert a["regs"] > 0
         print(k, a)
+
+
+@pytest.mark.parametrize("name", sorted(__import__("cases").MB_CASES))
+def test_packed_blocks_vs_reference_golden(name):
+    """Kind W (wave: q and w are states; Dirichlet + absorbing faces) and a
+    kind D model with a pointwise ODE block: (Ru, Rq, Rw), the tangent
+    blocks and (Mu, Mq, Mw) against the reference (disc.py:595-948)."""
+    from cases import MB_CASES
+    from paper_2205_07824_b200.system import SolverState
+    g = np.load(GOLDEN / f"{name}.npz")
+    s = system_for(MB_CASES[name])
+    assert s.multi_block
+    t = float(g["t"])
+    get = lambda k: g[k] if k in g else None  # noqa: E731
+    st = SolverState(u=g["u"], q=get("q"), w=get("w"), t=t)
+    for tag, blocks in (("R", s.residual(st)),
+                        ("J", s.residual_tangent(st, g["du"], get("dq"), get("dw"))),
+                        ("M", s.mass_apply(st, g["du"], get("dq"), get("dw")))):
+        for b, val in zip("uqw", blocks):
+            key = f"{tag}{b}"
+            if key in g:
+                assert val is not None, key
+                assert rel(val, g[key]) < TOL, (key, rel(val, g[key]))
+            else:
+                assert val is None, key
