@@ -71,9 +71,36 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
                               system.n_nodes * system.ncu, colors)
 
 
+class CompositeManager:
+    """Config 'composite' (driver.py:145-175): block-Jacobi plus reduced-basis
+    deflation built from the most recent Newton updates, inactive until
+    snapshots exist; `note_update` is the Newton callback, `build(x)` is
+    called by newton_solve at every Newton step (solver.py:241)."""
+
+    def __init__(self, system, block_jacobi, tangent_fn, rank=10, refresh=1):
+        self.system, self.block_jacobi, self.tangent_fn = system, block_jacobi, tangent_fn
+        self.rank, self.refresh = rank, max(1, refresh)
+        self.snapshots, self._builds, self._rb = [], 0, None
+
+    def note_update(self, x, d):
+        self.snapshots.append(d.clone())
+        self.snapshots = self.snapshots[-self.rank:]
+
+    def build(self, x):
+        from .solver import CompositePreconditioner, build_reduced_basis
+        self._builds += 1
+        if self.snapshots and (self._builds % self.refresh == 0 or self._rb is None):
+            try:
+                self._rb = build_reduced_basis(self.snapshots,
+                                               lambda v: self.tangent_fn(x, v), rank=self.rank)
+            except Exception:
+                self._rb = None
+        return CompositePreconditioner(self.block_jacobi, self._rb)
+
+
 def make_preconditioner(system, kind, residual_fn, tangent_fn, state_vec, steady=True,
-                        jv_mode="tangent"):
-    """driver.py:178-198 (identity, mass, block_jacobi)."""
+                        jv_mode="tangent", rb_rank=10, rb_refresh=1):
+    """driver.py:178-198 (identity, mass, block_jacobi, composite)."""
     if kind == "auto":
         kind = "block_jacobi" if steady else "mass"
     if kind == "identity":
@@ -82,6 +109,10 @@ def make_preconditioner(system, kind, residual_fn, tangent_fn, state_vec, steady
         return MassPreconditioner(system), None
     if kind == "block_jacobi":
         return build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode), None
+    if kind == "composite":
+        bj = build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode)
+        mgr = CompositeManager(system, bj, tangent_fn, rank=rb_rank, refresh=rb_refresh)
+        return mgr, mgr.note_update
     raise DriverError(f"unknown or unsupported preconditioner {kind!r}")
 
 
@@ -125,7 +156,7 @@ def solve_steady(system, state, newton_options=None, precond=None, callback=None
 
 
 def run_steady(system, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8, forcing=1e-8,
-               restart=250, gmres_max_iter=6000, max_iter=20, orth="mgs"):
+               restart=250, gmres_max_iter=6000, max_iter=20, orth="mgs", rb_rank=10):
     """Steady branch of run_simulation (driver.py:253-268) with the
     acceptance solver flags as defaults; returns (state, stats, timings)."""
     import torch
@@ -135,7 +166,7 @@ def run_steady(system, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8, forc
     u0 = torch.as_tensor(state.u, device=system.device).reshape(-1)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    M, cb = make_preconditioner(system, precond, res_fn, tan_fn, u0)
+    M, cb = make_preconditioner(system, precond, res_fn, tan_fn, u0, rb_rank=rb_rank)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     opts = NewtonOptions(abs_tol=abs_tol, rel_tol=rel_tol, max_iter=max_iter, forcing=forcing,

@@ -500,3 +500,73 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors):
                                  _lib.ptr(shifted), st), "ldg_bj_invert")
     del mats
     return BlockJacobiPreconditioner(inv_t, bs, shifted)
+
+
+# ---------------------------------------------------------------------------
+# Reduced-basis deflation and the composite preconditioner (solver.py:386-436)
+# ---------------------------------------------------------------------------
+
+
+class ReducedBasisPreconditioner:
+    """apply(r) = W H^-1 W^T r + (I - W W^T) r with H = W^T J W
+    (solver.py:386-399).  W is held as rows (rank x n) so W^T r is one
+    multi-dot sweep and W (y - c) one fused combine; H's LU stays on the host
+    (rank <= 10) like the reference's scipy lu_solve."""
+
+    def __init__(self, W_rows, H_lu):
+        import torch
+        self.W = W_rows
+        self._H_lu = H_lu
+        self._c = torch.empty(W_rows.shape[0], dtype=torch.float64, device=W_rows.device)
+
+    @property
+    def rank(self):
+        return self.W.shape[0]
+
+    def apply(self, r):
+        import torch
+        ops = vecops(r.device)
+        k = self.rank
+        ops.cgs_dots(self.W, k, r, self._c)                  # c = W^T r
+        c = self._c.cpu().numpy()
+        y = scipy.linalg.lu_solve(self._H_lu, c) - c
+        out = r.clone()
+        ops.combine(self.W, k, torch.as_tensor(y, device=r.device), out)
+        return out
+
+
+def build_reduced_basis(snapshots, op, rank=None, drop_tol=1e-10):
+    """Orthonormalise the snapshots (device QR), H = W^T (J W) through the
+    matrix-free operator, rank-deficient directions dropped
+    (solver.py:402-423).  Column signs of Q may differ from numpy's; W H^-1 W^T
+    and W W^T are invariant to them."""
+    import torch
+    if len(snapshots) == 0:
+        raise SolverError("reduced basis needs at least one snapshot")
+    S = torch.stack([s.reshape(-1) for s in snapshots], dim=1)
+    if rank is not None:
+        S = S[:, -rank:]
+    Q, R = torch.linalg.qr(S, mode="reduced")
+    d = torch.abs(torch.diagonal(R)).cpu().numpy()
+    keep = d > drop_tol * max(1.0, float(d.max()))
+    if not keep.any():
+        raise SolverError("all snapshot directions are degenerate")
+    W = Q[:, torch.as_tensor(np.nonzero(keep)[0], device=Q.device)].T.contiguous()
+    apply_op = op if callable(op) else op.apply
+    JW = torch.stack([apply_op(W[k]) for k in range(W.shape[0])])
+    H = (W @ JW.T).cpu().numpy()
+    return ReducedBasisPreconditioner(W, scipy.linalg.lu_factor(H))
+
+
+class CompositePreconditioner:
+    """Block-Jacobi, then the reduced-basis deflation (solver.py:426-436)."""
+
+    def __init__(self, block_jacobi, reduced_basis=None):
+        self.block_jacobi = block_jacobi
+        self.reduced_basis = reduced_basis
+
+    def apply(self, r):
+        z = self.block_jacobi.apply(r)
+        if self.reduced_basis is not None:
+            z = self.reduced_basis.apply(z)
+        return z

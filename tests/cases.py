@@ -173,6 +173,10 @@ SOLVE_CASES = {
     "nonlin_diff2d_quad_p3_n3_bj": dict(model=("text", NONLIN_DIFF2D.replace(
         "m1=1 + 0.5*u1*u1", "m1=0")), kind="quad", counts=[3, 3], p=3,
         precond="block_jacobi"),
+    # composite = block-Jacobi + reduced-basis deflation from Newton updates
+    "nonlin_diff2d_quad_p3_n3_composite": dict(model=("text", NONLIN_DIFF2D.replace(
+        "m1=1 + 0.5*u1*u1", "m1=0")), kind="quad", counts=[3, 3], p=3,
+        precond="composite", rb_rank=3),
 }
 
 # acceptance solver flags (test_acceptance.py:69-81)

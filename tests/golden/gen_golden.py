@@ -128,11 +128,16 @@ def gen_solve(name, spec):
     opts = NewtonOptions(abs_tol=f["abs_tol"], rel_tol=f["rel_tol"], max_iter=20,
                          forcing=f["forcing"], gmres_restart=f["restart"],
                          gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent")
-    pre = None
-    if spec["precond"] == "block_jacobi":
+    pre = cb = None
+    if spec["precond"] in ("block_jacobi", "composite"):
         rf, tf = _steady_fns(s)
         pre = build_pde_block_jacobi(s, rf, tf, s.pack(st.u), "tangent")
-    out_state, stats = solve_steady(s, st, opts, precond=pre)
+        if spec["precond"] == "composite":
+            # CompositeManager (driver.py:145-175) as make_preconditioner wires it
+            from ldgkit.driver import CompositeManager
+            pre = CompositeManager(s, pre, tf, rank=spec.get("rb_rank", 10), refresh=1)
+            cb = pre.note_update
+    out_state, stats = solve_steady(s, st, opts, precond=pre, callback=cb)
     np.savez_compressed(HERE / f"solve_{name}.npz", u=out_state.u,
                         newton_iters=np.array(stats.newton_iters),
                         gmres_iters=np.array(stats.gmres_iters),

@@ -61,7 +61,7 @@ def test_steady_solve_matches_reference(name, orth):
     st, stats, _ = run_steady(s, precond=spec["precond"], abs_tol=f["abs_tol"],
                               rel_tol=f["rel_tol"], forcing=f["forcing"],
                               restart=f["restart"], gmres_max_iter=f["gmres_max_iter"],
-                              orth=orth)
+                              orth=orth, rb_rank=spec.get("rb_rank", 10))
     assert stats.converged
     assert stats.newton_iters == int(g["newton_iters"])
     assert abs(stats.total_gmres_iters - int(np.sum(g["gmres_iters"]))) <= 1, \
