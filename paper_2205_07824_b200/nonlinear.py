@@ -392,7 +392,8 @@ class NlOperator:
         if self.tab.model.kind == "D":
             if q is None:
                 q = self.mixed(u, t)
-            dq = self.mixed(du, t, homogeneous=True)
+            if dq is None:                         # (partitioned callers pass it with halos)
+                dq = self.mixed(du, t, homogeneous=True)
         P = self._params(t, u=u, q=q, du=du, dq=dq, w=w, dw=dw, out=R, gq=self.gq(t))
         self._launch("nl_tangent", self.tab.ne, self.shape["NT"], P)
         return R

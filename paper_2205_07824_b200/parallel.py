@@ -94,7 +94,7 @@ class LocalTables:
         for k in ("nd", "n1", "ncu", "nf", "nfn", "p", "nmap", "d1", "m1", "s1", "clo", "chi",
                   "m1inv", "au", "aq", "flux_uses_u", "mass_coef", "mass_const", "source_zero",
                   "model", "master", "mesh", "topo", "bc_groups"):
-            setattr(self, k, getattr(tab, k))
+            setattr(self, k, getattr(tab, k, None))     # (generated-path tables lack au/aq)
         e0, e1 = plan.e0, plan.e1
         self.ne = plan.ne_loc
         self.geo, self.fnbr, self.finfo, self.ftau = plan.geo, plan.fnbr, plan.finfo, plan.ftau
@@ -294,3 +294,133 @@ class LocalBus:
                   .view(-1, per[self.parts.index(p)]))
         return [p.sys.operator_pass(2, p.u_ext, tangent, t, scratch=p.X, out=R)
                 for p, R in zip(self.parts, Rs)]
+
+
+# ---------------------------------------------------------------------------
+# generated-kernel (nonlinear / kind C) models
+# ---------------------------------------------------------------------------
+
+
+class LocalNlTables(LocalTables):
+    """NlTables interface over one partition: the affine maps and
+    element-face geometry sliced, boundary data restricted to the
+    partition's boundary rows."""
+
+    def __init__(self, tab, plan):
+        super().__init__(tab, plan)
+        for k in ("nq1", "fxi", "fw", "periodic", "nonlinear", "tau_i", "tau_b"):
+            setattr(self, k, getattr(tab, k))
+        e0, e1 = plan.e0, plan.e1
+        self.xmap = tab.xmap[e0:e1]
+        self.fgeo = tab.fgeo[e0:e1]
+        self.n_boundary = int(plan.brows.size)
+
+    def boundary_points(self, t):
+        g = self._g.boundary_points(t)
+        return g[self.plan.brows] if g.size else g
+
+
+class PartitionedNlSystem:
+    """One rank's share of a generated-kernel model: owned elements plus a
+    ghost layer.  Per residual: the ghost u rows (halo 1), the owned mixed
+    gradient, its ghost rows (halo 2, kind D), then the element kernel.  The
+    tangent exchanges the direction the same way; the base state's ghost u / q
+    are exchanged once per base (cached like the single-GPU base q)."""
+
+    def __init__(self, model, mesh, topology, master, nranks, rank, device=None,
+                 exchanger=None, tables=None):
+        import torch
+        from .nonlinear import NlOperator, NlTables
+        gtab = tables if tables is not None else NlTables(model, mesh, topology, master)
+        self.plan = PartitionPlan(gtab, nranks, rank)
+        self.local = LocalNlTables(gtab, self.plan)
+        self.device = torch.device(device if device is not None else "cuda")
+        self.nl = NlOperator(self.local, self.device)
+        self.exchanger = exchanger if exchanger is not None else HaloExchanger(self.plan)
+        p = self.plan
+        self.model, self.kind = model, model.kind
+        self.n_elements, self.n_nodes, self.ncu = p.ne_loc, master.n_nodes, model.ncu
+        self.nd = mesh.nd
+        self.n_dofs = p.ne_loc * master.n_nodes * model.ncu
+        rows = p.ne_loc + p.n_ghost
+        self._ushape = (rows, master.n_nodes, model.ncu)
+        self._qshape = (rows, master.n_nodes, model.ncu, mesh.nd)
+        self._base = None
+
+    def _new(self, shape):
+        import torch
+        return torch.zeros(shape, dtype=torch.float64, device=self.device)
+
+    def _exchange(self, arr):
+        if self.exchanger:
+            self.exchanger.exchange(arr)
+
+    def extend(self, u):
+        """(owned) -> (owned + ghost) rows with the halo filled."""
+        ext = self._new(self._ushape)
+        ext[: self.plan.ne_loc].copy_(u.reshape(self.plan.ne_loc, self.n_nodes, self.ncu))
+        self._exchange(ext)
+        return ext
+
+    def mixed_ext(self, u_ext, t, homogeneous=False):
+        q = self._new(self._qshape)
+        self.nl.mixed(u_ext, t, homogeneous, out=q[: self.plan.ne_loc])
+        self._exchange(q)
+        return q
+
+    def base_ext(self, base, t):
+        key = (base.data_ptr(), base._version, float(t))
+        if self._base is None or self._base[0] != key:
+            ue = self.extend(base)
+            qe = self.mixed_ext(ue, t) if self.kind == "D" else None
+            self._base = (key, ue, qe, base)
+        return self._base[1], self._base[2]
+
+    def residual_dev(self, u, t=0.0, out=None):
+        ue, qe = self.base_ext(u, t)
+        R = self.nl.residual(ue, t, q=qe)
+        return R[: self.plan.ne_loc] if out is None else out.copy_(R[: self.plan.ne_loc])
+
+    def tangent_dev(self, du, out=None, base=None, t=0.0):
+        ue, qe = self.base_ext(base, t)
+        de = self.extend(du)
+        dq = self.mixed_ext(de, t, homogeneous=True) if self.kind == "D" else None
+        R = self.nl.tangent(ue, de, t, q=qe, dq=dq)
+        return R[: self.plan.ne_loc] if out is None else out.copy_(R[: self.plan.ne_loc])
+
+
+def nl_apply_all(parts, us, tangent, bases=None, t=0.0):
+    """Single-process lockstep of R partitions of a generated-kernel model on
+    one GPU (ghost rows by device copies): the two halo steps of
+    PartitionedNlSystem with a LocalBus in place of NCCL."""
+    bus = LocalBus(parts)
+    n = len(parts)
+
+    def ext(vals):
+        arrs = []
+        for p, v in zip(parts, vals):
+            a = p._new(p._ushape)
+            a[: p.plan.ne_loc].copy_(v.reshape(p.plan.ne_loc, p.n_nodes, p.ncu))
+            arrs.append(a)
+        bus.fill(lambda p: arrs[parts.index(p)])
+        return arrs
+
+    def mixed(arrs, homogeneous):
+        if parts[0].kind != "D":
+            return [None] * n
+        qs = []
+        for p, a in zip(parts, arrs):
+            q = p._new(p._qshape)
+            p.nl.mixed(a, t, homogeneous, out=q[: p.plan.ne_loc])
+            qs.append(q)
+        bus.fill(lambda p: qs[parts.index(p)].reshape(qs[parts.index(p)].shape[0], -1))
+        return qs
+
+    base = ext(bases if bases is not None else us)
+    qb = mixed(base, False)
+    if not tangent:
+        return [p.nl.residual(a, t, q=q)[: p.plan.ne_loc] for p, a, q in zip(parts, base, qb)]
+    d = ext(us)
+    dq = mixed(d, True)
+    return [p.nl.tangent(a, b, t, q=q, dq=dd)[: p.plan.ne_loc]
+            for p, a, b, q, dd in zip(parts, base, d, qb, dq)]
