@@ -99,12 +99,15 @@ __device__ __forceinline__ int face_vol_node(int lf, int t) {
 // operator id of variable v (dphi for the differentiated direction).
 // ---------------------------------------------------------------------------
 enum { OP_PHI = 0, OP_DPHI = 1, OP_M1INV = 2 };
-__device__ __forceinline__ double op_at(int id, int k) {
-  return id == OP_PHI ? c_phi[k] : (id == OP_DPHI ? c_dphi[k] : c_m1inv[k]);
+template <int OPID>
+__device__ __forceinline__ double op_c(int k) {
+  return OPID == OP_PHI ? c_phi[k] : (OPID == OP_DPHI ? c_dphi[k] : c_m1inv[k]);
 }
-template <int D0, int D1, int D2, int AX, int NIN, int NOUT, bool TRANS, typename Sel>
-__device__ __forceinline__ void contract(const double* __restrict__ in, double* __restrict__ out,
-                                         int nvar, int tid, Sel sel) {
+
+// uniform-operator contraction (compile-time operator: constant-bank loads)
+template <int D0, int D1, int D2, int AX, int NIN, int NOUT, bool TRANS, int OPID>
+__device__ __forceinline__ void contract_u(const double* __restrict__ in, double* __restrict__ out,
+                                           int nvar, int tid) {
   constexpr int O0 = AX == 0 ? NOUT : D0, O1 = AX == 1 ? NOUT : D1, O2 = AX == 2 ? NOUT : D2;
   constexpr int I0 = AX == 0 ? NIN : D0, I1 = AX == 1 ? NIN : D1, I2 = AX == 2 ? NIN : D2;
   constexpr int OSZ = O0 * O1 * O2, ISZ = I0 * I1 * I2;
@@ -116,30 +119,28 @@ __device__ __forceinline__ void contract(const double* __restrict__ in, double* 
     const int o = AX == 0 ? o0 : (AX == 1 ? o1 : o2);
     const int base = v * ISZ + (AX == 0 ? 0 : o0) + (AX == 1 ? 0 : o1) * I0 +
                      (AX == 2 ? 0 : o2) * I0 * I1;
-    const int id = sel(v);
     double acc = 0.0;
 #pragma unroll
     for (int i = 0; i < NIN; ++i)
-      acc = fma(op_at(id, TRANS ? i * N1 + o : o * N1 + i), in[base + i * STR], acc);
+      acc = fma(op_c<OPID>(TRANS ? i * N1 + o : o * N1 + i), in[base + i * STR], acc);
     out[idx] = acc;
   }
 }
 
 // nodes -> volume quadrature points (all variables, operator phi)
 __device__ __forceinline__ void to_quad(double* a, double* b, int nvar, int tid, double*& res) {
-  auto phi = [](int) { return (int)OP_PHI; };
   if (ND == 3) {
-    contract<N1, N1, N1, 0, N1, NQ1, false>(a, b, nvar, tid, phi);
+    contract_u<N1, N1, N1, 0, N1, NQ1, false, OP_PHI>(a, b, nvar, tid);
     __syncthreads();
-    contract<NQ1, N1, N1, 1, N1, NQ1, false>(b, a, nvar, tid, phi);
+    contract_u<NQ1, N1, N1, 1, N1, NQ1, false, OP_PHI>(b, a, nvar, tid);
     __syncthreads();
-    contract<NQ1, NQ1, N1, 2, N1, NQ1, false>(a, b, nvar, tid, phi);
+    contract_u<NQ1, NQ1, N1, 2, N1, NQ1, false, OP_PHI>(a, b, nvar, tid);
     __syncthreads();
     res = b;
   } else {
-    contract<N1, N1, 1, 0, N1, NQ1, false>(a, b, nvar, tid, phi);
+    contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(a, b, nvar, tid);
     __syncthreads();
-    contract<NQ1, N1, 1, 1, N1, NQ1, false>(b, a, nvar, tid, phi);
+    contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(b, a, nvar, tid);
     __syncthreads();
     res = a;
   }
@@ -147,22 +148,35 @@ __device__ __forceinline__ void to_quad(double* a, double* b, int nvar, int tid,
 
 // quadrature fields [r][c] (r < ND: G_r, r = ND: source) -> nodes, applying
 // dphi^T along direction r and phi^T elsewhere (the transposed volume rule)
+// one transposed stage along axis AX over fields [r][c] (r = 0..ND): the
+// NCU fields of direction r == AX take dphi^T, the others phi^T
+template <int D0, int D1, int D2, int AX>
+__device__ __forceinline__ void from_quad_stage(const double* in, double* out, int nfield, int tid) {
+  constexpr int I0 = AX == 0 ? NQ1 : D0, I1 = AX == 1 ? NQ1 : D1, I2 = AX == 2 ? NQ1 : D2;
+  constexpr int O0 = AX == 0 ? N1 : D0, O1 = AX == 1 ? N1 : D1, O2 = AX == 2 ? N1 : D2;
+  constexpr int ISZ = I0 * I1 * I2, OSZ = O0 * O1 * O2;
+  const int lo = AX * NCU, hi = lo + NCU;
+  if (lo > 0) contract_u<D0, D1, D2, AX, NQ1, N1, true, OP_PHI>(in, out, lo, tid);
+  contract_u<D0, D1, D2, AX, NQ1, N1, true, OP_DPHI>(in + lo * ISZ, out + lo * OSZ, NCU, tid);
+  if (nfield > hi)
+    contract_u<D0, D1, D2, AX, NQ1, N1, true, OP_PHI>(in + hi * ISZ, out + hi * OSZ, nfield - hi, tid);
+}
+
+// quadrature fields [r][c] (r < ND: G_r, r = ND: source) -> nodes, applying
+// dphi^T along direction r and phi^T elsewhere (the transposed volume rule)
 __device__ __forceinline__ void from_quad(double* a, double* b, int nfield, int tid, double*& res) {
-  auto sel0 = [](int v) { return v / NCU == 0 ? (int)OP_DPHI : (int)OP_PHI; };
-  auto sel1 = [](int v) { return v / NCU == 1 ? (int)OP_DPHI : (int)OP_PHI; };
-  auto sel2 = [](int v) { return v / NCU == 2 ? (int)OP_DPHI : (int)OP_PHI; };
   if (ND == 3) {
-    contract<NQ1, NQ1, NQ1, 0, NQ1, N1, true>(a, b, nfield, tid, sel0);
+    from_quad_stage<NQ1, NQ1, NQ1, 0>(a, b, nfield, tid);
     __syncthreads();
-    contract<N1, NQ1, NQ1, 1, NQ1, N1, true>(b, a, nfield, tid, sel1);
+    from_quad_stage<N1, NQ1, NQ1, 1>(b, a, nfield, tid);
     __syncthreads();
-    contract<N1, N1, NQ1, 2, NQ1, N1, true>(a, b, nfield, tid, sel2);
+    from_quad_stage<N1, N1, NQ1, 2>(a, b, nfield, tid);
     __syncthreads();
     res = b;
   } else {
-    contract<NQ1, NQ1, 1, 0, NQ1, N1, true>(a, b, nfield, tid, sel0);
+    from_quad_stage<NQ1, NQ1, 1, 0>(a, b, nfield, tid);
     __syncthreads();
-    contract<N1, NQ1, 1, 1, NQ1, N1, true>(b, a, nfield, tid, sel1);
+    from_quad_stage<N1, NQ1, 1, 1>(b, a, nfield, tid);
     __syncthreads();
     res = a;
   }
@@ -192,6 +206,19 @@ __device__ __forceinline__ double state_at(const NlParams& P, int fam, int v, sz
   if (v < OW) return (fam ? P.dq : P.q)[(e * NB + node) * (NCU * ND) + (v - NCU)];
   return (fam ? P.dw : P.w)[(e * NB + node) * (NW > 0 ? NW : 1) + (v - OW)];
 }
+
+__device__ __forceinline__ const double* state_ptr(const NlParams& P, int fam, int v, sz_t e,
+                                                   int node) {
+  if (v < NCU) return (fam ? P.du : P.u) + (e * NB + node) * NCU + v;
+  if (v < OW) return (fam ? P.dq : P.q) + (e * NB + node) * (NCU * ND) + (v - NCU);
+  return (fam ? P.dw : P.w) + (e * NB + node) * (NW > 0 ? NW : 1) + (v - OW);
+}
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // mixed gradient (kind D): one thread per node, EPBM elements per block
@@ -295,8 +322,11 @@ struct RShape {
   // face phase: traces of every face at its Gauss points, own and neighbour
   // side [side][face][v][NQF], one face's staging pair, and the face fluxes
   static constexpr int TR = NFACE * NVA * NQF;
-  static constexpr int FACE = 2 * TR + 4 * NVA * MXF + NFACE * NQF * NCU;
-  static constexpr int WORK = 2 * BS > FACE ? 2 * BS : FACE;
+  static constexpr int NBF = NVA * NFN;                        // one face's neighbour nodes
+  static constexpr int FACE = 2 * TR + NBF + 2 * NVA * MXF + NFACE * NQF * NCU + 2 * NBF;
+  // the neighbour double buffer sits at the end of the work region, clear of
+  // the volume buffers, so face 0's gathers fly during the volume phase
+  static constexpr int WORK = 2 * BS + 2 * NBF > FACE ? 2 * BS + 2 * NBF : FACE;
   static constexpr int SMEM = NVA * NB + NCU * NB + WORK;         // doubles
 };
 
@@ -510,6 +540,22 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
   }
   __syncthreads();
 
+  // neighbour face nodes, one face ahead (cp.async into a double buffer)
+  double* NB2 = bA + S::WORK - 2 * S::NBF;
+  auto prefetch_face = [&](int lf, double* dst) {
+    const int info = P.finfo[e * NFACE + lf];
+    const bool interior = (info & 3) == 0;
+    const int nbr = P.fnbr[e * NFACE + lf];
+    for (int idx = tid; idx < S::NBF; idx += NT) {
+      const int v = idx / NFN, t = idx % NFN;
+      if (interior) cp_async8(dst + idx, state_ptr(P, v >= NV, v % NV, (sz_t)nbr,
+                                                   P.nmap[(info >> 8) * NFN + t]));
+      else dst[idx] = 0.0;
+    }
+    cp_async_commit();
+  };
+  prefetch_face(0, NB2);
+
   // ---- volume: interpolate to quadrature points
   double* vq;
   to_quad(bA, bB, NVA, tid, vq);
@@ -567,37 +613,28 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
   // neighbour staging at a time), then every face point's f^ at once, then
   // the lift with each (node, component) owned by one thread
   double* TRc = bA;                            // [side][face][v][NQF]
-  double* ST0 = bA + 2 * S::TR;                // staging [side][v][face grid]
-  double* ST1 = ST0 + 2 * NVA * MXF;
+  double* SO = bA + 2 * S::TR;                 // own face nodes [v][face grid]
+  double* ST1 = SO + S::NBF;                   // first-stage scratch [side][v][..]
   double* sF = ST1 + 2 * NVA * MXF;            // [face][NQF][NCU]
-  auto phi = [](int) { return (int)OP_PHI; };
   for (int lf = 0; lf < NFACE; ++lf) {
-    const int info = P.finfo[e * NFACE + lf];
-    const bool interior = (info & 3) == 0;
-    const int nbr = P.fnbr[e * NFACE + lf];
-    for (int idx = tid; idx < 2 * NVA * NFN; idx += NT) {
-      const int side = idx / (NVA * NFN), v = (idx / NFN) % NVA, t = idx % NFN;
-      double val = 0.0;
-      if (side == 0) val = sV[v * NB + face_vol_node(lf, t)];
-      else if (interior) val = state_at(P, v >= NV, v % NV, (sz_t)nbr, P.nmap[(info >> 8) * NFN + t]);
-      ST0[idx] = val;
-    }
+    if (lf + 1 < NFACE) prefetch_face(lf + 1, NB2 + ((lf + 1) & 1) * S::NBF);
+    else cp_async_commit();                    // (empty group keeps the counting uniform)
+    for (int idx = tid; idx < S::NBF; idx += NT)
+      SO[idx] = sV[(idx / NFN) * NB + face_vol_node(lf, idx % NFN)];
+    cp_async_wait1();                          // this face's neighbour nodes have landed
     __syncthreads();
-    const double* tr;
+    const double* nb = NB2 + (lf & 1) * S::NBF;
+    double* tro = TRc + (0 * NFACE + lf) * NVA * NQF;
+    double* trn = TRc + (1 * NFACE + lf) * NVA * NQF;
     if (ND == 3) {
-      contract<N1, N1, 1, 0, N1, NQ1, false>(ST0, ST1, 2 * NVA, tid, phi);
+      contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(SO, ST1, NVA, tid);
+      contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(nb, ST1 + NVA * NQ1 * N1, NVA, tid);
       __syncthreads();
-      contract<NQ1, N1, 1, 1, N1, NQ1, false>(ST1, ST0, 2 * NVA, tid, phi);
-      __syncthreads();
-      tr = ST0;
+      contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(ST1, tro, NVA, tid);
+      contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(ST1 + NVA * NQ1 * N1, trn, NVA, tid);
     } else {
-      contract<N1, 1, 1, 0, N1, NQ1, false>(ST0, ST1, 2 * NVA, tid, phi);
-      __syncthreads();
-      tr = ST1;
-    }
-    for (int idx = tid; idx < 2 * NVA * NQF; idx += NT) {
-      const int side = idx / (NVA * NQF), r = idx % (NVA * NQF);
-      TRc[(side * NFACE + lf) * NVA * NQF + r] = tr[idx];
+      contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(SO, tro, NVA, tid);
+      contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(nb, trn, NVA, tid);
     }
     __syncthreads();
   }
@@ -715,20 +752,19 @@ __device__ __forceinline__ void mass_body(const NlParams& P) {
   // phi^T along every axis: reuse from_quad with the source-field selector
   // (fields indexed >= ND*NCU take phi everywhere): shift by ND*NCU
   double* other = fld == bA ? bB : bA;
-  auto phi = [](int) { return (int)OP_PHI; };
   double* res;
   if (ND == 3) {
-    contract<NQ1, NQ1, NQ1, 0, NQ1, N1, true>(fld, other, NCU, tid, phi);
+    contract_u<NQ1, NQ1, NQ1, 0, NQ1, N1, true, OP_PHI>(fld, other, NCU, tid);
     __syncthreads();
-    contract<N1, NQ1, NQ1, 1, NQ1, N1, true>(other, fld, NCU, tid, phi);
+    contract_u<N1, NQ1, NQ1, 1, NQ1, N1, true, OP_PHI>(other, fld, NCU, tid);
     __syncthreads();
-    contract<N1, N1, NQ1, 2, NQ1, N1, true>(fld, other, NCU, tid, phi);
+    contract_u<N1, N1, NQ1, 2, NQ1, N1, true, OP_PHI>(fld, other, NCU, tid);
     __syncthreads();
     res = other;
   } else {
-    contract<NQ1, NQ1, 1, 0, NQ1, N1, true>(fld, other, NCU, tid, phi);
+    contract_u<NQ1, NQ1, 1, 0, NQ1, N1, true, OP_PHI>(fld, other, NCU, tid);
     __syncthreads();
-    contract<N1, NQ1, 1, 1, NQ1, N1, true>(other, fld, NCU, tid, phi);
+    contract_u<N1, NQ1, 1, 1, NQ1, N1, true, OP_PHI>(other, fld, NCU, tid);
     __syncthreads();
     res = fld;
   }
@@ -757,20 +793,19 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mass_inv(const __grid_consta
     bA[idx] = P.q[((sz_t)e * NB + a) * NCU + v];
   }
   __syncthreads();
-  auto mi = [](int) { return (int)OP_M1INV; };
   double* res;
   if (ND == 3) {
-    contract<N1, N1, N1, 0, N1, N1, false>(bA, bB, NCU, tid, mi);
+    contract_u<N1, N1, N1, 0, N1, N1, false, OP_M1INV>(bA, bB, NCU, tid);
     __syncthreads();
-    contract<N1, N1, N1, 1, N1, N1, false>(bB, bA, NCU, tid, mi);
+    contract_u<N1, N1, N1, 1, N1, N1, false, OP_M1INV>(bB, bA, NCU, tid);
     __syncthreads();
-    contract<N1, N1, N1, 2, N1, N1, false>(bA, bB, NCU, tid, mi);
+    contract_u<N1, N1, N1, 2, N1, N1, false, OP_M1INV>(bA, bB, NCU, tid);
     __syncthreads();
     res = bB;
   } else {
-    contract<N1, N1, 1, 0, N1, N1, false>(bA, bB, NCU, tid, mi);
+    contract_u<N1, N1, 1, 0, N1, N1, false, OP_M1INV>(bA, bB, NCU, tid);
     __syncthreads();
-    contract<N1, N1, 1, 1, N1, N1, false>(bB, bA, NCU, tid, mi);
+    contract_u<N1, N1, 1, 1, N1, N1, false, OP_M1INV>(bB, bA, NCU, tid);
     __syncthreads();
     res = bA;
   }
@@ -805,20 +840,19 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mass_q(const __grid_constant
   for (int idx = tid; idx < NQC * NQ; idx += NT) fld[idx] = c_qw[idx % NQ] * detj * vq[idx];
   __syncthreads();
   double* other = fld == bA ? bB : bA;
-  auto phi = [](int) { return (int)OP_PHI; };
   double* res;
   if (ND == 3) {
-    contract<NQ1, NQ1, NQ1, 0, NQ1, N1, true>(fld, other, NQC, tid, phi);
+    contract_u<NQ1, NQ1, NQ1, 0, NQ1, N1, true, OP_PHI>(fld, other, NQC, tid);
     __syncthreads();
-    contract<N1, NQ1, NQ1, 1, NQ1, N1, true>(other, fld, NQC, tid, phi);
+    contract_u<N1, NQ1, NQ1, 1, NQ1, N1, true, OP_PHI>(other, fld, NQC, tid);
     __syncthreads();
-    contract<N1, N1, NQ1, 2, NQ1, N1, true>(fld, other, NQC, tid, phi);
+    contract_u<N1, N1, NQ1, 2, NQ1, N1, true, OP_PHI>(fld, other, NQC, tid);
     __syncthreads();
     res = other;
   } else {
-    contract<NQ1, NQ1, 1, 0, NQ1, N1, true>(fld, other, NQC, tid, phi);
+    contract_u<NQ1, NQ1, 1, 0, NQ1, N1, true, OP_PHI>(fld, other, NQC, tid);
     __syncthreads();
-    contract<N1, NQ1, 1, 1, NQ1, N1, true>(other, fld, NQC, tid, phi);
+    contract_u<N1, NQ1, 1, 1, NQ1, N1, true, OP_PHI>(other, fld, NQC, tid);
     __syncthreads();
     res = fld;
   }
@@ -873,20 +907,19 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mass_inv_q(const __grid_cons
     bA[idx] = P.q[((sz_t)e * NB + a) * NQC + v];
   }
   __syncthreads();
-  auto mi = [](int) { return (int)OP_M1INV; };
   double* res;
   if (ND == 3) {
-    contract<N1, N1, N1, 0, N1, N1, false>(bA, bB, NQC, tid, mi);
+    contract_u<N1, N1, N1, 0, N1, N1, false, OP_M1INV>(bA, bB, NQC, tid);
     __syncthreads();
-    contract<N1, N1, N1, 1, N1, N1, false>(bB, bA, NQC, tid, mi);
+    contract_u<N1, N1, N1, 1, N1, N1, false, OP_M1INV>(bB, bA, NQC, tid);
     __syncthreads();
-    contract<N1, N1, N1, 2, N1, N1, false>(bA, bB, NQC, tid, mi);
+    contract_u<N1, N1, N1, 2, N1, N1, false, OP_M1INV>(bA, bB, NQC, tid);
     __syncthreads();
     res = bB;
   } else {
-    contract<N1, N1, 1, 0, N1, N1, false>(bA, bB, NQC, tid, mi);
+    contract_u<N1, N1, 1, 0, N1, N1, false, OP_M1INV>(bA, bB, NQC, tid);
     __syncthreads();
-    contract<N1, N1, 1, 1, N1, N1, false>(bB, bA, NQC, tid, mi);
+    contract_u<N1, N1, 1, 1, N1, N1, false, OP_M1INV>(bB, bA, NQC, tid);
     __syncthreads();
     res = bA;
   }

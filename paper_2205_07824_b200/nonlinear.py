@@ -304,8 +304,9 @@ class NlOperator:
         nd, nqf, mxf = tab.nd, tab.nq1 ** (tab.nd - 1), s["MXF"]
         for name, tan in (("nl_residual", False), ("nl_tangent", True)):
             nva = nv * (2 if tan else 1)
-            face = 2 * (2 * nd) * nva * nqf + 4 * nva * mxf + 2 * nd * nqf * ncu
-            work = max(2 * max(nva, ng) * mx, face)
+            nbf = nva * s["NB"] // s["N1"]          # one face's neighbour nodes (NVA x NFN)
+            face = 2 * (2 * nd) * nva * nqf + nbf + 2 * nva * mxf + 2 * nd * nqf * ncu + 2 * nbf
+            work = max(2 * max(nva, ng) * mx + 2 * nbf, face)
             self.smem[name] = 8 * (nva * nb + ncu * nb + work)
         nvm = ncu if s["MASS_CONST"] else 3 * ncu
         self.smem["nl_mass"] = self.smem["nl_mass_extra"] = 8 * 2 * max(nvm, ncu) * mx
