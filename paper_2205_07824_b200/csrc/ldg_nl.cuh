@@ -95,8 +95,9 @@ __device__ __forceinline__ int face_vol_node(int lf, int t) {
 // (D0 fastest) for NVAR variables stored [v][grid]:
 //   out[v][.., o, ..] = sum_i M(o, i) in[v][.., i, ..]
 // M(o, i) = op[o * N1 + i] (interpolation, rows = outputs) or, with TRANS,
-// op[i * N1 + o] (the transpose: quadrature -> nodes).  `sel(v)` picks the
-// operator id of variable v (dphi for the differentiated direction).
+// op[i * N1 + o] (the transpose: quadrature -> nodes); the operator (phi,
+// dphi or M1^-1) is a template parameter, so its entries are constant-bank
+// operands.
 // ---------------------------------------------------------------------------
 enum { OP_PHI = 0, OP_DPHI = 1, OP_M1INV = 2 };
 template <int OPID>
@@ -104,7 +105,6 @@ __device__ __forceinline__ double op_c(int k) {
   return OPID == OP_PHI ? c_phi[k] : (OPID == OP_DPHI ? c_dphi[k] : c_m1inv[k]);
 }
 
-// uniform-operator contraction (compile-time operator: constant-bank loads)
 template <int D0, int D1, int D2, int AX, int NIN, int NOUT, bool TRANS, int OPID>
 __device__ __forceinline__ void contract_u(const double* __restrict__ in, double* __restrict__ out,
                                            int nvar, int tid) {
