@@ -180,7 +180,7 @@ def load_traffic():
         return {}
 
 
-def nonlinear_lines(hbm):
+def nonlinear_lines(hbm, cpu=True):
     """Configs 4 and 2 on the generated-kernel path (scripts/nl_bench.py):
     3D compressible Navier-Stokes hex p=3 n=32 (10.5M DOFs) and 2D Euler quad
     p=4 n=256 (6.6M DOFs) residual / tangent GDOF/s with the SURVEY 8(d)
@@ -193,11 +193,28 @@ def nonlinear_lines(hbm):
               state=([1.0, 0.2, -0.1, 0.15, 25.0], 0.05))
     eu = dict(TRANSIENT_CASES["euler2d_vortex_quad_p3_dirk22"], counts=[256] * 2, p=4,
               state=([1.0, 0.2, -0.1, 2.5], 0.05))
+    small = {"config4_ns3d_hex_p3_n32": dict(ns, counts=[3] * 3),
+             "config2_euler2d_quad_p4_n256": dict(eu, counts=[6] * 2)}
     for name, spec in (("config4_ns3d_hex_p3_n32", ns), ("config2_euler2d_quad_p4_n256", eu)):
         _, r = nl_bench.run(name, spec, 10, hbm)
         out[name] = {k: r[k] for k in ("dofs", "tangent_gdofs", "residual_gdofs", "tangent_ms",
                                        "residual_ms", "tangent_bytes_per_dof",
                                        "tangent_frac_hbm")}
+        if cpu:
+            c = nl_bench.cpu_oracle_tangent(small[name])
+            out[name]["cpu_baseline"] = dict(c, sample=f"{c['dofs']}-DOF mesh of the same "
+                                                      "model / p, oracle tangent")
+    # implicit steps (time to solution per step; config 2 is
+    # quad p=4 n=64 with DIRK(1,1) = BDF1 and the mass preconditioner; config 4
+    # hex p=3 n=16 -- its reference transient block-Jacobi does not converge
+    # (DESIGN.md), so the mass preconditioner)
+    eu64 = dict(eu, counts=[64] * 2, stages=1, order=1)
+    ns16 = dict(ns, counts=[16] * 3, stages=1, order=1)
+    out["config2_step_euler_vortex_p4_n64_bdf1"] = nl_bench.run_transient(eu64, 3, 0.01)
+    # (dt 0.05 / 0.01 stall Newton within 20 iterations with the frozen-penalty
+    # linearisation -- as the reference itself does at n=3, measured -- so
+    # config 4 steps at dt = 0.002)
+    out["config4_step_ns3d_tgv_p3_n16_bdf1"] = nl_bench.run_transient(ns16, 2, 0.002)
     return out
 
 
@@ -419,7 +436,7 @@ def run_b200(args, rank, world):
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_nonlinear:
-        line["nonlinear"] = nonlinear_lines(hbm)
+        line["nonlinear"] = nonlinear_lines(hbm, cpu=not args.no_cpu_baseline)
     if world == 1 and not args.no_solve:
         line["solve"] = {"metric": "Newton-GMRES time to solution (s), config 3, block-Jacobi, "
                                    "acceptance flags", "dofs": ndof,

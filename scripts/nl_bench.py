@@ -106,5 +106,64 @@ def main():
     print(json.dumps(out))
 
 
+
+def run_transient(spec, steps, dt, precond="mass", flags=None):
+    """Wall time per implicit DIRK step (device Newton-GMRES, reference
+    transient solver flags), with Newton / GMRES counts."""
+    import time
+    import torch
+    from cases import TRANSIENT_FLAGS, build_case, b200_setup
+    from paper_2205_07824_b200.driver import MassPreconditioner, advance_step, dirk_tableau
+    from paper_2205_07824_b200.solver import NewtonOptions
+    from paper_2205_07824_b200.system import LdgSystem
+    f = dict(TRANSIENT_FLAGS, **(flags or {}))
+    s = LdgSystem(*build_case(spec, *b200_setup()))
+    st = s.interpolate_initial()
+    opts = NewtonOptions(abs_tol=f["abs_tol"], rel_tol=f["rel_tol"], max_iter=20,
+                         forcing=f["forcing"], gmres_restart=f["restart"],
+                         gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent",
+                         orth=f.get("orth", "cgs2"))
+    tab = dirk_tableau(spec["stages"], spec["order"])
+    M = MassPreconditioner(s)
+    from paper_2205_07824_b200.driver import TimeIntError
+    try:
+        st, _ = advance_step(s, st, dt, tab, opts, precond=M)   # warm-up (JIT, caches)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        newton, gm = [], []
+        for _ in range(steps):
+            st, stats = advance_step(s, st, dt, tab, opts, precond=M)
+            newton.append(stats.newton_iters)
+            gm.append(stats.gmres_iters)
+        torch.cuda.synchronize()
+    except TimeIntError as exc:
+        return {"dofs": s.n_dofs, "dt": dt, "failed": str(exc)}
+    per = (time.perf_counter() - t0) / steps
+    return {"dofs": s.n_dofs, "dt": dt, "steps": steps, "s_per_step": per,
+            "newton_per_step": newton, "gmres_per_step": gm, "precond": precond,
+            "max_abs_u": float(torch.max(torch.abs(st.u)).item())}
+
+
+def cpu_oracle_tangent(spec, reps=2):
+    """The oracle (reference numpy path) tangent on a small sample of a
+    config: GDOF/s on this host, 1 core."""
+    import time
+    from cases import build_case, b200_setup, case_state
+    from oracle import make_oracle
+    model, mesh, topo, master = build_case(spec, *b200_setup())
+    o = make_oracle(model, mesh, topo, master)
+    ne, nb, ncu = mesh.connectivity.shape[0], master.n_nodes, model.ncu
+    u = case_state(spec, ne, nb, ncu, 1)
+    du = np.random.default_rng(0).normal(size=u.shape)
+    o.residual_tangent(u, du)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        o.residual_tangent(u, du)
+        ts.append(time.perf_counter() - t0)
+    return {"dofs": ne * nb * ncu, "gdofs": ne * nb * ncu / float(np.median(ts)) / 1e9,
+            "cores": 1, "kind": "port"}
+
+
 if __name__ == "__main__":
     main()
