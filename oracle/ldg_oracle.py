@@ -14,9 +14,10 @@ golden vectors produced by the *unmodified* reference package
 ``/root/reference`` is mounted): residuals, tangents, mixed gradients and
 switch bits on hex/quad/tri/tet meshes.
 
-Scope: kinds D and C with the default trace rules, dirichlet / neumann
-boundaries, constant or state-dependent mass.  Kind W, pointwise ODE blocks
-and user u^/f^ overrides raise ``NotImplementedError``.
+Scope: kinds D and C with the default trace rules or user u^ / f^
+overrides, dirichlet / neumann boundaries, constant or state-dependent mass.
+Kind W and pointwise ODE blocks raise ``NotImplementedError`` (those device
+paths are pinned directly against the reference's golden vectors).
 """
 
 from __future__ import annotations
@@ -299,8 +300,7 @@ class OracleLdg:
     def __init__(self, model, mesh, topo, master, geom_master, face_map):
         if model.kind == "W" or model.nw > 0:
             raise NotImplementedError("oracle covers kinds D and C without ODEs")
-        if model.numflux.uhat is not None or model.numflux.fhat is not None:
-            raise NotImplementedError("u^/f^ overrides")
+
         self.model, self.mesh, self.topo, self.master = model, mesh, topo, master
         self.d = OracleDisc(mesh, topo, master, geom_master, face_map)
         self.kind, self.ncu, self.nd = model.kind, model.ncu, model.nd
@@ -340,6 +340,35 @@ class OracleLdg:
             for k in range(self.nd):
                 b[f"n{k + 1}"] = n[..., k].ravel()
         return b
+
+    def _face_bind(self, x, t, ul, ur, ql, qr, n):
+        """Face-override bindings over both traces (disc.py:516-547)."""
+        b = {"t": float(t)}
+        b.update(self.mu)
+        for k in range(self.nd):
+            b[f"x{k + 1}"] = x[..., k].ravel()
+            b[f"n{k + 1}"] = n[..., k].ravel()
+        for i in range(self.ncu):
+            b[f"ul{i + 1}"] = ul[..., i].ravel()
+            b[f"ur{i + 1}"] = ur[..., i].ravel()
+        if ql is not None:
+            for i in range(self.ncu):
+                for j in range(self.nd):
+                    b[f"ql{i + 1}_{j + 1}"] = ql[..., i, j].ravel()
+                    b[f"qr{i + 1}_{j + 1}"] = qr[..., i, j].ravel()
+        return b
+
+    def _face_seed(self, dul, dur, dql, dqr):
+        s = {}
+        for i in range(self.ncu):
+            s[f"ul{i + 1}"] = dul[..., i].ravel()
+            s[f"ur{i + 1}"] = dur[..., i].ravel()
+        if dql is not None:
+            for i in range(self.ncu):
+                for j in range(self.nd):
+                    s[f"ql{i + 1}_{j + 1}"] = dql[..., i, j].ravel()
+                    s[f"qr{i + 1}_{j + 1}"] = dqr[..., i, j].ravel()
+        return s
 
     def _seed(self, du=None, dq=None):
         s = {}
@@ -387,7 +416,11 @@ class OracleLdg:
         rhs = -np.einsum("eq,eqij,qa->eaij", d.wdetj, g, m.phi, optimize=True)
         if self.topo.elem_l.shape[0]:
             ul, ur = d.trace_l(u), d.trace_r(u)
-            if self.model.numflux.trace == "centered":
+            if self.model.uhat_plan() is not None:             # disc.py:500-504
+                uh, _ = self._eval(self.model.uhat_plan(),
+                                   self._face_bind(d.fi_x, t, ul, ur, None, None, d.fi_n),
+                                   d.fi_x.shape[:2], "uhat override")
+            elif self.model.numflux.trace == "centered":
                 uh = 0.5 * (ul + ur)
             else:
                 uh = np.where(self.switch[:, None, None], ul, ur)
@@ -473,19 +506,30 @@ class OracleLdg:
             dul, dur = d.trace_l(du), d.trace_r(du)
         shape = d.fi_x.shape[:2]
         sw = self.switch
+        ql = qr = dql = dqr = None
+        if q is not None:
+            ql, qr = d.trace_l(q), d.trace_r(q)
+            if tan:
+                dql, dqr = d.trace_l(dq), d.trace_r(dq)
+        fb = self._face_bind(d.fi_x, t, ul, ur, ql, qr, d.fi_n)
+        fs = self._face_seed(dul, dur, dql, dqr) if tan else None
+        if self.model.fhat_plan() is not None:                 # disc.py:753-758
+            f, df = self._eval(self.model.fhat_plan(), fb, shape, "fhat override", fs)
+            return df if tan else f
         if self.kind == "C":
             return self._llf(ul, ur, dul, dur, t, d.fi_x, d.fi_n, shape)
-        centered = self.model.numflux.trace == "centered"
-        uh = 0.5 * (ul + ur) if centered else np.where(sw[:, None, None], ul, ur)
-        duh = None
-        if tan:
-            duh = 0.5 * (dul + dur) if centered else np.where(sw[:, None, None], dul, dur)
-        ql, qr = d.trace_l(q), d.trace_r(q)
+        if self.model.uhat_plan() is not None:                 # disc.py:500-504
+            uh, duh = self._eval(self.model.uhat_plan(), fb, shape, "uhat override", fs)
+        else:
+            centered = self.model.numflux.trace == "centered"
+            uh = 0.5 * (ul + ur) if centered else np.where(sw[:, None, None], ul, ur)
+            duh = None
+            if tan:
+                duh = 0.5 * (dul + dur) if centered else np.where(sw[:, None, None], dul, dur)
         gc = self.model.numflux.grad_trace == "centered"
         qh = 0.5 * (ql + qr) if gc else np.where(sw[:, None, None, None], qr, ql)
         dqh = None
         if tan:
-            dql, dqr = d.trace_l(dq), d.trace_r(dq)
             dqh = 0.5 * (dql + dqr) if gc else np.where(sw[:, None, None, None], dqr, dql)
         bind = self._bind(d.fi_x, t, uh, qh, n=d.fi_n)
         f, df = self._eval(self.model.flux_plan(), bind, shape, "face flux",

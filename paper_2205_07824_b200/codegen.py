@@ -119,10 +119,45 @@ DSIG = ("const double* __restrict__ du, const double* __restrict__ dq, "
         "const double* __restrict__ dw")
 
 
-def emit_plan(plan, name, nd, mu):
+def face_symbol_ref(name, nd, mu):
+    """Device expression of a face-override symbol (model.py:61-73 spelling:
+    ul / ur / ql / qr over the LEFT / RIGHT traces, x, t, mu, n)."""
+    for pre, arr in (("ul", "uL"), ("ur", "uR")):
+        if name.startswith(pre) and name[2:].isdigit():
+            k = int(name[2:]) - 1
+            return f"{arr}[{k}]", (f"{arr}", k)
+    for pre, arr in (("ql", "qL"), ("qr", "qR")):
+        if name.startswith(pre) and "_" in name:
+            i, j = name[2:].split("_")
+            k = (int(i) - 1) * nd + int(j) - 1
+            return f"{arr}[{k}]", (f"{arr}", k)
+    if name[0] in "uqw" and not name.startswith("mu"):
+        raise CodegenError(f"symbol {name!r} is not available to face override plans")
+    return symbol_ref(name, nd, mu)
+
+
+FSIG = ("const double* __restrict__ x, double t, const double* __restrict__ uL, "
+        "const double* __restrict__ uR, const double* __restrict__ qL, "
+        "const double* __restrict__ qR, const double* __restrict__ n")
+FDSIG = ("const double* __restrict__ duL, const double* __restrict__ duR, "
+         "const double* __restrict__ dqL, const double* __restrict__ dqR")
+
+
+def emit_face_plan(plan, name, nd, mu):
+    """``name(x,t,uL,uR,qL,qR,n,out)`` and its dual for a u^ / f^ override
+    plan over the face symbols (disc.py:516-547)."""
+    return emit_plan(plan, name, nd, mu, resolver=face_symbol_ref, sig=FSIG, dsig=FDSIG,
+                     unused="  (void)x; (void)t; (void)uL; (void)uR; (void)qL; (void)qR; (void)n;",
+                     dunused="  (void)duL; (void)duR; (void)dqL; (void)dqR;")
+
+
+def emit_plan(plan, name, nd, mu, resolver=None, sig=None, dsig=None, unused=None,
+              dunused=None):
     """CUDA source of ``name(x,t,u,q,w,n,out)`` and
     ``name_d(x,t,u,q,w,n,du,dq,dw,out,dout)`` for a plan (one output slot per
     plan output).  Unused pointer arguments may be null."""
+    resolver = resolver or symbol_ref
+    sig, dsig = sig or SIG, dsig or DSIG
     ins_list = plan.instructions
     val, dual = [], []          # code expressions per instruction; dual None = 0
     lines_v, lines_d = [], []
@@ -133,7 +168,7 @@ def emit_plan(plan, name, nd, mu):
             dual.append(None)
             continue
         if tag == "sym":
-            code, seed = symbol_ref(ins[1], nd, mu)
+            code, seed = resolver(ins[1], nd, mu)
             val.append(code)
             dual.append(None if seed is None else f"d{seed[0]}[{seed[1]}]")
             continue
@@ -236,10 +271,11 @@ def emit_plan(plan, name, nd, mu):
     outs_v = [f"  out[{k}] = {val[r]};" for k, r in enumerate(plan.outputs)]
     outs_d = [f"  out[{k}] = {val[r]};\n  dout[{k}] = {dual[r] or '0.0'};"
               for k, r in enumerate(plan.outputs)]
-    unused = "  (void)x; (void)t; (void)u; (void)q; (void)w; (void)n;"
-    src = [f"__device__ __forceinline__ void {name}({SIG}, double* __restrict__ out) {{",
+    unused = unused or "  (void)x; (void)t; (void)u; (void)q; (void)w; (void)n;"
+    dunused = dunused or "  (void)du; (void)dq; (void)dw;"
+    src = [f"__device__ __forceinline__ void {name}({sig}, double* __restrict__ out) {{",
            unused, *lines_v, *outs_v, "}",
-           f"__device__ __forceinline__ void {name}_d({SIG}, {DSIG},",
+           f"__device__ __forceinline__ void {name}_d({sig}, {dsig},",
            "    double* __restrict__ out, double* __restrict__ dout) {",
-           unused, "  (void)du; (void)dq; (void)dw;", *lines_d, *outs_d, "}"]
+           unused, dunused, *lines_d, *outs_d, "}"]
     return "\n".join(src) + "\n"

@@ -64,6 +64,8 @@ struct NlParams {
   const double* dw;
   double* out;
   u64* bad;              // [0]: first element with a non-finite plan value
+  int homog;             // nl_mixed: 1 = dual of a u^ override (kind-W tangent lift)
+  int pad_;
 };
 
 __device__ __forceinline__ bool fin(double v) { return v - v == 0.0; }
@@ -244,7 +246,29 @@ nl_mixed(const __grid_constant__ NlParams P) {
       for (int c = 0; c < NCU; ++c) {
         const double own = su[slot][c][vn];
         double jump = 0.0;
-        if (kind == 0) {
+        if (kind == 0 && HAS_UHAT) {
+          // user u^ (affine in the traces, checked at setup), evaluated at
+          // the face nodes.  compute_mixed(du) evaluates it on du like on u
+          // (disc.py:446-449 -> 496-504); the kind-W tangent lift takes its
+          // dual, i.e. drops the constant part (P.homog)
+          double ul[NCU], ur[NCU], uh[NCU], u0[NCU], zr[NCU];
+          const bool right = info & 4;
+          const int nn = P.nmap[(info >> 8) * NFN + t];
+#pragma unroll
+          for (int k = 0; k < NCU; ++k) {
+            const double o = su[slot][k][vn], b = P.u[((sz_t)nbr * NB + nn) * NCU + k];
+            ul[k] = right ? b : o;
+            ur[k] = right ? o : b;
+            zr[k] = 0.0;
+          }
+          plan_uhat(nullptr, P.t, ul, ur, nullptr, nullptr, nullptr, uh);
+          if (P.homog) {
+            plan_uhat(nullptr, P.t, zr, zr, nullptr, nullptr, nullptr, u0);
+#pragma unroll
+            for (int k = 0; k < NCU; ++k) uh[k] -= u0[k];
+          }
+          jump = own - uh[c];
+        } else if (kind == 0) {
           const bool right = info & 4, sw = info & 8;
           const bool own_hat = !TRACE_CENTERED && (sw != right);   // u^ = own trace
           if (!own_hat) {
@@ -446,6 +470,23 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
   const double* uR = right ? vo : vn;
   const double* duL = uL + NV;
   const double* duR = uR + NV;
+  if (HAS_FHAT) {
+    // user numerical flux over both traces (disc.py:753-758)
+    const double* qL = NVQ ? uL + NCU : nullptr;
+    const double* qR = NVQ ? uR + NCU : nullptr;
+    double fo[NCU], dfo[NCU];
+    if (TANGENT)
+      plan_fhat_d(x, P.t, uL, uR, qL, qR, n, duL, duR, NVQ ? duL + NCU : nullptr,
+                  NVQ ? duR + NCU : nullptr, fo, dfo);
+    else
+      plan_fhat(x, P.t, uL, uR, qL, qR, n, fo);
+#pragma unroll
+    for (int c = 0; c < NCU; ++c) {
+      flag(P, e, fo[c]);
+      fh[c] = TANGENT ? dfo[c] : fo[c];
+    }
+    return;
+  }
   if (KIND_C) {
     // local Lax-Friedrichs (disc.py:724-751)
     double fR[NCU * ND], dfR[NCU * ND], lamL, lamR, dlamL = 0.0, dlamR = 0.0;
@@ -481,10 +522,20 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
   }
   // kind D / W: f(u^, q^, w^) . n + tau (u^- - u^) (disc.py:657-722)
   double uh[NCU], duh[NCU], qh[NVQ > 0 ? NVQ : 1], dqh[NVQ > 0 ? NVQ : 1];
+  if (HAS_UHAT) {                                      // user u^ (disc.py:502-504)
+    const double* qL = NVQ ? uL + NCU : nullptr;
+    const double* qR = NVQ ? uR + NCU : nullptr;
+    if (TANGENT)
+      plan_uhat_d(x, P.t, uL, uR, qL, qR, n, duL, duR, NVQ ? duL + NCU : nullptr,
+                  NVQ ? duR + NCU : nullptr, uh, duh);
+    else
+      plan_uhat(x, P.t, uL, uR, qL, qR, n, uh);
+  } else {
 #pragma unroll
-  for (int c = 0; c < NCU; ++c) {
-    uh[c] = TRACE_CENTERED ? 0.5 * (uL[c] + uR[c]) : (sw ? uL[c] : uR[c]);
-    if (TANGENT) duh[c] = TRACE_CENTERED ? 0.5 * (duL[c] + duR[c]) : (sw ? duL[c] : duR[c]);
+    for (int c = 0; c < NCU; ++c) {
+      uh[c] = TRACE_CENTERED ? 0.5 * (uL[c] + uR[c]) : (sw ? uL[c] : uR[c]);
+      if (TANGENT) duh[c] = TRACE_CENTERED ? 0.5 * (duL[c] + duR[c]) : (sw ? duL[c] : duR[c]);
+    }
   }
 #pragma unroll
   for (int k = 0; k < NVQ; ++k) {

@@ -45,7 +45,8 @@ class NlParams(C.Structure):
     _fields_ = [("ne", C.c_int32), ("nbface", C.c_int32), ("t", C.c_double),
                 ("scale", C.c_double)] + [(k, C.c_void_p) for k in (
                     "geo", "xmap", "fnbr", "finfo", "fgeo", "nmap", "gq", "gproj",
-                    "u", "q", "du", "dq", "w", "dw", "out", "bad")]
+                    "u", "q", "du", "dq", "w", "dw", "out", "bad")] + [
+                        ("homog", C.c_int32), ("pad_", C.c_int32)]
 
 
 def linear_path_reason(model):
@@ -55,6 +56,8 @@ def linear_path_reason(model):
         return f"kind {model.kind}"
     if model.nw > 0:
         return "pointwise ODE block"
+    if model.numflux.uhat is not None or model.numflux.fhat is not None:
+        return "u^ / f^ override"
     if model.ncu > 3:
         return "ncu > 3"
     mu = model.mu_bindings()
@@ -199,6 +202,15 @@ def generate_source(tab):
                         "(the gradient lift takes u^ at the face nodes)")
     nw = model.nw
     sw = model.sw_plan() if nw > 0 else None
+    uhat, fhat = model.uhat_plan(), model.fhat_plan()
+    if tab.periodic and any(p is not None and codegen.uses(p, "x") for p in (uhat, fhat)):
+        raise DiscError("face override plans reading x on periodic meshes are not supported")
+    if uhat is not None:
+        # the gradient lift takes u^ at the face nodes: exact for u^ affine in
+        # the traces with constant coefficients (no q, no x)
+        face_vars = {f"u{s}{i + 1}" for s in "lr" for i in range(ncu)}
+        if affine_form(uhat, mu, face_vars) is None:
+            raise DiscError("u^ overrides must be affine in ul / ur with constant coefficients")
     if tab.periodic and (codegen.uses(flux, "x") or (ws is not None and codegen.uses(ws, "x"))):
         raise DiscError("face plans reading x on periodic meshes are not supported")
     mforms = affine_form(mass, mu, set())
@@ -222,6 +234,7 @@ def generate_source(tab):
                 ODE_BETA=codegen.literal(ode.beta if ode is not None else 0.0),
                 HAS_WS=int(ws is not None), TRACE_CENTERED=int(model.numflux.trace == "centered"),
                 GRAD_CENTERED=int(model.numflux.grad_trace == "centered"),
+                HAS_UHAT=int(uhat is not None), HAS_FHAT=int(fhat is not None),
                 MASS_CONST=int(mass_const), NT=nt)
     lines = ["// generated by paper_2205_07824_b200/nonlinear.py -- do not edit"]
     lines += [f"#define {k} {v}" for k, v in defs.items()]
@@ -242,6 +255,10 @@ def generate_source(tab):
         lines.append(codegen.emit_plan(_ZeroPlan(1), "plan_ws", nd, mu))
     lines.append(codegen.emit_plan(mass, "plan_mass", nd, mu))
     lines.append(codegen.emit_plan(sw if sw is not None else _ZeroPlan(1), "plan_sw", nd, mu))
+    lines.append(codegen.emit_face_plan(uhat if uhat is not None else _ZeroPlan(ncu),
+                                        "plan_uhat", nd, mu))
+    lines.append(codegen.emit_face_plan(fhat if fhat is not None else _ZeroPlan(ncu),
+                                        "plan_fhat", nd, mu))
     src_text = "\n".join(lines) + "\n" + TEMPLATE.read_text()
     shapes = dict(defs, NB=nb, NQ=nq, NV=nv, MX=mx, MXF=mxf, NG=ng)
     return src_text, shapes
@@ -364,13 +381,14 @@ class NlOperator:
         return torch.empty(shape, dtype=torch.float64, device=self.device)
 
     # -- operators -------------------------------------------------------------
-    def mixed(self, u, t=0.0, homogeneous=False, out=None, state_q=None):
+    def mixed(self, u, t=0.0, homogeneous=False, out=None, state_q=None, linearised=False):
         """M^-1 (lifted gradient form) of u; `state_q` (kind W) is the state
         gradient absorbing boundaries take u^ from."""
         tab = self.tab
         q = out if out is not None else self._empty((tab.ne, self.shape["NB"], tab.ncu, tab.nd))
         P = self._params(t, u=u, q=state_q, out=q,
                          gproj=None if homogeneous else self.gproj(t))
+        P.homog = int(bool(linearised))
         nb = self.shape["NB"]
         epb = 1 if nb >= 128 else 128 // nb
         self._launch("nl_mixed", (tab.ne + epb - 1) // epb, epb * nb, P)
@@ -404,7 +422,7 @@ class NlOperator:
         (disc.py:866-874): the lift of (u, q) -- or of the direction (du, dq)
         with homogeneous Dirichlet data -- times the element mass."""
         tab = self.tab
-        qt = self.mixed(u, t, homogeneous=tangent, state_q=q)
+        qt = self.mixed(u, t, homogeneous=tangent, state_q=q, linearised=tangent)
         o = out if out is not None else self._empty(qt.shape)
         P = self._params(t, -1.0, q=qt, out=o)
         self._launch("nl_mass_q", tab.ne, self.shape["NT"], P)

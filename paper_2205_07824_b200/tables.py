@@ -195,10 +195,9 @@ class TensorTables:
             raise DiscError(f"B200 path supports kind C/D/W models, got {model.kind}"
                             if nonlinear else
                             f"linear B200 path supports kind D models, got {model.kind}")
-        if (model.nw > 0 and not nonlinear) or model.numflux.uhat is not None or \
-                model.numflux.fhat is not None:
-            raise DiscError("u^/f^ overrides are not supported on the B200 path (ODE blocks "
-                            "run on the generated path)")
+        if not nonlinear and (model.nw > 0 or model.numflux.uhat is not None or
+                              model.numflux.fhat is not None):
+            raise DiscError("ODE blocks and u^/f^ overrides run on the generated path")
         self.nd, self.p, self.ncu = mesh.nd, master.p, model.ncu
         self.n1 = master.p + 1
         if self.n1 > 7 or self.ncu > (5 if nonlinear else 3):

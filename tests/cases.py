@@ -116,6 +116,21 @@ NL_CASES = {
     "nonlin_diff2d_quad_p2": dict(
         model=("text", NONLIN_DIFF2D), kind="quad", counts=[3, 3], p=2,
         state=([0.2], 0.4)),
+    # user numerical-flux overrides (disc.py:502-504, 753-758)
+    "burgers2d_fhat_periodic_p3": dict(
+        model=("builtin", "burgers", 2, None), kind="quad", counts=[3, 3], p=3, periodic=2,
+        numflux=dict(fhat=["(ul1*ul1/2 + ur1*ur1/2)/2*(n1+n2) + 0.3*max(abs(ul1), abs(ur1))"
+                           "*(ul1-ur1)"]),
+        state=([0.5], 0.3)),
+    "poisson2d_uhat_p2": dict(
+        model=("builtin", "poisson", 2, None), kind="quad", counts=[3, 2], p=2,
+        bcs={t: ("dirichlet", ["x1*x2"]) for t in (1, 2, 3, 4)},
+        numflux=dict(uhat=["0.3*ul1 + 0.7*ur1"])),
+    "convdiff2d_fhat_periodic_p2": dict(
+        model=("builtin", "convection_diffusion", 2, [1.0, 0.5, 0.2]), kind="quad",
+        counts=[3, 3], p=2, periodic=2,
+        numflux=dict(fhat=["(mu1*n1+mu2*n2)*(ul1+ur1)/2 + mu3*((ql1_1+qr1_1)/2*n1 + "
+                           "(ql1_2+qr1_2)/2*n2) + 2*(ul1-ur1)"])),
     "nonlin_diff2d_quad_centered_p3": dict(
         model=("text", NONLIN_DIFF2D), kind="quad", counts=[2, 3], p=3,
         numflux=dict(trace="centered", grad_trace="centered", tau=2.0),
