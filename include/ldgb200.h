@@ -209,6 +209,10 @@ int ldg_combine(int64_t n, int k, const double* Z, int64_t ldz, const double* y,
                 double* x, void* stream);
 
 /* ---- block-Jacobi ---- */
+/* greedy distance-2 colouring of the element graph given by the interior
+ * faces (elem_l, elem_r) (solver.py:355-378, driver.py:109-142) */
+int ldg_color_distance2(int64_t ne, int64_t nfaces, const int32_t* elem_l,
+                        const int32_t* elem_r, int32_t* colors);
 int ldg_bj_probe_vector(int64_t nblk, int bs, const int32_t* members,
                         int64_t n_members, int k, double* v, void* stream);
 int ldg_bj_extract(int bs, const int32_t* members, int64_t n_members, int k,

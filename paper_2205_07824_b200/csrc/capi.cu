@@ -485,6 +485,53 @@ int ldg_apply_host(LdgHandle* h, int tangent, const double* v_host, double* out_
   return 0;
 }
 
+// Greedy colouring of the distance-2 element graph (solver.py:355-378,
+// driver.py:109-142): element v takes the smallest colour not used by an
+// already coloured element within two face-neighbour hops, v = 0, 1, ... in
+// order -- the reference's deterministic greedy on the squared adjacency.
+int ldg_color_distance2(int64_t ne, int64_t nfaces, const int32_t* elem_l,
+                        const int32_t* elem_r, int32_t* colors) {
+  if (ne < 0 || nfaces < 0 || (nfaces && (!elem_l || !elem_r)) || (ne && !colors))
+    return fail(2, "bad argument");
+  std::vector<int64_t> deg(ne + 1, 0);
+  for (int64_t f = 0; f < nfaces; ++f) {
+    const int a = elem_l[f], b = elem_r[f];
+    if (a < 0 || b < 0 || a >= ne || b >= ne) return fail(2, "face element out of range");
+    if (a == b) continue;
+    ++deg[a + 1];
+    ++deg[b + 1];
+  }
+  for (int64_t v = 0; v < ne; ++v) deg[v + 1] += deg[v];
+  std::vector<int32_t> adj(deg[ne]);
+  std::vector<int64_t> fill(deg.begin(), deg.end() - 1);
+  for (int64_t f = 0; f < nfaces; ++f) {
+    const int a = elem_l[f], b = elem_r[f];
+    if (a == b) continue;
+    adj[fill[a]++] = b;
+    adj[fill[b]++] = a;
+  }
+  std::vector<int64_t> stamp;                  // colour -> last element that saw it
+  for (int64_t v = 0; v < ne; ++v) colors[v] = -1;
+  for (int64_t v = 0; v < ne; ++v) {
+    auto mark = [&](int64_t u) {
+      if (u == v) return;
+      const int c = colors[u];
+      if (c < 0) return;
+      if ((int64_t)stamp.size() <= c) stamp.resize(c + 1, -1);
+      stamp[c] = v;
+    };
+    for (int64_t i = deg[v]; i < deg[v + 1]; ++i) {
+      const int u = adj[i];
+      mark(u);
+      for (int64_t j = deg[u]; j < deg[u + 1]; ++j) mark(adj[j]);
+    }
+    int c = 0;
+    while (c < (int)stamp.size() && stamp[c] == v) ++c;
+    colors[v] = c;
+  }
+  return 0;
+}
+
 int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
                         const double* q, const double* gproj,
                         const double* bsrc, double* R, void* stream) {

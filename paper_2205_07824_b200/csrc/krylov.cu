@@ -113,7 +113,9 @@ mgs_kernel(int64_t n, const double* __restrict__ vi, const double* __restrict__ 
   finish(partials, ticket, 1, h_out, false, sh);
 }
 
-// up to kMaxK dots <V_i, w> per sweep
+// up to kMaxK dots <V_i, w> per sweep; two consecutive entries per thread
+// (16 B loads) when the rows are 16 B aligned, so each of the k + 1 streams
+// has twice the bytes in flight per instruction
 __global__ void __launch_bounds__(kThreads)
 multidot_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
                 const double* __restrict__ w, double* partials,
@@ -123,11 +125,34 @@ multidot_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
 #pragma unroll
   for (int r = 0; r < kMaxK; ++r) acc[r] = 0.0;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
-    const double wv = w[i];
+  const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+  if (vec) {
+    const int64_t n2 = n >> 1;
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n2; i += stride) {
+      const double2 wv = w2[i];
 #pragma unroll
-    for (int r = 0; r < kMaxK; ++r)
-      if (r < k) acc[r] = fma(V[(int64_t)r * ldv + i], wv, acc[r]);
+      for (int r = 0; r < kMaxK; ++r)
+        if (r < k) {
+          const double2 v = reinterpret_cast<const double2*>(V + (int64_t)r * ldv)[i];
+          acc[r] = fma(v.x, wv.x, acc[r]);
+          acc[r] = fma(v.y, wv.y, acc[r]);
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int64_t i = n - 1;
+#pragma unroll
+      for (int r = 0; r < kMaxK; ++r)
+        if (r < k) acc[r] = fma(V[(int64_t)r * ldv + i], w[i], acc[r]);
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+      const double wv = w[i];
+#pragma unroll
+      for (int r = 0; r < kMaxK; ++r)
+        if (r < k) acc[r] = fma(V[(int64_t)r * ldv + i], wv, acc[r]);
+    }
   }
   for (int r = 0; r < k; ++r) {
     const double s = block_sum(acc[r], sh);
@@ -136,7 +161,8 @@ multidot_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
   finish(partials, ticket, k, h, false, sh);
 }
 
-// w -= sum_i h[i] V_i (i < k), optional ||w||
+// w -= sum_i h[i] V_i (i < k), optional ||w||.  Two entries per thread with
+// 16 B loads, the row loop unrolled by 4 into two accumulator pairs.
 __global__ void __launch_bounds__(kThreads)
 update_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
               const double* __restrict__ hcoef, double sign, double* __restrict__ w,
@@ -147,12 +173,56 @@ update_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
   __syncthreads();
   double s = 0.0;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
-    double acc = 0.0;
-    for (int r = 0; r < k; ++r) acc = fma(hs[r], V[(int64_t)r * ldv + i], acc);
-    const double wv = fma(sign, acc, w[i]);
-    w[i] = wv;
-    s = fma(wv, wv, s);
+  const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+  if (vec) {
+    const int64_t n2 = n >> 1;
+    double2* w2 = reinterpret_cast<double2*>(w);
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n2; i += stride) {
+      double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+      int r = 0;
+      for (; r + 4 <= k; r += 4) {
+        const double2 v0 = reinterpret_cast<const double2*>(V + (int64_t)r * ldv)[i];
+        const double2 v1 = reinterpret_cast<const double2*>(V + (int64_t)(r + 1) * ldv)[i];
+        const double2 v2 = reinterpret_cast<const double2*>(V + (int64_t)(r + 2) * ldv)[i];
+        const double2 v3 = reinterpret_cast<const double2*>(V + (int64_t)(r + 3) * ldv)[i];
+        ax = fma(hs[r], v0.x, ax);
+        ay = fma(hs[r], v0.y, ay);
+        bx = fma(hs[r + 1], v1.x, bx);
+        by = fma(hs[r + 1], v1.y, by);
+        ax = fma(hs[r + 2], v2.x, ax);
+        ay = fma(hs[r + 2], v2.y, ay);
+        bx = fma(hs[r + 3], v3.x, bx);
+        by = fma(hs[r + 3], v3.y, by);
+      }
+      for (; r < k; ++r) {
+        const double2 v0 = reinterpret_cast<const double2*>(V + (int64_t)r * ldv)[i];
+        ax = fma(hs[r], v0.x, ax);
+        ay = fma(hs[r], v0.y, ay);
+      }
+      double2 wv = w2[i];
+      wv.x = fma(sign, ax + bx, wv.x);
+      wv.y = fma(sign, ay + by, wv.y);
+      w2[i] = wv;
+      s = fma(wv.x, wv.x, s);
+      s = fma(wv.y, wv.y, s);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int64_t i = n - 1;
+      double acc = 0.0;
+      for (int r = 0; r < k; ++r) acc = fma(hs[r], V[(int64_t)r * ldv + i], acc);
+      const double wv = fma(sign, acc, w[i]);
+      w[i] = wv;
+      s = fma(wv, wv, s);
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+      double acc = 0.0;
+      for (int r = 0; r < k; ++r) acc = fma(hs[r], V[(int64_t)r * ldv + i], acc);
+      const double wv = fma(sign, acc, w[i]);
+      w[i] = wv;
+      s = fma(wv, wv, s);
+    }
   }
   if (!nrm) return;
   s = block_sum(s, sh);

@@ -15,7 +15,7 @@ import time
 import numpy as np
 
 from .solver import (NewtonOptions, build_block_jacobi, distance2_coloring,
-                     element_neighbor_sets, newton_solve)
+                     distance2_coloring_topology, element_neighbor_sets, newton_solve)
 
 
 class DriverError(RuntimeError):
@@ -66,7 +66,7 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
         raise DriverError("block-Jacobi on packed (u, q, w) systems is not supported on the "
                           "B200 path; use the mass preconditioner")
     if colors is None:
-        colors = distance2_coloring(element_neighbor_sets(system.topology, system.n_elements))
+        colors = distance2_coloring_topology(system.topology, system.n_elements)
     return build_block_jacobi(tangent_fn, state_vec, system.n_elements,
                               system.n_nodes * system.ncu, colors)
 

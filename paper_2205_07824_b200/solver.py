@@ -465,6 +465,21 @@ def distance2_coloring(neighbors):
     return greedy_coloring(adj2)
 
 
+def distance2_coloring_topology(topology, n_elements):
+    """distance2_coloring(element_neighbor_sets(topology)) in the native
+    library (same greedy order and result; linear time instead of Python
+    set algebra over ~10^5 elements)."""
+    import ctypes as C
+    lib = _lib.load(require_gpu=False)
+    el = np.ascontiguousarray(topology.elem_l, dtype=np.int32)
+    er = np.ascontiguousarray(topology.elem_r, dtype=np.int32)
+    out = np.empty(n_elements, dtype=np.int32)
+    _lib.check(lib.ldg_color_distance2(n_elements, el.size, el.ctypes.data_as(C.c_void_p),
+                                       er.ctypes.data_as(C.c_void_p),
+                                       out.ctypes.data_as(C.c_void_p)), "ldg_color_distance2")
+    return out.astype(np.int64)
+
+
 def element_neighbor_sets(topology, n_elements):
     """driver.py:109-116."""
     nb = [set() for _ in range(n_elements)]

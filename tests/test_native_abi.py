@@ -29,3 +29,21 @@ def test_library_exports_header_symbols():
 def test_table_struct_layout_matches_header():
     # 8 int32 + 5 pointers + 3*81 + 2*9 + 75 + 225 + 5 doubles
     assert ctypes.sizeof(_lib.LdgTables) == 8 * 4 + 5 * 8 + (3 * 81 + 18 + 75 + 225 + 5) * 8
+
+
+def test_native_distance2_coloring_matches_reference_greedy():
+    """ldg_color_distance2 == the reference's greedy on the squared graph
+    (solver.py:355-378) on structured, periodic and simplex meshes."""
+    import numpy as np
+    from paper_2205_07824_b200 import meshgen
+    from paper_2205_07824_b200.solver import (distance2_coloring, distance2_coloring_topology,
+                                              element_neighbor_sets)
+    for counts, kind, per in (([5, 4, 3], "hex", None), ([4, 4], "quad",
+                                                         [(1, 2, (1.0, 0.0)), (3, 4, (0.0, 1.0))]),
+                              ([3, 3, 2], "tet", None), ([6, 5], "tri", None)):
+        nd = len(counts)
+        mesh = meshgen.generate_structured([(0.0, 1.0)] * nd, counts, kind)
+        topo = meshgen.build_face_topology(mesh, per)
+        ne = mesh.connectivity.shape[0]
+        want = distance2_coloring(element_neighbor_sets(topo, ne))
+        assert np.array_equal(distance2_coloring_topology(topo, ne), want)
