@@ -657,21 +657,11 @@ static_assert(kPlanePer % 16 == 4, "element stride must be 4 mod 16 doubles");
 constexpr int kPlaneMaps = 16;               // node maps cached in shared memory
 }  // namespace
 
-// a[k * 4 + m] for a lane-dependent k without dynamically indexing the
-// parameter bank (which would copy the parameter block to local memory)
-__device__ __forceinline__ double sel4(const double* a, int k, int m) {
-  const double v0 = a[m], v1 = a[4 + m], v2 = a[8 + m], v3 = a[12 + m];
-  return k == 0 ? v0 : (k == 1 ? v1 : (k == 2 ? v2 : v3));
-}
-__device__ __forceinline__ double sel1(const double* a, int k) {
-  return k == 0 ? a[0] : (k == 1 ? a[1] : (k == 2 ? a[2] : a[3]));
-}
-
 #ifndef LDG_PLANE_MINB
 #define LDG_PLANE_MINB 2          // 2 persistent blocks per SM (shared-memory bound)
 #endif
 
-template <bool TANGENT, bool HAS_CU>
+template <bool TANGENT, bool HAS_CU, bool DIAG>
 __global__ void __launch_bounds__(kPlaneBlock, LDG_PLANE_MINB)
 plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
              const double* __restrict__ u, const double* __restrict__ gproj,
@@ -680,12 +670,27 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   constexpr int N1 = 4, NP = 16, NB = 64;
   extern __shared__ __align__(16) double psm[];
   __shared__ int s_map[kPlaneMaps * NP];
+  __shared__ double s_tab[4 * NP + 8];           // G, M^-1, M, D, clo, chi (rows picked by the plane index)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = threadIdx.x >> 2, k = threadIdx.x & 3;
   const int ls = lane >> 2;                                // element slot within the warp
   const bool map_smem = P.n_maps <= kPlaneMaps;
   if (map_smem)
     for (int x = threadIdx.x; x < P.n_maps * NP; x += kPlaneBlock) s_map[x] = __ldg(P.nmap + x);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int x = 0; x < NP; ++x) {
+      s_tab[x] = P.g1[x];
+      s_tab[NP + x] = P.m1inv[x];
+      s_tab[2 * NP + x] = P.m1[x];
+      s_tab[3 * NP + x] = P.d1[x];
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      s_tab[4 * NP + x] = P.clo[x];
+      s_tab[4 * NP + 4 + x] = P.chi[x];
+    }
+  }
   __syncthreads();
   double* sWarp = psm + warp * 8 * kPlanePer;              // the warp's 8 element regions
   double* sEl = sWarp + ls * kPlanePer;
@@ -810,7 +815,7 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   }
 #pragma unroll
   for (int m = 0; m < N1; ++m) {
-    const double dkm = sel4(P.d1, k, m);
+    const double dkm = s_tab[3 * NP + 4 * k + m];
 #pragma unroll
     for (int n = 0; n < NP; ++n) hz[n] = fma(dkm, sU[m * kPS + n], hz[n]);
   }
@@ -834,12 +839,14 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     }
   }
   __syncwarp();
-  double h[3][NP];                               // h_x, h_y, h_z of the plane
+  double h[2][NP];                               // h_x, h_y of the plane
   {
-    const double clk = sel1(P.clo, k), chk = sel1(P.chi, k);
+    // h_z goes straight to the thread's F_z row (shared): it is not needed in
+    // registers again until the flux combination, which keeps stage C spill-free
+    const double clk = s_tab[4 * NP + k], chk = s_tab[4 * NP + 4 + k];
 #pragma unroll
     for (int n = 0; n < NP; ++n)
-      h[2][n] = -hz[n] - clk * sJZ[(n >> 2) * kES + (n & 3)] + chk * sJZ[20 + (n >> 2) * kES + (n & 3)];
+      sT2[k * kPS + n] = -hz[n] - clk * sJZ[(n >> 2) * kES + (n & 3)] + chk * sJZ[20 + (n >> 2) * kES + (n & 3)];
   }
   // ---- C: x / y faces at this plane and the in-plane gradients; the
   // own-data face fluxes go to the thread's (now dead) u-plane slot
@@ -896,11 +903,23 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
 
   // ---- D: flux density F^q = C h (in place), face exports and the q^ own
   // share of the face fluxes, then F = F^q + Cu u
+  double* fz = sT2 + k * kPS;                    // this plane's h_z, then F_z
+  if (DIAG) {
+    const double c0 = sC[0], c1 = sC[4], c2 = sC[8];
 #pragma unroll
-  for (int n = 0; n < NP; ++n) {
-    const double h0 = h[0][n], h1 = h[1][n], h2 = h[2][n];
+    for (int n = 0; n < NP; ++n) {
+      h[0][n] *= c0;
+      h[1][n] *= c1;
+      fz[n] *= c2;
+    }
+  } else {
 #pragma unroll
-    for (int r = 0; r < 3; ++r) h[r][n] = fma(sC[3 * r], h0, fma(sC[3 * r + 1], h1, sC[3 * r + 2] * h2));
+    for (int n = 0; n < NP; ++n) {
+      const double h0 = h[0][n], h1 = h[1][n], h2 = fz[n];
+      h[0][n] = fma(sC[0], h0, fma(sC[1], h1, sC[2] * h2));
+      h[1][n] = fma(sC[3], h0, fma(sC[4], h1, sC[5] * h2));
+      fz[n] = fma(sC[6], h0, fma(sC[7], h1, sC[8] * h2));
+    }
   }
 #pragma unroll
   for (int s = 0; s < 2; ++s)
@@ -954,159 +973,152 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         }
       }
     }
-  if (k == 0 || k == 3) {                        // z face of this plane
-    const int f = k == 3;
-    const int inf = f ? info[1] : info[0];
+  // z faces: all four threads share them, thread k taking column i = k of the
+  // plane-0 / plane-3 F_z rows (conflict-free: bank 4e + k + 4j), so neither
+  // the own-share update nor the exports diverge on k
+  __syncwarp();                                  // F_z rows of planes 0 and 3 complete
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int inf = info[f];
     const int kind = inf & LDG_FACE_KIND_MASK;
-    if (kind != LDG_FACE_NEUMANN) {
-      const bool exp_ = (inf & LDG_FL_EXPORT) && active;
-      const double w_own = kind != LDG_FACE_INTERIOR ? 1.0
-                           : ((inf & LDG_FL_QOWN) ? 1.0 : ((inf & LDG_FL_QHALF) ? 0.5 : 0.0));
-      const double sgn = f ? 1.0 : -1.0;
-      double2* xp = reinterpret_cast<double2*>(X + ((size_t)e * 6 + f) * NP);
-      double* xb = nullptr;
+    if (kind == LDG_FACE_NEUMANN) continue;
+    const bool exp_ = (inf & LDG_FL_EXPORT) && active;
+    const double w_own = kind != LDG_FACE_INTERIOR ? 1.0
+                         : ((inf & LDG_FL_QOWN) ? 1.0 : ((inf & LDG_FL_QHALF) ? 0.5 : 0.0));
+    const double sgn = f ? 1.0 : -1.0;
+    const double* fzp = sT2 + (f ? 3 : 0) * kPS + k;
+    double xv[N1];
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {               // face node (i = k, j)
+      xv[j] = sgn * fzp[4 * j];
+      double* z0 = sFZ + f * 20 + j * kES + k;
+      *z0 = fma(w_own, xv[j], *z0);
+    }
+    if (exp_) {
+      double* xb = X + ((size_t)e * 6 + f) * NP;
+      bool mapped = false;
       int mid = 0, nax = 0;
-      if (exp_ && P.x_consumer) {
+      if (P.x_consumer) {
         const int nlf = (inf >> 4) & 7;
-        const double* nb2 = sIn + kInF + 2 * f + 1;
-        const size_t row = ((size_t)reinterpret_cast<const int2*>(nb2)->x * 6 + nlf) * NP;
-        if ((unsigned)inf & LDG_FL_XIDENT) {
-          xp = reinterpret_cast<double2*>(X + row);       // same node order: plain rows
-        } else {
+        xb = X + ((size_t)reinterpret_cast<const int2*>(sIn + kInF + 2 * f + 1)->x * 6 + nlf) * NP;
+        if (!((unsigned)inf & LDG_FL_XIDENT)) {
+          mapped = true;
           mid = (inf >> LDG_FACE_MAP_SHIFT) & 0xffff;
           nax = face_axis(3, nlf);
-          xb = X + row;
         }
       }
 #pragma unroll
-      for (int n = 0; n < NP; n += 2) {
-        const double x0 = sgn * h[2][n], x1 = sgn * h[2][n + 1];
-        if (xb) {
-          const int v0 = map_smem ? s_map[mid * NP + n] : __ldg(P.nmap + mid * NP + n);
-          const int v1 = map_smem ? s_map[mid * NP + n + 1] : __ldg(P.nmap + mid * NP + n + 1);
-          const int t0 = vol_to_face<N1, 3>(nax, v0), t1 = vol_to_face<N1, 3>(nax, v1);
-          if (t1 == t0 + 1 && (t0 & 1) == 0) {
-            *reinterpret_cast<double2*>(xb + t0) = make_double2(x0, x1);
-          } else {
-            xb[t0] = x0;
-            xb[t1] = x1;
-          }
+      for (int j = 0; j < N1; ++j) {
+        const int t = k + 4 * j;
+        int tn = t;
+        if (mapped) {
+          const int nv = map_smem ? s_map[mid * NP + t] : __ldg(P.nmap + mid * NP + t);
+          tn = vol_to_face<N1, 3>(nax, nv);
         }
-        double* z0 = sFZ + f * 20 + (n >> 2) * kES + (n & 3);
-        z0[0] = fma(w_own, x0, z0[0]);
-        z0[1] = fma(w_own, x1, z0[1]);
-        if (exp_ && !xb) xp[n / 2] = make_double2(x0, x1);
+        xb[tn] = xv[j];
       }
     }
   }
+  if (HAS_CU) __syncwarp();                      // F_z rows read before the Cu update
   if (HAS_CU) {
 #pragma unroll
-    for (int n = 0; n < NP; ++n)
-#pragma unroll
-      for (int r = 0; r < 3; ++r) h[r][n] = fma(sC[9 + r], up[n], h[r][n]);
+    for (int n = 0; n < NP; ++n) {
+      h[0][n] = fma(sC[9], up[n], h[0][n]);
+      h[1][n] = fma(sC[10], up[n], h[1][n]);
+      fz[n] = fma(sC[11], up[n], fz[n]);
+    }
   }
 
-  // ---- E: in-plane volume partials and x / y lifts, in place; T2 goes to
-  // shared memory as soon as it is formed (its region is not read before)
+  // ---- E: volume term through the factorisation S (x) M (x) M = M3 (G (x) I (x) I),
+  // G = M^-1 S:  R = M_z [ M_x M_y V + L_xy ],  V = -(G_x F_x + G_y F_y + G_z F_z)
+  // + M_z^-1 e_0 fh_z0 + M_z^-1 e_3 fh_z3 (the z-face lifts folded through M_z).
+  // 6 contractions per node instead of 8, and no divergent z-lift branch.
+  __syncwarp();                                  // F_z planes complete
+  double v[NP];
+#pragma unroll
+  for (int j = 0; j < N1; ++j)
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double a = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        a = fma(P.g1[i * N1 + m], h[0][m + 4 * j], a);
+        a = fma(P.g1[j * N1 + m], h[1][i + 4 * m], a);
+      }
+      v[i + 4 * j] = -a;
+    }
   {
-    double (&F)[3][NP] = h;
+    const double z0 = s_tab[NP + 4 * k], z3 = s_tab[NP + 4 * k + 3];
 #pragma unroll
-    for (int i = 0; i < N1; ++i) {               // M_y F_z, M_y F_x, S_y F_y along column i
-      double a1[N1], b1[N1], c1[N1];
+    for (int m = 0; m < N1; ++m) {
+      const double gkm = -s_tab[4 * k + m];
 #pragma unroll
-      for (int j = 0; j < N1; ++j) {
-        double x1 = 0.0, x2 = 0.0, x3 = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) {
-          x1 = fma(P.m1[j * N1 + m], F[0][i + 4 * m], x1);
-          x2 = fma(P.s1[j * N1 + m], F[1][i + 4 * m], x2);
-          x3 = fma(P.m1[j * N1 + m], F[2][i + 4 * m], x3);
-        }
-        a1[j] = x1;
-        b1[j] = x2;
-        c1[j] = x3;
-      }
-#pragma unroll
-      for (int j = 0; j < N1; ++j) {
-        F[0][i + 4 * j] = a1[j];
-        F[1][i + 4 * j] = b1[j];
-        F[2][i + 4 * j] = c1[j];
-      }
+      for (int n = 0; n < NP; ++n) v[n] = fma(gkm, sT2[m * kPS + n], v[n]);
     }
 #pragma unroll
-    for (int j = 0; j < N1; ++j) {               // along x, row j
-      double g1[N1];
-#pragma unroll
-      for (int i = 0; i < N1; ++i) {
-        double x1 = 0.0, x2 = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) {
-          x1 = fma(P.s1[i * N1 + m], F[0][m + 4 * j], x1);
-          x1 = fma(P.m1[i * N1 + m], F[1][m + 4 * j], x1);
-          x2 = fma(P.m1[i * N1 + m], F[2][m + 4 * j], x2);
-        }
-        g1[i] = x1;
-        sT2[k * kPS + i + 4 * j] = -x2;          // T2 = -M_x M_y F_z
-      }
-#pragma unroll
-      for (int i = 0; i < N1; ++i) F[0][i + 4 * j] = -g1[i];
-    }
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int a = 0; a < N1; ++a) {
-        double lx = 0.0, ly = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) {
-          lx = fma(P.m1[a * N1 + m], sXY[(s * 2 + 0) * 4 + m], lx);
-          ly = fma(P.m1[a * N1 + m], sXY[(s * 2 + 1) * 4 + m], ly);
-        }
-        F[0][(s ? 3 : 0) + 4 * a] += lx;
-        F[0][a + 4 * (s ? 3 : 0)] += ly;
-      }
+    for (int n = 0; n < NP; ++n)
+      v[n] = fma(z0, sFZ[(n >> 2) * kES + (n & 3)], fma(z3, sFZ[20 + (n >> 2) * kES + (n & 3)], v[n]));
   }
-  // T1 over the u planes (dead since the jump exchange above)
+  // M_y along each column i, then M_x along each row j
 #pragma unroll
-  for (int n = 0; n < NP; ++n) sU[k * kPS + n] = h[0][n];
+  for (int i = 0; i < N1; ++i) {
+    double c1[N1];
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {
+      double a = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) a = fma(P.m1[j * N1 + m], v[i + 4 * m], a);
+      c1[j] = a;
+    }
+#pragma unroll
+    for (int j = 0; j < N1; ++j) v[i + 4 * j] = c1[j];
+  }
+#pragma unroll
+  for (int j = 0; j < N1; ++j) {
+    double r1[N1];
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double a = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) a = fma(P.m1[i * N1 + m], v[m + 4 * j], a);
+      r1[i] = a;
+    }
+#pragma unroll
+    for (int i = 0; i < N1; ++i) v[i + 4 * j] = r1[i];
+  }
+  // x / y face lifts (M along the face) from the thread's own slot
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int a = 0; a < N1; ++a) {
+      double lx = 0.0, ly = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        lx = fma(P.m1[a * N1 + m], sXY[(s * 2 + 0) * 4 + m], lx);
+        ly = fma(P.m1[a * N1 + m], sXY[(s * 2 + 1) * 4 + m], ly);
+      }
+      v[(s ? 3 : 0) + 4 * a] += lx;
+      v[a + 4 * (s ? 3 : 0)] += ly;
+    }
+  // W over the thread's u-plane slot (its face fluxes are consumed above)
+#pragma unroll
+  for (int n = 0; n < NP; ++n) sU[k * kPS + n] = v[n];
   __syncwarp();
-  // ---- F: z contraction, z-face lifts, source; R rows out through shared
+  // ---- F: z contraction, source; R rows out through shared
   double out[NP];
 #pragma unroll
   for (int n = 0; n < NP; ++n) out[n] = 0.0;
 #pragma unroll
   for (int m = 0; m < N1; ++m) {
-    const double mk = sel4(P.m1, k, m), sk = sel4(P.s1, k, m);
+    const double mk = s_tab[2 * NP + 4 * k + m];
 #pragma unroll
-    for (int n = 0; n < NP; ++n)
-      out[n] = fma(mk, sU[m * kPS + n], fma(sk, sT2[m * kPS + n], out[n]));
-  }
-  if (k == 0 || k == 3) {
-    const int f = k == 3;
-    double w[NP];                                // (M_x (x) M_y) fh_z
-#pragma unroll
-    for (int j = 0; j < N1; ++j)
-#pragma unroll
-      for (int i = 0; i < N1; ++i) {
-        double a = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) a = fma(P.m1[i * N1 + m], sFZ[f * 20 + j * kES + m], a);
-        w[i + 4 * j] = a;
-      }
-#pragma unroll
-    for (int j = 0; j < N1; ++j)
-#pragma unroll
-      for (int i = 0; i < N1; ++i) {
-        double a = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) a = fma(P.m1[j * N1 + m], w[i + 4 * m], a);
-        out[i + 4 * j] += a;
-      }
+    for (int n = 0; n < NP; ++n) out[n] = fma(mk, sU[m * kPS + n], out[n]);
   }
   if (active) {
 #pragma unroll
     for (int n = 0; n < NP; ++n) bad_if(P, e, out[n]);
   }
-  __syncwarp();                                  // T1 / T2 reads done
+  __syncwarp();                                  // W reads done
 #pragma unroll
   for (int n = 0; n < NP; ++n) sU[k * kPS + n] = out[n];
   __syncwarp();
@@ -1326,19 +1338,25 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
       const int smem = kPlaneEpb * kPlanePer * (int)sizeof(double);
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(plane_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
       }
-      if (P.flux_uses_u) {
-        if (tangent) plane_kernel<true, true><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X);
-        else plane_kernel<false, true><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X);
+#define LDG_PLANE(T, C, D) plane_kernel<T, C, D><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X)
+      if (P.c_diag) {
+        if (P.flux_uses_u) { if (tangent) LDG_PLANE(true, true, true); else LDG_PLANE(false, true, true); }
+        else { if (tangent) LDG_PLANE(true, false, true); else LDG_PLANE(false, false, true); }
       } else {
-        if (tangent) plane_kernel<true, false><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X);
-        else plane_kernel<false, false><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X);
+        if (P.flux_uses_u) { if (tangent) LDG_PLANE(true, true, false); else LDG_PLANE(false, true, false); }
+        else { if (tangent) LDG_PLANE(true, false, false); else LDG_PLANE(false, false, false); }
       }
+#undef LDG_PLANE
       if (cudaGetLastError() != cudaSuccess) return 3;
     } else if (tangent) fused_kernel<N1, ND, NCU, true><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
     else fused_kernel<N1, ND, NCU, false><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);

@@ -34,6 +34,8 @@ struct TensorParams {
   double m1[LDG_MAX_N1 * LDG_MAX_N1];
   double s1[LDG_MAX_N1 * LDG_MAX_N1];
   double m1inv[LDG_MAX_N1 * LDG_MAX_N1];
+  double g1[LDG_MAX_N1 * LDG_MAX_N1];   // M1^-1 S1: S1 (x) M1 (x) M1 = (M1 (x) M1 (x) M1)(G1 (x) I (x) I)
+  int c_diag;            // every element's C block is diagonal (axis-aligned affine hexes)
   double clo[LDG_MAX_N1];
   double chi[LDG_MAX_N1];
   double au[LDG_MAX_NCU * 3 * LDG_MAX_NCU];
