@@ -657,6 +657,31 @@ static_assert(kPlanePer % 16 == 4, "element stride must be 4 mod 16 doubles");
 constexpr int kPlaneMaps = 16;               // node maps cached in shared memory
 }  // namespace
 
+// acc[n] += c * plane[n], n < 16, for a padded plane at offset m * kPS of a
+// 16-B aligned element region: 16-B loads wherever the pair is aligned (the
+// four threads of an element read the same plane, so a 16-B broadcast moves
+// twice the data per shared wavefront)
+template <int M>
+__device__ __forceinline__ void axpy_plane(double (&acc)[16], double c, const double* plane) {
+  if ((M * 17) % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double2 v = reinterpret_cast<const double2*>(plane)[j];
+      acc[2 * j] = fma(c, v.x, acc[2 * j]);
+      acc[2 * j + 1] = fma(c, v.y, acc[2 * j + 1]);
+    }
+  } else {
+    acc[0] = fma(c, plane[0], acc[0]);
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+      const double2 v = reinterpret_cast<const double2*>(plane + 1)[j];
+      acc[2 * j + 1] = fma(c, v.x, acc[2 * j + 1]);
+      acc[2 * j + 2] = fma(c, v.y, acc[2 * j + 2]);
+    }
+    acc[15] = fma(c, plane[15], acc[15]);
+  }
+}
+
 #ifndef LDG_PLANE_MINB
 #define LDG_PLANE_MINB 2          // 2 persistent blocks per SM (shared-memory bound)
 #endif
@@ -813,12 +838,11 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     up[n] = sU[k * kPS + n];
     hz[n] = 0.0;
   }
-#pragma unroll
-  for (int m = 0; m < N1; ++m) {
-    const double dkm = s_tab[3 * NP + 4 * k + m];
-#pragma unroll
-    for (int n = 0; n < NP; ++n) hz[n] = fma(dkm, sU[m * kPS + n], hz[n]);
-  }
+  static_assert(kPS == 17, "axpy_plane assumes the 17-double plane stride");
+  axpy_plane<0>(hz, s_tab[3 * NP + 4 * k + 0], sU + 0 * kPS);
+  axpy_plane<1>(hz, s_tab[3 * NP + 4 * k + 1], sU + 1 * kPS);
+  axpy_plane<2>(hz, s_tab[3 * NP + 4 * k + 2], sU + 2 * kPS);
+  axpy_plane<3>(hz, s_tab[3 * NP + 4 * k + 3], sU + 3 * kPS);
 #pragma unroll
   for (int f = 0; f < 2; ++f) {                 // faces 0 (z-, plane 0), 1 (z+, plane 3)
     const int kind = info[f] & LDG_FACE_KIND_MASK;
@@ -844,9 +868,10 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     // h_z goes straight to the thread's F_z row (shared): it is not needed in
     // registers again until the flux combination, which keeps stage C spill-free
     const double clk = s_tab[4 * NP + k], chk = s_tab[4 * NP + 4 + k];
+    const double c2 = DIAG ? sC[8] : 1.0;           // diagonal C: store F_z = C_zz h_z directly
 #pragma unroll
     for (int n = 0; n < NP; ++n)
-      sT2[k * kPS + n] = -hz[n] - clk * sJZ[(n >> 2) * kES + (n & 3)] + chk * sJZ[20 + (n >> 2) * kES + (n & 3)];
+      sT2[k * kPS + n] = c2 * (-hz[n] - clk * sJZ[(n >> 2) * kES + (n & 3)] + chk * sJZ[20 + (n >> 2) * kES + (n & 3)]);
   }
   // ---- C: x / y faces at this plane and the in-plane gradients; the
   // own-data face fluxes go to the thread's (now dead) u-plane slot
@@ -905,14 +930,14 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   // share of the face fluxes, then F = F^q + Cu u
   double* fz = sT2 + k * kPS;                    // this plane's h_z, then F_z
   if (DIAG) {
-    const double c0 = sC[0], c1 = sC[4], c2 = sC[8];
+    const double c0 = sC[0], c1 = sC[4];
 #pragma unroll
     for (int n = 0; n < NP; ++n) {
       h[0][n] *= c0;
       h[1][n] *= c1;
-      fz[n] *= c2;
     }
   } else {
+    __syncwarp();                                // keeps the C-block loads out of stage C
 #pragma unroll
     for (int n = 0; n < NP; ++n) {
       const double h0 = h[0][n], h1 = h[1][n], h2 = fz[n];
@@ -1049,12 +1074,10 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     }
   {
     const double z0 = s_tab[NP + 4 * k], z3 = s_tab[NP + 4 * k + 3];
-#pragma unroll
-    for (int m = 0; m < N1; ++m) {
-      const double gkm = -s_tab[4 * k + m];
-#pragma unroll
-      for (int n = 0; n < NP; ++n) v[n] = fma(gkm, sT2[m * kPS + n], v[n]);
-    }
+    axpy_plane<0>(v, -s_tab[4 * k + 0], sT2 + 0 * kPS);
+    axpy_plane<1>(v, -s_tab[4 * k + 1], sT2 + 1 * kPS);
+    axpy_plane<2>(v, -s_tab[4 * k + 2], sT2 + 2 * kPS);
+    axpy_plane<3>(v, -s_tab[4 * k + 3], sT2 + 3 * kPS);
 #pragma unroll
     for (int n = 0; n < NP; ++n)
       v[n] = fma(z0, sFZ[(n >> 2) * kES + (n & 3)], fma(z3, sFZ[20 + (n >> 2) * kES + (n & 3)], v[n]));
@@ -1108,12 +1131,10 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   double out[NP];
 #pragma unroll
   for (int n = 0; n < NP; ++n) out[n] = 0.0;
-#pragma unroll
-  for (int m = 0; m < N1; ++m) {
-    const double mk = s_tab[2 * NP + 4 * k + m];
-#pragma unroll
-    for (int n = 0; n < NP; ++n) out[n] = fma(mk, sU[m * kPS + n], out[n]);
-  }
+  axpy_plane<0>(out, s_tab[2 * NP + 4 * k + 0], sU + 0 * kPS);
+  axpy_plane<1>(out, s_tab[2 * NP + 4 * k + 1], sU + 1 * kPS);
+  axpy_plane<2>(out, s_tab[2 * NP + 4 * k + 2], sU + 2 * kPS);
+  axpy_plane<3>(out, s_tab[2 * NP + 4 * k + 3], sU + 3 * kPS);
   if (active) {
 #pragma unroll
     for (int n = 0; n < NP; ++n) bad_if(P, e, out[n]);
