@@ -1179,8 +1179,16 @@ struct P2Smem {
   static constexpr int EPB = (kFBlock / TPE) > 0 ? (kFBlock / TPE) : 1;
 };
 
+#ifndef LDG_P2P_MINB
+#define LDG_P2P_MINB 8        // persistent pass-2 blocks per SM (64 registers)
+#endif
+// one-shot pass 2: a 40-register budget (12 blocks / SM) measured 58.4 us vs
+// 64.6 us at the default on config 3; other shapes keep the default
 template <int N1, int ND, int NCU>
-__global__ void __launch_bounds__(kFBlock)
+constexpr int p2_min_blocks() { return (N1 == 4 && ND == 3 && NCU == 1) ? 12 : 1; }
+
+template <int N1, int ND, int NCU>
+__global__ void __launch_bounds__(kFBlock, p2_min_blocks<N1, ND, NCU>())
 complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
                 const double* __restrict__ X, double* __restrict__ R) {
   using S = P2Smem<N1, ND, NCU>;
@@ -1335,6 +1343,257 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
   }
 }
 
+// Persistent, software-pipelined pass 2 for consumer-slot exports (the
+// default layout): the exports of element e sit in e's own 2*ND slots, so
+// the only dependent load is the completion mask.  Each block walks its
+// element groups with a two-deep register pipeline — the masks of group
+// g + 2, the R columns and exports of group g + 1 are in flight while group
+// g is lifted and written — so HBM sees ~3 groups of loads per block instead
+// of one dependent chain.
+template <int N1, int ND, int NCU>
+__global__ void __launch_bounds__(kFBlock, LDG_P2P_MINB)
+complete_pipe_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+                     const double* __restrict__ X, double* __restrict__ R) {
+  using S = P2Smem<N1, ND, NCU>;
+  constexpr int NB = S::NB, NF = S::NF, TPE = S::TPE, EPB = S::EPB, NFACE = S::NFACE;
+  __shared__ double sv[EPB][NFACE][NF][NCU];
+  __shared__ double sw2[EPB][NFACE][NF][NCU];
+  const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
+  const int i = lt % N1, j = ND == 3 ? lt / N1 : 0;
+  double Mi[N1], Mj[N1];
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    Mi[m] = P.m1[i * N1 + m];
+    Mj[m] = P.m1[j * N1 + m];
+  }
+  const int nel = P.e1 - P.e0;
+  const int ngroups = (nel + EPB - 1) / EPB;
+  const int stride = gridDim.x;
+  const double wgt = P.grad_centered ? -0.5 : -1.0;
+  // groups in reverse order: pass 1 finished with the last elements, whose R
+  // rows and exports are still resident in L2
+  auto elem = [&](int g) { return P.e0 + (ngroups - 1 - g) * EPB + slot; };
+  auto load_mask = [&](int g) {
+    int m = 0;
+    const int e = elem(g);
+    if (g < ngroups && slot < EPB && e < P.e1) {
+#pragma unroll
+      for (int lf = 0; lf < NFACE; ++lf) {
+        const int info = __ldg(reinterpret_cast<const int*>(frec + (size_t)e * NFACE + lf) + 3);
+        m |= (info & LDG_FL_COMPLETE) ? (1 << lf) : 0;
+      }
+      m |= 1 << 30;                                  // active
+    }
+    return m;
+  };
+  auto load_data = [&](int g, int m, double (&rc)[NCU][N1], double (&xv)[NFACE][NCU]) {
+    const int e = elem(g);
+    const bool act = m & (1 << 30);
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c)
+        rc[c][k] = act ? __ldg(R + ((size_t)e * NB + (ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k)) * NCU + c)
+                       : 0.0;
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c)
+        xv[lf][c] = (m & (1 << lf)) ? __ldg(X + (((size_t)e * NFACE + lf) * NF + lt) * NCU + c) : 0.0;
+  };
+
+  int g = blockIdx.x;
+  int m_c = load_mask(g), m_n = load_mask(g + stride);
+  double r_c[NCU][N1], x_c[NFACE][NCU], r_n[NCU][N1], x_n[NFACE][NCU];
+  load_data(g, m_c, r_c, x_c);
+  for (; g < ngroups; g += stride) {
+    const int m_nn = load_mask(g + 2 * stride);
+    load_data(g + stride, m_n, r_n, x_n);
+    const int e = elem(g);
+    const bool active = m_c & (1 << 30);
+    const int mask = m_c & 63;
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) sv[slot][lf][lt][c] = wgt * x_c[lf][c];
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int lf = 0; lf < NFACE; ++lf) {
+        if (!(mask & (1 << lf))) continue;
+#pragma unroll
+        for (int c = 0; c < NCU; ++c) {
+          double w = 0.0;
+#pragma unroll
+          for (int aa = 0; aa < N1; ++aa)
+            w = fma(Mi[aa], sv[slot][lf][ND == 3 ? aa + N1 * j : aa][c], w);
+          sw2[slot][lf][lt][c] = w;
+        }
+      }
+    }
+    __syncthreads();
+    if (active && ND == 3) {
+#pragma unroll
+      for (int lf = 0; lf < NFACE; ++lf) {
+        if (!(mask & (1 << lf))) continue;
+#pragma unroll
+        for (int c = 0; c < NCU; ++c) {
+          double o = 0.0;
+#pragma unroll
+          for (int bb = 0; bb < N1; ++bb) o = fma(Mj[bb], sw2[slot][lf][i + N1 * bb][c], o);
+          sv[slot][lf][lt][c] = o;
+        }
+      }
+    }
+    __syncthreads();
+    if (active && mask) {
+      auto fval = [&](int lf, int t, int c) {
+        return ND == 3 ? sv[slot][lf][t][c] : sw2[slot][lf][t][c];
+      };
+      double* Re = R + (size_t)e * NB * NCU;
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) {
+        double acc[N1];
+#pragma unroll
+        for (int k = 0; k < N1; ++k) acc[k] = 0.0;
+        if (ND == 3) {
+          if (mask & 1) acc[0] += fval(0, i + N1 * j, c);
+          if (mask & 2) acc[N1 - 1] += fval(1, i + N1 * j, c);
+#pragma unroll
+          for (int k = 0; k < N1; ++k) {
+            if ((mask & 4) && j == 0) acc[k] += fval(2, i + N1 * k, c);
+            if ((mask & 8) && j == N1 - 1) acc[k] += fval(3, i + N1 * k, c);
+            if ((mask & 16) && i == 0) acc[k] += fval(4, j + N1 * k, c);
+            if ((mask & 32) && i == N1 - 1) acc[k] += fval(5, j + N1 * k, c);
+          }
+        } else {
+          if (mask & 1) acc[0] += fval(0, i, c);
+          if (mask & 4) acc[N1 - 1] += fval(2, i, c);
+#pragma unroll
+          for (int k = 0; k < N1; ++k) {
+            if ((mask & 8) && i == 0) acc[k] += fval(3, k, c);
+            if ((mask & 2) && i == N1 - 1) acc[k] += fval(1, k, c);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          const int node = ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k;
+          const double out = r_c[c][k] + acc[k];
+          bad_if(P, e, out);
+          Re[node * NCU + c] = out;
+        }
+      }
+    }
+    __syncthreads();                                  // sv / sw2 reused next group
+    m_c = m_n;
+    m_n = m_nn;
+#pragma unroll
+    for (int c = 0; c < NCU; ++c)
+#pragma unroll
+      for (int k = 0; k < N1; ++k) r_c[c][k] = r_n[c][k];
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) x_c[lf][c] = x_n[lf][c];
+  }
+}
+
+// Register-only pass 2 for hex p = 3, ncu = 1 with consumer-slot exports:
+// half a warp per element, lane t = i + 4j owns R column (i, j) and face node
+// t of every face.  A completion face's 16 exports arrive as one coalesced
+// 128 B row; (M1 (x) M1) is applied with 8 shuffles, the z faces land in the
+// lane's own column ends and the x / y faces reach their owner columns with 4
+// more shuffles.  No shared memory and no block barriers.
+#ifndef LDG_P2W_MINB
+#define LDG_P2W_MINB 4        // 64 registers: measured 49 us vs 71 us at 77 registers
+#endif
+#ifndef LDG_P2W_PIPE
+#define LDG_P2W_PIPE 1
+#endif
+#ifndef LDG_P2W_GRID
+#define LDG_P2W_GRID LDG_P2W_MINB   // blocks per SM in the grid
+#endif
+__global__ void __launch_bounds__(256, LDG_P2W_MINB)
+complete_warp_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+                     const double* __restrict__ X, double* __restrict__ R) {
+  constexpr int NB = 64, NF = 16;
+  const int lane = threadIdx.x & 31, half = lane >> 4, t = lane & 15;
+  const int i = t & 3, j = t >> 2, hb = half * 16;
+  double Mi[4], Mj[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    Mi[m] = P.m1[i * 4 + m];
+    Mj[m] = P.m1[j * 4 + m];
+  }
+  const double wgt = P.grad_centered ? -0.5 : -1.0;
+  const int nel = P.e1 - P.e0;
+  const int npairs = (nel + 1) >> 1;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  // pairs in reverse order: pass 1 finished with the last elements (L2-resident)
+  auto elem = [&](int w) { return P.e0 + (npairs - 1 - w) * 2 + half; };
+  auto load_info = [&](int w) {
+    const int e = elem(w);
+    return (w < npairs && e < P.e1 && t < 6)
+               ? __ldg(reinterpret_cast<const int*>(frec + (size_t)e * 6 + t) + 3) : 0;
+  };
+  int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+#if LDG_P2W_PIPE
+  int info_next = load_info(w);
+#endif
+  for (; w < npairs; w += nwarps) {
+    const int e = elem(w);
+    const bool active = e < P.e1;
+#if LDG_P2W_PIPE
+    const int info = info_next;                              // loaded one pair ahead
+    info_next = load_info(w + nwarps);
+#else
+    const int info = load_info(w);
+#endif
+    double r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r[k] = active ? __ldg(R + (size_t)e * NB + t + 16 * k) : 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, (info & LDG_FL_COMPLETE) != 0);
+    const unsigned any = (bal | (bal >> 16)) & 63;           // faces completed in either element
+    const int mask = (bal >> hb) & 63;
+    double x[6];
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf)
+      x[lf] = (mask >> lf) & 1 ? __ldg(X + ((size_t)e * 6 + lf) * NF + t) : 0.0;
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf) {
+      if (!((any >> lf) & 1)) continue;                      // warp-uniform
+      const double v = wgt * x[lf];
+      // w(a', b) = sum_a M[a'][a] v(a, b) on lane (a', b); L(a', b') = sum_b M[b'][b] w(a', b)
+      double wv = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) wv = fma(Mi[a], __shfl_sync(0xffffffffu, v, hb + a + 4 * j), wv);
+      double L = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) L = fma(Mj[b], __shfl_sync(0xffffffffu, wv, hb + i + 4 * b), L);
+      if (!((mask >> lf) & 1)) L = 0.0;
+      if (lf == 0) r[0] += L;                                // z-: node (i, j, 0)
+      else if (lf == 1) r[3] += L;                           // z+: node (i, j, 3)
+      else {
+        // y faces: node (i, 0|3, k) <- face node (i, k); x faces: node (0|3, j, k) <- (j, k)
+        const bool own = lf == 2 ? j == 0 : (lf == 3 ? j == 3 : (lf == 4 ? i == 0 : i == 3));
+        const int a0 = lf < 4 ? i : j;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double g = __shfl_sync(0xffffffffu, L, hb + a0 + 4 * k);
+          if (own) r[k] += g;
+        }
+      }
+    }
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bad_if(P, e, r[k]);
+        R[(size_t)e * NB + t + 16 * k] = r[k];
+      }
+    }
+  }
+}
+
 // --------------------------------------------------------------------------
 // dispatch
 // --------------------------------------------------------------------------
@@ -1384,7 +1643,28 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
     if (cudaGetLastError() != cudaSuccess) return 3;
   }
   if (pass & 2) {
-    complete_kernel<N1, ND, NCU><<<grid2, kFBlock, 0, s>>>(
+    static int nsm2 = 0;
+    if (!nsm2) cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, 0);
+    static const bool pipe = !getenv("LDG_P2_PLAIN");      // A/B timing of the one-shot kernel
+    bool done = false;
+    static const bool warp2 = !getenv("LDG_P2_BLOCKWISE");  // A/B timing
+    if constexpr (N1 == 4 && ND == 3 && NCU == 1) {
+      if (P.x_consumer && warp2) {
+        const int npairs = (nel + 1) / 2;
+        const int g = std::max(1, std::min((npairs + 7) / 8, nsm2 * LDG_P2W_GRID));
+        complete_warp_kernel<<<g, 256, 0, s>>>(P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
+        done = true;
+      }
+    }
+    if constexpr (NCU == 1 && N1 <= 6) {            // register pipeline fits 64 registers spill-free
+      if (!done && P.x_consumer && pipe) {
+        complete_pipe_kernel<N1, ND, NCU><<<std::min(grid2, nsm2 * LDG_P2P_MINB), kFBlock, 0, s>>>(
+            P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
+        done = true;
+      }
+    }
+    if (!done)
+      complete_kernel<N1, ND, NCU><<<grid2, kFBlock, 0, s>>>(
           P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 3;

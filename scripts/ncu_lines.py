@@ -2,7 +2,7 @@
 view): stall samples, instructions, shared wavefronts (excess = bank
 conflicts), local (spill) traffic.
 
-    python scripts/ncu_lines.py rep.ncu-rep [top]
+    python scripts/ncu_lines.py rep.ncu-rep [top] [kernel-regex]
 """
 import csv, io, subprocess, sys
 
@@ -10,9 +10,11 @@ KEYS = ["Warp Stall Sampling (All Samples)", "Instructions Executed", "L1 Wavefr
         "L1 Wavefronts Shared Excessive"]
 
 
-def main(path, top=40):
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+def main(path, top=40, kernel=None):
+    cmd = ["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if kernel:
+        cmd += ["--kernel-name", f"regex:{kernel}"]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Line No")
     head = rows[hi]
@@ -53,4 +55,5 @@ def main(path, top=40):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40,
+         sys.argv[3] if len(sys.argv) > 3 else None)
