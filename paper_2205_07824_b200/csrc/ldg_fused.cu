@@ -654,6 +654,12 @@ constexpr int kOffJ = 2 * kInSz, kOffF = kOffJ + 40, kOffE = kOffF + 40;
 constexpr int kPlanePer = kOffE + 4 * kPS;   // 340
 static_assert(kInF + 12 <= kInSz, "layout");
 static_assert(kPlanePer % 16 == 4, "element stride must be 4 mod 16 doubles");
+// element regions of a warp: stride kPlanePer, elements 4..7 skewed by 2
+// doubles, so the 8 elements' 16-B broadcast reads hit 8 distinct bank
+// quads (4e + 2(e >> 2) mod 16 = 0, 4, 8, 12, 2, 6, 10, 14) while 8-B
+// per-thread accesses (4e + k) stay conflict-free
+__host__ __device__ constexpr int plane_el(int e) { return e * kPlanePer + (e >> 2) * 2; }
+constexpr int kPlaneWarp = plane_el(8);      // doubles per warp region
 constexpr int kPlaneMaps = 16;               // node maps cached in shared memory
 }  // namespace
 
@@ -717,8 +723,8 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     }
   }
   __syncthreads();
-  double* sWarp = psm + warp * 8 * kPlanePer;              // the warp's 8 element regions
-  double* sEl = sWarp + ls * kPlanePer;
+  double* sWarp = psm + warp * kPlaneWarp;                 // the warp's 8 element regions
+  double* sEl = sWarp + plane_el(ls);
   double* sJZ = sEl + kOffJ;
   double* sFZ = sEl + kOffF;
   double* sT2 = sEl + kOffE;
@@ -740,20 +746,20 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       for (int x = 0; x < 16; ++x) {
         const int d = lane + 32 * x;                       // element d/64, plane, node
         if (d < ne_w * NB)
-          cp_async8(dst + (d >> 6) * kPlanePer + ((d >> 4) & 3) * kPS + (d & 15), ub + d);
+          cp_async8(dst + plane_el(d >> 6) + ((d >> 4) & 3) * kPS + (d & 15), ub + d);
       }
       const double* kb = P.kco + (size_t)e_w * P.kstride;
 #pragma unroll
       for (int x = 0; x < 2; ++x) {                        // 8 elements x 8 chunks of 16 B
         const int c = lane + 32 * x, el = c >> 3, part = c & 7;
         if (el < ne_w && 2 * part < P.kstride)
-          cp_async16(dst + el * kPlanePer + kInC + 2 * part, kb + (size_t)el * P.kstride + 2 * part);
+          cp_async16(dst + plane_el(el) + kInC + 2 * part, kb + (size_t)el * P.kstride + 2 * part);
       }
       const double* fb = reinterpret_cast<const double*>(frec + (size_t)e_w * 6);
 #pragma unroll
       for (int x = 0; x < 2; ++x) {                        // 8 elements x 6 records of 16 B
         const int c = lane + 32 * x, el = c / 6, part = c % 6;
-        if (c < 48 && el < ne_w) cp_async16(dst + el * kPlanePer + kInF + 2 * part, fb + 2 * c);
+        if (c < 48 && el < ne_w) cp_async16(dst + plane_el(el) + kInF + 2 * part, fb + 2 * c);
       }
     }
     cp_async_commit();
@@ -1151,7 +1157,7 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     for (int x = 0; x < 16; ++x) {
       const int d = lane + 32 * x;
       if (d < nval) {
-        double v = sW[(d >> 6) * kPlanePer + ((d >> 4) & 3) * kPS + (d & 15)];
+        double v = sW[plane_el(d >> 6) + ((d >> 4) & 3) * kPS + (d & 15)];
         if (sb) v += __ldg(sb + d);
         rb[d] = v;
       }
@@ -1615,7 +1621,7 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
       if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
       const int groups = (nel + 7) / 8;
       const int gp = std::max(1, std::min((groups + 3) / 4, nsm * LDG_PLANE_MINB));
-      const int smem = kPlaneEpb * kPlanePer * (int)sizeof(double);
+      const int smem = (kPlaneBlock / 32) * kPlaneWarp * (int)sizeof(double);
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(plane_kernel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -48,15 +48,16 @@ def main(path):
             if m in col:
                 print(f"  {m:<66} {r[col[m]]:>20} {units[col[m]]}")
         stalls = []
+        pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
         for h, i in col.items():
-            if h.startswith(STALL2) and h.endswith("_per_warp_active.pct"):
+            if h.startswith(pre) and h.endswith(suf):
                 try:
-                    stalls.append((float(r[i].replace(",", "")), h[len(STALL2):-len("_per_warp_active.pct")]))
+                    stalls.append((float(r[i].replace(",", "")), h[len(pre):-len(suf)]))
                 except ValueError:
                     pass
         stalls.sort(reverse=True)
-        print("  top stalls (% of warp-active cycles): " +
-              ", ".join(f"{n} {v:.1f}" for v, n in stalls[:8]))
+        print("  top stalls (warps stalled per issued instruction): " +
+              ", ".join(f"{n} {v:.2f}" for v, n in stalls[:8]))
 
 
 if __name__ == "__main__":
