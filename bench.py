@@ -180,6 +180,62 @@ def load_traffic():
         return {}
 
 
+def fp64_line(p1_ms):
+    """FP64 peak measured with a DFMA microbenchmark
+    (ldg_probe_fp64) and the pass-1 kernel's FP64 rate from its exact FP64
+    operation count (ncu smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}
+    of the same bench command, profiles/fp64_counts.json; an FMA counts 2)."""
+    import ctypes
+    from paper_2205_07824_b200._lib import load, check
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    check(load().ldg_probe_fp64(20000, ctypes.byref(tf), ctypes.byref(ms), None), "fp64 probe")
+    out = {"peak_tflops": tf.value, "peak_source": "ldg_probe_fp64 (8 DFMA chains/thread)"}
+    try:
+        cnt = json.loads((ROOT / "profiles" / "fp64_counts.json").read_text())
+        fl = cnt["pass1_flops"]
+        out.update({"pass1_flops_per_launch": fl, "pass1_tflops": fl / (p1_ms * 1e-3) / 1e12,
+                    "pass1_frac": fl / (p1_ms * 1e-3) / 1e12 / tf.value,
+                    "count_source": cnt.get("source")})
+    except Exception:
+        pass
+    return out
+
+
+def tet_line(hbm, n=44, reps=10):
+    """SURVEY 8(d) config-3 tet variant: 3D Poisson on the Kuhn-tet box n=44,
+    p=3 (10,222,080 DOFs), tangent J du on the dense simplex kernels
+    (csrc/ldg_dense.cu), L2 flushed between reps."""
+    import torch
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem
+    t0 = time.perf_counter()
+    m = model.load_model(str(ROOT / "tests" / "golden" / "poisson3d.model"))
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [n] * 3, "tet")
+    s = LdgSystem(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("tet", 3))
+    setup = time.perf_counter() - t0
+    g = torch.Generator(device="cuda").manual_seed(0)
+    du = torch.randn((s.n_elements, s.n_nodes, 1), dtype=torch.float64, device="cuda", generator=g)
+    out = torch.empty_like(du)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        s.tangent_dev(du, out=out)
+    st = torch.cuda.current_stream()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        s.tangent_dev(du, out=out)
+        b.record(st)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    nd = s.n_dofs
+    return {"workload": f"config 3 tet variant: Kuhn tets n={n}, p=3, tangent J du", "dofs": nd,
+            "ms": ms, "gdofs": nd / (ms * 1e-3) / 1e9,
+            "matvec_frac_72B": nd * 72 / (ms * 1e-3) / 1e9 / hbm, "setup_s": round(setup, 1)}
+
+
 def nonlinear_lines(hbm, cpu=True):
     """Configs 4 and 2 on the generated-kernel path (scripts/nl_bench.py):
     3D compressible Navier-Stokes hex p=3 n=32 (10.5M DOFs) and 2D Euler quad
@@ -420,7 +476,7 @@ def run_b200(args, rank, world):
                      "traffic_source": traffic.get("source"),
                      "algorithmic_bytes_per_dof": bytes_p1 / ndof, "ms": p1,
                      "peak_source": peak_src},
-        "pass2_roofline": {"kernel": "complete_kernel<4,3,1> (pass 2)", "achieved": ach_p2,
+        "pass2_roofline": {"kernel": "complete_warp_kernel (pass 2, shuffle face lift)", "achieved": ach_p2,
                            "frac": ach_p2 / hbm, "algorithmic_bytes_per_dof": bytes_p2 / ndof,
                            "traffic": traffic.get("pass2"), "ms": p2},
         "matvec_roofline": {"achieved": ach_mv, "peak": hbm, "unit": "GB/s",
@@ -435,6 +491,10 @@ def run_b200(args, rank, world):
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
     }
+    if world == 1:
+        line["fp64"] = fp64_line(p1)
+    if world == 1 and not args.no_tet:
+        line["tet"] = tet_line(hbm)
     if world == 1 and not args.no_nonlinear:
         line["nonlinear"] = nonlinear_lines(hbm, cpu=not args.no_cpu_baseline)
     if world == 1 and not args.no_solve:
@@ -461,6 +521,8 @@ def main():
     ap.add_argument("--elems", dest="n", type=int, default=N_ELEM,
                     help="hexes per direction per rank (default 54 -> 10,077,696 DOFs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tet", action="store_true",
+                    help="skip the config-3 tet variant (44^3 Kuhn tets, dense kernels)")
     ap.add_argument("--no-solve", action="store_true",
                     help="skip the Newton-GMRES time-to-solution measurement")
     ap.add_argument("--no-nonlinear", action="store_true",

@@ -246,6 +246,12 @@ int ldg_jit_launch(LdgModule* m, const char* kernel, int grid_x, int grid_y,
 int ldg_jit_attr(LdgModule* m, const char* kernel, int* regs, int* local_bytes,
                  int* static_smem);
 
+/* ---- measurement helper (no reference counterpart) ---- */
+/* FP64 FMA throughput of the current GPU: 8 independent DFMA chains per
+ * thread, 8 x 256-thread blocks per SM, `iters` FMAs per chain; returns
+ * TFLOP/s (2 flops per FMA) and the kernel time (SURVEY 8(d) FP64 peak) */
+int ldg_probe_fp64(int64_t iters, double* tflops, double* ms, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,6 +98,7 @@ _SIGS = {
                      C.c_void_p], C.c_int),
     "ldg_color_distance2": ([C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
                             C.c_int),
+    "ldg_probe_fp64": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_bj_probe_vector": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p,
                              C.c_void_p], C.c_int),
     "ldg_bj_extract": ([C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,

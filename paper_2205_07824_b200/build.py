@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "lib" / "libldgb200.so"
 SOURCES = ["capi.cu", "ldg_tensor.cu", "ldg_fused.cu", "ldg_dense.cu", "krylov.cu",
-           "bjacobi.cu", "jit.cu"]
+           "bjacobi.cu", "jit.cu", "probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
