@@ -332,12 +332,26 @@ int ldg_create_dense(const LdgDenseTables* t, LdgHandle** out) {
   upi(t->fnbr, ne * nf, &D.fnbr, "fnbr");
   upi(t->finfo, ne * nf, &D.finfo, "finfo");
   up(t->ftau, ne * nf, &D.ftau, "ftau");
-  up(t->dr, nd * nb * nb, &D.dr, "dr");
-  up(t->kr, nd * nb * nb, &D.kr, "kr");
-  up(t->lift, nf * nb * nq, &D.lift, "lift");
-  up(t->fluxop, nf * nb * nq, &D.fluxop, "fluxop");
-  up(t->phif, nf * nq * nb, &D.phif, "phif");
-  up(t->phio, nf * (size_t)t->nperm * nq * nb, &D.phio, "phio");
+  // operators are stored with the thread index (node a / face point s)
+  // fastest, so a warp's operator loads for a fixed contraction index are
+  // contiguous rows (2 L1 wavefronts instead of up to 32): the last two
+  // indices of every (.., row, col) table are swapped
+  auto tr = [](const double* src, size_t nmat, size_t rows, size_t cols) {
+    std::vector<double> o(nmat * rows * cols);
+    for (size_t m = 0; m < nmat; ++m)
+      for (size_t r = 0; r < rows; ++r)
+        for (size_t c = 0; c < cols; ++c) o[(m * cols + c) * rows + r] = src[(m * rows + r) * cols + c];
+    return o;
+  };
+  const auto drT = tr(t->dr, nd, nb, nb), krT = tr(t->kr, nd, nb, nb);
+  const auto liftT = tr(t->lift, nf, nb, nq), foT = tr(t->fluxop, nf, nb, nq);
+  const auto phifT = tr(t->phif, nf, nq, nb), phioT = tr(t->phio, nf * (size_t)t->nperm, nq, nb);
+  up(drT.data(), drT.size(), &D.dr, "dr");
+  up(krT.data(), krT.size(), &D.kr, "kr");
+  up(liftT.data(), liftT.size(), &D.lift, "lift");
+  up(foT.data(), foT.size(), &D.fluxop, "fluxop");
+  up(phifT.data(), phifT.size(), &D.phif, "phif");
+  up(phioT.data(), phioT.size(), &D.phio, "phio");
   cudaError_t e = cudaMalloc(&h->bad, sizeof(unsigned long long));
   if (e != cudaSuccess) rc |= fail(3, "bad flag", e);
   else cudaMemset(h->bad, 0xff, sizeof(unsigned long long));

@@ -82,16 +82,21 @@ mixed_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
       double alpha, b_, wo_, wn_;
       coeffs(P, info[f], alpha, b_, wo_, wn_);
       const int kind = info[f] & LDG_FACE_KIND_MASK;
-      const double* pf = P.phif + (f * NQF + lt) * NB;
-      const double* po = P.phio + ((((info[f] >> 4) & 7) * P.nperm + ((info[f] >> 8) & 0xff)) * NQF + lt) * NB;
+      if (alpha == 0.0) {
+#pragma unroll
+        for (int c = 0; c < NCU; ++c) sjump[slot][f][lt][c] = 0.0;
+        continue;
+      }
+      const double* pf = P.phif + f * NB * NQF + lt;
+      const double* po = P.phio + (((info[f] >> 4) & 7) * P.nperm + ((info[f] >> 8) & 0xff)) * NB * NQF + lt;
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
         double own = 0.0, oth = 0.0;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) own = fma(__ldg(pf + b), su[slot][c][b], own);
+        for (int b = 0; b < NB; ++b) own = fma(__ldg(pf + b * NQF), su[slot][c][b], own);
         if (kind == LDG_FACE_INTERIOR) {
 #pragma unroll
-          for (int b = 0; b < NB; ++b) oth = fma(__ldg(po + b), snb[slot][f][c][b], oth);
+          for (int b = 0; b < NB; ++b) oth = fma(__ldg(po + b * NQF), snb[slot][f][c][b], oth);
         } else if (kind == LDG_FACE_DIRICHLET && gval) {
           oth = __ldg(gval + ((size_t)nbr[f] * NQF + lt) * NCU + c);
         }
@@ -114,9 +119,9 @@ mixed_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
 #pragma unroll
     for (int r = 0; r < ND; ++r) {
       double a = 0.0;
-      const double* dr = P.dr + (r * NB + lt) * NB;
+      const double* dr = P.dr + r * NB * NB + lt;
 #pragma unroll
-      for (int b = 0; b < NB; ++b) a = fma(__ldg(dr + b), su[slot][c][b], a);
+      for (int b = 0; b < NB; ++b) a = fma(__ldg(dr + b * NB), su[slot][c][b], a);
       gr[r] = a;
     }
     double qd[ND];
@@ -129,10 +134,10 @@ mixed_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
     }
 #pragma unroll
     for (int f = 0; f < NFACE; ++f) {
-      const double* lf_ = P.lift + (f * NB + lt) * NQF;
+      const double* lf_ = P.lift + f * NQF * NB + lt;
       double l = 0.0;
 #pragma unroll
-      for (int s = 0; s < NQF; ++s) l = fma(__ldg(lf_ + s), sjump[slot][f][s][c], l);
+      for (int s = 0; s < NQF; ++s) l = fma(__ldg(lf_ + s * NB), sjump[slot][f][s][c], l);
       const double fac = __ldg(P.fsj + e * NFACE + f) / detj * l;
 #pragma unroll
       for (int d = 0; d < ND; ++d) qd[d] = fma(fac, __ldg(P.fnorm + (e * NFACE + f) * ND + d), qd[d]);
@@ -228,16 +233,18 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
       double alpha, beta, wo, wn;
       coeffs(P, info[f], alpha, beta, wo, wn);
       const int kind = info[f] & LDG_FACE_KIND_MASK;
-      const double* pf = P.phif + (f * NQF + lt) * NB;
-      const double* po = P.phio + ((((info[f] >> 4) & 7) * P.nperm + ((info[f] >> 8) & 0xff)) * NQF + lt) * NB;
+      const double* pf = P.phif + f * NB * NQF + lt;
+      const double* po = P.phio + (((info[f] >> 4) & 7) * P.nperm + ((info[f] >> 8) & 0xff)) * NB * NQF + lt;
+      const bool inter = kind == LDG_FACE_INTERIOR;
       double uo[NCU], un[NCU], qh[NQ];
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
         double a = 0.0, b2 = 0.0;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          a = fma(__ldg(pf + b), su[slot][c][b], a);
-          b2 = fma(__ldg(po + b), snu[slot][f][c][b], b2);
+        for (int b = 0; b < NB; ++b) a = fma(__ldg(pf + b * NQF), su[slot][c][b], a);
+        if (inter && (alpha != 0.0 || beta != 0.0)) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b) b2 = fma(__ldg(po + b * NQF), snu[slot][f][c][b], b2);
         }
         uo[c] = a;
         un[c] = kind == LDG_FACE_INTERIOR ? b2
@@ -246,10 +253,13 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
 #pragma unroll
       for (int cd = 0; cd < NQ; ++cd) {
         double a = 0.0, b2 = 0.0;
+        if (wo != 0.0) {
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          a = fma(__ldg(pf + b), sq[slot][cd][b], a);
-          b2 = fma(__ldg(po + b), snq[slot][f][cd][b], b2);
+          for (int b = 0; b < NB; ++b) a = fma(__ldg(pf + b * NQF), sq[slot][cd][b], a);
+        }
+        if (inter && wn != 0.0) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b) b2 = fma(__ldg(po + b * NQF), snq[slot][f][cd][b], b2);
         }
         qh[cd] = wo * a + wn * b2;
       }
@@ -292,17 +302,17 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
     double r = 0.0;
 #pragma unroll
     for (int rr = 0; rr < ND; ++rr) {
-      const double* kr = P.kr + (rr * NB + lt) * NB;
+      const double* kr = P.kr + rr * NB * NB + lt;
 #pragma unroll
-      for (int b = 0; b < NB; ++b) r = fma(__ldg(kr + b), sF[slot][rr][c][b], r);
+      for (int b = 0; b < NB; ++b) r = fma(__ldg(kr + b * NB), sF[slot][rr][c][b], r);
     }
     double out = -r;
 #pragma unroll
     for (int f = 0; f < NFACE; ++f) {
-      const double* fo = P.fluxop + (f * NB + lt) * NQF;
+      const double* fo = P.fluxop + f * NQF * NB + lt;
       double a = 0.0;
 #pragma unroll
-      for (int s = 0; s < NQF; ++s) a = fma(__ldg(fo + s), sfh[slot][f][s][c], a);
+      for (int s = 0; s < NQF; ++s) a = fma(__ldg(fo + s * NB), sfh[slot][f][s][c], a);
       out = fma(__ldg(P.fsj + e * NFACE + f), a, out);
     }
     if (!TANGENT && bsrc) out += __ldg(bsrc + ((size_t)e * NB + lt) * NCU + c);

@@ -15,12 +15,15 @@ struct DenseParams {
   const int32_t* fnbr;
   const int32_t* finfo;   // bits: kind | side | switch | nbr face << 4 | orientation << 8
   const double* ftau;
-  const double* dr;       // (nd, nb, nb)   collocation derivatives
-  const double* kr;       // (nd, nb, nb)   int d_r phi_a phi_b
-  const double* lift;     // (nface, nb, nqf)  M_ref^-1 Phi^T W
-  const double* fluxop;   // (nface, nb, nqf)  Phi^T W
-  const double* phif;     // (nface, nqf, nb)  own traces
-  const double* phio;     // (nface, nperm, nqf, nb) neighbour traces by orientation
+  // device copies are stored TRANSPOSED in their last two indices (the
+  // thread's row index fastest): dr/kr (nd, b, a), lift/fluxop (nface, s, a),
+  // phif (nface, b, s), phio (nface, nperm, b, s)
+  const double* dr;       // collocation derivatives
+  const double* kr;       // int d_r phi_a phi_b
+  const double* lift;     // M_ref^-1 Phi^T W
+  const double* fluxop;   // Phi^T W
+  const double* phif;     // own traces
+  const double* phio;     // neighbour traces by orientation
   unsigned long long* bad;
   double au[LDG_MAX_NCU * 3 * LDG_MAX_NCU];
   double aq[LDG_MAX_NCU * 3 * LDG_MAX_NCU * 3];
