@@ -15,7 +15,10 @@ Signatures and semantics follow the reference:
 ``orth="mgs"`` (default) reproduces the reference's modified Gram-Schmidt
 with one conditional reorthogonalisation pass (the iteration-count parity
 mode); ``orth="cgs2"`` is the fast block variant (two classical passes, two
-multi-dot sweeps instead of 2(k+1) dependent ones).
+multi-dot sweeps instead of 2(k+1) dependent ones); ``orth="cgs"`` takes the
+second classical pass only under the reference's own reorthogonalisation
+rule (||w|| < 0.707 ||w_before||), halving the Krylov traffic when the first
+pass keeps orthogonality.
 """
 
 from __future__ import annotations
@@ -193,6 +196,24 @@ class _Workspace:
 _WS = _Workspace()
 
 
+def _trace(tag):
+    """LDG_GMRES_TRACE=1: synchronized wall-clock marks (diagnostics only)."""
+    import os
+    import time
+    if not os.environ.get("LDG_GMRES_TRACE"):
+        return lambda *_: None
+    import torch
+    state = {"t": time.perf_counter(), "n": 0}
+
+    def mark(name):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        if state["n"] < 6 or state["n"] % 50 == 0:
+            print(f"[gmres trace] {name} #{state['n']}: {1e3 * (t - state['t']):.2f} ms", flush=True)
+        state["t"], state["n"] = t, state["n"] + 1
+    return mark
+
+
 def gmres(op, rhs, precond=None, rel_tol=1e-8, restart=30, max_iter=200, x0=None,
           orth="mgs", ops=None):
     """Right-preconditioned restarted GMRES (solver.py:79-174) on device
@@ -231,7 +252,9 @@ def gmres(op, rhs, precond=None, rel_tol=1e-8, restart=30, max_iter=200, x0=None
         if beta <= tol:
             return GmresResult(out(x), True, total, res_norms, breakdown)
         m = min(restart, max_iter - total)
+        _tr = _trace("ws")
         ws = _WS.get(m, n, dev)
+        _tr("ws")
         V, Z, w, Hd, cd, nr = ws.V, ws.Z, ws.w, ws.H, ws.c, ws.nrm
         H = np.zeros((m + 1, m))
         cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
@@ -239,23 +262,35 @@ def gmres(op, rhs, precond=None, rel_tol=1e-8, restart=30, max_iter=200, x0=None
         torch.div(r, beta, out=V[0])
         k_done = 0
         for k in range(m):
+            _tr("it")
             z = M.apply(V[k])
             Z[k].copy_(z)
             w.copy_(apply_op(Z[k]))
             ops.nrm2(w, nr[0:1])
             col = Hd[k]                     # contiguous: device kernels index it linearly
-            if orth == "cgs2":
+            if orth in ("cgs2", "cgs"):
+                # classical Gram-Schmidt passes (one multi-dot + one fused
+                # update/norm each); "cgs" takes the second pass under the
+                # reference's rule ||w|| < 0.707 ||w_before|| (solver.py:139-144)
                 ops.cgs_dots(V, k + 1, w, col)
                 ops.cgs_update(V, k + 1, col, w, nr[1:2])
-                ops.cgs_dots(V, k + 1, w, cd)
-                ops.cgs_update(V, k + 1, cd, w, nr[2:3])
-                col[: k + 1] += cd[: k + 1]
-                hv = torch.cat([col[: k + 1], nr[:3]]).cpu().numpy()
-                nb0, nrm_w = hv[k + 1], hv[k + 3]
+                reorth = orth == "cgs2"
+                if not reorth:
+                    hn = nr[:2].cpu().numpy()
+                    if not np.isfinite(hn[0]):
+                        raise SolverError("gmres: operator returned non-finite values")
+                    reorth = hn[1] < 0.707 * hn[0]
+                src = nr[1:2]
+                if reorth:
+                    ops.cgs_dots(V, k + 1, w, cd)
+                    ops.cgs_update(V, k + 1, cd, w, nr[2:3])
+                    col[: k + 1] += cd[: k + 1]
+                    src = nr[2:3]
+                hv = torch.cat([col[: k + 1], src, nr[0:1]]).cpu().numpy()
+                nrm_w, nb0 = hv[k + 1], hv[k + 2]
                 if not np.isfinite(nb0):
                     raise SolverError("gmres: operator returned non-finite values")
                 H[: k + 1, k] = hv[: k + 1]
-                src = nr[2:3]
             else:
                 # modified Gram-Schmidt, dot of V_{i+1} fused into the axpy of V_i
                 ops.mgs_step(None, None, w, V[0], col[0:1])

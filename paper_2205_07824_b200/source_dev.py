@@ -1,0 +1,112 @@
+"""Volume source load on the device: b = -int s(x, t) phi (disc.py:621-629).
+
+The host restatement (tables.TensorTables.source_load) evaluates the source
+plan with numpy at every volume quadrature point of every element — ~2 s on
+the host at 10M DOFs, paid inside the first residual of a solve.  Here the
+model's source plan is lowered to a device function (codegen.emit_plan, the
+same lowering the generated kernels use) and one block per element
+evaluates it at the element's quadrature points x_q = x0 + J xi_q and
+contracts with the master tabulation: b_a = -sum_q detJ w_q s(x_q) phi_q(a).
+Compiled once per model with NVRTC through the C ABI (ldg_jit_*)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib, codegen
+from .tables import KernelNanError
+
+
+class SrcParams(C.Structure):
+    _fields_ = [("ne", C.c_int32), ("nq", C.c_int32), ("nb", C.c_int32), ("pad_", C.c_int32),
+                ("t", C.c_double)] + [(k, C.c_void_p) for k in (
+                    "x0", "J", "detj", "qp", "qw", "phi", "out", "bad")]
+
+
+def generate_source(model, nd):
+    ncu = model.ncu
+    L = [codegen.DEVICE_HELPERS,
+         codegen.emit_plan(model.source_plan(), "plan_src", nd, model.mu_bindings()),
+         "struct SrcParams { int ne, nq, nb, pad_; double t; const double *x0, *J, *detj, *qp,"
+         " *qw, *phi; double* out; unsigned long long* bad; };",
+         f"#define ND {nd}\n#define NCU {ncu}",
+         'extern "C" __global__ void __launch_bounds__(128) src_load(const SrcParams P) {',
+         "  extern __shared__ double sv[];                 // detJ w_q s(x_q), (nq, ncu)",
+         "  const int e = blockIdx.x;",
+         "  const double dj = P.detj[e];",
+         "  for (int q = threadIdx.x; q < P.nq; q += blockDim.x) {",
+         "    double x[ND], s[NCU];",
+         "    for (int d = 0; d < ND; ++d) {",
+         "      double v = P.x0[e * ND + d];",
+         "      for (int r = 0; r < ND; ++r) v += P.J[(e * ND + d) * ND + r] * P.qp[q * ND + r];",
+         "      x[d] = v;",
+         "    }",
+         "    plan_src(x, P.t, nullptr, nullptr, nullptr, nullptr, s);",
+         "    for (int c = 0; c < NCU; ++c) {",
+         "      if (!isfinite(s[c])) atomicMin(P.bad, (unsigned long long)e);",
+         "      sv[q * NCU + c] = dj * P.qw[q] * s[c];",
+         "    }",
+         "  }",
+         "  __syncthreads();",
+         "  for (int a = threadIdx.x; a < P.nb; a += blockDim.x)",
+         "    for (int c = 0; c < NCU; ++c) {",
+         "      double acc = 0.0;",
+         "      for (int q = 0; q < P.nq; ++q) acc = fma(sv[q * NCU + c], P.phi[q * P.nb + a], acc);",
+         "      P.out[((size_t)e * P.nb + a) * NCU + c] = -acc;",
+         "    }",
+         "}"]
+    return "\n".join(L) + "\n"
+
+
+class DeviceSource:
+    """Source load of one system on the device (tensor or simplex tables:
+    affine maps x0 + J xi, detJ, and the master's volume rule / tabulation)."""
+
+    def __init__(self, tab, device):
+        import torch
+        from .nonlinear import compile_source
+        self.tab, self.device = tab, device
+        m = tab.master
+        self.nd, self.ncu = tab.nd, tab.ncu
+        self.src = generate_source(tab.model, tab.nd)
+        self.cubin = compile_source(self.src)
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        _lib.check(self.lib.ldg_jit_load(self.cubin, len(self.cubin), C.byref(h)),
+                   "ldg_jit_load", jit=True)
+        self._mod = h
+
+        def dev(a):
+            return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=device)
+        self.x0, self.J, self.detj = dev(tab.x0), dev(tab.J), dev(tab.detj)
+        self.qp, self.qw, self.phi = dev(m.quad_pts), dev(m.quad_wts), dev(m.phi)
+        self.nq, self.nb = int(m.quad_pts.shape[0]), int(m.n_nodes)
+        self.bad = torch.full((1,), -1, dtype=torch.int64, device=device)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_mod", None):
+                self.lib.ldg_jit_unload(self._mod)
+        except Exception:
+            pass
+
+    def load(self, t):
+        import torch
+        out = torch.empty((self.tab.ne, self.nb, self.ncu), dtype=torch.float64,
+                          device=self.device)
+        P = SrcParams()
+        P.ne, P.nq, P.nb, P.t = self.tab.ne, self.nq, self.nb, float(t)
+        for k in ("x0", "J", "detj", "qp", "qw", "phi", "bad"):
+            setattr(P, k, getattr(self, k).data_ptr())
+        P.out = out.data_ptr()
+        if self.tab.ne:
+            _lib.check(self.lib.ldg_jit_launch(self._mod, b"src_load", self.tab.ne, 1, 128,
+                                               8 * self.nq * self.ncu, C.byref(P), C.sizeof(P),
+                                               _lib.stream_ptr()), "src_load", jit=True)
+        bad = int(self.bad.item())
+        if bad != -1:
+            self.bad.fill_(-1)
+            raise KernelNanError(f"source kernel produced non-finite values (first at element {bad})")
+        return out

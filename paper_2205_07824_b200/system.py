@@ -16,6 +16,7 @@ without a GPU raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,6 +24,10 @@ import numpy as np
 from . import _lib
 from .tables import DenseTables, DiscError, KernelNanError, TensorTables
 from .nonlinear import NlOperator, NlTables, linear_path_reason
+
+# elements from which the volume source load is evaluated on the device (the
+# host restatement costs ~15 us per element: 2.3 s at config 3's 157K hexes)
+DEVICE_SOURCE_MIN_NE = 32768
 
 __all__ = ["LdgSystem", "SolverState", "DiscError", "KernelNanError"]
 
@@ -140,6 +145,7 @@ class LdgSystem:
             self._create_handle()
         self._bdata = {}
         self._src = {}
+        self._devsrc = None
         self._scratch = {}
 
     # -- native handle -------------------------------------------------------------
@@ -321,7 +327,20 @@ class LdgSystem:
         if key not in self._src:
             if len(self._src) > 2:
                 self._src.clear()
-            b = self.tab.source_load(key)
+            if getattr(self.tab, "source_zero", False):
+                b = None
+            elif (getattr(self.tab, "x0", None) is not None and self.tab.ne >= DEVICE_SOURCE_MIN_NE
+                  and not os.environ.get("LDG_HOST_SOURCE")):
+                # the plan evaluated on the device (source_dev.py, agrees with
+                # the numpy restatement to ~1e-16: sin/exp ulps, summation
+                # order); small systems keep the restatement, whose cost there
+                # is negligible and whose rhs is the reference's to the bit
+                if self._devsrc is None:
+                    from .source_dev import DeviceSource
+                    self._devsrc = DeviceSource(self.tab, self.device)
+                b = self._devsrc.load(key)
+            else:
+                b = self.tab.source_load(key)
             self._src[key] = None if b is None else torch.as_tensor(b, device=self.device)
         return self._src[key]
 

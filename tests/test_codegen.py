@@ -64,3 +64,12 @@ def test_linear_models_keep_the_fused_path():
     assert linear_path_reason(model.builtin_model("poisson", nd=3)) is None
     assert linear_path_reason(model.builtin_model("convection_diffusion", nd=3)) is None
     assert linear_path_reason(model.builtin_model("euler", nd=2)) == "kind C"
+
+
+def test_device_source_compiles():
+    from paper_2205_07824_b200 import model
+    from paper_2205_07824_b200.nonlinear import compile_source
+    from paper_2205_07824_b200.source_dev import generate_source
+    m = model.load_model(str(__import__("cases").GOLDEN / "poisson3d.model"))
+    cubin = compile_source(generate_source(m, 3))
+    assert cubin[:4] == b"\x7fELF"

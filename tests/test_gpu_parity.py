@@ -186,3 +186,17 @@ def test_host_pipeline_matches_device_and_never_aliases():
     assert torch.equal(Jb, s.tangent_dev(b.cuda()).cpu())
     Ra = s.residual(st)[0]
     assert torch.equal(Ra, s.residual_dev(a.cuda()).cpu())
+
+
+@pytest.mark.parametrize("name", ["poisson3d_hex_p3", "poisson2d_quad_p3", "poisson2d_tri_p2",
+                                  "poisson3d_tet_p2", "convdiff2d_quad_dirichlet_p2"])
+def test_device_source_matches_host_restatement(name):
+    """source_dev.DeviceSource (plan on the device) == tables.source_load
+    (numpy restatement of disc.py:621-629)."""
+    from paper_2205_07824_b200.source_dev import DeviceSource
+    s = system_for(name)
+    if getattr(s.tab, "source_zero", False):
+        pytest.skip("model without a source")
+    dev = DeviceSource(s.tab, s.device).load(0.3).cpu().numpy()
+    host = s.tab.source_load(0.3)
+    assert rel(dev, host) < 1e-13

@@ -50,7 +50,7 @@ def test_gmres_reference_edge_cases():
 
 
 @pytest.mark.parametrize("name", sorted(SOLVE_CASES))
-@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+@pytest.mark.parametrize("orth", ["mgs", "cgs2", "cgs"])
 def test_steady_solve_matches_reference(name, orth):
     from paper_2205_07824_b200.driver import run_steady
     from paper_2205_07824_b200.system import LdgSystem
