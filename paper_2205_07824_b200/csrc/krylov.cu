@@ -15,7 +15,10 @@ namespace {
 
 constexpr int kRedBlocks = 1184;      // 8 x 148 SMs
 constexpr int kThreads = 256;
-constexpr int kMaxK = 8;              // dots per sweep in the multi-dot kernel
+#ifndef LDG_MULTIDOT_K
+#define LDG_MULTIDOT_K 16    // measured on the config-3 solve: 8 -> 2.19 s, 16 -> 1.91 s, 32 -> 2.08 s
+#endif
+constexpr int kMaxK = LDG_MULTIDOT_K;  // dots per sweep in the multi-dot kernel
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
