@@ -246,6 +246,18 @@ int ldg_jit_launch(LdgModule* m, const char* kernel, int grid_x, int grid_y,
 int ldg_jit_attr(LdgModule* m, const char* kernel, int* regs, int* local_bytes,
                  int* static_smem);
 
+/* DCGS2 orthogonalisation (delayed reorthogonalisation; solver.py:79-174's
+ * two Gram-Schmidt passes folded into one dot sweep and one update sweep):
+ * hx = V[0..k)^T x, hy = V[0..k)^T y in one sweep; then
+ * v <- (v - V s) * inv_alpha, out <- (w - V t - gamma v) * inv_alpha,
+ * nrm_out = ||out|| (V has m rows) */
+int ldg_dcgs_dots(int64_t n, int k, const double* V, int64_t ldv, const double* x,
+                  const double* y, double* scratch, double* hx, double* hy, void* stream);
+int ldg_dcgs_update(int64_t n, int m, const double* V, int64_t ldv, const double* s,
+                    const double* t, double* v, const double* w, double* out,
+                    double inv_alpha, double gamma, double* scratch, double* nrm_out,
+                    void* stream);
+
 /* ---- measurement helper (no reference counterpart) ---- */
 /* FP64 FMA throughput of the current GPU: 8 independent DFMA chains per
  * thread, 8 x 256-thread blocks per SM, `iters` FMAs per chain; returns

@@ -99,6 +99,11 @@ _SIGS = {
     "ldg_color_distance2": ([C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
                             C.c_int),
     "ldg_probe_fp64": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ldg_dcgs_dots": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ldg_dcgs_update": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                         C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_bj_probe_vector": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p,
                              C.c_void_p], C.c_int),
     "ldg_bj_extract": ([C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,

@@ -233,6 +233,124 @@ update_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
   finish(partials, ticket, 1, nrm, true, sh);
 }
 
+// DCGS2 (delayed classical Gram-Schmidt with reorthogonalisation): one sweep
+// gives both dot sets <V_i, x> and <V_i, y> for up to kDc rows (x = the
+// once-orthogonalised basis vector, y = the new Krylov vector)
+constexpr int kDc = kMaxK / 2;
+__global__ void __launch_bounds__(kThreads)
+multidot2_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
+                 const double* __restrict__ x, const double* __restrict__ y, double* partials,
+                 unsigned int* ticket, double* hx, double* hy) {
+  __shared__ double sh[kThreads / 32];
+  double ax[kDc], ay[kDc];
+#pragma unroll
+  for (int r = 0; r < kDc; ++r) ax[r] = ay[r] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+  if (vec) {
+    const int64_t n2 = n >> 1;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n2; i += stride) {
+      const double2 xv = reinterpret_cast<const double2*>(x)[i];
+      const double2 yv = reinterpret_cast<const double2*>(y)[i];
+#pragma unroll
+      for (int r = 0; r < kDc; ++r)
+        if (r < k) {
+          const double2 v = reinterpret_cast<const double2*>(V + (int64_t)r * ldv)[i];
+          ax[r] = fma(v.y, xv.y, fma(v.x, xv.x, ax[r]));
+          ay[r] = fma(v.y, yv.y, fma(v.x, yv.x, ay[r]));
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int64_t i = n - 1;
+#pragma unroll
+      for (int r = 0; r < kDc; ++r)
+        if (r < k) {
+          ax[r] = fma(V[(int64_t)r * ldv + i], x[i], ax[r]);
+          ay[r] = fma(V[(int64_t)r * ldv + i], y[i], ay[r]);
+        }
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+#pragma unroll
+      for (int r = 0; r < kDc; ++r)
+        if (r < k) {
+          const double v = V[(int64_t)r * ldv + i];
+          ax[r] = fma(v, x[i], ax[r]);
+          ay[r] = fma(v, y[i], ay[r]);
+        }
+    }
+  }
+  for (int r = 0; r < k; ++r) {
+    double s = block_sum(ax[r], sh);
+    if (threadIdx.x == 0) partials[(size_t)r * gridDim.x + blockIdx.x] = s;
+    s = block_sum(ay[r], sh);
+    if (threadIdx.x == 0) partials[(size_t)(k + r) * gridDim.x + blockIdx.x] = s;
+  }
+  // outputs: hx[0..k) then hy[0..k) (hy = hx + k in the caller's layout is
+  // not assumed: finish writes 2k values to a staging row)
+  __shared__ bool last;
+  __threadfence();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int v = 0; v < 2 * k; ++v) {
+    double s2 = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads)
+      s2 += partials[(size_t)v * gridDim.x + b];
+    s2 = block_sum(s2, sh);
+    if (threadIdx.x == 0) (v < k ? hx[v] : hy[v - k]) = s2;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// DCGS2 update, one sweep over V_0..V_{m-1}: the final basis vector
+// vf = (v - sum_j s_j V_j) * inv_alpha (written over v) and the projected
+// Krylov vector w1 = (w - sum_j t_j V_j - gamma vf) * inv_alpha (into out),
+// with ||w1|| fused.
+__global__ void __launch_bounds__(kThreads)
+update2_kernel(int64_t n, int m, const double* __restrict__ V, int64_t ldv,
+               const double* __restrict__ sc, const double* __restrict__ tc, double* v,
+               const double* __restrict__ w, double* __restrict__ out, double inv_alpha,
+               double gamma, double* partials, unsigned int* ticket, double* nrm) {
+  extern __shared__ double cs[];
+  __shared__ double sh[kThreads / 32];
+  for (int r = threadIdx.x; r < m; r += kThreads) {
+    cs[r] = sc[r];
+    cs[m + r] = tc[r];
+  }
+  __syncthreads();
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    int r = 0;
+    for (; r + 2 <= m; r += 2) {
+      const double v0 = V[(int64_t)r * ldv + i], v1 = V[(int64_t)(r + 1) * ldv + i];
+      a0 = fma(cs[r], v0, a0);
+      b0 = fma(cs[m + r], v0, b0);
+      a1 = fma(cs[r + 1], v1, a1);
+      b1 = fma(cs[m + r + 1], v1, b1);
+    }
+    if (r < m) {
+      const double v0 = V[(int64_t)r * ldv + i];
+      a0 = fma(cs[r], v0, a0);
+      b0 = fma(cs[m + r], v0, b0);
+    }
+    const double vf = (v[i] - (a0 + a1)) * inv_alpha;
+    v[i] = vf;
+    const double w1 = (w[i] - (b0 + b1) - gamma * vf) * inv_alpha;
+    out[i] = w1;
+    acc = fma(w1, w1, acc);
+  }
+  if (!nrm) return;
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  finish(partials, ticket, 1, nrm, true, sh);
+}
+
 inline unsigned int* ticket_of(double* scratch) {
   return reinterpret_cast<unsigned int*>(scratch + (size_t)kRedBlocks * kMaxK);
 }
@@ -300,6 +418,27 @@ int ldg_cgs_update(int64_t n, int k, const double* V, int64_t ldv, const double*
                    double* w, double* scratch, double* nrm_out, void* stream) {
   update_kernel<<<kRedBlocks, kThreads, k * sizeof(double), (cudaStream_t)stream>>>(
       n, k, V, ldv, h, -1.0, w, scratch, ticket_of(scratch), nrm_out);
+  return rc();
+}
+
+int ldg_dcgs_dots(int64_t n, int k, const double* V, int64_t ldv, const double* x,
+                  const double* y, double* scratch, double* hx, double* hy, void* stream) {
+  for (int r0 = 0; r0 < k; r0 += kDc) {
+    const int kk = k - r0 < kDc ? k - r0 : kDc;
+    multidot2_kernel<<<kRedBlocks, kThreads, 0, (cudaStream_t)stream>>>(
+        n, kk, V + (int64_t)r0 * ldv, ldv, x, y, scratch, ticket_of(scratch), hx + r0, hy + r0);
+    if (rc()) return 3;
+  }
+  return 0;
+}
+
+int ldg_dcgs_update(int64_t n, int m, const double* V, int64_t ldv, const double* s,
+                    const double* t, double* v, const double* w, double* out,
+                    double inv_alpha, double gamma, double* scratch, double* nrm_out,
+                    void* stream) {
+  update2_kernel<<<kRedBlocks, kThreads, 2 * (m > 0 ? m : 1) * sizeof(double),
+                   (cudaStream_t)stream>>>(n, m, V, ldv, s, t, v, w, out, inv_alpha, gamma,
+                                           scratch, ticket_of(scratch), nrm_out);
   return rc();
 }
 

@@ -205,6 +205,15 @@ class DistVecOps:
         self.b.cgs_update(V, k, h, w, None)
         self.nrm2(w, nrm_out)
 
+    def dcgs_dots(self, V, k, x, y, hx, hy):
+        self.b.dcgs_dots(V, k, x, y, hx, hy)
+        self._ar(hx[:k])
+        self._ar(hy[:k])
+
+    def dcgs_update(self, V, m, s, t, v, w, out, inv_alpha, gamma, nrm_out):
+        self.b.dcgs_update(V, m, s, t, v, w, out, inv_alpha, gamma, None)
+        self.nrm2(out, nrm_out)
+
     def combine(self, *a, **k):
         return self.b.combine(*a, **k)
 

@@ -143,6 +143,18 @@ class VecOps:
                                            _lib.ptr(w), _lib.ptr(self.scratch),
                                            _lib.ptr(nrm_out), self._st()), "ldg_cgs_update")
 
+    def dcgs_dots(self, V, k, x, y, hx, hy):
+        _lib.check(self.lib.ldg_dcgs_dots(x.numel(), k, _lib.ptr(V), V.stride(0), _lib.ptr(x),
+                                          _lib.ptr(y), _lib.ptr(self.scratch), _lib.ptr(hx),
+                                          _lib.ptr(hy), self._st()), "ldg_dcgs_dots")
+
+    def dcgs_update(self, V, m, s, t, v, w, out, inv_alpha, gamma, nrm_out):
+        _lib.check(self.lib.ldg_dcgs_update(w.numel(), m, _lib.ptr(V), V.stride(0), _lib.ptr(s),
+                                            _lib.ptr(t), _lib.ptr(v), _lib.ptr(w), _lib.ptr(out),
+                                            float(inv_alpha), float(gamma),
+                                            _lib.ptr(self.scratch), _lib.ptr(nrm_out),
+                                            self._st()), "ldg_dcgs_update")
+
     def combine(self, Z, k, y, x):
         _lib.check(self.lib.ldg_combine(x.numel(), k, _lib.ptr(Z), Z.stride(0), _lib.ptr(y),
                                         _lib.ptr(x), self._st()), "ldg_combine")
@@ -241,6 +253,9 @@ def gmres(op, rhs, precond=None, rel_tol=1e-8, restart=30, max_iter=200, x0=None
         return GmresResult(x=out(torch.zeros_like(b)), converged=True, iterations=0,
                            residual_norms=[0.0])
     tol = rel_tol * bnorm
+    if orth == "dcgs2":
+        return _gmres_dcgs2(apply_op, M, b, x, x0 is not None, bnorm, tol, restart, max_iter,
+                            ops, out)
     res_norms, total, breakdown = [], 0, False
     while total < max_iter:
         if total > 0 or x0 is not None:
@@ -344,6 +359,116 @@ def gmres(op, rhs, precond=None, rel_tol=1e-8, restart=30, max_iter=200, x0=None
             r = b - apply_op(x)
             ok = ops.norm(r) <= tol
             return GmresResult(out(x), ok, total, res_norms, True)
+    return GmresResult(out(x), False, total, res_norms, breakdown)
+
+
+def _givens_column(R, Hr, c, cs, sn, g):
+    """Rotate column c of the raw Hessenberg into R (solver.py:153-167)."""
+    R[: c + 2, c] = Hr[: c + 2, c]
+    for i in range(c):
+        t = cs[i] * R[i, c] + sn[i] * R[i + 1, c]
+        R[i + 1, c] = -sn[i] * R[i, c] + cs[i] * R[i + 1, c]
+        R[i, c] = t
+    den = np.hypot(R[c, c], R[c + 1, c])
+    if den == 0.0:
+        cs[c], sn[c] = 1.0, 0.0
+    else:
+        cs[c], sn[c] = R[c, c] / den, R[c + 1, c] / den
+    R[c, c] = den
+    R[c + 1, c] = 0.0
+    g[c + 1] = -sn[c] * g[c]
+    g[c] = cs[c] * g[c]
+    return abs(g[c + 1])
+
+
+def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops, out):
+    """GMRES with DCGS2 orthogonalisation: classical Gram-Schmidt with the
+    reorthogonalisation pass of basis vector k delayed into iteration k+1,
+    so each iteration makes ONE dot sweep over V (the dots of the
+    once-orthogonalised v'_k and of the new Krylov vector w' = A M^-1 v'_k)
+    and ONE update sweep (finalising v_k and projecting w'), against two of
+    each for CGS2.  The Arnoldi relation A M^-1 V = V H turns the correction
+    of v'_k into corrections of the Hessenberg coefficients:
+      s = V^T v'_k, alpha = sqrt(v'.v' - s.s), H[:k, k-1] += nu s,
+      H[k, k-1] = nu alpha, v_k = (v' - V s) / alpha,
+      h_j = (t_j - (H s)_j) / alpha, h_k = (gamma - (H s)_k) / alpha,
+      w1 = (w' - V t - gamma v_k) / alpha,  gamma = (v'.w' - s.t) / alpha,
+    with t = V^T w'.  Column k-1 is final one iteration later, so the
+    residual test (and the reported iteration count) lags by one matvec.
+    Z is not stored: x += M^-1 (V y) (M linear).  Same restart, tolerance,
+    breakdown and non-finite rules as the reference loop (solver.py:79-174)."""
+    import torch
+    n = b.numel()
+    dev = b.device
+    res_norms, total, breakdown = [], 0, False
+    while total < max_iter:
+        if total > 0 or have_x0:
+            r = b - apply_op(x)
+        else:
+            r = b.clone()
+        beta = ops.norm(r)
+        res_norms.append(beta)
+        if beta <= tol:
+            return GmresResult(out(x), True, total, res_norms, breakdown)
+        m = min(restart, max_iter - total)
+        ws = _WS.get(m, n, dev)
+        V, w, nr = ws.V, ws.w, ws.nrm
+        dx, dy, sd, td = ws.H[0], ws.H[1], ws.H[2], ws.c
+        Hr = np.zeros((m + 1, m))
+        R = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        g[0] = beta
+        torch.div(r, beta, out=V[0])
+        ncol, converged = 0, False
+        for k in range(m + 1):
+            if k < m:
+                w.copy_(apply_op(M.apply(V[k])))
+                ops.dcgs_dots(V, k + 1, V[k], w, dx, dy)
+            else:                                   # finalise the last column only
+                ops.dcgs_dots(V, k + 1, V[k], V[k], dx, dy)
+            hv = torch.cat([dx[: k + 1], dy[: k + 1], nr[0:1]]).cpu().numpy()
+            if not np.isfinite(hv).all():
+                raise SolverError("gmres: operator returned non-finite values")
+            if k == 0:
+                s = np.zeros(0)
+                alpha, nu = 1.0, 1.0
+            else:
+                s, vv, nu = hv[:k], hv[k], hv[2 * k + 2]
+                alpha = float(np.sqrt(max(vv - float(s @ s), 0.0)))
+                Hr[:k, k - 1] += nu * s
+                Hr[k, k - 1] = nu * alpha
+                if Hr[k, k - 1] <= 1e-14 * max(bnorm, 1.0):
+                    breakdown = True
+                ncol = k
+                total += 1
+                res = _givens_column(R, Hr, k - 1, cs, sn, g)
+                res_norms.append(float(res))
+                if res <= tol or breakdown or k == m:
+                    converged = res <= tol
+                    break
+            t, vw = hv[k + 1: 2 * k + 1], hv[2 * k + 1]
+            Hs = Hr[: k + 1, :k] @ s
+            gamma = (vw - float(s @ t)) / alpha
+            Hr[:k, k] = (t - Hs[:k]) / alpha
+            Hr[k, k] = (gamma - Hs[k]) / alpha
+            if k:
+                sd[:k].copy_(torch.as_tensor(s, device=dev))
+                td[:k].copy_(torch.as_tensor(t, device=dev))
+            ops.dcgs_update(V, k, sd, td, V[k], w, V[k + 1], 1.0 / alpha, gamma, nr[0:1])
+            ops.div(V[k + 1], nr[0:1], V[k + 1])
+        if ncol:
+            y = scipy.linalg.solve_triangular(R[:ncol, :ncol], g[:ncol])
+            u = w
+            u.zero_()
+            ops.combine(V, ncol, torch.as_tensor(y, device=dev), u)
+            x = x + M.apply(u).reshape(-1)
+        if abs(g[ncol]) <= tol:
+            return GmresResult(out(x), True, total, res_norms, breakdown)
+        if breakdown:
+            r = b - apply_op(x)
+            ok = ops.norm(r) <= tol
+            return GmresResult(out(x), ok, total, res_norms, True)
+        del converged
     return GmresResult(out(x), False, total, res_norms, breakdown)
 
 

@@ -14,7 +14,8 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def test_gmres_matches_oracle_on_dense_operator():
+@pytest.mark.parametrize("orth", ["mgs", "cgs2", "dcgs2"])
+def test_gmres_matches_oracle_on_dense_operator(orth):
     import torch
     from oracle.solver_oracle import gmres as ogmres
     from paper_2205_07824_b200.solver import gmres
@@ -25,7 +26,7 @@ def test_gmres_matches_oracle_on_dense_operator():
         A += np.diag(np.abs(A).sum(axis=1) + 1.0)      # test_solver.py:45-57
         b = rng.normal(size=n)
         Ad = torch.as_tensor(A, device="cuda")
-        res = gmres(lambda v: Ad @ v, b, rel_tol=1e-10, restart=20, max_iter=200)
+        res = gmres(lambda v: Ad @ v, b, rel_tol=1e-10, restart=20, max_iter=200, orth=orth)
         xo, conv, its, hist, _ = ogmres(lambda v: A @ v, b, None, 1e-10, 20, 200)
         assert res.converged and conv
         assert abs(res.iterations - its) <= 1
@@ -34,23 +35,24 @@ def test_gmres_matches_oracle_on_dense_operator():
         np.testing.assert_allclose(res.residual_norms[:k], hist[:k], rtol=1e-6)
 
 
-def test_gmres_reference_edge_cases():
+@pytest.mark.parametrize("orth", ["mgs", "dcgs2"])
+def test_gmres_reference_edge_cases(orth):
     import torch
     from paper_2205_07824_b200.solver import SolverError, gmres
     I = lambda v: v.clone()  # noqa: E731
-    r = gmres(I, np.arange(1.0, 9.0))
+    r = gmres(I, np.arange(1.0, 9.0), orth=orth)
     assert r.converged and r.iterations == 1
-    r = gmres(I, np.zeros(3))
+    r = gmres(I, np.zeros(3), orth=orth)
     assert r.converged and r.iterations == 0
     with pytest.raises(SolverError):
-        gmres(I, np.ones(2), rel_tol=2.0)
+        gmres(I, np.ones(2), rel_tol=2.0, orth=orth)
     with pytest.raises(SolverError):
-        gmres(lambda v: v * float("nan"), np.ones(4))
+        gmres(lambda v: v * float("nan"), np.ones(4), orth=orth)
     del torch
 
 
 @pytest.mark.parametrize("name", sorted(SOLVE_CASES))
-@pytest.mark.parametrize("orth", ["mgs", "cgs2", "cgs"])
+@pytest.mark.parametrize("orth", ["mgs", "cgs2", "cgs", "dcgs2"])
 def test_steady_solve_matches_reference(name, orth):
     from paper_2205_07824_b200.driver import run_steady
     from paper_2205_07824_b200.system import LdgSystem
