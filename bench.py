@@ -128,7 +128,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def run_solve(system, orth="cgs2"):
+def run_solve(system, orth="dcgs2"):
     """Newton-GMRES time to solution on the bench system with the
     reference acceptance flags (test_acceptance.py:69-81), block-Jacobi."""
     import torch

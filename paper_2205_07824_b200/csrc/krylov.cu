@@ -236,7 +236,10 @@ update_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
 // DCGS2 (delayed classical Gram-Schmidt with reorthogonalisation): one sweep
 // gives both dot sets <V_i, x> and <V_i, y> for up to kDc rows (x = the
 // once-orthogonalised basis vector, y = the new Krylov vector)
-constexpr int kDc = kMaxK / 2;
+#ifndef LDG_DCGS_ROWS
+#define LDG_DCGS_ROWS 8
+#endif
+constexpr int kDc = LDG_DCGS_ROWS;    // basis rows per DCGS2 dot sweep (2 dots each)
 __global__ void __launch_bounds__(kThreads)
 multidot2_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
                  const double* __restrict__ x, const double* __restrict__ y, double* partials,
@@ -351,8 +354,9 @@ update2_kernel(int64_t n, int m, const double* __restrict__ V, int64_t ldv,
   finish(partials, ticket, 1, nrm, true, sh);
 }
 
+constexpr int kScratchRows = kMaxK > 2 * kDc ? kMaxK : 2 * kDc;
 inline unsigned int* ticket_of(double* scratch) {
-  return reinterpret_cast<unsigned int*>(scratch + (size_t)kRedBlocks * kMaxK);
+  return reinterpret_cast<unsigned int*>(scratch + (size_t)kRedBlocks * kScratchRows);
 }
 
 inline int grid_for(int64_t n) {
@@ -366,7 +370,7 @@ inline int rc() { return cudaGetLastError() == cudaSuccess ? 0 : 3; }
 
 extern "C" {
 
-int64_t ldg_reduce_scratch_doubles(void) { return (int64_t)kRedBlocks * kMaxK + 8; }
+int64_t ldg_reduce_scratch_doubles(void) { return (int64_t)kRedBlocks * kScratchRows + 8; }
 
 // NOTE: reductions always launch the full kRedBlocks grid so partial counts
 // (and therefore rounding) do not depend on n.

@@ -79,7 +79,7 @@ def cpu_solve(n):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=54)
-    ap.add_argument("--orth", default="cgs2")
+    ap.add_argument("--orth", default="dcgs2")
     ap.add_argument("--restart", type=int, default=250)
     ap.add_argument("--cpu-n", type=int, default=0)
     a = ap.parse_args()
