@@ -327,7 +327,38 @@ update2_kernel(int64_t n, int m, const double* __restrict__ V, int64_t ldv,
   __syncthreads();
   double acc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+  const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(v) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(w) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  int64_t i0 = 0;
+  if (vec) {                        // two entries per thread, 16-B loads
+    const int64_t n2 = n >> 1;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n2; i += stride) {
+      double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+#pragma unroll 4
+      for (int r = 0; r < m; ++r) {
+        const double2 vr = reinterpret_cast<const double2*>(V + (int64_t)r * ldv)[i];
+        ax = fma(cs[r], vr.x, ax);
+        ay = fma(cs[r], vr.y, ay);
+        bx = fma(cs[m + r], vr.x, bx);
+        by = fma(cs[m + r], vr.y, by);
+      }
+      double2 vv = reinterpret_cast<double2*>(v)[i];
+      const double2 wv = reinterpret_cast<const double2*>(w)[i];
+      vv.x = (vv.x - ax) * inv_alpha;
+      vv.y = (vv.y - ay) * inv_alpha;
+      reinterpret_cast<double2*>(v)[i] = vv;
+      double2 o;
+      o.x = (wv.x - bx - gamma * vv.x) * inv_alpha;
+      o.y = (wv.y - by - gamma * vv.y) * inv_alpha;
+      reinterpret_cast<double2*>(out)[i] = o;
+      acc = fma(o.x, o.x, acc);
+      acc = fma(o.y, o.y, acc);
+    }
+    i0 = n2 * 2;                    // odd tail below (one element)
+  }
+  for (int64_t i = i0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
     double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
     int r = 0;
     for (; r + 2 <= m; r += 2) {
