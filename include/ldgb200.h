@@ -13,12 +13,18 @@
  *   ldg_dot / ldg_nrm2 / ldg_axpy / ldg_scal / ldg_copy
  *                            numpy dot/norm/axpy in gmres     solver.py:98-145
  *   ldg_mgs_step             MGS dot+axpy pair                solver.py:130-138
- *   ldg_cgs_dots / ldg_cgs_update  block Gram-Schmidt (fast mode)
+ *   ldg_cgs_dots / ldg_cgs_update  block Gram-Schmidt (fast mode) solver.py:130-144
+ *   ldg_dcgs_dots / ldg_dcgs_update  delayed-reorth Gram-Schmidt     solver.py:130-144
  *   ldg_combine              x += Z^T y                       solver.py:163-164
+ *   ldg_color_distance2      greedy distance-2 colouring      solver.py:355-378
  *   ldg_bj_probe_vector      coloured unit probe              solver.py:327-330
  *   ldg_bj_extract           mats[b][:,k] = col[blocks[b]]    solver.py:331-334
  *   ldg_bj_invert            lu_factor (+1e-12 shift rule)    solver.py:335-345
  *   ldg_bj_apply             BlockJacobiPreconditioner.apply  solver.py:296-300
+ *   ldg_jit_*                NVRTC modules of the generated kernels (nonlinear
+ *                            models, disc.py:436-948; the volume source load
+ *                            disc.py:621-629)
+ *   ldg_probe_fp64           measurement helper (FP64 FMA peak), no counterpart
  *
  * Conventions: every double* / int* argument is DEVICE memory owned by the
  * caller (PyTorch tensors on the host side); the handle owns only the
