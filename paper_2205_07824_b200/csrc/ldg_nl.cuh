@@ -110,22 +110,33 @@ __device__ __forceinline__ double op_c(int k) {
 template <int D0, int D1, int D2, int AX, int NIN, int NOUT, bool TRANS, int OPID>
 __device__ __forceinline__ void contract_u(const double* __restrict__ in, double* __restrict__ out,
                                            int nvar, int tid) {
+  // one thread per pencil along AX: its NIN inputs are read once, all NOUT
+  // outputs formed with compile-time (warp-uniform) operator entries
   constexpr int O0 = AX == 0 ? NOUT : D0, O1 = AX == 1 ? NOUT : D1, O2 = AX == 2 ? NOUT : D2;
   constexpr int I0 = AX == 0 ? NIN : D0, I1 = AX == 1 ? NIN : D1, I2 = AX == 2 ? NIN : D2;
   constexpr int OSZ = O0 * O1 * O2, ISZ = I0 * I1 * I2;
-  constexpr int STR = AX == 0 ? 1 : (AX == 1 ? I0 : I0 * I1);
-  const int total = nvar * OSZ;
+  constexpr int P0 = AX == 0 ? 1 : D0, P1 = AX == 1 ? 1 : D1, P2 = AX == 2 ? 1 : D2;
+  constexpr int NPN = P0 * P1 * P2;
+  constexpr int ISTR = AX == 0 ? 1 : (AX == 1 ? I0 : I0 * I1);
+  constexpr int OSTR = AX == 0 ? 1 : (AX == 1 ? O0 : O0 * O1);
+  (void)I2;
+  (void)O2;
+  const int total = nvar * NPN;
   for (int idx = tid; idx < total; idx += NT) {
-    const int v = idx / OSZ, r = idx - v * OSZ;
-    const int o0 = r % O0, o1 = (r / O0) % O1, o2 = r / (O0 * O1);
-    const int o = AX == 0 ? o0 : (AX == 1 ? o1 : o2);
-    const int base = v * ISZ + (AX == 0 ? 0 : o0) + (AX == 1 ? 0 : o1) * I0 +
-                     (AX == 2 ? 0 : o2) * I0 * I1;
-    double acc = 0.0;
+    const int v = idx / NPN, r = idx - v * NPN;
+    const int p0 = r % P0, p1 = (r / P0) % P1, p2 = r / (P0 * P1);
+    const int ib = v * ISZ + p0 + p1 * I0 + p2 * I0 * I1;
+    const int ob = v * OSZ + p0 + p1 * O0 + p2 * O0 * O1;
+    double x[NIN];
 #pragma unroll
-    for (int i = 0; i < NIN; ++i)
-      acc = fma(op_c<OPID>(TRANS ? i * N1 + o : o * N1 + i), in[base + i * STR], acc);
-    out[idx] = acc;
+    for (int i = 0; i < NIN; ++i) x[i] = in[ib + i * ISTR];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < NIN; ++i) acc = fma(op_c<OPID>(TRANS ? i * N1 + o : o * N1 + i), x[i], acc);
+      out[ob + o * OSTR] = acc;
+    }
   }
 }
 
