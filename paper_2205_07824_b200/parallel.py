@@ -127,6 +127,14 @@ class HaloExchanger:
 
     def __init__(self, plan, group=None):
         self.plan, self.group = plan, group
+        self._idx = {}
+
+    def _rows(self, kind, q, rows, device):
+        key = (kind, q, str(device))
+        if key not in self._idx:                 # index rows uploaded once per peer
+            import torch
+            self._idx[key] = torch.as_tensor(rows, device=device)
+        return self._idx[key]
 
     def exchange(self, arr):
         import torch
@@ -137,7 +145,7 @@ class HaloExchanger:
         ops, recv_bufs = [], []
         flat = arr.reshape(arr.shape[0], -1)
         for q, rows in sorted(self.plan.send.items()):
-            idx = torch.as_tensor(rows, device=arr.device)
+            idx = self._rows("s", q, rows, arr.device)
             buf = flat.index_select(0, idx).contiguous()
             if stage:
                 buf = buf.cpu()
@@ -145,13 +153,13 @@ class HaloExchanger:
         for q, rows in sorted(self.plan.recv.items()):
             buf = torch.empty((rows.size, flat.shape[1]), dtype=arr.dtype,
                               device="cpu" if stage else arr.device)
-            recv_bufs.append((rows, buf))
+            recv_bufs.append((self._rows("r", q, rows, arr.device), buf))
             ops.append(dist.P2POp(dist.irecv, buf, q, group=self.group))
         if ops:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
-        for rows, buf in recv_bufs:
-            flat.index_copy_(0, torch.as_tensor(rows, device=arr.device), buf.to(arr.device))
+        for idx, buf in recv_bufs:
+            flat.index_copy_(0, idx, buf.to(arr.device))
         return arr
 
 
