@@ -500,7 +500,7 @@ def run_b200(args, rank, world):
     if world == 1 and not args.no_solve:
         line["solve"] = {"metric": "Newton-GMRES time to solution (s), config 3, block-Jacobi, "
                                    "acceptance flags", "dofs": ndof,
-                         "gpu": run_solve(s, "cgs2")}
+                         "gpu": run_solve(s)}
         if not args.no_cpu_baseline:
             line["solve"]["cpu_oracle_small"] = {"n": 3, **cpu_solve(3)}
     if not args.no_cpu_baseline:
