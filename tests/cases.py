@@ -300,3 +300,18 @@ TRANSIENT_CASES.update({
 })
 
 TRANSIENT_FLAGS = dict(abs_tol=1e-10, rel_tol=1e-9, forcing=None, restart=60, gmres_max_iter=600)
+
+
+# diagnostics cases (tests/golden/gen_diagnostics.py, tests/test_gpu_diagnostics.py):
+# case -> (exact u, exact q or None, functional integrand, t)
+DIAG = {
+    "poisson2d_quad_p3": (["sin(3.14159*x1)*sin(3.14159*x2)"],
+                          ["3.14159*cos(3.14159*x1)*sin(3.14159*x2)",
+                           "3.14159*sin(3.14159*x1)*cos(3.14159*x2)"],
+                          "u1*u1 + 0.5*q1_1*x2", 0.0),
+    "poisson3d_hex_p2": (["x1*x2 + exp(-x3)"], None, "abs(u1) + q1_3*q1_3", 0.0),
+    "poisson3d_tet_p2": (["x1 + x2*x3"], ["1", "x3", "x2"], "u1*x1", 0.0),
+    "convdiff2d_quad_dirichlet_p2": (["x1*x2 + 0.5"], None, "u1 + sin(x1)", 0.25),
+    "euler2d_quad_dirichlet_p2": (["1", "0.1*x2", "0.05", "2.6"], None,
+                                  "u4 - 0.5*(u2*u2 + u3*u3)/u1", 0.0),
+}

@@ -73,3 +73,14 @@ def test_device_source_compiles():
     m = model.load_model(str(__import__("cases").GOLDEN / "poisson3d.model"))
     cubin = compile_source(generate_source(m, 3))
     assert cubin[:4] == b"\x7fELF"
+
+
+def test_device_diagnostics_compile():
+    from cases import CASES
+    from paper_2205_07824_b200.diagnostics import _source
+    from paper_2205_07824_b200.expr import compile_texts
+    from paper_2205_07824_b200.nonlinear import compile_source
+    model = build_case(CASES["poisson2d_quad_p3"], *b200_setup())[0]
+    for texts, nf, mode in ((["sin(x1)*x2"], 1, 0), (["u1*u1 + q1_2"], 1, 1)):
+        src = _source(model, 2, compile_texts(texts, model.symbols), nf, mode)
+        assert compile_source(src)[:4] == b"\x7fELF"
