@@ -89,6 +89,14 @@ __device__ __forceinline__ void bad_if(const TensorParams& P, int e, double v) {
   if (!isfinite(v)) atomicMin(P.bad, (unsigned long long)e);
 }
 
+// non-finite test of many values with integer ops only: the largest
+// |exponent field| over the high words (inf / NaN have it all ones), one
+// branch and at most one atomic per thread
+__device__ __forceinline__ int hi_abs(double v) { return __double2hiint(v) & 0x7fffffff; }
+__device__ __forceinline__ void bad_if_any(const TensorParams& P, int e, int hmax) {
+  if (hmax >= 0x7ff00000) atomicMin(P.bad, (unsigned long long)e);
+}
+
 }  // namespace
 
 // --------------------------------------------------------------------------
@@ -1142,8 +1150,10 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   axpy_plane<2>(out, s_tab[2 * NP + 4 * k + 2], sU + 2 * kPS);
   axpy_plane<3>(out, s_tab[2 * NP + 4 * k + 3], sU + 3 * kPS);
   if (active) {
+    int hm = 0;
 #pragma unroll
-    for (int n = 0; n < NP; ++n) bad_if(P, e, out[n]);
+    for (int n = 0; n < NP; ++n) hm = max(hm, hi_abs(out[n]));
+    bad_if_any(P, e, hm);
   }
   __syncwarp();                                  // W reads done
 #pragma unroll
@@ -1591,11 +1601,13 @@ complete_warp_kernel(const __grid_constant__ TensorParams P, const FaceRec* __re
       }
     }
     if (active) {
+      int hm = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        bad_if(P, e, r[k]);
+        hm = max(hm, hi_abs(r[k]));
         R[(size_t)e * NB + t + 16 * k] = r[k];
       }
+      bad_if_any(P, e, hm);
     }
   }
 }

@@ -132,13 +132,19 @@ def test_device_path_is_deterministic_and_linear_at_scale():
     assert float(err) < 1e-13
 
 
-def test_nan_reported_with_element():
+@pytest.mark.parametrize("name", ["poisson3d_hex_p2", "poisson3d_hex_p3"])
+def test_nan_reported_with_element(name):
+    """hex p=2: pencil kernel; hex p=3: plane kernel + warp completion
+    kernel (integer exponent test, one atomic per thread)."""
     from paper_2205_07824_b200.system import KernelNanError, SolverState
-    s = system_for("poisson3d_hex_p2")
+    s = system_for(name)
     u = np.zeros((s.n_elements, s.n_nodes, 1))
     u[5, 3, 0] = np.nan
     with pytest.raises(KernelNanError, match="non-finite values"):
         s.residual(SolverState(u=u, q=None, w=None, t=0.0))
+    u[5, 3, 0] = np.inf
+    with pytest.raises(KernelNanError, match="non-finite values"):
+        s.residual_tangent(SolverState(u=u, q=None, w=None, t=0.0), u)
 
 
 @pytest.mark.parametrize("name,nparts", [("poisson3d_hex_p3", 3), ("convdiff3d_hex_periodic_p2", 4),
