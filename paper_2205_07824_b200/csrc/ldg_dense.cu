@@ -76,19 +76,22 @@ mixed_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
     }
   }
   __syncthreads();
-  if (active && lt < NQF) {
-#pragma unroll
-    for (int f = 0; f < NFACE; ++f) {
+  // face points: (face, point) pairs spread over all TPE lanes (NFACE * NQF
+  // items; the per-face loop of one point per lane left TPE - NQF idle)
+  if (active) {
+    for (int idx = lt; idx < NFACE * NQF; idx += TPE) {
+      const int f = idx / NQF, sp = idx - f * NQF;
+      const int inf = __ldg(P.finfo + e * NFACE + f);
       double alpha, b_, wo_, wn_;
-      coeffs(P, info[f], alpha, b_, wo_, wn_);
-      const int kind = info[f] & LDG_FACE_KIND_MASK;
+      coeffs(P, inf, alpha, b_, wo_, wn_);
+      const int kind = inf & LDG_FACE_KIND_MASK;
       if (alpha == 0.0) {
 #pragma unroll
-        for (int c = 0; c < NCU; ++c) sjump[slot][f][lt][c] = 0.0;
+        for (int c = 0; c < NCU; ++c) sjump[slot][f][sp][c] = 0.0;
         continue;
       }
-      const double* pf = P.phif + f * NB * NQF + lt;
-      const double* po = P.phio + (((info[f] >> 4) & 7) * P.nperm + ((info[f] >> 8) & 0xff)) * NB * NQF + lt;
+      const double* pf = P.phif + f * NB * NQF + sp;
+      const double* po = P.phio + (((inf >> 4) & 7) * P.nperm + ((inf >> 8) & 0xff)) * NB * NQF + sp;
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
         double own = 0.0, oth = 0.0;
@@ -98,9 +101,9 @@ mixed_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
 #pragma unroll
           for (int b = 0; b < NB; ++b) oth = fma(__ldg(po + b * NQF), snb[slot][f][c][b], oth);
         } else if (kind == LDG_FACE_DIRICHLET && gval) {
-          oth = __ldg(gval + ((size_t)nbr[f] * NQF + lt) * NCU + c);
+          oth = __ldg(gval + ((size_t)__ldg(P.fnbr + e * NFACE + f) * NQF + sp) * NCU + c);
         }
-        sjump[slot][f][lt][c] = alpha * (own - oth);
+        sjump[slot][f][sp][c] = alpha * (own - oth);
       }
     }
   }
@@ -227,14 +230,16 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
       }
     }
   }
-  if (active && lt < NQF) {
-#pragma unroll
-    for (int f = 0; f < NFACE; ++f) {
+  if (active) {
+    for (int idx = lt; idx < NFACE * NQF; idx += TPE) {      // (face, point) pairs over all lanes
+      const int f = idx / NQF, sp = idx - f * NQF;
+      const int inf = __ldg(P.finfo + e * NFACE + f);
+      const int nbf = __ldg(P.fnbr + e * NFACE + f);
       double alpha, beta, wo, wn;
-      coeffs(P, info[f], alpha, beta, wo, wn);
-      const int kind = info[f] & LDG_FACE_KIND_MASK;
-      const double* pf = P.phif + f * NB * NQF + lt;
-      const double* po = P.phio + (((info[f] >> 4) & 7) * P.nperm + ((info[f] >> 8) & 0xff)) * NB * NQF + lt;
+      coeffs(P, inf, alpha, beta, wo, wn);
+      const int kind = inf & LDG_FACE_KIND_MASK;
+      const double* pf = P.phif + f * NB * NQF + sp;
+      const double* po = P.phio + (((inf >> 4) & 7) * P.nperm + ((inf >> 8) & 0xff)) * NB * NQF + sp;
       const bool inter = kind == LDG_FACE_INTERIOR;
       double uo[NCU], un[NCU], qh[NQ];
 #pragma unroll
@@ -248,7 +253,7 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
         }
         uo[c] = a;
         un[c] = kind == LDG_FACE_INTERIOR ? b2
-                : ((!TANGENT && gval) ? __ldg(gval + ((size_t)nbr[f] * NQF + lt) * NCU + c) : 0.0);
+                : ((!TANGENT && gval) ? __ldg(gval + ((size_t)nbf * NQF + sp) * NCU + c) : 0.0);
       }
 #pragma unroll
       for (int cd = 0; cd < NQ; ++cd) {
@@ -271,7 +276,7 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
       for (int c = 0; c < NCU; ++c) {
         double fh;
         if (kind == LDG_FACE_NEUMANN) {
-          fh = (!TANGENT && gval) ? __ldg(gval + ((size_t)nbr[f] * NQF + lt) * NCU + c) : 0.0;
+          fh = (!TANGENT && gval) ? __ldg(gval + ((size_t)nbf * NQF + sp) * NCU + c) : 0.0;
         } else {
           double uh[NCU];
 #pragma unroll
@@ -291,7 +296,7 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
           }
           fh = fn + beta * tau * (uo[c] - un[c]);
         }
-        sfh[slot][f][lt][c] = fh;
+        sfh[slot][f][sp][c] = fh;
       }
     }
   }
