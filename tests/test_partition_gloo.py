@@ -58,8 +58,19 @@ class CpuOps:
     def combine(self, Z, k, y, x):
         x.add_(y[:k] @ Z[:k])
 
+    def dcgs_dots(self, V, k, x, y, hx, hy):
+        hx[:k] = V[:k] @ x
+        hy[:k] = V[:k] @ y
 
-def _worker(rank, world, port, name, q):
+    def dcgs_update(self, V, m, s, t, v, w, out, inv_alpha, gamma, nrm):
+        vf = (v - s[:m] @ V[:m]) * inv_alpha
+        v.copy_(vf)
+        out.copy_((w - t[:m] @ V[:m] - gamma * vf) * inv_alpha)
+        if nrm is not None:
+            nrm.fill_(float(torch.linalg.vector_norm(out)))
+
+
+def _worker(rank, world, port, name, q, orth):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -102,7 +113,7 @@ def _worker(rank, world, port, name, q):
         from paper_2205_07824_b200.solver import NewtonOptions, newton_solve
         ops = DistVecOps(CpuOps())
         opts = NewtonOptions(abs_tol=1e-11, rel_tol=3e-8, forcing=1e-10, gmres_restart=400,
-                             gmres_max_iter=2000, jv_mode="tangent", orth="cgs2")
+                             gmres_max_iter=2000, jv_mode="tangent", orth=orth)
         x, st = newton_solve(lambda v: apply(v, False), torch.zeros(plan.ne_loc * nb * ncu,
                                                                     dtype=torch.float64),
                              opts, tangent_fn=lambda x_, v: apply(v, True), ops=ops)
@@ -112,9 +123,10 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["poisson3d_hex_p3", "convdiff3d_hex_periodic_p2",
-                                  "poisson2d_quad_p3", "poisson3d_hex_centered_p2"])
-def test_partitioned_operator_and_solve_gloo(name):
+@pytest.mark.parametrize("name,orth", [("poisson3d_hex_p3", "cgs2"), ("convdiff3d_hex_periodic_p2", "cgs2"),
+                                       ("poisson2d_quad_p3", "cgs2"), ("poisson3d_hex_centered_p2", "cgs2"),
+                                       ("poisson3d_hex_p3", "dcgs2"), ("convdiff3d_hex_periodic_p2", "dcgs2")])
+def test_partitioned_operator_and_solve_gloo(name, orth):
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
     import tensor_emulation as emu
@@ -125,7 +137,7 @@ def test_partitioned_operator_and_solve_gloo(name):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, orth)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -147,7 +159,7 @@ def test_partitioned_operator_and_solve_gloo(name):
                                          None if tangent else bs)).reshape(-1)
 
     opts = NewtonOptions(abs_tol=1e-11, rel_tol=3e-8, forcing=1e-10, gmres_restart=400,
-                         gmres_max_iter=2000, jv_mode="tangent", orth="cgs2")
+                         gmres_max_iter=2000, jv_mode="tangent", orth=orth)
     x, st = newton_solve(lambda v: apply(v, False), torch.zeros(int(np.prod(shape)),
                                                                  dtype=torch.float64),
                          opts, tangent_fn=lambda x_, v: apply(v, True), ops=CpuOps())
