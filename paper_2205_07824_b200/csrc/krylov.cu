@@ -13,7 +13,10 @@
 
 namespace {
 
-constexpr int kRedBlocks = 1184;      // 8 x 148 SMs
+#ifndef LDG_RED_BLOCKS
+#define LDG_RED_BLOCKS 592     // 4 x 148 SMs; config-3 solve: 1184 -> 1.49 s, 592 -> 1.40 s, 296 -> 1.81 s
+#endif
+constexpr int kRedBlocks = LDG_RED_BLOCKS;
 constexpr int kThreads = 256;
 #ifndef LDG_MULTIDOT_K
 #define LDG_MULTIDOT_K 16    // measured on the config-3 solve: 8 -> 2.19 s, 16 -> 1.91 s, 32 -> 2.08 s
