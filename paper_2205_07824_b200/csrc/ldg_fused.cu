@@ -1674,7 +1674,9 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
         done = true;
       }
     }
-    if constexpr (NCU == 1 && N1 <= 6) {            // register pipeline fits 64 registers spill-free
+    // register-pipelined pass 2 (64 registers): measured faster for p <= 2
+    // (config 5: p=1 23.0 -> 23.4, p=2 27.6 -> 29.0 GDOF/s), slower for p = 4, 5
+    if constexpr (NCU == 1 && N1 <= 3) {
       if (!done && P.x_consumer && pipe) {
         complete_pipe_kernel<N1, ND, NCU><<<std::min(grid2, nsm2 * LDG_P2P_MINB), kFBlock, 0, s>>>(
             P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
