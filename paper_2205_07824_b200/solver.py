@@ -190,18 +190,19 @@ class _Workspace:
     def __init__(self):
         self.key = None
 
-    def get(self, m, n, device):
+    def get(self, m, n, device, need_z=True):
         import torch
         if self.key != (m, n, str(device)):
             self.V = self.Z = None
             torch.cuda.empty_cache()
             self.V = torch.empty((m + 1, n), dtype=torch.float64, device=device)
-            self.Z = torch.empty((m, n), dtype=torch.float64, device=device)
             self.w = torch.empty(n, dtype=torch.float64, device=device)
             self.H = torch.zeros((m + 1, m + 2), dtype=torch.float64, device=device)  # row k = column k of H
             self.c = torch.zeros(m + 2, dtype=torch.float64, device=device)
             self.nrm = torch.zeros(4, dtype=torch.float64, device=device)
             self.key = (m, n, str(device))
+        if need_z and self.Z is None:           # DCGS2 keeps no Z (x += M^-1 (V y))
+            self.Z = torch.empty((m, n), dtype=torch.float64, device=device)
         return self
 
 
@@ -411,7 +412,7 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
         if beta <= tol:
             return GmresResult(out(x), True, total, res_norms, breakdown)
         m = min(restart, max_iter - total)
-        ws = _WS.get(m, n, dev)
+        ws = _WS.get(m, n, dev, need_z=False)
         V, w, nr = ws.V, ws.w, ws.nrm
         dx, dy, sd, td = ws.H[0], ws.H[1], ws.H[2], ws.c
         Hr = np.zeros((m + 1, m))
