@@ -85,10 +85,6 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
-__device__ __forceinline__ void bad_if(const TensorParams& P, int e, double v) {
-  if (!isfinite(v)) atomicMin(P.bad, (unsigned long long)e);
-}
-
 // non-finite test of many values with integer ops only: the largest
 // |exponent field| over the high words (inf / NaN have it all ones), one
 // branch and at most one atomic per thread
@@ -551,14 +547,16 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         }
         out[0] += xl;
         out[N1 - 1] += xh;
+        int hm = 0;
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
           const int node = a + N1 * ta + N1 * N1 * tb;
           double o = out[a];
           if (!TANGENT && bsrc) o += __ldg(bsrc + ((size_t)e * NB + node) * NCU + c);
-          bad_if(P, e, o);
+          hm = max(hm, hi_abs(o));
           Re[node * NCU + c] = o;
         }
+        bad_if_any(P, e, hm);
       }
       if (NCU > 1) __syncthreads();
     } else {
@@ -599,6 +597,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
           a1[m] = sr[m + N1 * ta];
           a2[m] = sr[NBP + m + N1 * ta];
         }
+        int hm = 0;
 #pragma unroll
         for (int a = 0; a < N1; ++a) {
           double r = 0.0;
@@ -612,9 +611,10 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
           if (a == N1 - 1) o += sX[1 * N1 + ta];
           const int node = a + N1 * ta;
           if (!TANGENT && bsrc) o += __ldg(bsrc + ((size_t)e * NB + node) * NCU + c);
-          bad_if(P, e, o);
+          hm = max(hm, hi_abs(o));
           Re[node * NCU + c] = o;
         }
+        bad_if_any(P, e, hm);
       }
       __syncthreads();
     }
@@ -1349,13 +1349,15 @@ complete_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restric
         if ((mask & 2) && i == N1 - 1) acc[k] += fval(1, k, c);
       }
     }
+    int hm = 0;
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
       const int node = ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k;
       const double out = rcol[c][k] + acc[k];
-      bad_if(P, e, out);
+      hm = max(hm, hi_abs(out));
       Re[node * NCU + c] = out;
     }
+    bad_if_any(P, e, hm);
   }
 }
 
@@ -1491,13 +1493,15 @@ complete_pipe_kernel(const __grid_constant__ TensorParams P, const FaceRec* __re
             if ((mask & 2) && i == N1 - 1) acc[k] += fval(1, k, c);
           }
         }
+        int hm = 0;
 #pragma unroll
         for (int k = 0; k < N1; ++k) {
           const int node = ND == 3 ? i + N1 * j + N1 * N1 * k : i + N1 * k;
           const double out = r_c[c][k] + acc[k];
-          bad_if(P, e, out);
+          hm = max(hm, hi_abs(out));
           Re[node * NCU + c] = out;
         }
+        bad_if_any(P, e, hm);
       }
     }
     __syncthreads();                                  // sv / sw2 reused next group
