@@ -172,7 +172,7 @@ def cpu_solve(n):
 def load_traffic():
     """DRAM bytes per launch of the two fused kernels from the committed ncu
     --set full capture (profiles/traffic.json, written by
-    tools_ncu_traffic.py from the same bench command): dram__bytes_read.sum +
+    scripts/ncu_traffic.py from the same bench command): dram__bytes_read.sum +
     dram__bytes_write.sum.  Absent file -> null."""
     try:
         return json.loads((ROOT / "profiles" / "traffic.json").read_text())

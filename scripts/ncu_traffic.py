@@ -1,7 +1,7 @@
 """Write profiles/traffic.json: DRAM bytes per launch of the fused pass-1 /
 pass-2 kernels from an ncu --set full report of the bench command.
 
-    python tools_ncu_traffic.py gpurun_out/prof_bench.ncu-rep [source-note]
+    python scripts/ncu_traffic.py gpurun_out/prof_bench.ncu-rep [source-note]
 """
 import csv
 import json
