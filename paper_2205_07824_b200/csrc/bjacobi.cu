@@ -90,12 +90,22 @@ __device__ bool gauss_jordan(double* A, int bs, int* perm, double thr,
     for (int k = threadIdx.x; k < bs; k += kInvThreads)
       A[c * bs + k] = (k == c) ? inv : A[c * bs + k] * inv;
     __syncthreads();
-    for (int t = threadIdx.x; t < bs * bs; t += kInvThreads) {
-      const int r = t / bs, k = t % bs;
-      if (r == c) continue;
-      const double f = A[r * bs + c];
-      if (k == c) continue;
-      A[r * bs + k] = fma(-f, A[c * bs + k], A[r * bs + k]);
+    if (kInvThreads % bs == 0) {
+      // fixed column per thread, rows strided: no integer division per entry
+      const int k = threadIdx.x % bs, rstep = kInvThreads / bs;
+      if (k != c) {
+        const double ack = A[c * bs + k];
+        for (int r = threadIdx.x / bs; r < bs; r += rstep)
+          if (r != c) A[r * bs + k] = fma(-A[r * bs + c], ack, A[r * bs + k]);
+      }
+    } else {
+      for (int t = threadIdx.x; t < bs * bs; t += kInvThreads) {
+        const int r = t / bs, k = t % bs;
+        if (r == c) continue;
+        const double f = A[r * bs + c];
+        if (k == c) continue;
+        A[r * bs + k] = fma(-f, A[c * bs + k], A[r * bs + k]);
+      }
     }
     __syncthreads();
     for (int r = threadIdx.x; r < bs; r += kInvThreads)
