@@ -19,6 +19,9 @@ namespace ldg {
 namespace {
 
 constexpr int kDBlock = 128;
+#ifndef LDG_TET3_TPE
+#define LDG_TET3_TPE 32       // threads per tet p=3 element (>= nb = 20)
+#endif
 
 __device__ __forceinline__ void dbad(const DenseParams& P, int e, double v) {
   if (!isfinite(v)) atomicMin(P.bad, (unsigned long long)e);
@@ -53,7 +56,7 @@ mixed_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
   __shared__ double sjump[EPB][NFACE][NQF][NCU];
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
   const int e = blockIdx.x * EPB + slot;
-  const bool active = e < P.ne;
+  const bool active = slot < EPB && e < P.ne;   // TPE need not divide the block
   int info[NFACE], nbr[NFACE];
   if (active) {
 #pragma unroll
@@ -167,7 +170,7 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
   __shared__ double sfh[EPB][NFACE][NQF][NCU];
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE;
   const int e = blockIdx.x * EPB + slot;
-  const bool active = e < P.ne;
+  const bool active = slot < EPB && e < P.ne;   // TPE need not divide the block
   int info[NFACE], nbr[NFACE];
   double detj = 1.0, ij[ND][ND];
   if (active) {
@@ -359,7 +362,7 @@ int launch_dense(const DenseParams& P, int what, const double* u, const double* 
     // tet p = 1..3 (nqf = (p + 1)^2)
     case 30410: return run_dense<4, 4, 4, 3, 1, 4>(P, what, u, gval, bsrc, q, R, s);
     case 31010: return run_dense<10, 9, 4, 3, 1, 16>(P, what, u, gval, bsrc, q, R, s);
-    case 32010: return run_dense<20, 16, 4, 3, 1, 32>(P, what, u, gval, bsrc, q, R, s);
+    case 32010: return run_dense<20, 16, 4, 3, 1, LDG_TET3_TPE>(P, what, u, gval, bsrc, q, R, s);
     default: return 2;
   }
 }
