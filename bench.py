@@ -476,7 +476,7 @@ def run_b200(args, rank, world):
                      "traffic_source": traffic.get("source"),
                      "algorithmic_bytes_per_dof": bytes_p1 / ndof, "ms": p1,
                      "peak_source": peak_src},
-        "pass2_roofline": {"kernel": "complete_warp_kernel (pass 2, shuffle face lift)", "achieved": ach_p2,
+        "pass2_roofline": {"kernel": "complete_warp4_kernel (pass 2, shuffle face lift)", "achieved": ach_p2,
                            "frac": ach_p2 / hbm, "algorithmic_bytes_per_dof": bytes_p2 / ndof,
                            "traffic": traffic.get("pass2"), "ms": p2},
         "matvec_roofline": {"achieved": ach_mv, "peak": hbm, "unit": "GB/s",

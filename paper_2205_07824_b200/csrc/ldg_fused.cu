@@ -1530,11 +1530,16 @@ complete_pipe_kernel(const __grid_constant__ TensorParams P, const FaceRec* __re
 #ifndef LDG_P2W_PIPE
 #define LDG_P2W_PIPE 1
 #endif
+#ifndef LDG_P2W_MAXN1
+#define LDG_P2W_MAXN1 4       // warp completion for hex p = 1..LDG_P2W_MAXN1-1
+#endif
 #ifndef LDG_P2W_GRID
 #define LDG_P2W_GRID LDG_P2W_MINB   // blocks per SM in the grid
 #endif
+// hex p = 3 (N1 = 4): the hand-specialised variant (no spills; the generic
+// template below spills 12 B at N1 = 4 and measured 44 vs 42 us)
 __global__ void __launch_bounds__(256, LDG_P2W_MINB)
-complete_warp_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+complete_warp4_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
                      const double* __restrict__ X, double* __restrict__ R) {
   constexpr int NB = 64, NF = 16;
   const int lane = threadIdx.x & 31, half = lane >> 4, t = lane & 15;
@@ -1616,6 +1621,109 @@ complete_warp_kernel(const __grid_constant__ TensorParams P, const FaceRec* __re
   }
 }
 
+// generic p = 1, 2 (and any N1 with N1^2 <= 32)
+template <int N1>
+__global__ void __launch_bounds__(256, LDG_P2W_MINB)
+complete_warp_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+                     const double* __restrict__ X, double* __restrict__ R) {
+  // EPW elements per warp, NF = N1^2 lanes each (p = 1..4); lanes past
+  // EPW * NF only take part in the shuffles
+  constexpr int NF = N1 * N1, NB = NF * N1, EPW = 32 / NF;
+  constexpr bool FULL = EPW * NF == 32;                      // every lane owns a face node
+  const int lane = threadIdx.x & 31, slot = lane / NF, t = lane - slot * NF;
+  const int i = t % N1, j = t / N1, hb = slot * NF;
+  const bool lane_ok = FULL || slot < EPW;
+  auto src = [](int l) { return FULL ? l : (l & 31); };
+  double Mi[N1], Mj[N1];
+#pragma unroll
+  for (int m = 0; m < N1; ++m) {
+    Mi[m] = P.m1[i * N1 + m];
+    Mj[m] = P.m1[j * N1 + m];
+  }
+  const double wgt = P.grad_centered ? -0.5 : -1.0;
+  const int nel = P.e1 - P.e0;
+  const int ngroups = (nel + EPW - 1) / EPW;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  // groups in reverse order: pass 1 finished with the last elements (L2-resident)
+  auto elem = [&](int w) { return P.e0 + (ngroups - 1 - w) * EPW + slot; };
+  // face lf's record is loaded by lane t = lf (NF >= 6) or t = lf - NF (second
+  // load, p = 1 where NF = 4): the completion bits are two ballots
+  auto load_info = [&](int w) {
+    const int e = elem(w);
+    const bool ok = lane_ok && w < ngroups && e < P.e1;
+    int2 v = make_int2(0, 0);
+    if (ok && t < 6) v.x = __ldg(reinterpret_cast<const int*>(frec + (size_t)e * 6 + t) + 3);
+    if (NF < 6 && ok && t + NF < 6)
+      v.y = __ldg(reinterpret_cast<const int*>(frec + (size_t)e * 6 + t + NF) + 3);
+    return v;
+  };
+  int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+#if LDG_P2W_PIPE
+  int2 info_next = load_info(w);
+#endif
+  for (; w < ngroups; w += nwarps) {
+    const int e = elem(w);
+    const bool active = lane_ok && e < P.e1;
+#if LDG_P2W_PIPE
+    const int2 info = info_next;                             // loaded one group ahead
+    info_next = load_info(w + nwarps);
+#else
+    const int2 info = load_info(w);
+#endif
+    double r[N1];
+#pragma unroll
+    for (int k = 0; k < N1; ++k) r[k] = active ? __ldg(R + (size_t)e * NB + t + NF * k) : 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, (info.x & LDG_FL_COMPLETE) != 0);
+    const unsigned bal2 = NF < 6 ? __ballot_sync(0xffffffffu, (info.y & LDG_FL_COMPLETE) != 0) : 0u;
+    constexpr unsigned LO = NF < 6 ? (1u << NF) - 1u : 63u;
+    auto face_mask = [&](int base) {
+      return ((bal >> base) & LO) | (NF < 6 ? ((bal2 >> base) & ((1u << (6 - (NF < 6 ? NF : 0))) - 1u)) << NF : 0u);
+    };
+    unsigned any = 0;                                        // faces completed in any element
+#pragma unroll
+    for (int s2 = 0; s2 < EPW; ++s2) any |= face_mask(s2 * NF);
+    const int mask = lane_ok ? (int)face_mask(hb) : 0;
+    double x[6];
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf)
+      x[lf] = (mask >> lf) & 1 ? __ldg(X + ((size_t)e * 6 + lf) * NF + t) : 0.0;
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf) {
+      if (!((any >> lf) & 1)) continue;                      // warp-uniform
+      const double v = wgt * x[lf];
+      // w(a', b) = sum_a M[a'][a] v(a, b) on lane (a', b); L(a', b') = sum_b M[b'][b] w(a', b)
+      double wv = 0.0;
+#pragma unroll
+      for (int a2 = 0; a2 < N1; ++a2) wv = fma(Mi[a2], __shfl_sync(0xffffffffu, v, src(hb + a2 + N1 * j)), wv);
+      double L = 0.0;
+#pragma unroll
+      for (int b2 = 0; b2 < N1; ++b2) L = fma(Mj[b2], __shfl_sync(0xffffffffu, wv, src(hb + i + N1 * b2)), L);
+      if (!((mask >> lf) & 1)) L = 0.0;
+      if (lf == 0) r[0] += L;                                // z-: node (i, j, 0)
+      else if (lf == 1) r[N1 - 1] += L;                      // z+: node (i, j, N1-1)
+      else {
+        // y faces: node (i, 0|N1-1, k) <- face node (i, k); x faces: (0|N1-1, j, k) <- (j, k)
+        const bool own = lf == 2 ? j == 0 : (lf == 3 ? j == N1 - 1 : (lf == 4 ? i == 0 : i == N1 - 1));
+        const int a0 = lf < 4 ? i : j;
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          const double g = __shfl_sync(0xffffffffu, L, src(hb + a0 + N1 * k));
+          if (own) r[k] += g;
+        }
+      }
+    }
+    if (active) {
+      int hm = 0;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        hm = max(hm, hi_abs(r[k]));
+        R[(size_t)e * NB + t + NF * k] = r[k];
+      }
+      bad_if_any(P, e, hm);
+    }
+  }
+}
+
 // --------------------------------------------------------------------------
 // dispatch
 // --------------------------------------------------------------------------
@@ -1670,11 +1778,15 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
     static const bool pipe = !getenv("LDG_P2_PLAIN");      // A/B timing of the one-shot kernel
     bool done = false;
     static const bool warp2 = !getenv("LDG_P2_BLOCKWISE");  // A/B timing
-    if constexpr (N1 == 4 && ND == 3 && NCU == 1) {
+    if constexpr (N1 >= 2 && N1 <= LDG_P2W_MAXN1 && ND == 3 && NCU == 1) {
       if (P.x_consumer && warp2) {
-        const int npairs = (nel + 1) / 2;
-        const int g = std::max(1, std::min((npairs + 7) / 8, nsm2 * LDG_P2W_GRID));
-        complete_warp_kernel<<<g, 256, 0, s>>>(P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
+        constexpr int EPW = 32 / (N1 * N1);
+        const int ngr = (nel + EPW - 1) / EPW;
+        const int g = std::max(1, std::min((ngr + 7) / 8, nsm2 * LDG_P2W_GRID));
+        if constexpr (N1 == 4)
+          complete_warp4_kernel<<<g, 256, 0, s>>>(P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
+        else
+          complete_warp_kernel<N1><<<g, 256, 0, s>>>(P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
         done = true;
       }
     }
