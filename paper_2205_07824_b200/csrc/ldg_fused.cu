@@ -731,6 +731,9 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     }
   }
   __syncthreads();
+  // let the completion kernel's blocks launch as SMs free up (they wait on
+  // griddepcontrol.wait before touching R / X)
+  asm volatile("griddepcontrol.launch_dependents;");
   double* sWarp = psm + warp * kPlaneWarp;                 // the warp's 8 element regions
   double* sEl = sWarp + plane_el(ls);
   double* sJZ = sEl + kOffJ;
@@ -1563,8 +1566,11 @@ complete_warp4_kernel(const __grid_constant__ TensorParams P, const FaceRec* __r
   };
   int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
 #if LDG_P2W_PIPE
-  int info_next = load_info(w);
+  int info_next = load_info(w);                 // face records are static tables
 #endif
+  // programmatic dependent launch: everything above overlaps the tail of
+  // pass 1; R and the exports are read only after pass 1 has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (; w < npairs; w += nwarps) {
     const int e = elem(w);
     const bool active = e < P.e1;
@@ -1783,8 +1789,21 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
         constexpr int EPW = 32 / (N1 * N1);
         const int ngr = (nel + EPW - 1) / EPW;
         const int g = std::max(1, std::min((ngr + 7) / 8, nsm2 * LDG_P2W_GRID));
-        if constexpr (N1 == 4)
-          complete_warp4_kernel<<<g, 256, 0, s>>>(P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
+        if constexpr (N1 == 4) {
+          static const bool pdl = !getenv("LDG_NO_PDL");
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(g);
+          cfg.blockDim = dim3(256);
+          cfg.dynamicSmemBytes = 0;
+          cfg.stream = s;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          attr[0].val.programmaticStreamSerializationAllowed = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = pdl ? 1 : 0;
+          cudaLaunchKernelEx(&cfg, complete_warp4_kernel, P, reinterpret_cast<const FaceRec*>(P.frec),
+                             (const double*)X, R);
+        }
         else
           complete_warp_kernel<N1><<<g, 256, 0, s>>>(P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
         done = true;
