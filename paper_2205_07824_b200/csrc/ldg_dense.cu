@@ -18,7 +18,10 @@
 namespace ldg {
 namespace {
 
-constexpr int kDBlock = 128;
+#ifndef LDG_DENSE_BLOCK
+#define LDG_DENSE_BLOCK 128
+#endif
+constexpr int kDBlock = LDG_DENSE_BLOCK;
 #ifndef LDG_TET3_TPE
 #define LDG_TET3_TPE 24       // threads per tet p=3 element (>= nb = 20); measured 20: 3.57, 24: 3.27, 32: 3.40 ms
 #endif
