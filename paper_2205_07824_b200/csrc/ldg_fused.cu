@@ -1534,7 +1534,7 @@ complete_pipe_kernel(const __grid_constant__ TensorParams P, const FaceRec* __re
 #define LDG_P2W_PIPE 1
 #endif
 #ifndef LDG_P2W_MAXN1
-#define LDG_P2W_MAXN1 4       // warp completion for hex p = 1..LDG_P2W_MAXN1-1
+#define LDG_P2W_MAXN1 5       // warp completion for hex p = 1..LDG_P2W_MAXN1-1 (N1^2 <= 32)
 #endif
 #ifndef LDG_P2W_GRID
 #define LDG_P2W_GRID LDG_P2W_MINB   // blocks per SM in the grid
