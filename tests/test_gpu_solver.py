@@ -165,12 +165,16 @@ def test_dirk_transient_matches_reference(name):
             assert rel(getattr(st, k).cpu().numpy(), g[k]) < 1e-9
 
 
-def test_transient_block_jacobi_apply_matches_reference_ns3d():
+@pytest.mark.parametrize("library_lu", [False, True])
+def test_transient_block_jacobi_apply_matches_reference_ns3d(library_lu, monkeypatch):
     """Block-Jacobi of the steady closures at the initial Taylor-Green state
     (driver.py:270-274, solver.py:303-346): 8 periodic hex p=2 elements, 5
     components, 135 x 135 blocks, applied to a seeded vector vs the
-    reference's own build + lu_solve."""
+    reference's own build + lu_solve.  library_lu: the batched-LU path of
+    blocks beyond the shared-memory Gauss-Jordan (bs > 160, NS hex p=3)."""
     import torch
+    if library_lu:
+        monkeypatch.setenv("LDG_BJ_LIBRARY_LU", "1")
     from cases import TRANSIENT_CASES
     from paper_2205_07824_b200.driver import _steady_fns, build_pde_block_jacobi
     from paper_2205_07824_b200.system import LdgSystem
