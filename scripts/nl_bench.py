@@ -124,7 +124,18 @@ def run_transient(spec, steps, dt, precond="mass", flags=None):
                          gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent",
                          orth=f.get("orth", "cgs2"))
     tab = dirk_tableau(spec["stages"], spec["order"])
-    M = MassPreconditioner(s)
+    build_s = 0.0
+    if precond == "block_jacobi":
+        # the reference's transient block-Jacobi: built once from the steady
+        # closures at the initial state (driver.py:270-274)
+        from paper_2205_07824_b200.driver import _steady_fns, build_pde_block_jacobi
+        t0 = time.perf_counter()
+        rf, tf = _steady_fns(s)
+        M = build_pde_block_jacobi(s, rf, tf, torch.as_tensor(st.u, device=s.device).reshape(-1))
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
+    else:
+        M = MassPreconditioner(s)
     from paper_2205_07824_b200.driver import TimeIntError
     try:
         st, _ = advance_step(s, st, dt, tab, opts, precond=M)   # warm-up (JIT, caches)
@@ -141,6 +152,7 @@ def run_transient(spec, steps, dt, precond="mass", flags=None):
     per = (time.perf_counter() - t0) / steps
     return {"dofs": s.n_dofs, "dt": dt, "steps": steps, "s_per_step": per,
             "newton_per_step": newton, "gmres_per_step": gm, "precond": precond,
+            "precond_build_s": build_s,
             "max_abs_u": float(torch.max(torch.abs(st.u)).item())}
 
 
