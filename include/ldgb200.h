@@ -219,6 +219,11 @@ int ldg_combine(int64_t n, int k, const double* Z, int64_t ldz, const double* y,
  * faces (elem_l, elem_r) (solver.py:355-378, driver.py:109-142) */
 int ldg_color_distance2(int64_t ne, int64_t nfaces, const int32_t* elem_l,
                         const int32_t* elem_r, int32_t* colors);
+/* all bs probes of one colour through the handle's linear tangent: for each
+ * k, v = unit probe k, col = J v, extract into mats (solver.py:327-334) */
+int ldg_bj_probe_colour(LdgHandle* h, int64_t nblk, int bs, const int32_t* members,
+                        int64_t nm, double* v, double* col, double* scratch, double* mats,
+                        void* stream);
 int ldg_bj_probe_vector(int64_t nblk, int bs, const int32_t* members,
                         int64_t n_members, int k, double* v, void* stream);
 int ldg_bj_extract(int bs, const int32_t* members, int64_t n_members, int k,

@@ -104,6 +104,8 @@ _SIGS = {
     "ldg_dcgs_update": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                          C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ldg_bj_probe_colour": ([C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
+                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_bj_probe_vector": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p,
                              C.c_void_p], C.c_int),
     "ldg_bj_extract": ([C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,

@@ -421,6 +421,24 @@ int ldg_residual_tangent(LdgHandle* h, const double* du, double* scratch,
   return rc ? fail(rc, "residual_tangent launch", cudaGetLastError()) : 0;
 }
 
+// Block-Jacobi probes of one colour without a host round trip per direction
+// (solver.py:327-334): for k < bs, v = unit probe k on the colour's members,
+// col = J v (the handle's linear tangent), mats[:, :, k] <- col on the blocks.
+int ldg_bj_probe_colour(LdgHandle* h, int64_t nblk, int bs, const int32_t* members,
+                        int64_t nm, double* v, double* col, double* scratch, double* mats,
+                        void* stream) {
+  if (!h || !v || !col || !scratch || !mats || bs < 1) return fail(2, "bad argument");
+  for (int k = 0; k < bs; ++k) {
+    int rc = ldg_bj_probe_vector(nblk, bs, members, nm, k, v, stream);
+    if (rc) return fail(rc, "probe vector", cudaGetLastError());
+    rc = ldg_residual_tangent(h, v, scratch, col, stream);
+    if (rc) return rc;
+    rc = ldg_bj_extract(bs, members, nm, k, col, mats, stream);
+    if (rc) return fail(rc, "extract", cudaGetLastError());
+  }
+  return 0;
+}
+
 int ldg_operator_pass(LdgHandle* h, int pass, int tangent, const double* u,
                       const double* gproj, const double* bsrc, double* scratch,
                       double* R, void* stream) {

@@ -67,8 +67,13 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
                           "B200 path; use the mass preconditioner")
     if colors is None:
         colors = distance2_coloring_topology(system.topology, system.n_elements)
+    from .system import LdgSystem
+    native = None
+    if (type(system) is LdgSystem and system.nl is None
+            and getattr(system, "_h", None) is not None):
+        native = (system._h, system.scratch())        # the linear tangent ignores the base
     return build_block_jacobi(tangent_fn, state_vec, system.n_elements,
-                              system.n_nodes * system.ncu, colors)
+                              system.n_nodes * system.ncu, colors, native=native)
 
 
 class CompositeManager:

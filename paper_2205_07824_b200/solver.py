@@ -651,7 +651,7 @@ def element_neighbor_sets(topology, n_elements):
     return nb
 
 
-def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors):
+def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None):
     """Exact diagonal blocks by coloured unit probes through the tangent
     (solver.py:303-346): colours x bs device matvecs, then batched
     Gauss-Jordan inverses with the reference's 1e-12 shift rule."""
@@ -665,6 +665,14 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors):
     st = _lib.stream_ptr()
     for c in np.unique(colors):
         members = torch.as_tensor(np.nonzero(colors == c)[0].astype(np.int32), device=dev)
+        if native is not None:
+            # linear fused / dense operator: the colour's bs probes in one C call
+            h, scratch = native
+            col = torch.empty_like(v)
+            _lib.check(lib.ldg_bj_probe_colour(h, n_blocks, bs, _lib.ptr(members), members.numel(),
+                                               _lib.ptr(v), _lib.ptr(col), _lib.ptr(scratch),
+                                               _lib.ptr(mats), st), "ldg_bj_probe_colour")
+            continue
         for k in range(bs):
             _lib.check(lib.ldg_bj_probe_vector(n_blocks, bs, _lib.ptr(members), members.numel(),
                                                k, _lib.ptr(v), st), "probe")
