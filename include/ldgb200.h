@@ -234,6 +234,13 @@ int ldg_bj_invert(int64_t nblk, int bs, const double* mats, double* inv_t,
                   int32_t* shifted, void* stream);
 int ldg_bj_apply(int64_t nblk, int bs, const double* inv_t, const double* r,
                  double* z, void* stream);
+/* element blocks across a packed (u | q | w) vector (driver.py:128-142,
+ * _elementwise_blocks): idx[e*bs + j] = packed index of row j of block e;
+ * gather dst[i] = src[idx[i]], scatter dst[idx[i]] = src[i] */
+int ldg_permute_gather(int64_t n, const int64_t* idx, const double* src, double* dst,
+                       void* stream);
+int ldg_permute_scatter(int64_t n, const int64_t* idx, const double* src, double* dst,
+                        void* stream);
 
 /* ---- generated model kernels (nonlinear / kind-C path, csrc/jit.cu) ----
  * The pointwise flux / source / wavespeed / mass plans of a model

@@ -114,6 +114,10 @@ _SIGS = {
                       C.c_int),
     "ldg_bj_apply": ([C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
                      C.c_int),
+    "ldg_permute_gather": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+                           C.c_int),
+    "ldg_permute_scatter": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+                            C.c_int),
     "ldg_jit_last_error": ([], C.c_char_p),
     "ldg_jit_compile": ([C.c_char_p, C.c_char_p, C.c_void_p, C.c_int, C.c_void_p,
                          C.POINTER(C.c_int64)], C.c_int),

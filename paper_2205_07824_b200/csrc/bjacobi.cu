@@ -193,7 +193,28 @@ bj_apply_big_kernel(int bs, const double* __restrict__ inv_t,
   }
 }
 
+// packed (u | q | w) <-> element-major block order (driver.py:128-142):
+// dst[i] = src[idx[i]] and dst[idx[i]] = src[i]
+__global__ void gather_kernel(int64_t n, const int64_t* __restrict__ idx,
+                              const double* __restrict__ src, double* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+__global__ void scatter_kernel(int64_t n, const int64_t* __restrict__ idx,
+                               const double* __restrict__ src, double* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[idx[i]] = src[i];
+}
+
 inline int rc() { return cudaGetLastError() == cudaSuccess ? 0 : 3; }
+
+inline unsigned grid_for(int64_t n) {
+  const int64_t g = (n + 255) / 256;
+  return (unsigned)(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
+}
 
 }  // namespace
 
@@ -225,6 +246,22 @@ int ldg_bj_invert(int64_t nblk, int bs, const double* mats, double* inv_t,
   if (nblk > 0)
     invert_kernel<<<(unsigned)nblk, kInvThreads, sm, (cudaStream_t)stream>>>(bs, mats, inv_t,
                                                                              shifted);
+  return rc();
+}
+
+int ldg_permute_gather(int64_t n, const int64_t* idx, const double* src, double* dst,
+                       void* stream) {
+  if (n <= 0) return 0;
+  if (!idx || !src || !dst) return 2;
+  gather_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
+  return rc();
+}
+
+int ldg_permute_scatter(int64_t n, const int64_t* idx, const double* src, double* dst,
+                        void* stream) {
+  if (n <= 0) return 0;
+  if (!idx || !src || !dst) return 2;
+  scatter_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
   return rc();
 }
 

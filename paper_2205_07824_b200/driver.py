@@ -40,6 +40,7 @@ def _steady_fns(system):
     def tangent(uflat, v):
         return system.tangent_dev(v.reshape(shape), base=uflat.reshape(shape)).reshape(-1)
 
+    tangent.steady_tangent_of = system     # lets the block-Jacobi build probe natively
     return residual, tangent
 
 
@@ -56,24 +57,47 @@ class MassPreconditioner:
         return s.mass_inv_dev(r.reshape(s.n_elements, s.n_nodes, s.ncu)).reshape(-1)
 
 
+def elementwise_block_perm(system, device):
+    """Per-element dof indices across the packed (u, q, w) blocks
+    (driver.py:128-142, ``_elementwise_blocks``) as one int64 device vector:
+    perm[e*bs + j] = packed index of row j of element e's block."""
+    import torch
+    ne, nb = system.n_elements, system.n_nodes
+    sizes = [nb * system.ncu]
+    if system.kind == "W":
+        sizes.append(nb * system.ncu * system.nd)
+    if getattr(system, "nw", 0) > 0:
+        sizes.append(nb * system.nw)
+    offsets = np.cumsum([0] + [ne * s for s in sizes])
+    e = np.arange(ne, dtype=np.int64)[:, None]
+    cols = [off + e * s + np.arange(s, dtype=np.int64)[None, :]
+            for off, s in zip(offsets[:-1], sizes)]
+    return torch.as_tensor(np.concatenate(cols, axis=1).reshape(-1), device=device), sum(sizes)
+
+
 def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="tangent",
                            colors=None):
     """Exact per-element diagonal blocks via distance-2 coloured probing
-    (driver.py:119-125)."""
-    if jv_mode != "tangent":
-        raise DriverError("the B200 block-Jacobi build probes the tangent operator")
-    if getattr(system, "multi_block", False):
-        raise DriverError("block-Jacobi on packed (u, q, w) systems is not supported on the "
-                          "B200 path; use the mass preconditioner")
+    (driver.py:119-142), through the tangent or by finite differences
+    (``jv_mode``), across the packed blocks of kind-W / ODE systems."""
     if colors is None:
         colors = distance2_coloring_topology(system.topology, system.n_elements)
     from .system import LdgSystem
+    import torch
+    x = state_vec if isinstance(state_vec, torch.Tensor) else \
+        torch.as_tensor(np.asarray(state_vec, dtype=np.float64), device=system.device)
+    if getattr(system, "multi_block", False):
+        perm, bs = elementwise_block_perm(system, x.device)
+        return build_block_jacobi(tangent_fn, x, system.n_elements, bs, colors, perm=perm,
+                                  mode=jv_mode, residual_fn=residual_fn)
     native = None
-    if (type(system) is LdgSystem and system.nl is None
-            and getattr(system, "_h", None) is not None):
+    if (jv_mode == "tangent" and type(system) is LdgSystem and system.nl is None
+            and getattr(system, "_h", None) is not None
+            and getattr(tangent_fn, "steady_tangent_of", None) is system):
         native = (system._h, system.scratch())        # the linear tangent ignores the base
-    return build_block_jacobi(tangent_fn, state_vec, system.n_elements,
-                              system.n_nodes * system.ncu, colors, native=native)
+    return build_block_jacobi(tangent_fn, x, system.n_elements,
+                              system.n_nodes * system.ncu, colors, native=native,
+                              mode=jv_mode, residual_fn=residual_fn)
 
 
 class CompositeManager:

@@ -194,6 +194,20 @@ class DistVecOps:
         self.nrm2(x, out)
         return float(out.item())
 
+    def amax(self, x):
+        """Global max |x_i| (fd_epsilon's ||base||_inf, solver.py:187)."""
+        import torch
+        import torch.distributed as dist
+        m = x.abs().max().reshape(1) if x.numel() else x.new_zeros(1)
+        m = torch.where(torch.isnan(m), torch.full_like(m, float("inf")), m)
+        if m.is_cuda and dist.get_backend(self.group) == "gloo":
+            h = m.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX, group=self.group)
+            m.copy_(h)
+        else:
+            dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
+        return float(m.item())
+
     def axpy(self, *a, **k):
         return self.b.axpy(*a, **k)
 

@@ -121,6 +121,10 @@ class VecOps:
         self.nrm2(x, self.s[0:1])
         return float(self.s[0].item())
 
+    def amax(self, x):
+        """max |x_i| (host float); NaN propagates."""
+        return float(x.abs().max().item()) if x.numel() else 0.0
+
     def axpy(self, a, x, y, a_dev=None, sign=1.0):
         _lib.check(self.lib.ldg_axpy(x.numel(), float(a), _lib.ptr(a_dev), float(sign),
                                      _lib.ptr(x), _lib.ptr(y), self._st()), "ldg_axpy")
@@ -201,6 +205,8 @@ class _Workspace:
             self.H = torch.zeros((m + 1, m + 2), dtype=torch.float64, device=device)  # row k = column k of H
             self.c = torch.zeros(m + 2, dtype=torch.float64, device=device)
             self.nrm = torch.zeros(4, dtype=torch.float64, device=device)
+            # DCGS2 dot / coefficient vectors (k+1 <= m+1 entries each)
+            self.dv = torch.zeros((4, m + 2), dtype=torch.float64, device=device)
             self.key = (m, n, str(device))
         if need_z and self.Z is None:           # DCGS2 keeps no Z (x += M^-1 (V y))
             self.Z = torch.empty((m, n), dtype=torch.float64, device=device)
@@ -402,6 +408,10 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
     import torch
     n = b.numel()
     dev = b.device
+
+    def apply_op_into(dst, v):
+        dst.copy_(apply_op(M.apply(v)).reshape(-1))
+
     res_norms, total, breakdown = [], 0, False
     while total < max_iter:
         if total > 0 or have_x0:
@@ -415,16 +425,17 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
         m = min(restart, max_iter - total)
         ws = _WS.get(m, n, dev, need_z=False)
         V, w, nr = ws.V, ws.w, ws.nrm
-        dx, dy, sd, td = ws.H[0], ws.H[1], ws.H[2], ws.c
+        dx, dy, sd, td = ws.dv[0], ws.dv[1], ws.dv[2], ws.dv[3]
+        thr = 1e-14 * max(bnorm, 1.0)
         Hr = np.zeros((m + 1, m))
         R = np.zeros((m + 1, m))
         cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
         g[0] = beta
         torch.div(r, beta, out=V[0])
-        ncol, converged = 0, False
+        ncol, lucky = 0, False
         for k in range(m + 1):
-            if k < m:
-                w.copy_(apply_op(M.apply(V[k])))
+            if k < m and not lucky:
+                apply_op_into(w, V[k])
                 ops.dcgs_dots(V, k + 1, V[k], w, dx, dy)
             else:                                   # finalise the last column only
                 ops.dcgs_dots(V, k + 1, V[k], V[k], dx, dy)
@@ -435,18 +446,17 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
                 s = np.zeros(0)
                 alpha, nu = 1.0, 1.0
             else:
-                s, vv, nu = hv[:k], hv[k], hv[2 * k + 2]
-                alpha = float(np.sqrt(max(vv - float(s @ s), 0.0)))
+                s, vv = hv[:k], hv[k]
+                alpha = 0.0 if lucky else float(np.sqrt(max(vv - float(s @ s), 0.0)))
                 Hr[:k, k - 1] += nu * s
                 Hr[k, k - 1] = nu * alpha
-                if Hr[k, k - 1] <= 1e-14 * max(bnorm, 1.0):
+                if Hr[k, k - 1] <= thr:
                     breakdown = True
                 ncol = k
                 total += 1
                 res = _givens_column(R, Hr, k - 1, cs, sn, g)
                 res_norms.append(float(res))
                 if res <= tol or breakdown or k == m:
-                    converged = res <= tol
                     break
             t, vw = hv[k + 1: 2 * k + 1], hv[2 * k + 1]
             Hs = Hr[: k + 1, :k] @ s
@@ -457,7 +467,15 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
                 sd[:k].copy_(torch.as_tensor(s, device=dev))
                 td[:k].copy_(torch.as_tensor(t, device=dev))
             ops.dcgs_update(V, k, sd, td, V[k], w, V[k + 1], 1.0 / alpha, gamma, nr[0:1])
-            ops.div(V[k + 1], nr[0:1], V[k + 1])
+            # exact (lucky) breakdown: the projected vector vanished, so the
+            # next column is final without normalising it (0/0) or applying
+            # the operator to it (solver.py:142)
+            nu = float(nr[0].item())
+            if not np.isfinite(nu):
+                raise SolverError("gmres: operator returned non-finite values")
+            lucky = nu <= thr
+            if not lucky:
+                ops.div(V[k + 1], nr[0:1], V[k + 1])
         if ncol:
             y = scipy.linalg.solve_triangular(R[:ncol, :ncol], g[:ncol])
             u = w
@@ -470,7 +488,6 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
             r = b - apply_op(x)
             ok = ops.norm(r) <= tol
             return GmresResult(out(x), ok, total, res_norms, True)
-        del converged
     return GmresResult(out(x), False, total, res_norms, breakdown)
 
 
@@ -479,36 +496,48 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
 # ---------------------------------------------------------------------------
 
 
-def fd_epsilon(base, v):
-    """solver.py:182-190."""
+def fd_epsilon(base, v, ops=None):
+    """eps = sqrt(eps_mach) (1 + ||base||_inf) / ||v||_2 (solver.py:182-190).
+    With a distributed ``ops`` (parallel.DistVecOps) both norms are global
+    (allreduced sum of squares and max), so every rank perturbs by the same
+    eps."""
     import torch
-    vnorm = float(torch.linalg.vector_norm(v)) if isinstance(v, torch.Tensor) else \
-        float(np.linalg.norm(v))
+    if ops is not None and isinstance(v, torch.Tensor):
+        vnorm = ops.norm(v)
+        bmax = ops.amax(base)
+    else:
+        vnorm = float(torch.linalg.vector_norm(v)) if isinstance(v, torch.Tensor) else \
+            float(np.linalg.norm(v))
+        bmax = float(base.abs().max()) if isinstance(base, torch.Tensor) else \
+            float(np.abs(base).max())
     if vnorm == 0.0:
         raise SolverError("jacobian_vector: zero direction")
-    bmax = float(base.abs().max()) if isinstance(base, torch.Tensor) else \
-        float(np.abs(base).max())
     eps = np.sqrt(np.finfo(float).eps) * (1.0 + bmax) / vnorm
     if eps == 0.0 or not np.isfinite(eps):
         raise SolverError("jacobian_vector: step underflow")
     return float(eps)
 
 
-def jacobian_vector(residual_fn, base, v, mode="fd", base_residual=None, tangent_fn=None):
-    """solver.py:193-212."""
+def jacobian_vector(residual_fn, base, v, mode="fd", base_residual=None, tangent_fn=None,
+                    ops=None):
+    """solver.py:193-212.  ``ops`` (optional) makes the FD step size and the
+    non-finite check global across ranks."""
     if mode == "tangent":
         if tangent_fn is None:
             raise SolverError("tangent mode requires tangent_fn")
         return tangent_fn(base, v)
     if mode != "fd":
         raise SolverError(f"unknown jacobian mode {mode!r}")
-    eps = fd_epsilon(base, v)
+    eps = fd_epsilon(base, v, ops)
     r0 = residual_fn(base) if base_residual is None else base_residual
     r1 = residual_fn(base + eps * v)
     out = (r1 - r0) / eps
     import torch
-    fin = bool(torch.isfinite(out).all()) if isinstance(out, torch.Tensor) else \
-        bool(np.isfinite(out).all())
+    if isinstance(out, torch.Tensor):
+        bad = torch.logical_not(torch.isfinite(out).all()).to(torch.float64).reshape(1)
+        fin = (ops.amax(bad) if ops is not None else float(bad.item())) == 0.0
+    else:
+        fin = bool(np.isfinite(out).all())
     if not fin:
         raise SolverError("jacobian_vector: non-finite result")
     return out
@@ -540,8 +569,8 @@ def newton_solve(residual_fn, x0, options=None, precond=None, tangent_fn=None,
         M = precond.build(x) if hasattr(precond, "build") else precond
         xb, Rb = x, R
         op = LinearOperator(apply=lambda v: jacobian_vector(
-            residual_fn, xb, v, opts.jv_mode, base_residual=Rb, tangent_fn=tangent_fn),
-            n=x.numel())
+            residual_fn, xb, v, opts.jv_mode, base_residual=Rb, tangent_fn=tangent_fn,
+            ops=ops), n=x.numel())
         eta = opts.forcing if opts.forcing is not None else min(0.1, np.sqrt(rnorm))
         eta = min(max(eta, 1e-14), 0.9)
         lin = gmres(op, -R, precond=M, rel_tol=eta, restart=opts.gmres_restart,
@@ -584,20 +613,34 @@ def newton_solve(residual_fn, x0, options=None, precond=None, tangent_fn=None,
 
 class BlockJacobiPreconditioner:
     """z_b = A_b^-1 r_b per element block (solver.py:291-300); the inverses
-    are stored transposed on the device."""
+    are stored transposed on the device.  ``perm`` (packed kind-W / ODE
+    systems): perm[e*bs + j] = packed index of row j of element e's block
+    (driver.py:128-142), gathered / scattered by native kernels."""
 
-    def __init__(self, inv_t, bs, shifted=None):
+    def __init__(self, inv_t, bs, shifted=None, perm=None):
         self.inv_t, self.bs = inv_t, bs
         self.nblk = inv_t.shape[0]
         self.shifted = shifted
+        self.perm = perm
         self.lib = _lib.load()
 
     def apply(self, r):
         import torch
         rd, dev = _as_device(r)
         z = torch.empty_like(rd)
-        _lib.check(self.lib.ldg_bj_apply(self.nblk, self.bs, _lib.ptr(self.inv_t), _lib.ptr(rd),
-                                         _lib.ptr(z), _lib.stream_ptr()), "ldg_bj_apply")
+        st = _lib.stream_ptr()
+        if self.perm is None:
+            _lib.check(self.lib.ldg_bj_apply(self.nblk, self.bs, _lib.ptr(self.inv_t),
+                                             _lib.ptr(rd), _lib.ptr(z), st), "ldg_bj_apply")
+        else:
+            re, ze = torch.empty_like(rd), torch.empty_like(rd)
+            n = rd.numel()
+            _lib.check(self.lib.ldg_permute_gather(n, _lib.ptr(self.perm), _lib.ptr(rd),
+                                                   _lib.ptr(re), st), "ldg_permute_gather")
+            _lib.check(self.lib.ldg_bj_apply(self.nblk, self.bs, _lib.ptr(self.inv_t),
+                                             _lib.ptr(re), _lib.ptr(ze), st), "ldg_bj_apply")
+            _lib.check(self.lib.ldg_permute_scatter(n, _lib.ptr(self.perm), _lib.ptr(ze),
+                                                    _lib.ptr(z), st), "ldg_permute_scatter")
         return z if dev else z.cpu().numpy()
 
 
@@ -651,10 +694,15 @@ def element_neighbor_sets(topology, n_elements):
     return nb
 
 
-def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None):
-    """Exact diagonal blocks by coloured unit probes through the tangent
-    (solver.py:303-346): colours x bs device matvecs, then batched
-    Gauss-Jordan inverses with the reference's 1e-12 shift rule."""
+def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, perm=None,
+                       mode="tangent", residual_fn=None, base_residual=None):
+    """Exact diagonal blocks by coloured unit probes (solver.py:303-346):
+    colours x bs device Jacobian-vector products (``mode`` "tangent" through
+    ``tangent_fn``, "fd" through ``residual_fn`` like jacobian_vector), then
+    batched Gauss-Jordan inverses with the reference's 1e-12 shift rule.
+    ``native`` = (handle, scratch) runs a colour's probes in one C call
+    (only for the handle's own linear tangent); ``perm`` maps element-major
+    block rows to packed indices (kind W / ODE systems)."""
     import torch
     lib = _lib.load()
     x, _ = _as_device(state)
@@ -663,9 +711,24 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None):
     mats = torch.zeros((n_blocks, bs, bs), dtype=torch.float64, device=dev)
     v = torch.empty(n_blocks * bs, dtype=torch.float64, device=dev)
     st = _lib.stream_ptr()
+    if mode == "fd":
+        if residual_fn is None:
+            raise SolverError("fd block-Jacobi probing needs residual_fn")
+        R0 = residual_fn(x) if base_residual is None else base_residual
+    elif mode != "tangent":
+        raise SolverError(f"unknown jacobian mode {mode!r}")
+    if perm is not None:
+        vp = torch.empty_like(v)
+        ce = torch.empty_like(v)
+
+    def probe(vec):
+        if mode == "tangent":
+            return tangent_fn(x, vec)
+        return jacobian_vector(residual_fn, x, vec, "fd", base_residual=R0)
+
     for c in np.unique(colors):
         members = torch.as_tensor(np.nonzero(colors == c)[0].astype(np.int32), device=dev)
-        if native is not None:
+        if native is not None and perm is None and mode == "tangent":
             # linear fused / dense operator: the colour's bs probes in one C call
             h, scratch = native
             col = torch.empty_like(v)
@@ -676,7 +739,15 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None):
         for k in range(bs):
             _lib.check(lib.ldg_bj_probe_vector(n_blocks, bs, _lib.ptr(members), members.numel(),
                                                k, _lib.ptr(v), st), "probe")
-            col = tangent_fn(x, v)
+            if perm is None:
+                col = probe(v)
+            else:
+                _lib.check(lib.ldg_permute_scatter(v.numel(), _lib.ptr(perm), _lib.ptr(v),
+                                                   _lib.ptr(vp), st), "ldg_permute_scatter")
+                colp = probe(vp).reshape(-1).contiguous()
+                _lib.check(lib.ldg_permute_gather(v.numel(), _lib.ptr(perm), _lib.ptr(colp),
+                                                  _lib.ptr(ce), st), "ldg_permute_gather")
+                col = ce
             _lib.check(lib.ldg_bj_extract(bs, _lib.ptr(members), members.numel(), k,
                                           _lib.ptr(col), _lib.ptr(mats), st), "extract")
     if bs > BJ_SMEM_MAX_BS or os.environ.get("LDG_BJ_LIBRARY_LU"):
@@ -687,7 +758,7 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None):
         _lib.check(lib.ldg_bj_invert(n_blocks, bs, _lib.ptr(mats), _lib.ptr(inv_t),
                                      _lib.ptr(shifted), st), "ldg_bj_invert")
     del mats
-    return BlockJacobiPreconditioner(inv_t, bs, shifted)
+    return BlockJacobiPreconditioner(inv_t, bs, shifted, perm=perm)
 
 
 BJ_SMEM_MAX_BS = 160            # ldg_bj_invert's in-shared-memory limit (bjacobi.cu)

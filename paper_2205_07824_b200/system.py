@@ -347,6 +347,18 @@ class LdgSystem:
     def _stream(self):
         return _lib.stream_ptr()
 
+    def _clear_nan(self, *xs):
+        """Discard a stale device non-finite flag before a host-API call that
+        checks it (a device-path call, e.g. a rejected line-search trial, may
+        have left it set)."""
+        import torch
+        if any(isinstance(x, torch.Tensor) and x.is_cuda for x in xs):
+            return
+        if self.nl is not None:
+            self.nl.reset_bad()
+        elif getattr(self, "_h", None) is not None:
+            self.lib.ldg_last_bad_element(self._h)
+
     def _check_nan(self, label):
         if self.nl is not None:
             bad = self.nl.bad_element()
@@ -553,6 +565,7 @@ class LdgSystem:
         """disc.py:436-449."""
         if self.kind != "D":
             raise DiscError("compute_mixed applies to diffusion models")
+        self._clear_nan(u)
         ud, dev = self._dev(u)
         q = self.mixed_dev(ud.reshape(self.n_elements, self.n_nodes, self.ncu), t, homogeneous)
         if dev != "cuda":
@@ -567,6 +580,7 @@ class LdgSystem:
     def _packed_host(self, fn, state, *vecs):
         """Run a packed device operator on reference-shaped blocks; returns
         the (u, q, w) blocks like the reference."""
+        self._clear_nan(state.u)
         blocks = [self._dev(b)[0] if b is not None else None for b in
                   (state.u, state.q, state.w)]
         dev = self._dev(state.u)[1]
@@ -583,6 +597,7 @@ class LdgSystem:
 
     def residual(self, state):
         """disc.py:588-589 -> (Ru, Rq, Rw)."""
+        self._clear_nan(state.u)
         if self.nl is not None and self.multi_block:
             return self._packed_host(lambda Y: self.residual_packed_dev(Y, state.t), state)
         if self._pipelined(state.u):
@@ -597,6 +612,7 @@ class LdgSystem:
 
     def residual_tangent(self, state, du, dq=None, dw=None):
         """disc.py:591-593 (the reference linearisation)."""
+        self._clear_nan(du)
         if self.nl is not None and self.multi_block:
             return self._packed_host(lambda V, Y: self.tangent_packed_dev(V, Y, state.t),
                                      state, (du, dq, dw))
@@ -616,6 +632,7 @@ class LdgSystem:
 
     def mass_apply(self, state, vu, vq=None, vw=None):
         """disc.py:897-925."""
+        self._clear_nan(vu)
         if self.nl is not None and self.multi_block:
             return self._packed_host(lambda V, Y: self.mass_packed_dev(V, Y, state.t),
                                      state, (vu, vq, vw))

@@ -30,17 +30,25 @@ needs_ref = pytest.mark.skipif(not reference_available(),
 
 @needs_ref
 @pytest.mark.parametrize("kind,p", [(k, p) for k in ("line", "tri", "quad", "tet", "hex")
-                                    for p in (1, 2, 3, 5)])
+                                    for p in range(1, 9)])
 def test_master_bitexact_vs_reference(kind, p):
     sys.path.insert(0, REFERENCE_SRC)
     from ldgkit import master as RM
     from paper_2205_07824_b200 import refelem
-    a, b = RM.build_master(kind, p), refelem.build_master(kind, p)
-    for nm in ("nodes", "quad_pts", "quad_wts", "phi", "dphi", "vandermonde_inv"):
-        assert np.array_equal(getattr(a, nm), getattr(b, nm)), nm
-    for fa, fb in zip(a.faces, b.faces):
-        assert np.array_equal(fa.phi, fb.phi)
-        assert np.array_equal(fa.xi, fb.xi)
+    pairs = [(RM.build_master(kind, p), refelem.build_master(kind, p))]
+    if p <= 3:
+        pairs.append((RM.build_geom_master(kind, p), refelem.build_geom_master(kind, p)))
+    for a, b in pairs:
+        for nm in ("nodes", "quad_pts", "quad_wts", "phi", "dphi", "vandermonde",
+                   "vandermonde_inv", "nodes1d", "phi1d", "dphi1d"):
+            x, y = getattr(a, nm), getattr(b, nm)
+            assert (x is None and y is None) or np.array_equal(x, y), nm
+        assert a.n_faces == b.n_faces and a.quad_degree == b.quad_degree
+        for fa, fb in zip(a.faces, b.faces):
+            for nm in ("sigma", "weights", "xi", "phi"):
+                assert np.array_equal(getattr(fa, nm), getattr(fb, nm)), nm
+        pts = a.quad_pts[::2]
+        assert np.array_equal(a.eval_basis_grad(pts), b.eval_basis_grad(pts))
 
 
 @needs_ref
