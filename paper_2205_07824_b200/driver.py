@@ -185,7 +185,8 @@ def solve_steady(system, state, newton_options=None, precond=None, callback=None
 
 
 def run_steady(system, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8, forcing=1e-8,
-               restart=250, gmres_max_iter=6000, max_iter=20, orth="mgs", rb_rank=10):
+               restart=250, gmres_max_iter=6000, max_iter=20, orth="mgs", rb_rank=10,
+               jv_mode="tangent"):
     """Steady branch of run_simulation (driver.py:253-268) with the
     acceptance solver flags as defaults; returns (state, stats, timings)."""
     import torch
@@ -195,12 +196,13 @@ def run_steady(system, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8, forc
     u0 = torch.as_tensor(state.u, device=system.device).reshape(-1)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    M, cb = make_preconditioner(system, precond, res_fn, tan_fn, u0, rb_rank=rb_rank)
+    M, cb = make_preconditioner(system, precond, res_fn, tan_fn, u0, jv_mode=jv_mode,
+                                rb_rank=rb_rank)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     opts = NewtonOptions(abs_tol=abs_tol, rel_tol=rel_tol, max_iter=max_iter, forcing=forcing,
                          gmres_restart=restart, gmres_max_iter=gmres_max_iter,
-                         jv_mode="tangent", orth=orth)
+                         jv_mode=jv_mode, orth=orth)
     out, stats = solve_steady(system, state, opts, precond=M, callback=cb)
     torch.cuda.synchronize()
     t3 = time.perf_counter()

@@ -194,6 +194,34 @@ SOLVE_CASES = {
         precond="composite", rb_rank=3),
 }
 
+# exact solutions of the acceptance Poisson fixtures (test_acceptance.py:60-70)
+def poisson_exact(nd):
+    u = "*".join(f"sin(pi*x{k + 1})" for k in range(nd))
+    q = ["0-pi*" + "*".join(("cos" if k == j else "sin") + f"(pi*x{k + 1})"
+                            for k in range(nd)) for j in range(nd)]
+    return [u], q
+
+
+# config 1 (2D Poisson, unit square, p=3: the CPU-oracle parity case) and the
+# survey's reproduced known answers: acceptance flags,
+# reference solve_steady; the goldens also carry the reference's error_u / q
+for _kind, _n, _pre in (("quad", 8, "block_jacobi"), ("quad", 8, "identity"),
+                        ("tri", 8, "block_jacobi"), ("quad", 16, "block_jacobi"),
+                        ("tri", 16, "block_jacobi")):
+    SOLVE_CASES[f"config1_{_kind}_p3_n{_n}_{'bj' if _pre == 'block_jacobi' else 'id'}"] = dict(
+        model=("file", "poisson2d.model"), kind=_kind, counts=[_n, _n], p=3, precond=_pre,
+        exact=poisson_exact(2))
+# finite-difference Jacobian-vector mode (the reference's NewtonOptions
+# default, solver.py:81), also for the block-Jacobi probes (solver.py:322-330)
+SOLVE_CASES["nonlin_diff2d_quad_p3_n3_bj_fd"] = dict(
+    SOLVE_CASES["nonlin_diff2d_quad_p3_n3_bj"], jv_mode="fd")
+SOLVE_CASES["poisson2d_quad_p3_n4_id_fd"] = dict(
+    SOLVE_CASES["poisson2d_quad_p3_n4_id"], jv_mode="fd")
+for _kind in ("hex", "tet"):
+    SOLVE_CASES[f"known_poisson3d_{_kind}_p3_n4_bj"] = dict(
+        model=("file", "poisson3d.model"), kind=_kind, counts=[4, 4, 4], p=3,
+        precond="block_jacobi", exact=poisson_exact(3))
+
 # acceptance solver flags (test_acceptance.py:69-81)
 ACCEPT_FLAGS = dict(abs_tol=1e-11, rel_tol=3e-8, forcing=1e-8, restart=250,
                     gmres_max_iter=6000)

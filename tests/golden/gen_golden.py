@@ -127,22 +127,29 @@ def gen_solve(name, spec):
     f = ACCEPT_FLAGS
     opts = NewtonOptions(abs_tol=f["abs_tol"], rel_tol=f["rel_tol"], max_iter=20,
                          forcing=f["forcing"], gmres_restart=f["restart"],
-                         gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent")
+                         gmres_max_iter=f["gmres_max_iter"],
+                         jv_mode=spec.get("jv_mode", "tangent"))
     pre = cb = None
     if spec["precond"] in ("block_jacobi", "composite"):
         rf, tf = _steady_fns(s)
-        pre = build_pde_block_jacobi(s, rf, tf, s.pack(st.u), "tangent")
+        pre = build_pde_block_jacobi(s, rf, tf, s.pack(st.u), spec.get("jv_mode", "tangent"))
         if spec["precond"] == "composite":
             # CompositeManager (driver.py:145-175) as make_preconditioner wires it
             from ldgkit.driver import CompositeManager
             pre = CompositeManager(s, pre, tf, rank=spec.get("rb_rank", 10), refresh=1)
             cb = pre.note_update
     out_state, stats = solve_steady(s, st, opts, precond=pre, callback=cb)
+    extra = {}
+    if "exact" in spec:
+        from ldgkit.diagnostics import compute_l2_error
+        eu, eq = spec["exact"]
+        err = compute_l2_error(s, out_state, eu, eq)
+        extra = dict(error_u=np.array(err.error_u), error_q=np.array(err.error_q))
     np.savez_compressed(HERE / f"solve_{name}.npz", u=out_state.u,
                         newton_iters=np.array(stats.newton_iters),
                         gmres_iters=np.array(stats.gmres_iters),
-                        residual_norms=np.array(stats.residual_norms))
-    print("solve", name, stats.newton_iters, stats.gmres_iters)
+                        residual_norms=np.array(stats.residual_norms), **extra)
+    print("solve", name, stats.newton_iters, stats.gmres_iters, extra)
 
 
 def gen_transient(name, spec):

@@ -206,3 +206,57 @@ def test_device_source_matches_host_restatement(name):
     dev = DeviceSource(s.tab, s.device).load(0.3).cpu().numpy()
     host = s.tab.source_load(0.3)
     assert rel(dev, host) < 1e-13
+
+
+@pytest.mark.parametrize("shear", [False, True])
+def test_hex_p3_vs_oracle_at_scale(shear):
+    """The config-3 kernels past one persistent sweep: 30x28x26 hexes = 2,730
+    eight-element groups against the plane kernel's grid of 1,184 warps (and
+    the completion kernel's), so every warp runs the double-buffered loop at
+    least twice (buffer 1, prefetch of group g + stride).  Axis-aligned: the
+    DIAG branch; sheared: the general-C branch.  Oracle R and J du at 1e-12."""
+    from oracle import make_oracle
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem, SolverState
+    m = model.load_model(str(GOLDEN / "poisson3d.model"))
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [30, 28, 26], "hex")
+    if shear:
+        A = np.array([[1.0, 0.3, 0.1], [0.0, 1.0, 0.2], [0.0, 0.0, 0.9]])
+        mesh.vertices = mesh.vertices @ A.T
+        mesh.ho_nodes = mesh.ho_nodes @ A.T
+    topo = meshgen.build_face_topology(mesh)
+    master = refelem.build_master("hex", 3)
+    s = LdgSystem(m, mesh, topo, master)
+    assert s.n_elements // 8 > 2 * 1184
+    o = make_oracle(m, mesh, topo, master)
+    rng = np.random.default_rng(17)
+    u = rng.normal(size=(s.n_elements, s.n_nodes, 1))
+    du = rng.normal(size=u.shape)
+    st = SolverState(u=u, q=None, w=None, t=0.0)
+    assert rel(s.residual(st)[0], o.residual(u)) < TOL
+    assert rel(s.residual_tangent(st, du)[0], o.residual_tangent(u, du)) < TOL
+
+
+def test_fused_equals_unfused_at_config3_size():
+    """Config 3 (hex p=3, n=54, 10,077,696 DOFs) on the device: the fused
+    two-pass matvec (q never leaves the SM) against the unfused reference
+    structure (compute_mixed -> flux from q, disc.py:601-653), both for the
+    tangent and for the residual with source and Dirichlet data."""
+    import torch
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem
+    m = model.load_model(str(GOLDEN / "poisson3d.model"))
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [54] * 3, "hex")
+    s = LdgSystem(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("hex", 3))
+    assert s.n_dofs == 10_077_696
+    g = torch.Generator(device="cuda").manual_seed(0)
+    du = torch.randn((s.n_elements, s.n_nodes, 1), dtype=torch.float64, device="cuda",
+                     generator=g)
+    J = s.tangent_dev(du)
+    dq = s.mixed_dev(du, 0.0, homogeneous=True)
+    Ju = s.flux_from_mixed_dev(du, dq, True)
+    assert float(torch.linalg.norm(J - Ju) / torch.linalg.norm(Ju)) < TOL
+    R = s.residual_dev(du, 0.0)
+    q = s.mixed_dev(du, 0.0)
+    Ru = s.flux_from_mixed_dev(du, q, False, 0.0)
+    assert float(torch.linalg.norm(R - Ru) / torch.linalg.norm(Ru)) < TOL

@@ -73,3 +73,57 @@ def test_dense_algebra_matches_reference(name):
     assert rel(q, g["q"]) < 1e-13 and rel(dq, g["dq"]) < 1e-13
     assert rel(de.flux(t, g["u"], q, False, gv, bs), g["R"]) < 1e-13
     assert rel(de.flux(t, g["du"], dq, True), g["Jdu"]) < 1e-13
+
+
+def _ldgkit_setup():
+    import sys
+    from conftest import REFERENCE_SRC
+    sys.path.insert(0, REFERENCE_SRC)
+    from ldgkit import master as RMa
+    from ldgkit import mesh as RMe
+    from ldgkit import model as RMo
+    return RMo, RMe, RMa
+
+
+@pytest.mark.skipif(not __import__("conftest").reference_available(),
+                    reason="reference package not mounted")
+@pytest.mark.parametrize("name", ["poisson3d_hex_p3", "convdiff3d_hex_periodic_p2",
+                                  "poisson2d_tri_p2", "poisson3d_tet_p2"])
+def test_dropin_tables_from_ldgkit_objects(name):
+    """The drop-in claim: the device tables built from ldgkit's OWN setup
+    objects (PdeModel, Mesh, FaceTopology, MasterElement; disc.py:265) give
+    the reference operator, i.e. the B200 LdgSystem accepts exactly what a
+    reference caller passes."""
+    from paper_2205_07824_b200.tables import DenseTables
+    g = np.load(GOLDEN / f"{name}.npz")
+    parts = build_case(CASES[name], *_ldgkit_setup())
+    if CASES[name]["kind"] in ("quad", "hex"):
+        tab = TensorTables(*parts)
+        assert np.array_equal(tab.switch, g["switch"])
+        gp, bs = tab.boundary_projection(0.0), tab.source_load(0.0)
+        assert rel(emu.fused(tab, g["u"], False, gp, bs), g["R"]) < 1e-13
+        assert rel(emu.fused(tab, g["du"], True), g["Jdu"]) < 1e-13
+    else:
+        import dense_emulation as de
+        t = DenseTables(*parts)
+        assert np.array_equal(t.switch, g["switch"])
+        gv, bs = t.boundary_values(0.0), t.source_load(0.0)
+        q = de.mixed(t, g["u"], gv)
+        assert rel(de.flux(t, g["u"], q, False, gv, bs), g["R"]) < 1e-13
+        assert rel(de.flux(t, g["du"], de.mixed(t, g["du"]), True), g["Jdu"]) < 1e-13
+
+
+@pytest.mark.skipif(not __import__("conftest").reference_available(),
+                    reason="reference package not mounted")
+@pytest.mark.parametrize("name", ["euler2d_quad_periodic_p3", "ns3d_hex_periodic_p2"])
+def test_dropin_nl_tables_from_ldgkit_objects(name):
+    """Generated-kernel tables (NlTables) accept ldgkit's objects and agree
+    with the ones built from this package's setup restatement."""
+    from cases import NL_CASES
+    from paper_2205_07824_b200.nonlinear import NlTables
+    a = NlTables(*build_case(NL_CASES[name], *_ldgkit_setup()))
+    b = NlTables(*build_case(NL_CASES[name], *b200_setup()))
+    g = np.load(GOLDEN / f"{name}.npz")
+    assert np.array_equal(a.switch, g["switch"])
+    for k in ("geo", "xmap", "fgeo", "fnbr", "finfo"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
