@@ -147,6 +147,26 @@ def run_solve(system, orth="dcgs2"):
             "final_residual": stats.final_residual, "error_u": err}
 
 
+def run_solve_partitioned(s, world):
+    """Newton-GMRES time to solution on the N-slab box (each rank one slab;
+    allreduced DCGS2, rank-local block-Jacobi, face-node halos), the max over
+    ranks of the device-synchronised wall time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2205_07824_b200.parallel import run_steady_partitioned
+    u, stats, tm = run_steady_partitioned(s, orth="dcgs2")
+    t = torch.tensor([tm["precond_build_s"], tm["solve_s"]], dtype=torch.float64,
+                     device=s.device if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    b, sv = (float(x) for x in t.tolist())
+    return {"metric": "Newton-GMRES time to solution (s), N-slab config-3 box, block-Jacobi, "
+                      "acceptance flags", "dofs": world * s.n_dofs,
+            "gpu": {"orth": "dcgs2", "precond_build_s": b, "solve_s": sv,
+                    "time_to_solution_s": b + sv, "newton_iters": stats.newton_iters,
+                    "gmres_iters": stats.total_gmres_iters,
+                    "final_residual": stats.final_residual}}
+
+
 def cpu_solve(n):
     """Oracle (reference numpy path) steady solve on n^3 hexes, same flags."""
     from oracle import make_oracle
@@ -274,23 +294,94 @@ def nonlinear_lines(hbm, cpu=True):
     return out
 
 
+REF_SRC = ROOT / "baseline" / "_ref"      # the unmodified reference, pip --target install
+
+
+def _ref_worker(n, steps, warmup, barrier, q):
+    """One host process: the UNMODIFIED reference (ldgkit from baseline/_ref)
+    LdgSystem.residual_tangent on its own n^3 hex p=3 Poisson box (the
+    reference's numpy path, disc.py:591-593).  Steps are synchronised across
+    the workers by `barrier`; returns per-step seconds."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    sys.path.insert(0, str(REF_SRC))
+    from ldgkit import master as r_master, mesh as r_mesh, model as r_model
+    from ldgkit.disc import LdgSystem as RefSystem, SolverState as RefState
+    m = r_model.load_model(str(MODEL))
+    mesh = r_mesh.generate_structured([(0.0, 1.0)] * 3, [n] * 3, "hex")
+    s = RefSystem(m, mesh, r_mesh.build_face_topology(mesh), r_master.build_master("hex", P))
+    ne, nb = s.n_elements, s.n_nodes
+    u = np.random.default_rng(1).normal(size=(ne, nb, 1))
+    du = np.random.default_rng(0).normal(size=(ne, nb, 1))
+    st = RefState(u=u, q=None, w=None, t=0.0)
+    for _ in range(warmup):
+        s.residual_tangent(st, du)
+    ts = []
+    for _ in range(steps):
+        barrier.wait()
+        t0 = time.perf_counter()
+        s.residual_tangent(st, du)
+        ts.append(time.perf_counter() - t0)
+    q.put((ne * nb, ts))
+
+
+def reference_times(n, steps, warmup, procs):
+    """The reference's CPU path on `procs` host processes at once (each an
+    independent n^3 sample; the reference itself is single-threaded numpy):
+    per-step max over processes, total DOFs.  Uses ldgkit from baseline/_ref
+    when installed ("reference"), else the oracle port ("port", 1 process)."""
+    if not (REF_SRC / "ldgkit").is_dir():
+        ts, nd = cpu_oracle_times(n, steps)
+        return ts, nd, 1, "port"
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    barrier, q = ctx.Barrier(procs), ctx.Queue()
+    ps = [ctx.Process(target=_ref_worker, args=(n, steps, warmup, barrier, q)) for _ in range(procs)]
+    for p in ps:
+        p.start()
+    res = [q.get() for _ in ps]
+    for p in ps:
+        p.join()
+    ts = np.max(np.array([r[1] for r in res]), axis=0)
+    return list(ts), sum(r[0] for r in res), procs, "reference"
+
+
+def ref_procs():
+    """All host cores the reference arm may use (bounded: each process holds
+    a ~1 GB reference Discretization of the sample)."""
+    try:
+        c = len(os.sched_getaffinity(0))
+    except Exception:
+        c = os.cpu_count() or 1
+    return max(1, min(c, 64))
+
+
 def run_reference(args, rank):
-    """The reference CPU path (oracle port of ldgkit's numpy implementation)."""
+    """The reference's own CPU implementation of the path (ldgkit's
+    LdgSystem.residual_tangent from baseline/_ref, unmodified), on all the
+    host cores: one reference process per core, each on a bounded
+    n=CPU_SAMPLE_N sample of config 3, steps synchronised, per-step time the
+    max over processes."""
     if rank != 0:
         return
-    ts, ndof = cpu_oracle_times(CPU_SAMPLE_N, max(args.steps, 1))
+    procs = ref_procs()
+    ts, ndof, cores, kind = reference_times(CPU_SAMPLE_N, max(args.steps, 1), args.warmup, procs)
     med = float(np.median(ts))
     v = ndof / med / 1e9
+    sample = (f"{cores} processes x {ndof // cores}-DOF hex p=3 Poisson boxes (n={CPU_SAMPLE_N}, "
+              f"config 3's model/order) of "
+              + ("ldgkit.disc.LdgSystem.residual_tangent (unmodified, baseline/_ref)"
+                 if kind == "reference" else "the oracle port (baseline/_ref absent)")
+              + f"; median over {len(ts)} synchronised steps of the max over processes")
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": "GDOF/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"3D Poisson hex p=3 tangent matvec; bounded sample "
-                               f"n={CPU_SAMPLE_N} ({ndof} DOFs) of config 3"},
-        "cpu_baseline": {"value": v, "unit": "GDOF/s", "cores": 1, "kind": "port",
-                         "sample": f"{ndof}-DOF hex p=3 Poisson tangent, median of "
-                                   f"{len(ts)} calls (numpy c_einsum path: 1 core)"},
+        "config": {"workload": f"config 3 (3D Poisson hex p=3) tangent matvec J(u)du; "
+                               f"bounded samples, {ndof} DOFs per step over {cores} cores",
+                   "full_size_extrapolation_s": 10077696 / (v * 1e9)},
+        "cpu_baseline": {"value": v, "unit": "GDOF/s", "cores": cores, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": v, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -319,7 +410,7 @@ def run_b200(args, rank, world):
     du = torch.randn((ne, nb, 1), dtype=torch.float64, device=dev, generator=gen)
     dR = torch.empty_like(du)
     X = core.scratch() if world == 1 else s.X
-    u_in = du if world == 1 else s.u_ext
+    u_in = du                          # partitioned: ghost rows come from s.u_ghost
     dq = torch.empty((ne, nb, 1, 3), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
     lib, h = core.lib, core._h
@@ -403,43 +494,55 @@ def run_b200(args, rank, world):
     bytes_p1 = 8 * ndof + 8 * ndof + 8 * exports * nfn
     bytes_p2 = 16 * ndof + 8 * completes * nfn
 
-    # e2e through the public drop-in call with pinned host buffers
+    # e2e through the public drop-in call with host buffers: numpy in -> numpy
+    # out (the reference's calling convention, disc.py:588-593; pageable input
+    # staged by the library's host threads) and, beside it, pinned torch CPU
+    # tensors
+    du_np = du.cpu().numpy()
     du_host = du.cpu().pin_memory()
-    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world == 1:
-        st = SolverState(u=du_host, q=None, w=None, t=0.0)
 
-        def e2e_step():
-            return s.residual_tangent(st, du_host)[0]
-    else:
-        out_host = torch.empty(du_host.shape, dtype=torch.float64, pin_memory=True)
+    def e2e_time(x_host):
+        if world == 1:
+            st = SolverState(u=x_host, q=None, w=None, t=0.0)
 
-        def e2e_step():
-            d = du_host.to(dev, non_blocking=True)
-            r = s.tangent_dev(d)
-            out_host.copy_(r, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            return out_host
-    for _ in range(max(args.warmup, 3)):     # same pattern as the timed loop (the caller
-        out = e2e_step()                      # holds the previous result)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0 = time.perf_counter()
-    ea.record(stream)
-    for _ in range(args.steps):
-        out = e2e_step()
-    eb.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = ea.elapsed_time(eb) / args.steps
-    wall_e2e = (time.perf_counter() - e0) / args.steps * 1e3
-    assert out.device.type == "cpu"
-    emax = torch.tensor([e2e_ms], dtype=torch.float64,
-                        device=dev if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu")
-    if world > 1:
-        dist.all_reduce(emax, op=dist.ReduceOp.MAX)
-    e2e_ms = float(emax.item())
+            def e2e_step():
+                return s.residual_tangent(st, x_host)[0]
+        else:
+            out_host = torch.empty(du_host.shape, dtype=torch.float64, pin_memory=True)
 
+            def e2e_step():
+                d = torch.as_tensor(x_host).to(dev, non_blocking=True)
+                r = s.tangent_dev(d)
+                out_host.copy_(r, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return out_host
+        for _ in range(max(args.warmup, 3)):     # same pattern as the timed loop (the caller
+            out = e2e_step()                      # holds the previous result)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0 = time.perf_counter()
+        ea.record(stream)
+        for _ in range(args.steps):
+            out = e2e_step()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        ms = ea.elapsed_time(eb) / args.steps
+        wall = (time.perf_counter() - e0) / args.steps * 1e3
+        assert not (isinstance(out, torch.Tensor) and out.is_cuda)
+        emax = torch.tensor([ms], dtype=torch.float64,
+                            device=dev if dist.is_initialized() and dist.get_backend() == "nccl"
+                            else "cpu")
+        if world > 1:
+            dist.all_reduce(emax, op=dist.ReduceOp.MAX)
+        return float(emax.item()), wall
+    e2e_ms, wall_e2e = e2e_time(du_np)
+    e2e_pin_ms, wall_pin = e2e_time(du_host)
+
+    solve_line = None
+    if world > 1 and not args.no_solve:
+        solve_line = run_solve_partitioned(s, world)
     if rank != 0:
         return
     pk = peaks()
@@ -467,9 +570,11 @@ def run_b200(args, rank, world):
         "e2e": {"value": world * ndof / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
                 "h2d_bytes_per_step": ndof * 8, "d2h_bytes_per_step": ndof * 8,
                 "ms_per_step": e2e_ms, "wall_ms_per_step": wall_e2e,
-                "call": ("LdgSystem.residual_tangent(state, du) with pinned torch CPU du"
-                         if world == 1 else
-                         "PartitionedLdgSystem.tangent_dev on the H2D copy of pinned du, D2H of R")},
+                "call": ("LdgSystem.residual_tangent(state, du) with numpy du -> numpy R "
+                         "(the reference's calling convention)" if world == 1 else
+                         "PartitionedLdgSystem.tangent_dev on the H2D copy of numpy du, D2H of R"),
+                "pinned_torch": {"value": world * ndof / (e2e_pin_ms * 1e-3) / 1e9,
+                                 "ms_per_step": e2e_pin_ms, "wall_ms_per_step": wall_pin}},
         "roofline": {"bound": "hbm", "kernel": p1_name,
                      "achieved": ach_p1, "peak": hbm, "unit": "GB/s",
                      "frac": ach_p1 / hbm, "traffic": traffic.get("pass1"),
@@ -501,16 +606,21 @@ def run_b200(args, rank, world):
                          "gpu": run_solve(s)}
         if not args.no_cpu_baseline:
             line["solve"]["cpu_oracle_small"] = {"n": 3, **cpu_solve(3)}
+    if world > 1 and solve_line is not None:
+        line["solve"] = solve_line
     if world == 1 and not args.no_tet:
         line["tet"] = tet_line(hbm)
     if world == 1 and not args.no_nonlinear:
         line["nonlinear"] = nonlinear_lines(hbm, cpu=not args.no_cpu_baseline)
     if not args.no_cpu_baseline:
-        ts, nd_cpu = cpu_oracle_times(CPU_SAMPLE_N, 3)
+        ts, nd_cpu, cores, kind = reference_times(CPU_SAMPLE_N, 3, 1, ref_procs())
         v = nd_cpu / float(np.median(ts)) / 1e9
-        line["cpu_baseline"] = {"value": v, "unit": "GDOF/s", "cores": 1, "kind": "port",
-                                "sample": f"{nd_cpu}-DOF hex p=3 Poisson tangent (n="
-                                          f"{CPU_SAMPLE_N}), median of 3 after 1 warm-up"}
+        line["cpu_baseline"] = {
+            "value": v, "unit": "GDOF/s", "cores": cores, "kind": kind,
+            "sample": f"{cores} processes x {nd_cpu // cores}-DOF hex p=3 Poisson tangent (n="
+                      f"{CPU_SAMPLE_N}) of " + ("ldgkit (unmodified, baseline/_ref)"
+                                                 if kind == "reference" else "the oracle port")
+                      + ", median of 3 synchronised steps after 1 warm-up"}
     print(json.dumps(line), flush=True)
 
 
@@ -531,6 +641,16 @@ def main():
                     help="skip the generated-kernel (configs 2 / 4) throughput lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # self-launch one rank per GPU (the driver's torchrun command, same flags)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
     if args.impl == "reference":

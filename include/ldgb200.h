@@ -174,6 +174,23 @@ int ldg_apply_host(LdgHandle* h, int tangent, const double* v_host, double* out_
                    const double* bsrc, int nchunk, const int32_t* starts,
                    const int32_t* dep, void* stream);
 
+/* ldg_apply_host for a PAGEABLE v_host (a numpy array: the reference's
+ * calling convention, ldgkit/disc.py:588-593): each chunk is copied into the
+ * pinned staging buffer `stage` (ne * nb * ncu doubles) by the host threads
+ * (OpenMP) and sent while the next chunk is staged.  out_host stays pinned.
+ * stage == NULL behaves exactly like ldg_apply_host. */
+int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, double* stage,
+                          double* out_host, double* v_dev, double* R_dev, double* scratch,
+                          const double* gproj, const double* bsrc, int nchunk,
+                          const int32_t* starts, const int32_t* dep, void* stream);
+
+/* Partitioned operators: neighbour element rows >= ghost0 are
+ * read from u_ghost (row nbr - ghost0) instead of the state vector, so a
+ * rank's owned vector is used in place and only the halo lands in the side
+ * buffer.  ghost0 < 0 switches it off.  (Reference: none -- the reference is
+ * single-process; this is the B200 multi-GPU layer.) */
+int ldg_set_ghost_rows(LdgHandle* h, int ghost0, const double* u_ghost);
+
 /* Unfused reference structure, kept for comparison: flux pass from a
  * precomputed q = compute_mixed(u) (72 B/DOF of HBM traffic at nd = 3). */
 int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
@@ -281,6 +298,9 @@ int ldg_dcgs_update(int64_t n, int m, const double* V, int64_t ldv, const double
  * thread, 8 x 256-thread blocks per SM, `iters` FMAs per chain; returns
  * TFLOP/s (2 flops per FMA) and the kernel time (SURVEY 8(d) FP64 peak) */
 int ldg_probe_fp64(int64_t iters, double* tflops, double* ms, void* stream);
+/* mode 0: DFMA, 1: FP64 tensor core (mma.sync m8n8k4 f64), 2: both in one
+ * loop (tflops = their sum) -- decides whether DMMA adds FP64 throughput */
+int ldg_probe_fp64_mode(int mode, int64_t iters, double* tflops, double* ms, void* stream);
 
 #ifdef __cplusplus
 }

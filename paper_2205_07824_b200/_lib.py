@@ -72,6 +72,7 @@ _SIGS = {
     "ldg_compute_mixed": ([C.c_void_p] * 5, C.c_int),
     "ldg_scratch_doubles": ([C.c_void_p], C.c_int64),
     "ldg_set_export_layout": ([C.c_void_p, C.c_int], C.c_int),
+    "ldg_set_ghost_rows": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
     "ldg_residual": ([C.c_void_p] * 7, C.c_int),
     "ldg_residual_tangent": ([C.c_void_p] * 5, C.c_int),
     "ldg_operator_pass": ([C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 6, C.c_int),
@@ -80,6 +81,8 @@ _SIGS = {
     "ldg_apply_host": ([C.c_void_p, C.c_int] + [C.c_void_p] * 7 + [C.c_int, C.c_void_p,
                                                                  C.c_void_p, C.c_void_p],
                        C.c_int),
+    "ldg_apply_host_staged": ([C.c_void_p, C.c_int] + [C.c_void_p] * 8
+                              + [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_flux_from_mixed": ([C.c_void_p, C.c_int] + [C.c_void_p] * 6, C.c_int),
     "ldg_mass_apply": ([C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_mass_inv_apply": ([C.c_void_p] * 4, C.c_int),
@@ -99,6 +102,7 @@ _SIGS = {
     "ldg_color_distance2": ([C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
                             C.c_int),
     "ldg_probe_fp64": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ldg_probe_fp64_mode": ([C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_dcgs_dots": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_dcgs_update": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,

@@ -45,7 +45,7 @@ def build(force=False, verbose=False, out=None, defines=()):
     lib.parent.mkdir(parents=True, exist_ok=True)
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                    "--expt-relaxed-constexpr", "-I", str(ROOT / "include"),
+                    "--expt-relaxed-constexpr", "-Xcompiler", "-fopenmp", "-I", str(ROOT / "include"),
                     "-I", str(CSRC)] + [f"-D{d}" for d in defines]
     if verbose:
         flags += ["-Xptxas", "-v"]
@@ -63,7 +63,7 @@ def build(force=False, verbose=False, out=None, defines=()):
         if p.returncode:
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "shared", *map(str, objs), "-lnvrtc",
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "shared", *map(str, objs), "-lnvrtc", "-lgomp",
            "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-o", str(tmp)]
     subprocess.run(cmd, check=True)
     os.replace(tmp, lib)

@@ -1,10 +1,13 @@
 // C ABI of libldgb200.so: handle lifecycle and the operator entry points.
 // See include/ldgb200.h for the reference interface each one replaces.
 
+#include <climits>
+#include <cstdint>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <vector>
 #include "ldg_dense.cuh"
@@ -69,6 +72,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
     return fail(2, "unsupported tensor configuration");
   LdgHandle* h = new LdgHandle();
   memset(&h->P, 0, sizeof(h->P));
+  h->P.ghost0 = INT32_MAX;
   const size_t ne = (size_t)t->ne, nf = 2 * t->nd;
   size_t nfn = t->nd == 3 ? (size_t)t->n1 * t->n1 : (size_t)t->n1;
   int rc = 0;
@@ -308,6 +312,7 @@ int ldg_create_dense(const LdgDenseTables* t, LdgHandle** out) {
   h->dense = 1;
   memset(&h->D, 0, sizeof(h->D));
   memset(&h->P, 0, sizeof(h->P));
+  h->P.ghost0 = INT32_MAX;
   ldg::DenseParams& D = h->D;
   D.ne = t->ne; D.nd = t->nd; D.nb = t->nb; D.nqf = t->nqf; D.nface = t->nface;
   D.nperm = t->nperm; D.ncu = t->ncu; D.trace_centered = t->trace_centered;
@@ -369,6 +374,18 @@ int ldg_create_dense(const LdgDenseTables* t, LdgHandle** out) {
 int ldg_set_export_layout(LdgHandle* h, int consumer) {
   if (!h || h->dense) return fail(2, "export layout applies to tensor handles");
   h->P.x_consumer = consumer ? 1 : 0;
+  return 0;
+}
+
+// Partitioned operators: neighbour rows >= ghost0 come from u_ghost (the
+// halo buffer) instead of the state vector, so the owned vector is used in
+// place (no per-call copy into an owned+ghost array).  ghost0 < 0 resets.
+int ldg_set_ghost_rows(LdgHandle* h, int ghost0, const double* u_ghost) {
+  if (!h) return fail(2, "null handle");
+  if (h->dense) return fail(2, "not available for simplex systems");
+  if (ghost0 >= 0 && !u_ghost) return fail(2, "ghost rows need a buffer");
+  h->P.ghost0 = ghost0 < 0 ? INT32_MAX : ghost0;
+  h->P.u_ghost = ghost0 < 0 ? nullptr : u_ghost;
   return 0;
 }
 
@@ -474,9 +491,24 @@ int ldg_apply_host(LdgHandle* h, int tangent, const double* v_host, double* out_
                    double* v_dev, double* R_dev, double* scratch, const double* gproj,
                    const double* bsrc, int nchunk, const int32_t* starts,
                    const int32_t* dep, void* stream) {
+  return ldg_apply_host_staged(h, tangent, v_host, nullptr, out_host, v_dev, R_dev, scratch,
+                               gproj, bsrc, nchunk, starts, dep, stream);
+}
+
+// Same pipeline for a PAGEABLE input (a numpy array, the reference's calling
+// convention, disc.py:588-593): each chunk is first copied into the pinned
+// staging buffer `stage` by the OpenMP host threads, then sent; the copy of
+// chunk c+1 on the host overlaps the H2D of chunk c and the kernels of the
+// chunks already resident.  stage == NULL: v_host is pinned (ldg_apply_host).
+int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, double* stage,
+                          double* out_host, double* v_dev, double* R_dev, double* scratch,
+                          const double* gproj, const double* bsrc, int nchunk,
+                          const int32_t* starts, const int32_t* dep, void* stream) {
   if (!h || !v_host || !out_host || !v_dev || !R_dev || !scratch || nchunk < 1 || !starts || !dep)
     return fail(2, "bad argument");
   if (h->dense) return fail(2, "not available for simplex systems");
+  for (int c = 0; c < nchunk; ++c)
+    if (dep[c] < c || dep[c] >= nchunk || starts[c + 1] < starts[c]) return fail(2, "bad chunk plan");
   cudaStream_t s = (cudaStream_t)stream;
   if (!h->s_in) {
     cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking);
@@ -494,33 +526,48 @@ int ldg_apply_host(LdgHandle* h, int tangent, const double* v_host, double* out_
                      h->P.ncu;
   cudaEventRecord(h->ev_start, s);
   cudaStreamWaitEvent(h->s_in, h->ev_start, 0);
+  int next1 = 0, next2 = 0;           // next chunk whose pass 1 / pass 2 is to be issued
   for (int c = 0; c < nchunk; ++c) {
     const size_t a = (size_t)starts[c] * row, n = (size_t)(starts[c + 1] - starts[c]) * row;
-    cudaMemcpyAsync(v_dev + a, v_host + a, n * sizeof(double), cudaMemcpyHostToDevice, h->s_in);
+    const double* src = v_host + a;
+    if (stage) {
+      // 1 MB slices over the host threads (first touch of the pinned pages
+      // happened at allocation; memcpy bandwidth scales with threads)
+      const int64_t slice = 1 << 17, ns = (int64_t)((n + slice - 1) / slice);
+#pragma omp parallel for schedule(static)
+      for (int64_t k = 0; k < ns; ++k) {
+        const size_t o = (size_t)k * slice, m = std::min((size_t)slice, n - o);
+        memcpy(stage + a + o, v_host + a + o, m * sizeof(double));
+      }
+      src = stage + a;
+    }
+    cudaMemcpyAsync(v_dev + a, src, n * sizeof(double), cudaMemcpyHostToDevice, h->s_in);
     cudaEventRecord(h->ev_in[c], h->s_in);
-  }
-  std::vector<char> done(nchunk, 0);
-  for (int c = 0; c < nchunk; ++c) {
-    cudaStreamWaitEvent(s, h->ev_in[dep[c]], 0);
-    ldg::TensorParams Q = h->P;
-    Q.e0 = starts[c];
-    Q.e1 = starts[c + 1];
-    int rc = ldg::launch_fused_pass(Q, 1, tangent != 0, v_dev, gproj, bsrc, R_dev, scratch, s);
-    if (rc) return fail(rc, "pass 1 launch", cudaGetLastError());
-    for (int d = 0; d < nchunk; ++d) {
-      if (done[d] || dep[d] > c) continue;
-      Q.e0 = starts[d];
-      Q.e1 = starts[d + 1];
-      rc = ldg::launch_fused_pass(Q, 2, tangent != 0, v_dev, gproj, bsrc, R_dev, scratch, s);
-      if (rc) return fail(rc, "pass 2 launch", cudaGetLastError());
-      cudaEventRecord(h->ev_p2[d], s);
-      cudaStreamWaitEvent(h->s_out, h->ev_p2[d], 0);
-      const size_t a = (size_t)starts[d] * row, n = (size_t)(starts[d + 1] - starts[d]) * row;
-      cudaMemcpyAsync(out_host + a, R_dev + a, n * sizeof(double), cudaMemcpyDeviceToHost,
-                      h->s_out);
-      done[d] = 1;
+    // every pass whose inputs are now in flight can be queued
+    while (next1 < nchunk && dep[next1] <= c) {
+      cudaStreamWaitEvent(s, h->ev_in[dep[next1]], 0);
+      ldg::TensorParams Q = h->P;
+      Q.e0 = starts[next1];
+      Q.e1 = starts[next1 + 1];
+      int rc = ldg::launch_fused_pass(Q, 1, tangent != 0, v_dev, gproj, bsrc, R_dev, scratch, s);
+      if (rc) return fail(rc, "pass 1 launch", cudaGetLastError());
+      ++next1;
+      while (next2 < next1 && dep[next2] < next1) {
+        Q.e0 = starts[next2];
+        Q.e1 = starts[next2 + 1];
+        rc = ldg::launch_fused_pass(Q, 2, tangent != 0, v_dev, gproj, bsrc, R_dev, scratch, s);
+        if (rc) return fail(rc, "pass 2 launch", cudaGetLastError());
+        cudaEventRecord(h->ev_p2[next2], s);
+        cudaStreamWaitEvent(h->s_out, h->ev_p2[next2], 0);
+        const size_t a2 = (size_t)starts[next2] * row,
+                     n2 = (size_t)(starts[next2 + 1] - starts[next2]) * row;
+        cudaMemcpyAsync(out_host + a2, R_dev + a2, n2 * sizeof(double), cudaMemcpyDeviceToHost,
+                        h->s_out);
+        ++next2;
+      }
     }
   }
+  if (next2 != nchunk) return fail(2, "chunk plan left passes unissued");
   if (getenv("LDG_PIPE_DEBUG")) {       // timeline of the copies and kernels
     cudaEvent_t t1, t2, t3;
     cudaEventCreate(&t1); cudaEventCreate(&t2); cudaEventCreate(&t3);
@@ -593,6 +640,7 @@ int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
                         const double* bsrc, double* R, void* stream) {
   if (!h || !u || !q || !R) return fail(2, "null argument");
   if (h->dense) return fail(2, "not available for simplex systems");
+  if (h->P.ghost0 != INT32_MAX) return fail(2, "the unfused flux pass has no ghost-row mode");
   int rc = ldg::launch_flux(h->P, tangent != 0, u, q, gproj, bsrc, R, (cudaStream_t)stream);
   return rc ? fail(rc, "flux launch", cudaGetLastError()) : 0;
 }

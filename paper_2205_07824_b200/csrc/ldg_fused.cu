@@ -234,7 +234,7 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       if (kind == LDG_FACE_INTERIOR) {
         if (info & LDG_FL_UNBR) {
           const int mid = (info >> LDG_FACE_MAP_SHIFT) & 0xffff;
-          src[lf] = u + ((size_t)nbr * NB + __ldg(P.nmap + mid * NF + lt)) * NCU;
+          src[lf] = nbr_row(P, u, nbr, NB * NCU) + (size_t)__ldg(P.nmap + mid * NF + lt) * NCU;
         }
       } else if (!TANGENT && gproj) {
         src[lf] = gproj + ((size_t)nbr * NF + lt) * NCU;
@@ -816,7 +816,7 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
         if (kind == LDG_FACE_INTERIOR) {
           if (info[lf] & LDG_FL_UNBR) {
             const int mid = (info[lf] >> LDG_FACE_MAP_SHIFT) & 0xffff;
-            const double* base = u + (size_t)nbr[lf] * NB;
+            const double* base = nbr_row(P, u, nbr[lf], NB);
             int nn[N1];
 #pragma unroll
             for (int a = 0; a < N1; ++a)

@@ -116,7 +116,7 @@ mixed_kernel(const __grid_constant__ TensorParams P,
           const double own = su[slot][c][vn];
           double jump = 0.0;
           if (!own_hat) {
-            const double other = __ldg(u + ((size_t)nbr * NB + nn) * NCU + c);
+            const double other = __ldg(nbr_row(P, u, nbr, NB * NCU) + (size_t)nn * NCU + c);
             jump = P.trace_centered ? 0.5 * (own - other) : own - other;
           }
           sj[slot][lf][lt][c] = jump;

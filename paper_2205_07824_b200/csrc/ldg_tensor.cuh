@@ -30,6 +30,11 @@ struct TensorParams {
   int chunk_start[LDG_MAX_CHUNKS + 1];
   int chunk_dep[LDG_MAX_CHUNKS];   // last chunk whose pass 1 pass 2 of this chunk reads
   unsigned long long* bad;  // first non-finite element (atomicMin)
+  // partitioned operators: neighbour rows >= ghost0 are read from u_ghost
+  // (row nbr - ghost0) instead of u, so a rank's owned vector is used in
+  // place and only the halo lands in a side buffer (INT32_MAX: no ghosts)
+  int ghost0;
+  const double* u_ghost;
   double d1[LDG_MAX_N1 * LDG_MAX_N1];
   double m1[LDG_MAX_N1 * LDG_MAX_N1];
   double s1[LDG_MAX_N1 * LDG_MAX_N1];
@@ -42,6 +47,12 @@ struct TensorParams {
   double aq[LDG_MAX_NCU * 3 * LDG_MAX_NCU * 3];
   double mass_coef[LDG_MAX_NCU];
 };
+
+// start of neighbour element `nbr`'s row (`row` doubles) of the state u
+__device__ __forceinline__ const double* nbr_row(const TensorParams& P, const double* u, int nbr,
+                                                 int row) {
+  return nbr >= P.ghost0 ? P.u_ghost + (size_t)(nbr - P.ghost0) * row : u + (size_t)nbr * row;
+}
 
 // hex local faces (master.py:43-44): z-, z+, y-, y+, x-, x+
 // quad local faces: y-, x+, y+, x-

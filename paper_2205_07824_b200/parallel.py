@@ -83,6 +83,70 @@ class PartitionPlan:
                 self.send[q] = rows.astype(np.int64)          # local owned rows, sorted
         if np.any(self.fnbr < 0):
             raise DiscError("partition left an unresolved neighbour")
+        self._face_halo(tab)
+
+    def _cut_pairs(self, tab, recv_rank, send_rank):
+        """Cut (element, face) slots of recv_rank's elements whose neighbour
+        send_rank owns, as (neighbour global id, neighbour volume nodes read,
+        neighbour local face) -- computed identically on both sides from the
+        global tables, so the send and receive orders agree."""
+        a, b = self.ranges[recv_rank]
+        info = tab.finfo[a:b]
+        nbr = tab.fnbr[a:b].astype(np.int64)
+        interior = (info & 3) == 0
+        cut = interior & (self.owner[np.where(interior, nbr, 0)] == send_rank) & \
+            ((nbr < a) | (nbr >= b))
+        el, lf = np.nonzero(cut)
+        g = nbr[el, lf]
+        mid = (info[el, lf] >> 8) & 0xffff
+        nlf = (info[el, lf] >> 4) & 7
+        return g, np.asarray(tab.nmap)[mid], nlf
+
+    def _face_halo(self, tab):
+        """Face-node halo lists: per peer, only the neighbour
+        face nodes the cut faces read (n1^(nd-1) per face instead of the
+        whole n1^nd element row) and only the export slot of the face that
+        faces this rank (one of 2 nd).  Flat row indices:
+          u_recv[q]: rows of u_ghost viewed (n_ghost * nb, ncu)
+          u_send[q]: rows of the owned u viewed (ne_loc * nb, ncu)
+          x_recv[q] / x_send[q]: rows of X viewed (rows * 2nd, nfn * ncu)."""
+        nb = int(tab.n1) ** int(tab.nd)
+        nf = int(tab.nf)
+        self.nb, self.nf = nb, nf
+        self.u_recv, self.u_send, self.x_recv, self.x_send = {}, {}, {}, {}
+        me = self.rank
+        for q in range(self.nranks):
+            if q == me:
+                continue
+            for recv_rank, send_rank, own in ((me, q, False), (q, me, True)):
+                g, nodes, nlf = self._cut_pairs(tab, recv_rank, send_rank)
+                if g.size == 0:
+                    continue
+                un = np.unique(g[:, None] * nb + nodes)             # (element, node) keys
+                xk = np.unique(g * nf + nlf)                          # (element, face) keys
+                if own:                  # I send: rows of my owned arrays
+                    self.u_send[q] = un - self.e0 * nb
+                    self.x_send[q] = xk - self.e0 * nf
+                else:                    # I receive: rows of my ghost arrays
+                    gk = np.searchsorted(self.ghosts, un // nb)
+                    self.u_recv[q] = gk * nb + un % nb
+                    xg = np.searchsorted(self.ghosts, xk // nf)
+                    self.x_recv[q] = (self.ne_loc + xg) * nf + xk % nf
+        # owned elements with a ghost neighbour; when they sit at the two ends
+        # of the range (x-slabs) [a, b) is the interior, computed while the
+        # halos are in flight
+        touch = (np.where((self.finfo & 3) == 0, self.fnbr, -1) >= self.ne_loc).any(axis=1)
+        idx = np.nonzero(touch)[0]
+        a = 0
+        while a < self.ne_loc and touch[a]:
+            a += 1
+        b = self.ne_loc
+        while b > a and touch[b - 1]:
+            b -= 1
+        if touch[a:b].any():                  # boundary elements inside: no overlap
+            a = b = 0
+        self.interior = (a, b)
+        self.n_boundary = int(idx.size)
 
 
 class LocalTables:
@@ -163,6 +227,49 @@ class HaloExchanger:
         return arr
 
 
+class _Pending:
+    """In-flight list exchange: wait() completes the receives and scatters
+    them into the destination (on the current stream for NCCL)."""
+
+    def __init__(self, works, recv_bufs, dst, stage):
+        self.works, self.recv_bufs, self.dst, self.stage = works, recv_bufs, dst, stage
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        for idx, buf in self.recv_bufs:
+            self.dst.index_copy_(0, idx, buf.to(self.dst.device) if self.stage else buf)
+        self.works = []
+
+
+class FaceHaloExchanger(HaloExchanger):
+    """Face-node halos (PartitionPlan.u_send / u_recv, x_send / x_recv):
+    rows gathered from a flat source, sent with batched NCCL point-to-point
+    ops, scattered into a flat destination on wait().  start() returns at
+    once on NCCL (the transfer runs on NCCL's stream while the caller
+    launches interior work); gloo (CPU tests, ranks sharing one GPU) stages
+    through the host and completes before returning."""
+
+    def start(self, src, dst, send, recv):
+        import torch
+        import torch.distributed as dist
+        stage = src.is_cuda and dist.get_backend(self.group) == "gloo"
+        ops, recv_bufs = [], []
+        for q, rows in sorted(send.items()):
+            buf = src.index_select(0, self._rows(("s", id(send)), q, rows, src.device))
+            ops.append(dist.P2POp(dist.isend, buf.cpu() if stage else buf, q, group=self.group))
+        for q, rows in sorted(recv.items()):
+            buf = torch.empty((rows.size,) + tuple(dst.shape[1:]), dtype=dst.dtype,
+                              device="cpu" if stage else dst.device)
+            recv_bufs.append((self._rows(("r", id(recv)), q, rows, dst.device), buf))
+            ops.append(dist.P2POp(dist.irecv, buf, q, group=self.group))
+        works = dist.batch_isend_irecv(ops) if ops else []
+        p = _Pending(works, recv_bufs, dst, stage)
+        if stage:
+            p.wait()
+        return p
+
+
 class DistVecOps:
     """VecOps with every reduction allreduced over the process group (sum
     of per-rank partials; norms from allreduced squares)."""
@@ -228,9 +335,18 @@ class DistVecOps:
         self.nrm2(w, nrm_out)
 
     def dcgs_dots(self, V, k, x, y, hx, hy):
+        """Both dot sweeps' partials in ONE allreduce (hx, hy side by side
+        in a scratch row)."""
+        import torch
         self.b.dcgs_dots(V, k, x, y, hx, hy)
-        self._ar(hx[:k])
-        self._ar(hy[:k])
+        buf = getattr(self, "_dd", None)
+        if buf is None or buf.numel() < 2 * k or buf.device != hx.device:
+            buf = self._dd = torch.empty(2 * max(k, 256), dtype=hx.dtype, device=hx.device)
+        buf[:k].copy_(hx[:k])
+        buf[k:2 * k].copy_(hy[:k])
+        self._ar(buf[:2 * k])
+        hx[:k].copy_(buf[:k])
+        hy[:k].copy_(buf[k:2 * k])
 
     def dcgs_update(self, V, m, s, t, v, w, out, inv_alpha, gamma, nrm_out):
         self.b.dcgs_update(V, m, s, t, v, w, out, inv_alpha, gamma, None)
@@ -242,11 +358,21 @@ class DistVecOps:
 
 class PartitionedLdgSystem:
     """One rank's share of the LDG operator on its GPU: owned elements plus a
-    ghost layer, native fused passes, halo exchanges in between.
+    ghost layer, native fused passes, face-node halo exchanges in between.
 
-    ``exchange(arr)`` fills the ghost rows of an (owned + ghost, ...) array;
-    the default is the NCCL/gloo :class:`HaloExchanger`.  Vectors handed to
-    ``residual_dev`` / ``tangent_dev`` hold the owned elements only.
+    The owned vector is used in place: neighbour rows >= n_owned are read
+    from the ghost buffer ``u_ghost`` (``ldg_set_ghost_rows``), which holds
+    only the face nodes the cut faces read.  Per operator application
+    (``apply``), with [a, b) the owned elements that touch no ghost:
+
+      start u halo      | pass 1 on [a, b)        (overlapped)
+      wait; pass 1 on the rest
+      start export halo | pass 2 on [a, b)        (overlapped)
+      wait; pass 2 on the rest
+
+    ``exchanger=False`` leaves the halos to the caller (:class:`LocalBus`).
+    Vectors handed to ``residual_dev`` / ``tangent_dev`` hold the owned
+    elements only.
     """
 
     def __init__(self, model, mesh, topology, master, nranks, rank, device=None,
@@ -254,37 +380,79 @@ class PartitionedLdgSystem:
         import torch
         from .system import LdgSystem
         from .tables import TensorTables
+        from . import _lib as L
         gtab = tables if tables is not None else TensorTables(model, mesh, topology, master)
         self.plan = PartitionPlan(gtab, nranks, rank)
         self.local = LocalTables(gtab, self.plan)
         self.sys = LdgSystem(model, mesh, topology, master, device=device, tables=self.local)
         # exports stay in the producer's rows: those rows are what the halo
         # exchange ships to the ranks holding the element as a ghost
-        from . import _lib as L
         L.check(self.sys.lib.ldg_set_export_layout(self.sys._h, 0), "ldg_set_export_layout")
-        self.exchanger = exchanger if exchanger is not None else HaloExchanger(self.plan)
+        self.exchanger = exchanger if exchanger is not None else FaceHaloExchanger(self.plan)
         p = self.plan
         self.n_elements, self.n_nodes, self.ncu = p.ne_loc, master.n_nodes, model.ncu
         self.n_dofs = p.ne_loc * master.n_nodes * model.ncu
         self.kind, self.model, self.device = model.kind, model, self.sys.device
-        self.u_ext = torch.zeros((p.ne_loc + p.n_ghost, master.n_nodes, model.ncu),
-                                 dtype=torch.float64, device=self.sys.device)
+        self.u_ghost = torch.zeros((max(p.n_ghost, 1), master.n_nodes, model.ncu),
+                                   dtype=torch.float64, device=self.sys.device)
+        L.check(self.sys.lib.ldg_set_ghost_rows(self.sys._h, p.ne_loc, L.ptr(self.u_ghost)),
+                "ldg_set_ghost_rows")
         self.X = self.sys.scratch(rows=p.ne_loc + p.n_ghost)
+        self._xper = self.X.numel() // (p.ne_loc + p.n_ghost)
+
+    def x_rows(self):
+        """The export scratch viewed (rows * 2nd, nfn * ncu): one row per
+        element face slot."""
+        p = self.plan
+        return self.X[: (p.ne_loc + p.n_ghost) * self._xper].view(
+            (p.ne_loc + p.n_ghost) * p.nf, self._xper // p.nf)
+
+    def start_u_halo(self, u):
+        p = self.plan
+        return self.exchanger.start(u.reshape(p.ne_loc * p.nb, self.ncu),
+                                    self.u_ghost.view(-1, self.ncu), p.u_send, p.u_recv)
+
+    def start_x_halo(self):
+        xr = self.x_rows()
+        return self.exchanger.start(xr, xr, self.plan.x_send, self.plan.x_recv)
+
+    def _pass(self, which, u, tangent, t, R, e0, e1):
+        from . import _lib as L
+        if e1 <= e0:
+            return
+        g = None if tangent else self.sys.boundary_data(t)
+        b = None if tangent else self.sys.source_data(t)
+        L.check(self.sys.lib.ldg_operator_pass_range(
+            self.sys._h, which, int(bool(tangent)), L.ptr(u), L.ptr(g), L.ptr(b),
+            L.ptr(self.X), L.ptr(R), int(e0), int(e1), self.sys._stream()),
+            "ldg_operator_pass_range")
 
     def apply(self, u, tangent, t=0.0, out=None, exchange=True):
         p = self.plan
-        self.u_ext[:p.ne_loc].copy_(u.reshape(p.ne_loc, self.n_nodes, self.ncu))
-        if exchange:
-            self.exchanger.exchange(self.u_ext)
-        R = self.sys.operator_pass(1, self.u_ext, tangent, t, scratch=self.X, out=out)
-        if exchange:
-            self.exchange_exports()
-        return self.sys.operator_pass(2, self.u_ext, tangent, t, scratch=self.X, out=R)
+        u = u.reshape(p.ne_loc, self.n_nodes, self.ncu)
+        if not u.is_contiguous():
+            u = u.contiguous()
+        R = out if out is not None else self.sys._empty((p.ne_loc, self.n_nodes, self.ncu))
+        a, b = p.interior
+        if not exchange:                       # halos filled by the caller
+            self._pass(1, u, tangent, t, R, 0, p.ne_loc)
+            return R
+        pend = self.start_u_halo(u)
+        self._pass(1, u, tangent, t, R, a, b)
+        pend.wait()
+        self._pass(1, u, tangent, t, R, 0, a)
+        self._pass(1, u, tangent, t, R, b, p.ne_loc)
+        pend = self.start_x_halo()
+        self._pass(2, u, tangent, t, R, a, b)
+        pend.wait()
+        self._pass(2, u, tangent, t, R, 0, a)
+        self._pass(2, u, tangent, t, R, b, p.ne_loc)
+        return R
 
-    def exchange_exports(self):
-        p = self.plan
-        per = self.X.numel() // (p.ne_loc + p.n_ghost)
-        self.exchanger.exchange(self.X[: (p.ne_loc + p.n_ghost) * per].view(-1, per))
+    def complete(self, u, tangent, t=0.0, R=None):
+        """Pass 2 over all owned elements (after the caller's export halo)."""
+        self._pass(2, u, tangent, t, R, 0, self.plan.ne_loc)
+        return R
 
     def residual_dev(self, u, t=0.0, out=None):
         return self.apply(u, False, t, out)
@@ -297,13 +465,14 @@ class PartitionedLdgSystem:
 class LocalBus:
     """Single-process stand-in for the halo exchange among R partitions
     living on one GPU (partition and halo logic testable without
-    8 GPUs): ghost rows are copied device-to-device from the owners."""
+    8 GPUs): ghost rows (generated path) or ghost face nodes / export slots
+    (fused path, the same lists the NCCL exchanger ships) are copied
+    device-to-device from the owners."""
 
     def __init__(self, parts):
         self.parts = parts
 
     def fill(self, getter):
-        import torch
         for p in self.parts:
             plan = p.plan
             arr = getter(p)
@@ -312,19 +481,26 @@ class LocalBus:
                 q = int(plan.owner[g])
                 src = getter(self.parts[q])
                 flat[plan.ne_loc + k].copy_(src.reshape(src.shape[0], -1)[g - self.parts[q].plan.e0])
-        del torch
+
+    def _lists(self, srcs, dsts, send, recv):
+        import torch
+        for r, p in enumerate(self.parts):
+            for q, rows in getattr(p.plan, recv).items():
+                srows = getattr(self.parts[q].plan, send)[r]
+                dev = dsts[r].device
+                vals = srcs[q].index_select(0, torch.as_tensor(srows, device=dev))
+                dsts[r].index_copy_(0, torch.as_tensor(rows, device=dev), vals)
 
     def apply_all(self, us, tangent, t=0.0):
         """Operator on every partition in lockstep (pass 1 -> exports -> pass 2)."""
-        for p, u in zip(self.parts, us):
-            p.u_ext[:p.plan.ne_loc].copy_(u.reshape(p.plan.ne_loc, p.n_nodes, p.ncu))
-        self.fill(lambda p: p.u_ext)
-        Rs = [p.sys.operator_pass(1, p.u_ext, tangent, t, scratch=p.X) for p in self.parts]
-        per = [p.X.numel() // (p.plan.ne_loc + p.plan.n_ghost) for p in self.parts]
-        self.fill(lambda p: p.X[: (p.plan.ne_loc + p.plan.n_ghost) * per[self.parts.index(p)]]
-                  .view(-1, per[self.parts.index(p)]))
-        return [p.sys.operator_pass(2, p.u_ext, tangent, t, scratch=p.X, out=R)
-                for p, R in zip(self.parts, Rs)]
+        us = [u.reshape(p.plan.ne_loc, p.n_nodes, p.ncu).contiguous()
+              for p, u in zip(self.parts, us)]
+        self._lists([u.reshape(-1, p.ncu) for p, u in zip(self.parts, us)],
+                    [p.u_ghost.view(-1, p.ncu) for p in self.parts], "u_send", "u_recv")
+        Rs = [p.apply(u, tangent, t, exchange=False) for p, u in zip(self.parts, us)]
+        xs = [p.x_rows() for p in self.parts]
+        self._lists(xs, xs, "x_send", "x_recv")
+        return [p.complete(u, tangent, t, R) for p, u, R in zip(self.parts, us, Rs)]
 
 
 # ---------------------------------------------------------------------------
@@ -455,3 +631,70 @@ def nl_apply_all(parts, us, tangent, bases=None, t=0.0):
     dq = mixed(d, True)
     return [p.nl.tangent(a, b, t, q=q, dq=dd)[: p.plan.ne_loc]
             for p, a, b, q, dd in zip(parts, base, d, qb, dq)]
+
+
+# ---------------------------------------------------------------------------
+# distributed steady solve (fused linear path)
+# ---------------------------------------------------------------------------
+
+
+def block_jacobi_partitioned(psys, colors_global):
+    """Element block-Jacobi of one rank (solver.py:303-346 on the owned
+    blocks): the GLOBAL distance-2 colouring restricted to the owned
+    elements, every probe through the partitioned tangent WITH its halos.
+    (A rank-local probe is not enough: a ghost neighbour's face export
+    depends on the owned element's probe through the shared face's jump, and
+    that export is computed on the ghost's owner.)  All ranks run the same
+    number of colours and probes, so the halo exchanges pair up."""
+    import torch
+    from .solver import build_block_jacobi
+    p = psys.plan
+    colors = np.asarray(colors_global)[p.e0:p.e1]
+    ncol = int(np.max(colors_global)) + 1
+    x = torch.zeros(psys.n_dofs, dtype=torch.float64, device=psys.device)
+    shape = (psys.n_elements, psys.n_nodes, psys.ncu)
+    M = build_block_jacobi(lambda xb, v: psys.tangent_dev(v.reshape(shape)).reshape(-1), x,
+                           p.ne_loc, psys.n_nodes * psys.ncu, colors, all_colors=ncol)
+    torch.cuda.synchronize(psys.device)
+    return M
+
+
+def run_steady_partitioned(psys, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8,
+                           forcing=1e-8, restart=250, gmres_max_iter=6000, max_iter=20,
+                           orth="dcgs2", group=None):
+    """driver.run_steady on one rank of an element-partitioned system:
+    Newton-GMRES with allreduced Krylov reductions (DistVecOps), rank-local
+    block-Jacobi (global colouring), halos every operator application.
+    Returns (u owned, stats, timings)."""
+    import time
+    import torch
+    from .driver import DriverError
+    from .solver import NewtonOptions, distance2_coloring_topology, newton_solve, vecops
+    if psys.kind != "D" or not psys.model.is_steady():
+        raise DriverError("partitioned steady solves need a steady kind-D model")
+    t0 = time.perf_counter()
+    st = psys.sys.interpolate_initial()
+    shape = (psys.n_elements, psys.n_nodes, psys.ncu)
+    u0 = torch.as_tensor(np.ascontiguousarray(st.u), device=psys.device).reshape(-1)
+    ops = DistVecOps(vecops(psys.device), group)
+    torch.cuda.synchronize(psys.device)
+    t1 = time.perf_counter()
+    M = None
+    if precond == "block_jacobi":
+        tab = psys.local._g
+        colors = distance2_coloring_topology(tab.topo, tab.ne)
+        M = block_jacobi_partitioned(psys, colors)
+    elif precond not in ("identity", None):
+        raise DriverError(f"unsupported partitioned preconditioner {precond!r}")
+    t2 = time.perf_counter()
+    opts = NewtonOptions(abs_tol=abs_tol, rel_tol=rel_tol, max_iter=max_iter, forcing=forcing,
+                         gmres_restart=restart, gmres_max_iter=gmres_max_iter,
+                         jv_mode="tangent", orth=orth)
+    x, stats = newton_solve(lambda v: psys.residual_dev(v.reshape(shape)).reshape(-1), u0, opts,
+                            precond=M,
+                            tangent_fn=lambda xb, v: psys.tangent_dev(v.reshape(shape)).reshape(-1),
+                            ops=ops)
+    torch.cuda.synchronize(psys.device)
+    t3 = time.perf_counter()
+    return x.reshape(shape), stats, {"init_s": t1 - t0, "precond_build_s": t2 - t1,
+                                     "solve_s": t3 - t2}

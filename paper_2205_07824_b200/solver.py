@@ -695,14 +695,16 @@ def element_neighbor_sets(topology, n_elements):
 
 
 def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, perm=None,
-                       mode="tangent", residual_fn=None, base_residual=None):
+                       mode="tangent", residual_fn=None, base_residual=None, all_colors=None):
     """Exact diagonal blocks by coloured unit probes (solver.py:303-346):
     colours x bs device Jacobian-vector products (``mode`` "tangent" through
     ``tangent_fn``, "fd" through ``residual_fn`` like jacobian_vector), then
     batched Gauss-Jordan inverses with the reference's 1e-12 shift rule.
     ``native`` = (handle, scratch) runs a colour's probes in one C call
     (only for the handle's own linear tangent); ``perm`` maps element-major
-    block rows to packed indices (kind W / ODE systems)."""
+    block rows to packed indices (kind W / ODE systems).  ``all_colors``
+    (partitioned systems): probe colours 0..all_colors-1 even where this
+    rank owns no element of a colour, so the ranks' halo exchanges pair."""
     import torch
     lib = _lib.load()
     x, _ = _as_device(state)
@@ -726,7 +728,7 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, per
             return tangent_fn(x, vec)
         return jacobian_vector(residual_fn, x, vec, "fd", base_residual=R0)
 
-    for c in np.unique(colors):
+    for c in (np.unique(colors) if all_colors is None else range(all_colors)):
         members = torch.as_tensor(np.nonzero(colors == c)[0].astype(np.int32), device=dev)
         if native is not None and perm is None and mode == "tangent":
             # linear fused / dense operator: the colour's bs probes in one C call

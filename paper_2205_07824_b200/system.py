@@ -504,50 +504,70 @@ class LdgSystem:
             self._pipe = (starts, [int(d) for d in dep])
         return self._pipe
 
-    def _pinned_out(self, shape):
+    def _pinned_out(self, shape, as_numpy=False):
         """A pinned host result buffer.  Every call returns a new array as far
         as the caller can tell (disc.py returns fresh arrays): a pooled buffer
         is reused only once the pool holds its last reference, which avoids a
-        cudaHostAlloc (~60 ms for 80 MB) per call in a solver loop."""
+        cudaHostAlloc (~60 ms for 80 MB) per call in a solver loop.  With
+        as_numpy the pool holds (tensor, numpy view) pairs and the VIEW is
+        what the caller gets and what the reference count is taken of (a
+        view does not hold a reference to the tensor object)."""
         import sys
         import torch
-        pool = self._scratch.setdefault(("pinned_out", shape), [])
-        for buf in pool:
-            if sys.getrefcount(buf) <= 3:        # the pool list, `buf`, the argument
-                return buf
+        pool = self._scratch.setdefault(("pinned_out", shape, as_numpy), [])
+        for i in range(len(pool)):
+            obj = pool[i][1] if as_numpy else pool[i]
+            if sys.getrefcount(obj) <= 3:        # the pool entry, `obj`, the argument
+                return pool[i]
         buf = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        item = (buf, buf.numpy()) if as_numpy else buf
         if len(pool) < 4:
-            pool.append(buf)
-        return buf
+            pool.append(item)
+        return item
 
     def _host_pipeline(self, v, tangent, t):
-        """J v or R(v) for a CPU torch tensor v through ldg_apply_host: H2D of
-        the chunks on a copy stream, the two fused passes per chunk as soon as
+        """J v or R(v) for a host v through ldg_apply_host_staged: H2D of the
+        chunks on a copy stream, the two fused passes per chunk as soon as
         their neighbour rows have arrived, D2H of each finished chunk on a
         second copy stream (PCIe in both directions overlaps the kernels and
-        each other)."""
+        each other).  A pinned torch tensor is sent directly; a numpy array
+        (pageable, the reference's convention) is staged chunk by chunk into
+        a pinned buffer by the library's host threads, overlapped with the
+        transfers.  Returns a pinned torch tensor, or for numpy input a
+        numpy view of one (no extra host copy)."""
         import torch
         starts, dep = self._pipe_plan()
         shape = (self.n_elements, self.n_nodes, self.ncu)
-        vh = v.reshape(shape)
-        if not vh.is_pinned():
-            vh = vh.pin_memory()
-        vh = vh.contiguous()
+        is_np = isinstance(v, np.ndarray)
+        if is_np:
+            vh = np.ascontiguousarray(v, dtype=np.float64).reshape(shape)
+            src, stage = vh.ctypes.data, self._scratch.get(("stage", shape))
+            if stage is None:
+                stage = self._scratch[("stage", shape)] = torch.empty(
+                    shape, dtype=torch.float64, pin_memory=True)
+            stage_p = C.c_void_p(stage.data_ptr())
+        else:
+            vh = v.reshape(shape)
+            if not vh.is_pinned():
+                vh = vh.pin_memory()
+            vh = vh.contiguous()
+            src, stage_p = vh.data_ptr(), None
         key = ("pipe", shape)
         if key not in self._scratch:
             self._scratch[key] = (self._empty(shape), self._empty(shape),
                                   np.asarray(starts, dtype=np.int32),
                                   np.asarray(dep, dtype=np.int32))
         vd, R, st_, dp_ = self._scratch[key]
-        out = self._pinned_out(tuple(v.shape))     # returned as is (no view)
+        out = self._pinned_out(tuple(v.shape), as_numpy=is_np)
+        out, out_np = out if is_np else (out, None)
         g = None if tangent else self.boundary_data(t)
         b = None if tangent else self.source_data(t)
-        _lib.check(self.lib.ldg_apply_host(
-            self._h, int(bool(tangent)), C.c_void_p(vh.data_ptr()), C.c_void_p(out.data_ptr()),
+        _lib.check(self.lib.ldg_apply_host_staged(
+            self._h, int(bool(tangent)), C.c_void_p(src), stage_p, C.c_void_p(out.data_ptr()),
             _lib.ptr(vd), _lib.ptr(R), _lib.ptr(self.scratch()), _lib.ptr(g), _lib.ptr(b),
             len(dep), st_.ctypes.data_as(C.c_void_p), dp_.ctypes.data_as(C.c_void_p),
-            self._stream()), "ldg_apply_host")
-        return out
+            self._stream()), "ldg_apply_host_staged")
+        return out_np if is_np else out
 
     # -- reference-shaped API ------------------------------------------------------------------
     def _ret(self, x, origin):
@@ -574,8 +594,10 @@ class LdgSystem:
 
     def _pipelined(self, x):
         import torch
-        return (isinstance(x, torch.Tensor) and not x.is_cuda and self.nl is None
-                and not self.dense and getattr(self, "_h", None) is not None)
+        host = (isinstance(x, np.ndarray) and x.dtype == np.float64) or \
+            (isinstance(x, torch.Tensor) and not x.is_cuda)
+        return (host and self.nl is None and not self.dense
+                and getattr(self, "_h", None) is not None)
 
     def _packed_host(self, fn, state, *vecs):
         """Run a packed device operator on reference-shaped blocks; returns

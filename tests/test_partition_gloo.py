@@ -78,28 +78,33 @@ def _worker(rank, world, port, name, q, orth):
         sys.path.insert(0, os.path.dirname(__file__))
         import tensor_emulation as emu
         from cases import CASES, GOLDEN, b200_setup, build_case
-        from paper_2205_07824_b200.parallel import (DistVecOps, HaloExchanger, LocalTables,
+        from paper_2205_07824_b200.parallel import (DistVecOps, FaceHaloExchanger, LocalTables,
                                                     PartitionPlan)
         from paper_2205_07824_b200.tables import TensorTables
         g = np.load(GOLDEN / f"{name}.npz")
         tab = TensorTables(*build_case(CASES[name], *b200_setup()))
         plan = PartitionPlan(tab, world, rank)
         loc = LocalTables(tab, plan)
-        halo = HaloExchanger(plan)
+        halo = FaceHaloExchanger(plan)
         ne_ext = plan.ne_loc + plan.n_ghost
         nb, ncu = g["u"].shape[1:]
         gp = loc.boundary_projection(0.0)
         bs = loc.source_load(0.0)
 
         def apply(uvec, tangent):
+            # face-node halos: only the ghost face nodes the cut faces read
+            # are filled (the rest of u_ext's ghost rows stays zero) and only
+            # the export slot facing this rank; the result must still be exact
             u_ext = torch.zeros((ne_ext, nb, ncu), dtype=torch.float64)
             u_ext[:plan.ne_loc] = uvec.reshape(plan.ne_loc, nb, ncu)
-            halo.exchange(u_ext)
+            halo.start(u_ext[:plan.ne_loc].reshape(-1, ncu), u_ext[plan.ne_loc:].reshape(-1, ncu),
+                       plan.u_send, plan.u_recv).wait()
             R, X = emu.pass1(loc, u_ext.numpy(), tangent, None if tangent else gp,
                              None if tangent else bs)
             X_ext = torch.zeros((ne_ext,) + X.shape[1:], dtype=torch.float64)
             X_ext[:plan.ne_loc] = torch.as_tensor(X)
-            halo.exchange(X_ext)
+            xr = X_ext.reshape(ne_ext * X.shape[1], -1)
+            halo.start(xr, xr, plan.x_send, plan.x_recv).wait()
             return torch.as_tensor(emu.pass2(loc, X_ext.numpy(), R)).reshape(-1)
 
         e0, e1 = plan.e0, plan.e1
@@ -118,7 +123,7 @@ def _worker(rank, world, port, name, q, orth):
                                                                     dtype=torch.float64),
                              opts, tangent_fn=lambda x_, v: apply(v, True), ops=ops)
         q.put((rank, float(err), st.newton_iters, st.total_gmres_iters, e0, e1,
-               x.numpy().copy(), plan.n_ghost, sorted(plan.send), sorted(plan.recv)))
+               x.numpy().copy(), plan.n_ghost, sorted(plan.u_send), sorted(plan.u_recv)))
     finally:
         dist.destroy_process_group()
 
