@@ -286,6 +286,20 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
       for (int m = 0; m < n1; ++m) v += P.m1inv[r * n1 + m] * t->s1[m * n1 + c];
       P.g1[r * n1 + c] = v;
     }
+  for (int r = 0; r < n1; ++r) {
+    double gl = 0.0, gh = 0.0;
+    for (int m = 0; m < n1; ++m) {
+      gl += P.g1[r * n1 + m] * P.clo[m];
+      gh += P.g1[r * n1 + m] * P.chi[m];
+    }
+    P.gclo[r] = gl;
+    P.gchi[r] = gh;
+    for (int c = 0; c < n1; ++c) {
+      double v = 0.0;
+      for (int m = 0; m < n1; ++m) v += P.g1[r * n1 + m] * P.d1[m * n1 + c];
+      P.gd1[r * n1 + c] = v;
+    }
+  }
   *out = h;
   return 0;
 }

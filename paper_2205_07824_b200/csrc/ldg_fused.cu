@@ -659,7 +659,13 @@ constexpr int kES = 5;                       // padded stride of a thread's 4 fa
 // own u-plane slot between the u exchange and the T1 store.
 constexpr int kInSz = 96, kInC = 4 * kPS, kInF = kInC + 16;
 constexpr int kOffJ = 2 * kInSz, kOffF = kOffJ + 40, kOffE = kOffF + 40;
-constexpr int kPlanePer = kOffE + 4 * kPS;   // 340
+#ifndef LDG_PLANE_DMMA
+#define LDG_PLANE_DMMA 0          // A/B: z contractions on the FP64 tensor core (mma.sync m8n8k4):
+#endif                            // bit 0: R = M_z W, bit 1: D_z u and (G D)_z u
+// [340, 408): per-thread z volume term (DMMA variant, plane stride 17 like
+// the other planes: conflict-free), padded to 4 mod 16
+constexpr int kOffVZ = kOffE + 4 * kPS;
+constexpr int kPlanePer = (LDG_PLANE_DMMA & 2) ? kOffVZ + 4 * kPS + 12 : kOffE + 4 * kPS;   // 420 | 340
 static_assert(kInF + 12 <= kInSz, "layout");
 static_assert(kPlanePer % 16 == 4, "element stride must be 4 mod 16 doubles");
 // element regions of a warp: stride kPlanePer, elements 4..7 skewed by 2
@@ -696,6 +702,18 @@ __device__ __forceinline__ void axpy_plane(double (&acc)[16], double c, const do
   }
 }
 
+// D[8x8] = A[8x4] B[4x8] on the FP64 tensor core.  Plane mapping: lane
+// l = 4 slot + k supplies A[slot][k] = its plane-k value of one in-plane node
+// and B[k][c] (a per-lane operator constant); it receives D[slot][2k] and
+// D[slot][2k+1].  With B[m][2r + e] = Op_e[r][m] that is (Op_0 z u)[k] and
+// (Op_1 z u)[k] of its own plane: a z contraction of 8 elements in one
+// instruction, no shared-memory exchange.
+__device__ __forceinline__ void dmma_zplane(double& d0, double& d1, double a, double b) {
+  double c0 = 0.0, c1 = 0.0;
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
+      : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
 #ifndef LDG_PLANE_MINB
 #define LDG_PLANE_MINB 2          // 2 persistent blocks per SM (shared-memory bound)
 #endif
@@ -709,7 +727,7 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   constexpr int N1 = 4, NP = 16, NB = 64;
   extern __shared__ __align__(16) double psm[];
   __shared__ int s_map[kPlaneMaps * NP];
-  __shared__ double s_tab[4 * NP + 8];           // G, M^-1, M, D, clo, chi (rows picked by the plane index)
+  __shared__ double s_tab[5 * NP + 16];          // G, M^-1, M, D, clo, chi, GD, G clo, G chi
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = threadIdx.x >> 2, k = threadIdx.x & 3;
   const int ls = lane >> 2;                                // element slot within the warp
@@ -728,9 +746,19 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     for (int x = 0; x < 4; ++x) {
       s_tab[4 * NP + x] = P.clo[x];
       s_tab[4 * NP + 4 + x] = P.chi[x];
+      s_tab[5 * NP + 8 + x] = P.gclo[x];
+      s_tab[5 * NP + 12 + x] = P.gchi[x];
     }
+#pragma unroll
+    for (int x = 0; x < NP; ++x) s_tab[4 * NP + 8 + x] = P.gd1[x];
   }
   __syncthreads();
+  // per-lane B fragments of the z contractions: column c = lane / 4 =
+  // 2 r + e, row m = lane % 4 (see dmma_zplane); read where used
+  const int bc = (threadIdx.x & 31) >> 2, bm = threadIdx.x & 3;
+  const int bDG_at = ((bc & 1) ? 4 * NP + 8 : 3 * NP) + 4 * (bc >> 1) + bm;   // D | GD
+  const int bM_at = (bc & 1) ? -1 : 2 * NP + 4 * (bc >> 1) + bm;             // M | 0
+  (void)bDG_at; (void)bM_at;
   // let the completion kernel's blocks launch as SMs free up (they wait on
   // griddepcontrol.wait before touching R / X)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -850,16 +878,31 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
 
   // ---- B: d/dz from all four planes; z-face jumps / own-data flux, row j = k
   double up[NP], hz[NP];
+  constexpr bool ZMMA = (LDG_PLANE_DMMA & 2) && DIAG && !HAS_CU;
+  double* sVZ = sEl + kOffVZ + kPS * k;         // this thread's z volume term (ZMMA)
+  (void)sVZ;
 #pragma unroll
   for (int n = 0; n < NP; ++n) {
     up[n] = sU[k * kPS + n];
     hz[n] = 0.0;
   }
   static_assert(kPS == 17, "axpy_plane assumes the 17-double plane stride");
-  axpy_plane<0>(hz, s_tab[3 * NP + 4 * k + 0], sU + 0 * kPS);
-  axpy_plane<1>(hz, s_tab[3 * NP + 4 * k + 1], sU + 1 * kPS);
-  axpy_plane<2>(hz, s_tab[3 * NP + 4 * k + 2], sU + 2 * kPS);
-  axpy_plane<3>(hz, s_tab[3 * NP + 4 * k + 3], sU + 3 * kPS);
+  if constexpr (ZMMA) {
+    // hz = D_z u and gz = (G D)_z u of this plane in 16 tensor-core steps;
+    // gz waits in the thread's VZ slot (folded with the z lifts below)
+    const double bDG = s_tab[bDG_at];
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+      double gz;
+      dmma_zplane(hz[n], gz, up[n], bDG);
+      sVZ[n] = gz;
+    }
+  } else {
+    axpy_plane<0>(hz, s_tab[3 * NP + 4 * k + 0], sU + 0 * kPS);
+    axpy_plane<1>(hz, s_tab[3 * NP + 4 * k + 1], sU + 1 * kPS);
+    axpy_plane<2>(hz, s_tab[3 * NP + 4 * k + 2], sU + 2 * kPS);
+    axpy_plane<3>(hz, s_tab[3 * NP + 4 * k + 3], sU + 3 * kPS);
+  }
 #pragma unroll
   for (int f = 0; f < 2; ++f) {                 // faces 0 (z-, plane 0), 1 (z+, plane 3)
     const int kind = info[f] & LDG_FACE_KIND_MASK;
@@ -886,9 +929,21 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     // registers again until the flux combination, which keeps stage C spill-free
     const double clk = s_tab[4 * NP + k], chk = s_tab[4 * NP + 4 + k];
     const double c2 = DIAG ? sC[8] : 1.0;           // diagonal C: store F_z = C_zz h_z directly
+    if constexpr (ZMMA) {
+      // -G_z F_z = c_zz (gz + (G clo)_k jz_lo - (G chi)_k jz_hi): the z part
+      // of the volume term without a plane exchange
+      const double gl = s_tab[5 * NP + 8 + k], gh = s_tab[5 * NP + 12 + k];
 #pragma unroll
-    for (int n = 0; n < NP; ++n)
-      sT2[k * kPS + n] = c2 * (-hz[n] - clk * sJZ[(n >> 2) * kES + (n & 3)] + chk * sJZ[20 + (n >> 2) * kES + (n & 3)]);
+      for (int n = 0; n < NP; ++n) {
+        const double jl = sJZ[(n >> 2) * kES + (n & 3)], jh = sJZ[20 + (n >> 2) * kES + (n & 3)];
+        sT2[k * kPS + n] = c2 * (-hz[n] - clk * jl + chk * jh);
+        sVZ[n] = c2 * (sVZ[n] + gl * jl - gh * jh);
+      }
+    } else {
+#pragma unroll
+      for (int n = 0; n < NP; ++n)
+        sT2[k * kPS + n] = c2 * (-hz[n] - clk * sJZ[(n >> 2) * kES + (n & 3)] + chk * sJZ[20 + (n >> 2) * kES + (n & 3)]);
+    }
   }
   // ---- C: x / y faces at this plane and the in-plane gradients; the
   // own-data face fluxes go to the thread's (now dead) u-plane slot
@@ -1091,10 +1146,15 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     }
   {
     const double z0 = s_tab[NP + 4 * k], z3 = s_tab[NP + 4 * k + 3];
-    axpy_plane<0>(v, -s_tab[4 * k + 0], sT2 + 0 * kPS);
-    axpy_plane<1>(v, -s_tab[4 * k + 1], sT2 + 1 * kPS);
-    axpy_plane<2>(v, -s_tab[4 * k + 2], sT2 + 2 * kPS);
-    axpy_plane<3>(v, -s_tab[4 * k + 3], sT2 + 3 * kPS);
+    if constexpr (ZMMA) {
+#pragma unroll
+      for (int n = 0; n < NP; ++n) v[n] += sVZ[n];
+    } else {
+      axpy_plane<0>(v, -s_tab[4 * k + 0], sT2 + 0 * kPS);
+      axpy_plane<1>(v, -s_tab[4 * k + 1], sT2 + 1 * kPS);
+      axpy_plane<2>(v, -s_tab[4 * k + 2], sT2 + 2 * kPS);
+      axpy_plane<3>(v, -s_tab[4 * k + 3], sT2 + 3 * kPS);
+    }
 #pragma unroll
     for (int n = 0; n < NP; ++n)
       v[n] = fma(z0, sFZ[(n >> 2) * kES + (n & 3)], fma(z3, sFZ[20 + (n >> 2) * kES + (n & 3)], v[n]));
@@ -1140,18 +1200,28 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       v[(s ? 3 : 0) + 4 * a] += lx;
       v[a + 4 * (s ? 3 : 0)] += ly;
     }
-  // W over the thread's u-plane slot (its face fluxes are consumed above)
-#pragma unroll
-  for (int n = 0; n < NP; ++n) sU[k * kPS + n] = v[n];
-  __syncwarp();
   // ---- F: z contraction, source; R rows out through shared
   double out[NP];
+  if constexpr ((LDG_PLANE_DMMA & 1) != 0) {
+    // R = M_z W on the tensor core, straight from the registers
+    const double bM = bM_at < 0 ? 0.0 : s_tab[bM_at];
 #pragma unroll
-  for (int n = 0; n < NP; ++n) out[n] = 0.0;
-  axpy_plane<0>(out, s_tab[2 * NP + 4 * k + 0], sU + 0 * kPS);
-  axpy_plane<1>(out, s_tab[2 * NP + 4 * k + 1], sU + 1 * kPS);
-  axpy_plane<2>(out, s_tab[2 * NP + 4 * k + 2], sU + 2 * kPS);
-  axpy_plane<3>(out, s_tab[2 * NP + 4 * k + 3], sU + 3 * kPS);
+    for (int n = 0; n < NP; ++n) {
+      double unused;
+      dmma_zplane(out[n], unused, v[n], bM);
+    }
+  } else {
+    // W over the thread's u-plane slot (its face fluxes are consumed above)
+#pragma unroll
+    for (int n = 0; n < NP; ++n) sU[k * kPS + n] = v[n];
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < NP; ++n) out[n] = 0.0;
+    axpy_plane<0>(out, s_tab[2 * NP + 4 * k + 0], sU + 0 * kPS);
+    axpy_plane<1>(out, s_tab[2 * NP + 4 * k + 1], sU + 1 * kPS);
+    axpy_plane<2>(out, s_tab[2 * NP + 4 * k + 2], sU + 2 * kPS);
+    axpy_plane<3>(out, s_tab[2 * NP + 4 * k + 3], sU + 3 * kPS);
+  }
   if (active) {
     int hm = 0;
 #pragma unroll

@@ -40,6 +40,8 @@ struct TensorParams {
   double s1[LDG_MAX_N1 * LDG_MAX_N1];
   double m1inv[LDG_MAX_N1 * LDG_MAX_N1];
   double g1[LDG_MAX_N1 * LDG_MAX_N1];   // M1^-1 S1: S1 (x) M1 (x) M1 = (M1 (x) M1 (x) M1)(G1 (x) I (x) I)
+  double gd1[LDG_MAX_N1 * LDG_MAX_N1];  // G1 D1 (the volume term of -D u along one axis)
+  double gclo[LDG_MAX_N1], gchi[LDG_MAX_N1];   // G1 clo, G1 chi (the volume term of the lifts)
   int c_diag;            // every element's C block is diagonal (axis-aligned affine hexes)
   double clo[LDG_MAX_N1];
   double chi[LDG_MAX_N1];

@@ -132,7 +132,7 @@ def reference_switch(mesh, topo, master, geom, chunk=1 << 16):
             ho = mesh.ho_nodes[topo.elem_l[s]]
             if nd == 1:
                 raise DiscError("1D meshes are not supported by the B200 path")
-            tang = np.einsum("qgd,sd,kgc->kqcs", gd, T, ho)
+            tang = _tangents(gd, T, ho)
             if nd == 2:
                 t = tang[:, :, :, 0]
                 nv = np.stack([t[:, :, 1], -t[:, :, 0]], axis=-1)
@@ -146,6 +146,28 @@ def reference_switch(mesh, topo, master, geom, chunk=1 << 16):
     return (nbar @ beta) > 0.0
 
 
+def _tangents(gd, T, ho, rows=4096):
+    """np.einsum("qgd,sd,kgc->kqcs", gd, T, ho) -- the reference's own
+    face-tangent contraction, whose rounding decides the switch bit of
+    near-tie faces -- split over element rows on host threads (numpy's
+    einsum releases the GIL).  Every output row is the same einsum on the
+    same operands, so the result is bit-identical to the single call."""
+    k = ho.shape[0]
+    if k <= rows:
+        return np.einsum("qgd,sd,kgc->kqcs", gd, T, ho)
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+    out = np.empty((k, gd.shape[0], ho.shape[2], T.shape[0]))
+    starts = range(0, k, rows)
+
+    def run(a):
+        out[a:a + rows] = np.einsum("qgd,sd,kgc->kqcs", gd, T, ho[a:a + rows])
+
+    with ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1))) as ex:
+        list(ex.map(run, starts))
+    return out
+
+
 def _reference_switch_subset(mesh, master, geom, elems, lfs):
     """reference_switch restricted to the given (left element, face) list."""
     nd = mesh.nd
@@ -157,7 +179,7 @@ def _reference_switch_subset(mesh, master, geom, elems, lfs):
         gd = geom.eval_basis_grad(master.faces[lf].xi)
         _, T = face_map(mesh.elem_kind, lf)
         ho = mesh.ho_nodes[elems[sel]]
-        tang = np.einsum("qgd,sd,kgc->kqcs", gd, T, ho)
+        tang = _tangents(gd, T, ho)
         if nd == 2:
             t = tang[:, :, :, 0]
             nv = np.stack([t[:, :, 1], -t[:, :, 0]], axis=-1)
@@ -693,8 +715,8 @@ class DenseTables:
         tr = np.asarray(topo.translation, dtype=float)
         if tr.shape[0] != nfi:
             tr = np.zeros((nfi, self.nd))
-        o_l = self._orient(el, fl, er, fr, tr)
-        o_r = self._orient(er, fr, el, fl, -tr)
+        o_l = self._orient_fast(el, fl, er, fr, tr)
+        o_r = self._orient_fast(er, fr, el, fl, -tr)
         sw = self.switch.astype(np.int32)
         fnbr[el, fl] = er
         fnbr[er, fr] = el
@@ -748,7 +770,36 @@ class DenseTables:
     def face_points(self, elems, lf, pts=None):
         """Physical coordinates of face-lf quadrature points of elements."""
         xi = self.master.faces[lf].xi if pts is None else pts
-        return self.x0[elems][:, None, :] + np.einsum("edr,qr->eqd", self.J[elems], xi)
+        J = self.J[elems]                   # (e, d, r): one (e d) x r by r x q GEMM
+        e, d = J.shape[0], J.shape[1]
+        y = (J.reshape(e * d, -1) @ np.ascontiguousarray(xi.T)).reshape(e, d, -1)
+        return self.x0[elems][:, None, :] + y.transpose(0, 2, 1)
+
+    def _orient_fast(self, ea, fa, eb, fbb, shift):
+        """_orient from the shared vertex ids where the two faces share
+        their vertices (a conforming face: the permutation pi with
+        ids_b[pi[i]] = ids_a[i] is the one whose points land on this side's,
+        since both face maps are affine in the vertices); geometric matching
+        only for the rest (periodic faces, whose vertices are translates)."""
+        F = np.asarray(refelem.FACES[self.kind])
+        conn = np.asarray(self.mesh.connectivity)
+        nvf = F.shape[1]
+        out = np.full(ea.size, -1, dtype=np.int32)
+        if conn.shape[1] >= F.max() + 1 and ea.size:
+            ga = conn[ea[:, None], F[fa]]
+            gb = conn[eb[:, None], F[fbb]]
+            eq = ga[:, :, None] == gb[:, None, :]
+            ok = (eq.sum(axis=2) == 1).all(axis=1) & (eq.sum(axis=1) == 1).all(axis=1)
+            pi = eq.argmax(axis=2)
+            code = (pi * (nvf ** np.arange(nvf))).sum(axis=1)
+            lut = np.full(nvf ** nvf, -1, dtype=np.int32)
+            for o, p in enumerate(self.perms):
+                lut[int(sum(v * nvf ** i for i, v in enumerate(p)))] = o
+            out[ok] = lut[code[ok]]
+        rest = np.nonzero(out < 0)[0]
+        if rest.size:
+            out[rest] = self._orient(ea[rest], fa[rest], eb[rest], fbb[rest], shift[rest])
+        return out
 
     def _orient(self, ea, fa, eb, fbb, shift, chunk=1 << 15):
         n = ea.size

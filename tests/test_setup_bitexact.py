@@ -73,3 +73,26 @@ def test_mesh_topology_bitexact_vs_reference(kind, counts, per):
         for k in TOPO:
             assert np.array_equal(getattr(t1, k), getattr(t2, k)), k
         assert np.array_equal(np.array(t1.perm), np.array(t2.perm))
+
+
+def test_simplex_face_orientation_from_vertex_ids_matches_geometry():
+    """DenseTables._orient_fast (shared vertex ids, geometry only for
+    periodic faces) == the geometric point matching on every face."""
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.tables import DenseTables
+    root = GOLDEN
+    for kind, counts, per, p in (("tet", [5, 4, 3], None, 2), ("tri", [6, 5], None, 3),
+                                 ("tri", [4, 4], [(1, 2, (1.0, 0.0)), (3, 4, (0.0, 1.0))], 3),
+                                 ("tet", [3, 3, 3], [(1, 2, (1.0, 0.0, 0.0))], 2)):
+        nd = len(counts)
+        m = model.load_model(str(root / ("poisson3d.model" if nd == 3 else "poisson2d.model")))
+        mesh = meshgen.generate_structured([(0.0, 1.0)] * nd, counts, kind)
+        topo = meshgen.build_face_topology(mesh, per)
+        T = DenseTables(m, mesh, topo, refelem.build_master(kind, p))
+        el, fl, er, fr = (np.asarray(a, dtype=np.int64) for a in
+                          (topo.elem_l, topo.face_l, topo.elem_r, topo.face_r))
+        tr = np.asarray(topo.translation, dtype=float)
+        if tr.shape[0] != el.size:
+            tr = np.zeros((el.size, nd))
+        assert np.array_equal(T._orient(el, fl, er, fr, tr), T._orient_fast(el, fl, er, fr, tr))
+        assert np.array_equal(T._orient(er, fr, el, fl, -tr), T._orient_fast(er, fr, el, fl, -tr))
