@@ -227,6 +227,53 @@ ACCEPT_FLAGS = dict(abs_tol=1e-11, rel_tol=3e-8, forcing=1e-8, restart=250,
                     gmres_max_iter=6000)
 
 
+def warp_periodic(x, amp):
+    """A smooth map of the unit box onto itself, periodic in every direction
+    (translates of periodic faces stay translates): non-affine elements."""
+    y = x.copy()
+    nd = x.shape[-1]
+    for d in range(nd):
+        ph = np.ones(x.shape[:-1])
+        for k in range(nd):
+            if k != d:
+                ph = ph * np.sin(2 * np.pi * x[..., k])
+        y[..., d] = x[..., d] + amp * ph
+    return y
+
+
+def curved_mesh(spec, mesh_mod):
+    """Non-affine meshes.  With the reference's mesh module (golden
+    generation) they are built by its own generators -- the curved O-grid
+    annulus (mesh.py:216-273 + curve_boundary, mesh.py:695) or a periodic
+    warp of a p_geom structured box; otherwise (B200 side, GPU box) the
+    arrays stored in the golden file are loaded into this package's Mesh."""
+    c = spec["curved"]
+    if hasattr(mesh_mod, "curve_boundary"):
+        if c[0] == "annulus":
+            _, nt, nr, r0, r1, pg = c
+            m0 = mesh_mod.generate_annulus_ogrid(nt, nr, r0, r1, spec["kind"], p_geom=pg)
+            return mesh_mod.curve_boundary(m0, 1, mesh_mod.circle_projection((0.0, 0.0), r0))
+        _, pg, amp = c
+        nd = {"quad": 2, "hex": 3}[spec["kind"]]
+        m = mesh_mod.generate_structured([(0.0, 1.0)] * nd, spec["counts"], spec["kind"],
+                                         p_geom=pg)
+        m.ho_nodes = warp_periodic(m.ho_nodes, amp)
+        return m
+    g = np.load(GOLDEN / spec["mesh_file"])
+    return mesh_mod.Mesh(nd=int(g["mesh_nd"]), elem_kind=str(g["mesh_kind"]),
+                         vertices=g["mesh_vertices"], connectivity=g["mesh_connectivity"],
+                         p_geom=int(g["mesh_p_geom"]), ho_nodes=g["mesh_ho_nodes"],
+                         boundary_faces=g["mesh_boundary_faces"])
+
+
+def mesh_arrays(mesh):
+    return dict(mesh_nd=np.array(mesh.nd), mesh_kind=np.array(mesh.elem_kind),
+                mesh_vertices=np.asarray(mesh.vertices),
+                mesh_connectivity=np.asarray(mesh.connectivity),
+                mesh_p_geom=np.array(mesh.p_geom), mesh_ho_nodes=np.asarray(mesh.ho_nodes),
+                mesh_boundary_faces=np.asarray(mesh.boundary_faces))
+
+
 def build_case(spec, model_mod, mesh_mod, master_mod):
     """Return (model, mesh, topo, master) built with the given API modules."""
     src = spec["model"]
@@ -250,7 +297,10 @@ def build_case(spec, model_mod, mesh_mod, master_mod):
     kind = spec["kind"]
     nd = {"quad": 2, "tri": 2, "hex": 3, "tet": 3}[kind]
     dom = spec.get("domain", (0.0, 1.0))
-    mesh = mesh_mod.generate_structured([tuple(dom)] * nd, spec["counts"], kind)
+    if "curved" in spec:
+        mesh = curved_mesh(spec, mesh_mod)
+    else:
+        mesh = mesh_mod.generate_structured([tuple(dom)] * nd, spec["counts"], kind)
     per = BOX_PERIODIC[spec["periodic"]] if spec.get("periodic") else None
     if per is not None and dom != (0.0, 1.0):
         L = dom[1] - dom[0]
@@ -317,6 +367,29 @@ TRANSIENT_CASES.update({
         domain=(0.0, 2 * np.pi), init=TGV_INIT, stages=1, order=1, dt=0.05, steps=1,
         precond="mass", bj_apply=True),
 })
+
+# non-affine (curved) elements on the generated path: the shallow-water
+# free-stream known answer on the curved O-grid annulus (the reference's
+# acceptance criterion 6, on quads) and Euler 3D on a periodically warped
+# p_geom = 2 hex box; R at the free stream, R / J du / M y at a perturbed state
+CURVED_CASES = {
+    "curved_sw_annulus_quad_p3": dict(
+        model=("builtin", "shallow_water", 2, [2.0]), kind="quad", p=3,
+        curved=("annulus", 16, 4, 1.0, 3.0, 3), mesh_file="curved_sw_annulus_quad_p3.npz",
+        bcs={1: ("dirichlet", ["1.3", "0.4", "-0.2"]), 2: ("dirichlet", ["1.3", "0.4", "-0.2"])},
+        free=[1.3, 0.4, -0.2], state=([1.3, 0.4, -0.2], 0.05)),
+    "curved_euler_hex_warp_p2": dict(
+        model=("builtin", "euler", 3, None), kind="hex", counts=[3, 3, 3], p=2, periodic=3,
+        curved=("warp", 2, 0.04), mesh_file="curved_euler_hex_warp_p2.npz",
+        free=[1.0, 0.2, -0.1, 0.15, 2.5], state=([1.0, 0.2, -0.1, 0.15, 2.5], 0.05)),
+}
+
+# block-Jacobi of the steady closures on NS hex p=3 (320 x 320 blocks, beyond
+# the shared-memory Gauss-Jordan): build + apply only (bj_ns3d_hex_p3.npz)
+BJ_CASES = {
+    "bj_ns3d_hex_p3": dict(model=("file", "ns3d.model"), kind="hex", counts=[2, 2, 2], p=3,
+                           periodic=3, domain=(0.0, 2 * np.pi), init=TGV_INIT),
+}
 
 TRANSIENT_CASES.update({
     "wave2d_quad_p3_dirk22": dict(

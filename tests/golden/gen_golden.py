@@ -30,7 +30,8 @@ from ldgkit.driver import _steady_fns, build_pde_block_jacobi  # noqa: E402
 from ldgkit.solver import NewtonOptions  # noqa: E402
 from ldgkit.timeint import solve_steady  # noqa: E402
 
-from cases import (ACCEPT_FLAGS, CASES, MB_CASES, NL_CASES, SOLVE_CASES,  # noqa: E402
+from cases import (ACCEPT_FLAGS, BJ_CASES, CASES, CURVED_CASES, MB_CASES, NL_CASES,  # noqa: E402
+                   SOLVE_CASES, mesh_arrays,
                    TRANSIENT_CASES, TRANSIENT_FLAGS, build_case, case_state, seeded_state)
 
 
@@ -197,7 +198,46 @@ def gen_transient(name, spec):
     print("transient", name, newton, gm, float(np.abs(st.u).max()))
 
 
+def gen_curved(name, spec):
+    """Curved / non-affine meshes (disc.py:91-180 per-point geometry): the
+    mesh arrays, R at the free stream, R / J du / M y at a perturbed state."""
+    model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
+    s = LdgSystem(model, mesh, topo, master)
+    ne, nb, ncu = s.n_elements, s.n_nodes, s.ncu
+    uf = np.broadcast_to(np.asarray(spec["free"], dtype=float), (ne, nb, ncu)).copy()
+    u = case_state(spec, ne, nb, ncu, 1)
+    du = seeded_state(ne, nb, ncu, 0)
+    y = seeded_state(ne, nb, ncu, 2)
+    st = SolverState(u=u, q=None, w=None, t=0.0)
+    out = dict(u_free=uf, R_free=s.residual(SolverState(u=uf, q=None, w=None, t=0.0))[0],
+               u=u, du=du, y=y, R=s.residual(st)[0], Jdu=s.residual_tangent(st, du)[0],
+               M=s.mass_apply(st, y)[0], **mesh_arrays(mesh), **topo_arrays(s))
+    np.savez_compressed(HERE / spec["mesh_file"], **out)
+    print("curved", name, ne * nb * ncu, "free-stream |R|", float(np.abs(out["R_free"]).max()))
+
+
+def gen_bj(name, spec):
+    """The reference's block-Jacobi of the steady closures at the initial
+    state (driver.py:119-142, solver.py:303-346) applied to a seeded vector."""
+    model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
+    s = LdgSystem(model, mesh, topo, master)
+    s0 = s.interpolate_initial()
+    rf, tf = _steady_fns(s)
+    bj = build_pde_block_jacobi(s, rf, tf, s.pack(s0.u), "tangent")
+    r = np.random.default_rng(9).normal(size=s.n_dofs)
+    np.savez_compressed(HERE / f"{name}.npz", bj_r=r, bj_z=bj.apply(r))
+    print("bj", name, s.n_dofs)
+
+
 if __name__ == "__main__":
+    if "--curved-only" in sys.argv:
+        for n, sp in CURVED_CASES.items():
+            gen_curved(n, sp)
+        sys.exit(0)
+    if "--bj-only" in sys.argv:
+        for n, sp in BJ_CASES.items():
+            gen_bj(n, sp)
+        sys.exit(0)
     if "--nl-only" in sys.argv:
         for n, sp in NL_CASES.items():
             gen_nl_case(n, sp)
@@ -228,3 +268,7 @@ if __name__ == "__main__":
         gen_solve(n, sp)
     for n, sp in TRANSIENT_CASES.items():
         gen_transient(n, sp)
+    for n, sp in BJ_CASES.items():
+        gen_bj(n, sp)
+    for n, sp in CURVED_CASES.items():
+        gen_curved(n, sp)
