@@ -246,9 +246,14 @@ int ldg_bj_probe_vector(int64_t nblk, int bs, const int32_t* members,
 int ldg_bj_extract(int bs, const int32_t* members, int64_t n_members, int k,
                    const double* col, double* mats, void* stream);
 /* mats (nblk, bs, bs) row-major -> inv_t (nblk, bs, bs) holding inverse^T;
- * shifted (nblk) int flags: 1 where the 1e-12 shift rule fired. */
+ * shifted (nblk) int flags: 1 where the 1e-12 shift rule fired
+ * (solver.py:336-346: lu_factor, shift, lu_solve).  Any bs: blocks up to 160
+ * in shared memory, larger ones through ldg_bj_invert_global. */
 int ldg_bj_invert(int64_t nblk, int bs, const double* mats, double* inv_t,
                   int32_t* shifted, void* stream);
+/* the same Gauss-Jordan on a global (L2-resident) working copy, any bs */
+int ldg_bj_invert_global(int64_t nblk, int bs, const double* mats, double* inv_t,
+                         int32_t* shifted, void* stream);
 int ldg_bj_apply(int64_t nblk, int bs, const double* inv_t, const double* r,
                  double* z, void* stream);
 /* element blocks across a packed (u | q | w) vector (driver.py:128-142,

@@ -116,6 +116,8 @@ _SIGS = {
                         C.c_void_p], C.c_int),
     "ldg_bj_invert": ([C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
                       C.c_int),
+    "ldg_bj_invert_global": ([C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+                      C.c_int),
     "ldg_bj_apply": ([C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
                      C.c_int),
     "ldg_permute_gather": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],

@@ -10,6 +10,7 @@
 // stored transposed so the apply (a batched GEMV, HBM-bound on the block
 // matrices) reads it fully coalesced.
 
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "ldgb200.h"
@@ -158,6 +159,115 @@ invert_kernel(int bs, const double* __restrict__ mats, double* __restrict__ inv_
   }
 }
 
+// Blocks beyond the shared-memory limit (NS hex p=3: 320 x 320 = 800 KB):
+// the same Gauss-Jordan with partial pivoting, one CTA per block, on a
+// global (L2-resident) working copy W.  Per column: warp-0 pivot search (first
+// max, like idamax), row swap, pivot-row scaling, the rank-1 update with a
+// fixed column per thread (the multiplier A[r][c] is a warp broadcast, the
+// row segment is coalesced) and the pivot-column update.  Same pivots and
+// the same regularisation rule as invert_kernel.
+constexpr int kBigThreads = 512;
+
+__device__ bool gauss_jordan_global(double* A, int bs, int* perm, double thr, int* ipiv) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int c = 0; c < bs; ++c) {
+    if (threadIdx.x < 32) {
+      double best = -1.0;
+      int br = c;
+      for (int r = c + threadIdx.x; r < bs; r += 32) {
+        const double a = fabs(A[(size_t)r * bs + c]);
+        if (a > best) { best = a; br = r; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+        if (ob > best || (ob == best && orr < br)) { best = ob; br = orr; }
+      }
+      if (threadIdx.x == 0) *ipiv = br;
+    }
+    __syncthreads();
+    const int p = *ipiv;
+    if (threadIdx.x == 0) perm[c] = p;
+    if (p != c)
+      for (int k = threadIdx.x; k < bs; k += kBigThreads) {
+        const double t = A[(size_t)c * bs + k];
+        A[(size_t)c * bs + k] = A[(size_t)p * bs + k];
+        A[(size_t)p * bs + k] = t;
+      }
+    __syncthreads();
+    const double piv = A[(size_t)c * bs + c];
+    if (threadIdx.x == 0 && (!(fabs(piv) >= thr) || !isfinite(piv))) bad = 1;
+    const double inv = 1.0 / piv;
+    __syncthreads();
+    for (int k = threadIdx.x; k < bs; k += kBigThreads)
+      A[(size_t)c * bs + k] = (k == c) ? inv : A[(size_t)c * bs + k] * inv;
+    __syncthreads();
+    for (int k = threadIdx.x; k < bs; k += kBigThreads) {
+      if (k == c) continue;
+      const double ack = A[(size_t)c * bs + k];
+      for (int r = 0; r < bs; ++r)
+        if (r != c) A[(size_t)r * bs + k] = fma(-A[(size_t)r * bs + c], ack, A[(size_t)r * bs + k]);
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < bs; r += kBigThreads)
+      if (r != c) A[(size_t)r * bs + c] = -A[(size_t)r * bs + c] * inv;
+    __syncthreads();
+  }
+  for (int c = bs - 1; c >= 0; --c) {
+    const int p = perm[c];
+    if (p != c)
+      for (int r = threadIdx.x; r < bs; r += kBigThreads) {
+        const double t = A[(size_t)r * bs + c];
+        A[(size_t)r * bs + c] = A[(size_t)r * bs + p];
+        A[(size_t)r * bs + p] = t;
+      }
+    __syncthreads();
+  }
+  return bad == 0;
+}
+
+__global__ void __launch_bounds__(kBigThreads)
+invert_global_kernel(int bs, int64_t b0, const double* __restrict__ mats, double* __restrict__ work,
+                     double* __restrict__ inv_t, int32_t* __restrict__ shifted, int* __restrict__ perms) {
+  __shared__ double red[kBigThreads / 32];
+  __shared__ int ipiv;
+  const int64_t b = b0 + blockIdx.x;
+  const size_t n2 = (size_t)bs * bs;
+  const double* M = mats + b * n2;
+  double* A = work + blockIdx.x * n2;
+  int* perm = perms + (size_t)blockIdx.x * bs;
+  double amax = 0.0;
+  for (size_t t = threadIdx.x; t < n2; t += kBigThreads) {
+    A[t] = M[t];
+    amax = fmax(amax, fabs(A[t]));
+  }
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double r = threadIdx.x < kBigThreads / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if (threadIdx.x == 0) red[0] = r;
+  }
+  __syncthreads();
+  const double thr = 1e-14 * fmax(1.0, red[0]);
+  const bool ok = gauss_jordan_global(A, bs, perm, thr, &ipiv);
+  if (!ok) {
+    for (size_t t = threadIdx.x; t < n2; t += kBigThreads)
+      A[t] = M[t] + ((t / bs) == (t % bs) ? 1e-12 : 0.0);
+    __syncthreads();
+    gauss_jordan_global(A, bs, perm, 0.0, &ipiv);
+  }
+  if (threadIdx.x == 0 && shifted) shifted[b] = ok ? 0 : 1;
+  double* O = inv_t + b * n2;
+  for (size_t t = threadIdx.x; t < n2; t += kBigThreads) {
+    const size_t r = t / bs, c = t % bs;
+    O[c * bs + r] = A[t];
+  }
+}
+
 // z_b = inv_b r_b with inv stored transposed: thread i reads column i of
 // inv_t rows (coalesced), r_b from shared memory.
 __global__ void __launch_bounds__(256)
@@ -237,9 +347,37 @@ int ldg_bj_extract(int bs, const int32_t* members, int64_t nm, int k,
   return rc();
 }
 
+// global-memory Gauss-Jordan (any block size; ldg_bj_invert takes it for
+// blocks beyond the shared-memory limit), a bounded number of blocks at a
+// time so one wave's working copies stay L2-resident
+int ldg_bj_invert_global(int64_t nblk, int bs, const double* mats, double* inv_t,
+                         int32_t* shifted, void* stream) {
+  if (bs < 1 || nblk < 0) return 2;
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t chunk = std::min<int64_t>(nblk, 2 * (int64_t)nsm);
+  if (chunk <= 0) return 0;
+  double* work = nullptr;
+  int* perms = nullptr;
+  const size_t n2 = (size_t)bs * bs;
+  if (cudaMallocAsync(&work, chunk * n2 * sizeof(double), s) != cudaSuccess) return 3;
+  if (cudaMallocAsync(&perms, chunk * bs * sizeof(int), s) != cudaSuccess) return 3;
+  for (int64_t b0 = 0; b0 < nblk; b0 += chunk) {
+    const int64_t nb = std::min(chunk, nblk - b0);
+    invert_global_kernel<<<(unsigned)nb, kBigThreads, 0, s>>>(bs, b0, mats, work, inv_t,
+                                                              shifted, perms);
+  }
+  cudaFreeAsync(work, s);
+  cudaFreeAsync(perms, s);
+  return rc();
+}
+
 int ldg_bj_invert(int64_t nblk, int bs, const double* mats, double* inv_t,
                   int32_t* shifted, void* stream) {
-  if (bs > kMaxSmemBs) return 2;
+  if (bs < 1) return 2;
+  if (bs > kMaxSmemBs) return ldg_bj_invert_global(nblk, bs, mats, inv_t, shifted, stream);
   const size_t sm = (size_t)bs * bs * sizeof(double);
   if (sm > 48 * 1024)
     cudaFuncSetAttribute(invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

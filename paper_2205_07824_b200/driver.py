@@ -76,7 +76,7 @@ def elementwise_block_perm(system, device):
 
 
 def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="tangent",
-                           colors=None):
+                           colors=None, invert="auto"):
     """Exact per-element diagonal blocks via distance-2 coloured probing
     (driver.py:119-142), through the tangent or by finite differences
     (``jv_mode``), across the packed blocks of kind-W / ODE systems."""
@@ -89,7 +89,7 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
     if getattr(system, "multi_block", False):
         perm, bs = elementwise_block_perm(system, x.device)
         return build_block_jacobi(tangent_fn, x, system.n_elements, bs, colors, perm=perm,
-                                  mode=jv_mode, residual_fn=residual_fn)
+                                  mode=jv_mode, residual_fn=residual_fn, invert=invert)
     native = None
     if (jv_mode == "tangent" and type(system) is LdgSystem and system.nl is None
             and getattr(system, "_h", None) is not None
@@ -97,7 +97,7 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
         native = (system._h, system.scratch())        # the linear tangent ignores the base
     return build_block_jacobi(tangent_fn, x, system.n_elements,
                               system.n_nodes * system.ncu, colors, native=native,
-                              mode=jv_mode, residual_fn=residual_fn)
+                              mode=jv_mode, residual_fn=residual_fn, invert=invert)
 
 
 class CompositeManager:

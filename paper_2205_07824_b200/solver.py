@@ -695,7 +695,8 @@ def element_neighbor_sets(topology, n_elements):
 
 
 def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, perm=None,
-                       mode="tangent", residual_fn=None, base_residual=None, all_colors=None):
+                       mode="tangent", residual_fn=None, base_residual=None, all_colors=None,
+                       invert="auto"):
     """Exact diagonal blocks by coloured unit probes (solver.py:303-346):
     colours x bs device Jacobian-vector products (``mode`` "tangent" through
     ``tangent_fn``, "fd" through ``residual_fn`` like jacobian_vector), then
@@ -752,47 +753,18 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, per
                 col = ce
             _lib.check(lib.ldg_bj_extract(bs, _lib.ptr(members), members.numel(), k,
                                           _lib.ptr(col), _lib.ptr(mats), st), "extract")
-    if bs > BJ_SMEM_MAX_BS or os.environ.get("LDG_BJ_LIBRARY_LU"):
-        inv_t, shifted = _invert_large(mats)
-    else:
-        inv_t = torch.empty_like(mats)
-        shifted = torch.zeros(n_blocks, dtype=torch.int32, device=dev)
-        _lib.check(lib.ldg_bj_invert(n_blocks, bs, _lib.ptr(mats), _lib.ptr(inv_t),
-                                     _lib.ptr(shifted), st), "ldg_bj_invert")
+    inv_t = torch.empty_like(mats)
+    shifted = torch.zeros(n_blocks, dtype=torch.int32, device=dev)
+    # blocks <= 160 in shared memory, larger ones (NS hex p=3: 320) on an
+    # L2-resident global working copy; invert="global" forces the latter
+    fn = lib.ldg_bj_invert_global if invert == "global" else lib.ldg_bj_invert
+    _lib.check(fn(n_blocks, bs, _lib.ptr(mats), _lib.ptr(inv_t), _lib.ptr(shifted), st),
+               "ldg_bj_invert")
     del mats
     return BlockJacobiPreconditioner(inv_t, bs, shifted, perm=perm)
 
 
 BJ_SMEM_MAX_BS = 160            # ldg_bj_invert's in-shared-memory limit (bjacobi.cu)
-
-
-def _invert_large(mats, chunk=None):
-    """Blocks too large for the shared-memory Gauss-Jordan (e.g. NS hex
-    p=3: 320 x 320): batched LU with partial pivoting (cuSOLVER through
-    torch.linalg, the same pivoting as scipy.linalg.lu_factor), the
-    reference's regularisation rule on the U diagonal (|pivot| < 1e-14
-    max(1, max|A|) or non-finite -> A + 1e-12 I, solver.py:336-345), then the
-    inverse from the factors; stored transposed for ldg_bj_apply."""
-    import torch
-    nb, bs, _ = mats.shape
-    chunk = chunk or max(1, int(2e9 // (bs * bs * 8)))
-    inv_t = torch.empty_like(mats)
-    shifted = torch.zeros(nb, dtype=torch.int32, device=mats.device)
-    eye = torch.eye(bs, dtype=mats.dtype, device=mats.device)
-    for a in range(0, nb, chunk):
-        A = mats[a:a + chunk]
-        LU, piv, _ = torch.linalg.lu_factor_ex(A)
-        d = LU.diagonal(dim1=-2, dim2=-1)
-        thr = 1e-14 * torch.clamp(A.abs().amax(dim=(-2, -1)), min=1.0)
-        bad = ~((d.abs() >= thr[:, None]).all(dim=-1) & torch.isfinite(d).all(dim=-1))
-        if bool(bad.any()):
-            idx = torch.nonzero(bad).reshape(-1)
-            LU2, piv2, _ = torch.linalg.lu_factor_ex(A[idx] + 1e-12 * eye)
-            LU[idx], piv[idx] = LU2, piv2
-            shifted[a + idx] = 1
-        inv = torch.linalg.lu_solve(LU, piv, eye.expand(A.shape[0], bs, bs))
-        inv_t[a:a + chunk] = inv.transpose(-1, -2)
-    return inv_t, shifted
 
 
 # ---------------------------------------------------------------------------

@@ -265,21 +265,37 @@ def test_dirk_transient_matches_reference(name):
             assert rel(getattr(st, k).cpu().numpy(), g[k]) < 1e-9
 
 
-@pytest.mark.parametrize("library_lu", [False, True])
-def test_transient_block_jacobi_apply_matches_reference_ns3d(library_lu, monkeypatch):
+@pytest.mark.parametrize("invert", ["auto", "global"])
+def test_transient_block_jacobi_apply_matches_reference_ns3d(invert):
     """Block-Jacobi of the steady closures at the initial Taylor-Green state
     (driver.py:270-274, solver.py:303-346): 8 periodic hex p=2 elements, 5
     components, 135 x 135 blocks, applied to a seeded vector vs the
-    reference's own build + lu_solve.  library_lu: the batched-LU path of
-    blocks beyond the shared-memory Gauss-Jordan (bs > 160, NS hex p=3)."""
+    reference's own build + lu_solve.  invert="global": the global-memory
+    Gauss-Jordan of the blocks beyond the shared-memory limit."""
     import torch
-    if library_lu:
-        monkeypatch.setenv("LDG_BJ_LIBRARY_LU", "1")
     from cases import TRANSIENT_CASES
     from paper_2205_07824_b200.driver import _steady_fns, build_pde_block_jacobi
     from paper_2205_07824_b200.system import LdgSystem
     g = np.load(GOLDEN / "transient_ns3d_tgv_hex_p2_dirk11.npz")
     s = LdgSystem(*build_case(TRANSIENT_CASES["ns3d_tgv_hex_p2_dirk11"], *b200_setup()))
+    u0 = torch.as_tensor(s.interpolate_initial().u, device="cuda").reshape(-1)
+    rf, tf = _steady_fns(s)
+    M = build_pde_block_jacobi(s, rf, tf, u0, invert=invert)
+    z = M.apply(torch.as_tensor(g["bj_r"], device="cuda")).cpu().numpy()
+    assert rel(z, g["bj_z"]) < 1e-9, rel(z, g["bj_z"])
+
+
+def test_block_jacobi_320_blocks_match_reference_ns3d_hex_p3():
+    """NS hex p=3 (config 4's element): 320 x 320 blocks, beyond the
+    shared-memory Gauss-Jordan, inverted by the hand-written global-memory
+    kernel; applied to a seeded vector vs the reference's build + lu_solve."""
+    import torch
+    from cases import BJ_CASES
+    from paper_2205_07824_b200.driver import _steady_fns, build_pde_block_jacobi
+    from paper_2205_07824_b200.system import LdgSystem
+    g = np.load(GOLDEN / "bj_ns3d_hex_p3.npz")
+    s = LdgSystem(*build_case(BJ_CASES["bj_ns3d_hex_p3"], *b200_setup()))
+    assert s.n_nodes * s.ncu == 320
     u0 = torch.as_tensor(s.interpolate_initial().u, device="cuda").reshape(-1)
     rf, tf = _steady_fns(s)
     M = build_pde_block_jacobi(s, rf, tf, u0)
