@@ -66,7 +66,16 @@ struct NlParams {
   u64* bad;              // [0]: first element with a non-finite plan value
   int homog;             // nl_mixed: 1 = dual of a u^ override (kind-W tangent lift)
   int pad_;
+  // CURVED (non-affine elements, disc.py:91-180 per-point geometry):
+  const double* vgeo;    // (ne, NQ, 1 + ND*ND + ND): detJ, invjt[d][r], x at the volume points
+  const double* ffgeo;   // (ne, NFACE, NQF, 2 ND + 1): left normal, w |t1 x t2|, x per face point
+  const double* minv;    // (ne, NB, NB) inverse element mass matrices
 };
+#ifndef CURVED
+#define CURVED 0
+#endif
+constexpr int VG = 1 + ND * ND + ND;           // vgeo entries per volume point
+constexpr int FG = 2 * ND + 1;                 // ffgeo entries per face point
 
 __device__ __forceinline__ bool fin(double v) { return v - v == 0.0; }
 // (ldg_sign / ldg_min / ldg_max, used by the plans, come with the prelude)
@@ -622,15 +631,23 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
   double* vq;
   to_quad(bA, bB, NVA, tid, vq);
   double* gbuf = vq == bA ? bB : bA;
-  const double* geo = P.geo + (sz_t)e * (1 + ND * ND);
-  const double detj = geo[0];
+  const double* geo_e = P.geo + (sz_t)e * (1 + ND * ND);
   for (int p = tid; p < NQ; p += NT) {
     double val[NVA];
 #pragma unroll
     for (int v = 0; v < NVA; ++v) val[v] = vq[v * NQ + p];
-    double xi[ND], x[ND];
-    quad_point(p, xi);
-    phys_point(P, e, xi, x);
+    double x[ND];
+    // affine: one (detJ, invJ^T) per element and x = x0 + J xi; curved: per point
+    const double* geo = CURVED ? P.vgeo + ((sz_t)e * NQ + p) * VG : geo_e;
+    const double detj = geo[0];
+    if (CURVED) {
+#pragma unroll
+      for (int d = 0; d < ND; ++d) x[d] = geo[1 + ND * ND + d];
+    } else {
+      double xi[ND];
+      quad_point(p, xi);
+      phys_point(P, e, xi, x);
+    }
     double f[NCU * ND], df[NCU * ND], s[NCU], ds[NCU];
     const double* qv = NVQ ? val + NCU : nullptr;
     const double* wv = NW ? val + OW : nullptr;
@@ -708,11 +725,17 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
     const bool sw = info & 8;
     const int brow = P.fnbr[e * NFACE + lf];
     const double* fg = P.fgeo + ((sz_t)e * NFACE + lf) * (ND + 2);
+    const double* ff = CURVED ? P.ffgeo + (((sz_t)e * NFACE + lf) * NQF + s) * FG : fg;
     double n[ND];
 #pragma unroll
-    for (int d = 0; d < ND; ++d) n[d] = fg[d];
+    for (int d = 0; d < ND; ++d) n[d] = ff[d];
     double x[ND];
-    phys_point(P, e, &c_fxi[(lf * NQF + s) * ND], x);
+    if (CURVED) {
+#pragma unroll
+      for (int d = 0; d < ND; ++d) x[d] = ff[ND + 1 + d];
+    } else {
+      phys_point(P, e, &c_fxi[(lf * NQF + s) * ND], x);
+    }
     double vo[NVA], vn[NVA];
 #pragma unroll
     for (int v = 0; v < NVA; ++v) {
@@ -721,7 +744,7 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
     }
     double fh[NCU];
     face_flux<TANGENT>(P, e, kind, right, sw, brow, s, x, n, fg[ND + 1], vo, vn, fh);
-    const double w = c_fw[lf * NQF + s] * fg[ND] * (right ? -1.0 : 1.0);
+    const double w = (CURVED ? ff[ND] : c_fw[lf * NQF + s] * fg[ND]) * (right ? -1.0 : 1.0);
 #pragma unroll
     for (int c = 0; c < NCU; ++c) sF[(lf * NQF + s) * NCU + c] = w * fh[c];
   }
@@ -785,16 +808,21 @@ __device__ __forceinline__ void mass_body(const NlParams& P) {
   double* vq;
   to_quad(bA, bB, NL, tid, vq);
   double* fld = vq == bA ? bB : bA;
-  const double detj = P.geo[(sz_t)e * (1 + ND * ND)];
   for (int p = tid; p < NQ; p += NT) {
+    const double detj = CURVED ? P.vgeo[((sz_t)e * NQ + p) * VG] : P.geo[(sz_t)e * (1 + ND * ND)];
     double m[NCU], dm[NCU];
     if (MASS_CONST) {
 #pragma unroll
       for (int c = 0; c < NCU; ++c) { m[c] = c_mass[c]; dm[c] = 0.0; }
     } else {
       double xi[ND], x[ND], uq[NCU], duq[NCU];
-      quad_point(p, xi);
-      phys_point(P, e, xi, x);
+      if (CURVED) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) x[d] = P.vgeo[((sz_t)e * NQ + p) * VG + 1 + ND * ND + d];
+      } else {
+        quad_point(p, xi);
+        phys_point(P, e, xi, x);
+      }
 #pragma unroll
       for (int c = 0; c < NCU; ++c) {
         uq[c] = vq[(NCU + c) * NQ + p];
@@ -855,6 +883,17 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mass_inv(const __grid_consta
     bA[idx] = P.q[((sz_t)e * NB + a) * NCU + v];
   }
   __syncthreads();
+  if (CURVED) {
+    // non-affine: the element's own inverse mass matrix (disc.py:107-110)
+    const double* mi = P.minv + (sz_t)e * NB * NB;
+    for (int idx = tid; idx < NCU * NB; idx += NT) {
+      const int a = idx / NCU, c = idx % NCU;
+      double acc = 0.0;
+      for (int b = 0; b < NB; ++b) acc = fma(mi[a * NB + b], bA[c * NB + b], acc);
+      P.out[(sz_t)e * NB * NCU + idx] = P.scale * acc;
+    }
+    return;
+  }
   double* res;
   if (ND == 3) {
     contract_u<N1, N1, N1, 0, N1, N1, false, OP_M1INV>(bA, bB, NCU, tid);

@@ -46,7 +46,8 @@ class NlParams(C.Structure):
                 ("scale", C.c_double)] + [(k, C.c_void_p) for k in (
                     "geo", "xmap", "fnbr", "finfo", "fgeo", "nmap", "gq", "gproj",
                     "u", "q", "du", "dq", "w", "dw", "out", "bad")] + [
-                        ("homog", C.c_int32), ("pad_", C.c_int32)]
+                        ("homog", C.c_int32), ("pad_", C.c_int32)] + [(k, C.c_void_p) for k in (
+                            "vgeo", "ffgeo", "minv")]
 
 
 def linear_path_reason(model):
@@ -109,6 +110,56 @@ class NlTables(TensorTables):
         self.fgeo = fgeo
         tr = np.asarray(t.translation, dtype=float)
         self.periodic = tr.size > 0 and bool(np.any(tr != 0.0))
+        if self.curved:
+            self._curved_tables(el, fl, er, fr, tr)
+
+    def _curved_tables(self, el, fl, er, fr, tr):
+        """Per-point geometry of non-affine elements for the CURVED kernels:
+          vgeo  (ne, NQ, 1 + nd^2 + nd): detJ, invJ^T, x at the volume points
+          ffgeo (ne, nf, NQF, 2 nd + 1): per face point (kernel order) the
+                LEFT element's unit normal, weight x |t1 x t2| and x at the
+                physically matching left point -- both sides of an interior
+                face evaluate f^ on bitwise identical inputs, as the
+                reference's scatter of +/- one value (disc.py:641-653)
+          minv  (ne, nb, nb): inverse element mass matrices (disc.py:107-110)."""
+        m, nd, ne, nf = self.master, self.nd, self.ne, self.nf
+        if self.model.kind != "C" or self.model.nw > 0:
+            raise DiscError("curved elements are supported for kind C models without "
+                            "ODE blocks on the B200 path (the mixed gradient's collocation "
+                            "identities need affine elements)")
+        self.vgeo = np.concatenate([self.detj_q[..., None], self.invjt_q.reshape(ne, -1, nd * nd),
+                                    self.xq_q], axis=2)
+        nqf = self.fxi.shape[1]
+        ffgeo = np.zeros((ne, nf, nqf, 2 * nd + 1))
+
+        def pack(x, n, mag, lf):
+            return np.concatenate([n, (self.fw[lf][None, :] * mag)[..., None], x], axis=2)
+
+        scale2 = (1e-9 * max(self.mesh.diameter(), 1.0)) ** 2
+        for lf in range(nf):
+            sel = np.nonzero(fl == lf)[0]
+            if sel.size:
+                x, n, mag = self.face_point_geometry(el[sel], lf, self.fxi[lf])
+                ffgeo[el[sel], lf] = pack(x, n, mag, lf)
+        for lf in range(nf):
+            sel = np.nonzero(fr == lf)[0]
+            if sel.size == 0:
+                continue
+            xr, _, _ = self.face_point_geometry(er[sel], lf, self.fxi[lf])
+            left = ffgeo[el[sel], fl[sel]]                      # (k, nqf, 2nd+1)
+            xl = left[..., nd + 1:] + (tr[sel][:, None, :] if tr.shape[0] == el.size else 0.0)
+            d2 = ((xr[:, :, None, :] - xl[:, None, :, :]) ** 2).sum(axis=-1)
+            j = d2.argmin(axis=2)
+            if np.take_along_axis(d2, j[..., None], axis=2).max() > scale2:
+                raise DiscError("curved face points do not match across an interior face")
+            ffgeo[er[sel], lf] = np.take_along_axis(left, j[..., None], axis=1)
+        for lf in range(nf):
+            s_ = np.nonzero(self.fb == lf)[0]
+            if s_.size:
+                x, n, mag = self.face_point_geometry(self.eb[s_], lf, self.fxi[lf])
+                ffgeo[self.eb[s_], lf] = pack(x, n, mag, lf)
+        self.ffgeo = ffgeo
+        self.minv = np.linalg.inv(np.einsum("eq,qa,qb->eab", self.wdetj_q, m.phi, m.phi))
 
     def _check_quadrature(self):
         """The reference's volume rule is the tensor Gauss rule (x fastest)
@@ -162,11 +213,17 @@ class NlTables(TensorTables):
                 if s.size == 0:
                     continue
                 e = self.eb[s]
-                xq = self.x0[e][:, None, :] + np.einsum("edr,qr->eqd", self.J[e], self.fxi[lf])
+                if self.curved:
+                    ff = self.ffgeo[e, lf]
+                    xq, nq = ff[..., self.nd + 1:], ff[..., :self.nd]
+                else:
+                    xq = self.x0[e][:, None, :] + np.einsum("edr,qr->eqd", self.J[e],
+                                                            self.fxi[lf])
+                    nq = np.repeat(self.n_bnd[s][:, None, :], nqf, axis=1)
                 b = {"t": float(t), **mu}
                 for k in range(self.nd):
                     b[f"x{k + 1}"] = xq[..., k].ravel()
-                    b[f"n{k + 1}"] = np.repeat(self.n_bnd[s, k], nqf)
+                    b[f"n{k + 1}"] = nq[..., k].ravel()
                 g = evaluate(plan, b)
                 if g.shape[1] != s.size * nqf:
                     g = np.broadcast_to(g, (g.shape[0], s.size * nqf))
@@ -235,7 +292,7 @@ def generate_source(tab):
                 HAS_WS=int(ws is not None), TRACE_CENTERED=int(model.numflux.trace == "centered"),
                 GRAD_CENTERED=int(model.numflux.grad_trace == "centered"),
                 HAS_UHAT=int(uhat is not None), HAS_FHAT=int(fhat is not None),
-                MASS_CONST=int(mass_const), NT=nt)
+                MASS_CONST=int(mass_const), NT=nt, CURVED=int(bool(getattr(tab, "curved", False))))
     lines = ["// generated by paper_2205_07824_b200/nonlinear.py -- do not edit"]
     lines += [f"#define {k} {v}" for k, v in defs.items()]
     mc = np.zeros(ncu)
@@ -313,6 +370,10 @@ class NlOperator:
         self.finfo = dev(tab.finfo, np.int32)
         self.fgeo = dev(tab.fgeo, np.float64)
         self.nmap = dev(tab.nmap, np.int32)
+        curved = getattr(tab, "curved", False)
+        self.vgeo = dev(tab.vgeo, np.float64) if curved else None
+        self.ffgeo = dev(tab.ffgeo, np.float64) if curved else None
+        self.minv = dev(tab.minv, np.float64) if curved else None
         self.bad = torch.full((1,), -1, dtype=torch.int64, device=device)
         self._bq, self._bp = {}, {}
         s = self.shape
@@ -371,6 +432,9 @@ class NlOperator:
         P.ne, P.nbface, P.t, P.scale = self.tab.ne, self.tab.n_boundary, float(t), float(scale)
         for k in ("geo", "xmap", "fnbr", "finfo", "fgeo", "nmap"):
             setattr(P, k, getattr(self, k).data_ptr())
+        for k in ("vgeo", "ffgeo", "minv"):
+            v = getattr(self, k)
+            setattr(P, k, None if v is None else v.data_ptr())
         P.bad = self.bad.data_ptr()
         for k, v in ptrs.items():
             setattr(P, k, None if v is None else v.data_ptr())

@@ -70,20 +70,28 @@ class _Disc:
 
     @property
     def wdetj(self):
+        if getattr(self._t, "curved", False):
+            return self._t.wdetj_q
         return self._t.detj[:, None] * self._t.master.quad_wts[None, :]
 
     @property
     def xq(self):
         t = self._t
+        if getattr(t, "curved", False):
+            return t.xq_q
         return t.x0[:, None, :] + np.einsum("edr,qr->eqd", t.J, t.master.quad_pts)
 
     @property
     def detj(self):
+        if getattr(self._t, "curved", False):
+            return self._t.detj_q
         return np.repeat(self._t.detj[:, None], self._t.master.quad_pts.shape[0], axis=1)
 
     @property
     def mass_inv(self):
         t = self._t
+        if getattr(t, "curved", False):
+            return t.minv
         if hasattr(t, "minv"):                      # simplex: M_e = detJ M_ref
             return t.minv[None, :, :] / t.detj[:, None, None]
         mi = t.m1inv

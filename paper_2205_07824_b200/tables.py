@@ -277,10 +277,17 @@ class TensorTables:
         gd = geom.eval_basis_grad(corners)                    # (nv, ng, nd)
         J = np.einsum("egd,vgr->evdr", mesh.ho_nodes, gd)
         scale = max(mesh.diameter(), 1.0)
-        if np.max(np.abs(J - J[:, :1])) > 1e-11 * scale:
-            raise DiscError("B200 tensor path needs affine elements (curved or "
-                            "non-parallelepiped elements are not supported yet)")
-        J = J[:, 0]
+        self.curved = bool(np.max(np.abs(J - J[:, :1])) > 1e-11 * scale)
+        if self.curved:
+            if not self.nonlinear:
+                raise DiscError("curved (non-affine) elements run on the generated path only")
+            self._curved_geometry(geom)
+            # element-level affine stand-ins (the Jacobian at the reference
+            # centre): only the table builders' approximate uses read them
+            J = np.einsum("egd,gr->edr", mesh.ho_nodes,
+                          geom.eval_basis_grad(np.zeros((1, nd)))[0])
+        else:
+            J = J[:, 0]
         self.detj = np.linalg.det(J)
         if np.any(self.detj <= 0):
             bad = int(np.argmax(self.detj <= 0))
@@ -291,13 +298,56 @@ class TensorTables:
         self.J = J
         self.geo = np.concatenate([self.detj[:, None], self.invjt.reshape(self.ne, -1)], axis=1)
         m = self.master
-        self.elem_vol = self.detj * m.quad_wts.sum()
+        self.elem_vol = self.wdetj_q.sum(axis=1) if self.curved else self.detj * m.quad_wts.sum()
+
+    def _curved_geometry(self, geom):
+        """Per-quadrature-point metrics of non-affine elements, the
+        reference's own pipeline (disc.py:91-104): J = sum_g x_g grad N_g at
+        the volume points, detJ, invJ^T, the weighted detJ and the physical
+        points; per-face-point normals / weighted surface jacobians follow
+        in face_point_geometry (disc.py:139-180)."""
+        mesh, m = self.mesh, self.master
+        ho = mesh.ho_nodes
+        gphi = geom.eval_basis(m.quad_pts)
+        gdphi = geom.eval_basis_grad(m.quad_pts)
+        Jq = np.einsum("egd,qgr->eqdr", ho, gdphi)
+        detj = np.linalg.det(Jq)
+        if np.any(detj <= 0):
+            bad = int(np.argwhere(detj.min(axis=1) <= 0)[0][0])
+            raise DiscError(f"nonpositive Jacobian in element {bad}")
+        self.detj_q = detj
+        self.invjt_q = np.linalg.inv(Jq).transpose(0, 1, 3, 2)
+        self.wdetj_q = m.quad_wts[None, :] * detj
+        self.xq_q = np.einsum("qg,egd->eqd", gphi, ho)
+
+    def face_point_geometry(self, elems, lf, xi=None):
+        """(x, unit normal, |t1 x t2| without the weight) at reference face
+        points xi (default: the master's face rule) of local face lf -- the
+        reference's face pipeline (disc.py:139-180: tangents
+        dx/dsigma = grad N . T, n = t1 x t2 / |t1 x t2|)."""
+        geom = self.geom_master
+        xi = self.master.faces[lf].xi if xi is None else xi
+        ho = self.mesh.ho_nodes[elems]
+        x = np.einsum("qg,kgd->kqd", geom.eval_basis(xi), ho)
+        _, T = face_map(self.master.kind, lf)
+        tang = _tangents(geom.eval_basis_grad(xi), T, ho)
+        if self.nd == 2:
+            t = tang[:, :, :, 0]
+            nv = np.stack([t[:, :, 1], -t[:, :, 0]], axis=-1)
+        else:
+            nv = np.cross(tang[:, :, :, 0], tang[:, :, :, 1])
+        mag = np.linalg.norm(nv, axis=-1)
+        return x, nv / mag[:, :, None], mag
 
     def node_coords(self, elems=None, nodes=None):
-        """Physical coordinates of solution nodes (affine map)."""
+        """Physical coordinates of solution nodes (the geometry map; affine:
+        x0 + J xi)."""
         m = self.master
         xi = m.nodes if nodes is None else m.nodes[nodes]
         e = slice(None) if elems is None else elems
+        if getattr(self, "curved", False):
+            ho = self.mesh.ho_nodes[e]
+            return np.einsum("ng,egd->end", self.geom_master.eval_basis(xi), ho)
         return self.x0[e][:, None, :] + np.einsum("edr,nr->end", self.J[e], xi)
 
     def _flux_coefficients(self):
@@ -352,7 +402,14 @@ class TensorTables:
         return a + n1 * b + n1 * n1 * io
 
     def face_normal_area(self, elems, lf):
-        """Outward unit normal and |t1 x t2| of local face lf (affine)."""
+        """Outward unit normal and |t1 x t2| of local face lf (affine; for
+        curved elements the face-rule average normal and the area over the
+        reference face measure, for the per-face quantities only)."""
+        if getattr(self, "curved", False):
+            _, n, mag = self.face_point_geometry(elems, lf)
+            w = self.master.faces[lf].weights
+            nb = n.mean(axis=1)
+            return nb / np.linalg.norm(nb, axis=1)[:, None], (mag * w).sum(axis=1) / w.sum()
         _, T = face_map(self.master.kind, lf)
         tn = np.cross(T[0], T[1]) if self.nd == 3 else np.array([T[0][1], -T[0][0]])
         v = np.einsum("edr,r->ed", self.invjt[elems], tn)
@@ -459,6 +516,9 @@ class TensorTables:
         nfi = el.size
         if nfi == 0:
             return np.zeros(0, dtype=bool)
+        if getattr(self, "curved", False):
+            # non-affine faces: the reference's own normal-average pipeline
+            return _reference_switch_subset(self.mesh, self.master, self.geom_master, el, fl)
         n = np.zeros((nfi, self.nd))
         for lf in range(self.nf):
             sel = np.nonzero(fl == lf)[0]

@@ -11,7 +11,7 @@ pow / tanh subgradient rules, switch and centered traces."""
 import numpy as np
 import pytest
 
-from cases import GOLDEN, NL_CASES, b200_setup, build_case, case_state
+from cases import CURVED_CASES, GOLDEN, NL_CASES, b200_setup, build_case, case_state
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
@@ -205,3 +205,43 @@ def test_partitioned_generated_operator_two_ranks_gloo(tmp_path):
     J = np.concatenate([np.load(f"{out}_{r}.npz")["J"] for r in range(2)])
     assert rel(R, g["R"]) < TOL
     assert rel(J, g["Jdu"]) < TOL
+
+
+@pytest.mark.parametrize("name", sorted(CURVED_CASES))
+def test_curved_elements_vs_reference_golden(name):
+    """Non-affine elements (per-point metrics, disc.py:91-180) on the
+    generated path vs the unmodified reference on the same mesh: the curved
+    O-grid annulus (shallow water, Dirichlet, the reference's acceptance
+    criterion 6 on quads) and a periodically warped p_geom = 2 hex box
+    (Euler).  Topology and switch bits bit-exact; the free-stream residual
+    vanishes like the reference's (<= 1e-10, criterion 6's bar; the
+    reference reaches ~6e-15); R, J du and M y at a perturbed state to 1e-12."""
+    from paper_2205_07824_b200.system import LdgSystem, SolverState
+    spec = CURVED_CASES[name]
+    g = np.load(GOLDEN / spec["mesh_file"])
+    model, mesh, topo, master = build_case(spec, *b200_setup())
+    s = LdgSystem(model, mesh, topo, master)
+    assert s.tab.curved
+    assert np.array_equal(np.asarray(topo.elem_l), g["elem_l"])
+    assert np.array_equal(s.tab.switch, g["switch"])
+    Rf = s.residual(SolverState(u=g["u_free"], q=None, w=None, t=0.0))[0]
+    assert np.abs(Rf).max() <= 1e-10, np.abs(Rf).max()
+    st = SolverState(u=g["u"], q=None, w=None, t=0.0)
+    assert rel(s.residual(st)[0], g["R"]) < TOL
+    assert rel(s.residual_tangent(st, g["du"])[0], g["Jdu"]) < TOL
+    assert rel(s.mass_apply(st, g["y"])[0], g["M"]) < TOL
+
+
+def test_curved_mass_inverse_roundtrip():
+    """MassPreconditioner on curved elements: the per-element inverse mass
+    (disc.py:107-110) undoes mass_apply."""
+    import torch
+    from paper_2205_07824_b200.driver import MassPreconditioner
+    from paper_2205_07824_b200.system import LdgSystem
+    spec = CURVED_CASES["curved_sw_annulus_quad_p3"]
+    s = LdgSystem(*build_case(spec, *b200_setup()))
+    y = torch.as_tensor(np.random.default_rng(3).normal(size=(s.n_elements, s.n_nodes, s.ncu)),
+                        device="cuda")
+    My = s.mass_apply_dev(y)
+    back = MassPreconditioner(s).apply(My.reshape(-1)).reshape(y.shape)
+    assert float(torch.linalg.vector_norm(back - y) / torch.linalg.vector_norm(y)) < 1e-12
