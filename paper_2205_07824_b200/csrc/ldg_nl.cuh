@@ -357,6 +357,182 @@ nl_mixed(const __grid_constant__ NlParams P) {
 }
 
 // ---------------------------------------------------------------------------
+// mixed gradient on CURVED elements (kind D): the reference's quadrature
+// form (disc.py:436-490) -- the GLL collocation identities of nl_mixed need
+// affine elements:
+//   rhs_a[i][j] = -sum_q w detJ (invJ^T grad u_i)_j phi_a
+//                 + sum_faces sum_s wsj (u_i - u^_i) n_j phi_a,   q = M_e^-1 rhs
+// one element per block; u^ by the trace rules at the face points (switch /
+// centered, Dirichlet data at the face points, Neumann u^ = u).
+// ---------------------------------------------------------------------------
+constexpr int NGQ = NCU * ND;                  // gradient fields [c][j]
+constexpr int MCS_BUF = (NGQ > NCU ? NGQ : NCU) * MX;
+constexpr int MCS_SMEM = NCU * NB + 3 * MCS_BUF + NGQ * NB + 2 * NFACE * NCU * NQF +
+                         4 * NCU * MXF + NFACE * NQF * NGQ;
+
+template <int R>
+__device__ __forceinline__ void grad_dir(const double* su, double* a, double* b, double* out,
+                                         int tid) {
+  // d/dxi_R at the volume points: dphi along R, phi along the other axes
+  if (ND == 3) {
+    contract_u<N1, N1, N1, 0, N1, NQ1, false, R == 0 ? OP_DPHI : OP_PHI>(su, a, NCU, tid);
+    __syncthreads();
+    contract_u<NQ1, N1, N1, 1, N1, NQ1, false, R == 1 ? OP_DPHI : OP_PHI>(a, b, NCU, tid);
+    __syncthreads();
+    contract_u<NQ1, NQ1, N1, 2, N1, NQ1, false, R == 2 ? OP_DPHI : OP_PHI>(b, out, NCU, tid);
+  } else {
+    contract_u<N1, N1, 1, 0, N1, NQ1, false, R == 0 ? OP_DPHI : OP_PHI>(su, a, NCU, tid);
+    __syncthreads();
+    contract_u<NQ1, N1, 1, 1, N1, NQ1, false, R == 1 ? OP_DPHI : OP_PHI>(a, out, NCU, tid);
+  }
+  __syncthreads();
+}
+
+extern "C" __global__ void __launch_bounds__(NT) nl_mixed_curved(const __grid_constant__ NlParams P) {
+  extern __shared__ __align__(16) double smc[];
+  double* su = smc;                            // [c][node]
+  double* bA = su + NCU * NB;
+  double* bB = bA + MCS_BUF;
+  double* G = bB + MCS_BUF;                    // [r][c][q] reference derivatives, then fields
+  double* rhs = G + MCS_BUF;                   // [c j][node]
+  double* TR = rhs + NGQ * NB;                 // [side][face][c][NQF]
+  double* FN = TR + 2 * NFACE * NCU * NQF;     // face nodes own | nbr [c][NFN], stage scratch
+  double* FJ = FN + 4 * NCU * MXF;             // [face][s][c j]
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (e >= P.ne) return;
+  for (int idx = tid; idx < NCU * NB; idx += NT) {
+    const int c = idx / NB, a = idx % NB;
+    su[idx] = P.u[((sz_t)e * NB + a) * NCU + c];
+  }
+  __syncthreads();
+  // ---- volume: grad u at the points, -w detJ invJ^T grad u, phi^T back
+  grad_dir<0>(su, bA, bB, G + 0 * NCU * NQ, tid);
+  grad_dir<1>(su, bA, bB, G + 1 * NCU * NQ, tid);
+  if (ND == 3) grad_dir<2>(su, bA, bB, G + 2 * NCU * NQ, tid);
+  for (int p = tid; p < NQ; p += NT) {
+    const double* gp = P.vgeo + ((sz_t)e * NQ + p) * VG;
+    const double wd = c_qw[p] * gp[0];
+    double gr[ND][NCU];
+#pragma unroll
+    for (int r = 0; r < ND; ++r)
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) gr[r][c] = G[(r * NCU + c) * NQ + p];
+#pragma unroll
+    for (int c = 0; c < NCU; ++c)
+#pragma unroll
+      for (int j = 0; j < ND; ++j) {
+        double a = 0.0;
+#pragma unroll
+        for (int r = 0; r < ND; ++r) a = fma(gp[1 + j * ND + r], gr[r][c], a);
+        bA[(c * ND + j) * NQ + p] = -wd * a;
+      }
+  }
+  __syncthreads();
+  {
+    double* res;
+    if (ND == 3) {
+      contract_u<NQ1, NQ1, NQ1, 0, NQ1, N1, true, OP_PHI>(bA, bB, NGQ, tid);
+      __syncthreads();
+      contract_u<N1, NQ1, NQ1, 1, NQ1, N1, true, OP_PHI>(bB, bA, NGQ, tid);
+      __syncthreads();
+      contract_u<N1, N1, NQ1, 2, NQ1, N1, true, OP_PHI>(bA, bB, NGQ, tid);
+      res = bB;
+    } else {
+      contract_u<NQ1, NQ1, 1, 0, NQ1, N1, true, OP_PHI>(bA, bB, NGQ, tid);
+      __syncthreads();
+      contract_u<N1, NQ1, 1, 1, NQ1, N1, true, OP_PHI>(bB, bA, NGQ, tid);
+      res = bA;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < NGQ * NB; idx += NT) rhs[idx] = res[idx];
+  }
+  // ---- faces: own / neighbour traces at the face points
+  for (int lf = 0; lf < NFACE; ++lf) {
+    const int info = P.finfo[e * NFACE + lf];
+    const bool interior = (info & 3) == 0;
+    const int nbr = P.fnbr[e * NFACE + lf];
+    double* own = FN;
+    double* oth = FN + NCU * MXF;
+    double* st = FN + 2 * NCU * MXF;
+    for (int idx = tid; idx < NCU * NFN; idx += NT) {
+      const int c = idx / NFN, t = idx % NFN;
+      own[idx] = su[c * NB + face_vol_node(lf, t)];
+      oth[idx] = interior ? P.u[((sz_t)nbr * NB + P.nmap[(info >> 8) * NFN + t]) * NCU + c] : 0.0;
+    }
+    __syncthreads();
+    double* tro = TR + (0 * NFACE + lf) * NCU * NQF;
+    double* trn = TR + (1 * NFACE + lf) * NCU * NQF;
+    if (ND == 3) {
+      contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(own, st, NCU, tid);
+      contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(oth, st + NCU * NQ1 * N1, NCU, tid);
+      __syncthreads();
+      contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(st, tro, NCU, tid);
+      contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(st + NCU * NQ1 * N1, trn, NCU, tid);
+    } else {
+      contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(own, tro, NCU, tid);
+      contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(oth, trn, NCU, tid);
+    }
+    __syncthreads();
+  }
+  // ---- per face point: wsj (u - u^) n (left frame, sign of the side)
+  for (int it = tid; it < NFACE * NQF; it += NT) {
+    const int lf = it / NQF, sp = it % NQF;
+    const int info = P.finfo[e * NFACE + lf];
+    const int kind = info & 3;
+    const bool right = kind == 0 && (info & 4);
+    const bool sw = info & 8;
+    const int brow = P.fnbr[e * NFACE + lf];
+    const double* ff = P.ffgeo + (((sz_t)e * NFACE + lf) * NQF + sp) * FG;
+    const double w = ff[ND] * (right ? -1.0 : 1.0);
+#pragma unroll
+    for (int c = 0; c < NCU; ++c) {
+      const double uo = TR[((0 * NFACE + lf) * NCU + c) * NQF + sp];
+      const double un = TR[((1 * NFACE + lf) * NCU + c) * NQF + sp];
+      double jump = 0.0;
+      if (kind == 0) {
+        if (TRACE_CENTERED) jump = 0.5 * (uo - un);
+        else if (sw == right) jump = uo - un;           // u^ = the neighbour's trace
+      } else if (kind == 1) {
+        jump = uo - (P.gq ? P.gq[((sz_t)brow * NQF + sp) * NCU + c] : 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < ND; ++j) FJ[(lf * NQF + sp) * NGQ + c * ND + j] = w * jump * ff[j];
+    }
+  }
+  __syncthreads();
+  // lift onto the face nodes (GLL: a basis trace lives on its face's nodes)
+  for (int it = tid; it < NB * NGQ; it += NT) {
+    const int a = it / NGQ, cj = it % NGQ;
+    const int ia[3] = {a % N1, (a / N1) % N1, ND == 3 ? a / (N1 * N1) : 0};
+    double acc = 0.0;
+#pragma unroll
+    for (int lf = 0; lf < NFACE; ++lf) {
+      const int ax = face_axis(lf);
+      if (ia[ax] != (face_side(lf) ? N1 - 1 : 0)) continue;
+      const int t0 = ia[ax == 0 ? 1 : 0];
+      const int t1 = ND == 3 ? ia[ax == 2 ? 1 : 2] : 0;
+#pragma unroll
+      for (int sp = 0; sp < NQF; ++sp) {
+        const int s0 = sp % NQ1, s1 = ND == 3 ? sp / NQ1 : 0;
+        const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1] : c_phi[s0 * N1 + t0];
+        acc = fma(ph, FJ[(lf * NQF + sp) * NGQ + cj], acc);
+      }
+    }
+    rhs[cj * NB + a] += acc;
+  }
+  __syncthreads();
+  // ---- q = M_e^-1 rhs
+  const double* mi = P.minv + (sz_t)e * NB * NB;
+  for (int it = tid; it < NB * NGQ; it += NT) {
+    const int a = it / NGQ, cj = it % NGQ;
+    double acc = 0.0;
+    for (int b = 0; b < NB; ++b) acc = fma(mi[a * NB + b], rhs[cj * NB + b], acc);
+    flag(P, e, acc);
+    P.out[((sz_t)e * NB + a) * NGQ + cj] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // residual / tangent: one element per block of NT threads
 // ---------------------------------------------------------------------------
 template <bool TANGENT>

@@ -36,13 +36,13 @@ class ErrorNorms:
 class DiagParams(C.Structure):
     _fields_ = [("ne", C.c_int32), ("nq", C.c_int32), ("nb", C.c_int32), ("mode", C.c_int32),
                 ("t", C.c_double)] + [(k, C.c_void_p) for k in (
-                    "x0", "J", "detj", "qp", "qw", "phi", "u", "q", "w", "out")]
+                    "x0", "J", "detj", "qp", "qw", "phi", "u", "q", "w", "out", "xq", "wdq")]
 
 
 _MODULES = {}
 
 
-def _source(model, nd, plan, nf, mode):
+def _source(model, nd, plan, nf, mode, curved=False):
     """mode 0: L2 partials of nf fields (state field f vs plan output f);
     mode 1: functional (plan output 0 at (x, t, u~, q~, w~))."""
     ncu, nw = model.ncu, model.nw
@@ -50,9 +50,9 @@ def _source(model, nd, plan, nf, mode):
     L = [codegen.DEVICE_HELPERS,
          codegen.emit_plan(plan, "plan_g", nd, model.mu_bindings()),
          "struct DiagParams { int ne, nq, nb, mode; double t; const double *x0, *J, *detj, *qp,"
-         " *qw, *phi, *u, *q, *w; double* out; };",
+         " *qw, *phi, *u, *q, *w; double* out; const double *xq, *wdq; };",
          f"#define ND {nd}\n#define NCU {ncu}\n#define NQV {nq_}\n#define NW {max(nw, 1)}\n"
-         f"#define NFLD {nf}\n#define MODE {mode}",
+         f"#define NFLD {nf}\n#define MODE {mode}\n#define CURVED {int(curved)}",
          'extern "C" __global__ void __launch_bounds__(128) diag_kernel(const DiagParams P) {',
          "  __shared__ double red[2][128];",
          "  const int e = blockIdx.x;",
@@ -61,9 +61,13 @@ def _source(model, nd, plan, nf, mode):
          "  for (int q = threadIdx.x; q < P.nq; q += blockDim.x) {",
          "    double x[ND];",
          "    for (int d = 0; d < ND; ++d) {",
+         "#if CURVED",
+         "      x[d] = P.xq[((size_t)e * P.nq + q) * ND + d];",   # per-point geometry map
+         "#else",
          "      double v = P.x0[e * ND + d];",
          "      for (int r = 0; r < ND; ++r) v += P.J[(e * ND + d) * ND + r] * P.qp[q * ND + r];",
          "      x[d] = v;",
+         "#endif",
          "    }",
          "    const double* ph = P.phi + (size_t)q * P.nb;",
          "    double uq[NCU], qq[NQV], wq[NW];",
@@ -76,7 +80,11 @@ def _source(model, nd, plan, nf, mode):
          "      if (P.q) for (int c = 0; c < NQV; ++c) qq[c] = fma(f, P.q[((size_t)e * P.nb + a) * NQV + c], qq[c]);",
          "      if (P.w) for (int c = 0; c < NW; ++c) wq[c] = fma(f, P.w[((size_t)e * P.nb + a) * NW + c], wq[c]);",
          "    }",
+         "#if CURVED",
+         "    const double wd = P.wdq[(size_t)e * P.nq + q];",
+         "#else",
          "    const double wd = dj * P.qw[q];",
+         "#endif",
          "    double g[NFLD];",
          "    plan_g(x, P.t, uq, qq, wq, nullptr, g);",
          "#if MODE == 0",
@@ -138,7 +146,8 @@ def _partials(system, plan, nf, mode, t, u, q=None, w=None):
     import torch
     tab = system.tab
     m = tab.master
-    src = _source(system.model, system.nd, plan, nf, mode)
+    curved = bool(getattr(tab, "curved", False))
+    src = _source(system.model, system.nd, plan, nf, mode, curved)
     mod = _module(src)
     out = torch.empty(2 * tab.ne, dtype=torch.float64, device=system.device)
     P = DiagParams()
@@ -149,6 +158,9 @@ def _partials(system, plan, nf, mode, t, u, q=None, w=None):
     P.qp = _dev(system, "qp", m.quad_pts).data_ptr()
     P.qw = _dev(system, "qw", m.quad_wts).data_ptr()
     P.phi = _dev(system, "phi", m.phi).data_ptr()
+    if curved:                  # disc.py:91-104: x and w detJ per volume point
+        P.xq = _dev(system, "xq", tab.xq_q).data_ptr()
+        P.wdq = _dev(system, "wdq", tab.wdetj_q).data_ptr()
     keep = [_as_dev(system, u), _as_dev(system, q), _as_dev(system, w)]
     P.u = keep[0].data_ptr()
     P.q = None if keep[1] is None else keep[1].data_ptr()

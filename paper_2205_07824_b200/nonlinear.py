@@ -123,10 +123,10 @@ class NlTables(TensorTables):
                 reference's scatter of +/- one value (disc.py:641-653)
           minv  (ne, nb, nb): inverse element mass matrices (disc.py:107-110)."""
         m, nd, ne, nf = self.master, self.nd, self.ne, self.nf
-        if self.model.kind != "C" or self.model.nw > 0:
-            raise DiscError("curved elements are supported for kind C models without "
-                            "ODE blocks on the B200 path (the mixed gradient's collocation "
-                            "identities need affine elements)")
+        if self.model.kind not in ("C", "D") or self.model.nw > 0 or \
+                self.model.numflux.uhat is not None:
+            raise DiscError("curved elements are supported for kind C / D models without "
+                            "ODE blocks or u^ overrides on the B200 path")
         self.vgeo = np.concatenate([self.detj_q[..., None], self.invjt_q.reshape(ne, -1, nd * nd),
                                     self.xq_q], axis=2)
         nqf = self.fxi.shape[1]
@@ -389,6 +389,10 @@ class NlOperator:
         nvm = ncu if s["MASS_CONST"] else 3 * ncu
         self.smem["nl_mass"] = self.smem["nl_mass_extra"] = 8 * 2 * max(nvm, ncu) * mx
         self.smem["nl_mass_inv"] = 8 * 2 * ncu * nb
+        ngq, nqf_ = ncu * nd, tab.nq1 ** (nd - 1)
+        mcs = max(ngq, ncu) * mx
+        self.smem["nl_mixed_curved"] = 8 * (ncu * nb + 3 * mcs + ngq * nb + 2 * 2 * nd * ncu * nqf_
+                                            + 4 * ncu * mxf + 2 * nd * nqf_ * ngq)
         self.smem["nl_mass_q"] = 8 * 2 * ncu * tab.nd * mx
         self.smem["nl_mass_inv_q"] = 8 * 2 * ncu * tab.nd * nb
 
@@ -450,6 +454,11 @@ class NlOperator:
         gradient absorbing boundaries take u^ from."""
         tab = self.tab
         q = out if out is not None else self._empty((tab.ne, self.shape["NB"], tab.ncu, tab.nd))
+        if getattr(tab, "curved", False):
+            # quadrature form with per-point metrics and M_e^-1 (disc.py:436-490)
+            P = self._params(t, u=u, out=q, gq=None if homogeneous else self.gq(t))
+            self._launch("nl_mixed_curved", tab.ne, self.shape["NT"], P)
+            return q
         P = self._params(t, u=u, q=state_q, out=q,
                          gproj=None if homogeneous else self.gproj(t))
         P.homog = int(bool(linearised))

@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .tables import DenseTables, DiscError, KernelNanError, TensorTables
+from .tables import DenseTables, DiscError, KernelNanError, TensorTables, mesh_is_affine
 from .nonlinear import NlOperator, NlTables, linear_path_reason
 
 # elements from which the volume source load is evaluated on the device (the
@@ -128,6 +128,9 @@ class LdgSystem:
         self.dense = master.kind in ("tri", "tet")
         self.nl = None
         self.nl_reason = None if self.dense else linear_path_reason(model)
+        if self.nl_reason is None and not self.dense and tables is None and \
+                not mesh_is_affine(mesh):
+            self.nl_reason = "curved (non-affine) elements"
         if tables is not None and self.nl_reason is not None:
             raise DiscError(f"prebuilt (partitioned) tables support linear models only "
                             f"({self.nl_reason})")

@@ -199,6 +199,16 @@ def _reference_switch_subset(mesh, master, geom, elems, lfs):
 # ---------------------------------------------------------------------------
 
 
+def mesh_is_affine(mesh):
+    """True when every element's geometry map is affine (the Jacobian at the
+    reference corners agrees to roundoff) -- the fused / dense kernels'
+    precondition; curved meshes run on the generated path."""
+    geom = refelem.build_geom_master(mesh.elem_kind, mesh.p_geom)
+    gd = geom.eval_basis_grad(refelem.VERTS[mesh.elem_kind])
+    J = np.einsum("egd,vgr->evdr", mesh.ho_nodes, gd)
+    return not bool(np.max(np.abs(J - J[:, :1])) > 1e-11 * max(mesh.diameter(), 1.0))
+
+
 class TensorTables:
     """Host arrays for the tensor-product (quad/hex) kernels."""
 
@@ -280,7 +290,8 @@ class TensorTables:
         self.curved = bool(np.max(np.abs(J - J[:, :1])) > 1e-11 * scale)
         if self.curved:
             if not self.nonlinear:
-                raise DiscError("curved (non-affine) elements run on the generated path only")
+                raise DiscError("curved (non-affine) elements run on the generated path "
+                                "(quad / hex) only")
             self._curved_geometry(geom)
             # element-level affine stand-ins (the Jacobian at the reference
             # centre): only the table builders' approximate uses read them

@@ -378,11 +378,26 @@ CURVED_CASES = {
         curved=("annulus", 16, 4, 1.0, 3.0, 3), mesh_file="curved_sw_annulus_quad_p3.npz",
         bcs={1: ("dirichlet", ["1.3", "0.4", "-0.2"]), 2: ("dirichlet", ["1.3", "0.4", "-0.2"])},
         free=[1.3, 0.4, -0.2], state=([1.3, 0.4, -0.2], 0.05)),
+    "curved_poisson_annulus_quad_p3": dict(
+        model=("builtin", "poisson", 2, None), kind="quad", p=3,
+        curved=("annulus", 16, 4, 1.0, 3.0, 3), mesh_file="curved_poisson_annulus_quad_p3.npz",
+        bcs={1: ("dirichlet", ["log(sqrt(x1*x1 + x2*x2))"]),
+             2: ("dirichlet", ["log(sqrt(x1*x1 + x2*x2))"])}),
+    "curved_ns_hex_warp_p2": dict(
+        model=("file", "ns3d.model"), kind="hex", counts=[3, 3, 3], p=2, periodic=3,
+        curved=("warp", 2, 0.04), mesh_file="curved_ns_hex_warp_p2.npz",
+        free=[1.0, 0.2, -0.1, 0.15, 25.0], state=([1.0, 0.2, -0.1, 0.15, 25.0], 0.05)),
     "curved_euler_hex_warp_p2": dict(
         model=("builtin", "euler", 3, None), kind="hex", counts=[3, 3, 3], p=2, periodic=3,
         curved=("warp", 2, 0.04), mesh_file="curved_euler_hex_warp_p2.npz",
         free=[1.0, 0.2, -0.1, 0.15, 2.5], state=([1.0, 0.2, -0.1, 0.15, 2.5], 0.05)),
 }
+
+# steady Newton-GMRES on the curved annulus: Poisson with u = log r on both
+# circles (harmonic: the exact solution), block-Jacobi, acceptance flags
+SOLVE_CASES["curved_poisson_annulus_quad_p3_bj"] = dict(
+    CURVED_CASES["curved_poisson_annulus_quad_p3"], precond="block_jacobi",
+    exact=(["log(sqrt(x1*x1 + x2*x2))"], None))
 
 # block-Jacobi of the steady closures on NS hex p=3 (320 x 320 blocks, beyond
 # the shared-memory Gauss-Jordan): build + apply only (bj_ns3d_hex_p3.npz)

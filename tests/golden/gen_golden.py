@@ -145,7 +145,9 @@ def gen_solve(name, spec):
         from ldgkit.diagnostics import compute_l2_error
         eu, eq = spec["exact"]
         err = compute_l2_error(s, out_state, eu, eq)
-        extra = dict(error_u=np.array(err.error_u), error_q=np.array(err.error_q))
+        extra = dict(error_u=np.array(err.error_u))
+        if err.error_q is not None:
+            extra["error_q"] = np.array(err.error_q)
     np.savez_compressed(HERE / f"solve_{name}.npz", u=out_state.u,
                         newton_iters=np.array(stats.newton_iters),
                         gmres_iters=np.array(stats.gmres_iters),
@@ -204,16 +206,20 @@ def gen_curved(name, spec):
     model, mesh, topo, master = build_case(spec, R_model, R_mesh, R_master)
     s = LdgSystem(model, mesh, topo, master)
     ne, nb, ncu = s.n_elements, s.n_nodes, s.ncu
-    uf = np.broadcast_to(np.asarray(spec["free"], dtype=float), (ne, nb, ncu)).copy()
     u = case_state(spec, ne, nb, ncu, 1)
     du = seeded_state(ne, nb, ncu, 0)
     y = seeded_state(ne, nb, ncu, 2)
     st = SolverState(u=u, q=None, w=None, t=0.0)
-    out = dict(u_free=uf, R_free=s.residual(SolverState(u=uf, q=None, w=None, t=0.0))[0],
-               u=u, du=du, y=y, R=s.residual(st)[0], Jdu=s.residual_tangent(st, du)[0],
+    out = dict(u=u, du=du, y=y, R=s.residual(st)[0], Jdu=s.residual_tangent(st, du)[0],
                M=s.mass_apply(st, y)[0], **mesh_arrays(mesh), **topo_arrays(s))
+    if "free" in spec:
+        uf = np.broadcast_to(np.asarray(spec["free"], dtype=float), (ne, nb, ncu)).copy()
+        out.update(u_free=uf, R_free=s.residual(SolverState(u=uf, q=None, w=None, t=0.0))[0])
+    if s.kind == "D":
+        out.update(q=s.compute_mixed(u, 0.0), dq=s.compute_mixed(du, 0.0, homogeneous=True))
     np.savez_compressed(HERE / spec["mesh_file"], **out)
-    print("curved", name, ne * nb * ncu, "free-stream |R|", float(np.abs(out["R_free"]).max()))
+    print("curved", name, ne * nb * ncu, "free-stream |R|",
+          float(np.abs(out["R_free"]).max()) if "R_free" in out else None)
 
 
 def gen_bj(name, spec):
