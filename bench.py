@@ -478,8 +478,7 @@ def run_b200(args, rank, world):
     t_ms = float(tmax.item())
     traffic = load_traffic()
     p1_name = ("plane_kernel<tangent> (pass 1, z-plane mapping, persistent)"
-               if (core.tab.n1 == 4 and core.tab.nd == 3 and core.ncu == 1
-                   and os.environ.get("LDG_PASS1_VARIANT", "") != "pencil")
+               if (core.tab.n1 == 4 and core.tab.nd == 3 and core.ncu == 1)
                else "fused_kernel<tangent> (pass 1, pencil mapping)")
     # algorithmic bytes of the fused passes from the face tables
     tab = core.tab

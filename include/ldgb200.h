@@ -191,6 +191,13 @@ int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, doubl
  * single-process; this is the B200 multi-GPU layer.) */
 int ldg_set_ghost_rows(LdgHandle* h, int ghost0, const double* u_ghost);
 
+/* Kernel-selection options of a tensor handle (A/B measurements, tests);
+ * the defaults are the measured-best choices: "pass1_variant" (0 plane |
+ * 1 pencil), "c_diag" (0 forces the general flux-coefficient branch),
+ * "p2_mode" (0 warp + PDL | 1 no PDL | 2 block | 3 one-shot).  No reference
+ * counterpart. */
+int ldg_set_option(LdgHandle* h, const char* name, int value);
+
 /* Unfused reference structure, kept for comparison: flux pass from a
  * precomputed q = compute_mixed(u) (72 B/DOF of HBM traffic at nd = 3). */
 int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,

@@ -193,7 +193,6 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
             break;
           }
     }
-    if (const char* v = getenv("LDG_CDIAG")) diag = diag && atoi(v) != 0;   // A/B timing
     h->c_diag = diag ? 1 : 0;
   }
   cudaError_t e = cudaMalloc(&h->bad, sizeof(unsigned long long));
@@ -212,19 +211,15 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
   P.geo = h->geo; P.fnbr = h->fnbr; P.finfo = h->finfo; P.ftau = h->ftau;
   P.nmap = h->nmap; P.bad = h->bad; P.frec = h->frec; P.kco = h->kco; P.kstride = h->kstride;
   P.c_diag = h->c_diag;
-  {
-    const char* v = getenv("LDG_PASS1_VARIANT");    // "pencil" forces the v9 kernel (A/B timing)
-    P.variant = (v && strcmp(v, "pencil") == 0) ? 1 : 0;
-  }
+  P.variant = 0;
+  P.p2_mode = 0;
   P.e0 = 0;
   P.e1 = t->ne;
   P.x_consumer = 1;
   {
     // chunk-interleaved schedule of the fused operator (ldg_fused.cu run_fused):
     // chunk_dep[c] = last chunk whose exports pass 2 of chunk c reads
-    int nch = 1;                       // measured: chunking loses (launch tails outweigh L2 reuse)
-    if (const char* v = getenv("LDG_CHUNKS")) nch = atoi(v);
-    nch = nch < 1 ? 1 : (nch > ldg::LDG_MAX_CHUNKS ? ldg::LDG_MAX_CHUNKS : nch);
+    const int nch = 1;                 // measured: chunking loses (launch tails outweigh L2 reuse)
     const int ne = t->ne, nf = 2 * t->nd;
     P.nchunk = nch;
     for (int c = 0; c <= nch; ++c) {
@@ -400,6 +395,23 @@ int ldg_set_ghost_rows(LdgHandle* h, int ghost0, const double* u_ghost) {
   if (ghost0 >= 0 && !u_ghost) return fail(2, "ghost rows need a buffer");
   h->P.ghost0 = ghost0 < 0 ? INT32_MAX : ghost0;
   h->P.u_ghost = ghost0 < 0 ? nullptr : u_ghost;
+  return 0;
+}
+
+// Kernel-selection options of one handle (A/B measurements and tests; the
+// defaults are the measured-best choices):
+//   "pass1_variant" 0 plane kernel where it applies | 1 pencil kernel
+//   "c_diag"        0 forces the general flux-coefficient branch
+//   "p2_mode"       0 warp kernel + PDL | 1 without PDL | 2 block kernel | 3 one-shot
+int ldg_set_option(LdgHandle* h, const char* name, int value) {
+  if (!h || !name) return fail(2, "bad argument");
+  if (h->dense) return fail(2, "options apply to tensor handles");
+  if (!strcmp(name, "pass1_variant")) h->P.variant = value ? 1 : 0;
+  else if (!strcmp(name, "c_diag")) h->P.c_diag = (value && h->c_diag) ? 1 : 0;
+  else if (!strcmp(name, "p2_mode")) {
+    if (value < 0 || value > 3) return fail(2, "p2_mode is 0..3");
+    h->P.p2_mode = value;
+  } else return fail(2, "unknown option");
   return 0;
 }
 
@@ -582,21 +594,6 @@ int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, doubl
     }
   }
   if (next2 != nchunk) return fail(2, "chunk plan left passes unissued");
-  if (getenv("LDG_PIPE_DEBUG")) {       // timeline of the copies and kernels
-    cudaEvent_t t1, t2, t3;
-    cudaEventCreate(&t1); cudaEventCreate(&t2); cudaEventCreate(&t3);
-    cudaEventRecord(t1, h->s_in);
-    cudaEventRecord(t2, s);
-    cudaEventRecord(t3, h->s_out);
-    cudaStreamSynchronize(h->s_out);
-    cudaStreamSynchronize(h->s_in);
-    cudaStreamSynchronize(s);
-    float a = 0, b = 0;
-    cudaEventElapsedTime(&a, t1, t3);
-    cudaEventElapsedTime(&b, t2, t3);
-    fprintf(stderr, "pipe: D2H end - H2D end %.3f ms, D2H end - compute end %.3f ms\n", a, b);
-    cudaEventDestroy(t1); cudaEventDestroy(t2); cudaEventDestroy(t3);
-  }
   cudaError_t e = cudaStreamSynchronize(h->s_out);
   if (e != cudaSuccess) return fail(3, "host pipeline", e);
   return 0;

@@ -22,6 +22,9 @@ namespace {
 #define LDG_DENSE_BLOCK 128
 #endif
 constexpr int kDBlock = LDG_DENSE_BLOCK;
+#ifndef LDG_DENSE_MMA
+#define LDG_DENSE_MMA 1       // ncu = 1: operator contractions on the FP64 tensor core
+#endif
 #ifndef LDG_TET3_TPE
 #define LDG_TET3_TPE 24       // threads per tet p=3 element (>= nb = 20); measured 20: 3.57, 24: 3.27, 32: 3.40 ms
 #endif
@@ -332,6 +335,302 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
   }
 }
 
+// --------------------------------------------------------------------------
+// Tensor-core variants (ncu = 1): the element-independent contractions --
+// own face traces (phif), the collocation gradient (dr), the lifts, the volume
+// term (K_r) and the face lift (Phi^T W) -- batched over the 8 elements of a
+// block as GEMMs on the FP64 tensor core (mma.sync m8n8k4: A = an 8 x 4 slice
+// of the operator, B = 4 nodes x 8 elements, D = 8 outputs x 8 elements).  One
+// A entry now feeds 8 elements instead of 1 (the scalar kernels above issue
+// one operator load per FMA: LSU-bound).  The orientation-dependent neighbour
+// traces stay on the FP64 pipe.  Same arithmetic identities and outputs.
+// --------------------------------------------------------------------------
+constexpr int kMmaEpb = 8;
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// C(m, e) = sum_k A1(m, k) B1(k, e) [+ sum_k A2(m, k) B2(k, e)] for one 8-row
+// tile mt and the block's 8 elements; A(m, k) = A[k * AK + m] (operator,
+// column-major as stored), B(k, e) = B[e * BE + k] (shared), C(m, e) =
+// C[e * CE + m] (shared).  Rows m >= M are zero-padded and not stored.
+template <int M, int K1, int AK1, int BE1, int K2, int AK2, int BE2, int CE>
+__device__ __forceinline__ void gemm8_tile(int mt, const double* __restrict__ A1, const double* B1,
+                                           const double* __restrict__ A2, const double* B2,
+                                           double* C) {
+  const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+  const int m = mt * 8 + r;
+  double d0 = 0.0, d1 = 0.0;
+#pragma unroll 5
+  for (int k0 = 0; k0 < K1; k0 += 4) {
+    const int k = k0 + c;
+    const double a = (m < M && k < K1) ? __ldg(A1 + k * AK1 + m) : 0.0;
+    const double b = k < K1 ? B1[r * BE1 + k] : 0.0;
+    dmma884(d0, d1, a, b);
+  }
+  if (K2 > 0) {
+#pragma unroll 4
+    for (int k0 = 0; k0 < K2; k0 += 4) {
+      const int k = k0 + c;
+      const double a = (m < M && k < K2) ? __ldg(A2 + k * AK2 + m) : 0.0;
+      const double b = k < K2 ? B2[r * BE2 + k] : 0.0;
+      dmma884(d0, d1, a, b);
+    }
+  }
+  if (m < M) {
+    C[(2 * c) * CE + m] = d0;
+    C[(2 * c + 1) * CE + m] = d1;
+  }
+}
+
+template <int NB, int NQF, int NFACE, int ND, int TPE>
+__global__ void __launch_bounds__(kMmaEpb * TPE)
+mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__ u,
+                const double* __restrict__ gval, double* __restrict__ q) {
+  constexpr int EPB = kMmaEpb, NT = EPB * TPE, NW = NT / 32;
+  constexpr int MTN = (NB + 7) / 8, MTF = (NQF + 7) / 8;
+  __shared__ double su[EPB][NB];
+  __shared__ double snb[EPB][NFACE][NB];
+  __shared__ double sto[EPB][NFACE][NQF];     // own traces
+  __shared__ double sjump[EPB][NFACE][NQF];
+  __shared__ double sg[EPB][ND][NB];          // reference-direction derivatives
+  __shared__ double sl[EPB][NFACE][NB];       // lifted jumps
+  const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * EPB + slot;
+  const bool active = e < P.ne;
+  int info[NFACE], nbr[NFACE];
+#pragma unroll
+  for (int f = 0; f < NFACE; ++f) {
+    info[f] = active ? __ldg(P.finfo + e * NFACE + f) : LDG_FACE_NEUMANN;
+    nbr[f] = active ? __ldg(P.fnbr + e * NFACE + f) : 0;
+  }
+  if (lt < NB) {
+    su[slot][lt] = active ? __ldg(u + (size_t)e * NB + lt) : 0.0;
+#pragma unroll
+    for (int f = 0; f < NFACE; ++f) {
+      double a_, b_, wo_, wn_;
+      coeffs(P, info[f], a_, b_, wo_, wn_);
+      const bool need = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR && a_ != 0.0;
+      snb[slot][f][lt] = need ? __ldg(u + (size_t)nbr[f] * NB + lt) : 0.0;
+    }
+  }
+  __syncthreads();
+  // tensor core: own traces (phif_f u) and the gradient (dr_r u)
+  for (int job = warp; job < NFACE * MTF + ND * MTN; job += NW) {
+    if (job < NFACE * MTF) {
+      const int f = job / MTF, mt = job % MTF;
+      gemm8_tile<NQF, NB, NQF, NB, 0, 1, 1, NFACE * NQF>(
+          mt, P.phif + f * NB * NQF, &su[0][0], nullptr, nullptr, &sto[0][f][0]);
+    } else {
+      const int j = job - NFACE * MTF, r = j / MTN, mt = j % MTN;
+      gemm8_tile<NB, NB, NB, NB, 0, 1, 1, ND * NB>(
+          mt, P.dr + r * NB * NB, &su[0][0], nullptr, nullptr, &sg[0][r][0]);
+    }
+  }
+  __syncthreads();
+  if (active) {
+    for (int idx = lt; idx < NFACE * NQF; idx += TPE) {
+      const int f = idx / NQF, sp = idx - f * NQF;
+      const int inf = __ldg(P.finfo + e * NFACE + f);
+      double alpha, b_, wo_, wn_;
+      coeffs(P, inf, alpha, b_, wo_, wn_);
+      const int kind = inf & LDG_FACE_KIND_MASK;
+      double jump = 0.0;
+      if (alpha != 0.0) {
+        double oth = 0.0;
+        if (kind == LDG_FACE_INTERIOR) {
+          const double* po = P.phio + (((inf >> 4) & 7) * P.nperm + ((inf >> 8) & 0xff)) * NB * NQF + sp;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) oth = fma(__ldg(po + b * NQF), snb[slot][f][b], oth);
+        } else if (kind == LDG_FACE_DIRICHLET && gval) {
+          oth = __ldg(gval + (size_t)__ldg(P.fnbr + e * NFACE + f) * NQF + sp);
+        }
+        jump = alpha * (sto[slot][f][sp] - oth);
+      }
+      sjump[slot][f][sp] = jump;
+    }
+  } else {
+    for (int idx = lt; idx < NFACE * NQF; idx += TPE) sjump[slot][idx / NQF][idx % NQF] = 0.0;
+  }
+  __syncthreads();
+  // tensor core: the lifts M_ref^-1 Phi^T W jump, per face
+  for (int job = warp; job < NFACE * MTN; job += NW) {
+    const int f = job / MTN, mt = job % MTN;
+    gemm8_tile<NB, NQF, NB, NFACE * NQF, 0, 1, 1, NFACE * NB>(
+        mt, P.lift + f * NQF * NB, &sjump[0][f][0], nullptr, nullptr, &sl[0][f][0]);
+  }
+  __syncthreads();
+  if (!active || lt >= NB) return;
+  const double* g = P.geo + (size_t)e * (1 + ND * ND);
+  const double detj = __ldg(g);
+  double qd[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    double a = 0.0;
+#pragma unroll
+    for (int r = 0; r < ND; ++r) a = fma(__ldg(g + 1 + d * ND + r), sg[slot][r][lt], a);
+    qd[d] = -a;
+  }
+#pragma unroll
+  for (int f = 0; f < NFACE; ++f) {
+    const double fac = __ldg(P.fsj + e * NFACE + f) / detj * sl[slot][f][lt];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) qd[d] = fma(fac, __ldg(P.fnorm + (e * NFACE + f) * ND + d), qd[d]);
+  }
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    dbad(P, e, qd[d]);
+    q[((size_t)e * NB + lt) * ND + d] = qd[d];
+  }
+}
+
+template <int NB, int NQF, int NFACE, int ND, int TPE, bool TANGENT>
+__global__ void __launch_bounds__(kMmaEpb * TPE)
+flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__ u,
+               const double* __restrict__ q, const double* __restrict__ gval,
+               const double* __restrict__ bsrc, double* __restrict__ R) {
+  constexpr int EPB = kMmaEpb, NT = EPB * TPE, NW = NT / 32, NV = 1 + ND;
+  constexpr int MTN = (NB + 7) / 8, MTF = (NQF + 7) / 8;
+  // dynamic shared memory (> 48 KB at tet p = 3); sR reuses the trace region
+  extern __shared__ __align__(16) double dsm[];
+  auto& sv = *reinterpret_cast<double (*)[EPB][NV][NB]>(dsm);                  // u, q_1..q_ND
+  auto& snu = *reinterpret_cast<double (*)[EPB][NFACE][NB]>(dsm + EPB * NV * NB);
+  auto& snq = *reinterpret_cast<double (*)[EPB][NFACE][ND][NB]>(
+      dsm + EPB * (NV + NFACE) * NB);
+  auto& sF = *reinterpret_cast<double (*)[EPB][ND][NB]>(
+      dsm + EPB * (NV + NFACE + NFACE * ND) * NB);                             // -detJ invJ^T f
+  auto& sto = *reinterpret_cast<double (*)[EPB][NFACE][NV][NQF]>(
+      dsm + EPB * (NV + NFACE + NFACE * ND + ND) * NB);                        // own traces
+  auto& sfh = *reinterpret_cast<double (*)[EPB][NFACE * NQF]>(
+      dsm + EPB * (NV + NFACE + NFACE * ND + ND) * NB + EPB * NFACE * NV * NQF);  // sJ f^
+  auto& sR = *reinterpret_cast<double (*)[EPB][NB]>(&sto[0][0][0][0]);
+  const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * EPB + slot;
+  const bool active = e < P.ne;
+  int info[NFACE], nbr[NFACE];
+#pragma unroll
+  for (int f = 0; f < NFACE; ++f) {
+    info[f] = active ? __ldg(P.finfo + e * NFACE + f) : LDG_FACE_NEUMANN;
+    nbr[f] = active ? __ldg(P.fnbr + e * NFACE + f) : 0;
+  }
+  double detj = 1.0, ij[ND][ND];
+  {
+    const double* g = P.geo + (size_t)(active ? e : 0) * (1 + ND * ND);
+    detj = __ldg(g);
+#pragma unroll
+    for (int d = 0; d < ND; ++d)
+#pragma unroll
+      for (int r = 0; r < ND; ++r) ij[d][r] = __ldg(g + 1 + d * ND + r);
+  }
+  if (lt < NB) {
+    sv[slot][0][lt] = active ? __ldg(u + (size_t)e * NB + lt) : 0.0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) sv[slot][1 + d][lt] = active ? __ldg(q + ((size_t)e * NB + lt) * ND + d) : 0.0;
+#pragma unroll
+    for (int f = 0; f < NFACE; ++f) {
+      double alpha, beta, wo, wn;
+      coeffs(P, info[f], alpha, beta, wo, wn);
+      const bool inter = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR;
+      const bool nu = inter && (alpha != 0.0 || beta != 0.0);
+      const bool nq = inter && wn != 0.0;
+      snu[slot][f][lt] = nu ? __ldg(u + (size_t)nbr[f] * NB + lt) : 0.0;
+#pragma unroll
+      for (int d = 0; d < ND; ++d)
+        snq[slot][f][d][lt] = nq ? __ldg(q + ((size_t)nbr[f] * NB + lt) * ND + d) : 0.0;
+    }
+  }
+  __syncthreads();
+  // nodal flux density in reference directions, negated (the volume term
+  // enters R with a minus sign)
+  if (lt < NB) {
+    double f[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      double a = 0.0;
+      if (P.flux_uses_u) a = fma(P.au[d * LDG_MAX_NCU], sv[slot][0][lt], a);
+#pragma unroll
+      for (int x = 0; x < ND; ++x) a = fma(P.aq[d * LDG_MAX_NCU * 3 + x], sv[slot][1 + x][lt], a);
+      f[d] = a;
+    }
+#pragma unroll
+    for (int r = 0; r < ND; ++r) {
+      double a = 0.0;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) a = fma(ij[d][r], f[d], a);
+      sF[slot][r][lt] = -detj * a;
+    }
+  }
+  // tensor core: own traces of u and q on every face
+  for (int job = warp; job < NFACE * NV * MTF; job += NW) {
+    const int f = job / (NV * MTF), v = (job / MTF) % NV, mt = job % MTF;
+    gemm8_tile<NQF, NB, NQF, NV * NB, 0, 1, 1, NFACE * NV * NQF>(
+        mt, P.phif + f * NB * NQF, &sv[0][v][0], nullptr, nullptr, &sto[0][f][v][0]);
+  }
+  __syncthreads();
+  if (active) {
+    for (int idx = lt; idx < NFACE * NQF; idx += TPE) {      // (face, point) pairs over all lanes
+      const int f = idx / NQF, sp = idx - f * NQF;
+      const int inf = __ldg(P.finfo + e * NFACE + f);
+      const int nbf = __ldg(P.fnbr + e * NFACE + f);
+      double alpha, beta, wo, wn;
+      coeffs(P, inf, alpha, beta, wo, wn);
+      const int kind = inf & LDG_FACE_KIND_MASK;
+      const bool inter = kind == LDG_FACE_INTERIOR;
+      const double* po = P.phio + (((inf >> 4) & 7) * P.nperm + ((inf >> 8) & 0xff)) * NB * NQF + sp;
+      const double uo = sto[slot][f][0][sp];
+      double un = 0.0;
+      if (inter && (alpha != 0.0 || beta != 0.0)) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) un = fma(__ldg(po + b * NQF), snu[slot][f][b], un);
+      } else if (!inter && !TANGENT && gval) {
+        un = __ldg(gval + (size_t)nbf * NQF + sp);
+      }
+      double qh[ND];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        double b2 = 0.0;
+        if (inter && wn != 0.0) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b) b2 = fma(__ldg(po + b * NQF), snq[slot][f][d][b], b2);
+        }
+        qh[d] = wo * sto[slot][f][1 + d][sp] + wn * b2;
+      }
+      double fh;
+      if (kind == LDG_FACE_NEUMANN) {
+        fh = (!TANGENT && gval) ? __ldg(gval + (size_t)nbf * NQF + sp) : 0.0;
+      } else {
+        const double uh = uo - alpha * (uo - un);
+        double fn = 0.0;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          double a = 0.0;
+          if (P.flux_uses_u) a = fma(P.au[d * LDG_MAX_NCU], uh, a);
+#pragma unroll
+          for (int x = 0; x < ND; ++x) a = fma(P.aq[d * LDG_MAX_NCU * 3 + x], qh[x], a);
+          fn = fma(a, __ldg(P.fnorm + (e * NFACE + f) * ND + d), fn);
+        }
+        fh = fn + beta * __ldg(P.ftau + e * NFACE + f) * (uo - un);
+      }
+      sfh[slot][idx] = __ldg(P.fsj + e * NFACE + f) * fh;
+    }
+  } else {
+    for (int idx = lt; idx < NFACE * NQF; idx += TPE) sfh[slot][idx] = 0.0;
+  }
+  __syncthreads();
+  // tensor core: R = sum_r K_r (-F_r) + sum_f Phi_f^T W (sJ f^)
+  for (int mt = warp; mt < MTN; mt += NW)
+    gemm8_tile<NB, ND * NB, NB, ND * NB, NFACE * NQF, NB, NFACE * NQF, NB>(
+        mt, P.kr, &sF[0][0][0], P.fluxop, &sfh[0][0], &sR[0][0]);
+  __syncthreads();
+  if (!active || lt >= NB) return;
+  double out = sR[slot][lt];
+  if (!TANGENT && bsrc) out += __ldg(bsrc + (size_t)e * NB + lt);
+  dbad(P, e, out);
+  R[(size_t)e * NB + lt] = out;
+}
+
 template <int NB, int NQF, int NFACE, int ND, int NCU, int TPE>
 int run_dense(const DenseParams& P, int what, const double* u, const double* gval,
               const double* bsrc, double* q, double* R, cudaStream_t s) {
@@ -339,6 +638,28 @@ int run_dense(const DenseParams& P, int what, const double* u, const double* gva
   const int grid = (P.ne + EPB - 1) / EPB;
   if (grid <= 0) return 0;
   // what: 0 = mixed only (q from u), 1 = residual, 2 = tangent
+  if constexpr (NCU == 1 && LDG_DENSE_MMA) {
+    // tensor-core variants (8 elements per block, batched operator GEMMs)
+    const int gm = (P.ne + kMmaEpb - 1) / kMmaEpb;
+    constexpr int fsm = (int)sizeof(double) * kMmaEpb *
+                        ((1 + ND + NFACE + NFACE * ND + ND) * NB + NFACE * (1 + ND) * NQF + NFACE * NQF);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(flux_dense_mma<NB, NQF, NFACE, ND, TPE, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+      cudaFuncSetAttribute(flux_dense_mma<NB, NQF, NFACE, ND, TPE, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+      attr = true;
+    }
+    mixed_dense_mma<NB, NQF, NFACE, ND, TPE><<<gm, kMmaEpb * TPE, 0, s>>>(
+        P, u, what == 2 ? nullptr : gval, q);
+    if (cudaGetLastError() != cudaSuccess) return 3;
+    if (what == 1)
+      flux_dense_mma<NB, NQF, NFACE, ND, TPE, false><<<gm, kMmaEpb * TPE, fsm, s>>>(P, u, q, gval, bsrc, R);
+    else if (what == 2)
+      flux_dense_mma<NB, NQF, NFACE, ND, TPE, true><<<gm, kMmaEpb * TPE, fsm, s>>>(P, u, q, nullptr, nullptr, R);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  }
   mixed_dense<NB, NQF, NFACE, ND, NCU, TPE><<<grid, kDBlock, 0, s>>>(P, u, what == 2 ? nullptr : gval, q);
   if (cudaGetLastError() != cudaSuccess) return 3;
   if (what == 1)

@@ -1851,16 +1851,16 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
   if (pass & 2) {
     static int nsm2 = 0;
     if (!nsm2) cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, 0);
-    static const bool pipe = !getenv("LDG_P2_PLAIN");      // A/B timing of the one-shot kernel
+    const bool pipe = P.p2_mode != 3;                 // one-shot block kernel (A/B)
     bool done = false;
-    static const bool warp2 = !getenv("LDG_P2_BLOCKWISE");  // A/B timing
+    const bool warp2 = P.p2_mode < 2;                 // block kernel (A/B)
     if constexpr (N1 >= 2 && N1 <= LDG_P2W_MAXN1 && ND == 3 && NCU == 1) {
       if (P.x_consumer && warp2) {
         constexpr int EPW = 32 / (N1 * N1);
         const int ngr = (nel + EPW - 1) / EPW;
         const int g = std::max(1, std::min((ngr + 7) / 8, nsm2 * LDG_P2W_GRID));
         if constexpr (N1 == 4) {
-          static const bool pdl = !getenv("LDG_NO_PDL");
+          const bool pdl = P.p2_mode == 0;
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3(g);
           cfg.blockDim = dim3(256);

@@ -24,6 +24,8 @@ struct TensorParams {
   const double* kco;      // (ne, kstride): C, Cu, sJ per face axis (fused kernels)
   int kstride;
   int variant;           // pass-1 kernel: 0 auto (plane kernel where it applies), 1 pencil kernel
+  int p2_mode;           // pass-2 kernel: 0 auto (warp kernel + PDL), 1 no PDL, 2 block kernel,
+                         // 3 one-shot block kernel (A/B through ldg_set_option)
   int e0, e1;            // element range of this launch (chunked schedules)
   int x_consumer;        // 1: exports land in the consuming neighbour's slots (pass 2 reads its own)
   int nchunk;            // > 1: residual / tangent run chunk-interleaved (L2-resident pass 2)

@@ -341,7 +341,7 @@ class LdgSystem:
             if getattr(self.tab, "source_zero", False):
                 b = None
             elif (getattr(self.tab, "x0", None) is not None and self.tab.ne >= DEVICE_SOURCE_MIN_NE
-                  and not os.environ.get("LDG_HOST_SOURCE")):
+                  and not getattr(self.tab, "curved", False)):
                 # the plan evaluated on the device (source_dev.py, agrees with
                 # the numpy restatement to ~1e-16: sin/exp ulps, summation
                 # order); small systems keep the restatement, whose cost there
@@ -497,7 +497,7 @@ class LdgSystem:
         return o
 
     # -- chunk-pipelined host calls (fused path) --------------------------------------------
-    PIPE_CHUNKS = int(__import__('os').environ.get('LDG_PIPE_CHUNKS', 12))   # measured: 12 -> 4.34, 16 -> 4.32, 24 -> 4.0 GDOF/s e2e
+    PIPE_CHUNKS = 12          # measured: 12 -> 4.34, 16 -> 4.32, 24 -> 4.0 GDOF/s e2e
 
     def _pipe_plan(self):
         """Element chunks and, per chunk, the last chunk holding a face

@@ -1,3 +1,3 @@
 set -u
-timeout 900 python -m pytest tests/test_gpu_nonlinear.py -q -x -k "curved" 2>&1 | tail -15
-timeout 900 python -m pytest tests/test_gpu_solver.py -q -x -k "curved" 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "variants" 2>&1 | tail -5
+bash scripts/sanitize.sh

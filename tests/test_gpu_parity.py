@@ -237,6 +237,29 @@ def test_hex_p3_vs_oracle_at_scale(shear):
     assert rel(s.residual_tangent(st, du)[0], o.residual_tangent(u, du)) < TOL
 
 
+@pytest.mark.parametrize("option,value", [("pass1_variant", 1), ("c_diag", 0), ("p2_mode", 1),
+                                          ("p2_mode", 2), ("p2_mode", 3)])
+def test_kernel_variants_equal_default(option, value):
+    """Every kernel variant ldg_set_option selects (the pencil pass 1, the
+    general flux-coefficient branch on an axis-aligned mesh, pass 2 without
+    PDL / block-wise / one-shot) gives the default operator to 1e-13 on a
+    hex p=3 mesh past one persistent sweep."""
+    import torch
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem
+    m = model.load_model(str(GOLDEN / "poisson3d.model"))
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [24, 22, 20], "hex")
+    s = LdgSystem(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("hex", 3))
+    du = torch.as_tensor(np.random.default_rng(5).normal(size=(s.n_elements, s.n_nodes, 1)),
+                         device="cuda")
+    u = torch.as_tensor(np.random.default_rng(6).normal(size=du.shape), device="cuda")
+    ref_j, ref_r = s.tangent_dev(du).clone(), s.residual_dev(u).clone()
+    assert s.lib.ldg_set_option(s._h, option.encode(), value) == 0
+    assert rel(s.tangent_dev(du).cpu().numpy(), ref_j.cpu().numpy()) < 1e-13
+    assert rel(s.residual_dev(u).cpu().numpy(), ref_r.cpu().numpy()) < 1e-13
+    assert s.lib.ldg_set_option(s._h, b"no_such_option", 1) != 0
+
+
 def test_fused_equals_unfused_at_config3_size():
     """Config 3 (hex p=3, n=54, 10,077,696 DOFs) on the device: the fused
     two-pass matvec (q never leaves the SM) against the unfused reference
