@@ -168,7 +168,9 @@ multidot_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
 }
 
 // w -= sum_i h[i] V_i (i < k), optional ||w||.  Two entries per thread with
-// 16 B loads, the row loop unrolled by 4 into two accumulator pairs.
+// 16 B loads, the row loop unrolled by 4 into two accumulator pairs.  The
+// coefficient row in shared memory is padded by two doubles: the compiler
+// reads the odd tail as a 16-B pair (compute-sanitizer memcheck).
 __global__ void __launch_bounds__(kThreads)
 update_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
               const double* __restrict__ hcoef, double sign, double* __restrict__ w,
@@ -454,7 +456,7 @@ int ldg_cgs_dots(int64_t n, int k, const double* V, int64_t ldv, const double* w
 
 int ldg_cgs_update(int64_t n, int k, const double* V, int64_t ldv, const double* h,
                    double* w, double* scratch, double* nrm_out, void* stream) {
-  update_kernel<<<kRedBlocks, kThreads, k * sizeof(double), (cudaStream_t)stream>>>(
+  update_kernel<<<kRedBlocks, kThreads, (k + 2) * sizeof(double), (cudaStream_t)stream>>>(
       n, k, V, ldv, h, -1.0, w, scratch, ticket_of(scratch), nrm_out);
   return rc();
 }
@@ -474,7 +476,7 @@ int ldg_dcgs_update(int64_t n, int m, const double* V, int64_t ldv, const double
                     const double* t, double* v, const double* w, double* out,
                     double inv_alpha, double gamma, double* scratch, double* nrm_out,
                     void* stream) {
-  update2_kernel<<<kRedBlocks, kThreads, 2 * (m > 0 ? m : 1) * sizeof(double),
+  update2_kernel<<<kRedBlocks, kThreads, (2 * (m > 0 ? m : 1) + 2) * sizeof(double),
                    (cudaStream_t)stream>>>(n, m, V, ldv, s, t, v, w, out, inv_alpha, gamma,
                                            scratch, ticket_of(scratch), nrm_out);
   return rc();
@@ -482,7 +484,7 @@ int ldg_dcgs_update(int64_t n, int m, const double* V, int64_t ldv, const double
 
 int ldg_combine(int64_t n, int k, const double* Z, int64_t ldz, const double* y,
                 double* x, void* stream) {
-  update_kernel<<<grid_for(n), kThreads, k * sizeof(double), (cudaStream_t)stream>>>(
+  update_kernel<<<grid_for(n), kThreads, (k + 2) * sizeof(double), (cudaStream_t)stream>>>(
       n, k, Z, ldz, y, 1.0, x, nullptr, nullptr, nullptr);
   return rc();
 }

@@ -346,6 +346,10 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
 // traces stay on the FP64 pipe.  Same arithmetic identities and outputs.
 // --------------------------------------------------------------------------
 constexpr int kMmaEpb = 8;
+// per-element pitch of the GEMM operands in shared memory: == 4 (mod 16)
+// doubles, so the 8 elements of a B / C fragment spread over the banks
+// (a multiple of 16 put all 8 in one bank: 4-8-way conflicts)
+__host__ __device__ constexpr int mma_pitch(int n) { return n + ((4 - n % 16) + 16) % 16; }
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -392,11 +396,13 @@ mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict_
   constexpr int EPB = kMmaEpb, NT = EPB * TPE, NW = NT / 32;
   constexpr int MTN = (NB + 7) / 8, MTF = (NQF + 7) / 8;
   __shared__ double su[EPB][NB];
-  __shared__ double snb[EPB][NFACE][NB];
-  __shared__ double sto[EPB][NFACE][NQF];     // own traces
-  __shared__ double sjump[EPB][NFACE][NQF];
-  __shared__ double sg[EPB][ND][NB];          // reference-direction derivatives
-  __shared__ double sl[EPB][NFACE][NB];       // lifted jumps
+  constexpr int PNB = mma_pitch(NFACE * NB);
+  __shared__ double snb[EPB * PNB];                 // neighbour u [e][f][b]
+  constexpr int PF = mma_pitch(NFACE * NQF), PG = mma_pitch(ND * NB), PL = mma_pitch(NFACE * NB);
+  __shared__ double sto[EPB * PF];            // own traces [e][f][s]
+  __shared__ double sjump[EPB * PF];          // [e][f][s]
+  __shared__ double sg[EPB * PG];             // reference-direction derivatives [e][r][a]
+  __shared__ double sl[EPB * PL];             // lifted jumps [e][f][a]
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE, warp = threadIdx.x >> 5;
   const int e = blockIdx.x * EPB + slot;
   const bool active = e < P.ne;
@@ -413,7 +419,7 @@ mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict_
       double a_, b_, wo_, wn_;
       coeffs(P, info[f], a_, b_, wo_, wn_);
       const bool need = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR && a_ != 0.0;
-      snb[slot][f][lt] = need ? __ldg(u + (size_t)nbr[f] * NB + lt) : 0.0;
+      snb[slot * PNB + f * NB + lt] = need ? __ldg(u + (size_t)nbr[f] * NB + lt) : 0.0;
     }
   }
   __syncthreads();
@@ -421,12 +427,12 @@ mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict_
   for (int job = warp; job < NFACE * MTF + ND * MTN; job += NW) {
     if (job < NFACE * MTF) {
       const int f = job / MTF, mt = job % MTF;
-      gemm8_tile<NQF, NB, NQF, NB, 0, 1, 1, NFACE * NQF>(
-          mt, P.phif + f * NB * NQF, &su[0][0], nullptr, nullptr, &sto[0][f][0]);
+      gemm8_tile<NQF, NB, NQF, NB, 0, 1, 1, PF>(
+          mt, P.phif + f * NB * NQF, &su[0][0], nullptr, nullptr, sto + f * NQF);
     } else {
       const int j = job - NFACE * MTF, r = j / MTN, mt = j % MTN;
-      gemm8_tile<NB, NB, NB, NB, 0, 1, 1, ND * NB>(
-          mt, P.dr + r * NB * NB, &su[0][0], nullptr, nullptr, &sg[0][r][0]);
+      gemm8_tile<NB, NB, NB, NB, 0, 1, 1, PG>(
+          mt, P.dr + r * NB * NB, &su[0][0], nullptr, nullptr, sg + r * NB);
     }
   }
   __syncthreads();
@@ -443,23 +449,23 @@ mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict_
         if (kind == LDG_FACE_INTERIOR) {
           const double* po = P.phio + (((inf >> 4) & 7) * P.nperm + ((inf >> 8) & 0xff)) * NB * NQF + sp;
 #pragma unroll
-          for (int b = 0; b < NB; ++b) oth = fma(__ldg(po + b * NQF), snb[slot][f][b], oth);
+          for (int b = 0; b < NB; ++b) oth = fma(__ldg(po + b * NQF), snb[slot * PNB + f * NB + b], oth);
         } else if (kind == LDG_FACE_DIRICHLET && gval) {
           oth = __ldg(gval + (size_t)__ldg(P.fnbr + e * NFACE + f) * NQF + sp);
         }
-        jump = alpha * (sto[slot][f][sp] - oth);
+        jump = alpha * (sto[slot * PF + idx] - oth);
       }
-      sjump[slot][f][sp] = jump;
+      sjump[slot * PF + idx] = jump;
     }
   } else {
-    for (int idx = lt; idx < NFACE * NQF; idx += TPE) sjump[slot][idx / NQF][idx % NQF] = 0.0;
+    for (int idx = lt; idx < NFACE * NQF; idx += TPE) sjump[slot * PF + idx] = 0.0;
   }
   __syncthreads();
   // tensor core: the lifts M_ref^-1 Phi^T W jump, per face
   for (int job = warp; job < NFACE * MTN; job += NW) {
     const int f = job / MTN, mt = job % MTN;
-    gemm8_tile<NB, NQF, NB, NFACE * NQF, 0, 1, 1, NFACE * NB>(
-        mt, P.lift + f * NQF * NB, &sjump[0][f][0], nullptr, nullptr, &sl[0][f][0]);
+    gemm8_tile<NB, NQF, NB, PF, 0, 1, 1, PL>(
+        mt, P.lift + f * NQF * NB, sjump + f * NQF, nullptr, nullptr, sl + f * NB);
   }
   __syncthreads();
   if (!active || lt >= NB) return;
@@ -470,12 +476,12 @@ mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict_
   for (int d = 0; d < ND; ++d) {
     double a = 0.0;
 #pragma unroll
-    for (int r = 0; r < ND; ++r) a = fma(__ldg(g + 1 + d * ND + r), sg[slot][r][lt], a);
+    for (int r = 0; r < ND; ++r) a = fma(__ldg(g + 1 + d * ND + r), sg[slot * PG + r * NB + lt], a);
     qd[d] = -a;
   }
 #pragma unroll
   for (int f = 0; f < NFACE; ++f) {
-    const double fac = __ldg(P.fsj + e * NFACE + f) / detj * sl[slot][f][lt];
+    const double fac = __ldg(P.fsj + e * NFACE + f) / detj * sl[slot * PL + f * NB + lt];
 #pragma unroll
     for (int d = 0; d < ND; ++d) qd[d] = fma(fac, __ldg(P.fnorm + (e * NFACE + f) * ND + d), qd[d]);
   }
@@ -493,19 +499,19 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
                const double* __restrict__ bsrc, double* __restrict__ R) {
   constexpr int EPB = kMmaEpb, NT = EPB * TPE, NW = NT / 32, NV = 1 + ND;
   constexpr int MTN = (NB + 7) / 8, MTF = (NQF + 7) / 8;
-  // dynamic shared memory (> 48 KB at tet p = 3); sR reuses the trace region
+  // dynamic shared memory (> 48 KB at tet p = 3), GEMM operands at
+  // conflict-free element pitches (mma_pitch); sR reuses the trace region
+  constexpr int PV = mma_pitch(NV * NB), PT = mma_pitch(NFACE * NV * NQF);
+  constexpr int PH = mma_pitch(NFACE * NQF), PF = mma_pitch(ND * NB);
   extern __shared__ __align__(16) double dsm[];
-  auto& sv = *reinterpret_cast<double (*)[EPB][NV][NB]>(dsm);                  // u, q_1..q_ND
-  auto& snu = *reinterpret_cast<double (*)[EPB][NFACE][NB]>(dsm + EPB * NV * NB);
-  auto& snq = *reinterpret_cast<double (*)[EPB][NFACE][ND][NB]>(
-      dsm + EPB * (NV + NFACE) * NB);
-  auto& sF = *reinterpret_cast<double (*)[EPB][ND][NB]>(
-      dsm + EPB * (NV + NFACE + NFACE * ND) * NB);                             // -detJ invJ^T f
-  auto& sto = *reinterpret_cast<double (*)[EPB][NFACE][NV][NQF]>(
-      dsm + EPB * (NV + NFACE + NFACE * ND + ND) * NB);                        // own traces
-  auto& sfh = *reinterpret_cast<double (*)[EPB][NFACE * NQF]>(
-      dsm + EPB * (NV + NFACE + NFACE * ND + ND) * NB + EPB * NFACE * NV * NQF);  // sJ f^
-  auto& sR = *reinterpret_cast<double (*)[EPB][NB]>(&sto[0][0][0][0]);
+  double* sv = dsm;                                          // [e][v][b]: u, q_1..q_ND
+  constexpr int PNU = mma_pitch(NFACE * NB), PNQ = mma_pitch(NFACE * ND * NB);
+  double* snu = dsm + EPB * PV;                                     // [e][f][b] neighbour u
+  double* snq = snu + EPB * PNU;                                    // [e][f][d][b] neighbour q
+  double* sF = snq + EPB * PNQ;                                     // [e][r][b]: -detJ invJ^T f
+  double* sto = sF + EPB * PF;                                      // [e][f][v][s] own traces
+  double* sfh = sto + EPB * PT;                                     // [e][f s]: sJ f^
+  double* sR = sto;                                                 // [e][a]
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE, warp = threadIdx.x >> 5;
   const int e = blockIdx.x * EPB + slot;
   const bool active = e < P.ne;
@@ -525,9 +531,10 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
       for (int r = 0; r < ND; ++r) ij[d][r] = __ldg(g + 1 + d * ND + r);
   }
   if (lt < NB) {
-    sv[slot][0][lt] = active ? __ldg(u + (size_t)e * NB + lt) : 0.0;
+    sv[slot * PV + lt] = active ? __ldg(u + (size_t)e * NB + lt) : 0.0;
 #pragma unroll
-    for (int d = 0; d < ND; ++d) sv[slot][1 + d][lt] = active ? __ldg(q + ((size_t)e * NB + lt) * ND + d) : 0.0;
+    for (int d = 0; d < ND; ++d)
+      sv[slot * PV + (1 + d) * NB + lt] = active ? __ldg(q + ((size_t)e * NB + lt) * ND + d) : 0.0;
 #pragma unroll
     for (int f = 0; f < NFACE; ++f) {
       double alpha, beta, wo, wn;
@@ -535,10 +542,11 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
       const bool inter = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR;
       const bool nu = inter && (alpha != 0.0 || beta != 0.0);
       const bool nq = inter && wn != 0.0;
-      snu[slot][f][lt] = nu ? __ldg(u + (size_t)nbr[f] * NB + lt) : 0.0;
+      snu[slot * PNU + f * NB + lt] = nu ? __ldg(u + (size_t)nbr[f] * NB + lt) : 0.0;
 #pragma unroll
       for (int d = 0; d < ND; ++d)
-        snq[slot][f][d][lt] = nq ? __ldg(q + ((size_t)nbr[f] * NB + lt) * ND + d) : 0.0;
+        snq[slot * PNQ + (f * ND + d) * NB + lt] =
+            nq ? __ldg(q + ((size_t)nbr[f] * NB + lt) * ND + d) : 0.0;
     }
   }
   __syncthreads();
@@ -549,9 +557,10 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
       double a = 0.0;
-      if (P.flux_uses_u) a = fma(P.au[d * LDG_MAX_NCU], sv[slot][0][lt], a);
+      if (P.flux_uses_u) a = fma(P.au[d * LDG_MAX_NCU], sv[slot * PV + lt], a);
 #pragma unroll
-      for (int x = 0; x < ND; ++x) a = fma(P.aq[d * LDG_MAX_NCU * 3 + x], sv[slot][1 + x][lt], a);
+      for (int x = 0; x < ND; ++x)
+        a = fma(P.aq[d * LDG_MAX_NCU * 3 + x], sv[slot * PV + (1 + x) * NB + lt], a);
       f[d] = a;
     }
 #pragma unroll
@@ -559,14 +568,14 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
       double a = 0.0;
 #pragma unroll
       for (int d = 0; d < ND; ++d) a = fma(ij[d][r], f[d], a);
-      sF[slot][r][lt] = -detj * a;
+      sF[slot * PF + r * NB + lt] = -detj * a;
     }
   }
   // tensor core: own traces of u and q on every face
   for (int job = warp; job < NFACE * NV * MTF; job += NW) {
     const int f = job / (NV * MTF), v = (job / MTF) % NV, mt = job % MTF;
-    gemm8_tile<NQF, NB, NQF, NV * NB, 0, 1, 1, NFACE * NV * NQF>(
-        mt, P.phif + f * NB * NQF, &sv[0][v][0], nullptr, nullptr, &sto[0][f][v][0]);
+    gemm8_tile<NQF, NB, NQF, PV, 0, 1, 1, PT>(
+        mt, P.phif + f * NB * NQF, sv + v * NB, nullptr, nullptr, sto + (f * NV + v) * NQF);
   }
   __syncthreads();
   if (active) {
@@ -579,24 +588,28 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
       const int kind = inf & LDG_FACE_KIND_MASK;
       const bool inter = kind == LDG_FACE_INTERIOR;
       const double* po = P.phio + (((inf >> 4) & 7) * P.nperm + ((inf >> 8) & 0xff)) * NB * NQF + sp;
-      const double uo = sto[slot][f][0][sp];
-      double un = 0.0;
-      if (inter && (alpha != 0.0 || beta != 0.0)) {
+      const double* to = sto + slot * PT + f * NV * NQF + sp;
+      const double uo = to[0];
+      // neighbour traces: one pass over the orientation's tabulation feeds u
+      // and every q component (each entry loaded once)
+      double un = 0.0, qn[ND];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) un = fma(__ldg(po + b * NQF), snu[slot][f][b], un);
+      for (int d = 0; d < ND; ++d) qn[d] = 0.0;
+      const bool need_u = inter && (alpha != 0.0 || beta != 0.0), need_q = inter && wn != 0.0;
+      if (need_u || need_q) {
+#pragma unroll 4
+        for (int b = 0; b < NB; ++b) {
+          const double ph = __ldg(po + b * NQF);
+          un = fma(ph, snu[slot * PNU + f * NB + b], un);
+#pragma unroll
+          for (int d = 0; d < ND; ++d) qn[d] = fma(ph, snq[slot * PNQ + (f * ND + d) * NB + b], qn[d]);
+        }
       } else if (!inter && !TANGENT && gval) {
         un = __ldg(gval + (size_t)nbf * NQF + sp);
       }
       double qh[ND];
 #pragma unroll
-      for (int d = 0; d < ND; ++d) {
-        double b2 = 0.0;
-        if (inter && wn != 0.0) {
-#pragma unroll
-          for (int b = 0; b < NB; ++b) b2 = fma(__ldg(po + b * NQF), snq[slot][f][d][b], b2);
-        }
-        qh[d] = wo * sto[slot][f][1 + d][sp] + wn * b2;
-      }
+      for (int d = 0; d < ND; ++d) qh[d] = wo * to[(1 + d) * NQF] + wn * qn[d];
       double fh;
       if (kind == LDG_FACE_NEUMANN) {
         fh = (!TANGENT && gval) ? __ldg(gval + (size_t)nbf * NQF + sp) : 0.0;
@@ -613,19 +626,19 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
         }
         fh = fn + beta * __ldg(P.ftau + e * NFACE + f) * (uo - un);
       }
-      sfh[slot][idx] = __ldg(P.fsj + e * NFACE + f) * fh;
+      sfh[slot * PH + idx] = __ldg(P.fsj + e * NFACE + f) * fh;
     }
   } else {
-    for (int idx = lt; idx < NFACE * NQF; idx += TPE) sfh[slot][idx] = 0.0;
+    for (int idx = lt; idx < NFACE * NQF; idx += TPE) sfh[slot * PH + idx] = 0.0;
   }
   __syncthreads();
   // tensor core: R = sum_r K_r (-F_r) + sum_f Phi_f^T W (sJ f^)
   for (int mt = warp; mt < MTN; mt += NW)
-    gemm8_tile<NB, ND * NB, NB, ND * NB, NFACE * NQF, NB, NFACE * NQF, NB>(
-        mt, P.kr, &sF[0][0][0], P.fluxop, &sfh[0][0], &sR[0][0]);
+    gemm8_tile<NB, ND * NB, NB, PF, NFACE * NQF, NB, PH, NB>(
+        mt, P.kr, sF, P.fluxop, sfh, sR);
   __syncthreads();
   if (!active || lt >= NB) return;
-  double out = sR[slot][lt];
+  double out = sR[slot * NB + lt];
   if (!TANGENT && bsrc) out += __ldg(bsrc + (size_t)e * NB + lt);
   dbad(P, e, out);
   R[(size_t)e * NB + lt] = out;
@@ -642,7 +655,9 @@ int run_dense(const DenseParams& P, int what, const double* u, const double* gva
     // tensor-core variants (8 elements per block, batched operator GEMMs)
     const int gm = (P.ne + kMmaEpb - 1) / kMmaEpb;
     constexpr int fsm = (int)sizeof(double) * kMmaEpb *
-                        ((1 + ND + NFACE + NFACE * ND + ND) * NB + NFACE * (1 + ND) * NQF + NFACE * NQF);
+                        (mma_pitch((1 + ND) * NB) + mma_pitch(NFACE * NB) + mma_pitch(NFACE * ND * NB) +
+                         mma_pitch(ND * NB) +
+                         mma_pitch(NFACE * (1 + ND) * NQF) + mma_pitch(NFACE * NQF));
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(flux_dense_mma<NB, NQF, NFACE, ND, TPE, false>,

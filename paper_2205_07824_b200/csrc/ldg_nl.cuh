@@ -130,6 +130,15 @@ __device__ __forceinline__ void contract_u(const double* __restrict__ in, double
   constexpr int OSTR = AX == 0 ? 1 : (AX == 1 ? O0 : O0 * O1);
   (void)I2;
   (void)O2;
+  // x-axis pencils sit NIN (NOUT) doubles apart, so with an even length the
+  // lanes of a warp hit the same banks (4-way at 4): those reads / writes are
+  // issued in a lane-rotated order (rotation s = (lane / G) mod len, G =
+  // 16 / gcd(len, 16)) and put back in registers with selects -- 2 shared
+  // wavefronts per 256 B instead of 8; the arithmetic order is unchanged
+  constexpr bool SKEW_IN = AX == 0 && NIN % 2 == 0;
+  constexpr bool SKEW_OUT = AX == 0 && NOUT % 2 == 0;
+  constexpr int GIN = NIN % 8 == 0 ? 2 : (NIN % 4 == 0 ? 4 : 8);
+  constexpr int GOUT = NOUT % 8 == 0 ? 2 : (NOUT % 4 == 0 ? 4 : 8);
   const int total = nvar * NPN;
   for (int idx = tid; idx < total; idx += NT) {
     const int v = idx / NPN, r = idx - v * NPN;
@@ -137,14 +146,50 @@ __device__ __forceinline__ void contract_u(const double* __restrict__ in, double
     const int ib = v * ISZ + p0 + p1 * I0 + p2 * I0 * I1;
     const int ob = v * OSZ + p0 + p1 * O0 + p2 * O0 * O1;
     double x[NIN];
+    if (SKEW_IN) {
+      const int sh = ((idx & 31) / GIN) % NIN;
+      double rr[NIN];
 #pragma unroll
-    for (int i = 0; i < NIN; ++i) x[i] = in[ib + i * ISTR];
+      for (int j = 0; j < NIN; ++j) {
+        int jj = j + sh;
+        if (jj >= NIN) jj -= NIN;
+        rr[j] = in[ib + jj];
+      }
+#pragma unroll
+      for (int i = 0; i < NIN; ++i) {
+        double val = rr[i];
+#pragma unroll
+        for (int k = 1; k < NIN; ++k)
+          if (sh == k) val = rr[(i - k + NIN) % NIN];
+        x[i] = val;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NIN; ++i) x[i] = in[ib + i * ISTR];
+    }
+    double y[NOUT];
 #pragma unroll
     for (int o = 0; o < NOUT; ++o) {
       double acc = 0.0;
 #pragma unroll
       for (int i = 0; i < NIN; ++i) acc = fma(op_c<OPID>(TRANS ? i * N1 + o : o * N1 + i), x[i], acc);
-      out[ob + o * OSTR] = acc;
+      y[o] = acc;
+    }
+    if (SKEW_OUT) {
+      const int sh = ((idx & 31) / GOUT) % NOUT;
+#pragma unroll
+      for (int j = 0; j < NOUT; ++j) {
+        int jj = j + sh;
+        if (jj >= NOUT) jj -= NOUT;
+        double val = y[j];
+#pragma unroll
+        for (int k = 1; k < NOUT; ++k)
+          if (sh == k) val = y[(j + k) % NOUT];
+        out[ob + jj] = val;
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) out[ob + o * OSTR] = y[o];
     }
   }
 }

@@ -800,26 +800,53 @@ class ReducedBasisPreconditioner:
         return out
 
 
-def build_reduced_basis(snapshots, op, rank=None, drop_tol=1e-10):
-    """Orthonormalise the snapshots (device QR), H = W^T (J W) through the
-    matrix-free operator, rank-deficient directions dropped
-    (solver.py:402-423).  Column signs of Q may differ from numpy's; W H^-1 W^T
-    and W W^T are invariant to them."""
+def build_reduced_basis(snapshots, op, rank=None, drop_tol=1e-10, ops=None):
+    """Orthonormalise the snapshots, H = W^T (J W) through the matrix-free
+    operator, rank-deficient directions dropped (solver.py:402-423).  The
+    reference's Householder QR is replaced by classical Gram-Schmidt with a
+    second pass on the device vector kernels (ldg_cgs_dots / ldg_cgs_update /
+    ldg_nrm2; allreduced through ``ops`` on partitioned systems): the same
+    R diagonal |R_jj| (the norm of s_j's component orthogonal to the earlier
+    snapshots) decides what is dropped, and W H^-1 W^T and W W^T do not depend
+    on which orthonormal basis of the span is taken (column signs included)."""
     import torch
     if len(snapshots) == 0:
         raise SolverError("reduced basis needs at least one snapshot")
-    S = torch.stack([s.reshape(-1) for s in snapshots], dim=1)
+    snaps = [s.reshape(-1) for s in snapshots]
     if rank is not None:
-        S = S[:, -rank:]
-    Q, R = torch.linalg.qr(S, mode="reduced")
-    d = torch.abs(torch.diagonal(R)).cpu().numpy()
-    keep = d > drop_tol * max(1.0, float(d.max()))
+        snaps = snaps[-rank:]
+    dev = snaps[0].device
+    ops = ops or vecops(dev)
+    k, n = len(snaps), snaps[0].numel()
+    Q = torch.empty((k, n), dtype=torch.float64, device=dev)
+    h = torch.zeros(max(k, 1), dtype=torch.float64, device=dev)
+    h2 = torch.zeros_like(h)
+    nr = torch.zeros(2, dtype=torch.float64, device=dev)
+    rdiag = np.zeros(k)
+    for j in range(k):
+        w = Q[j]
+        w.copy_(snaps[j])
+        if j:
+            ops.cgs_dots(Q, j, w, h)
+            ops.cgs_update(Q, j, h, w, None)
+            ops.cgs_dots(Q, j, w, h2)                   # reorthogonalisation pass
+            ops.cgs_update(Q, j, h2, w, None)
+        ops.nrm2(w, nr[0:1])
+        rdiag[j] = float(nr[0].item())
+        if rdiag[j] > 0.0:
+            ops.div(w, nr[0:1], w)
+    keep = rdiag > drop_tol * max(1.0, float(rdiag.max()))
     if not keep.any():
         raise SolverError("all snapshot directions are degenerate")
-    W = Q[:, torch.as_tensor(np.nonzero(keep)[0], device=Q.device)].T.contiguous()
+    W = Q[torch.as_tensor(np.nonzero(keep)[0], device=dev)].contiguous()
     apply_op = op if callable(op) else op.apply
-    JW = torch.stack([apply_op(W[k]) for k in range(W.shape[0])])
-    H = (W @ JW.T).cpu().numpy()
+    r = W.shape[0]
+    H = np.zeros((r, r))
+    hc = torch.zeros(r, dtype=torch.float64, device=dev)
+    for c in range(r):
+        jw = apply_op(W[c]).reshape(-1).contiguous()
+        ops.cgs_dots(W, r, jw, hc)                      # column c of W^T J W
+        H[:, c] = hc.cpu().numpy()
     return ReducedBasisPreconditioner(W, scipy.linalg.lu_factor(H))
 
 
