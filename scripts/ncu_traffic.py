@@ -27,7 +27,7 @@ for r in rows[2:]:
     name = r[idx["Kernel Name"]]
     b = mb(r, "dram__bytes_read.sum") + mb(r, "dram__bytes_write.sum")
     key = "pass1" if ("plane_kernel" in name or "fused_kernel" in name) else (
-        "pass2" if "complete_kernel" in name else name[:40])
+        "pass2" if "complete" in name else name[:40])
     res.setdefault(key, b)
     res.setdefault(key + "_kernel", name[:80])
 json.dump(res, open("profiles/traffic.json", "w"), indent=1)
