@@ -223,6 +223,11 @@ int ldg_axpy(int64_t n, double a_host, const double* a_dev, double sign,
 /* y = x * (1 / *den_dev)  (reference: V[k+1] = w / H[k+1,k]) */
 int ldg_div_scalar(int64_t n, const double* x, const double* den_dev, double* y,
                    void* stream);
+/* y = x / *den where *den > thr, y untouched otherwise (a NaN den included):
+ * the DCGS2 normalisation without reading den on the host (solver.py:142's
+ * breakdown test is taken on the host one dot sweep later) */
+int ldg_div_scalar_guarded(int64_t n, const double* x, const double* den, double thr,
+                           double* y, void* stream);
 /* fused MGS step: w -= h_in * Vi ; h_out = <Vnext, w> (Vnext may be NULL) */
 int ldg_mgs_step(int64_t n, const double* vi, const double* h_in, double* w,
                  const double* vnext, double* scratch, double* h_out,

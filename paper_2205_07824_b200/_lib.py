@@ -93,6 +93,8 @@ _SIGS = {
     "ldg_axpy": ([C.c_int64, C.c_double, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p,
                   C.c_void_p], C.c_int),
     "ldg_div_scalar": ([C.c_int64] + [C.c_void_p] * 4, C.c_int),
+    "ldg_div_scalar_guarded": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                C.c_void_p], C.c_int),
     "ldg_mgs_step": ([C.c_int64] + [C.c_void_p] * 7, C.c_int),
     "ldg_cgs_dots": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                       C.c_void_p, C.c_void_p], C.c_int),

@@ -557,9 +557,10 @@ int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, doubl
     const size_t a = (size_t)starts[c] * row, n = (size_t)(starts[c + 1] - starts[c]) * row;
     const double* src = v_host + a;
     if (stage) {
-      // 1 MB slices over the host threads (first touch of the pinned pages
-      // happened at allocation; memcpy bandwidth scales with threads)
-      const int64_t slice = 1 << 17, ns = (int64_t)((n + slice - 1) / slice);
+      // 64 KB slices over the host threads: a ~7 MB chunk spreads over every
+      // core (1 MB slices left most threads idle: memcpy bandwidth scales
+      // with the threads copying)
+      const int64_t slice = 1 << 13, ns = (int64_t)((n + slice - 1) / slice);
 #pragma omp parallel for schedule(static)
       for (int64_t k = 0; k < ns; ++k) {
         const size_t o = (size_t)k * slice, m = std::min((size_t)slice, n - o);

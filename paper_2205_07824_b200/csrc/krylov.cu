@@ -314,6 +314,108 @@ multidot2_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// The whole DCGS2 dot sweep in ONE launch: block (c, s) of a 2D grid takes
+// basis rows [8c, 8c + 8) over column slab s, with the row chunk c varying
+// fastest in launch order, so the ceil(k / 8) blocks of one slab run
+// together and read that slab of x and y from DRAM once (the others hit L2;
+// the chunked launches re-read x and y from DRAM per chunk).  Per-(row, slab)
+// partials, summed in slab order by the last block: deterministic.
+#ifndef LDG_UPD2_UNROLL
+#define LDG_UPD2_UNROLL 4
+#endif
+constexpr int kUpd2Unroll = LDG_UPD2_UNROLL;
+#ifndef LDG_DCGS_ALL
+#define LDG_DCGS_ALL 1                 // A/B: 0 = one launch per 8-row chunk
+#endif
+constexpr int kDcSlabs = 296;          // 2 x 148 SMs
+constexpr int kDcMaxK = 512;           // restart <= 511
+__global__ void __launch_bounds__(kThreads)
+multidot2_all_kernel(int64_t n, int k, const double* __restrict__ V, int64_t ldv,
+                     const double* __restrict__ x, const double* __restrict__ y,
+                     double* partials, unsigned int* ticket, double* hx, double* hy) {
+  __shared__ double red[2 * kDc][kThreads / 32];
+  const int c = blockIdx.x, slab = blockIdx.y, nslab = gridDim.y;
+  const int r0 = c * kDc, kk = min(kDc, k - r0);
+  double ax[kDc], ay[kDc];
+#pragma unroll
+  for (int r = 0; r < kDc; ++r) ax[r] = ay[r] = 0.0;
+  const int64_t n2 = n >> 1;
+  const int64_t per = (n2 + nslab - 1) / nslab;
+  const int64_t i0 = (int64_t)slab * per, i1 = min(n2, i0 + per);
+  const double* Vc = V + (int64_t)r0 * ldv;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
+    const double2 xv = reinterpret_cast<const double2*>(x)[i];
+    const double2 yv = reinterpret_cast<const double2*>(y)[i];
+#pragma unroll
+    for (int r = 0; r < kDc; ++r)
+      if (r < kk) {
+        const double2 v = reinterpret_cast<const double2*>(Vc + (int64_t)r * ldv)[i];
+        ax[r] = fma(v.y, xv.y, fma(v.x, xv.x, ax[r]));
+        ay[r] = fma(v.y, yv.y, fma(v.x, yv.x, ay[r]));
+      }
+  }
+  if ((n & 1) && slab == nslab - 1 && threadIdx.x == 0) {
+    const int64_t i = n - 1;
+#pragma unroll
+    for (int r = 0; r < kDc; ++r)
+      if (r < kk) {
+        ax[r] = fma(Vc[(int64_t)r * ldv + i], x[i], ax[r]);
+        ay[r] = fma(Vc[(int64_t)r * ldv + i], y[i], ay[r]);
+      }
+  }
+  // all 2 kk sums of the block at once: warp shuffles, then one pass over warps
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < kDc; ++r) {
+    double a = ax[r], b = ay[r];
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+      red[r][warp] = a;
+      red[kDc + r][warp] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * kDc) {
+    const int v = threadIdx.x, r = v % kDc;
+    if (r < kk) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < kThreads / 32; ++w2) t += red[v][w2];
+      const int row = (v < kDc ? 0 : k) + r0 + r;            // x rows [0, k), y rows [k, 2k)
+      partials[(size_t)row * nslab + slab] = t;
+    }
+  }
+  (void)ticket; (void)hx; (void)hy;
+}
+
+// the per-row sums of multidot2_all_kernel's partials: one warp per row
+// (fixed lane / slab assignment and shuffle tree: deterministic)
+__global__ void __launch_bounds__(kThreads)
+multidot2_finish_kernel(int k, int nslab, const double* __restrict__ partials, double* hx,
+                        double* hy) {
+  const int v = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (v >= 2 * k) return;
+  double s = 0.0;
+  for (int b = lane; b < nslab; b += 32) s += partials[(size_t)v * nslab + b];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) (v < k ? hx[v] : hy[v - k]) = s;
+}
+
+// y = x / *den where *den > thr, untouched otherwise (also for a NaN den):
+// the DCGS2 normalisation of the next basis vector without a host round
+// trip; the host sees den with the next dot sweep and handles breakdown
+__global__ void div_guarded_kernel(int64_t n, const double* __restrict__ x,
+                                   const double* __restrict__ den, double thr,
+                                   double* __restrict__ y) {
+  const double d = *den;
+  if (!(d > thr)) return;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
+    y[i] = x[i] / d;
+}
+
 // DCGS2 update, one sweep over V_0..V_{m-1}: the final basis vector
 // vf = (v - sum_j s_j V_j) * inv_alpha (written over v) and the projected
 // Krylov vector w1 = (w - sum_j t_j V_j - gamma vf) * inv_alpha (into out),
@@ -341,7 +443,9 @@ update2_kernel(int64_t n, int m, const double* __restrict__ V, int64_t ldv,
     const int64_t n2 = n >> 1;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n2; i += stride) {
       double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
-#pragma unroll 4
+      // LDG_UPD2_UNROLL rows in flight per thread (memory-level parallelism
+      // of the m-row sweep); the accumulation order over r is unchanged
+#pragma unroll kUpd2Unroll
       for (int r = 0; r < m; ++r) {
         const double2 vr = reinterpret_cast<const double2*>(V + (int64_t)r * ldv)[i];
         ax = fma(cs[r], vr.x, ax);
@@ -406,7 +510,9 @@ inline int rc() { return cudaGetLastError() == cudaSuccess ? 0 : 3; }
 
 extern "C" {
 
-int64_t ldg_reduce_scratch_doubles(void) { return (int64_t)kRedBlocks * kScratchRows + 8; }
+int64_t ldg_reduce_scratch_doubles(void) {
+  return (int64_t)kRedBlocks * kScratchRows + 8 + (int64_t)2 * kDcMaxK * kDcSlabs;
+}
 
 // NOTE: reductions always launch the full kRedBlocks grid so partial counts
 // (and therefore rounding) do not depend on n.
@@ -427,6 +533,12 @@ int ldg_axpy(int64_t n, double a_host, const double* a_dev, double sign,
              const double* x, double* y, void* stream) {
   axpy_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, a_host, a_dev,
                                                                   sign, x, y);
+  return rc();
+}
+
+int ldg_div_scalar_guarded(int64_t n, const double* x, const double* den, double thr,
+                           double* y, void* stream) {
+  div_guarded_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, den, thr, y);
   return rc();
 }
 
@@ -463,6 +575,19 @@ int ldg_cgs_update(int64_t n, int k, const double* V, int64_t ldv, const double*
 
 int ldg_dcgs_dots(int64_t n, int k, const double* V, int64_t ldv, const double* x,
                   const double* y, double* scratch, double* hx, double* hy, void* stream) {
+  const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+  if (LDG_DCGS_ALL && k > 0 && k <= kDcMaxK && vec && n >= 2 * kDcSlabs) {
+    double* part = scratch + (size_t)kRedBlocks * kScratchRows + 8;
+    const dim3 grid((unsigned)((k + kDc - 1) / kDc), kDcSlabs);
+    multidot2_all_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        n, k, V, ldv, x, y, part, ticket_of(scratch), hx, hy);
+    const int wpb = kThreads / 32;
+    multidot2_finish_kernel<<<(2 * k + wpb - 1) / wpb, kThreads, 0, (cudaStream_t)stream>>>(
+        k, kDcSlabs, part, hx, hy);
+    return rc();
+  }
   for (int r0 = 0; r0 < k; r0 += kDc) {
     const int kk = k - r0 < kDc ? k - r0 : kDc;
     multidot2_kernel<<<kRedBlocks, kThreads, 0, (cudaStream_t)stream>>>(

@@ -321,6 +321,9 @@ class DistVecOps:
     def div(self, *a, **k):
         return self.b.div(*a, **k)
 
+    def div_guarded(self, *a, **k):
+        return self.b.div_guarded(*a, **k)
+
     def mgs_step(self, vi, h_in, w, vnext, h_out):
         self.b.mgs_step(vi, h_in, w, vnext, h_out)
         if vnext is not None:

@@ -133,6 +133,11 @@ class VecOps:
         _lib.check(self.lib.ldg_div_scalar(x.numel(), _lib.ptr(x), _lib.ptr(den_dev),
                                            _lib.ptr(out), self._st()), "ldg_div_scalar")
 
+    def div_guarded(self, x, den_dev, thr, out):
+        _lib.check(self.lib.ldg_div_scalar_guarded(x.numel(), _lib.ptr(x), _lib.ptr(den_dev),
+                                                   float(thr), _lib.ptr(out), self._st()),
+                   "ldg_div_scalar_guarded")
+
     def mgs_step(self, vi, h_in, w, vnext, h_out):
         _lib.check(self.lib.ldg_mgs_step(w.numel(), _lib.ptr(vi), _lib.ptr(h_in), _lib.ptr(w),
                                          _lib.ptr(vnext), _lib.ptr(self.scratch),
@@ -426,15 +431,23 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
         ws = _WS.get(m, n, dev, need_z=False)
         V, w, nr = ws.V, ws.w, ws.nrm
         dx, dy, sd, td = ws.dv[0], ws.dv[1], ws.dv[2], ws.dv[3]
+        # s | t go to the device in one pinned copy per iteration (the stream
+        # has synchronised on the next dot read before the buffer is reused)
+        st_h = torch.empty(2 * (m + 2), dtype=torch.float64, pin_memory=dev.type == "cuda")
+        st_d = torch.empty(2 * (m + 2), dtype=torch.float64, device=dev)
         thr = 1e-14 * max(bnorm, 1.0)
         Hr = np.zeros((m + 1, m))
         R = np.zeros((m + 1, m))
         cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
         g[0] = beta
         torch.div(r, beta, out=V[0])
+        nr.zero_()
         ncol, lucky = 0, False
         for k in range(m + 1):
-            if k < m and not lucky:
+            # one host round trip per iteration: the dots of this sweep and
+            # the norm nu of the previous update (its breakdown test deferred
+            # to here; the normalisation ran on the device only when nu > thr)
+            if k < m:
                 apply_op_into(w, V[k])
                 ops.dcgs_dots(V, k + 1, V[k], w, dx, dy)
             else:                                   # finalise the last column only
@@ -442,6 +455,14 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
             hv = torch.cat([dx[: k + 1], dy[: k + 1], nr[0:1]]).cpu().numpy()
             if not np.isfinite(hv).all():
                 raise SolverError("gmres: operator returned non-finite values")
+            if k:
+                nu = float(hv[2 * k + 2])
+                lucky = nu <= thr
+                if lucky and k < m:
+                    # exact breakdown: V[k] is final unnormalised, the operator
+                    # is not applied to it (solver.py:142); redo the sweep
+                    ops.dcgs_dots(V, k + 1, V[k], V[k], dx, dy)
+                    hv = torch.cat([dx[: k + 1], dy[: k + 1], nr[0:1]]).cpu().numpy()
             if k == 0:
                 s = np.zeros(0)
                 alpha, nu = 1.0, 1.0
@@ -464,18 +485,12 @@ def _gmres_dcgs2(apply_op, M, b, x, have_x0, bnorm, tol, restart, max_iter, ops,
             Hr[:k, k] = (t - Hs[:k]) / alpha
             Hr[k, k] = (gamma - Hs[k]) / alpha
             if k:
-                sd[:k].copy_(torch.as_tensor(s, device=dev))
-                td[:k].copy_(torch.as_tensor(t, device=dev))
-            ops.dcgs_update(V, k, sd, td, V[k], w, V[k + 1], 1.0 / alpha, gamma, nr[0:1])
-            # exact (lucky) breakdown: the projected vector vanished, so the
-            # next column is final without normalising it (0/0) or applying
-            # the operator to it (solver.py:142)
-            nu = float(nr[0].item())
-            if not np.isfinite(nu):
-                raise SolverError("gmres: operator returned non-finite values")
-            lucky = nu <= thr
-            if not lucky:
-                ops.div(V[k + 1], nr[0:1], V[k + 1])
+                st_h[:k] = torch.from_numpy(np.ascontiguousarray(s))
+                st_h[k:2 * k] = torch.from_numpy(np.ascontiguousarray(t))
+                st_d[: 2 * k].copy_(st_h[: 2 * k], non_blocking=True)
+            ops.dcgs_update(V, k, st_d[:k], st_d[k: 2 * k] if k else st_d[:0], V[k], w, V[k + 1],
+                            1.0 / alpha, gamma, nr[0:1])
+            ops.div_guarded(V[k + 1], nr[0:1], thr, V[k + 1])
         if ncol:
             y = scipy.linalg.solve_triangular(R[:ncol, :ncol], g[:ncol])
             u = w

@@ -41,6 +41,10 @@ class CpuOps:
     def div(self, x, den, out):
         torch.div(x, den, out=out)
 
+    def div_guarded(self, x, den, thr, out):
+        if float(den) > thr:
+            torch.div(x, den, out=out)
+
     def mgs_step(self, vi, h_in, w, vnext, h_out):
         if vi is not None:
             w.sub_(h_in * vi)
