@@ -153,6 +153,44 @@ def run_solve(system, orth="dcgs2"):
             "final_residual": stats.final_residual, "error_u": err}
 
 
+def run_strong(args, world, dev, steps=10):
+    """Strong scaling beside the weak-scaling headline: the fixed config-3
+    box (n^3 hexes in total, 10.08M DOFs at n = 54) split into `world`
+    x-slabs, the partitioned tangent matvec timed like the headline (CUDA
+    events on the stream, L2 flushed, max over ranks).  GDOF/s of the whole
+    box; the driver computes efficiency from per-N values itself."""
+    import torch
+    import torch.distributed as dist
+    from paper_2205_07824_b200.parallel import PartitionedLdgSystem
+    m, mesh, topo, master = build_problem(args.n, nx_mult=1)
+    ps = PartitionedLdgSystem(m, mesh, topo, master, world, int(os.environ.get("RANK", 0)),
+                              device=dev)
+    g = torch.Generator(device=dev).manual_seed(7)
+    du = torch.randn((ps.n_elements, ps.n_nodes, 1), dtype=torch.float64, device=dev, generator=g)
+    dR = torch.empty_like(du)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        ps.tangent_dev(du, out=dR)
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+    torch.cuda.synchronize()
+    dist.barrier()
+    for k in range(steps):
+        flush.fill_(float(k))
+        ev[k][0].record(stream)
+        ps.tangent_dev(du, out=dR)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    t = torch.tensor([ms], dtype=torch.float64,
+                     device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total = mesh.connectivity.shape[0] * master.n_nodes
+    return {"workload": f"config 3 box n={args.n} (fixed, {total} DOFs) split over {world} ranks",
+            "dofs": total, "ms_per_step": ms, "gdofs": total / (ms * 1e-3) / 1e9}
+
+
 def run_solve_partitioned(s, world):
     """Newton-GMRES time to solution on the N-slab box (each rank one slab;
     allreduced DCGS2, rank-local block-Jacobi, face-node halos), the max over
@@ -548,6 +586,7 @@ def run_b200(args, rank, world):
     solve_line = None
     if world > 1 and not args.no_solve:
         solve_line = run_solve_partitioned(s, world)
+    strong_line = run_strong(args, world, dev) if world > 1 else None
     if rank != 0:
         return
     pk = peaks()
@@ -613,6 +652,8 @@ def run_b200(args, rank, world):
             line["solve"]["cpu_oracle_small"] = {"n": 3, **cpu_solve(3)}
     if world > 1 and solve_line is not None:
         line["solve"] = solve_line
+    if strong_line is not None:
+        line["strong_scaling"] = strong_line
     if world == 1 and not args.no_tet:
         line["tet"] = tet_line(hbm)
     if world == 1 and not args.no_nonlinear:

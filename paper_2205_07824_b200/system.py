@@ -157,6 +157,13 @@ class LdgSystem:
         self._bdata = {}
         self._src = {}
         self._devsrc = None
+        if (not self.dense and self.nl is None and not getattr(self.tab, "source_zero", False)
+                and getattr(self.tab, "x0", None) is not None and self.tab.ne >= DEVICE_SOURCE_MIN_NE
+                and not getattr(self.tab, "curved", False)):
+            # NVRTC-compile the source plan now (setup) rather than inside the
+            # first residual of a solve
+            from .source_dev import DeviceSource
+            self._devsrc = DeviceSource(self.tab, self.device)
         self._scratch = {}
 
     # -- native handle -------------------------------------------------------------

@@ -1,2 +1,3 @@
 set -u
-ORTH=dcgs2 bash scripts/ab_solve.sh variants/upd8/libldgb200.so
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+ORTH=dcgs2 bash scripts/ab_solve.sh
