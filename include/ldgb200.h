@@ -190,6 +190,10 @@ int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, doubl
  * buffer.  ghost0 < 0 switches it off.  (Reference: none -- the reference is
  * single-process; this is the B200 multi-GPU layer.) */
 int ldg_set_ghost_rows(LdgHandle* h, int ghost0, const double* u_ghost);
+/* the same for simplex (dense) handles: ghost rows of u and of the mixed
+ * gradient q (the flux pass reads the neighbours' q) */
+int ldg_set_ghost_rows_dense(LdgHandle* h, int ghost0, const double* u_ghost,
+                             const double* q_ghost);
 
 /* Kernel-selection options of a tensor handle (A/B measurements, tests);
  * the defaults are the measured-best choices: "pass1_variant" (0 plane |
@@ -199,7 +203,8 @@ int ldg_set_ghost_rows(LdgHandle* h, int ghost0, const double* u_ghost);
 int ldg_set_option(LdgHandle* h, const char* name, int value);
 
 /* Unfused reference structure, kept for comparison: flux pass from a
- * precomputed q = compute_mixed(u) (72 B/DOF of HBM traffic at nd = 3). */
+ * precomputed q = compute_mixed(u) (72 B/DOF of HBM traffic at nd = 3); on
+ * simplex handles the dense flux pass (disc.py:595-653 given q). */
 int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
                         const double* q, const double* gproj,
                         const double* bsrc, double* R, void* stream);

@@ -74,6 +74,7 @@ _SIGS = {
     "ldg_set_export_layout": ([C.c_void_p, C.c_int], C.c_int),
     "ldg_set_ghost_rows": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
     "ldg_set_option": ([C.c_void_p, C.c_char_p, C.c_int], C.c_int),
+    "ldg_set_ghost_rows_dense": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_residual": ([C.c_void_p] * 7, C.c_int),
     "ldg_residual_tangent": ([C.c_void_p] * 5, C.c_int),
     "ldg_operator_pass": ([C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 6, C.c_int),

@@ -323,6 +323,7 @@ int ldg_create_dense(const LdgDenseTables* t, LdgHandle** out) {
   memset(&h->P, 0, sizeof(h->P));
   h->P.ghost0 = INT32_MAX;
   ldg::DenseParams& D = h->D;
+  D.ghost0 = INT32_MAX;
   D.ne = t->ne; D.nd = t->nd; D.nb = t->nb; D.nqf = t->nqf; D.nface = t->nface;
   D.nperm = t->nperm; D.ncu = t->ncu; D.trace_centered = t->trace_centered;
   D.grad_centered = t->grad_centered; D.flux_uses_u = t->flux_uses_u;
@@ -389,9 +390,19 @@ int ldg_set_export_layout(LdgHandle* h, int consumer) {
 // Partitioned operators: neighbour rows >= ghost0 come from u_ghost (the
 // halo buffer) instead of the state vector, so the owned vector is used in
 // place (no per-call copy into an owned+ghost array).  ghost0 < 0 resets.
+int ldg_set_ghost_rows_dense(LdgHandle* h, int ghost0, const double* u_ghost,
+                             const double* q_ghost) {
+  if (!h || !h->dense) return fail(2, "dense handle expected");
+  if (ghost0 >= 0 && (!u_ghost || !q_ghost)) return fail(2, "ghost rows need buffers");
+  h->D.ghost0 = ghost0 < 0 ? INT32_MAX : ghost0;
+  h->D.u_ghost = ghost0 < 0 ? nullptr : u_ghost;
+  h->D.q_ghost = ghost0 < 0 ? nullptr : q_ghost;
+  return 0;
+}
+
 int ldg_set_ghost_rows(LdgHandle* h, int ghost0, const double* u_ghost) {
   if (!h) return fail(2, "null handle");
-  if (h->dense) return fail(2, "not available for simplex systems");
+  if (h->dense) return fail(2, "dense handles take ldg_set_ghost_rows_dense");
   if (ghost0 >= 0 && !u_ghost) return fail(2, "ghost rows need a buffer");
   h->P.ghost0 = ghost0 < 0 ? INT32_MAX : ghost0;
   h->P.u_ghost = ghost0 < 0 ? nullptr : u_ghost;
@@ -651,7 +662,13 @@ int ldg_flux_from_mixed(LdgHandle* h, int tangent, const double* u,
                         const double* q, const double* gproj,
                         const double* bsrc, double* R, void* stream) {
   if (!h || !u || !q || !R) return fail(2, "null argument");
-  if (h->dense) return fail(2, "not available for simplex systems");
+  if (h->dense) {
+    // the simplex path's second pass on its own (partitioned systems
+    // exchange the ghost q rows between compute_mixed and this)
+    int rc = ldg::launch_dense(h->D, tangent ? 4 : 3, u, gproj, bsrc, const_cast<double*>(q), R,
+                               (cudaStream_t)stream);
+    return rc ? fail(rc, "dense flux launch", cudaGetLastError()) : 0;
+  }
   if (h->P.ghost0 != INT32_MAX) return fail(2, "the unfused flux pass has no ghost-row mode");
   int rc = ldg::launch_flux(h->P, tangent != 0, u, q, gproj, bsrc, R, (cudaStream_t)stream);
   return rc ? fail(rc, "flux launch", cudaGetLastError()) : 0;

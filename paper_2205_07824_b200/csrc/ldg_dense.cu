@@ -80,7 +80,7 @@ mixed_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
         const bool need = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR && a_ != 0.0;
 #pragma unroll
         for (int c = 0; c < NCU; ++c)
-          snb[slot][f][c][lt] = need ? __ldg(u + ((size_t)nbr[f] * NB + lt) * NCU + c) : 0.0;
+          snb[slot][f][c][lt] = need ? __ldg(dense_nbr_row<false>(P, u, nbr[f], NB * NCU) + lt * NCU + c) : 0.0;
       }
     }
   }
@@ -205,10 +205,10 @@ flux_dense(const __grid_constant__ DenseParams P, const double* __restrict__ u,
         const bool nq = inter && wn != 0.0;
 #pragma unroll
         for (int c = 0; c < NCU; ++c)
-          snu[slot][f][c][lt] = nu ? __ldg(u + ((size_t)nbr[f] * NB + lt) * NCU + c) : 0.0;
+          snu[slot][f][c][lt] = nu ? __ldg(dense_nbr_row<false>(P, u, nbr[f], NB * NCU) + lt * NCU + c) : 0.0;
 #pragma unroll
         for (int cd = 0; cd < NQ; ++cd)
-          snq[slot][f][cd][lt] = nq ? __ldg(q + ((size_t)nbr[f] * NB + lt) * NQ + cd) : 0.0;
+          snq[slot][f][cd][lt] = nq ? __ldg(dense_nbr_row<true>(P, q, nbr[f], NB * NQ) + lt * NQ + cd) : 0.0;
       }
     }
   }
@@ -419,7 +419,7 @@ mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict_
       double a_, b_, wo_, wn_;
       coeffs(P, info[f], a_, b_, wo_, wn_);
       const bool need = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR && a_ != 0.0;
-      snb[slot * PNB + f * NB + lt] = need ? __ldg(u + (size_t)nbr[f] * NB + lt) : 0.0;
+      snb[slot * PNB + f * NB + lt] = need ? __ldg(dense_nbr_row<false>(P, u, nbr[f], NB) + lt) : 0.0;
     }
   }
   __syncthreads();
@@ -542,11 +542,11 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
       const bool inter = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR;
       const bool nu = inter && (alpha != 0.0 || beta != 0.0);
       const bool nq = inter && wn != 0.0;
-      snu[slot * PNU + f * NB + lt] = nu ? __ldg(u + (size_t)nbr[f] * NB + lt) : 0.0;
+      snu[slot * PNU + f * NB + lt] = nu ? __ldg(dense_nbr_row<false>(P, u, nbr[f], NB) + lt) : 0.0;
 #pragma unroll
       for (int d = 0; d < ND; ++d)
         snq[slot * PNQ + (f * ND + d) * NB + lt] =
-            nq ? __ldg(q + ((size_t)nbr[f] * NB + lt) * ND + d) : 0.0;
+            nq ? __ldg(dense_nbr_row<true>(P, q, nbr[f], NB * ND) + lt * ND + d) : 0.0;
     }
   }
   __syncthreads();
@@ -666,20 +666,22 @@ int run_dense(const DenseParams& P, int what, const double* u, const double* gva
                            cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
       attr = true;
     }
-    mixed_dense_mma<NB, NQF, NFACE, ND, TPE><<<gm, kMmaEpb * TPE, 0, s>>>(
-        P, u, what == 2 ? nullptr : gval, q);
+    if (what <= 2)
+      mixed_dense_mma<NB, NQF, NFACE, ND, TPE><<<gm, kMmaEpb * TPE, 0, s>>>(
+          P, u, what == 2 ? nullptr : gval, q);
     if (cudaGetLastError() != cudaSuccess) return 3;
-    if (what == 1)
+    if (what == 1 || what == 3)
       flux_dense_mma<NB, NQF, NFACE, ND, TPE, false><<<gm, kMmaEpb * TPE, fsm, s>>>(P, u, q, gval, bsrc, R);
-    else if (what == 2)
+    else if (what == 2 || what == 4)
       flux_dense_mma<NB, NQF, NFACE, ND, TPE, true><<<gm, kMmaEpb * TPE, fsm, s>>>(P, u, q, nullptr, nullptr, R);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
   }
-  mixed_dense<NB, NQF, NFACE, ND, NCU, TPE><<<grid, kDBlock, 0, s>>>(P, u, what == 2 ? nullptr : gval, q);
+  if (what <= 2)
+    mixed_dense<NB, NQF, NFACE, ND, NCU, TPE><<<grid, kDBlock, 0, s>>>(P, u, what == 2 ? nullptr : gval, q);
   if (cudaGetLastError() != cudaSuccess) return 3;
-  if (what == 1)
+  if (what == 1 || what == 3)
     flux_dense<NB, NQF, NFACE, ND, NCU, TPE, false><<<grid, kDBlock, 0, s>>>(P, u, q, gval, bsrc, R);
-  else if (what == 2)
+  else if (what == 2 || what == 4)
     flux_dense<NB, NQF, NFACE, ND, NCU, TPE, true><<<grid, kDBlock, 0, s>>>(P, u, q, nullptr, nullptr, R);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

@@ -25,11 +25,25 @@ struct DenseParams {
   const double* phif;     // own traces
   const double* phio;     // neighbour traces by orientation
   unsigned long long* bad;
+  // partitioned operators: neighbour rows >= ghost0 come from the halo
+  // buffers (u_ghost / q_ghost, row nbr - ghost0); INT32_MAX: no ghosts
+  int ghost0;
+  const double* u_ghost;
+  const double* q_ghost;
   double au[LDG_MAX_NCU * 3 * LDG_MAX_NCU];
   double aq[LDG_MAX_NCU * 3 * LDG_MAX_NCU * 3];
 };
 
-// what: 0 mixed (q = compute_mixed(u, gval)), 1 residual, 2 tangent
+// start of neighbour element nbr's row (`row` doubles) of u (q when Q)
+template <bool Q>
+__device__ __forceinline__ const double* dense_nbr_row(const DenseParams& P, const double* base,
+                                                       int nbr, int row) {
+  return nbr >= P.ghost0 ? (Q ? P.q_ghost : P.u_ghost) + (size_t)(nbr - P.ghost0) * row
+                         : base + (size_t)nbr * row;
+}
+
+// what: 0 mixed (q = compute_mixed(u, gval)), 1 residual, 2 tangent,
+//       3 flux pass from a given q (residual), 4 flux pass (tangent)
 int launch_dense(const DenseParams& P, int what, const double* u, const double* gval,
                  const double* bsrc, double* q, double* R, cudaStream_t s);
 

@@ -83,7 +83,12 @@ class PartitionPlan:
                 self.send[q] = rows.astype(np.int64)          # local owned rows, sorted
         if np.any(self.fnbr < 0):
             raise DiscError("partition left an unresolved neighbour")
-        self._face_halo(tab)
+        if hasattr(tab, "nmap"):          # tensor tables: face-node halos
+            self._face_halo(tab)
+        else:                             # simplex tables: whole ghost rows
+            self.interior = (0, 0)
+            self.row_send = {q: r for q, r in self.send.items()}
+            self.row_recv = {q: r - self.ne_loc for q, r in self.recv.items()}
 
     def _cut_pairs(self, tab, recv_rank, send_rank):
         """Cut (element, face) slots of recv_rank's elements whose neighbour
@@ -462,6 +467,102 @@ class PartitionedLdgSystem:
 
     def tangent_dev(self, du, out=None, base=None, t=0.0):
         """Linear fused operator: the tangent reads neither base nor t."""
+        return self.apply(du, True, 0.0, out)
+
+
+class LocalDenseTables:
+    """DenseTables interface over one partition (simplex elements): rows
+    sliced, neighbours renumbered to [owned | ghosts], the element-independent
+    operators shared."""
+
+    def __init__(self, tab, plan):
+        self._g, self.plan = tab, plan
+        for k in ("kind", "nd", "p", "ncu", "nb", "nqf", "nf", "perms", "perm_pts", "dr", "kr",
+                  "minv", "lift", "fluxop", "phif", "phio", "au", "aq", "flux_uses_u",
+                  "mass_const", "mass_coef", "source_zero", "model", "master", "mesh", "topo",
+                  "bc_groups", "face_area_ref", "geom_master"):
+            setattr(self, k, getattr(tab, k, None))
+        e0, e1 = plan.e0, plan.e1
+        self.ne = plan.ne_loc
+        self.fnbr, self.finfo, self.ftau = plan.fnbr, plan.finfo, plan.ftau
+        self.geo = plan.geo
+        self.fnorm, self.fsj = tab.fnorm[e0:e1], tab.fsj[e0:e1]
+        self.detj, self.invjt = tab.detj[e0:e1], tab.invjt[e0:e1]
+        self.J, self.x0 = tab.J[e0:e1], tab.x0[e0:e1]
+        self.elem_vol = tab.elem_vol[e0:e1]
+        self.switch, self.fi_h, self.fb_h = tab.switch, tab.fi_h, tab.fb_h
+        self.curved = False
+
+    def node_coords(self, elems=None, nodes=None):
+        e = np.arange(self.plan.e0, self.plan.e1) if elems is None else \
+            np.asarray(elems) + self.plan.e0
+        return self._g.node_coords(e, nodes)
+
+    def boundary_values(self, t):
+        g = self._g.boundary_values(t)
+        return g[self.plan.brows] if g.size else g
+
+    def source_load(self, t):
+        b = self._g.source_load(t)
+        return None if b is None else b[self.plan.e0:self.plan.e1]
+
+
+class PartitionedDenseSystem:
+    """One rank's share of a simplex (tri / tet) system: owned elements plus
+    a ghost layer, the dense mixed and flux passes with whole-row halos of u
+    and of the mixed gradient q in between (the flux pass reads the
+    neighbours' q).  Neighbour rows >= n_owned come from the halo buffers
+    (``ldg_set_ghost_rows_dense``), so the owned vector is used in place."""
+
+    def __init__(self, model, mesh, topology, master, nranks, rank, device=None,
+                 exchanger=None, tables=None):
+        import torch
+        from . import _lib as L
+        from .system import LdgSystem
+        from .tables import DenseTables
+        gtab = tables if tables is not None else DenseTables(model, mesh, topology, master)
+        self.plan = PartitionPlan(gtab, nranks, rank)
+        self.local = LocalDenseTables(gtab, self.plan)
+        self.sys = LdgSystem(model, mesh, topology, master, device=device, tables=self.local)
+        self.exchanger = exchanger if exchanger is not None else FaceHaloExchanger(self.plan)
+        p = self.plan
+        self.n_elements, self.n_nodes, self.ncu, self.nd = p.ne_loc, master.n_nodes, model.ncu, mesh.nd
+        self.n_dofs = p.ne_loc * master.n_nodes * model.ncu
+        self.kind, self.model, self.device = model.kind, model, self.sys.device
+        ng = max(p.n_ghost, 1)
+        self.u_ghost = torch.zeros((ng, self.n_nodes, self.ncu), dtype=torch.float64,
+                                   device=self.device)
+        self.q_ghost = torch.zeros((ng, self.n_nodes, self.ncu, self.nd), dtype=torch.float64,
+                                   device=self.device)
+        L.check(self.sys.lib.ldg_set_ghost_rows_dense(self.sys._h, p.ne_loc, L.ptr(self.u_ghost),
+                                                      L.ptr(self.q_ghost)),
+                "ldg_set_ghost_rows_dense")
+
+    def start_u_halo(self, u):
+        p = self.plan
+        return self.exchanger.start(u.reshape(p.ne_loc, -1), self.u_ghost.view(self.u_ghost.shape[0], -1),
+                                    p.row_send, p.row_recv)
+
+    def start_q_halo(self, q):
+        p = self.plan
+        return self.exchanger.start(q.reshape(p.ne_loc, -1), self.q_ghost.view(self.q_ghost.shape[0], -1),
+                                    p.row_send, p.row_recv)
+
+    def apply(self, u, tangent, t=0.0, out=None, exchange=True):
+        """R(u) or J du: u halo, mixed pass (owned), q halo, flux pass."""
+        p = self.plan
+        u = u.reshape(p.ne_loc, self.n_nodes, self.ncu).contiguous()
+        if exchange:
+            self.start_u_halo(u).wait()
+        q = self.sys.mixed_dev(u, t, homogeneous=tangent)
+        if exchange:
+            self.start_q_halo(q).wait()
+        return self.sys.flux_from_mixed_dev(u, q, tangent, t, out=out)
+
+    def residual_dev(self, u, t=0.0, out=None):
+        return self.apply(u, False, t, out)
+
+    def tangent_dev(self, du, out=None, base=None, t=0.0):
         return self.apply(du, True, 0.0, out)
 
 

@@ -311,10 +311,12 @@ def _solve_rank(rank, world, port, name, orth, out):
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2205_07824_b200.parallel import PartitionedLdgSystem, run_steady_partitioned
+        from paper_2205_07824_b200.parallel import (PartitionedDenseSystem, PartitionedLdgSystem,
+                                                    run_steady_partitioned)
         spec = SOLVE_CASES[name]
         f = ACCEPT_FLAGS
-        s = PartitionedLdgSystem(*build_case(spec, *b200_setup()), nranks=world, rank=rank)
+        cls = PartitionedDenseSystem if spec["kind"] in ("tri", "tet") else PartitionedLdgSystem
+        s = cls(*build_case(spec, *b200_setup()), nranks=world, rank=rank)
         u, stats, _ = run_steady_partitioned(s, precond=spec["precond"], abs_tol=f["abs_tol"],
                                              rel_tol=f["rel_tol"], forcing=f["forcing"],
                                              restart=f["restart"],
@@ -328,7 +330,9 @@ def _solve_rank(rank, world, port, name, orth, out):
 
 @pytest.mark.parametrize("name,orth", [("known_poisson3d_hex_p3_n4_bj", "dcgs2"),
                                        ("known_poisson3d_hex_p3_n4_bj", "mgs"),
-                                       ("config1_quad_p3_n8_bj", "dcgs2")])
+                                       ("config1_quad_p3_n8_bj", "dcgs2"),
+                                       ("config1_tri_p3_n8_bj", "dcgs2"),
+                                       ("known_poisson3d_tet_p3_n4_bj", "dcgs2")])
 def test_partitioned_newton_gmres_two_ranks_matches_reference(tmp_path, name, orth):
     """The CUDA PartitionedLdgSystem on two ranks sharing the GPU (gloo
     staging of the face-node halos, allreduced DCGS2 / MGS reductions,
