@@ -319,7 +319,8 @@ def nonlinear_lines(hbm, cpu=True):
         _, r = nl_bench.run(name, spec, 10, hbm)
         out[name] = {k: r[k] for k in ("dofs", "tangent_gdofs", "residual_gdofs", "tangent_ms",
                                        "residual_ms", "tangent_bytes_per_dof",
-                                       "tangent_frac_hbm")}
+                                       "tangent_frac_hbm", "tangent_uncached_gdofs",
+                                       "base_cache_ms")}
         if cpu:
             c = nl_bench.cpu_oracle_tangent(small[name])
             out[name]["cpu_baseline"] = dict(c, sample=f"{c['dofs']}-DOF mesh of the same "

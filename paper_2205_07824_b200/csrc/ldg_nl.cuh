@@ -70,6 +70,9 @@ struct NlParams {
   const double* vgeo;    // (ne, NQ, 1 + ND*ND + ND): detJ, invjt[d][r], x at the volume points
   const double* ffgeo;   // (ne, NFACE, NQF, 2 ND + 1): left normal, w |t1 x t2|, x per face point
   const double* minv;    // (ne, NB, NB) inverse element mass matrices
+  // base-state cache of the tangent (built once per base by nl_base_cache):
+  // [ne][NV][NQ] volume-point values, then [ne][side][face][NV][NQF] traces
+  double* bcache;
 };
 #ifndef CURVED
 #define CURVED 0
@@ -580,9 +583,14 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mixed_curved(const __grid_co
 // ---------------------------------------------------------------------------
 // residual / tangent: one element per block of NT threads
 // ---------------------------------------------------------------------------
-template <bool TANGENT>
+__device__ __forceinline__ int e_of_block() { return blockIdx.x; }
+
+// CACHE: 0 none; 1 tangent reading the base state (u, q, w at the volume and
+// face points) from P.bcache, so only the direction's NV variables are
+// interpolated; 2 building that cache (base variables only)
+template <bool TANGENT, int CACHE = 0>
 struct RShape {
-  static constexpr int NVA = NV * (TANGENT ? 2 : 1);              // u,q (+ du,dq)
+  static constexpr int NVA = CACHE == 1 ? NV : NV * (TANGENT ? 2 : 1);  // variables in smem
   static constexpr int BS = (NVA > NG ? NVA : NG) * MX;           // one volume work buffer
   // face phase: traces of every face at its Gauss points, own and neighbour
   // side [side][face][v][NQF], one face's staging pair, and the face fluxes
@@ -810,10 +818,14 @@ __device__ __forceinline__ void face_flux(const NlParams& P, int e, int kind, bo
   }
 }
 
-template <bool TANGENT>
+template <bool TANGENT, int CACHE = 0>
 __device__ __forceinline__ void residual_body(const NlParams& P) {
-  using S = RShape<TANGENT>;
-  constexpr int NVA = S::NVA;
+  using S = RShape<TANGENT, CACHE>;
+  constexpr int NVA = S::NVA;                  // variables held in shared memory
+  constexpr int NVL = NV * (TANGENT ? 2 : 1);  // variables of a point (base | direction)
+  const double* bvol = CACHE == 1 ? P.bcache + (sz_t)e_of_block() * NV * NQ : nullptr;
+  const double* bfac = CACHE == 1 ? P.bcache + (sz_t)P.ne * NV * NQ +
+                                        (sz_t)e_of_block() * 2 * NFACE * NV * NQF : nullptr;
   extern __shared__ __align__(16) double smem_r[];
   double* sV = smem_r;                      // [NVA][NB] node values
   double* sR = sV + NVA * NB;             // [NCU][NB] residual accumulator
@@ -825,7 +837,7 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
   // ---- load u, q (+ du, dq) of the element: [v][node]
   for (int idx = tid; idx < NVA * NB; idx += NT) {
     const int v = idx / NB, a = idx % NB;
-    const int fam = v >= NV, vv = v % NV;
+    const int fam = CACHE == 1 ? 1 : (v >= NV), vv = v % NV;
     const double val = state_at(P, fam, vv, (sz_t)e, a);
     sV[idx] = val;
     bA[idx] = val;
@@ -840,7 +852,7 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
     const int nbr = P.fnbr[e * NFACE + lf];
     for (int idx = tid; idx < S::NBF; idx += NT) {
       const int v = idx / NFN, t = idx % NFN;
-      if (interior) cp_async8(dst + idx, state_ptr(P, v >= NV, v % NV, (sz_t)nbr,
+      if (interior) cp_async8(dst + idx, state_ptr(P, CACHE == 1 ? 1 : (v >= NV), v % NV, (sz_t)nbr,
                                                    P.nmap[(info >> 8) * NFN + t]));
       else dst[idx] = 0.0;
     }
@@ -853,10 +865,15 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
   to_quad(bA, bB, NVA, tid, vq);
   double* gbuf = vq == bA ? bB : bA;
   const double* geo_e = P.geo + (sz_t)e * (1 + ND * ND);
-  for (int p = tid; p < NQ; p += NT) {
-    double val[NVA];
+  if (CACHE == 2) {
+    // base cache: the volume-point values; the face traces below
+    for (int idx = tid; idx < NV * NQ; idx += NT) P.bcache[(sz_t)e * NV * NQ + idx] = vq[idx];
+  }
+  for (int p = tid; p < (CACHE == 2 ? 0 : NQ); p += NT) {
+    double val[NVL];
 #pragma unroll
-    for (int v = 0; v < NVA; ++v) val[v] = vq[v * NQ + p];
+    for (int v = 0; v < NVL; ++v)
+      val[v] = CACHE == 1 ? (v < NV ? bvol[v * NQ + p] : vq[(v - NV) * NQ + p]) : vq[v * NQ + p];
     double x[ND];
     // affine: one (detJ, invJ^T) per element and x = x0 + J xi; curved: per point
     const double* geo = CURVED ? P.vgeo + ((sz_t)e * NQ + p) * VG : geo_e;
@@ -898,14 +915,16 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
     }
   }
   __syncthreads();
-  double* rn;
-  from_quad(gbuf, vq, NG, tid, rn);
-  for (int idx = tid; idx < NCU * NB; idx += NT) {
-    const int c = idx / NB, a = idx % NB;
-    double acc = 0.0;
+  if (CACHE != 2) {
+    double* rn;
+    from_quad(gbuf, vq, NG, tid, rn);
+    for (int idx = tid; idx < NCU * NB; idx += NT) {
+      const int c = idx / NB, a = idx % NB;
+      double acc = 0.0;
 #pragma unroll
-    for (int r = 0; r <= ND; ++r) acc += rn[(r * NCU + c) * NB + a];
-    sR[idx] = -acc;
+      for (int r = 0; r <= ND; ++r) acc += rn[(r * NCU + c) * NB + a];
+      sR[idx] = -acc;
+    }
   }
   __syncthreads();
 
@@ -938,6 +957,12 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
     }
     __syncthreads();
   }
+  if (CACHE == 2) {
+    // base cache: the traces [side][face][v][NQF] of the base variables
+    double* dst = P.bcache + (sz_t)P.ne * NV * NQ + (sz_t)e * 2 * NFACE * NV * NQF;
+    for (int idx = tid; idx < 2 * NFACE * NV * NQF; idx += NT) dst[idx] = TRc[idx];
+    return;
+  }
   for (int it = tid; it < NFACE * NQF; it += NT) {
     const int lf = it / NQF, s = it % NQF;
     const int info = P.finfo[e * NFACE + lf];
@@ -957,11 +982,17 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
     } else {
       phys_point(P, e, &c_fxi[(lf * NQF + s) * ND], x);
     }
-    double vo[NVA], vn[NVA];
+    double vo[NVL], vn[NVL];
 #pragma unroll
-    for (int v = 0; v < NVA; ++v) {
-      vo[v] = TRc[((0 * NFACE + lf) * NVA + v) * NQF + s];
-      vn[v] = TRc[((1 * NFACE + lf) * NVA + v) * NQF + s];
+    for (int v = 0; v < NVL; ++v) {
+      if (CACHE == 1 && v < NV) {
+        vo[v] = bfac[((0 * NFACE + lf) * NV + v) * NQF + s];
+        vn[v] = bfac[((1 * NFACE + lf) * NV + v) * NQF + s];
+      } else {
+        const int vs = CACHE == 1 ? v - NV : v;
+        vo[v] = TRc[((0 * NFACE + lf) * NVA + vs) * NQF + s];
+        vn[v] = TRc[((1 * NFACE + lf) * NVA + vs) * NQF + s];
+      }
     }
     double fh[NCU];
     face_flux<TANGENT>(P, e, kind, right, sw, brow, s, x, n, fg[ND + 1], vo, vn, fh);
@@ -1003,6 +1034,12 @@ extern "C" __global__ void __launch_bounds__(NT) nl_residual(const __grid_consta
 }
 extern "C" __global__ void __launch_bounds__(NT) nl_tangent(const __grid_constant__ NlParams P) {
   residual_body<true>(P);
+}
+extern "C" __global__ void __launch_bounds__(NT) nl_tangent_cached(const __grid_constant__ NlParams P) {
+  residual_body<true, 1>(P);
+}
+extern "C" __global__ void __launch_bounds__(NT) nl_base_cache(const __grid_constant__ NlParams P) {
+  residual_body<false, 2>(P);
 }
 
 // ---------------------------------------------------------------------------

@@ -63,7 +63,19 @@ def run(name, spec, reps, peak):
     r = {"dofs": s.n_dofs, "kind": model.kind, "ncu": s.ncu, "p": master.p,
          "elements": s.n_elements}
     r["residual_ms"] = timed(lambda: nl.residual(u, 0.0, q=q, out=out), reps, flush)
+    # GMRES matvec: the base state's point values come from the per-base
+    # cache (built once per Newton step, timed separately); the uncached
+    # tangent (the base interpolated every call) beside it
     r["tangent_ms"] = timed(lambda: nl.tangent(u, du, 0.0, q=q, out=out), reps, flush)
+    r["tangent_cached_ms"] = timed(lambda: nl.tangent(u, du, 0.0, q=q, out=out, cached=True),
+                                   reps, flush)
+    r["tangent_uncached_ms"] = timed(lambda: nl.tangent(u, du, 0.0, q=q, out=out, cached=False),
+                                     reps, flush)
+
+    def rebuild():
+        nl._bkey = None
+        nl.base_cache(u, 0.0, q)
+    r["base_cache_ms"] = timed(rebuild, reps, flush)
     if q is not None:
         r["mixed_ms"] = timed(lambda: nl.mixed(du, 0.0, True, out=dq), reps, flush)
         P = nl._params(0.0, u=u, q=q, du=du, dq=dq, out=out, gq=nl.gq(0.0))
@@ -75,11 +87,13 @@ def run(name, spec, reps, peak):
         r["tangent_kernel_ms"] = r["tangent_ms"]
         bpd = 24                          # kind C tangent: du, base u, dR
     r["tangent_gdofs"] = s.n_dofs / r["tangent_ms"] / 1e6
+    r["tangent_uncached_gdofs"] = s.n_dofs / r["tangent_uncached_ms"] / 1e6
     r["residual_gdofs"] = s.n_dofs / r["residual_ms"] / 1e6
     r["tangent_bytes_per_dof"] = bpd
     r["tangent_achieved_gbs"] = bpd * s.n_dofs / r["tangent_ms"] / 1e6
     r["tangent_frac_hbm"] = r["tangent_achieved_gbs"] / peak
-    r["attrs"] = {k: nl.kernel_attrs(k) for k in ("nl_residual", "nl_tangent", "nl_mixed")}
+    r["attrs"] = {k: nl.kernel_attrs(k) for k in ("nl_residual", "nl_tangent", "nl_tangent_cached",
+                                                   "nl_mixed")}
     return name, r
 
 
