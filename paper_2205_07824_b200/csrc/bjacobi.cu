@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "ldgb200.h"
+#include "nvtx.cuh"
 
 namespace {
 
@@ -352,6 +353,7 @@ int ldg_bj_extract(int bs, const int32_t* members, int64_t nm, int k,
 // time so one wave's working copies stay L2-resident
 int ldg_bj_invert_global(int64_t nblk, int bs, const double* mats, double* inv_t,
                          int32_t* shifted, void* stream) {
+  NvtxRange nvtx_("ldg_bj_invert_global");
   if (bs < 1 || nblk < 0) return 2;
   cudaStream_t s = (cudaStream_t)stream;
   int dev = 0, nsm = 0;
@@ -376,6 +378,7 @@ int ldg_bj_invert_global(int64_t nblk, int bs, const double* mats, double* inv_t
 
 int ldg_bj_invert(int64_t nblk, int bs, const double* mats, double* inv_t,
                   int32_t* shifted, void* stream) {
+  NvtxRange nvtx_("ldg_bj_invert");
   if (bs < 1) return 2;
   if (bs > kMaxSmemBs) return ldg_bj_invert_global(nblk, bs, mats, inv_t, shifted, stream);
   const size_t sm = (size_t)bs * bs * sizeof(double);
@@ -405,6 +408,7 @@ int ldg_permute_scatter(int64_t n, const int64_t* idx, const double* src, double
 
 int ldg_bj_apply(int64_t nblk, int bs, const double* inv_t, const double* r, double* z,
                  void* stream) {
+  NvtxRange nvtx_("ldg_bj_apply");
   cudaStream_t s = (cudaStream_t)stream;
   if (nblk <= 0) return 0;
   if (bs <= 256) {

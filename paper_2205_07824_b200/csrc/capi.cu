@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 #include "ldg_dense.cuh"
+#include "nvtx.cuh"
 #include "ldg_tensor.cuh"
 
 namespace {
@@ -435,6 +436,7 @@ int64_t ldg_last_bad_element(LdgHandle* h) {
 
 int ldg_compute_mixed(LdgHandle* h, const double* u, const double* gproj,
                       double* q, void* stream) {
+  NvtxRange nvtx_("ldg_compute_mixed");
   if (!h || !u || !q) return fail(2, "null argument");
   if (h->dense) {
     int rc = ldg::launch_dense(h->D, 0, u, gproj, nullptr, q, nullptr, (cudaStream_t)stream);
@@ -454,6 +456,7 @@ int64_t ldg_scratch_doubles(LdgHandle* h) {
 
 int ldg_residual(LdgHandle* h, const double* u, const double* gproj,
                  const double* bsrc, double* scratch, double* R, void* stream) {
+  NvtxRange nvtx_("ldg_residual");
   if (!h || !u || !R || !scratch) return fail(2, "null argument");
   if (h->dense) {
     int rc = ldg::launch_dense(h->D, 1, u, gproj, bsrc, scratch, R, (cudaStream_t)stream);
@@ -465,6 +468,7 @@ int ldg_residual(LdgHandle* h, const double* u, const double* gproj,
 
 int ldg_residual_tangent(LdgHandle* h, const double* du, double* scratch,
                          double* dR, void* stream) {
+  NvtxRange nvtx_("ldg_residual_tangent");
   if (!h || !du || !scratch || !dR) return fail(2, "null argument");
   if (h->dense) {
     int rc = ldg::launch_dense(h->D, 2, du, nullptr, nullptr, scratch, dR, (cudaStream_t)stream);
@@ -481,6 +485,7 @@ int ldg_residual_tangent(LdgHandle* h, const double* du, double* scratch,
 int ldg_bj_probe_colour(LdgHandle* h, int64_t nblk, int bs, const int32_t* members,
                         int64_t nm, double* v, double* col, double* scratch, double* mats,
                         void* stream) {
+  NvtxRange nvtx_("ldg_bj_probe_colour");
   if (!h || !v || !col || !scratch || !mats || bs < 1) return fail(2, "bad argument");
   for (int k = 0; k < bs; ++k) {
     int rc = ldg_bj_probe_vector(nblk, bs, members, nm, k, v, stream);
@@ -496,6 +501,7 @@ int ldg_bj_probe_colour(LdgHandle* h, int64_t nblk, int bs, const int32_t* membe
 int ldg_operator_pass(LdgHandle* h, int pass, int tangent, const double* u,
                       const double* gproj, const double* bsrc, double* scratch,
                       double* R, void* stream) {
+  NvtxRange nvtx_("ldg_operator_pass");
   if (!h || !u || !R || !scratch || pass < 1 || pass > 2) return fail(2, "bad argument");
   if (h->dense) return fail(2, "not available for simplex systems");
   int rc = ldg::launch_fused_pass(h->P, pass, tangent != 0, u, gproj, bsrc, R, scratch,
@@ -506,6 +512,7 @@ int ldg_operator_pass(LdgHandle* h, int pass, int tangent, const double* u,
 int ldg_operator_pass_range(LdgHandle* h, int pass, int tangent, const double* u,
                             const double* gproj, const double* bsrc, double* scratch,
                             double* R, int e0, int e1, void* stream) {
+  NvtxRange nvtx_("ldg_operator_pass_range");
   if (!h || !u || !R || !scratch || pass < 1 || pass > 2) return fail(2, "bad argument");
   if (h->dense) return fail(2, "not available for simplex systems");
   if (e0 < 0 || e1 > h->P.ne || e0 > e1) return fail(2, "element range out of bounds");
@@ -541,6 +548,7 @@ int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, doubl
                           double* out_host, double* v_dev, double* R_dev, double* scratch,
                           const double* gproj, const double* bsrc, int nchunk,
                           const int32_t* starts, const int32_t* dep, void* stream) {
+  NvtxRange nvtx_("ldg_apply_host_staged");
   if (!h || !v_host || !out_host || !v_dev || !R_dev || !scratch || nchunk < 1 || !starts || !dep)
     return fail(2, "bad argument");
   if (h->dense) return fail(2, "not available for simplex systems");

@@ -221,6 +221,16 @@ class _Workspace:
 _WS = _Workspace()
 
 
+def _nvtx(name, like):
+    """NVTX range around a solver phase on CUDA data (timeline tools name the
+    GMRES cycles and the block-Jacobi build); a no-op context otherwise."""
+    import contextlib
+    import torch
+    if isinstance(like, torch.Tensor) and like.is_cuda:
+        return torch.cuda.nvtx.range(name)
+    return contextlib.nullcontext()
+
+
 def _trace(tag):
     """LDG_GMRES_TRACE=1: synchronized wall-clock marks (diagnostics only)."""
     import os
@@ -588,8 +598,9 @@ def newton_solve(residual_fn, x0, options=None, precond=None, tangent_fn=None,
             ops=ops), n=x.numel())
         eta = opts.forcing if opts.forcing is not None else min(0.1, np.sqrt(rnorm))
         eta = min(max(eta, 1e-14), 0.9)
-        lin = gmres(op, -R, precond=M, rel_tol=eta, restart=opts.gmres_restart,
-                    max_iter=opts.gmres_max_iter, orth=opts.orth, ops=ops)
+        with _nvtx(f"gmres (newton step {stats.newton_iters})", x):
+            lin = gmres(op, -R, precond=M, rel_tol=eta, restart=opts.gmres_restart,
+                        max_iter=opts.gmres_max_iter, orth=opts.orth, ops=ops)
         stats.gmres_iters.append(lin.iterations)
         d = lin.x
         step, accepted = 1.0, False
