@@ -505,10 +505,12 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
   constexpr int PH = mma_pitch(NFACE * NQF), PF = mma_pitch(ND * NB);
   extern __shared__ __align__(16) double dsm[];
   double* sv = dsm;                                          // [e][v][b]: u, q_1..q_ND
-  constexpr int PNU = mma_pitch(NFACE * NB), PNQ = mma_pitch(NFACE * ND * NB);
-  double* snu = dsm + EPB * PV;                                     // [e][f][b] neighbour u
-  double* snq = snu + EPB * PNU;                                    // [e][f][d][b] neighbour q
-  double* sF = snq + EPB * PNQ;                                     // [e][r][b]: -detJ invJ^T f
+  // neighbour u and q of a node side by side ([e][f][b][u q1 q2 q3], 4
+  // doubles): the trace loop takes each node's four values in two 16-B loads
+  constexpr int PNV = mma_pitch(NFACE * NB * 4) + 4;               // == 8 (mod 16): 16-B aligned
+  static_assert(ND + 1 <= 4, "packed neighbour layout");
+  double* snv = dsm + EPB * PV;
+  double* sF = snv + EPB * PNV;                                     // [e][r][b]: -detJ invJ^T f
   double* sto = sF + EPB * PF;                                      // [e][f][v][s] own traces
   double* sfh = sto + EPB * PT;                                     // [e][f s]: sJ f^
   double* sR = sto;                                                 // [e][a]
@@ -542,11 +544,12 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
       const bool inter = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR;
       const bool nu = inter && (alpha != 0.0 || beta != 0.0);
       const bool nq = inter && wn != 0.0;
-      snu[slot * PNU + f * NB + lt] = nu ? __ldg(dense_nbr_row<false>(P, u, nbr[f], NB) + lt) : 0.0;
+      double* nv4 = snv + slot * PNV + (f * NB + lt) * 4;
+      nv4[0] = nu ? __ldg(dense_nbr_row<false>(P, u, nbr[f], NB) + lt) : 0.0;
 #pragma unroll
-      for (int d = 0; d < ND; ++d)
-        snq[slot * PNQ + (f * ND + d) * NB + lt] =
-            nq ? __ldg(dense_nbr_row<true>(P, q, nbr[f], NB * ND) + lt * ND + d) : 0.0;
+      for (int d = 0; d < 3; ++d)
+        nv4[1 + d] = (d < ND && nq) ? __ldg(dense_nbr_row<true>(P, q, nbr[f], NB * ND) + lt * ND + d)
+                                    : 0.0;
     }
   }
   __syncthreads();
@@ -600,9 +603,12 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
 #pragma unroll 4
         for (int b = 0; b < NB; ++b) {
           const double ph = __ldg(po + b * NQF);
-          un = fma(ph, snu[slot * PNU + f * NB + b], un);
-#pragma unroll
-          for (int d = 0; d < ND; ++d) qn[d] = fma(ph, snq[slot * PNQ + (f * ND + d) * NB + b], qn[d]);
+          const double2* nv2 = reinterpret_cast<const double2*>(snv + slot * PNV + (f * NB + b) * 4);
+          const double2 a01 = nv2[0], a23 = nv2[1];
+          un = fma(ph, a01.x, un);
+          qn[0] = fma(ph, a01.y, qn[0]);
+          if (ND > 1) qn[1] = fma(ph, a23.x, qn[1]);
+          if (ND > 2) qn[2] = fma(ph, a23.y, qn[2]);
         }
       } else if (!inter && !TANGENT && gval) {
         un = __ldg(gval + (size_t)nbf * NQF + sp);
@@ -655,7 +661,7 @@ int run_dense(const DenseParams& P, int what, const double* u, const double* gva
     // tensor-core variants (8 elements per block, batched operator GEMMs)
     const int gm = (P.ne + kMmaEpb - 1) / kMmaEpb;
     constexpr int fsm = (int)sizeof(double) * kMmaEpb *
-                        (mma_pitch((1 + ND) * NB) + mma_pitch(NFACE * NB) + mma_pitch(NFACE * ND * NB) +
+                        (mma_pitch((1 + ND) * NB) + mma_pitch(NFACE * NB * 4) + 4 +
                          mma_pitch(ND * NB) +
                          mma_pitch(NFACE * (1 + ND) * NQF) + mma_pitch(NFACE * NQF));
     static bool attr = false;

@@ -32,17 +32,17 @@
 typedef unsigned long long u64;
 typedef unsigned long long sz_t;  // (no <cstddef> under NVRTC)
 
-constexpr int NB = ND == 3 ? N1 * N1 * N1 : N1 * N1;
-constexpr int NQ = ND == 3 ? NQ1 * NQ1 * NQ1 : NQ1 * NQ1;
-constexpr int NFN = ND == 3 ? N1 * N1 : N1;
-constexpr int NQF = ND == 3 ? NQ1 * NQ1 : NQ1;
+constexpr int NB = ND == 3 ? N1 * N1 * N1 : (ND == 2 ? N1 * N1 : N1);
+constexpr int NQ = ND == 3 ? NQ1 * NQ1 * NQ1 : (ND == 2 ? NQ1 * NQ1 : NQ1);
+constexpr int NFN = ND == 3 ? N1 * N1 : (ND == 2 ? N1 : 1);   // a 1D face is one point
+constexpr int NQF = ND == 3 ? NQ1 * NQ1 : (ND == 2 ? NQ1 : 1);
 constexpr int NFACE = 2 * ND;
 constexpr int NVQ = KIND_C ? 0 : NCU * ND;
 constexpr int NV = NCU + NVQ + NW;             // state variables per point (u, q, w)
 constexpr int OW = NCU + NVQ;                  // offset of w within a point's variables
 constexpr int KMAX = N1 > NQ1 ? N1 : NQ1;
-constexpr int MX = ND == 3 ? KMAX * KMAX * KMAX : KMAX * KMAX;
-constexpr int MXF = ND == 3 ? KMAX * KMAX : KMAX;
+constexpr int MX = ND == 3 ? KMAX * KMAX * KMAX : (ND == 2 ? KMAX * KMAX : KMAX);
+constexpr int MXF = ND == 3 ? KMAX * KMAX : (ND == 2 ? KMAX : 1);
 constexpr int NG = NCU * (ND + 1);             // G_r (r < ND) and the source field
 
 struct NlParams {
@@ -88,15 +88,16 @@ __device__ __forceinline__ void flag(const NlParams& P, int e, double v) {
 
 // hex local faces z-, z+, y-, y+, x-, x+; quad y-, x+, y+, x- (master.py:43-44)
 __device__ __forceinline__ int face_axis(int lf) {
-  return ND == 3 ? (lf < 2 ? 2 : (lf < 4 ? 1 : 0)) : ((lf == 0 || lf == 2) ? 1 : 0);
+  return ND == 3 ? (lf < 2 ? 2 : (lf < 4 ? 1 : 0)) : (ND == 2 ? ((lf == 0 || lf == 2) ? 1 : 0) : 0);
 }
 __device__ __forceinline__ int face_side(int lf) {
-  return ND == 3 ? (lf & 1) : (lf == 1 || lf == 2 ? 1 : 0);
+  return ND == 3 ? (lf & 1) : (ND == 2 ? (lf == 1 || lf == 2 ? 1 : 0) : lf);
 }
 // volume node of face node t (t = i_a0 + N1 i_a1 over the tangential axes a0 < a1)
 __device__ __forceinline__ int face_vol_node(int lf, int t) {
   const int ax = face_axis(lf);
   const int io = face_side(lf) ? N1 - 1 : 0;
+  if (ND == 1) return io;
   if (ND == 2) return ax == 0 ? io + N1 * t : t + N1 * io;
   const int a = t % N1, b = t / N1;
   if (ax == 0) return io + N1 * a + N1 * N1 * b;
@@ -207,12 +208,16 @@ __device__ __forceinline__ void to_quad(double* a, double* b, int nvar, int tid,
     contract_u<NQ1, NQ1, N1, 2, N1, NQ1, false, OP_PHI>(a, b, nvar, tid);
     __syncthreads();
     res = b;
-  } else {
+  } else if (ND == 2) {
     contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(a, b, nvar, tid);
     __syncthreads();
     contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(b, a, nvar, tid);
     __syncthreads();
     res = a;
+  } else {
+    contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(a, b, nvar, tid);
+    __syncthreads();
+    res = b;
   }
 }
 
@@ -243,19 +248,23 @@ __device__ __forceinline__ void from_quad(double* a, double* b, int nfield, int 
     from_quad_stage<N1, N1, NQ1, 2>(a, b, nfield, tid);
     __syncthreads();
     res = b;
-  } else {
+  } else if (ND == 2) {
     from_quad_stage<NQ1, NQ1, 1, 0>(a, b, nfield, tid);
     __syncthreads();
     from_quad_stage<N1, NQ1, 1, 1>(b, a, nfield, tid);
     __syncthreads();
     res = a;
+  } else {
+    from_quad_stage<NQ1, 1, 1, 0>(a, b, nfield, tid);
+    __syncthreads();
+    res = b;
   }
 }
 
 __device__ __forceinline__ void quad_point(int p, double* xi) {
   xi[0] = c_xq1[p % NQ1];
-  xi[1] = c_xq1[(p / NQ1) % NQ1];
-  if (ND == 3) xi[2] = c_xq1[p / (NQ1 * NQ1)];
+  if (ND >= 2) xi[ND >= 2 ? 1 : 0] = c_xq1[(p / NQ1) % NQ1];
+  if (ND == 3) xi[ND == 3 ? 2 : 0] = c_xq1[p / (NQ1 * NQ1)];
 }
 
 __device__ __forceinline__ void phys_point(const NlParams& P, int e, const double* xi, double* x) {
@@ -393,7 +402,8 @@ nl_mixed(const __grid_constant__ NlParams P) {
       const int nidx = ix[ax];
       int t;
       if (ND == 3) t = ax == 0 ? j + N1 * k : (ax == 1 ? i + N1 * k : i + N1 * j);
-      else t = ax == 0 ? j : i;
+      else if (ND == 2) t = ax == 0 ? j : i;
+      else t = 0;
       const double cf = hi ? c_chi[nidx] : c_clo[nidx];
       const double v = (hi ? cf : -cf) * sj[slot][lf][t][c];
 #pragma unroll
@@ -428,10 +438,12 @@ __device__ __forceinline__ void grad_dir(const double* su, double* a, double* b,
     contract_u<NQ1, N1, N1, 1, N1, NQ1, false, R == 1 ? OP_DPHI : OP_PHI>(a, b, NCU, tid);
     __syncthreads();
     contract_u<NQ1, NQ1, N1, 2, N1, NQ1, false, R == 2 ? OP_DPHI : OP_PHI>(b, out, NCU, tid);
-  } else {
+  } else if (ND == 2) {
     contract_u<N1, N1, 1, 0, N1, NQ1, false, R == 0 ? OP_DPHI : OP_PHI>(su, a, NCU, tid);
     __syncthreads();
     contract_u<NQ1, N1, 1, 1, N1, NQ1, false, R == 1 ? OP_DPHI : OP_PHI>(a, out, NCU, tid);
+  } else {
+    contract_u<N1, 1, 1, 0, N1, NQ1, false, R == 0 ? OP_DPHI : OP_PHI>(su, out, NCU, tid);
   }
   __syncthreads();
 }
@@ -516,9 +528,14 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mixed_curved(const __grid_co
       __syncthreads();
       contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(st, tro, NCU, tid);
       contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(st + NCU * NQ1 * N1, trn, NCU, tid);
-    } else {
+    } else if (ND == 2) {
       contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(own, tro, NCU, tid);
       contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(oth, trn, NCU, tid);
+    } else {                                   // a point face: the trace is the end node
+      for (int idx = tid; idx < NCU; idx += NT) {
+        tro[idx] = own[idx];
+        trn[idx] = oth[idx];
+      }
     }
     __syncthreads();
   }
@@ -562,7 +579,8 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mixed_curved(const __grid_co
 #pragma unroll
       for (int sp = 0; sp < NQF; ++sp) {
         const int s0 = sp % NQ1, s1 = ND == 3 ? sp / NQ1 : 0;
-        const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1] : c_phi[s0 * N1 + t0];
+        const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1]
+                                  : (ND == 2 ? c_phi[s0 * N1 + t0] : 1.0);
         acc = fma(ph, FJ[(lf * NQF + sp) * NGQ + cj], acc);
       }
     }
@@ -951,9 +969,14 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
       __syncthreads();
       contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(ST1, tro, NVA, tid);
       contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(ST1 + NVA * NQ1 * N1, trn, NVA, tid);
-    } else {
+    } else if (ND == 2) {
       contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(SO, tro, NVA, tid);
       contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(nb, trn, NVA, tid);
+    } else {                                   // a point face: the trace is the end node
+      for (int idx = tid; idx < NVA; idx += NT) {
+        tro[idx] = SO[idx];
+        trn[idx] = nb[idx];
+      }
     }
     __syncthreads();
   }
@@ -1016,7 +1039,8 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
 #pragma unroll
       for (int s = 0; s < NQF; ++s) {
         const int s0 = s % NQ1, s1 = ND == 3 ? s / NQ1 : 0;
-        const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1] : c_phi[s0 * N1 + t0];
+        const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1]
+                                  : (ND == 2 ? c_phi[s0 * N1 + t0] : 1.0);
         acc = fma(ph, sF[(lf * NQF + s) * NCU + c], acc);
       }
     }
@@ -1109,12 +1133,16 @@ __device__ __forceinline__ void mass_body(const NlParams& P) {
     contract_u<N1, N1, NQ1, 2, NQ1, N1, true, OP_PHI>(fld, other, NCU, tid);
     __syncthreads();
     res = other;
-  } else {
+  } else if (ND == 2) {
     contract_u<NQ1, NQ1, 1, 0, NQ1, N1, true, OP_PHI>(fld, other, NCU, tid);
     __syncthreads();
     contract_u<N1, NQ1, 1, 1, NQ1, N1, true, OP_PHI>(other, fld, NCU, tid);
     __syncthreads();
     res = fld;
+  } else {
+    contract_u<NQ1, 1, 1, 0, NQ1, N1, true, OP_PHI>(fld, other, NCU, tid);
+    __syncthreads();
+    res = other;
   }
   for (int idx = tid; idx < NCU * NB; idx += NT) {
     const int a = idx / NCU, c = idx % NCU;
@@ -1161,12 +1189,16 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mass_inv(const __grid_consta
     contract_u<N1, N1, N1, 2, N1, N1, false, OP_M1INV>(bA, bB, NCU, tid);
     __syncthreads();
     res = bB;
-  } else {
+  } else if (ND == 2) {
     contract_u<N1, N1, 1, 0, N1, N1, false, OP_M1INV>(bA, bB, NCU, tid);
     __syncthreads();
     contract_u<N1, N1, 1, 1, N1, N1, false, OP_M1INV>(bB, bA, NCU, tid);
     __syncthreads();
     res = bA;
+  } else {
+    contract_u<N1, 1, 1, 0, N1, N1, false, OP_M1INV>(bA, bB, NCU, tid);
+    __syncthreads();
+    res = bB;
   }
   const double inv = P.scale / P.geo[(sz_t)e * (1 + ND * ND)];
   for (int idx = tid; idx < NCU * NB; idx += NT) {
@@ -1208,12 +1240,16 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mass_q(const __grid_constant
     contract_u<N1, N1, NQ1, 2, NQ1, N1, true, OP_PHI>(fld, other, NQC, tid);
     __syncthreads();
     res = other;
-  } else {
+  } else if (ND == 2) {
     contract_u<NQ1, NQ1, 1, 0, NQ1, N1, true, OP_PHI>(fld, other, NQC, tid);
     __syncthreads();
     contract_u<N1, NQ1, 1, 1, NQ1, N1, true, OP_PHI>(other, fld, NQC, tid);
     __syncthreads();
     res = fld;
+  } else {
+    contract_u<NQ1, 1, 1, 0, NQ1, N1, true, OP_PHI>(fld, other, NQC, tid);
+    __syncthreads();
+    res = other;
   }
   for (int idx = tid; idx < NQC * NB; idx += NT) {
     const int a = idx / NQC, v = idx % NQC;
@@ -1275,12 +1311,16 @@ extern "C" __global__ void __launch_bounds__(NT) nl_mass_inv_q(const __grid_cons
     contract_u<N1, N1, N1, 2, N1, N1, false, OP_M1INV>(bA, bB, NQC, tid);
     __syncthreads();
     res = bB;
-  } else {
+  } else if (ND == 2) {
     contract_u<N1, N1, 1, 0, N1, N1, false, OP_M1INV>(bA, bB, NQC, tid);
     __syncthreads();
     contract_u<N1, N1, 1, 1, N1, N1, false, OP_M1INV>(bB, bA, NQC, tid);
     __syncthreads();
     res = bA;
+  } else {
+    contract_u<N1, 1, 1, 0, N1, N1, false, OP_M1INV>(bA, bB, NQC, tid);
+    __syncthreads();
+    res = bB;
   }
   const double inv = P.scale / P.geo[(sz_t)e * (1 + ND * ND)];
   for (int idx = tid; idx < NQC * NB; idx += NT) {

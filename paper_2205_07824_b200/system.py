@@ -131,6 +131,8 @@ class LdgSystem:
         if self.nl_reason is None and not self.dense and tables is None and \
                 not mesh_is_affine(mesh):
             self.nl_reason = "curved (non-affine) elements"
+        if self.nl_reason is None and mesh.nd == 1:
+            self.nl_reason = "1D elements (the fused kernels are quad / hex)"
         if tables is not None and self.nl_reason is not None:
             raise DiscError(f"prebuilt (partitioned) tables support linear models only "
                             f"({self.nl_reason})")

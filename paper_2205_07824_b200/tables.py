@@ -27,7 +27,8 @@ from .expr import evaluate
 from .refelem import FACES, face_map
 
 # local face -> (normal axis, high side) for the tensor kinds
-FACE_AXIS = {"quad": [(1, 0), (0, 1), (1, 1), (0, 0)],
+FACE_AXIS = {"line": [(0, 0), (0, 1)],
+             "quad": [(1, 0), (0, 1), (1, 1), (0, 0)],
              "hex": [(2, 0), (2, 1), (1, 0), (1, 1), (0, 0), (0, 1)]}
 
 
@@ -199,6 +200,16 @@ def _reference_switch_subset(mesh, master, geom, elems, lfs):
 # ---------------------------------------------------------------------------
 
 
+def _line_master_tables(m):
+    """1D GLL / Gauss tables of a line master in the attributes the tensor
+    tables read (a line master's own tabulations are already 1D)."""
+    if getattr(m, "phi1d", None) is None:
+        m.nodes1d = np.asarray(m.nodes)[:, 0].copy()
+        m.phi1d = np.asarray(m.phi)
+        m.dphi1d = np.asarray(m.dphi)[:, :, 0]
+        m.quad1d = (np.asarray(m.quad_pts)[:, 0].copy(), np.asarray(m.quad_wts))
+
+
 def mesh_is_affine(mesh):
     """True when every element's geometry map is affine (the Jacobian at the
     reference corners agrees to roundoff) -- the fused / dense kernels'
@@ -221,8 +232,10 @@ class TensorTables:
         kind = master.kind
         if kind != mesh.elem_kind:
             raise DiscError("master element kind does not match the mesh")
-        if kind not in ("quad", "hex"):
+        if kind not in ("quad", "hex") and not (kind == "line" and nonlinear):
             raise DiscError(f"B200 tensor path needs quad/hex elements, got {kind}")
+        if kind == "line":
+            _line_master_tables(master)
         if model.kind not in (("C", "D", "W") if nonlinear else ("D",)):
             raise DiscError(f"B200 path supports kind C/D/W models, got {model.kind}"
                             if nonlinear else
@@ -256,7 +269,9 @@ class TensorTables:
         if m.nodes1d is None or np.max(np.abs(m.nodes1d - x1)) > 1e-13:
             raise DiscError("tensor path needs GLL solution nodes")
         L = m.phi1d
-        if self.nd == 3:
+        if self.nd == 1:
+            kron = L
+        elif self.nd == 3:
             kron = np.einsum("zk,yj,xi->zyxkji", L, L, L).reshape(m.phi.shape)
         else:
             kron = np.einsum("yj,xi->yxji", L, L).reshape(m.phi.shape)
@@ -403,6 +418,8 @@ class TensorTables:
         ax, hi = FACE_AXIS[self.master.kind][lf]
         io = n1 - 1 if hi else 0
         t = np.arange(self.nfn)
+        if nd == 1:
+            return np.full(1, io)
         if nd == 2:
             return io + n1 * t if ax == 0 else t + n1 * io
         a, b = t % n1, t // n1
@@ -416,6 +433,11 @@ class TensorTables:
         """Outward unit normal and |t1 x t2| of local face lf (affine; for
         curved elements the face-rule average normal and the area over the
         reference face measure, for the per-face quantities only)."""
+        if self.nd == 1:
+            # a point face: the reference normal, unit measure (disc.py:158-163)
+            sgn = 1.0 if FACE_AXIS[self.master.kind][lf][1] else -1.0
+            elems = np.asarray(elems)
+            return np.full((elems.size, 1), sgn), np.ones(elems.size)
         if getattr(self, "curved", False):
             _, n, mag = self.face_point_geometry(elems, lf)
             w = self.master.faces[lf].weights
@@ -464,6 +486,8 @@ class TensorTables:
                 n_l[sel], sj = self.face_normal_area(el[sel], lf)
                 area[sel] = sj * fw
         fi_h = 0.5 * (self.elem_vol[el] + self.elem_vol[er]) / np.maximum(area, 1e-300)
+        if self.nd == 1:                                   # disc.py:130-133
+            fi_h = 0.5 * (self.elem_vol[el] + self.elem_vol[er])
         tau_i = (tau / fi_h if over_h else np.full(nfi, tau)) + lam(n_l)
         self.fi_h = fi_h
         # neighbour node maps
@@ -505,6 +529,8 @@ class TensorTables:
                 nb_[sel], sj = self.face_normal_area(eb[sel], lf)
                 area_b[sel] = sj * fw
         fb_h = self.elem_vol[eb] / np.maximum(area_b, 1e-300)
+        if self.nd == 1:
+            fb_h = self.elem_vol[eb]
         tau_b = (tau / fb_h if over_h else np.full(eb.size, tau)) + lam(nb_)
         self.fb_h = fb_h
         self.n_left, self.sj_left, self.n_bnd, self.sj_bnd = n_l, area / fw, nb_, area_b / fw
@@ -527,6 +553,9 @@ class TensorTables:
         nfi = el.size
         if nfi == 0:
             return np.zeros(0, dtype=bool)
+        if self.nd == 1:
+            # nbar = the reference face normal (disc.py:158-163), beta_hat = 1
+            return np.asarray(fl) == 1
         if getattr(self, "curved", False):
             # non-affine faces: the reference's own normal-average pipeline
             return _reference_switch_subset(self.mesh, self.master, self.geom_master, el, fl)
@@ -820,6 +849,8 @@ class DenseTables:
                 nb_[sel], sj = self.face_normal_area(eb[sel], lf)
                 area_b[sel] = sj * m.faces[lf].weights.sum()
         fb_h = self.elem_vol[eb] / np.maximum(area_b, 1e-300)
+        if self.nd == 1:
+            fb_h = self.elem_vol[eb]
         tau_b = (tau / fb_h if over_h else np.full(eb.size, tau)) + lam(nb_)
         self.fb_h = fb_h
         fnbr[eb, fb] = np.arange(eb.size, dtype=np.int32)

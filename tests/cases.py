@@ -15,6 +15,7 @@ import numpy as np
 GOLDEN = Path(__file__).parent / "golden"
 
 BOX_PERIODIC = {
+    1: [(1, 2, (1.0,))],
     2: [(1, 2, (1.0, 0.0)), (3, 4, (0.0, 1.0))],
     3: [(1, 2, (1.0, 0.0, 0.0)), (3, 4, (0.0, 1.0, 0.0)), (5, 6, (0.0, 0.0, 1.0))],
 }
@@ -295,7 +296,7 @@ def build_case(spec, model_mod, mesh_mod, master_mod):
         for k, v in spec["numflux"].items():
             setattr(model.numflux, k, v)
     kind = spec["kind"]
-    nd = {"quad": 2, "tri": 2, "hex": 3, "tet": 3}[kind]
+    nd = {"line": 1, "quad": 2, "tri": 2, "hex": 3, "tet": 3}[kind]
     dom = spec.get("domain", (0.0, 1.0))
     if "curved" in spec:
         mesh = curved_mesh(spec, mesh_mod)
@@ -368,6 +369,21 @@ TRANSIENT_CASES.update({
         precond="mass", bj_apply=True),
 })
 
+# 1D (line elements) on the generated path: the reference's criterion-7
+# FD-vs-tangent case (1D Burgers, periodic, p = 3, 6 elements,
+# test_solver.py:146-168), a Dirichlet Poisson and a periodic
+# convection-diffusion (kind D: the mixed gradient too)
+NL_CASES.update({
+    "burgers1d_line_periodic_p3": dict(model=("builtin", "burgers", 1, None), kind="line",
+                                       counts=[6], p=3, periodic=1, state=([1.0], 0.3)),
+    "poisson1d_line_dirichlet_p3": dict(model=("builtin", "poisson", 1, None), kind="line",
+                                        counts=[7], p=3,
+                                        bcs={1: ("dirichlet", ["sin(x1)"]),
+                                             2: ("dirichlet", ["sin(x1)"])}),
+    "convdiff1d_line_periodic_p4": dict(model=("builtin", "convection_diffusion", 1, [1.0, 0.05]),
+                                        kind="line", counts=[5], p=4, periodic=1),
+})
+
 # non-affine (curved) elements on the generated path: the shallow-water
 # free-stream known answer on the curved O-grid annulus (the reference's
 # acceptance criterion 6, on quads) and Euler 3D on a periodically warped
@@ -392,6 +408,12 @@ CURVED_CASES = {
         curved=("warp", 2, 0.04), mesh_file="curved_euler_hex_warp_p2.npz",
         free=[1.0, 0.2, -0.1, 0.15, 2.5], state=([1.0, 0.2, -0.1, 0.15, 2.5], 0.05)),
 }
+
+# 1D steady solve (generated path, block-Jacobi): Poisson on 8 line
+# elements with u = sin(x) Dirichlet data (the reference flags)
+SOLVE_CASES["poisson1d_line_p3_n8_bj"] = dict(
+    model=("builtin", "poisson", 1, None), kind="line", counts=[8], p=3,
+    bcs={1: ("dirichlet", ["sin(x1)"]), 2: ("dirichlet", ["sin(x1)"])}, precond="block_jacobi")
 
 # steady Newton-GMRES on the curved annulus: Poisson with u = log r on both
 # circles (harmonic: the exact solution), block-Jacobi, acceptance flags
