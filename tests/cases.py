@@ -411,9 +411,13 @@ CURVED_CASES = {
 
 # 1D steady solve (generated path, block-Jacobi): Poisson on 8 line
 # elements with u = sin(x) Dirichlet data (the reference flags)
+# (the Newton stop is the reference's rel_tol 3e-8 on a residual that starts
+# at 104 -- the 1/h penalty of 8 elements -- and ends at 2.6e-7: the solution
+# is defined to ~1e-7, so this case's solution bar is 1e-6; counts exact)
 SOLVE_CASES["poisson1d_line_p3_n8_bj"] = dict(
     model=("builtin", "poisson", 1, None), kind="line", counts=[8], p=3,
-    bcs={1: ("dirichlet", ["sin(x1)"]), 2: ("dirichlet", ["sin(x1)"])}, precond="block_jacobi")
+    bcs={1: ("dirichlet", ["sin(x1)"]), 2: ("dirichlet", ["sin(x1)"])}, precond="block_jacobi",
+    u_tol=1e-6)
 
 # steady Newton-GMRES on the curved annulus: Poisson with u = log r on both
 # circles (harmonic: the exact solution), block-Jacobi, acceptance flags
