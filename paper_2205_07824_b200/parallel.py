@@ -700,6 +700,105 @@ class PartitionedNlSystem:
         return R[: self.plan.ne_loc] if out is None else out.copy_(R[: self.plan.ne_loc])
 
 
+class PartitionedPackedSystem(PartitionedNlSystem):
+    """A partitioned generated-kernel system with packed [u | q | w] states
+    (kind W: q is a state; pointwise ODE blocks w): the residual / tangent
+    of the u block read the neighbours' u, q and w (face traces, w^ = the
+    mean), so those blocks get ghost rows; the gradient equation of kind W
+    reads the neighbours' u; the ODE block, the mass and its inverse are
+    element- or node-local (disc.py:595-653, 866-948)."""
+
+    @property
+    def nw(self):
+        return self.model.nw
+
+    @property
+    def multi_block(self):
+        return self.kind == "W" or self.model.nw > 0
+
+    def block_sizes(self):
+        ne, nb = self.plan.ne_loc, self.n_nodes
+        sizes = [ne * nb * self.ncu]
+        if self.kind == "W":
+            sizes.append(ne * nb * self.ncu * self.nd)
+        if self.nw > 0:
+            sizes.append(ne * nb * self.nw)
+        return sizes
+
+    @property
+    def n_packed(self):
+        return int(sum(self.block_sizes()))
+
+    def unpack(self, Y):
+        ne, nb = self.plan.ne_loc, self.n_nodes
+        sizes = self.block_sizes()
+        parts, o = [], 0
+        for k in sizes:
+            parts.append(Y[o:o + k])
+            o += k
+        u = parts[0].reshape(ne, nb, self.ncu)
+        q = parts[1].reshape(ne, nb, self.ncu, self.nd) if self.kind == "W" else None
+        w = parts[-1].reshape(ne, nb, self.nw) if self.nw > 0 else None
+        return u, q, w
+
+    @staticmethod
+    def _cat(parts):
+        import torch
+        return torch.cat([p.reshape(-1) for p in parts if p is not None])
+
+    def _ext(self, a):
+        """(owned, ...) -> (owned + ghost, ...) with the ghost rows filled."""
+        if a is None:
+            return None
+        ext = self._new((self.plan.ne_loc + self.plan.n_ghost,) + tuple(a.shape[1:]))
+        ext[: self.plan.ne_loc].copy_(a)
+        self._exchange(ext)
+        return ext
+
+    def residual_packed_dev(self, Y, t=0.0):
+        u, q, w = self.unpack(Y)
+        ue, we = self._ext(u), self._ext(w)
+        if self.kind == "D":
+            qe = self.mixed_ext(ue, t)
+        else:
+            qe = self._ext(q)
+        ne = self.plan.ne_loc
+        Ru = self.nl.residual(ue, t, q=qe, w=we)[:ne]
+        Rq = self.nl.gradient_residual(ue, qe, t) if self.kind == "W" else None
+        Rw = self.nl.ode(ue, qe, we, t)[:ne] if self.nw > 0 else None
+        return self._cat([Ru, None if Rq is None else Rq[:ne], Rw])
+
+    def tangent_packed_dev(self, V, Y, t=0.0):
+        u, q, w = self.unpack(Y)
+        du, dq, dw = self.unpack(V)
+        ue, we, due, dwe = self._ext(u), self._ext(w), self._ext(du), self._ext(dw)
+        if self.kind == "D":
+            qe = self.mixed_ext(ue, t)
+            dqe = self.mixed_ext(due, t, homogeneous=True)
+        else:
+            qe, dqe = self._ext(q), self._ext(dq)
+        ne = self.plan.ne_loc
+        dRu = self.nl.tangent(ue, due, t, q=qe, w=we, dq=dqe, dw=dwe)[:ne]
+        dRq = self.nl.gradient_residual(due, dqe, t, tangent=True)[:ne] if self.kind == "W" \
+            else None
+        dRw = self.nl.ode(ue, qe, we, t, du=due, dq=dqe, dw=dwe)[:ne] if self.nw > 0 else None
+        return self._cat([dRu, dRq, dRw])
+
+    def mass_packed_dev(self, V, Y, t=0.0, scale=1.0):
+        u, _, _ = self.unpack(Y)
+        vu, vq, vw = self.unpack(V)
+        Mu = self.nl.mass(vu, u, t, scale)
+        Mq = self.nl.mass_q(vq, scale) if self.kind == "W" else None
+        Mw = (scale * self.model.ode.alpha) * vw if self.nw > 0 else None
+        return self._cat([Mu, Mq, Mw])
+
+    def mass_inv_packed_dev(self, V):
+        vu, vq, vw = self.unpack(V)
+        return self._cat([self.nl.mass_inv(vu),
+                          self.nl.mass_inv_q(vq) if self.kind == "W" else None,
+                          vw / self.model.ode.alpha if self.nw > 0 else None])
+
+
 def nl_apply_all(parts, us, tangent, bases=None, t=0.0):
     """Single-process lockstep of R partitions of a generated-kernel model on
     one GPU (ghost rows by device copies): the two halo steps of
