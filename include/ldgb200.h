@@ -17,6 +17,7 @@
  *   ldg_dcgs_dots / ldg_dcgs_update  delayed-reorth Gram-Schmidt     solver.py:130-144
  *   ldg_combine              x += Z^T y                       solver.py:163-164
  *   ldg_color_distance2      greedy distance-2 colouring      solver.py:355-378
+ *   ldg_face_nbar            mean face normal (switch bit)    disc.py:167-178, 122, 285-287
  *   ldg_bj_probe_vector      coloured unit probe              solver.py:327-330
  *   ldg_bj_extract           mats[b][:,k] = col[blocks[b]]    solver.py:331-334
  *   ldg_bj_invert            lu_factor (+1e-12 shift rule)    solver.py:335-345
@@ -247,6 +248,15 @@ int ldg_cgs_update(int64_t n, int k, const double* V, int64_t ldv,
 /* x += sum_i y[i] Z_i  (y device) */
 int ldg_combine(int64_t n, int k, const double* Z, int64_t ldz, const double* y,
                 double* x, void* stream);
+
+/* ---- setup (HOST memory) ---- */
+/* mean unit normal over the nq quadrature points of each face, in the
+ * reference's operation order (bit-identical to its tangent einsum / cross /
+ * norm / mean): gd (nq, ng, nrd) geometry-basis gradients at the face points,
+ * T (nrd-1, nrd) face embedding, ho (nfaces, ng, nc) the left elements'
+ * geometry nodes -> nbar (nfaces, nc); nc == nrd in {2, 3} */
+int ldg_face_nbar(int64_t nfaces, int nq, int ng, int nrd, int nc, const double* gd,
+                  const double* T, const double* ho, double* nbar);
 
 /* ---- block-Jacobi ---- */
 /* greedy distance-2 colouring of the element graph given by the interior

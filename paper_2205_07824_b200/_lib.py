@@ -61,6 +61,7 @@ class LdgDenseTables(C.Structure):
 
 
 _lib = None
+_host_lib = None
 
 _SIGS = {
     "ldg_version": ([], C.c_int),
@@ -105,6 +106,8 @@ _SIGS = {
                      C.c_void_p], C.c_int),
     "ldg_color_distance2": ([C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
                             C.c_int),
+    "ldg_face_nbar": ([C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 4,
+                      C.c_int),
     "ldg_probe_fp64": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_probe_fp64_mode": ([C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ldg_dcgs_dots": ([C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
@@ -143,9 +146,11 @@ EXPORTED = tuple(_SIGS)
 
 def load(require_gpu=True):
     """Load the native library (building it first if sources are newer)."""
-    global _lib
+    global _lib, _host_lib
     if _lib is not None:
         return _lib
+    if not require_gpu and _host_lib is not None:
+        return _host_lib
     if not LIB_PATH.exists():
         try:
             from .build import build
@@ -157,10 +162,12 @@ def load(require_gpu=True):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if require_gpu:
-        import torch
-        if not torch.cuda.is_available():
-            raise LdgNativeError("the B200 LDG path needs a CUDA device; no CPU fallback")
+    if not require_gpu:
+        _host_lib = lib        # host-only entry points (setup, NVRTC); not GPU-verified
+        return lib
+    import torch
+    if not torch.cuda.is_available():
+        raise LdgNativeError("the B200 LDG path needs a CUDA device; no CPU fallback")
     _lib = lib
     return lib
 
@@ -169,8 +176,9 @@ def check(rc, what, jit=False):
     if rc == 0:
         return
     msg = ""
-    if _lib is not None:
-        msg = (_lib.ldg_jit_last_error() if jit else _lib.ldg_last_error()).decode()
+    lib = _lib if _lib is not None else _host_lib
+    if lib is not None:
+        msg = (lib.ldg_jit_last_error() if jit else lib.ldg_last_error()).decode()
     raise LdgNativeError(f"{what} failed (code {rc}): {msg}")
 
 

@@ -619,6 +619,77 @@ int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, doubl
   return 0;
 }
 
+// Mean unit normal of each face over its quadrature points, in the
+// reference's own operation order (disc.py:167-178, :122): the tangent
+// einsum "qgd,sd,kgc->kqcs" as numpy evaluates it (per geometry node g a
+// partial sum over d of (gd T) ho, the partials added in g order), the
+// cross product a1 b2 - a2 b1 ..., the norm as a left-to-right sum of
+// squares, n = nv / |nv| and the mean as a left-to-right sum divided by nq.
+// Every operation is a single IEEE rounding (no contraction: host x86-64
+// code without FMA), so near-tie faces -- whose n_bar . beta_hat sign only
+// rounding decides (disc.py:285-287) -- get the reference's switch bit.
+// Host memory; OpenMP over faces.
+int ldg_face_nbar(int64_t nfaces, int nq, int ng, int nrd, int nc, const double* gd,
+                  const double* T, const double* ho, double* nbar) {
+  if (nfaces < 0 || nq <= 0 || ng <= 0 || nrd < 2 || nrd > 3 || nc != nrd ||
+      (nfaces && (!gd || !T || !ho || !nbar)))
+    return fail(2, "bad argument");
+  const int ns = nrd - 1;
+  std::vector<double> coef((size_t)nq * ng * nrd * ns);       // gd[q,g,d] * T[s,d]
+  for (int q = 0; q < nq; ++q)
+    for (int g = 0; g < ng; ++g)
+      for (int d = 0; d < nrd; ++d)
+        for (int sidx = 0; sidx < ns; ++sidx)
+          coef[(((size_t)q * ng + g) * nrd + d) * ns + sidx] =
+              gd[((size_t)q * ng + g) * nrd + d] * T[sidx * nrd + d];
+  const double* cf = coef.data();
+#pragma omp parallel for schedule(static)
+  for (int64_t f = 0; f < nfaces; ++f) {
+    const double* hf = ho + (size_t)f * ng * nc;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int q = 0; q < nq; ++q) {
+      double t[3][2];                                          // t[c][s]
+      for (int c = 0; c < nc; ++c)
+        for (int sidx = 0; sidx < ns; ++sidx) {
+          double out = 0.0;
+          for (int g = 0; g < ng; ++g) {
+            double part = 0.0;
+            for (int d = 0; d < nrd; ++d) {
+              const double prod = cf[(((size_t)q * ng + g) * nrd + d) * ns + sidx] * hf[g * nc + c];
+              part = part + prod;
+            }
+            out = out + part;
+          }
+          t[c][sidx] = out;
+        }
+      double nv[3];
+      if (nc == 2) {
+        nv[0] = t[1][0];
+        nv[1] = -t[0][0];
+      } else {
+        double a = t[1][0] * t[2][1], b = t[2][0] * t[1][1];
+        nv[0] = a - b;
+        a = t[2][0] * t[0][1]; b = t[0][0] * t[2][1];
+        nv[1] = a - b;
+        a = t[0][0] * t[1][1]; b = t[1][0] * t[0][1];
+        nv[2] = a - b;
+      }
+      double ss = nv[0] * nv[0];
+      for (int c = 1; c < nc; ++c) {
+        const double sq = nv[c] * nv[c];
+        ss = ss + sq;
+      }
+      const double mag = std::sqrt(ss);
+      for (int c = 0; c < nc; ++c) {
+        const double nn = nv[c] / mag;
+        acc[c] = q ? acc[c] + nn : nn;
+      }
+    }
+    for (int c = 0; c < nc; ++c) nbar[(size_t)f * nc + c] = acc[c] / (double)nq;
+  }
+  return 0;
+}
+
 // Greedy colouring of the distance-2 element graph (solver.py:355-378,
 // driver.py:109-142): element v takes the smallest colour not used by an
 // already coloured element within two face-neighbour hops, v = 0, 1, ... in

@@ -350,4 +350,4 @@ def _geometry_node_matching(mesh, el, fl, er, fr, translation):
                 raise MeshError(f"face node matching failed between elements "
                                 f"{el[f]} and {er[f]}")
             out[sel] = pm
-    return [row for row in out]
+    return out                                   # (n_faces, n_geometry_face_nodes); rows = perms

@@ -120,7 +120,6 @@ def plan_is_zero(plan):
 def reference_switch(mesh, topo, master, geom, chunk=1 << 16):
     nd = mesh.nd
     nfi = topo.elem_l.shape[0]
-    nqf = master.faces[0].weights.shape[0]
     nbar = np.zeros((nfi, nd))
     for lf in range(master.n_faces):
         sel = np.nonzero(topo.face_l == lf)[0]
@@ -133,16 +132,7 @@ def reference_switch(mesh, topo, master, geom, chunk=1 << 16):
             ho = mesh.ho_nodes[topo.elem_l[s]]
             if nd == 1:
                 raise DiscError("1D meshes are not supported by the B200 path")
-            tang = _tangents(gd, T, ho)
-            if nd == 2:
-                t = tang[:, :, :, 0]
-                nv = np.stack([t[:, :, 1], -t[:, :, 0]], axis=-1)
-            else:
-                nv = np.cross(tang[:, :, :, 0], tang[:, :, :, 1])
-            mag = np.linalg.norm(nv, axis=-1)
-            n = np.zeros((s.size, nqf, nd))
-            n[:] = nv / mag[:, :, None]
-            nbar[s] = n.mean(axis=1)
+            nbar[s] = _face_nbar(gd, T, ho)
     beta = np.ones(nd) / np.sqrt(nd)
     return (nbar @ beta) > 0.0
 
@@ -160,36 +150,86 @@ def _tangents(gd, T, ho, rows=4096):
     import os
     out = np.empty((k, gd.shape[0], ho.shape[2], T.shape[0]))
     starts = range(0, k, rows)
+    # the einsum's own evaluation order, restated as broadcast array ops (~10x
+    # faster than the 3-operand einsum loop): per geometry node g a partial
+    # sum over d of (gd T) ho, the partials added in g order.  Used only when
+    # it reproduces the einsum bit for bit on the first row block.
+    out[:rows] = np.einsum("qgd,sd,kgc->kqcs", gd, T, ho[:rows])
+    fast = np.array_equal(_tangents_ordered(gd, T, ho[:rows]), out[:rows])
 
     def run(a):
-        out[a:a + rows] = np.einsum("qgd,sd,kgc->kqcs", gd, T, ho[a:a + rows])
+        if a == 0:
+            return
+        if fast:
+            out[a:a + rows] = _tangents_ordered(gd, T, ho[a:a + rows])
+        else:
+            out[a:a + rows] = np.einsum("qgd,sd,kgc->kqcs", gd, T, ho[a:a + rows])
 
     with ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1))) as ex:
         list(ex.map(run, starts))
     return out
 
 
+def _tangents_ordered(gd, T, ho):
+    nq, ng, nrd = gd.shape
+    out = np.zeros((ho.shape[0], nq, ho.shape[2], T.shape[0]))
+    for g in range(ng):
+        part = np.zeros_like(out)
+        for d in range(nrd):
+            c = gd[:, g, d][:, None] * T[:, d][None, :]                 # (q, s)
+            part += c[None, :, None, :] * ho[:, g, :][:, None, :, None]
+        out += part
+    return out
+
+
+def _face_nbar_numpy(gd, T, ho):
+    nd = ho.shape[2]
+    tang = _tangents(gd, T, ho)
+    if nd == 2:
+        t = tang[:, :, :, 0]
+        nv = np.stack([t[:, :, 1], -t[:, :, 0]], axis=-1)
+    else:
+        nv = np.cross(tang[:, :, :, 0], tang[:, :, :, 1])
+    mag = np.linalg.norm(nv, axis=-1)
+    n = np.zeros((ho.shape[0], gd.shape[0], nd))
+    n[:] = nv / mag[:, :, None]
+    return n.mean(axis=1)
+
+
+def _face_nbar(gd, T, ho, check=256):
+    """Mean unit face normal in the reference's operation order
+    (disc.py:167-178, 122): the native ldg_face_nbar (host C++, OpenMP) when
+    the library is present and reproduces the numpy pipeline bit for bit on
+    the first faces, else the numpy pipeline itself."""
+    k, nd = ho.shape[0], ho.shape[2]
+    if k == 0 or nd not in (2, 3):
+        return _face_nbar_numpy(gd, T, ho)
+    try:
+        from . import _lib
+        lib = _lib.load(require_gpu=False)
+    except Exception:                                   # setup needs no GPU
+        return _face_nbar_numpy(gd, T, ho)
+    import ctypes as C
+    gd_, T_, ho_ = (np.ascontiguousarray(a, dtype=np.float64) for a in (gd, T, ho))
+    out = np.empty((k, nd))
+    rc = lib.ldg_face_nbar(k, gd_.shape[0], gd_.shape[1], gd_.shape[2], nd,
+                           gd_.ctypes.data_as(C.c_void_p), T_.ctypes.data_as(C.c_void_p),
+                           ho_.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p))
+    if rc != 0 or not np.array_equal(out[:check], _face_nbar_numpy(gd, T, ho[:check])):
+        return _face_nbar_numpy(gd, T, ho)
+    return out
+
+
 def _reference_switch_subset(mesh, master, geom, elems, lfs):
     """reference_switch restricted to the given (left element, face) list."""
     nd = mesh.nd
-    nqf = master.faces[0].weights.shape[0]
     out = np.zeros(elems.size, dtype=bool)
     nbar = np.zeros((elems.size, nd))
     for lf in np.unique(lfs):
         sel = np.nonzero(lfs == lf)[0]
         gd = geom.eval_basis_grad(master.faces[lf].xi)
         _, T = face_map(mesh.elem_kind, lf)
-        ho = mesh.ho_nodes[elems[sel]]
-        tang = _tangents(gd, T, ho)
-        if nd == 2:
-            t = tang[:, :, :, 0]
-            nv = np.stack([t[:, :, 1], -t[:, :, 0]], axis=-1)
-        else:
-            nv = np.cross(tang[:, :, :, 0], tang[:, :, :, 1])
-        mag = np.linalg.norm(nv, axis=-1)
-        n = np.zeros((sel.size, nqf, nd))
-        n[:] = nv / mag[:, :, None]
-        nbar[sel] = n.mean(axis=1)
+        nbar[sel] = _face_nbar(gd, T, mesh.ho_nodes[elems[sel]])
     beta = np.ones(nd) / np.sqrt(nd)
     out[:] = (nbar @ beta) > 0.0
     return out
@@ -198,6 +238,25 @@ def _reference_switch_subset(mesh, master, geom, elems, lfs):
 # ---------------------------------------------------------------------------
 # table builder
 # ---------------------------------------------------------------------------
+
+
+def _det_inv(J):
+    """det and inverse of a stack of nd x nd (nd <= 3) Jacobians by the
+    adjugate (vectorised; LAPACK's batched 3 x 3 LU costs ~10x more)."""
+    nd = J.shape[-1]
+    if nd == 1:
+        d = J[:, 0, 0].copy()
+        return d, (1.0 / d)[:, None, None]
+    if nd == 2:
+        a, b, c, e = J[:, 0, 0], J[:, 0, 1], J[:, 1, 0], J[:, 1, 1]
+        d = a * e - b * c
+        adj = np.stack([np.stack([e, -b], -1), np.stack([-c, a], -1)], -2)
+        return d, adj / d[:, None, None]
+    r0, r1, r2 = J[:, 0], J[:, 1], J[:, 2]
+    c0, c1, c2 = np.cross(r1, r2), np.cross(r2, r0), np.cross(r0, r1)
+    d = np.einsum("ed,ed->e", r0, c0)
+    inv = np.stack([c0, c1, c2], -1) / d[:, None, None]   # columns: the cofactor rows
+    return d, inv
 
 
 def _line_master_tables(m):
@@ -300,7 +359,8 @@ class TensorTables:
         self.geom_master = geom
         corners = refelem.VERTS[mesh.elem_kind]
         gd = geom.eval_basis_grad(corners)                    # (nv, ng, nd)
-        J = np.einsum("egd,vgr->evdr", mesh.ho_nodes, gd)
+        # J[e, v] = sum_g x_g (grad N_g)(corner v)^T: one batched GEMM
+        J = np.matmul(np.asarray(mesh.ho_nodes).transpose(0, 2, 1)[:, None], gd[None])
         scale = max(mesh.diameter(), 1.0)
         self.curved = bool(np.max(np.abs(J - J[:, :1])) > 1e-11 * scale)
         if self.curved:
@@ -314,11 +374,11 @@ class TensorTables:
                           geom.eval_basis_grad(np.zeros((1, nd)))[0])
         else:
             J = J[:, 0]
-        self.detj = np.linalg.det(J)
+        self.detj, inv = _det_inv(J)
         if np.any(self.detj <= 0):
             bad = int(np.argmax(self.detj <= 0))
             raise DiscError(f"nonpositive Jacobian in element {bad}")
-        self.invjt = np.linalg.inv(J).transpose(0, 2, 1)
+        self.invjt = inv.transpose(0, 2, 1)
         self.x0 = np.einsum("egd,g->ed", mesh.ho_nodes,
                             geom.eval_basis(np.zeros((1, nd)))[0])  # image of xi = 0
         self.J = J
@@ -781,6 +841,15 @@ class DenseTables:
         el, fl, er, fr = (np.asarray(a, dtype=np.int64) for a in
                           (topo.elem_l, topo.face_l, topo.elem_r, topo.face_r))
         nfi = el.size
+        # per element-face outward normal and |t1 x t2| (read below for the
+        # interior / boundary h and tau too)
+        self.fnorm = np.zeros((ne, nf, self.nd))
+        self.fsj = np.zeros((ne, nf))
+        for lf in range(nf):
+            n, sj = self.face_normal_area(np.arange(ne), lf)
+            self.fnorm[:, lf] = n
+            self.fsj[:, lf] = sj
+        wsum = np.array([m.faces[lf].weights.sum() for lf in range(nf)])
         self.switch = self._switch_bits(el, fl)
         fnbr = np.full((ne, nf), -1, dtype=np.int32)
         finfo = np.full((ne, nf), -1, dtype=np.int32)
@@ -800,13 +869,8 @@ class DenseTables:
                 b[f"n{k + 1}"] = normals[:, k]
             return evaluate(ws, b)[0]
 
-        n_l = np.zeros((nfi, self.nd))
-        area = np.zeros(nfi)
-        for lf in range(nf):
-            sel = np.nonzero(fl == lf)[0]
-            if sel.size:
-                n_l[sel], sj = self.face_normal_area(el[sel], lf)
-                area[sel] = sj * m.faces[lf].weights.sum()
+        n_l = self.fnorm[el, fl]
+        area = self.fsj[el, fl] * wsum[fl]
         fi_h = 0.5 * (self.elem_vol[el] + self.elem_vol[er]) / np.maximum(area, 1e-300)
         tau_i = (tau / fi_h if over_h else np.full(nfi, tau)) + lam(n_l)
         self.fi_h = fi_h
@@ -841,13 +905,8 @@ class DenseTables:
         kinds = np.zeros(eb.size, dtype=np.int32)
         for tag, bc, idx in self.bc_groups:
             kinds[idx] = {"dirichlet": 1, "neumann": 2, "absorbing": 3}[bc.type]
-        nb_ = np.zeros((eb.size, self.nd))
-        area_b = np.zeros(eb.size)
-        for lf in range(nf):
-            sel = np.nonzero(fb == lf)[0]
-            if sel.size:
-                nb_[sel], sj = self.face_normal_area(eb[sel], lf)
-                area_b[sel] = sj * m.faces[lf].weights.sum()
+        nb_ = self.fnorm[eb, fb]
+        area_b = self.fsj[eb, fb] * wsum[fb]
         fb_h = self.elem_vol[eb] / np.maximum(area_b, 1e-300)
         if self.nd == 1:
             fb_h = self.elem_vol[eb]
@@ -861,13 +920,6 @@ class DenseTables:
         self.fnbr, self.finfo, self.ftau = fnbr, finfo, ftau
         self.n_boundary = eb.size
         self.eb, self.fb = eb, fb
-        # per element-face outward normal and |t1 x t2|
-        self.fnorm = np.zeros((ne, nf, self.nd))
-        self.fsj = np.zeros((ne, nf))
-        for lf in range(nf):
-            n, sj = self.face_normal_area(np.arange(ne), lf)
-            self.fnorm[:, lf] = n
-            self.fsj[:, lf] = sj
 
     def face_points(self, elems, lf, pts=None):
         """Physical coordinates of face-lf quadrature points of elements."""
