@@ -191,7 +191,7 @@ def run_steady(system, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8, forc
     acceptance solver flags as defaults; returns (state, stats, timings)."""
     import torch
     t0 = time.perf_counter()
-    state = system.interpolate_initial()
+    state = system.interpolate_initial_dev()
     res_fn, tan_fn = _steady_fns(system)
     u0 = torch.as_tensor(state.u, device=system.device).reshape(-1)
     torch.cuda.synchronize()

@@ -876,9 +876,9 @@ def run_steady_partitioned(psys, precond="block_jacobi", abs_tol=1e-11, rel_tol=
     if psys.kind != "D" or not psys.model.is_steady():
         raise DriverError("partitioned steady solves need a steady kind-D model")
     t0 = time.perf_counter()
-    st = psys.sys.interpolate_initial()
+    st = psys.sys.interpolate_initial_dev()
     shape = (psys.n_elements, psys.n_nodes, psys.ncu)
-    u0 = torch.as_tensor(np.ascontiguousarray(st.u), device=psys.device).reshape(-1)
+    u0 = st.u.reshape(-1)
     ops = DistVecOps(vecops(psys.device), group)
     torch.cuda.synchronize(psys.device)
     t1 = time.perf_counter()

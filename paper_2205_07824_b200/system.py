@@ -780,3 +780,20 @@ class LdgSystem:
         if self.nw > 0:
             w = np.ascontiguousarray(vals[..., k:k + self.nw])
         return SolverState(u=u, q=q, w=w, t=0.0)
+
+    def interpolate_initial_dev(self):
+        """interpolate_initial with the init plan evaluated on the device at
+        every node (source_dev.device_initial_values): device u / q / w, no
+        host pass over the nodes."""
+        from .source_dev import device_initial_values
+        v = device_initial_values(self.tab, self.model, self.device)
+        k = self.ncu
+        u = v[..., :k].contiguous()
+        q = w = None
+        if self.kind == "W":
+            q = v[..., k:k + self.ncu * self.nd].contiguous().reshape(
+                self.n_elements, self.n_nodes, self.ncu, self.nd)
+            k += self.ncu * self.nd
+        if self.nw > 0:
+            w = v[..., k:k + self.nw].contiguous()
+        return SolverState(u=u, q=q, w=w, t=0.0)

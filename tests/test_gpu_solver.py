@@ -359,3 +359,38 @@ def test_partitioned_newton_gmres_two_ranks_matches_reference(tmp_path, name, or
                                                    g["gmres_iters"].tolist())), \
             (p["gmres"], g["gmres_iters"])
     assert rel(u, g["u"]) < 1e-10, rel(u, g["u"])
+
+
+@pytest.mark.parametrize("name", ["convdiff2d_quad_p3_dirk22", "convdiff3d_hex_p2_dirk11",
+                                  "euler2d_vortex_quad_p3_dirk22", "ns3d_tgv_hex_p2_dirk11",
+                                  "wave2d_quad_p3_dirk22"])
+def test_device_initial_state_matches_reference(name):
+    """interpolate_initial_dev (init plan evaluated on the device at every
+    node, disc.py:420-432) vs the reference's own initial state (golden u0)
+    and the host restatement (u, and q / w where the model has them)."""
+    from cases import TRANSIENT_CASES
+    from paper_2205_07824_b200.system import LdgSystem
+    g = np.load(GOLDEN / f"transient_{name}.npz")
+    s = LdgSystem(*build_case(TRANSIENT_CASES[name], *b200_setup()))
+    d = s.interpolate_initial_dev()
+    h = s.interpolate_initial()
+    assert d.u.is_cuda
+    assert rel(d.u.cpu().numpy(), g["u0"]) < 1e-13
+    for a, b in ((d.u, h.u), (d.q, h.q), (d.w, h.w)):
+        assert (a is None) == (b is None)
+        if a is not None:
+            assert a.shape == b.shape
+            assert rel(a.cpu().numpy(), b) < 1e-13 or np.linalg.norm(b) == 0.0
+
+
+def test_device_initial_state_curved_and_simplex():
+    """Curved (geometry-map node positions) and tet (dense tables) systems:
+    device initial state vs the host restatement."""
+    from cases import CURVED_CASES, SOLVE_CASES
+    from paper_2205_07824_b200.system import LdgSystem
+    for spec in (CURVED_CASES["curved_poisson_annulus_quad_p3"],
+                 dict(SOLVE_CASES["known_poisson3d_tet_p3_n4_bj"],
+                      init="sin(pi*x1)*cos(2*x2)*x3")):
+        s = LdgSystem(*build_case(spec, *b200_setup()))
+        d, h = s.interpolate_initial_dev(), s.interpolate_initial()
+        assert rel(d.u.cpu().numpy(), h.u) < 1e-13 or np.linalg.norm(h.u) == 0.0
