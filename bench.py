@@ -150,7 +150,8 @@ def run_solve(system, orth="dcgs2"):
             "warm": {"precond_build_s": tm2["precond_build_s"], "solve_s": tm2["solve_s"],
                      "time_to_solution_s": tm2["precond_build_s"] + tm2["solve_s"]},
             "newton_iters": stats.newton_iters, "gmres_iters": stats.total_gmres_iters,
-            "final_residual": stats.final_residual, "error_u": err}
+            "final_residual": stats.final_residual, "error_u": err,
+            "bj_blocks": tm.get("bj_blocks"), "bj_inverses": tm.get("bj_inverses")}
 
 
 def run_strong(args, world, dev, steps=10):

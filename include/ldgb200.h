@@ -22,6 +22,7 @@
  *   ldg_bj_extract           mats[b][:,k] = col[blocks[b]]    solver.py:331-334
  *   ldg_bj_invert            lu_factor (+1e-12 shift rule)    solver.py:335-345
  *   ldg_bj_apply             BlockJacobiPreconditioner.apply  solver.py:296-300
+ *   ldg_bj_apply_tiles       same, blocks shared by element classes
  *   ldg_jit_*                NVRTC modules of the generated kernels (nonlinear
  *                            models, disc.py:436-948; the volume source load
  *                            disc.py:621-629)
@@ -283,6 +284,15 @@ int ldg_bj_invert_global(int64_t nblk, int bs, const double* mats, double* inv_t
                          int32_t* shifted, void* stream);
 int ldg_bj_apply(int64_t nblk, int bs, const double* inv_t, const double* r,
                  double* z, void* stream);
+/* BlockJacobiPreconditioner.apply (solver.py:296-300) with the inverses
+ * shared by classes of elements whose blocks are bit-identical (interior
+ * elements of one geometry class on structured meshes): tile t applies
+ * class tile_cls[t]'s inverse (inv_t: classes x bs x bs, transposed) to the
+ * rows of up to ldg_bj_tile_elems() elements tile_el[t * E .. t * E + E)
+ * (-1 = unused slot) */
+int ldg_bj_tile_elems(void);
+int ldg_bj_apply_tiles(int64_t ntiles, int bs, const double* inv_t, const int32_t* tile_cls,
+                       const int32_t* tile_el, const double* r, double* z, void* stream);
 /* element blocks across a packed (u | q | w) vector (driver.py:128-142,
  * _elementwise_blocks): idx[e*bs + j] = packed index of row j of block e;
  * gather dst[i] = src[idx[i]], scatter dst[idx[i]] = src[i] */

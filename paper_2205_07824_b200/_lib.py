@@ -106,6 +106,8 @@ _SIGS = {
                      C.c_void_p], C.c_int),
     "ldg_color_distance2": ([C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
                             C.c_int),
+    "ldg_bj_tile_elems": ([], C.c_int),
+    "ldg_bj_apply_tiles": ([C.c_int64, C.c_int] + [C.c_void_p] * 6, C.c_int),
     "ldg_face_nbar": ([C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 4,
                       C.c_int),
     "ldg_probe_fp64": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),

@@ -304,6 +304,49 @@ bj_apply_big_kernel(int bs, const double* __restrict__ inv_t,
   }
 }
 
+// class-shared blocks (structured meshes: interior elements of one geometry
+// class have bit-identical blocks): a tile = up to kTileE elements of one
+// class; thread i owns output row i and reuses each inverse entry
+// inv_t[cls][j][i] (one L1 / L2 load) for the tile's elements, whose r rows
+// sit in shared memory as [j][element] (16-B broadcast reads of 2 elements)
+constexpr int kTileE = 16;
+constexpr int kTileS = kTileE + 2;      // row stride: 16-B aligned rows, 4-way (not 32-way) store conflicts
+__global__ void __launch_bounds__(256)
+bj_apply_tiles_kernel(int bs, const double* __restrict__ inv_t, const int32_t* __restrict__ tile_cls,
+                      const int32_t* __restrict__ tile_el, const double* __restrict__ r,
+                      double* __restrict__ z) {
+  extern __shared__ __align__(16) double rt[];                // [j][kTileS]
+  const int64_t t = blockIdx.x;
+  const int32_t* els = tile_el + t * kTileE;
+  for (int x = threadIdx.x; x < kTileE * bs; x += blockDim.x) {
+    const int e = x / bs, j = x % bs;                          // coalesced along j
+    const int32_t el = els[e];
+    rt[j * kTileS + e] = el >= 0 ? r[(int64_t)el * bs + j] : 0.0;
+  }
+  __syncthreads();
+  const double* It = inv_t + (int64_t)tile_cls[t] * bs * bs;
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) {
+    double acc[kTileE];
+#pragma unroll
+    for (int e = 0; e < kTileE; ++e) acc[e] = 0.0;
+    for (int j = 0; j < bs; ++j) {
+      const double a = __ldg(It + (int64_t)j * bs + i);
+      const double2* rj = reinterpret_cast<const double2*>(rt + j * kTileS);
+#pragma unroll
+      for (int e2 = 0; e2 < kTileE / 2; ++e2) {
+        const double2 v = rj[e2];
+        acc[2 * e2] = fma(a, v.x, acc[2 * e2]);
+        acc[2 * e2 + 1] = fma(a, v.y, acc[2 * e2 + 1]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < kTileE; ++e) {
+      const int32_t el = els[e];
+      if (el >= 0) z[(int64_t)el * bs + i] = acc[e];
+    }
+  }
+}
+
 // packed (u | q | w) <-> element-major block order (driver.py:128-142):
 // dst[i] = src[idx[i]] and dst[idx[i]] = src[i]
 __global__ void gather_kernel(int64_t n, const int64_t* __restrict__ idx,
@@ -403,6 +446,24 @@ int ldg_permute_scatter(int64_t n, const int64_t* idx, const double* src, double
   if (n <= 0) return 0;
   if (!idx || !src || !dst) return 2;
   scatter_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
+  return rc();
+}
+
+int ldg_bj_tile_elems() { return kTileE; }
+
+int ldg_bj_apply_tiles(int64_t ntiles, int bs, const double* inv_t, const int32_t* tile_cls,
+                       const int32_t* tile_el, const double* r, double* z, void* stream) {
+  NvtxRange nvtx_("ldg_bj_apply_tiles");
+  if (ntiles <= 0) return 0;
+  if (bs < 1 || !inv_t || !tile_cls || !tile_el || !r || !z) return 2;
+  const int threads = std::min(256, ((bs + 31) / 32) * 32);
+  const size_t sm = (size_t)kTileS * bs * sizeof(double);
+  if (sm > 48 * 1024 &&
+      cudaFuncSetAttribute(bj_apply_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sm) != cudaSuccess)
+    return 3;
+  bj_apply_tiles_kernel<<<(unsigned)ntiles, threads, sm, (cudaStream_t)stream>>>(
+      bs, inv_t, tile_cls, tile_el, r, z);
   return rc();
 }
 

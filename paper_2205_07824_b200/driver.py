@@ -14,8 +14,9 @@ import time
 
 import numpy as np
 
-from .solver import (NewtonOptions, build_block_jacobi, distance2_coloring,
-                     distance2_coloring_topology, element_neighbor_sets, newton_solve)
+from .solver import (BlockJacobiPreconditioner, NewtonOptions, build_block_jacobi,
+                     distance2_coloring, distance2_coloring_topology, element_neighbor_sets,
+                     newton_solve)
 
 
 class DriverError(RuntimeError):
@@ -76,7 +77,7 @@ def elementwise_block_perm(system, device):
 
 
 def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="tangent",
-                           colors=None, invert="auto"):
+                           colors=None, invert="auto", share=True):
     """Exact per-element diagonal blocks via distance-2 coloured probing
     (driver.py:119-142), through the tangent or by finite differences
     (``jv_mode``), across the packed blocks of kind-W / ODE systems."""
@@ -89,7 +90,8 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
     if getattr(system, "multi_block", False):
         perm, bs = elementwise_block_perm(system, x.device)
         return build_block_jacobi(tangent_fn, x, system.n_elements, bs, colors, perm=perm,
-                                  mode=jv_mode, residual_fn=residual_fn, invert=invert)
+                                  mode=jv_mode, residual_fn=residual_fn, invert=invert,
+                                  share=share)
     native = None
     if (jv_mode == "tangent" and type(system) is LdgSystem and system.nl is None
             and getattr(system, "_h", None) is not None
@@ -97,7 +99,7 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
         native = (system._h, system.scratch())        # the linear tangent ignores the base
     return build_block_jacobi(tangent_fn, x, system.n_elements,
                               system.n_nodes * system.ncu, colors, native=native,
-                              mode=jv_mode, residual_fn=residual_fn, invert=invert)
+                              mode=jv_mode, residual_fn=residual_fn, invert=invert, share=share)
 
 
 class CompositeManager:
@@ -209,7 +211,11 @@ def run_steady(system, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8, forc
     if not stats.converged:
         raise DriverError(f"steady Newton solve did not converge "
                           f"(residual {stats.final_residual:.3e})")
-    return out, stats, {"init_s": t1 - t0, "precond_build_s": t2 - t1, "solve_s": t3 - t2}
+    tm = {"init_s": t1 - t0, "precond_build_s": t2 - t1, "solve_s": t3 - t2}
+    if isinstance(M, BlockJacobiPreconditioner):
+        tm["bj_blocks"] = M.nblk
+        tm["bj_inverses"] = int(M.inv_t.shape[0])     # < bj_blocks: class-shared inverses
+    return out, stats, tm
 
 
 # ---------------------------------------------------------------------------

@@ -643,12 +643,30 @@ class BlockJacobiPreconditioner:
     systems): perm[e*bs + j] = packed index of row j of element e's block
     (driver.py:128-142), gathered / scattered by native kernels."""
 
-    def __init__(self, inv_t, bs, shifted=None, perm=None):
+    def __init__(self, inv_t, bs, shifted=None, perm=None, classes=None):
+        import torch
         self.inv_t, self.bs = inv_t, bs
-        self.nblk = inv_t.shape[0]
         self.shifted = shifted
         self.perm = perm
         self.lib = _lib.load()
+        self.classes = classes
+        if classes is None:
+            self.nblk = inv_t.shape[0]
+            return
+        self.nblk = int(classes.numel())
+        self.tile_cls, self.tile_el = class_tiles(classes, inv_t.shape[0],
+                                                  int(self.lib.ldg_bj_tile_elems()))
+        self.ntiles = int(self.tile_cls.numel())
+
+    def _apply_blocks(self, r, z, st):
+        if self.classes is None:
+            _lib.check(self.lib.ldg_bj_apply(self.nblk, self.bs, _lib.ptr(self.inv_t),
+                                             _lib.ptr(r), _lib.ptr(z), st), "ldg_bj_apply")
+        else:
+            _lib.check(self.lib.ldg_bj_apply_tiles(self.ntiles, self.bs, _lib.ptr(self.inv_t),
+                                                   _lib.ptr(self.tile_cls), _lib.ptr(self.tile_el),
+                                                   _lib.ptr(r), _lib.ptr(z), st),
+                       "ldg_bj_apply_tiles")
 
     def apply(self, r):
         import torch
@@ -656,15 +674,13 @@ class BlockJacobiPreconditioner:
         z = torch.empty_like(rd)
         st = _lib.stream_ptr()
         if self.perm is None:
-            _lib.check(self.lib.ldg_bj_apply(self.nblk, self.bs, _lib.ptr(self.inv_t),
-                                             _lib.ptr(rd), _lib.ptr(z), st), "ldg_bj_apply")
+            self._apply_blocks(rd, z, st)
         else:
             re, ze = torch.empty_like(rd), torch.empty_like(rd)
             n = rd.numel()
             _lib.check(self.lib.ldg_permute_gather(n, _lib.ptr(self.perm), _lib.ptr(rd),
                                                    _lib.ptr(re), st), "ldg_permute_gather")
-            _lib.check(self.lib.ldg_bj_apply(self.nblk, self.bs, _lib.ptr(self.inv_t),
-                                             _lib.ptr(re), _lib.ptr(ze), st), "ldg_bj_apply")
+            self._apply_blocks(re, ze, st)
             _lib.check(self.lib.ldg_permute_scatter(n, _lib.ptr(self.perm), _lib.ptr(ze),
                                                     _lib.ptr(z), st), "ldg_permute_scatter")
         return z if dev else z.cpu().numpy()
@@ -722,14 +738,16 @@ def element_neighbor_sets(topology, n_elements):
 
 def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, perm=None,
                        mode="tangent", residual_fn=None, base_residual=None, all_colors=None,
-                       invert="auto"):
+                       invert="auto", share=True):
     """Exact diagonal blocks by coloured unit probes (solver.py:303-346):
     colours x bs device Jacobian-vector products (``mode`` "tangent" through
     ``tangent_fn``, "fd" through ``residual_fn`` like jacobian_vector), then
     batched Gauss-Jordan inverses with the reference's 1e-12 shift rule.
     ``native`` = (handle, scratch) runs a colour's probes in one C call
     (only for the handle's own linear tangent); ``perm`` maps element-major
-    block rows to packed indices (kind W / ODE systems).  ``all_colors``
+    block rows to packed indices (kind W / ODE systems).  ``share``: blocks
+    that are bit-identical (structured meshes) are inverted once and applied
+    per class (_block_classes; same z bit for bit).  ``all_colors``
     (partitioned systems): probe colours 0..all_colors-1 even where this
     rank owns no element of a colour, so the ranks' halo exchanges pair."""
     import torch
@@ -779,15 +797,78 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, per
                 col = ce
             _lib.check(lib.ldg_bj_extract(bs, _lib.ptr(members), members.numel(), k,
                                           _lib.ptr(col), _lib.ptr(mats), st), "extract")
+    classes = _block_classes(mats) if share else None
+    if classes is not None:
+        cls, reps = classes
+        mats = mats[reps].contiguous()
+    nb_inv = mats.shape[0]
     inv_t = torch.empty_like(mats)
-    shifted = torch.zeros(n_blocks, dtype=torch.int32, device=dev)
+    shifted = torch.zeros(nb_inv, dtype=torch.int32, device=dev)
     # blocks <= 160 in shared memory, larger ones (NS hex p=3: 320) on an
     # L2-resident global working copy; invert="global" forces the latter
     fn = lib.ldg_bj_invert_global if invert == "global" else lib.ldg_bj_invert
-    _lib.check(fn(n_blocks, bs, _lib.ptr(mats), _lib.ptr(inv_t), _lib.ptr(shifted), st),
+    _lib.check(fn(nb_inv, bs, _lib.ptr(mats), _lib.ptr(inv_t), _lib.ptr(shifted), st),
                "ldg_bj_invert")
     del mats
+    if classes is not None:
+        return BlockJacobiPreconditioner(inv_t, bs, shifted[cls], perm=perm, classes=cls)
     return BlockJacobiPreconditioner(inv_t, bs, shifted, perm=perm)
+
+
+def class_tiles(classes, nclass, E):
+    """Element tiles of one class each for ldg_bj_apply_tiles: (class per
+    tile, E element ids per tile, -1 padded), elements in increasing order
+    within a class."""
+    import torch
+    n = int(classes.numel())
+    order = torch.argsort(classes, stable=True)
+    cs = classes[order]
+    counts = torch.bincount(cs, minlength=nclass)
+    starts = torch.cumsum(counts, 0) - counts
+    ntile_c = (counts + E - 1) // E
+    tile_cls = torch.repeat_interleave(torch.arange(nclass, device=cs.device), ntile_c)
+    first = torch.cumsum(ntile_c, 0) - ntile_c                  # first tile of each class
+    pos = torch.arange(n, device=cs.device) - starts[cs]         # rank within the class
+    slot = (first[cs] + pos // E) * E + pos % E
+    tile_el = torch.full((int(ntile_c.sum()) * E,), -1, dtype=torch.int32, device=cs.device)
+    tile_el[slot] = order.to(torch.int32)
+    return tile_cls.to(torch.int32).contiguous(), tile_el
+
+
+BJ_SHARE_MAX_FRACTION = 0.125   # share inverses when classes <= 1/8 of the blocks
+
+
+def _block_classes(mats, chunk=4096):
+    """Classes of bit-identical blocks (structured meshes: every interior
+    element of one geometry class probes to the same block, bit for bit):
+    an exact integer hash of the blocks' bit patterns, then every block is
+    compared with its class representative -- any mismatch (a hash
+    collision) and no sharing.  Returns (class per block, representative
+    block per class) or None when sharing would not pay."""
+    import torch
+    nblk = mats.shape[0]
+    if nblk < 64:
+        return None
+    flat = mats.reshape(nblk, -1)
+    gen = torch.Generator(device="cpu").manual_seed(0x5eed)
+    w = torch.randint(1, 2 ** 62, (2, flat.shape[1]), generator=gen, dtype=torch.int64)
+    w = (w * 2 + 1).to(mats.device)                      # odd multipliers
+    keys = torch.empty((nblk, 2), dtype=torch.int64, device=mats.device)
+    for a in range(0, nblk, chunk):
+        bits = flat[a:a + chunk].view(torch.int64)
+        keys[a:a + chunk, 0] = (bits * w[0]).sum(dim=1)    # wraps mod 2^64: exact, order-free
+        keys[a:a + chunk, 1] = ((bits ^ (bits >> 31)) * w[1]).sum(dim=1)
+    uniq, cls = torch.unique(keys, dim=0, return_inverse=True)
+    nclass = uniq.shape[0]
+    if nclass > BJ_SHARE_MAX_FRACTION * nblk:
+        return None
+    reps = torch.full((nclass,), nblk, dtype=torch.int64, device=mats.device)
+    reps.scatter_reduce_(0, cls, torch.arange(nblk, device=mats.device), reduce="amin")
+    for a in range(0, nblk, chunk):
+        c = cls[a:a + chunk]
+        if not bool((flat[a:a + chunk] == flat[reps[c]]).all()):
+            return None
+    return cls, reps
 
 
 BJ_SMEM_MAX_BS = 160            # ldg_bj_invert's in-shared-memory limit (bjacobi.cu)

@@ -240,25 +240,6 @@ def _reference_switch_subset(mesh, master, geom, elems, lfs):
 # ---------------------------------------------------------------------------
 
 
-def _det_inv(J):
-    """det and inverse of a stack of nd x nd (nd <= 3) Jacobians by the
-    adjugate (vectorised; LAPACK's batched 3 x 3 LU costs ~10x more)."""
-    nd = J.shape[-1]
-    if nd == 1:
-        d = J[:, 0, 0].copy()
-        return d, (1.0 / d)[:, None, None]
-    if nd == 2:
-        a, b, c, e = J[:, 0, 0], J[:, 0, 1], J[:, 1, 0], J[:, 1, 1]
-        d = a * e - b * c
-        adj = np.stack([np.stack([e, -b], -1), np.stack([-c, a], -1)], -2)
-        return d, adj / d[:, None, None]
-    r0, r1, r2 = J[:, 0], J[:, 1], J[:, 2]
-    c0, c1, c2 = np.cross(r1, r2), np.cross(r2, r0), np.cross(r0, r1)
-    d = np.einsum("ed,ed->e", r0, c0)
-    inv = np.stack([c0, c1, c2], -1) / d[:, None, None]   # columns: the cofactor rows
-    return d, inv
-
-
 def _line_master_tables(m):
     """1D GLL / Gauss tables of a line master in the attributes the tensor
     tables read (a line master's own tabulations are already 1D)."""
@@ -359,8 +340,7 @@ class TensorTables:
         self.geom_master = geom
         corners = refelem.VERTS[mesh.elem_kind]
         gd = geom.eval_basis_grad(corners)                    # (nv, ng, nd)
-        # J[e, v] = sum_g x_g (grad N_g)(corner v)^T: one batched GEMM
-        J = np.matmul(np.asarray(mesh.ho_nodes).transpose(0, 2, 1)[:, None], gd[None])
+        J = np.einsum("egd,vgr->evdr", mesh.ho_nodes, gd)
         scale = max(mesh.diameter(), 1.0)
         self.curved = bool(np.max(np.abs(J - J[:, :1])) > 1e-11 * scale)
         if self.curved:
@@ -374,11 +354,14 @@ class TensorTables:
                           geom.eval_basis_grad(np.zeros((1, nd)))[0])
         else:
             J = J[:, 0]
-        self.detj, inv = _det_inv(J)
+        # numpy's det / inv as the reference calls them (disc.py:94-96): the
+        # geometry bits feed every operator coefficient, and the 1e-10
+        # solution bar of the identity-preconditioned solves rides on them
+        self.detj = np.linalg.det(J)
         if np.any(self.detj <= 0):
             bad = int(np.argmax(self.detj <= 0))
             raise DiscError(f"nonpositive Jacobian in element {bad}")
-        self.invjt = inv.transpose(0, 2, 1)
+        self.invjt = np.linalg.inv(J).transpose(0, 2, 1)
         self.x0 = np.einsum("egd,g->ed", mesh.ho_nodes,
                             geom.eval_basis(np.zeros((1, nd)))[0])  # image of xi = 0
         self.J = J
