@@ -27,6 +27,10 @@
  *                            models, disc.py:436-948; the volume source load
  *                            disc.py:621-629)
  *   ldg_probe_fp64           measurement helper (FP64 FMA peak), no counterpart
+ *   ldg_comm_* / ldg_set_halo_plan / ldg_apply_dist
+ *                            multi-GPU boundary (SURVEY 8(b) "ldg_comm_init(ncclComm_t,
+ *                            partition), halo exchange inside the matvec"); the
+ *                            reference is single-process (no counterpart)
  *
  * Conventions: every double* / int* argument is DEVICE memory owned by the
  * caller (PyTorch tensors on the host side); the handle owns only the
@@ -343,6 +347,36 @@ int ldg_probe_fp64(int64_t iters, double* tflops, double* ms, void* stream);
 /* mode 0: DFMA, 1: FP64 tensor core (mma.sync m8n8k4 f64), 2: both in one
  * loop (tflops = their sum) -- decides whether DMMA adds FP64 throughput */
 int ldg_probe_fp64_mode(int mode, int64_t iters, double* tflops, double* ms, void* stream);
+
+/* ---- multi-GPU: element partitions, halos inside the operator call ---- */
+/* NCCL transport: rank 0 gets a 128-byte unique id, the caller broadcasts
+ * it (any transport), every rank attaches a communicator to its handle
+ * (collective, blocking).  libnccl.so.2 is dlopen'ed (the process's own
+ * first); code 4 = NCCL error / NCCL missing. */
+int ldg_comm_unique_id(uint8_t* id128);
+int ldg_comm_init(LdgHandle* h, int nranks, int rank, const uint8_t* id128);
+/* in-process transport: handles hs[0..n) on one device act as ranks 0..n-1,
+ * each driven from its own host thread (tests, one-GPU pools) */
+int ldg_comm_init_local(LdgHandle** hs, int n);
+/* The rank's partition (parallel.py PartitionPlan): ne_owned owned elements,
+ * [interior0, interior1) touch no ghost (computed while halos fly), u_ghost
+ * the ghost rows the kernels read (ldg_set_ghost_rows).  Per peer k (ranks
+ * ascending): u rows (width u_width doubles = ncu) sent from the owned
+ * vector, u_send_idx[u_send_off[k] .. u_send_off[k+1]), received into
+ * u_ghost rows u_recv_idx[...]; export rows of X (width x_width doubles)
+ * likewise.  Index lists are host arrays, copied. */
+int ldg_set_halo_plan(LdgHandle* h, int ne_owned, int interior0, int interior1, double* u_ghost,
+                      int u_width, int x_width, int npeers, const int32_t* peers,
+                      const int64_t* u_send_off, const int64_t* u_send_idx,
+                      const int64_t* u_recv_off, const int64_t* u_recv_idx,
+                      const int64_t* x_send_off, const int64_t* x_send_idx,
+                      const int64_t* x_recv_off, const int64_t* x_recv_idx);
+/* R = residual (tangent = 0) or J u (tangent = 1) of the rank's owned
+ * elements, both halo exchanges inside the call and overlapped with the
+ * interior elements' passes (X: the export scratch, owned + ghost slots) */
+int ldg_apply_dist(LdgHandle* h, int tangent, const double* u, const double* gproj,
+                   const double* bsrc, double* X, double* R, void* stream);
+int ldg_comm_destroy(LdgHandle* h);
 
 #ifdef __cplusplus
 }

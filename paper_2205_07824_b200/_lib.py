@@ -108,6 +108,13 @@ _SIGS = {
                             C.c_int),
     "ldg_bj_tile_elems": ([], C.c_int),
     "ldg_bj_apply_tiles": ([C.c_int64, C.c_int] + [C.c_void_p] * 6, C.c_int),
+    "ldg_comm_unique_id": ([C.c_void_p], C.c_int),
+    "ldg_comm_init": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "ldg_comm_init_local": ([C.c_void_p, C.c_int], C.c_int),
+    "ldg_set_halo_plan": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                           C.c_int] + [C.c_void_p] * 9, C.c_int),
+    "ldg_apply_dist": ([C.c_void_p, C.c_int] + [C.c_void_p] * 6, C.c_int),
+    "ldg_comm_destroy": ([C.c_void_p], C.c_int),
     "ldg_face_nbar": ([C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 4,
                       C.c_int),
     "ldg_probe_fp64": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),

@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "lib" / "libldgb200.so"
 SOURCES = ["capi.cu", "ldg_tensor.cu", "ldg_fused.cu", "ldg_dense.cu", "krylov.cu",
-           "bjacobi.cu", "jit.cu", "probe.cu"]
+           "bjacobi.cu", "jit.cu", "probe.cu", "comm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -63,7 +63,7 @@ def build(force=False, verbose=False, out=None, defines=()):
         if p.returncode:
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "shared", *map(str, objs), "-lnvrtc", "-lgomp",
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "shared", *map(str, objs), "-lnvrtc", "-lgomp", "-ldl",
            "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-o", str(tmp)]
     subprocess.run(cmd, check=True)
     os.replace(tmp, lib)

@@ -59,6 +59,11 @@ struct LdgHandle {
   cudaEvent_t ev_start = nullptr;
 };
 
+namespace ldg {
+// error reporting for the other translation units of the C ABI (comm.cu)
+int set_error(int code, const char* what, cudaError_t e) { return fail(code, what, e); }
+}  // namespace ldg
+
 extern "C" {
 
 int ldg_version(void) { return 1; }
@@ -302,6 +307,7 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
 
 int ldg_destroy(LdgHandle* h) {
   if (!h) return 0;
+  ldg_comm_destroy(h);                   // the handle's communicator / halo plan, if any
   for (void* p : h->dense_bufs) cudaFree(p);
   cudaFree(h->geo); cudaFree(h->fnbr); cudaFree(h->finfo); cudaFree(h->ftau);
   cudaFree(h->nmap); cudaFree(h->frec); cudaFree(h->kco); cudaFree(h->bad);

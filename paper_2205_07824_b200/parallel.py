@@ -457,17 +457,96 @@ class PartitionedLdgSystem:
         self._pass(2, u, tangent, t, R, b, p.ne_loc)
         return R
 
+    # -- native halos: the exchange inside the C call (ldg_apply_dist) ---------------------
+    def _native_plan(self):
+        """ldg_set_halo_plan from the PartitionPlan lists (peers ascending;
+        u rows of width ncu, export rows of width nfn * ncu)."""
+        import ctypes as C
+        from . import _lib as L
+        p = self.plan
+        peers = sorted(set(p.u_send) | set(p.u_recv) | set(p.x_send) | set(p.x_recv))
+
+        def flat(d):
+            rows = [np.asarray(d.get(q, np.zeros(0)), dtype=np.int64) for q in peers]
+            off = np.zeros(len(peers) + 1, dtype=np.int64)
+            off[1:] = np.cumsum([r.size for r in rows]) if rows else []
+            idx = np.concatenate(rows) if rows else np.zeros(0, dtype=np.int64)
+            return off, np.ascontiguousarray(idx)
+        arrs = [flat(d) for d in (p.u_send, p.u_recv, p.x_send, p.x_recv)]
+        self._native_keep = arrs
+        ptrs = []
+        for off, idx in arrs:
+            ptrs += [off.ctypes.data_as(C.c_void_p), idx.ctypes.data_as(C.c_void_p)]
+        pr = np.asarray(peers, dtype=np.int32)
+        self._native_keep.append(pr)
+        a, b = p.interior
+        L.check(self.sys.lib.ldg_set_halo_plan(
+            self.sys._h, p.ne_loc, int(a), int(b), L.ptr(self.u_ghost), self.ncu,
+            self._xper // p.nf, len(peers), pr.ctypes.data_as(C.c_void_p), *ptrs),
+            "ldg_set_halo_plan")
+
+    def attach_native_comm(self, group=None):
+        """NCCL communicator inside the library (ldg_comm_init): rank 0's
+        unique id broadcast over the process group, then the halo plan."""
+        import ctypes as C
+        import torch.distributed as dist
+        from . import _lib as L
+        idb = (C.c_uint8 * 128)()
+        if self.plan.rank == 0:
+            L.check(self.sys.lib.ldg_comm_unique_id(idb), "ldg_comm_unique_id")
+        obj = [bytes(idb)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        L.check(self.sys.lib.ldg_comm_init(self.sys._h, self.plan.nranks, self.plan.rank, idb),
+                "ldg_comm_init")
+        self._native_plan()
+        self.native = True
+
+    def apply_native(self, u, tangent, t=0.0, out=None):
+        """The operator with both halo exchanges inside ldg_apply_dist (same
+        schedule as :meth:`apply`)."""
+        from . import _lib as L
+        p = self.plan
+        u = u.reshape(p.ne_loc, self.n_nodes, self.ncu)
+        if not u.is_contiguous():
+            u = u.contiguous()
+        R = out if out is not None else self.sys._empty((p.ne_loc, self.n_nodes, self.ncu))
+        g = None if tangent else self.sys.boundary_data(t)
+        b = None if tangent else self.sys.source_data(t)
+        L.check(self.sys.lib.ldg_apply_dist(self.sys._h, int(bool(tangent)), L.ptr(u), L.ptr(g),
+                                            L.ptr(b), L.ptr(self.X), L.ptr(R),
+                                            self.sys._stream()), "ldg_apply_dist")
+        return R
+
     def complete(self, u, tangent, t=0.0, R=None):
         """Pass 2 over all owned elements (after the caller's export halo)."""
         self._pass(2, u, tangent, t, R, 0, self.plan.ne_loc)
         return R
 
+    native = False          # True once attach_native_comm: halos inside ldg_apply_dist
+
     def residual_dev(self, u, t=0.0, out=None):
+        if self.native:
+            return self.apply_native(u, False, t, out)
         return self.apply(u, False, t, out)
 
     def tangent_dev(self, du, out=None, base=None, t=0.0):
         """Linear fused operator: the tangent reads neither base nor t."""
+        if self.native:
+            return self.apply_native(du, True, 0.0, out)
         return self.apply(du, True, 0.0, out)
+
+
+def link_native_local(parts):
+    """In-process transport of the native halos (ldg_comm_init_local): the
+    partitions' handles act as ranks 0..n-1 of one device; drive each
+    partition's apply_native from its own host thread."""
+    import ctypes as C
+    from . import _lib as L
+    hs = (C.c_void_p * len(parts))(*[p.sys._h.value for p in parts])
+    L.check(parts[0].sys.lib.ldg_comm_init_local(hs, len(parts)), "ldg_comm_init_local")
+    for p in parts:
+        p._native_plan()
 
 
 class LocalDenseTables:

@@ -311,3 +311,109 @@ def test_fused_equals_unfused_at_config3_size():
     q = s.mixed_dev(du, 0.0)
     Ru = s.flux_from_mixed_dev(du, q, False, 0.0)
     assert float(torch.linalg.norm(R - Ru) / torch.linalg.norm(Ru)) < TOL
+
+
+def _threaded(fns):
+    """Run callables concurrently, one host thread (and one CUDA stream)
+    each, like ranks; returns their results in order."""
+    import threading
+    import torch
+    out, err = [None] * len(fns), []
+
+    def run(i):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[i] = fns[i]()
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:          # surfaced below
+            err.append(e)
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(len(fns))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    assert not err, err
+    assert all(not t.is_alive() for t in ts), "a rank hung"
+    return out
+
+
+@pytest.mark.parametrize("name,nparts", [("poisson3d_hex_p3", 3), ("convdiff3d_hex_periodic_p2", 4),
+                                         ("poisson2d_quad_p3", 2)])
+def test_native_halos_in_process_match_reference(name, nparts):
+    """ldg_apply_dist (both halo exchanges inside the C call, the in-process
+    transport of ldg_comm_init_local standing in for NCCL on a one-GPU pool):
+    partitions driven from concurrent host threads assemble to the
+    reference operator, over repeated calls (the mailbox rounds)."""
+    import torch
+    from paper_2205_07824_b200.parallel import PartitionedLdgSystem, link_native_local
+    from paper_2205_07824_b200.tables import TensorTables
+    g = np.load(GOLDEN / f"{name}.npz")
+    parts_in = build_case(CASES[name], *b200_setup())
+    tab = TensorTables(*parts_in)
+    parts = [PartitionedLdgSystem(*parts_in, nranks=nparts, rank=r, tables=tab, exchanger=False)
+             for r in range(nparts)]
+    link_native_local(parts)
+    for _ in range(2):
+        for key, tangent, want in (("u", False, "R"), ("du", True, "Jdu")):
+            us = [torch.as_tensor(g[key][p.plan.e0:p.plan.e1], device="cuda").contiguous()
+                  for p in parts]
+            Rs = _threaded([lambda p=p, u=u: p.apply_native(u, tangent) for p, u in zip(parts, us)])
+            R = np.concatenate([r.cpu().numpy() for r in Rs])
+            assert rel(R, g[want]) < TOL, (key, rel(R, g[want]))
+
+
+@pytest.mark.parametrize("nparts", [2, 3])
+def test_native_halos_in_process_match_global_at_scale(nparts):
+    """hex p=3 n=8 (interior ranges overlap the halos): ldg_apply_dist on
+    2 / 3 in-process ranks vs the single-GPU operator, bit for bit up to the
+    summation order (1e-13)."""
+    import torch
+    from paper_2205_07824_b200.parallel import PartitionedLdgSystem, link_native_local
+    from paper_2205_07824_b200.system import LdgSystem
+    from paper_2205_07824_b200.tables import TensorTables
+    spec = dict(model=("file", "poisson3d.model"), kind="hex", counts=[8, 8, 8], p=3)
+    parts_in = build_case(spec, *b200_setup())
+    tab = TensorTables(*parts_in)
+    s = LdgSystem(*parts_in, tables=tab)
+    parts = [PartitionedLdgSystem(*parts_in, nranks=nparts, rank=r, tables=tab, exchanger=False)
+             for r in range(nparts)]
+    assert any(p.plan.interior[1] > p.plan.interior[0] for p in parts)
+    link_native_local(parts)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    u = torch.randn((s.n_elements, s.n_nodes, 1), dtype=torch.float64, device="cuda", generator=gen)
+    want = s.tangent_dev(u).cpu().numpy()
+    want_r = s.residual_dev(u).cpu().numpy()
+    for _ in range(3):
+        Rs = _threaded([lambda p=p: p.apply_native(u[p.plan.e0:p.plan.e1], True) for p in parts])
+        assert rel(np.concatenate([r.cpu().numpy() for r in Rs]), want) < 1e-13
+        Rs = _threaded([lambda p=p: p.apply_native(u[p.plan.e0:p.plan.e1], False) for p in parts])
+        assert rel(np.concatenate([r.cpu().numpy() for r in Rs]), want_r) < 1e-13
+
+
+def test_native_comm_nccl_single_rank():
+    """The NCCL transport end to end on a one-rank communicator: libnccl
+    dlopen'ed, unique id broadcast over torch.distributed, ncclCommInitRank,
+    the halo plan (no peers) and ldg_apply_dist equal the single-GPU
+    operator."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2205_07824_b200.parallel import PartitionedLdgSystem
+    from paper_2205_07824_b200.system import LdgSystem
+    from paper_2205_07824_b200.tables import TensorTables
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0)
+    try:
+        spec = dict(model=("file", "poisson3d.model"), kind="hex", counts=[4, 4, 4], p=3)
+        parts_in = build_case(spec, *b200_setup())
+        tab = TensorTables(*parts_in)
+        s = LdgSystem(*parts_in, tables=tab)
+        p = PartitionedLdgSystem(*parts_in, nranks=1, rank=0, tables=tab, exchanger=False)
+        p.attach_native_comm()
+        u = torch.randn((s.n_elements, s.n_nodes, 1), dtype=torch.float64, device="cuda")
+        assert rel(p.apply_native(u, True).cpu().numpy(), s.tangent_dev(u).cpu().numpy()) < 1e-13
+        assert rel(p.apply_native(u, False).cpu().numpy(), s.residual_dev(u).cpu().numpy()) < 1e-13
+    finally:
+        dist.destroy_process_group()
