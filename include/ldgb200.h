@@ -295,6 +295,12 @@ int ldg_bj_apply(int64_t nblk, int bs, const double* inv_t, const double* r,
  * rows of up to ldg_bj_tile_elems() elements tile_el[t * E .. t * E + E)
  * (-1 = unused slot) */
 int ldg_bj_tile_elems(void);
+/* class detection: keys[2b, 2b+1] = two exact 64-bit hashes of block b's bit
+ * pattern (wrapping sums, order-free); *bad = 1 unless every block is bit
+ * for bit equal to block rep[b] (bad: device int, set by the caller to 0) */
+int ldg_bj_block_keys(int64_t nblk, int bs, const double* mats, uint64_t* keys, void* stream);
+int ldg_bj_class_verify(int64_t nblk, int bs, const double* mats, const int64_t* rep, int32_t* bad,
+                        void* stream);
 int ldg_bj_apply_tiles(int64_t ntiles, int bs, const double* inv_t, const int32_t* tile_cls,
                        const int32_t* tile_el, const double* r, double* z, void* stream);
 /* element blocks across a packed (u | q | w) vector (driver.py:128-142,

@@ -107,6 +107,8 @@ _SIGS = {
     "ldg_color_distance2": ([C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
                             C.c_int),
     "ldg_bj_tile_elems": ([], C.c_int),
+    "ldg_bj_block_keys": ([C.c_int64, C.c_int] + [C.c_void_p] * 3, C.c_int),
+    "ldg_bj_class_verify": ([C.c_int64, C.c_int] + [C.c_void_p] * 4, C.c_int),
     "ldg_bj_apply_tiles": ([C.c_int64, C.c_int] + [C.c_void_p] * 6, C.c_int),
     "ldg_comm_unique_id": ([C.c_void_p], C.c_int),
     "ldg_comm_init": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),

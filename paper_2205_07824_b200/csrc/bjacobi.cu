@@ -304,6 +304,58 @@ bj_apply_big_kernel(int bs, const double* __restrict__ inv_t,
   }
 }
 
+// exact keys of the blocks' bit patterns (class detection): two wrapping
+// 64-bit sums of bits(M[t]) * odd(t), odd() a position hash, so identical
+// blocks give identical keys whatever the reduction order
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return (z ^ (z >> 31)) | 1ull;
+}
+
+__global__ void __launch_bounds__(256)
+block_hash_kernel(int bs, const double* __restrict__ mats, unsigned long long* __restrict__ keys) {
+  __shared__ unsigned long long s0[256], s1[256];
+  const int64_t b = blockIdx.x;
+  const int64_t n2 = (int64_t)bs * bs;
+  const unsigned long long* M = reinterpret_cast<const unsigned long long*>(mats + b * n2);
+  unsigned long long h0 = 0, h1 = 0;
+  for (int64_t t = threadIdx.x; t < n2; t += blockDim.x) {
+    const unsigned long long v = M[t];
+    h0 += v * mix64((uint64_t)t);
+    h1 += (v ^ (v >> 29)) * mix64((uint64_t)t + 0x1234567ull);
+  }
+  s0[threadIdx.x] = h0;
+  s1[threadIdx.x] = h1;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s0[threadIdx.x] += s0[threadIdx.x + o];
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    keys[2 * b] = s0[0];
+    keys[2 * b + 1] = s1[0];
+  }
+}
+
+// every block equal (bit for bit) to its class representative?  *bad = 1 if not
+__global__ void __launch_bounds__(256)
+class_verify_kernel(int bs, const double* __restrict__ mats, const int64_t* __restrict__ rep,
+                    int* __restrict__ bad) {
+  const int64_t b = blockIdx.x, r = rep[b];
+  if (r == b) return;
+  const int64_t n2 = (int64_t)bs * bs;
+  const unsigned long long* A = reinterpret_cast<const unsigned long long*>(mats + b * n2);
+  const unsigned long long* B = reinterpret_cast<const unsigned long long*>(mats + r * n2);
+  int diff = 0;
+  for (int64_t t = threadIdx.x; t < n2; t += blockDim.x) diff |= A[t] != B[t];
+  if (__syncthreads_or(diff) && threadIdx.x == 0) *bad = 1;
+}
+
 // class-shared blocks (structured meshes: interior elements of one geometry
 // class have bit-identical blocks): a tile = up to kTileE elements of one
 // class; thread i owns output row i and reuses each inverse entry
@@ -446,6 +498,24 @@ int ldg_permute_scatter(int64_t n, const int64_t* idx, const double* src, double
   if (n <= 0) return 0;
   if (!idx || !src || !dst) return 2;
   scatter_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, idx, src, dst);
+  return rc();
+}
+
+int ldg_bj_block_keys(int64_t nblk, int bs, const double* mats, uint64_t* keys, void* stream) {
+  NvtxRange nvtx_("ldg_bj_block_keys");
+  if (nblk <= 0) return 0;
+  if (bs < 1 || !mats || !keys) return 2;
+  block_hash_kernel<<<(unsigned)nblk, 256, 0, (cudaStream_t)stream>>>(
+      bs, mats, reinterpret_cast<unsigned long long*>(keys));
+  return rc();
+}
+
+int ldg_bj_class_verify(int64_t nblk, int bs, const double* mats, const int64_t* rep, int32_t* bad,
+                        void* stream) {
+  NvtxRange nvtx_("ldg_bj_class_verify");
+  if (nblk <= 0) return 0;
+  if (bs < 1 || !mats || !rep || !bad) return 2;
+  class_verify_kernel<<<(unsigned)nblk, 256, 0, (cudaStream_t)stream>>>(bs, mats, rep, bad);
   return rc();
 }
 

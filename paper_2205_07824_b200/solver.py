@@ -818,60 +818,68 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, per
 def class_tiles(classes, nclass, E):
     """Element tiles of one class each for ldg_bj_apply_tiles: (class per
     tile, E element ids per tile, -1 padded), elements in increasing order
-    within a class."""
+    within a class.  Host index arithmetic (numpy), uploaded once."""
     import torch
-    n = int(classes.numel())
-    order = torch.argsort(classes, stable=True)
-    cs = classes[order]
-    counts = torch.bincount(cs, minlength=nclass)
-    starts = torch.cumsum(counts, 0) - counts
+    dev = classes.device if isinstance(classes, torch.Tensor) else torch.device("cpu")
+    cls = classes.cpu().numpy() if isinstance(classes, torch.Tensor) else np.asarray(classes)
+    n = cls.size
+    order = np.argsort(cls, kind="stable")
+    cs = cls[order]
+    counts = np.bincount(cs, minlength=nclass)
+    starts = np.cumsum(counts) - counts
     ntile_c = (counts + E - 1) // E
-    tile_cls = torch.repeat_interleave(torch.arange(nclass, device=cs.device), ntile_c)
-    first = torch.cumsum(ntile_c, 0) - ntile_c                  # first tile of each class
-    pos = torch.arange(n, device=cs.device) - starts[cs]         # rank within the class
+    tile_cls = np.repeat(np.arange(nclass), ntile_c)
+    first = np.cumsum(ntile_c) - ntile_c                      # first tile of each class
+    pos = np.arange(n) - starts[cs]                           # rank within the class
     slot = (first[cs] + pos // E) * E + pos % E
-    tile_el = torch.full((int(ntile_c.sum()) * E,), -1, dtype=torch.int32, device=cs.device)
-    tile_el[slot] = order.to(torch.int32)
-    return tile_cls.to(torch.int32).contiguous(), tile_el
+    tile_el = np.full(int(ntile_c.sum()) * E, -1, dtype=np.int32)
+    tile_el[slot] = order
+    return (torch.as_tensor(tile_cls.astype(np.int32), device=dev),
+            torch.as_tensor(tile_el, device=dev))
 
 
 BJ_SHARE_MAX_FRACTION = 0.125   # share inverses when classes <= 1/8 of the blocks
 
 
-def _block_classes(mats, chunk=4096):
+def _block_classes(mats):
     """Classes of bit-identical blocks (structured meshes: every interior
     element of one geometry class probes to the same block, bit for bit):
-    an exact integer hash of the blocks' bit patterns, then every block is
-    compared with its class representative -- any mismatch (a hash
-    collision) and no sharing.  Returns (class per block, representative
-    block per class) or None when sharing would not pay."""
+    exact keys of the blocks' bit patterns (device: ldg_bj_block_keys, two
+    wrapping 64-bit sums; host: the bit rows themselves), grouped on the
+    host, then on the device every block is compared with its class
+    representative (ldg_bj_class_verify) -- any mismatch (a key collision)
+    and no sharing.  Returns (class per block, representative block per
+    class) as tensors on the blocks' device, or None when sharing would not
+    pay.  No torch sort / unique kernels: their first use costs a few
+    hundred ms of module loading in a fresh process."""
     import torch
     nblk = mats.shape[0]
     if nblk < 64:
         return None
     flat = mats.reshape(nblk, -1)
-    gen = torch.Generator(device="cpu").manual_seed(0x5eed)
-    w = torch.randint(1, 2 ** 62, (2, flat.shape[1]), generator=gen, dtype=torch.int64)
-    w = (w * 2 + 1).to(mats.device)                      # odd multipliers
-    keys = torch.empty((nblk, 2), dtype=torch.int64, device=mats.device)
-    for a in range(0, nblk, chunk):
-        bits = flat[a:a + chunk].view(torch.int64)
-        keys[a:a + chunk, 0] = (bits * w[0]).sum(dim=1)    # wraps mod 2^64: exact, order-free
-        keys[a:a + chunk, 1] = ((bits ^ (bits >> 31)) * w[1]).sum(dim=1)
-    uniq, cls = torch.unique(keys, dim=0, return_inverse=True)
-    nclass = uniq.shape[0]
-    if nclass > BJ_SHARE_MAX_FRACTION * nblk:
+    if mats.is_cuda:
+        lib = _lib.load()
+        keys = torch.empty((nblk, 2), dtype=torch.int64, device=mats.device)
+        _lib.check(lib.ldg_bj_block_keys(nblk, mats.shape[1], _lib.ptr(mats), _lib.ptr(keys),
+                                         _lib.stream_ptr()), "ldg_bj_block_keys")
+        kh = keys.cpu().numpy()
+    else:
+        kh = flat.numpy().view(np.int64)
+    rows = np.ascontiguousarray(kh).view(np.dtype((np.void, kh.shape[1] * 8))).ravel()
+    _, reps, cls = np.unique(rows, return_index=True, return_inverse=True)
+    cls = cls.reshape(-1)
+    if reps.size > BJ_SHARE_MAX_FRACTION * nblk:
         return None
-    reps = torch.full((nclass,), nblk, dtype=torch.int64, device=mats.device)
-    reps.scatter_reduce_(0, cls, torch.arange(nblk, device=mats.device), reduce="amin")
-    for a in range(0, nblk, chunk):
-        c = cls[a:a + chunk]
-        if not bool((flat[a:a + chunk] == flat[reps[c]]).all()):
+    if mats.is_cuda:
+        rep_of = torch.as_tensor(reps[cls].astype(np.int64), device=mats.device)
+        bad = torch.zeros(1, dtype=torch.int32, device=mats.device)
+        _lib.check(lib.ldg_bj_class_verify(nblk, mats.shape[1], _lib.ptr(mats), _lib.ptr(rep_of),
+                                           _lib.ptr(bad), _lib.stream_ptr()), "ldg_bj_class_verify")
+        if int(bad.item()):
             return None
-    return cls, reps
-
-
-BJ_SMEM_MAX_BS = 160            # ldg_bj_invert's in-shared-memory limit (bjacobi.cu)
+    dev = mats.device
+    return (torch.as_tensor(cls.astype(np.int64), device=dev),
+            torch.as_tensor(reps.astype(np.int64), device=dev))
 
 
 # ---------------------------------------------------------------------------

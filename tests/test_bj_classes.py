@@ -13,7 +13,7 @@ def test_block_classes_groups_bit_identical_blocks():
     proto = rng.normal(size=(5, 6, 6))
     which = rng.integers(0, 5, size=400)
     mats = torch.as_tensor(proto[which].copy())
-    cls, reps = _block_classes(mats, chunk=64)
+    cls, reps = _block_classes(mats)
     assert reps.numel() == 5
     assert torch.equal(mats[reps[cls]], mats)
     # same class <=> same prototype
