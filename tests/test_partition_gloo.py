@@ -121,7 +121,7 @@ def _worker(rank, world, port, name, q, orth):
         # distributed Newton-GMRES on the partitioned operator
         from paper_2205_07824_b200.solver import NewtonOptions, newton_solve
         ops = DistVecOps(CpuOps())
-        opts = NewtonOptions(abs_tol=1e-11, rel_tol=3e-8, forcing=1e-10, gmres_restart=400,
+        opts = NewtonOptions(abs_tol=1e-13, rel_tol=1e-11, forcing=1e-12, gmres_restart=400,
                              gmres_max_iter=2000, jv_mode="tangent", orth=orth)
         x, st = newton_solve(lambda v: apply(v, False), torch.zeros(plan.ne_loc * nb * ncu,
                                                                     dtype=torch.float64),
@@ -167,7 +167,7 @@ def test_partitioned_operator_and_solve_gloo(name, orth):
         return torch.as_tensor(emu.fused(tab, u, tangent, None if tangent else gp,
                                          None if tangent else bs)).reshape(-1)
 
-    opts = NewtonOptions(abs_tol=1e-11, rel_tol=3e-8, forcing=1e-10, gmres_restart=400,
+    opts = NewtonOptions(abs_tol=1e-13, rel_tol=1e-11, forcing=1e-12, gmres_restart=400,
                          gmres_max_iter=2000, jv_mode="tangent", orth=orth)
     x, st = newton_solve(lambda v: apply(v, False), torch.zeros(int(np.prod(shape)),
                                                                  dtype=torch.float64),
