@@ -471,6 +471,8 @@ def run_b200(args, rank, world):
     dq = torch.empty((ne, nb, 1, 3), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
     lib, h = core.lib, core._h
+    if args.fused is not None:
+        L.check(lib.ldg_set_option(h, b"fused", int(args.fused)), "fused option")
 
     def step():
         if world == 1:
@@ -694,6 +696,8 @@ def main():
     ap.add_argument("--elems", dest="n", type=int, default=N_ELEM,
                     help="hexes per direction per rank (default 54 -> 10,077,696 DOFs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused", type=int, default=None,
+                    help="A/B: 1 / 0 forces the one-launch operator on / off (ldg_set_option 'fused')")
     ap.add_argument("--no-tet", action="store_true",
                     help="skip the config-3 tet variant (44^3 Kuhn tets, dense kernels)")
     ap.add_argument("--no-solve", action="store_true",

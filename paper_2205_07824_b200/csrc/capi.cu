@@ -53,6 +53,8 @@ struct LdgHandle {
   int kstride = 0;
   int c_diag = 0;
   unsigned long long* bad = nullptr;
+  int* fuse = nullptr;           // one-launch operator: counters and per-group windows
+  int2* fuse_dep = nullptr;
   // host-pipeline resources (ldg_apply_host): copy streams, chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_p2;
@@ -251,6 +253,47 @@ int ldg_create(const LdgTables* t, LdgHandle** out) {
     }
     for (int k = 0; k < nch; ++k) P.chunk_dep[k] = dep[k];
   }
+  P.fused = 0;
+  P.fuse = nullptr;
+  P.fuse_dep = nullptr;
+  P.fuse_nwin = 0;
+  if (t->nd == 3 && t->n1 == 4 && t->ncu == 1 && t->ne > 0) {
+    // one-launch operator: for each 8-element group the range of 32-group
+    // windows whose pass 1 its pass 2 reads (its own R rows, the exports of
+    // the neighbours across its completion faces)
+    const int ne = t->ne, ng = (ne + 7) / 8, nwin = (ng + 31) / 32;
+    std::vector<int2> gdep(ng);
+    for (int g = 0; g < ng; ++g) {
+      int lo = g >> 5, hi = g >> 5;
+      for (int e = 8 * g; e < std::min(ne, 8 * g + 8); ++e)
+        for (int lf = 0; lf < 6; ++lf) {
+          int32_t pair[2];
+          memcpy(pair, &h_rec_host[(size_t)(e * 6 + lf) * 2 + 1], sizeof(pair));
+          if ((pair[1] & LDG_FACE_KIND_MASK) != LDG_FACE_INTERIOR || !(pair[1] & LDG_FL_COMPLETE)) continue;
+          const int w = (pair[0] / 8) >> 5;
+          lo = std::min(lo, w);
+          hi = std::max(hi, w);
+        }
+      gdep[g] = make_int2(lo, hi);
+    }
+    int* ctr = nullptr;
+    int2* d = nullptr;
+    if (cudaMalloc(&ctr, (3 + nwin) * sizeof(int)) == cudaSuccess &&
+        cudaMalloc(&d, ng * sizeof(int2)) == cudaSuccess &&
+        cudaMemset(ctr, 0, (3 + nwin) * sizeof(int)) == cudaSuccess &&
+        cudaMemcpy(d, gdep.data(), ng * sizeof(int2), cudaMemcpyHostToDevice) == cudaSuccess) {
+      h->fuse = ctr;
+      h->fuse_dep = d;
+      P.fuse = ctr;
+      P.fuse_dep = d;
+      P.fuse_nwin = nwin;
+      P.fused = LDG_FUSED_DEFAULT;
+    } else {
+      cudaFree(ctr);
+      cudaFree(d);
+      cudaGetLastError();
+    }
+  }
   const int n1 = t->n1;
   // tables arrive with row stride n1 packed at the front of each array
   memcpy(P.d1, t->d1, sizeof(P.d1));
@@ -311,6 +354,7 @@ int ldg_destroy(LdgHandle* h) {
   for (void* p : h->dense_bufs) cudaFree(p);
   cudaFree(h->geo); cudaFree(h->fnbr); cudaFree(h->finfo); cudaFree(h->ftau);
   cudaFree(h->nmap); cudaFree(h->frec); cudaFree(h->kco); cudaFree(h->bad);
+  cudaFree(h->fuse); cudaFree(h->fuse_dep);
   for (auto e : h->ev_in) cudaEventDestroy(e);
   for (auto e : h->ev_p2) cudaEventDestroy(e);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
@@ -426,6 +470,7 @@ int ldg_set_option(LdgHandle* h, const char* name, int value) {
   if (h->dense) return fail(2, "options apply to tensor handles");
   if (!strcmp(name, "pass1_variant")) h->P.variant = value ? 1 : 0;
   else if (!strcmp(name, "c_diag")) h->P.c_diag = (value && h->c_diag) ? 1 : 0;
+  else if (!strcmp(name, "fused")) h->P.fused = (value && h->P.fuse) ? 1 : 0;
   else if (!strcmp(name, "p2_mode")) {
     if (value < 0 || value > 3) return fail(2, "p2_mode is 0..3");
     h->P.p2_mode = value;

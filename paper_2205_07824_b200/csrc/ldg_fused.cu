@@ -24,6 +24,7 @@
 // for hex, i with the j column for quads) = one thread per face node.
 
 #include <algorithm>
+#include <climits>
 #include "ldg_tensor.cuh"
 
 namespace ldg {
@@ -714,11 +715,87 @@ __device__ __forceinline__ void dmma_zplane(double& d0, double& d1, double a, do
       : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
+// Pass 2 of one 8-element group inside the one-launch operator: the
+// arithmetic of complete_warp4_kernel (half a warp per element, lane t = i + 4j
+// owns R column (i, j) and face node t), four element pairs with all their
+// loads issued together.  R rows and exports were written by other SMs earlier
+// in the same launch: read through L2 (__ldcg), never the read-only path.
+__device__ __forceinline__ void complete_group4(const TensorParams& P, const FaceRec* __restrict__ frec,
+                                                const double* X, double* R, int e_w, int lane,
+                                                const double* sM) {
+  constexpr int NB = 64, NF = 16;
+  const int half = lane >> 4, t = lane & 15, i = t & 3, j = t >> 2, hb = half * 16;
+  const double wgt = P.grad_centered ? -0.5 : -1.0;
+  int info[4];
+  double r[4][4], x[4][6];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int e = e_w + 2 * p + half;
+    info[p] = (e < P.e1 && t < 6) ? __ldg(reinterpret_cast<const int*>(frec + (size_t)e * 6 + t) + 3) : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r[p][k] = e < P.e1 ? __ldcg(R + (size_t)e * NB + t + 16 * k) : 0.0;
+  }
+  unsigned any[4];
+  int mask[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const unsigned bal = __ballot_sync(0xffffffffu, (info[p] & LDG_FL_COMPLETE) != 0);
+    any[p] = (bal | (bal >> 16)) & 63;
+    mask[p] = (bal >> hb) & 63;
+    const int e = e_w + 2 * p + half;
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf)
+      x[p][lf] = (mask[p] >> lf) & 1 ? __ldcg(X + ((size_t)e * 6 + lf) * NF + t) : 0.0;
+  }
+  double Mi[4], Mj[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    Mi[m] = sM[i * 4 + m];
+    Mj[m] = sM[j * 4 + m];
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int e = e_w + 2 * p + half;
+#pragma unroll
+    for (int lf = 0; lf < 6; ++lf) {
+      if (!((any[p] >> lf) & 1)) continue;                  // warp-uniform
+      const double v = wgt * x[p][lf];
+      double wv = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) wv = fma(Mi[a], __shfl_sync(0xffffffffu, v, hb + a + 4 * j), wv);
+      double L = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) L = fma(Mj[b], __shfl_sync(0xffffffffu, wv, hb + i + 4 * b), L);
+      if (!((mask[p] >> lf) & 1)) L = 0.0;
+      if (lf == 0) r[p][0] += L;
+      else if (lf == 1) r[p][3] += L;
+      else {
+        const bool own = lf == 2 ? j == 0 : (lf == 3 ? j == 3 : (lf == 4 ? i == 0 : i == 3));
+        const int a0 = lf < 4 ? i : j;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double gg = __shfl_sync(0xffffffffu, L, hb + a0 + 4 * k);
+          if (own) r[p][k] += gg;
+        }
+      }
+    }
+    if (e < P.e1) {
+      int hm = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        hm = max(hm, hi_abs(r[p][k]));
+        R[(size_t)e * NB + t + 16 * k] = r[p][k];
+      }
+      bad_if_any(P, e, hm);
+    }
+  }
+}
+
 #ifndef LDG_PLANE_MINB
 #define LDG_PLANE_MINB 2          // 2 persistent blocks per SM (shared-memory bound)
 #endif
 
-template <bool TANGENT, bool HAS_CU, bool DIAG>
+template <bool TANGENT, bool HAS_CU, bool DIAG, bool FUSED>
 __global__ void __launch_bounds__(kPlaneBlock, LDG_PLANE_MINB)
 plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
              const double* __restrict__ u, const double* __restrict__ gproj,
@@ -770,7 +847,54 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   const int nel = P.e1 - P.e0;
   const int ngroups = (nel + 7) >> 3;
   const int stride = gridDim.x * (kPlaneBlock / 32);
-  int g = blockIdx.x * (kPlaneBlock / 32) + warp;
+  // FUSED: pass-1 groups are claimed in order from a device counter (every
+  // claimed group is finished by a running warp, so a warp waiting for pass-1
+  // windows never waits on a block that is not resident)
+  // lane 0 issues the claim; the value is broadcast only where it is used, so
+  // the atomic's latency hides behind a group's work
+  auto claim_raw = [&](int which) {
+    int v = 0;
+    if (FUSED && lane == 0) v = atomicAdd(P.fuse + which, 1);
+    return v;
+  };
+  auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
+  int g = FUSED ? bcast(claim_raw(0)) : blockIdx.x * (kPlaneBlock / 32) + warp;
+  int g_pend = claim_raw(0);                               // FUSED: the group after next
+  // FUSED pass 2, one step per pass-1 group so no load waits in line: a warp
+  // claims a group (stage 1), reads its window range (stage 2), then checks
+  // the windows each step and completes the group once every 32-group window
+  // of pass 1 it reads has been published, so its R rows and exports are
+  // re-read from L2; draining waits only after pass 1 is exhausted
+  int p2_stage = FUSED ? 1 : 0, p2_raw = claim_raw(1), p2_mine = -1;
+  int2 p2_dep = make_int2(0, -1);
+  auto fused_p2 = [&](bool wait) {
+    if constexpr (FUSED) {
+      if (p2_stage == 1) {
+        p2_mine = bcast(p2_raw);
+        if (p2_mine >= ngroups) { p2_stage = 0; return; }
+        p2_dep = __ldg(P.fuse_dep + p2_mine);
+        p2_stage = 2;
+        if (!wait) return;
+      }
+      if (p2_stage != 2) return;
+      for (long spin = 0;; ++spin) {
+        bool ok = true;
+        for (int w = min(p2_dep.x + lane, p2_dep.y); w <= p2_dep.y; w += 32) {
+          int c;
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(c) : "l"(P.fuse + 3 + w) : "memory");
+          ok &= c >= min(32, ngroups - 32 * w);
+        }
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (!wait) return;
+        if (spin > (1l << 26)) __trap();               // never: every claimed group completes
+        __nanosleep(128);
+      }
+      __syncwarp();                                  // every lane's acquire precedes the reads
+      complete_group4(P, frec, X, R, P.e0 + 8 * p2_mine, lane, s_tab + 2 * NP);
+      p2_raw = claim_raw(1);
+      p2_stage = 1;
+    }
+  };
 
   // prefetch of one group of 8 elements into input buffer `buf`: u rows
   // (coalesced 8 B copies into the padded planes), the coefficient blocks and
@@ -805,9 +929,11 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
   };
 
   prefetch(g, 0);
-  for (int it = 0; g < ngroups; g += stride, ++it) {
+  for (int it = 0; g < ngroups; ++it) {
     const int cur = it & 1;
-    prefetch(g + stride, cur ^ 1);
+    const int gnext = FUSED ? bcast(g_pend) : g + stride;
+    prefetch(gnext, cur ^ 1);
+    if (FUSED) g_pend = claim_raw(0);
     cp_async_wait_group1();                                // this group's data landed
     __syncwarp();
     const int e = P.e0 + g * 8 + ls;
@@ -1247,6 +1373,523 @@ plane_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
     }
   }
   __syncwarp();                                  // this buffer is refilled two groups on
+  if constexpr (FUSED) {
+    // publish this group (its R rows and exports) and complete one pass-2
+    // group whose windows are done, if this warp holds one
+    __syncwarp();                                   // the warp's R / export stores precede
+    if (lane == 0)                                  // lane 0's release (cumulativity)
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" :: "l"(P.fuse + 3 + (g >> 5)) : "memory");
+    fused_p2(false);
+  }
+  g = gnext;
+  }
+  if constexpr (FUSED) {
+    while (p2_stage != 0) fused_p2(true);
+    // the last warp out resets the counters for the next launch
+    int last = 0;
+    if (lane == 0) last = atomicAdd(P.fuse + 2, 1) == (int)gridDim.x * (kPlaneBlock / 32) - 1;
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      for (int x = lane; x < 3 + P.fuse_nwin; x += 32) P.fuse[x] = 0;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// pass 1, plane mapping for hex p = 1, 2 (N1 = 2, 3; ncu = 1): config 5
+// --------------------------------------------------------------------------
+//
+// The same stages and arithmetic as plane_kernel, with N1 threads per element
+// (thread k owns z-plane k, N1^2 nodes in registers) and 32 / N1 elements per
+// warp (N1 = 3: 10 elements on lanes 0..29; lanes 30, 31 run a dummy slot with
+// no global side effects so every __syncwarp is reached).  At these orders the
+// pencil kernel (one thread per face node) spends most of its time on
+// shared-memory transposes of tiny pencils and per-element setup; here the
+// x / y work and the flux combination stay in registers and only the u, F_z
+// and W planes are exchanged, as at p = 3.  The thread-private x / y face
+// fluxes get their own slot (4 N1 doubles do not fit a u plane below N1 = 4).
+
+namespace {
+template <int N1>
+struct PlaneG {
+  static constexpr int NP = N1 * N1, NB = N1 * N1 * N1;
+  // plane / z-face row strides: N1 = 3 takes 11 / 3 (a bank-conflict model
+  // of the kernel's shared accesses, scripts/plane_banks.py: 17% fewer
+  // wavefronts than 10 / 4); N1 = 2 keeps 5 / 3
+  static constexpr int PS = N1 == 3 ? NP + 2 : NP + 1;
+  static constexpr int ES = N1 == 3 ? N1 : N1 + 1;
+  static constexpr int XS = 4 * N1 + 1;             // x / y face-flux slot stride
+  static constexpr int EPW = 32 / N1;               // elements per warp
+  static constexpr int NSLOT = EPW + ((32 % N1) ? 1 : 0);
+  static constexpr int InC = N1 * PS + ((N1 * PS) & 1);   // coefficient block (16-B aligned)
+  static constexpr int InF = InC + 16;              // six 16-B face records
+  static constexpr int InSz = InF + 12;             // one input buffer
+  static constexpr int OffJ = 2 * InSz;             // z-face jumps [face][row j][i]
+  static constexpr int OffF = OffJ + 2 * N1 * ES;   // z-face fluxes
+  static constexpr int OffE = OffF + 2 * N1 * ES;   // F_z planes
+  static constexpr int OffXY = OffE + N1 * PS;      // x / y face fluxes per thread
+  static constexpr int Raw = OffXY + N1 * XS;
+  static constexpr int PER = Raw + (20 - Raw % 16) % 16;   // element stride = 4 (mod 16)
+  static constexpr int WPB = N1 == 2 ? 4 : 2;       // warps per block
+  static constexpr int MINB = N1 == 2 ? 3 : 5;      // blocks per SM (shared-memory bound)
+  __host__ __device__ static constexpr int el(int e) { return e * PER + (e >> 2) * 2; }
+  static constexpr int WARP = el(NSLOT);            // doubles per warp region
+  static_assert(PER % 16 == 4 && InSz % 2 == 0, "layout");
+};
+
+// acc[n] += c * plane[n] for a plane at an offset of OFF doubles from a 16-B
+// boundary: 16-B loads wherever the pair is aligned
+template <int NP, int OFF>
+__device__ __forceinline__ void axpy_g(double (&acc)[NP], double c, const double* plane) {
+  constexpr int H = OFF & 1;
+  if constexpr (H) acc[0] = fma(c, plane[0], acc[0]);
+#pragma unroll
+  for (int j = 0; j < (NP - H) / 2; ++j) {
+    const double2 v = reinterpret_cast<const double2*>(plane + H)[j];
+    acc[H + 2 * j] = fma(c, v.x, acc[H + 2 * j]);
+    acc[H + 2 * j + 1] = fma(c, v.y, acc[H + 2 * j + 1]);
+  }
+  if constexpr (((NP - H) & 1) != 0) acc[NP - 1] = fma(c, plane[NP - 1], acc[NP - 1]);
+}
+
+// acc += sum_m sgn coef[m] plane_m over the N1 planes at base + m PS
+template <int N1, int PS, int M = 0>
+__device__ __forceinline__ void axpy_planes(double (&acc)[N1 * N1], const double* coef, double sgn,
+                                            const double* base) {
+  if constexpr (M < N1) {
+    axpy_g<N1 * N1, M * PS>(acc, sgn * coef[M], base + M * PS);
+    axpy_planes<N1, PS, M + 1>(acc, coef, sgn, base);
+  }
+}
+}  // namespace
+
+template <int N1, bool TANGENT, bool HAS_CU, bool DIAG>
+__global__ void __launch_bounds__(PlaneG<N1>::WPB * 32, PlaneG<N1>::MINB)
+plane_kernel_g(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+               const double* __restrict__ u, const double* __restrict__ gproj,
+               const double* __restrict__ bsrc, double* __restrict__ R,
+               double* __restrict__ X) {
+  using G = PlaneG<N1>;
+  constexpr int NP = G::NP, NB = G::NB, PS = G::PS, ES = G::ES, EPW = G::EPW;
+  constexpr int LO = 0, HI = N1 - 1;
+  extern __shared__ __align__(16) double psm[];
+  __shared__ int s_map[kPlaneMaps * NP];
+  __shared__ double s_tab[4 * NP + 2 * N1];        // G, M^-1, M, D, clo, chi
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ls = lane / N1, k = lane % N1;          // element slot (EPW: dummy), plane
+  const bool map_smem = P.n_maps <= kPlaneMaps;
+  if (map_smem)
+    for (int x = threadIdx.x; x < P.n_maps * NP; x += blockDim.x) s_map[x] = __ldg(P.nmap + x);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int x = 0; x < NP; ++x) {
+      s_tab[x] = P.g1[x];
+      s_tab[NP + x] = P.m1inv[x];
+      s_tab[2 * NP + x] = P.m1[x];
+      s_tab[3 * NP + x] = P.d1[x];
+    }
+#pragma unroll
+    for (int x = 0; x < N1; ++x) {
+      s_tab[4 * NP + x] = P.clo[x];
+      s_tab[4 * NP + N1 + x] = P.chi[x];
+    }
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  double* sWarp = psm + warp * G::WARP;
+  double* sEl = sWarp + G::el(ls);
+  double* sJZ = sEl + G::OffJ;
+  double* sFZ = sEl + G::OffF;
+  double* sT2 = sEl + G::OffE;
+  double* sXY = sEl + G::OffXY + k * G::XS;         // this thread's x / y face fluxes
+  const int nel = P.e1 - P.e0;
+  const int ngroups = (nel + EPW - 1) / EPW;
+  const int stride = gridDim.x * G::WPB;
+  int g = blockIdx.x * G::WPB + warp;
+
+  auto prefetch = [&](int gg, int buf) {
+    if (gg < ngroups) {
+      const int e_w = P.e0 + gg * EPW;
+      const int ne_w = min(EPW, P.e1 - e_w);
+      const double* ub = u + (size_t)e_w * NB;
+      double* dst = sWarp + buf * G::InSz;
+#pragma unroll
+      for (int x = 0; x < (EPW * NB + 31) / 32; ++x) {
+        const int d = lane + 32 * x;
+        if (d < ne_w * NB) cp_async8(dst + G::el(d / NB) + ((d / NP) % N1) * PS + d % NP, ub + d);
+      }
+      const double* kb = P.kco + (size_t)e_w * P.kstride;
+#pragma unroll
+      for (int x = 0; x < (EPW * 8 + 31) / 32; ++x) {
+        const int c = lane + 32 * x, el = c >> 3, part = c & 7;
+        if (el < ne_w && 2 * part < P.kstride)
+          cp_async16(dst + G::el(el) + G::InC + 2 * part, kb + (size_t)el * P.kstride + 2 * part);
+      }
+      const double* fb = reinterpret_cast<const double*>(frec + (size_t)e_w * 6);
+#pragma unroll
+      for (int x = 0; x < (EPW * 6 + 31) / 32; ++x) {
+        const int c = lane + 32 * x, el = c / 6, part = c % 6;
+        if (el < ne_w) cp_async16(dst + G::el(el) + G::InF + 2 * part, fb + 2 * c);
+      }
+    }
+    cp_async_commit();
+  };
+
+  prefetch(g, 0);
+  for (int it = 0; g < ngroups; g += stride, ++it) {
+    const int cur = it & 1;
+    prefetch(g + stride, cur ^ 1);
+    cp_async_wait_group1();
+    __syncwarp();
+    const int e = P.e0 + g * EPW + ls;
+    const int e_w = P.e0 + g * EPW;
+    const bool active = ls < EPW && e < P.e1;
+    double* sIn = sEl + cur * G::InSz;
+    double* sU = sIn;
+    double* sC = sIn + G::InC;
+    double* sW = sWarp + cur * G::InSz;
+
+    // ---- A: records and gathers (face node of this thread's N1 values:
+    // x faces (j, k) -> j + N1 k, y faces (i, k) -> i + N1 k, z faces row j = k)
+    double tau[6];
+    int info[6], nbr[6];
+    double ext[6][N1];
+    if (active) {
+#pragma unroll
+      for (int lf = 0; lf < 6; ++lf) {
+        const double* r = sIn + G::InF + 2 * lf;
+        tau[lf] = r[0];
+        const int2 w = *reinterpret_cast<const int2*>(r + 1);
+        nbr[lf] = w.x;
+        info[lf] = w.y;
+      }
+#pragma unroll
+      for (int lf = 0; lf < 6; ++lf) {
+        const int kind = info[lf] & LDG_FACE_KIND_MASK;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) ext[lf][a] = 0.0;
+        if (kind == LDG_FACE_INTERIOR) {
+          if (info[lf] & LDG_FL_UNBR) {
+            const int mid = (info[lf] >> LDG_FACE_MAP_SHIFT) & 0xffff;
+            const double* base = nbr_row(P, u, nbr[lf], NB);
+#pragma unroll
+            for (int a = 0; a < N1; ++a) {
+              const int t = a + N1 * k;
+              ext[lf][a] = __ldg(base + (map_smem ? s_map[mid * NP + t] : __ldg(P.nmap + mid * NP + t)));
+            }
+          }
+        } else if (!TANGENT && gproj) {
+#pragma unroll
+          for (int a = 0; a < N1; ++a) ext[lf][a] = __ldg(gproj + (size_t)nbr[lf] * NP + N1 * k + a);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int lf = 0; lf < 6; ++lf) {
+        tau[lf] = 0.0;
+        info[lf] = LDG_FACE_NEUMANN;
+        nbr[lf] = 0;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) ext[lf][a] = 0.0;
+      }
+    }
+
+    // ---- B: d/dz from all planes; z-face jumps / own-data flux, row j = k
+    double up[NP], hz[NP];
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+      up[n] = sU[k * PS + n];
+      hz[n] = 0.0;
+    }
+    axpy_planes<N1, PS>(hz, s_tab + 3 * NP + N1 * k, 1.0, sU);
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {                   // faces 0 (z-, plane 0), 1 (z+, plane N1-1)
+      const int kind = info[f] & LDG_FACE_KIND_MASK;
+      const int acode = (info[f] >> LDG_FL_ALPHA_SHIFT) & 3;
+      const double alpha = acode == 1 ? 1.0 : (acode == 2 ? 0.5 : 0.0);
+      const bool neu = kind == LDG_FACE_NEUMANN;
+      const double sgn = f ? 1.0 : -1.0;
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        const double uo = sU[(f ? HI : LO) * PS + i + N1 * k];
+        const double ex = ext[f][i];
+        const double d = uo - ex;
+        const double jmp = alpha * d;
+        double fh = tau[f] * (neu ? ex : d);
+        if (HAS_CU && !neu) fh = fma(sgn * sC[11], uo - jmp, fh);
+        sJZ[f * N1 * ES + k * ES + i] = jmp;
+        sFZ[f * N1 * ES + k * ES + i] = fh;
+      }
+    }
+    __syncwarp();
+    {
+      const double clk = s_tab[4 * NP + k], chk = s_tab[4 * NP + N1 + k];
+      const double c2 = DIAG ? sC[8] : 1.0;
+#pragma unroll
+      for (int n = 0; n < NP; ++n)
+        sT2[k * PS + n] = c2 * (-hz[n] - clk * sJZ[(n / N1) * ES + n % N1] +
+                                chk * sJZ[N1 * ES + (n / N1) * ES + n % N1]);
+    }
+    // ---- C: x / y faces at this plane and the in-plane gradients
+    double h[2][NP];
+    double alx[2], aly[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+#pragma unroll
+      for (int ax = 0; ax < 2; ++ax) {
+        const int lf = ax == 0 ? 4 + s : 2 + s;
+        const int kind = info[lf] & LDG_FACE_KIND_MASK;
+        const int acode = (info[lf] >> LDG_FL_ALPHA_SHIFT) & 3;
+        const double alpha = acode == 1 ? 1.0 : (acode == 2 ? 0.5 : 0.0);
+        if (ax == 0) alx[s] = alpha;
+        else aly[s] = alpha;
+        const bool neu = kind == LDG_FACE_NEUMANN;
+        const double sgn = s ? 1.0 : -1.0;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
+          const double uo = ax == 0 ? up[(s ? HI : LO) + N1 * a] : up[a + N1 * (s ? HI : LO)];
+          const double ex = ext[lf][a];
+          const double d = uo - ex;
+          double fh = tau[lf] * (neu ? ex : d);
+          if (HAS_CU && !neu) fh = fma(sgn * sC[9 + ax], uo - alpha * d, fh);
+          sXY[(s * 2 + ax) * N1 + a] = fh;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {
+      const double jxl = alx[0] * (up[N1 * j] - ext[4][j]);
+      const double jxh = alx[1] * (up[HI + N1 * j] - ext[5][j]);
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double vx = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) vx = fma(P.d1[i * N1 + m], up[m + N1 * j], vx);
+        h[0][i + N1 * j] = -vx - P.clo[i] * jxl + P.chi[i] * jxh;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      const double jyl = aly[0] * (up[i] - ext[2][i]);
+      const double jyh = aly[1] * (up[i + N1 * HI] - ext[3][i]);
+#pragma unroll
+      for (int j = 0; j < N1; ++j) {
+        double vy = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) vy = fma(P.d1[j * N1 + m], up[i + N1 * m], vy);
+        h[1][i + N1 * j] = -vy - P.clo[j] * jyl + P.chi[j] * jyh;
+      }
+    }
+
+    // ---- D: flux density F^q = C h, face exports and the own q^ share
+    double* fz = sT2 + k * PS;
+    if (DIAG) {
+      const double c0 = sC[0], c1 = sC[4];
+#pragma unroll
+      for (int n = 0; n < NP; ++n) {
+        h[0][n] *= c0;
+        h[1][n] *= c1;
+      }
+    } else {
+      __syncwarp();
+#pragma unroll
+      for (int n = 0; n < NP; ++n) {
+        const double h0 = h[0][n], h1 = h[1][n], h2 = fz[n];
+        h[0][n] = fma(sC[0], h0, fma(sC[1], h1, sC[2] * h2));
+        h[1][n] = fma(sC[3], h0, fma(sC[4], h1, sC[5] * h2));
+        fz[n] = fma(sC[6], h0, fma(sC[7], h1, sC[8] * h2));
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int ax = 0; ax < 2; ++ax) {
+        const int lf = ax == 0 ? 4 + s : 2 + s;
+        const int kind = info[lf] & LDG_FACE_KIND_MASK;
+        if (kind == LDG_FACE_NEUMANN) continue;
+        const bool exp_ = (info[lf] & LDG_FL_EXPORT) && active;
+        const double w_own = kind != LDG_FACE_INTERIOR ? 1.0
+                             : ((info[lf] & LDG_FL_QOWN) ? 1.0 : ((info[lf] & LDG_FL_QHALF) ? 0.5 : 0.0));
+        const double sgn = s ? 1.0 : -1.0;
+        double xv[N1];
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
+          const int n = ax == 0 ? (s ? HI : LO) + N1 * a : a + N1 * (s ? HI : LO);
+          xv[a] = sgn * h[ax][n];
+          sXY[(s * 2 + ax) * N1 + a] = fma(w_own, xv[a], sXY[(s * 2 + ax) * N1 + a]);
+        }
+        if (exp_) {
+          const int inf = info[lf];
+          if (P.x_consumer) {                        // the neighbour's slot, in its face-node order
+            const int nlf = (inf >> 4) & 7;
+            double* xb = X + ((size_t)nbr[lf] * 6 + nlf) * NP;
+            if ((unsigned)inf & LDG_FL_XIDENT) {
+#pragma unroll
+              for (int a = 0; a < N1; ++a) xb[a + N1 * k] = xv[a];
+            } else {
+              const int mid = (inf >> LDG_FACE_MAP_SHIFT) & 0xffff;
+              const int nax = face_axis(3, nlf);
+#pragma unroll
+              for (int a = 0; a < N1; ++a) {
+                const int t = a + N1 * k;
+                const int nv = map_smem ? s_map[mid * NP + t] : __ldg(P.nmap + mid * NP + t);
+                xb[vol_to_face<N1, 3>(nax, nv)] = xv[a];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int a = 0; a < N1; ++a) X[((size_t)e * 6 + lf) * NP + a + N1 * k] = xv[a];
+          }
+        }
+      }
+    // z faces: thread k takes column i = k of the plane-0 / plane-(N1-1) F_z rows
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int inf = info[f];
+      const int kind = inf & LDG_FACE_KIND_MASK;
+      if (kind == LDG_FACE_NEUMANN) continue;
+      const bool exp_ = (inf & LDG_FL_EXPORT) && active;
+      const double w_own = kind != LDG_FACE_INTERIOR ? 1.0
+                           : ((inf & LDG_FL_QOWN) ? 1.0 : ((inf & LDG_FL_QHALF) ? 0.5 : 0.0));
+      const double sgn = f ? 1.0 : -1.0;
+      const double* fzp = sT2 + (f ? HI : LO) * PS + k;
+      double xv[N1];
+#pragma unroll
+      for (int j = 0; j < N1; ++j) {                // face node (i = k, j)
+        xv[j] = sgn * fzp[N1 * j];
+        double* z0 = sFZ + f * N1 * ES + j * ES + k;
+        *z0 = fma(w_own, xv[j], *z0);
+      }
+      if (exp_) {
+        double* xb = X + ((size_t)e * 6 + f) * NP;
+        bool mapped = false;
+        int mid = 0, nax = 0;
+        if (P.x_consumer) {
+          const int nlf = (inf >> 4) & 7;
+          xb = X + ((size_t)nbr[f] * 6 + nlf) * NP;
+          if (!((unsigned)inf & LDG_FL_XIDENT)) {
+            mapped = true;
+            mid = (inf >> LDG_FACE_MAP_SHIFT) & 0xffff;
+            nax = face_axis(3, nlf);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < N1; ++j) {
+          const int t = k + N1 * j;
+          int tn = t;
+          if (mapped) {
+            const int nv = map_smem ? s_map[mid * NP + t] : __ldg(P.nmap + mid * NP + t);
+            tn = vol_to_face<N1, 3>(nax, nv);
+          }
+          xb[tn] = xv[j];
+        }
+      }
+    }
+    if (HAS_CU) {
+      __syncwarp();                                  // F_z rows read before the Cu update
+#pragma unroll
+      for (int n = 0; n < NP; ++n) {
+        h[0][n] = fma(sC[9], up[n], h[0][n]);
+        h[1][n] = fma(sC[10], up[n], h[1][n]);
+        fz[n] = fma(sC[11], up[n], fz[n]);
+      }
+    }
+
+    // ---- E: R = M_z [M_x M_y V + L_xy], V = -(G_x F_x + G_y F_y + G_z F_z)
+    // + M_z^-1 (e_0 fh_z0 + e_{N1-1} fh_z1)
+    __syncwarp();                                    // F_z planes complete
+    double v[NP];
+#pragma unroll
+    for (int j = 0; j < N1; ++j)
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          a = fma(P.g1[i * N1 + m], h[0][m + N1 * j], a);
+          a = fma(P.g1[j * N1 + m], h[1][i + N1 * m], a);
+        }
+        v[i + N1 * j] = -a;
+      }
+    axpy_planes<N1, PS>(v, s_tab + N1 * k, -1.0, sT2);
+    {
+      const double z0 = s_tab[NP + N1 * k], z1 = s_tab[NP + N1 * k + HI];
+#pragma unroll
+      for (int n = 0; n < NP; ++n)
+        v[n] = fma(z0, sFZ[(n / N1) * ES + n % N1], fma(z1, sFZ[N1 * ES + (n / N1) * ES + n % N1], v[n]));
+    }
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double c1[N1];
+#pragma unroll
+      for (int j = 0; j < N1; ++j) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) a = fma(P.m1[j * N1 + m], v[i + N1 * m], a);
+        c1[j] = a;
+      }
+#pragma unroll
+      for (int j = 0; j < N1; ++j) v[i + N1 * j] = c1[j];
+    }
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {
+      double r1[N1];
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) a = fma(P.m1[i * N1 + m], v[m + N1 * j], a);
+        r1[i] = a;
+      }
+#pragma unroll
+      for (int i = 0; i < N1; ++i) v[i + N1 * j] = r1[i];
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int a = 0; a < N1; ++a) {
+        double lx = 0.0, ly = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          lx = fma(P.m1[a * N1 + m], sXY[(s * 2 + 0) * N1 + m], lx);
+          ly = fma(P.m1[a * N1 + m], sXY[(s * 2 + 1) * N1 + m], ly);
+        }
+        v[(s ? HI : LO) + N1 * a] += lx;
+        v[a + N1 * (s ? HI : LO)] += ly;
+      }
+    // ---- F: z contraction, R rows out through shared
+#pragma unroll
+    for (int n = 0; n < NP; ++n) sU[k * PS + n] = v[n];
+    __syncwarp();
+    double out[NP];
+#pragma unroll
+    for (int n = 0; n < NP; ++n) out[n] = 0.0;
+    axpy_planes<N1, PS>(out, s_tab + 2 * NP + N1 * k, 1.0, sU);
+    if (active) {
+      int hm = 0;
+#pragma unroll
+      for (int n = 0; n < NP; ++n) hm = max(hm, hi_abs(out[n]));
+      bad_if_any(P, e, hm);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < NP; ++n) sU[k * PS + n] = out[n];
+    __syncwarp();
+    {
+      const int nval = min(EPW, P.e1 - e_w) * NB;
+      double* rb = R + (size_t)e_w * NB;
+      const double* sb = (!TANGENT && bsrc) ? bsrc + (size_t)e_w * NB : nullptr;
+#pragma unroll
+      for (int x = 0; x < (EPW * NB + 31) / 32; ++x) {
+        const int d = lane + 32 * x;
+        if (d < nval) {
+          double val = sW[G::el(d / NB) + ((d / NP) % N1) * PS + d % NP];
+          if (sb) val += __ldg(sb + d);
+          rb[d] = val;
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -1804,6 +2447,43 @@ complete_warp_kernel(const __grid_constant__ TensorParams P, const FaceRec* __re
 // dispatch
 // --------------------------------------------------------------------------
 
+// plane-mapped pass 1 at hex p = 1, 2: persistent grid of MINB blocks per SM
+template <int N1>
+static int launch_plane_g(const TensorParams& P, bool tangent, const FaceRec* fr, const double* u,
+                          const double* gproj, const double* bsrc, double* R, double* X,
+                          cudaStream_t s) {
+  using G = PlaneG<N1>;
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int nel = P.e1 - P.e0;
+  const int groups = (nel + G::EPW - 1) / G::EPW;
+  const int gp = std::max(1, std::min((groups + G::WPB - 1) / G::WPB, nsm * G::MINB));
+  const int smem = G::WPB * G::WARP * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(plane_kernel_g<N1, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel_g<N1, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel_g<N1, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel_g<N1, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel_g<N1, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel_g<N1, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel_g<N1, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel_g<N1, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+#define LDG_PLANE_G(T, C, D) \
+  plane_kernel_g<N1, T, C, D><<<gp, G::WPB * 32, smem, s>>>(P, fr, u, gproj, bsrc, R, X)
+  if (P.c_diag) {
+    if (P.flux_uses_u) { if (tangent) LDG_PLANE_G(true, true, true); else LDG_PLANE_G(false, true, true); }
+    else { if (tangent) LDG_PLANE_G(true, false, true); else LDG_PLANE_G(false, false, true); }
+  } else {
+    if (P.flux_uses_u) { if (tangent) LDG_PLANE_G(true, true, false); else LDG_PLANE_G(false, true, false); }
+    else { if (tangent) LDG_PLANE_G(true, false, false); else LDG_PLANE_G(false, false, false); }
+  }
+#undef LDG_PLANE_G
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 template <int N1, int ND, int NCU>
 static int run_pass(const TensorParams& P, int pass, bool tangent, const double* u,
                     const double* gproj, const double* bsrc, double* R, double* X,
@@ -1824,17 +2504,17 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
       const int smem = (kPlaneBlock / 32) * kPlaneWarp * (int)sizeof(double);
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(plane_kernel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(plane_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<true, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(plane_kernel<false, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
       }
-#define LDG_PLANE(T, C, D) plane_kernel<T, C, D><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X)
+#define LDG_PLANE(T, C, D) plane_kernel<T, C, D, false><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X)
       if (P.c_diag) {
         if (P.flux_uses_u) { if (tangent) LDG_PLANE(true, true, true); else LDG_PLANE(false, true, true); }
         else { if (tangent) LDG_PLANE(true, false, true); else LDG_PLANE(false, false, true); }
@@ -1844,6 +2524,11 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
       }
 #undef LDG_PLANE
       if (cudaGetLastError() != cudaSuccess) return 3;
+    } else if constexpr ((N1 == 2 || N1 == 3) && ND == 3 && NCU == 1) {
+      if (P.variant == 0) {
+        if (int rc = launch_plane_g<N1>(P, tangent, fr, u, gproj, bsrc, R, X, s)) return rc;
+      } else if (tangent) fused_kernel<N1, ND, NCU, true><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
+      else fused_kernel<N1, ND, NCU, false><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
     } else if (tangent) fused_kernel<N1, ND, NCU, true><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
     else fused_kernel<N1, ND, NCU, false><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
     if (cudaGetLastError() != cudaSuccess) return 3;
@@ -1901,10 +2586,51 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
 // (chunk_dep, computed from the face table at ldg_create), while that
 // chunk's R rows and exports are still resident in L2, so pass 2 costs L2
 // rather than HBM traffic.
+// One-launch operator (hex p = 3, ncu = 1): plane_kernel<.., FUSED> runs pass 1
+// and, as the pass-1 windows it reads complete, pass 2 of each group, so the R
+// rows and exports pass 2 re-reads come from L2 instead of HBM.
+static int launch_plane_fused(const TensorParams& P, bool tangent, const double* u,
+                              const double* gproj, const double* bsrc, double* R, double* X,
+                              cudaStream_t s) {
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int groups = (P.e1 - P.e0 + 7) / 8;
+  const int gp = std::max(1, std::min((groups + 3) / 4, nsm * LDG_PLANE_MINB));
+  const int smem = (kPlaneBlock / 32) * kPlaneWarp * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(plane_kernel<true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel<false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel<true, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel<false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(plane_kernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const FaceRec* fr = reinterpret_cast<const FaceRec*>(P.frec);
+#define LDG_PLANE_F(T, C, D) plane_kernel<T, C, D, true><<<gp, kPlaneBlock, smem, s>>>(P, fr, u, gproj, bsrc, R, X)
+  if (P.c_diag) {
+    if (P.flux_uses_u) { if (tangent) LDG_PLANE_F(true, true, true); else LDG_PLANE_F(false, true, true); }
+    else { if (tangent) LDG_PLANE_F(true, false, true); else LDG_PLANE_F(false, false, true); }
+  } else {
+    if (P.flux_uses_u) { if (tangent) LDG_PLANE_F(true, true, false); else LDG_PLANE_F(false, true, false); }
+    else { if (tangent) LDG_PLANE_F(true, false, false); else LDG_PLANE_F(false, false, false); }
+  }
+#undef LDG_PLANE_F
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 template <int N1, int ND, int NCU>
 static int run_fused(const TensorParams& P, bool tangent, const double* u,
                      const double* gproj, const double* bsrc, double* R, double* X,
                      cudaStream_t s) {
+  if constexpr (N1 == 4 && ND == 3 && NCU == 1) {
+    if (P.fused && P.fuse && P.nchunk <= 1 && P.e0 == 0 && P.e1 == P.ne && P.ghost0 == INT32_MAX &&
+        P.x_consumer && P.p2_mode == 0 && P.variant == 0)
+      return launch_plane_fused(P, tangent, u, gproj, bsrc, R, X, s);
+  }
   if (P.nchunk <= 1) return run_pass<N1, ND, NCU>(P, 3, tangent, u, gproj, bsrc, R, X, s);
   // pass 2 chunks go to a side stream so they overlap the next pass-1 chunk
   // (fork / join with events: also valid under CUDA graph capture)

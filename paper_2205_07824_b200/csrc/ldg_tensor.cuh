@@ -8,6 +8,10 @@ namespace ldg {
 
 constexpr int LDG_MAX_CHUNKS = 16;
 
+#ifndef LDG_FUSED_DEFAULT
+#define LDG_FUSED_DEFAULT 0       // one-launch operator (ldg_set_option "fused")
+#endif
+
 // Operator data passed by value (__grid_constant__) to every launch.  The
 // 1D tables are tiny and read uniformly across a warp, so they live in the
 // kernel parameter bank (constant cache), which DFMA can consume directly.
@@ -37,6 +41,13 @@ struct TensorParams {
   // place and only the halo lands in a side buffer (INT32_MAX: no ghosts)
   int ghost0;
   const double* u_ghost;
+  // one-launch operator (hex p = 3, ncu = 1): pass 1 and pass 2 in one
+  // persistent kernel, pass 2 of a group as soon as the pass-1 windows it
+  // reads are complete (ldg_fused.cu plane_kernel<.., FUSED>)
+  int fused;              // 1: run_fused takes the one-launch kernel where it applies
+  int* fuse;              // [0] pass-1 claims, [1] pass-2 claims, [2] exited warps, [3..) windows
+  const int2* fuse_dep;   // per 8-element group: first / last 32-group window pass 2 reads
+  int fuse_nwin;
   double d1[LDG_MAX_N1 * LDG_MAX_N1];
   double m1[LDG_MAX_N1 * LDG_MAX_N1];
   double s1[LDG_MAX_N1 * LDG_MAX_N1];

@@ -81,11 +81,12 @@ def test_convdiff_periodic_p1_to_p5_vs_oracle():
         assert rel(s.residual_tangent(st, u)[0], o.residual_tangent(u, u)) < TOL, p
 
 
+@pytest.mark.parametrize("p", [1, 2, 3])
 @pytest.mark.parametrize("model_name", ["poisson", "convection_diffusion"])
-def test_sheared_hex_p3_vs_oracle(model_name):
+def test_sheared_hex_vs_oracle(model_name, p):
     """Affinely sheared hexes: the element coefficient blocks C = detJ J^-T A J^-1
-    are full 3x3 (the plane kernel's general-C branch; axis-aligned boxes take
-    the diagonal branch)."""
+    are full 3x3 (the plane kernels' general-C branch; axis-aligned boxes take
+    the diagonal branch); p = 1, 2: plane_kernel_g, p = 3: plane_kernel."""
     from oracle import make_oracle
     from paper_2205_07824_b200 import meshgen, model, refelem
     from paper_2205_07824_b200.system import LdgSystem, SolverState
@@ -100,7 +101,7 @@ def test_sheared_hex_p3_vs_oracle(model_name):
     mesh.vertices = mesh.vertices @ A.T
     mesh.ho_nodes = mesh.ho_nodes @ A.T
     topo = meshgen.build_face_topology(mesh)
-    master = refelem.build_master("hex", 3)
+    master = refelem.build_master("hex", p)
     s = LdgSystem(m, mesh, topo, master)
     o = make_oracle(m, mesh, topo, master)
     rng = np.random.default_rng(11)
@@ -265,9 +266,39 @@ def test_hex_p3_vs_oracle_at_scale(shear):
     assert rel(s.residual_tangent(st, du)[0], o.residual_tangent(u, du)) < TOL
 
 
-@pytest.mark.parametrize("option,value", [("pass1_variant", 1), ("c_diag", 0), ("p2_mode", 1),
-                                          ("p2_mode", 2), ("p2_mode", 3)])
-def test_kernel_variants_equal_default(option, value):
+@pytest.mark.parametrize("p,counts,sweep", [(2, [32, 32, 30], 148 * 5 * 2 * 10),
+                                            (1, [40, 40, 36], 148 * 3 * 4 * 16)])
+def test_hex_p1_p2_vs_oracle_at_scale(p, counts, sweep):
+    """plane_kernel_g (hex p = 1, 2, config 5) past one persistent sweep:
+    more than twice the elements one sweep of its grid covers (MINB blocks
+    per SM x warps per block x 32 / N1 elements per warp), so every warp runs
+    the double-buffered loop at least twice; also the last partial group
+    (p = 2: 10 elements per warp).  Oracle R and J du at 1e-12."""
+    from oracle import make_oracle
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem, SolverState
+    m = model.builtin_model("convection_diffusion", nd=3, mu=[0.6, -0.3, 0.4, 0.7])
+    m.bcs = {t: model.BoundaryCondition(type="dirichlet", data=["x1*x3 - 0.2*x2"])
+             for t in range(1, 7)}
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, counts, "hex")
+    topo = meshgen.build_face_topology(mesh)
+    master = refelem.build_master("hex", p)
+    s = LdgSystem(m, mesh, topo, master)
+    assert s.n_elements > 2 * sweep
+    o = make_oracle(m, mesh, topo, master)
+    rng = np.random.default_rng(19)
+    u = rng.normal(size=(s.n_elements, s.n_nodes, 1))
+    du = rng.normal(size=u.shape)
+    st = SolverState(u=u, q=None, w=None, t=0.0)
+    assert rel(s.residual(st)[0], o.residual(u)) < TOL
+    assert rel(s.residual_tangent(st, du)[0], o.residual_tangent(u, du)) < TOL
+
+
+@pytest.mark.parametrize("option,value,p", [("pass1_variant", 1, 3), ("c_diag", 0, 3), ("p2_mode", 1, 3),
+                                            ("p2_mode", 2, 3), ("p2_mode", 3, 3),
+                                            ("pass1_variant", 1, 2), ("c_diag", 0, 2),
+                                            ("pass1_variant", 1, 1), ("c_diag", 0, 1)])
+def test_kernel_variants_equal_default(option, value, p):
     """Every kernel variant ldg_set_option selects (the pencil pass 1, the
     general flux-coefficient branch on an axis-aligned mesh, pass 2 without
     PDL / block-wise / one-shot) gives the default operator to 1e-13 on a
@@ -276,8 +307,9 @@ def test_kernel_variants_equal_default(option, value):
     from paper_2205_07824_b200 import meshgen, model, refelem
     from paper_2205_07824_b200.system import LdgSystem
     m = model.load_model(str(GOLDEN / "poisson3d.model"))
-    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [24, 22, 20], "hex")
-    s = LdgSystem(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("hex", 3))
+    counts = {3: [24, 22, 20], 2: [32, 32, 30], 1: [40, 40, 36]}[p]
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, counts, "hex")
+    s = LdgSystem(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("hex", p))
     du = torch.as_tensor(np.random.default_rng(5).normal(size=(s.n_elements, s.n_nodes, 1)),
                          device="cuda")
     u = torch.as_tensor(np.random.default_rng(6).normal(size=du.shape), device="cuda")
@@ -417,3 +449,41 @@ def test_native_comm_nccl_single_rank():
         assert rel(p.apply_native(u, False).cpu().numpy(), s.residual_dev(u).cpu().numpy()) < 1e-13
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("model_name,shear", [("poisson", False), ("poisson", True),
+                                              ("convection_diffusion", False)])
+def test_one_launch_operator_bitwise_equal_two_launch(model_name, shear):
+    """The one-launch operator (plane_kernel<.., FUSED>, ldg_set_option "fused"):
+    pass 2 of each 8-element group runs in the same persistent launch once the
+    pass-1 windows it reads are published.  Same arithmetic in the same order
+    as plane_kernel + complete_warp4_kernel, so R and J du are BITWISE equal to
+    the two-launch operator, over repeated launches (the claim / window
+    counters reset themselves at the end of each launch), at a size past one
+    persistent sweep (2,730 groups vs 1,184 warps); DIAG, general-C and
+    convective (Cu) branches."""
+    import torch
+    from paper_2205_07824_b200 import meshgen, model, refelem
+    from paper_2205_07824_b200.system import LdgSystem
+    if model_name == "poisson":
+        m = model.load_model(str(GOLDEN / "poisson3d.model"))
+    else:
+        m = model.builtin_model("convection_diffusion", nd=3, mu=[0.6, -0.3, 0.4, 0.7])
+        m.bcs = {t: model.BoundaryCondition(type="dirichlet", data=["x1*x3 - 0.2*x2"])
+                 for t in range(1, 7)}
+    mesh = meshgen.generate_structured([(0.0, 1.0)] * 3, [30, 28, 26], "hex")
+    if shear:
+        A = np.array([[1.0, 0.3, 0.1], [0.0, 1.0, 0.2], [0.0, 0.0, 0.9]])
+        mesh.vertices = mesh.vertices @ A.T
+        mesh.ho_nodes = mesh.ho_nodes @ A.T
+    s = LdgSystem(m, mesh, meshgen.build_face_topology(mesh), refelem.build_master("hex", 3))
+    rng = np.random.default_rng(23)
+    du = torch.as_tensor(rng.normal(size=(s.n_elements, s.n_nodes, 1)), device="cuda")
+    u = torch.as_tensor(rng.normal(size=du.shape), device="cuda")
+    out = {}
+    for fused in (0, 1):
+        assert s.lib.ldg_set_option(s._h, b"fused", fused) == 0
+        out[fused] = [(s.tangent_dev(du).clone(), s.residual_dev(u).clone()) for _ in range(3)]
+    for k in range(3):
+        assert torch.equal(out[1][k][0], out[0][0][0])
+        assert torch.equal(out[1][k][1], out[0][0][1])
