@@ -10,6 +10,9 @@
 #include <algorithm>
 #include <string>
 #include <vector>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 #include "ldg_dense.cuh"
 #include "nvtx.cuh"
 #include "ldg_tensor.cuh"
@@ -60,6 +63,35 @@ struct LdgHandle {
   std::vector<cudaEvent_t> ev_in, ev_p2;
   cudaEvent_t ev_start = nullptr;
 };
+
+#ifndef LDG_STAGE_NT
+#define LDG_STAGE_NT 1            // staging copies with non-temporal stores (0: memcpy)
+#endif
+// pageable -> pinned staging copy of one slice: the pinned destination is not
+// read again by the host, so non-temporal 16-B stores skip the read-for-
+// ownership of every destination line (2 instead of 3 memory transfers per
+// byte); SSE2 only (baseline x86-64)
+static void stage_copy(double* dst, const double* src, size_t n) {
+#if LDG_STAGE_NT && defined(__x86_64__)
+  size_t i = 0;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) != 0) {      // 16-B align the destination
+    dst[0] = src[0];
+    i = 1;
+  }
+  for (; i + 8 <= n; i += 8) {
+    const __m128d a0 = _mm_loadu_pd(src + i), a1 = _mm_loadu_pd(src + i + 2);
+    const __m128d a2 = _mm_loadu_pd(src + i + 4), a3 = _mm_loadu_pd(src + i + 6);
+    _mm_stream_pd(dst + i, a0);
+    _mm_stream_pd(dst + i + 2, a1);
+    _mm_stream_pd(dst + i + 4, a2);
+    _mm_stream_pd(dst + i + 6, a3);
+  }
+  for (; i < n; ++i) dst[i] = src[i];
+  _mm_sfence();
+#else
+  memcpy(dst, src, n * sizeof(double));
+#endif
+}
 
 namespace ldg {
 // error reporting for the other translation units of the C ABI (comm.cu)
@@ -634,7 +666,7 @@ int ldg_apply_host_staged(LdgHandle* h, int tangent, const double* v_host, doubl
 #pragma omp parallel for schedule(static)
       for (int64_t k = 0; k < ns; ++k) {
         const size_t o = (size_t)k * slice, m = std::min((size_t)slice, n - o);
-        memcpy(stage + a + o, v_host + a + o, m * sizeof(double));
+        stage_copy(stage + a + o, v_host + a + o, m);
       }
       src = stage + a;
     }

@@ -1429,7 +1429,7 @@ struct PlaneG {
   static constexpr int OffXY = OffE + N1 * PS;      // x / y face fluxes per thread
   static constexpr int Raw = OffXY + N1 * XS;
   static constexpr int PER = Raw + (20 - Raw % 16) % 16;   // element stride = 4 (mod 16)
-  static constexpr int WPB = N1 == 2 ? 4 : 2;       // warps per block
+  static constexpr int WPB = N1 == 2 ? 4 : (N1 == 3 ? 2 : 1);   // warps per block
   static constexpr int MINB = N1 == 2 ? 3 : 5;      // blocks per SM (shared-memory bound)
   __host__ __device__ static constexpr int el(int e) { return e * PER + (e >> 2) * 2; }
   static constexpr int WARP = el(NSLOT);            // doubles per warp region
@@ -1891,6 +1891,402 @@ plane_kernel_g(const __grid_constant__ TensorParams P, const FaceRec* __restrict
     }
     __syncwarp();
   }
+}
+
+// --------------------------------------------------------------------------
+// pass 1 at hex p = 1 (ncu = 1): one thread per element, no exchange at all
+// --------------------------------------------------------------------------
+//
+// An 8-node element fits one thread's registers, so every contraction of the
+// plane kernel's stages (same arithmetic, same order per z-plane k) runs
+// in registers with compile-time operator entries; nothing goes through
+// shared memory.  The element's u row, coefficient block and face records are
+// 16-B loads of contiguous rows (a warp covers 32 consecutive elements).
+// Face node t of a face: z faces (i, j) -> i + 2j, y faces (i, k) -> i + 2k,
+// x faces (j, k) -> j + 2k; node n = i + 2j + 4k.
+
+template <bool TANGENT, bool HAS_CU, bool DIAG>
+__global__ void __launch_bounds__(128, 3)
+elem_kernel_p1(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+               const double* __restrict__ u, const double* __restrict__ gproj,
+               const double* __restrict__ bsrc, double* __restrict__ R,
+               double* __restrict__ X) {
+  constexpr int N1 = 2, NP = 4, NB = 8;
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int e = P.e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= P.e1) return;
+  double uu[NB];
+  {
+    const double2* up = reinterpret_cast<const double2*>(u + (size_t)e * NB);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 v = __ldg(up + q);
+      uu[2 * q] = v.x;
+      uu[2 * q + 1] = v.y;
+    }
+  }
+  double C[12];
+  {
+    const double2* kp = reinterpret_cast<const double2*>(P.kco + (size_t)e * P.kstride);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const double2 v = __ldg(kp + q);
+      C[2 * q] = v.x;
+      C[2 * q + 1] = v.y;
+    }
+  }
+  double tau[6];
+  int info[6], nbr[6];
+#pragma unroll
+  for (int lf = 0; lf < 6; ++lf) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(frec + (size_t)e * 6 + lf));
+    tau[lf] = v.x;
+    nbr[lf] = __double2loint(v.y);
+    info[lf] = __double2hiint(v.y);
+  }
+  const bool map_ok = true;
+  (void)map_ok;
+  double ext[6][NP];
+#pragma unroll
+  for (int lf = 0; lf < 6; ++lf) {
+    const int kind = info[lf] & LDG_FACE_KIND_MASK;
+#pragma unroll
+    for (int t = 0; t < NP; ++t) ext[lf][t] = 0.0;
+    if (kind == LDG_FACE_INTERIOR) {
+      if (info[lf] & LDG_FL_UNBR) {
+        const int mid = (info[lf] >> LDG_FACE_MAP_SHIFT) & 0xffff;
+        const double* base = nbr_row(P, u, nbr[lf], NB);
+#pragma unroll
+        for (int t = 0; t < NP; ++t) ext[lf][t] = __ldg(base + __ldg(P.nmap + mid * NP + t));
+      }
+    } else if (!TANGENT && gproj) {
+#pragma unroll
+      for (int t = 0; t < NP; ++t) ext[lf][t] = __ldg(gproj + (size_t)nbr[lf] * NP + t);
+    }
+  }
+  auto alpha_of = [&](int lf) {
+    const int acode = (info[lf] >> LDG_FL_ALPHA_SHIFT) & 3;
+    return acode == 1 ? 1.0 : (acode == 2 ? 0.5 : 0.0);
+  };
+  auto w_own_of = [&](int lf) {
+    const int kind = info[lf] & LDG_FACE_KIND_MASK;
+    return kind != LDG_FACE_INTERIOR ? 1.0
+           : ((info[lf] & LDG_FL_QOWN) ? 1.0 : ((info[lf] & LDG_FL_QHALF) ? 0.5 : 0.0));
+  };
+
+  // ---- z faces (planes 0 and 1): jumps and own-data fluxes; F_z planes
+  double jz[2][NP], fhz[2][NP], fz[2][NP];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const bool neu = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_NEUMANN;
+    const double alpha = alpha_of(f), sgn = f ? 1.0 : -1.0;
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+      const double uo = uu[n + NP * f], ex = ext[f][n];
+      const double d = uo - ex;
+      const double jmp = alpha * d;
+      double fh = tau[f] * (neu ? ex : d);
+      if (HAS_CU && !neu) fh = fma(sgn * C[11], uo - jmp, fh);
+      jz[f][n] = jmp;
+      fhz[f][n] = fh;
+    }
+  }
+  {
+    const double c2 = DIAG ? C[8] : 1.0;
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int n = 0; n < NP; ++n) {
+        double hz = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) hz = fma(P.d1[k * N1 + m], uu[n + NP * m], hz);
+        fz[k][n] = c2 * (-hz - P.clo[k] * jz[0][n] + P.chi[k] * jz[1][n]);
+      }
+  }
+  // ---- x / y faces per plane: own-data fluxes, gradients, flux density
+  double fxy[N1][4][N1];                        // [plane][s * 2 + ax][face-row a]
+  double hx[N1][NP], hy[N1][NP];
+  double alx[2], aly[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    alx[s] = alpha_of(4 + s);
+    aly[s] = alpha_of(2 + s);
+  }
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    const double* up = uu + NP * k;
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int ax = 0; ax < 2; ++ax) {
+        const int lf = ax == 0 ? 4 + s : 2 + s;
+        const bool neu = (info[lf] & LDG_FACE_KIND_MASK) == LDG_FACE_NEUMANN;
+        const double alpha = ax == 0 ? alx[s] : aly[s], sgn = s ? 1.0 : -1.0;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
+          const double uo = ax == 0 ? up[s + N1 * a] : up[a + N1 * s];
+          const double ex = ext[lf][a + N1 * k];
+          const double d = uo - ex;
+          double fh = tau[lf] * (neu ? ex : d);
+          if (HAS_CU && !neu) fh = fma(sgn * C[9 + ax], uo - alpha * d, fh);
+          fxy[k][s * 2 + ax][a] = fh;
+        }
+      }
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {
+      const double jxl = alx[0] * (up[N1 * j] - ext[4][j + N1 * k]);
+      const double jxh = alx[1] * (up[1 + N1 * j] - ext[5][j + N1 * k]);
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double vx = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) vx = fma(P.d1[i * N1 + m], up[m + N1 * j], vx);
+        hx[k][i + N1 * j] = -vx - P.clo[i] * jxl + P.chi[i] * jxh;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      const double jyl = aly[0] * (up[i] - ext[2][i + N1 * k]);
+      const double jyh = aly[1] * (up[i + N1] - ext[3][i + N1 * k]);
+#pragma unroll
+      for (int j = 0; j < N1; ++j) {
+        double vy = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) vy = fma(P.d1[j * N1 + m], up[i + N1 * m], vy);
+        hy[k][i + N1 * j] = -vy - P.clo[j] * jyl + P.chi[j] * jyh;
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+      if (DIAG) {
+        hx[k][n] *= C[0];
+        hy[k][n] *= C[4];
+      } else {
+        const double h0 = hx[k][n], h1 = hy[k][n], h2 = fz[k][n];
+        hx[k][n] = fma(C[0], h0, fma(C[1], h1, C[2] * h2));
+        hy[k][n] = fma(C[3], h0, fma(C[4], h1, C[5] * h2));
+        fz[k][n] = fma(C[6], h0, fma(C[7], h1, C[8] * h2));
+      }
+    }
+  }
+  // ---- exports and the own share of f(., q^)
+  auto put = [&](int lf, int t, double v) {
+    const int inf = info[lf];
+    if (P.x_consumer) {
+      const int nlf = (inf >> 4) & 7;
+      double* xb = X + ((size_t)nbr[lf] * 6 + nlf) * NP;
+      if ((unsigned)inf & LDG_FL_XIDENT) xb[t] = v;
+      else {
+        const int mid = (inf >> LDG_FACE_MAP_SHIFT) & 0xffff;
+        xb[vol_to_face<N1, 3>(face_axis(3, nlf), __ldg(P.nmap + mid * NP + t))] = v;
+      }
+    } else {
+      X[((size_t)e * 6 + lf) * NP + t] = v;
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < N1; ++k)
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int ax = 0; ax < 2; ++ax) {
+        const int lf = ax == 0 ? 4 + s : 2 + s;
+        if ((info[lf] & LDG_FACE_KIND_MASK) == LDG_FACE_NEUMANN) continue;
+        const bool exp_ = info[lf] & LDG_FL_EXPORT;
+        const double w_own = w_own_of(lf), sgn = s ? 1.0 : -1.0;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) {
+          const int n = ax == 0 ? s + N1 * a : a + N1 * s;
+          const double xv = sgn * (ax == 0 ? hx[k][n] : hy[k][n]);
+          fxy[k][s * 2 + ax][a] = fma(w_own, xv, fxy[k][s * 2 + ax][a]);
+          if (exp_) put(lf, a + N1 * k, xv);
+        }
+      }
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    if ((info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_NEUMANN) continue;
+    const bool exp_ = info[f] & LDG_FL_EXPORT;
+    const double w_own = w_own_of(f), sgn = f ? 1.0 : -1.0;
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+      const double xv = sgn * fz[f][n];
+      fhz[f][n] = fma(w_own, xv, fhz[f][n]);
+      if (exp_) put(f, n, xv);
+    }
+  }
+  if (HAS_CU) {
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int n = 0; n < NP; ++n) {
+        hx[k][n] = fma(C[9], uu[n + NP * k], hx[k][n]);
+        hy[k][n] = fma(C[10], uu[n + NP * k], hy[k][n]);
+        fz[k][n] = fma(C[11], uu[n + NP * k], fz[k][n]);
+      }
+  }
+  // ---- volume term and lifts per plane, then the z contraction
+  double w[N1][NP];
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    double v[NP];
+#pragma unroll
+    for (int j = 0; j < N1; ++j)
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          a = fma(P.g1[i * N1 + m], hx[k][m + N1 * j], a);
+          a = fma(P.g1[j * N1 + m], hy[k][i + N1 * m], a);
+        }
+        v[i + N1 * j] = -a;
+      }
+#pragma unroll
+    for (int m = 0; m < N1; ++m)
+#pragma unroll
+      for (int n = 0; n < NP; ++n) v[n] = fma(-P.g1[k * N1 + m], fz[m][n], v[n]);
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+      v[n] = fma(P.m1inv[k * N1], fhz[0][n], fma(P.m1inv[k * N1 + 1], fhz[1][n], v[n]));
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double c1[N1];
+#pragma unroll
+      for (int j = 0; j < N1; ++j) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) a = fma(P.m1[j * N1 + m], v[i + N1 * m], a);
+        c1[j] = a;
+      }
+#pragma unroll
+      for (int j = 0; j < N1; ++j) v[i + N1 * j] = c1[j];
+    }
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {
+      double r1[N1];
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) a = fma(P.m1[i * N1 + m], v[m + N1 * j], a);
+        r1[i] = a;
+      }
+#pragma unroll
+      for (int i = 0; i < N1; ++i) v[i + N1 * j] = r1[i];
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int a = 0; a < N1; ++a) {
+        double lx = 0.0, ly = 0.0;
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          lx = fma(P.m1[a * N1 + m], fxy[k][s * 2 + 0][m], lx);
+          ly = fma(P.m1[a * N1 + m], fxy[k][s * 2 + 1][m], ly);
+        }
+        v[s + N1 * a] += lx;
+        v[a + N1 * s] += ly;
+      }
+#pragma unroll
+    for (int n = 0; n < NP; ++n) w[k][n] = v[n];
+  }
+  double out[NB];
+#pragma unroll
+  for (int k = 0; k < N1; ++k)
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+      double a = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) a = fma(P.m1[k * N1 + m], w[m][n], a);
+      out[n + NP * k] = a;
+    }
+  if (!TANGENT && bsrc) {
+    const double2* bp = reinterpret_cast<const double2*>(bsrc + (size_t)e * NB);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 b = __ldg(bp + q);
+      out[2 * q] += b.x;
+      out[2 * q + 1] += b.y;
+    }
+  }
+  int hm = 0;
+#pragma unroll
+  for (int n = 0; n < NB; ++n) hm = max(hm, hi_abs(out[n]));
+  bad_if_any(P, e, hm);
+  double2* rp = reinterpret_cast<double2*>(R + (size_t)e * NB);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) rp[q] = make_double2(out[2 * q], out[2 * q + 1]);
+}
+
+// pass 2 at hex p = 1 (consumer-slot exports), one thread per element: the
+// element's R row, the exports of its completion faces (one 32-B row each)
+// lifted by M1 (x) M1 in registers, in complete_warp_kernel's face and
+// contraction order
+__global__ void __launch_bounds__(256)
+complete_elem_p1(const __grid_constant__ TensorParams P, const FaceRec* __restrict__ frec,
+                 const double* __restrict__ X, double* __restrict__ R) {
+  constexpr int N1 = 2, NP = 4, NB = 8;
+  const int e = P.e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= P.e1) return;
+  const double wgt = P.grad_centered ? -0.5 : -1.0;
+  int info[6];
+#pragma unroll
+  for (int lf = 0; lf < 6; ++lf) info[lf] = __ldg(reinterpret_cast<const int*>(frec + (size_t)e * 6 + lf) + 3);
+  double r[NB];
+  {
+    const double2* rp = reinterpret_cast<const double2*>(R + (size_t)e * NB);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 v = rp[q];
+      r[2 * q] = v.x;
+      r[2 * q + 1] = v.y;
+    }
+  }
+#pragma unroll
+  for (int lf = 0; lf < 6; ++lf) {
+    if (!(info[lf] & LDG_FL_COMPLETE)) continue;
+    const double2* xp = reinterpret_cast<const double2*>(X + ((size_t)e * 6 + lf) * NP);
+    const double2 x0 = __ldg(xp), x1 = __ldg(xp + 1);
+    const double v[NP] = {wgt * x0.x, wgt * x0.y, wgt * x1.x, wgt * x1.y};
+    // w(a', b) = sum_a M[a'][a] v(a, b);  L(a', b') = sum_b M[b'][b] w(a', b)
+    double w[NP], L[NP];
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+      for (int a2 = 0; a2 < N1; ++a2) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < N1; ++a) acc = fma(P.m1[a2 * N1 + a], v[a + N1 * b], acc);
+        w[a2 + N1 * b] = acc;
+      }
+#pragma unroll
+    for (int b2 = 0; b2 < N1; ++b2)
+#pragma unroll
+      for (int a2 = 0; a2 < N1; ++a2) {
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b < N1; ++b) acc = fma(P.m1[b2 * N1 + b], w[a2 + N1 * b], acc);
+        L[a2 + N1 * b2] = acc;
+      }
+    // face node (a, b) -> volume node: z faces (a, b, 0|1), y faces (a, 0|1, b),
+    // x faces (0|1, a, b)
+    const int side = lf & 1;
+#pragma unroll
+    for (int b = 0; b < N1; ++b)
+#pragma unroll
+      for (int a = 0; a < N1; ++a) {
+        const int node = lf < 2 ? a + N1 * b + NP * side
+                                : (lf < 4 ? a + N1 * side + NP * b : side + N1 * a + NP * b);
+        r[node] += L[a + N1 * b];
+      }
+  }
+  int hm = 0;
+#pragma unroll
+  for (int n = 0; n < NB; ++n) hm = max(hm, hi_abs(r[n]));
+  bad_if_any(P, e, hm);
+  double2* rp = reinterpret_cast<double2*>(R + (size_t)e * NB);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) rp[q] = make_double2(r[2 * q], r[2 * q + 1]);
 }
 
 // --------------------------------------------------------------------------
@@ -2447,6 +2843,33 @@ complete_warp_kernel(const __grid_constant__ TensorParams P, const FaceRec* __re
 // dispatch
 // --------------------------------------------------------------------------
 
+#ifndef LDG_P1_ELEM
+#define LDG_P1_ELEM 0             // A/B: hex p = 1 thread-per-element pass 1 (measured 200 vs
+#endif                            // 184 us for plane_kernel_g<2>: latency-bound on 12 B/DOF of
+                                  // face records + 12 B/DOF of coefficient blocks)
+#ifndef LDG_P2_ELEM1
+#define LDG_P2_ELEM1 0            // A/B: hex p = 1 thread-per-element pass 2 (config 5 p = 1:
+#endif                            // 37.7 vs 38.3 GDOF/s with complete_warp_kernel<2>)
+static int launch_elem_p1(const TensorParams& P, bool tangent, const FaceRec* fr, const double* u,
+                          const double* gproj, const double* bsrc, double* R, double* X,
+                          cudaStream_t s) {
+  const int nel = P.e1 - P.e0;
+  const int grid = (nel + 127) / 128;
+#define LDG_ELEM1(T, C, D) elem_kernel_p1<T, C, D><<<grid, 128, 0, s>>>(P, fr, u, gproj, bsrc, R, X)
+  if (P.c_diag) {
+    if (P.flux_uses_u) { if (tangent) LDG_ELEM1(true, true, true); else LDG_ELEM1(false, true, true); }
+    else { if (tangent) LDG_ELEM1(true, false, true); else LDG_ELEM1(false, false, true); }
+  } else {
+    if (P.flux_uses_u) { if (tangent) LDG_ELEM1(true, true, false); else LDG_ELEM1(false, true, false); }
+    else { if (tangent) LDG_ELEM1(true, false, false); else LDG_ELEM1(false, false, false); }
+  }
+#undef LDG_ELEM1
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+#ifndef LDG_PLANE_G5
+#define LDG_PLANE_G5 0            // A/B: 5 = plane_kernel_g at hex p = 4 as well
+#endif
 // plane-mapped pass 1 at hex p = 1, 2: persistent grid of MINB blocks per SM
 template <int N1>
 static int launch_plane_g(const TensorParams& P, bool tangent, const FaceRec* fr, const double* u,
@@ -2524,8 +2947,10 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
       }
 #undef LDG_PLANE
       if (cudaGetLastError() != cudaSuccess) return 3;
-    } else if constexpr ((N1 == 2 || N1 == 3) && ND == 3 && NCU == 1) {
-      if (P.variant == 0) {
+    } else if constexpr ((N1 == 2 || N1 == 3 || N1 == LDG_PLANE_G5) && ND == 3 && NCU == 1) {
+      if (P.variant == 0 && N1 == 2 && LDG_P1_ELEM) {
+        if (int rc = launch_elem_p1(P, tangent, fr, u, gproj, bsrc, R, X, s)) return rc;
+      } else if (P.variant == 0) {
         if (int rc = launch_plane_g<N1>(P, tangent, fr, u, gproj, bsrc, R, X, s)) return rc;
       } else if (tangent) fused_kernel<N1, ND, NCU, true><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
       else fused_kernel<N1, ND, NCU, false><<<grid, kFBlock, 0, s>>>(P, fr, u, gproj, bsrc, R, X);
@@ -2539,8 +2964,14 @@ static int run_pass(const TensorParams& P, int pass, bool tangent, const double*
     const bool pipe = P.p2_mode != 3;                 // one-shot block kernel (A/B)
     bool done = false;
     const bool warp2 = P.p2_mode < 2;                 // block kernel (A/B)
+    if constexpr (N1 == 2 && ND == 3 && NCU == 1 && LDG_P2_ELEM1) {
+      if (P.x_consumer && P.p2_mode == 0) {
+        complete_elem_p1<<<(nel + 255) / 256, 256, 0, s>>>(P, reinterpret_cast<const FaceRec*>(P.frec), X, R);
+        done = true;
+      }
+    }
     if constexpr (N1 >= 2 && N1 <= LDG_P2W_MAXN1 && ND == 3 && NCU == 1) {
-      if (P.x_consumer && warp2) {
+      if (!done && P.x_consumer && warp2) {
         constexpr int EPW = 32 / (N1 * N1);
         const int ngr = (nel + EPW - 1) / EPW;
         const int g = std::max(1, std::min((ngr + 7) / 8, nsm2 * LDG_P2W_GRID));

@@ -297,7 +297,8 @@ def test_hex_p1_p2_vs_oracle_at_scale(p, counts, sweep):
 @pytest.mark.parametrize("option,value,p", [("pass1_variant", 1, 3), ("c_diag", 0, 3), ("p2_mode", 1, 3),
                                             ("p2_mode", 2, 3), ("p2_mode", 3, 3),
                                             ("pass1_variant", 1, 2), ("c_diag", 0, 2),
-                                            ("pass1_variant", 1, 1), ("c_diag", 0, 1)])
+                                            ("pass1_variant", 1, 1), ("c_diag", 0, 1),
+                                            ("p2_mode", 1, 1)])
 def test_kernel_variants_equal_default(option, value, p):
     """Every kernel variant ldg_set_option selects (the pencil pass 1, the
     general flux-coefficient branch on an axis-aligned mesh, pass 2 without
