@@ -37,6 +37,11 @@ constexpr int NQ = ND == 3 ? NQ1 * NQ1 * NQ1 : (ND == 2 ? NQ1 * NQ1 : NQ1);
 constexpr int NFN = ND == 3 ? N1 * N1 : (ND == 2 ? N1 : 1);   // a 1D face is one point
 constexpr int NQF = ND == 3 ? NQ1 * NQ1 : (ND == 2 ? NQ1 : 1);
 constexpr int NFACE = 2 * ND;
+#ifndef NL_FB
+#define NL_FB NFACE
+#endif
+constexpr int NFB = NL_FB;                     // faces per batch of the face phase (divides NFACE)
+static_assert(NFACE % NFB == 0, "face batch");
 constexpr int NVQ = KIND_C ? 0 : NCU * ND;
 constexpr int NV = NCU + NVQ + NW;             // state variables per point (u, q, w)
 constexpr int OW = NCU + NVQ;                  // offset of w within a point's variables
@@ -612,9 +617,11 @@ struct RShape {
   static constexpr int BS = (NVA > NG ? NVA : NG) * MX;           // one volume work buffer
   // face phase: traces of every face at its Gauss points, own and neighbour
   // side [side][face][v][NQF], one face's staging pair, and the face fluxes
-  static constexpr int TR = NFACE * NVA * NQF;
+  // (per batch of NFB faces: NFB < NFACE halves / thirds the face phase's
+  // shared memory, which is what bounds the blocks per SM in 3D)
+  static constexpr int TR = NFB * NVA * NQF;
   static constexpr int NBF = NVA * NFN;                        // one face's neighbour nodes
-  static constexpr int FACE = 2 * TR + NBF + 2 * NVA * MXF + NFACE * NQF * NCU + 2 * NBF;
+  static constexpr int FACE = 2 * TR + NBF + 2 * NVA * MXF + NFB * NQF * NCU + 2 * NBF;
   // the neighbour double buffer sits at the end of the work region, clear of
   // the volume buffers, so face 0's gathers fly during the volume phase
   static constexpr int WORK = 2 * BS + 2 * NBF > FACE ? 2 * BS + 2 * NBF : FACE;
@@ -946,107 +953,116 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
   }
   __syncthreads();
 
-  // ---- faces: traces of all faces at their Gauss points (one face's own and
-  // neighbour staging at a time), then every face point's f^ at once, then
-  // the lift with each (node, component) owned by one thread
-  double* TRc = bA;                            // [side][face][v][NQF]
+  // ---- faces, in batches of NFB: traces of the batch's faces at their Gauss
+  // points (one face's own and neighbour staging at a time), then every face
+  // point's f^ of the batch at once, then the lift with each (node, component)
+  // owned by one thread
+  double* TRc = bA;                            // [side][face of the batch][v][NQF]
   double* SO = bA + 2 * S::TR;                 // own face nodes [v][face grid]
   double* ST1 = SO + S::NBF;                   // first-stage scratch [side][v][..]
-  double* sF = ST1 + 2 * NVA * MXF;            // [face][NQF][NCU]
-  for (int lf = 0; lf < NFACE; ++lf) {
-    if (lf + 1 < NFACE) prefetch_face(lf + 1, NB2 + ((lf + 1) & 1) * S::NBF);
-    else cp_async_commit();                    // (empty group keeps the counting uniform)
-    for (int idx = tid; idx < S::NBF; idx += NT)
-      SO[idx] = sV[(idx / NFN) * NB + face_vol_node(lf, idx % NFN)];
-    cp_async_wait1();                          // this face's neighbour nodes have landed
-    __syncthreads();
-    const double* nb = NB2 + (lf & 1) * S::NBF;
-    double* tro = TRc + (0 * NFACE + lf) * NVA * NQF;
-    double* trn = TRc + (1 * NFACE + lf) * NVA * NQF;
-    if (ND == 3) {
-      contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(SO, ST1, NVA, tid);
-      contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(nb, ST1 + NVA * NQ1 * N1, NVA, tid);
+  double* sF = ST1 + 2 * NVA * MXF;            // [face of the batch][NQF][NCU]
+  for (int b0 = 0; b0 < NFACE; b0 += NFB) {
+    for (int lf = b0; lf < b0 + NFB; ++lf) {
+      if (lf + 1 < NFACE) prefetch_face(lf + 1, NB2 + ((lf + 1) & 1) * S::NBF);
+      else cp_async_commit();                  // (empty group keeps the counting uniform)
+      for (int idx = tid; idx < S::NBF; idx += NT)
+        SO[idx] = sV[(idx / NFN) * NB + face_vol_node(lf, idx % NFN)];
+      cp_async_wait1();                        // this face's neighbour nodes have landed
       __syncthreads();
-      contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(ST1, tro, NVA, tid);
-      contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(ST1 + NVA * NQ1 * N1, trn, NVA, tid);
-    } else if (ND == 2) {
-      contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(SO, tro, NVA, tid);
-      contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(nb, trn, NVA, tid);
-    } else {                                   // a point face: the trace is the end node
-      for (int idx = tid; idx < NVA; idx += NT) {
-        tro[idx] = SO[idx];
-        trn[idx] = nb[idx];
+      const double* nb = NB2 + (lf & 1) * S::NBF;
+      double* tro = TRc + (0 * NFB + lf - b0) * NVA * NQF;
+      double* trn = TRc + (1 * NFB + lf - b0) * NVA * NQF;
+      if (ND == 3) {
+        contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(SO, ST1, NVA, tid);
+        contract_u<N1, N1, 1, 0, N1, NQ1, false, OP_PHI>(nb, ST1 + NVA * NQ1 * N1, NVA, tid);
+        __syncthreads();
+        contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(ST1, tro, NVA, tid);
+        contract_u<NQ1, N1, 1, 1, N1, NQ1, false, OP_PHI>(ST1 + NVA * NQ1 * N1, trn, NVA, tid);
+      } else if (ND == 2) {
+        contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(SO, tro, NVA, tid);
+        contract_u<N1, 1, 1, 0, N1, NQ1, false, OP_PHI>(nb, trn, NVA, tid);
+      } else {                                 // a point face: the trace is the end node
+        for (int idx = tid; idx < NVA; idx += NT) {
+          tro[idx] = SO[idx];
+          trn[idx] = nb[idx];
+        }
       }
+      __syncthreads();
+    }
+    if (CACHE == 2) {
+      // base cache: the traces [side][face][v][NQF] of the base variables
+      double* dst = P.bcache + (sz_t)P.ne * NV * NQ + (sz_t)e * 2 * NFACE * NV * NQF;
+      for (int idx = tid; idx < 2 * NFB * NV * NQF; idx += NT) {
+        const int side = idx / (NFB * NV * NQF), rest = idx % (NFB * NV * NQF);
+        dst[(side * NFACE + b0) * NV * NQF + rest] = TRc[idx];
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int it = tid; it < NFB * NQF; it += NT) {
+      const int lfb = it / NQF, s = it % NQF, lf = b0 + lfb;
+      const int info = P.finfo[e * NFACE + lf];
+      const int kind = info & 3;
+      const bool right = kind == 0 && (info & 4);
+      const bool sw = info & 8;
+      const int brow = P.fnbr[e * NFACE + lf];
+      const double* fg = P.fgeo + ((sz_t)e * NFACE + lf) * (ND + 2);
+      const double* ff = CURVED ? P.ffgeo + (((sz_t)e * NFACE + lf) * NQF + s) * FG : fg;
+      double n[ND];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) n[d] = ff[d];
+      double x[ND];
+      if (CURVED) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) x[d] = ff[ND + 1 + d];
+      } else {
+        phys_point(P, e, &c_fxi[(lf * NQF + s) * ND], x);
+      }
+      double vo[NVL], vn[NVL];
+#pragma unroll
+      for (int v = 0; v < NVL; ++v) {
+        if (CACHE == 1 && v < NV) {
+          vo[v] = bfac[((0 * NFACE + lf) * NV + v) * NQF + s];
+          vn[v] = bfac[((1 * NFACE + lf) * NV + v) * NQF + s];
+        } else {
+          const int vs = CACHE == 1 ? v - NV : v;
+          vo[v] = TRc[((0 * NFB + lfb) * NVA + vs) * NQF + s];
+          vn[v] = TRc[((1 * NFB + lfb) * NVA + vs) * NQF + s];
+        }
+      }
+      double fh[NCU];
+      face_flux<TANGENT>(P, e, kind, right, sw, brow, s, x, n, fg[ND + 1], vo, vn, fh);
+      const double w = (CURVED ? ff[ND] : c_fw[lf * NQF + s] * fg[ND]) * (right ? -1.0 : 1.0);
+#pragma unroll
+      for (int c = 0; c < NCU; ++c) sF[(lfb * NQF + s) * NCU + c] = w * fh[c];
+    }
+    __syncthreads();
+    // lift: thread owns (volume node, component) and sums the batch's faces through it
+    for (int it = tid; it < NB * NCU; it += NT) {
+      const int a = it / NCU, c = it % NCU;
+      const int ia[3] = {a % N1, (a / N1) % N1, ND == 3 ? a / (N1 * N1) : 0};
+      double acc = 0.0;
+#pragma unroll
+      for (int lfb = 0; lfb < NFB; ++lfb) {
+        const int lf = b0 + lfb;
+        const int ax = face_axis(lf);
+        if (ia[ax] != (face_side(lf) ? N1 - 1 : 0)) continue;
+        // face-node coordinates (t0, t1) over the tangential axes, ascending
+        const int t0 = ia[ax == 0 ? 1 : 0];
+        const int t1 = ND == 3 ? ia[ax == 2 ? 1 : 2] : 0;
+#pragma unroll
+        for (int s = 0; s < NQF; ++s) {
+          const int s0 = s % NQ1, s1 = ND == 3 ? s / NQ1 : 0;
+          const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1]
+                                    : (ND == 2 ? c_phi[s0 * N1 + t0] : 1.0);
+          acc = fma(ph, sF[(lfb * NQF + s) * NCU + c], acc);
+        }
+      }
+      sR[c * NB + a] += acc;
     }
     __syncthreads();
   }
-  if (CACHE == 2) {
-    // base cache: the traces [side][face][v][NQF] of the base variables
-    double* dst = P.bcache + (sz_t)P.ne * NV * NQ + (sz_t)e * 2 * NFACE * NV * NQF;
-    for (int idx = tid; idx < 2 * NFACE * NV * NQF; idx += NT) dst[idx] = TRc[idx];
-    return;
-  }
-  for (int it = tid; it < NFACE * NQF; it += NT) {
-    const int lf = it / NQF, s = it % NQF;
-    const int info = P.finfo[e * NFACE + lf];
-    const int kind = info & 3;
-    const bool right = kind == 0 && (info & 4);
-    const bool sw = info & 8;
-    const int brow = P.fnbr[e * NFACE + lf];
-    const double* fg = P.fgeo + ((sz_t)e * NFACE + lf) * (ND + 2);
-    const double* ff = CURVED ? P.ffgeo + (((sz_t)e * NFACE + lf) * NQF + s) * FG : fg;
-    double n[ND];
-#pragma unroll
-    for (int d = 0; d < ND; ++d) n[d] = ff[d];
-    double x[ND];
-    if (CURVED) {
-#pragma unroll
-      for (int d = 0; d < ND; ++d) x[d] = ff[ND + 1 + d];
-    } else {
-      phys_point(P, e, &c_fxi[(lf * NQF + s) * ND], x);
-    }
-    double vo[NVL], vn[NVL];
-#pragma unroll
-    for (int v = 0; v < NVL; ++v) {
-      if (CACHE == 1 && v < NV) {
-        vo[v] = bfac[((0 * NFACE + lf) * NV + v) * NQF + s];
-        vn[v] = bfac[((1 * NFACE + lf) * NV + v) * NQF + s];
-      } else {
-        const int vs = CACHE == 1 ? v - NV : v;
-        vo[v] = TRc[((0 * NFACE + lf) * NVA + vs) * NQF + s];
-        vn[v] = TRc[((1 * NFACE + lf) * NVA + vs) * NQF + s];
-      }
-    }
-    double fh[NCU];
-    face_flux<TANGENT>(P, e, kind, right, sw, brow, s, x, n, fg[ND + 1], vo, vn, fh);
-    const double w = (CURVED ? ff[ND] : c_fw[lf * NQF + s] * fg[ND]) * (right ? -1.0 : 1.0);
-#pragma unroll
-    for (int c = 0; c < NCU; ++c) sF[(lf * NQF + s) * NCU + c] = w * fh[c];
-  }
-  __syncthreads();
-  // lift: thread owns (volume node, component) and sums the faces through it
-  for (int it = tid; it < NB * NCU; it += NT) {
-    const int a = it / NCU, c = it % NCU;
-    const int ia[3] = {a % N1, (a / N1) % N1, ND == 3 ? a / (N1 * N1) : 0};
-    double acc = 0.0;
-#pragma unroll
-    for (int lf = 0; lf < NFACE; ++lf) {
-      const int ax = face_axis(lf);
-      if (ia[ax] != (face_side(lf) ? N1 - 1 : 0)) continue;
-      // face-node coordinates (t0, t1) over the tangential axes, ascending
-      const int t0 = ia[ax == 0 ? 1 : 0];
-      const int t1 = ND == 3 ? ia[ax == 2 ? 1 : 2] : 0;
-#pragma unroll
-      for (int s = 0; s < NQF; ++s) {
-        const int s0 = s % NQ1, s1 = ND == 3 ? s / NQ1 : 0;
-        const double ph = ND == 3 ? c_phi[s0 * N1 + t0] * c_phi[s1 * N1 + t1]
-                                  : (ND == 2 ? c_phi[s0 * N1 + t0] : 1.0);
-        acc = fma(ph, sF[(lf * NQF + s) * NCU + c], acc);
-      }
-    }
-    sR[c * NB + a] += acc;
-  }
-  __syncthreads();
+  if (CACHE == 2) return;
   for (int idx = tid; idx < NCU * NB; idx += NT) {
     const int a = idx / NCU, c = idx % NCU;
     P.out[(sz_t)e * NB * NCU + idx] = sR[c * NB + a];

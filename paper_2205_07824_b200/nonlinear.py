@@ -39,6 +39,14 @@ from .tables import FACE_AXIS, DiscError, KernelNanError, TensorTables, affine_f
     plan_is_zero, uses_any
 
 TEMPLATE = Path(__file__).resolve().parent / "csrc" / "ldg_nl.cuh"
+# 3D element kernels: threads per element and faces per batch of the face
+# phase.  Batches of 2 (opposite faces) need a third of the trace buffer, so
+# 4-5 blocks fit an SM, but measured slower on the config-4 NS tangent (3.15 -
+# 3.72 vs 4.23 GDOF/s, scripts/nl_ab.py, profiles/r2_nl_launch_shape_ab.jsonl):
+# a batch's 32 face points leave 3 of 4 warps idle in the flux sweep
+NT_3D = 128
+FACE_BATCH_3D = 6
+MINB_3D = 3                 # blocks per SM the 3D residual / tangent kernels are register-capped for
 
 
 class NlParams(C.Structure):
@@ -282,7 +290,8 @@ def generate_source(tab):
     # get at least 128 (contractions and face work have more parallelism)
     nt = min(256, ((max(nq, nb) + 31) // 32) * 32)
     if nd == 3:
-        nt = max(nt, 128)
+        nt = max(nt, NT_3D)
+    fb = FACE_BATCH_3D if nd == 3 else 2 * nd
     ng = ncu * (nd + 1)
     ode = model.ode
     defs = dict(ND=nd, N1=n1, NQ1=nq1, NCU=ncu, NW=nw, KIND_C=int(model.kind == "C"),
@@ -292,7 +301,9 @@ def generate_source(tab):
                 HAS_WS=int(ws is not None), TRACE_CENTERED=int(model.numflux.trace == "centered"),
                 GRAD_CENTERED=int(model.numflux.grad_trace == "centered"),
                 HAS_UHAT=int(uhat is not None), HAS_FHAT=int(fhat is not None),
-                MASS_CONST=int(mass_const), NT=nt, CURVED=int(bool(getattr(tab, "curved", False))))
+                MASS_CONST=int(mass_const), NT=nt, CURVED=int(bool(getattr(tab, "curved", False))),
+                NL_FB=fb, NL_RES_MINB=MINB_3D if nd == 3 else 1,
+                NL_TAN_MINB=MINB_3D if nd == 3 else 1)
     lines = ["// generated by paper_2205_07824_b200/nonlinear.py -- do not edit"]
     lines += [f"#define {k} {v}" for k, v in defs.items()]
     mc = np.zeros(ncu)
@@ -383,7 +394,8 @@ class NlOperator:
         for name, nva in (("nl_residual", nv), ("nl_tangent", 2 * nv), ("nl_tangent_cached", nv),
                           ("nl_base_cache", nv)):
             nbf = nva * s["NB"] // s["N1"]          # one face's neighbour nodes (NVA x NFN)
-            face = 2 * (2 * nd) * nva * nqf + nbf + 2 * nva * mxf + 2 * nd * nqf * ncu + 2 * nbf
+            fb = s["NL_FB"]                         # faces per batch of the face phase
+            face = 2 * fb * nva * nqf + nbf + 2 * nva * mxf + fb * nqf * ncu + 2 * nbf
             work = max(2 * max(nva, ng) * mx + 2 * nbf, face)
             self.smem[name] = 8 * (nva * nb + ncu * nb + work)
         nvm = ncu if s["MASS_CONST"] else 3 * ncu
