@@ -437,6 +437,24 @@ def run_reference(args, rank):
     }), flush=True)
 
 
+def config5_lines(hbm):
+    """BASELINE config 5: 3D convection-diffusion tangent matvec, fully
+    periodic unit cube, hex p = 1..5 at ~10M DOFs each (scripts/
+    sweep_config5.py: CUDA events on the launching stream, L2 flushed
+    between reps, median of 10)."""
+    import gc
+    import torch
+    sys.path.insert(0, str(Path(__file__).resolve().parent / "scripts"))
+    import sweep_config5
+    rows = []
+    for p in (1, 2, 3, 4, 5):
+        rows.append(sweep_config5.run_p(p, 10, hbm))
+        gc.collect()
+        torch.cuda.empty_cache()
+    return {"metric": "config 5: 3D conv-diff periodic tangent matvec GDOF/s, p = 1..5",
+            "unit": "GDOF/s", "rows": rows}
+
+
 def run_b200(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -675,6 +693,8 @@ def run_b200(args, rank, world):
         line["tet"] = tet_line(hbm)
     if world == 1 and not args.no_nonlinear:
         line["nonlinear"] = nonlinear_lines(hbm, cpu=not args.no_cpu_baseline)
+    if world == 1 and not args.no_config5:
+        line["config5"] = config5_lines(hbm)
     if not args.no_cpu_baseline:
         ts, nd_cpu, cores, kind = reference_times(CPU_SAMPLE_N, 3, 1, ref_procs())
         v = nd_cpu / float(np.median(ts)) / 1e9
@@ -700,6 +720,8 @@ def main():
                     help="A/B: 1 / 0 forces the one-launch operator on / off (ldg_set_option 'fused')")
     ap.add_argument("--no-tet", action="store_true",
                     help="skip the config-3 tet variant (44^3 Kuhn tets, dense kernels)")
+    ap.add_argument("--no-config5", action="store_true",
+                    help="skip the config-5 sweep (conv-diff periodic, hex p = 1..5, ~10M DOFs each)")
     ap.add_argument("--no-solve", action="store_true",
                     help="skip the Newton-GMRES time-to-solution measurement")
     ap.add_argument("--no-nonlinear", action="store_true",

@@ -204,8 +204,9 @@ int ldg_set_ghost_rows_dense(LdgHandle* h, int ghost0, const double* u_ghost,
 /* Kernel-selection options of a tensor handle (A/B measurements, tests);
  * the defaults are the measured-best choices: "pass1_variant" (0 plane |
  * 1 pencil), "c_diag" (0 forces the general flux-coefficient branch),
- * "p2_mode" (0 warp + PDL | 1 no PDL | 2 block | 3 one-shot).  No reference
- * counterpart. */
+ * "p2_mode" (0 warp + PDL | 1 no PDL | 2 block | 3 one-shot), "fused"
+ * (1: hex p = 3 passes 1 and 2 in one persistent launch; measured slower,
+ * off).  No reference counterpart. */
 int ldg_set_option(LdgHandle* h, const char* name, int value);
 
 /* Unfused reference structure, kept for comparison: flux pass from a

@@ -68,7 +68,7 @@ def run_p(p, reps, hbm):
             "fused_bytes_per_dof": bytes_fused / nd_,
             "fused_frac_hbm": bytes_fused / (ms * 1e-3) / 1e9 / hbm,
             "survey_72B_frac_hbm": 72 * nd_ / (ms * 1e-3) / 1e9 / hbm,
-            "pass1_kernel": {1: "elem_p1", 2: "plane_g", 3: "plane"}.get(p, "pencil"), "setup_s": round(setup, 1)}
+            "pass1_kernel": {1: "plane_g", 2: "plane_g", 3: "plane"}.get(p, "pencil"), "setup_s": round(setup, 1)}
 
 
 def main():
