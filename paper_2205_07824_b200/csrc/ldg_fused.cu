@@ -125,8 +125,18 @@ struct __align__(16) FaceRec {
   int32_t info;
 };
 
+// N1 values whose planes are NOT rotated (every N1 that is not a power of
+// two): the rotation's index arithmetic and the conflicts it leaves cost more
+// than it saves (ncu, config-5 pencil pass 1, scripts/ncu_ab.sh: p = 4
+// 216.7 -> 186.2 us, bank-conflict excess 20.7M -> 11.4M wavefronts,
+// instructions 112.8M -> 87.7M; p = 5 208.6 -> 187.1 us, 13.0M -> 9.2M; a
+// padded k-stride at p = 5 measured no better: 187.7 us)
+#ifndef LDG_SWZ_ID_MASK
+#define LDG_SWZ_ID_MASK ((1 << 3) | (1 << 5) | (1 << 6) | (1 << 7))
+#endif
 template <int N1>
 __device__ __forceinline__ int swz(int i, int j, int k) {
+  if ((LDG_SWZ_ID_MASK >> N1) & 1) return i + N1 * j + N1 * N1 * k;
   if ((N1 & (N1 - 1)) == 0) return (i ^ k) + N1 * (j ^ k) + N1 * N1 * k;   // XOR swizzle
   int a = i + k, b = j + k;                                                  // rotation
   a -= a >= N1 ? N1 : 0;
