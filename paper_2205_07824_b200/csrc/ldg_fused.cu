@@ -144,6 +144,10 @@ __device__ __forceinline__ int swz(int i, int j, int k) {
   return a + N1 * b + N1 * N1 * k;
 }
 
+#ifndef LDG_P1_MINB_MAXN1
+#define LDG_P1_MINB_MAXN1 6       // pencil pass 1: register cap to the shared-memory block count up to this N1
+                                  // (N1 = 5, 6: ncu 186.3 -> 175.5 us, 186.6 -> 179.7 us)
+#endif
 template <int N1, int ND, int NCU>
 struct P1Smem {
   static constexpr int NF = ND == 3 ? N1 * N1 : N1;
@@ -169,7 +173,7 @@ struct P1Smem {
   static constexpr int SMEM_BLOCKS = (227 * 1024) / (EPB * PER * 8 + MAXMAPS * NF * 4 + 1024);
   static constexpr int EPB_S2 = (kFSmemDoubles - MAXMAPS * NF / 2) / PER;
   // (only where the register budget fits without spills: hex, ncu = 1, p <= 3)
-  static constexpr int MINB = (ND == 3 && NCU == 1 && N1 <= 4)
+  static constexpr int MINB = (ND == 3 && NCU == 1 && N1 <= LDG_P1_MINB_MAXN1)
                                   ? (SMEM_BLOCKS < 1 ? 1 : (SMEM_BLOCKS > 8 ? 8 : SMEM_BLOCKS))
                                   : 1;
 };
@@ -2317,13 +2321,18 @@ struct P2Smem {
   static constexpr int EPB = (kFBlock / TPE) > 0 ? (kFBlock / TPE) : 1;
 };
 
+#ifndef LDG_P2_MINB6
+#define LDG_P2_MINB6 8            // hex p = 5 block pass 2: 8 blocks / SM (64 registers; ncu 77.1 -> 68.3 us)
+#endif
 #ifndef LDG_P2P_MINB
 #define LDG_P2P_MINB 8        // persistent pass-2 blocks per SM (64 registers)
 #endif
 // one-shot pass 2: a 40-register budget (12 blocks / SM) measured 58.4 us vs
 // 64.6 us at the default on config 3; other shapes keep the default
 template <int N1, int ND, int NCU>
-constexpr int p2_min_blocks() { return (N1 == 4 && ND == 3 && NCU == 1) ? 12 : 1; }
+constexpr int p2_min_blocks() {
+  return (N1 == 4 && ND == 3 && NCU == 1) ? 12 : ((N1 == 6 && ND == 3 && NCU == 1) ? LDG_P2_MINB6 : 1);
+}
 
 template <int N1, int ND, int NCU>
 __global__ void __launch_bounds__(kFBlock, p2_min_blocks<N1, ND, NCU>())
