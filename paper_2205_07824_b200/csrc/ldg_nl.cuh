@@ -1075,7 +1075,13 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
 extern "C" __global__ void __launch_bounds__(NT, NL_RES_MINB) nl_residual(const __grid_constant__ NlParams P) {
   residual_body<false>(P);
 }
+// uncached tangent: register-capped only where the prelude asks (2D kind-C
+// models: NL_TANU_MINB from nonlinear.MINB_2D_C)
+#ifdef NL_TANU_MINB
+extern "C" __global__ void __launch_bounds__(NT, NL_TANU_MINB) nl_tangent(const __grid_constant__ NlParams P) {
+#else
 extern "C" __global__ void __launch_bounds__(NT) nl_tangent(const __grid_constant__ NlParams P) {
+#endif
   residual_body<true>(P);
 }
 #ifndef NL_TAN_MINB

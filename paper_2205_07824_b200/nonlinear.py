@@ -47,6 +47,12 @@ TEMPLATE = Path(__file__).resolve().parent / "csrc" / "ldg_nl.cuh"
 NT_3D = 128
 FACE_BATCH_3D = 6
 MINB_3D = 3                 # blocks per SM the 3D residual / tangent kernels are register-capped for
+# 2D kind-C models (one warp per element): residual and uncached tangent
+# capped to 24 blocks / SM (config-2 Euler p = 4, scripts/nl_ab.py: tangent
+# 15.8 -> 17.0 GDOF/s, residual 25.0 -> 26.7; 32 blocks: 15.2 / 27.1;
+# profiles/r2_nl_launch_shape_ab.jsonl); other 2D models keep the compiler's
+# choice
+MINB_2D_C = 24
 
 
 class NlParams(C.Structure):
@@ -292,6 +298,7 @@ def generate_source(tab):
     if nd == 3:
         nt = max(nt, NT_3D)
     fb = FACE_BATCH_3D if nd == 3 else 2 * nd
+    kind_c2 = nd == 2 and model.kind == "C"
     ng = ncu * (nd + 1)
     ode = model.ode
     defs = dict(ND=nd, N1=n1, NQ1=nq1, NCU=ncu, NW=nw, KIND_C=int(model.kind == "C"),
@@ -302,8 +309,10 @@ def generate_source(tab):
                 GRAD_CENTERED=int(model.numflux.grad_trace == "centered"),
                 HAS_UHAT=int(uhat is not None), HAS_FHAT=int(fhat is not None),
                 MASS_CONST=int(mass_const), NT=nt, CURVED=int(bool(getattr(tab, "curved", False))),
-                NL_FB=fb, NL_RES_MINB=MINB_3D if nd == 3 else 1,
+                NL_FB=fb, NL_RES_MINB=MINB_3D if nd == 3 else (MINB_2D_C if kind_c2 else 1),
                 NL_TAN_MINB=MINB_3D if nd == 3 else 1)
+    if kind_c2:
+        defs["NL_TANU_MINB"] = MINB_2D_C
     lines = ["// generated by paper_2205_07824_b200/nonlinear.py -- do not edit"]
     lines += [f"#define {k} {v}" for k, v in defs.items()]
     mc = np.zeros(ncu)
