@@ -2331,7 +2331,7 @@ struct P2Smem {
 // 64.6 us at the default on config 3; other shapes keep the default
 template <int N1, int ND, int NCU>
 constexpr int p2_min_blocks() {
-  return (N1 == 4 && ND == 3 && NCU == 1) ? 12 : ((N1 == 6 && ND == 3 && NCU == 1) ? LDG_P2_MINB6 : 1);
+  return (N1 == 4 && ND == 3 && NCU == 1) ? 12 : (((N1 == 5 || N1 == 6) && ND == 3 && NCU == 1) ? LDG_P2_MINB6 : 1);
 }
 
 template <int N1, int ND, int NCU>
