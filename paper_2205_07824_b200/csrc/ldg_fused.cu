@@ -280,7 +280,8 @@ fused_kernel(const __grid_constant__ TensorParams P, const FaceRec* __restrict__
       const double sgn = face_side(ND, lf) ? 1.0 : -1.0;
       (void)ax;
       const int vn_ = fvol<N1, ND>(lf, lt);
-      const int vs = ND == 3 ? swz<N1>(vn_ % N1, (vn_ / N1) % N1, vn_ / (N1 * N1)) : vn_;
+      const int vs = (ND == 3 && !((LDG_SWZ_ID_MASK >> N1) & 1))
+                         ? swz<N1>(vn_ % N1, (vn_ / N1) % N1, vn_ / (N1 * N1)) : vn_;
       // coefficient form (ldg_create): with d = u_own - u_other (u_other =
       // neighbour trace, Dirichlet g, or 0), every rule of disc.py:492-574 and
       // :657-821 is jump = alpha d, sJ * sigma * tau (u_L - u^) = rec.tau * d;
