@@ -659,7 +659,13 @@ def run_b200(args, rank, world):
                      "frac": ach_p1 / hbm, "traffic": traffic.get("pass1"),
                      "traffic_source": traffic.get("source"),
                      "algorithmic_bytes_per_dof": bytes_p1 / ndof, "ms": p1,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     # what bounds it instead (same ncu capture): the L1 / shared
+                     # pipe, with 8 warps / SM of a 255-register kernel
+                     "pipes": {k: traffic.get("pass1_" + k) for k in
+                               ("l1tex_busy", "issue_active", "fp64_pipe", "shared_wavefronts")}
+                              if traffic.get("pass1_l1tex_busy") is not None else None,
+                     "pipes_source": traffic.get("pipes_source")},
         "pass2_roofline": {"kernel": "complete_warp4_kernel (pass 2, shuffle face lift)", "achieved": ach_p2,
                            "frac": ach_p2 / hbm, "algorithmic_bytes_per_dof": bytes_p2 / ndof,
                            "traffic": traffic.get("pass2"), "ms": p2},

@@ -30,5 +30,14 @@ for r in rows[2:]:
         "pass2" if "complete" in name else name[:40])
     res.setdefault(key, b)
     res.setdefault(key + "_kernel", name[:80])
+    if key == "pass1" and "pass1_l1tex_busy" not in res:
+        # what bounds pass 1 instead of DRAM (bench.py roofline.pipes)
+        f = lambda k: float(r[idx[k]].replace(",", ""))
+        res["pass1_l1tex_busy"] = f("l1tex__throughput.avg.pct_of_peak_sustained_active") / 100
+        res["pass1_issue_active"] = f("smsp__issue_active.avg.pct_of_peak_sustained_active") / 100
+        res["pass1_fp64_pipe"] = f("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active") / 100
+        res["pass1_shared_wavefronts"] = f("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+        res["pipes_source"] = res["source"] + " (l1tex__throughput, smsp__issue_active, " \
+            "sm__inst_executed_pipe_fp64, l1tex__data_pipe_lsu_wavefronts_mem_shared)"
 json.dump(res, open("profiles/traffic.json", "w"), indent=1)
 print(json.dumps(res))
