@@ -544,12 +544,17 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
       const bool inter = (info[f] & LDG_FACE_KIND_MASK) == LDG_FACE_INTERIOR;
       const bool nu = inter && (alpha != 0.0 || beta != 0.0);
       const bool nq = inter && wn != 0.0;
-      double* nv4 = snv + slot * PNV + (f * NB + lt) * 4;
-      nv4[0] = nu ? __ldg(dense_nbr_row<false>(P, u, nbr[f], NB) + lt) : 0.0;
+      // the node's four values assembled in registers, stored as two 16-B
+      // words (four 8-B stores at a 32-B lane stride were 4-way conflicted)
+      double w4[4];
+      w4[0] = nu ? __ldg(dense_nbr_row<false>(P, u, nbr[f], NB) + lt) : 0.0;
 #pragma unroll
       for (int d = 0; d < 3; ++d)
-        nv4[1 + d] = (d < ND && nq) ? __ldg(dense_nbr_row<true>(P, q, nbr[f], NB * ND) + lt * ND + d)
-                                    : 0.0;
+        w4[1 + d] = (d < ND && nq) ? __ldg(dense_nbr_row<true>(P, q, nbr[f], NB * ND) + lt * ND + d)
+                                   : 0.0;
+      double2* nv2 = reinterpret_cast<double2*>(snv + slot * PNV + (f * NB + lt) * 4);
+      nv2[0] = make_double2(w4[0], w4[1]);
+      nv2[1] = make_double2(w4[2], w4[3]);
     }
   }
   __syncthreads();
