@@ -351,6 +351,9 @@ constexpr int kMmaEpb = 8;
 // (a multiple of 16 put all 8 in one bank: 4-8-way conflicts)
 __host__ __device__ constexpr int mma_pitch(int n) { return n + ((4 - n % 16) + 16) % 16; }
 
+#ifndef LDG_MMA_CHAINS
+#define LDG_MMA_CHAINS 2
+#endif
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
@@ -366,26 +369,37 @@ __device__ __forceinline__ void gemm8_tile(int mt, const double* __restrict__ A1
                                            double* C) {
   const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
   const int m = mt * 8 + r;
-  double d0 = 0.0, d1 = 0.0;
-#pragma unroll 5
+  // LDG_MMA_CHAINS independent accumulator chains (k-steps dealt round
+  // robin, summed at the end), so consecutive tensor-core steps do not wait
+  // on each other's accumulator
+  constexpr int NCH = LDG_MMA_CHAINS;
+  double d0[NCH], d1[NCH];
+#pragma unroll
+  for (int x = 0; x < NCH; ++x) d0[x] = d1[x] = 0.0;
+#pragma unroll
   for (int k0 = 0; k0 < K1; k0 += 4) {
     const int k = k0 + c;
     const double a = (m < M && k < K1) ? __ldg(A1 + k * AK1 + m) : 0.0;
     const double b = k < K1 ? B1[r * BE1 + k] : 0.0;
-    dmma884(d0, d1, a, b);
+    dmma884(d0[(k0 / 4) % NCH], d1[(k0 / 4) % NCH], a, b);
   }
   if (K2 > 0) {
-#pragma unroll 4
+#pragma unroll
     for (int k0 = 0; k0 < K2; k0 += 4) {
       const int k = k0 + c;
       const double a = (m < M && k < K2) ? __ldg(A2 + k * AK2 + m) : 0.0;
       const double b = k < K2 ? B2[r * BE2 + k] : 0.0;
-      dmma884(d0, d1, a, b);
+      dmma884(d0[(k0 / 4 + 1) % NCH], d1[(k0 / 4 + 1) % NCH], a, b);
     }
   }
+#pragma unroll
+  for (int x = 1; x < NCH; ++x) {
+    d0[0] += d0[x];
+    d1[0] += d1[x];
+  }
   if (m < M) {
-    C[(2 * c) * CE + m] = d0;
-    C[(2 * c + 1) * CE + m] = d1;
+    C[(2 * c) * CE + m] = d0[0];
+    C[(2 * c + 1) * CE + m] = d1[0];
   }
 }
 
