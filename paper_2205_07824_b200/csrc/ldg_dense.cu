@@ -351,6 +351,10 @@ constexpr int kMmaEpb = 8;
 // (a multiple of 16 put all 8 in one bank: 4-8-way conflicts)
 __host__ __device__ constexpr int mma_pitch(int n) { return n + ((4 - n % 16) + 16) % 16; }
 
+#ifndef LDG_TRACE_UNROLL
+#define LDG_TRACE_UNROLL 20       // neighbour-trace loop unroll (table loads in flight; ncu: 4 -> 20 281 -> 272 us)
+#endif
+constexpr int kTraceUnroll = LDG_TRACE_UNROLL;
 #ifndef LDG_MMA_CHAINS
 #define LDG_MMA_CHAINS 2
 #endif
@@ -619,7 +623,7 @@ flux_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict__
       for (int d = 0; d < ND; ++d) qn[d] = 0.0;
       const bool need_u = inter && (alpha != 0.0 || beta != 0.0), need_q = inter && wn != 0.0;
       if (need_u || need_q) {
-#pragma unroll 4
+#pragma unroll (kTraceUnroll)
         for (int b = 0; b < NB; ++b) {
           const double ph = __ldg(po + b * NQF);
           const double2* nv2 = reinterpret_cast<const double2*>(snv + slot * PNV + (f * NB + b) * 4);
