@@ -421,9 +421,22 @@ mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict_
   __shared__ double sjump[EPB * PF];          // [e][f][s]
   __shared__ double sg[EPB * PG];             // reference-direction derivatives [e][r][a]
   __shared__ double sl[EPB * PL];             // lifted jumps [e][f][a]
+  // element geometry for the final combination, loaded with the first loads
+  // (detj, invJ^T, then per face sJ and the normal): its latency no longer
+  // sits after the last barrier
+  constexpr int NGE = 1 + ND * ND + NFACE * (1 + ND);
+  __shared__ double sgeo[EPB][NGE];
   const int slot = threadIdx.x / TPE, lt = threadIdx.x % TPE, warp = threadIdx.x >> 5;
   const int e = blockIdx.x * EPB + slot;
   const bool active = e < P.ne;
+  if (active)
+    for (int x = lt; x < NGE; x += TPE) {
+      double v;
+      if (x < 1 + ND * ND) v = __ldg(P.geo + (size_t)e * (1 + ND * ND) + x);
+      else if (x < 1 + ND * ND + NFACE) v = __ldg(P.fsj + e * NFACE + (x - 1 - ND * ND));
+      else v = __ldg(P.fnorm + e * NFACE * ND + (x - 1 - ND * ND - NFACE));
+      sgeo[slot][x] = v;
+    }
   int info[NFACE], nbr[NFACE];
 #pragma unroll
   for (int f = 0; f < NFACE; ++f) {
@@ -487,21 +500,21 @@ mixed_dense_mma(const __grid_constant__ DenseParams P, const double* __restrict_
   }
   __syncthreads();
   if (!active || lt >= NB) return;
-  const double* g = P.geo + (size_t)e * (1 + ND * ND);
-  const double detj = __ldg(g);
+  const double* g = sgeo[slot];
+  const double detj = g[0];
   double qd[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
     double a = 0.0;
 #pragma unroll
-    for (int r = 0; r < ND; ++r) a = fma(__ldg(g + 1 + d * ND + r), sg[slot * PG + r * NB + lt], a);
+    for (int r = 0; r < ND; ++r) a = fma(g[1 + d * ND + r], sg[slot * PG + r * NB + lt], a);
     qd[d] = -a;
   }
 #pragma unroll
   for (int f = 0; f < NFACE; ++f) {
-    const double fac = __ldg(P.fsj + e * NFACE + f) / detj * sl[slot * PL + f * NB + lt];
+    const double fac = g[1 + ND * ND + f] / detj * sl[slot * PL + f * NB + lt];
 #pragma unroll
-    for (int d = 0; d < ND; ++d) qd[d] = fma(fac, __ldg(P.fnorm + (e * NFACE + f) * ND + d), qd[d]);
+    for (int d = 0; d < ND; ++d) qd[d] = fma(fac, g[1 + ND * ND + NFACE + f * ND + d], qd[d]);
   }
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
