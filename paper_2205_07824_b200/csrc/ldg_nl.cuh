@@ -40,6 +40,9 @@ constexpr int NFACE = 2 * ND;
 #ifndef NL_FB
 #define NL_FB NFACE
 #endif
+#ifndef NL_LOAD_BATCH
+#define NL_LOAD_BATCH 1
+#endif
 constexpr int NFB = NL_FB;                     // faces per batch of the face phase (divides NFACE)
 static_assert(NFACE % NFB == 0, "face batch");
 constexpr int NVQ = KIND_C ? 0 : NCU * ND;
@@ -859,13 +862,26 @@ __device__ __forceinline__ void residual_body(const NlParams& P) {
   const int e = blockIdx.x, tid = threadIdx.x;
   if (e >= P.ne) return;
 
-  // ---- load u, q (+ du, dq) of the element: [v][node]
-  for (int idx = tid; idx < NVA * NB; idx += NT) {
-    const int v = idx / NB, a = idx % NB;
-    const int fam = CACHE == 1 ? 1 : (v >= NV), vv = v % NV;
-    const double val = state_at(P, fam, vv, (sz_t)e, a);
-    sV[idx] = val;
-    bA[idx] = val;
+  // ---- load u, q (+ du, dq) of the element: [v][node], NL_LOAD_BATCH
+  // loads in flight per thread before their stores
+  constexpr int LB = NL_LOAD_BATCH;
+  for (int i0 = tid; i0 < NVA * NB; i0 += LB * NT) {
+    double val[LB];
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * NT;
+      const int v = idx / NB, a = idx % NB;
+      const int fam = CACHE == 1 ? 1 : (v >= NV), vv = v % NV;
+      val[b] = idx < NVA * NB ? state_at(P, fam, vv, (sz_t)e, a) : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * NT;
+      if (idx < NVA * NB) {
+        sV[idx] = val[b];
+        bA[idx] = val[b];
+      }
+    }
   }
   __syncthreads();
 

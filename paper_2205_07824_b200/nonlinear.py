@@ -53,6 +53,7 @@ MINB_3D = 3                 # blocks per SM the 3D residual / tangent kernels ar
 # profiles/r2_nl_launch_shape_ab.jsonl); other 2D models keep the compiler's
 # choice
 MINB_2D_C = 24
+LOAD_BATCH = 10             # element-load loads in flight per thread (NL_LOAD_BATCH; NS 3D tangent 4.23 -> 4.40 GDOF/s)
 
 
 class NlParams(C.Structure):
@@ -310,7 +311,7 @@ def generate_source(tab):
                 HAS_UHAT=int(uhat is not None), HAS_FHAT=int(fhat is not None),
                 MASS_CONST=int(mass_const), NT=nt, CURVED=int(bool(getattr(tab, "curved", False))),
                 NL_FB=fb, NL_RES_MINB=MINB_3D if nd == 3 else (MINB_2D_C if kind_c2 else 1),
-                NL_TAN_MINB=MINB_3D if nd == 3 else 1)
+                NL_TAN_MINB=MINB_3D if nd == 3 else 1, NL_LOAD_BATCH=LOAD_BATCH)
     if kind_c2:
         defs["NL_TANU_MINB"] = MINB_2D_C
     lines = ["// generated by paper_2205_07824_b200/nonlinear.py -- do not edit"]

@@ -40,10 +40,12 @@ def main():
                               **{k: v[k] for k in ("tangent_gdofs", "residual_gdofs", "attrs") if k in v}}),
                   flush=True)
             continue
-        nt, fb, minb = (int(x) for x in sh.split(","))
+        vals = [int(x) for x in sh.split(",")]
+        nt, fb, minb = vals[:3]
+        nonlinear.LOAD_BATCH = vals[3] if len(vals) > 3 else nonlinear.LOAD_BATCH
         nonlinear.NT_3D, nonlinear.FACE_BATCH_3D, nonlinear.MINB_3D = nt, fb, minb
         _, v = nl_bench.run("config4_ns3d_hex_p3", ns, a.reps, peak)
-        print(json.dumps({"nt": nt, "fb": fb, "minb": minb,
+        print(json.dumps({"nt": nt, "fb": fb, "minb": minb, "load_batch": nonlinear.LOAD_BATCH,
                           **{k: v[k] for k in ("tangent_gdofs", "residual_gdofs", "tangent_ms",
                                                "residual_ms", "tangent_uncached_gdofs",
                                                "base_cache_ms", "attrs")
