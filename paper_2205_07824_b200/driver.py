@@ -77,7 +77,7 @@ def elementwise_block_perm(system, device):
 
 
 def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="tangent",
-                           colors=None, invert="auto", share=True):
+                           colors=None, invert="auto", share=True, scratch=None):
     """Exact per-element diagonal blocks via distance-2 coloured probing
     (driver.py:119-142), through the tangent or by finite differences
     (``jv_mode``), across the packed blocks of kind-W / ODE systems."""
@@ -99,7 +99,8 @@ def build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode="
         native = (system._h, system.scratch())        # the linear tangent ignores the base
     return build_block_jacobi(tangent_fn, x, system.n_elements,
                               system.n_nodes * system.ncu, colors, native=native,
-                              mode=jv_mode, residual_fn=residual_fn, invert=invert, share=share)
+                              mode=jv_mode, residual_fn=residual_fn, invert=invert, share=share,
+                              scratch=scratch)
 
 
 class CompositeManager:
@@ -130,8 +131,9 @@ class CompositeManager:
 
 
 def make_preconditioner(system, kind, residual_fn, tangent_fn, state_vec, steady=True,
-                        jv_mode="tangent", rb_rank=10, rb_refresh=1):
-    """driver.py:178-198 (identity, mass, block_jacobi, composite)."""
+                        jv_mode="tangent", rb_rank=10, rb_refresh=1, scratch=None):
+    """driver.py:178-198 (identity, mass, block_jacobi, composite).  ``scratch``:
+    device memory the block-Jacobi build may use for its probed blocks."""
     if kind == "auto":
         kind = "block_jacobi" if steady else "mass"
     if kind == "identity":
@@ -139,9 +141,11 @@ def make_preconditioner(system, kind, residual_fn, tangent_fn, state_vec, steady
     if kind == "mass":
         return MassPreconditioner(system), None
     if kind == "block_jacobi":
-        return build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode), None
+        return build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode,
+                                      scratch=scratch), None
     if kind == "composite":
-        bj = build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode)
+        bj = build_pde_block_jacobi(system, residual_fn, tangent_fn, state_vec, jv_mode,
+                                    scratch=scratch)
         mgr = CompositeManager(system, bj, tangent_fn, rank=rb_rank, refresh=rb_refresh)
         return mgr, mgr.note_update
     raise DriverError(f"unknown or unsupported preconditioner {kind!r}")
@@ -198,8 +202,17 @@ def run_steady(system, precond="block_jacobi", abs_tol=1e-11, rel_tol=3e-8, forc
     u0 = torch.as_tensor(state.u, device=system.device).reshape(-1)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
+    scratch = None
+    if precond in ("block_jacobi", "composite") and u0.is_cuda:
+        # the first GMRES cycle's Krylov basis, allocated now (inside the timed
+        # build) and lent to the block-Jacobi build for its probed blocks:
+        # one multi-GB allocation in a fresh process instead of two
+        from .solver import _WS
+        m = min(restart, gmres_max_iter)
+        scratch = _WS.get(m, u0.numel(), u0.device, need_z=orth != "dcgs2").V
     M, cb = make_preconditioner(system, precond, res_fn, tan_fn, u0, jv_mode=jv_mode,
-                                rb_rank=rb_rank)
+                                rb_rank=rb_rank, scratch=scratch)
+    del scratch
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     opts = NewtonOptions(abs_tol=abs_tol, rel_tol=rel_tol, max_iter=max_iter, forcing=forcing,

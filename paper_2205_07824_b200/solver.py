@@ -738,7 +738,7 @@ def element_neighbor_sets(topology, n_elements):
 
 def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, perm=None,
                        mode="tangent", residual_fn=None, base_residual=None, all_colors=None,
-                       invert="auto", share=True):
+                       invert="auto", share=True, scratch=None):
     """Exact diagonal blocks by coloured unit probes (solver.py:303-346):
     colours x bs device Jacobian-vector products (``mode`` "tangent" through
     ``tangent_fn``, "fd" through ``residual_fn`` like jacobian_vector), then
@@ -755,7 +755,14 @@ def build_block_jacobi(tangent_fn, state, n_blocks, bs, colors, native=None, per
     x, _ = _as_device(state)
     dev = x.device
     colors = np.asarray(colors, dtype=np.int64)
-    mats = torch.zeros((n_blocks, bs, bs), dtype=torch.float64, device=dev)
+    if scratch is not None and scratch.is_cuda and scratch.dtype == torch.float64 and \
+            scratch.numel() >= n_blocks * bs * bs and scratch.device == dev:
+        # borrowed device memory (run_steady lends the Krylov basis, unused
+        # until GMRES starts): no multi-GB allocation of its own
+        mats = scratch.reshape(-1)[:n_blocks * bs * bs].view(n_blocks, bs, bs)
+        mats.zero_()
+    else:
+        mats = torch.zeros((n_blocks, bs, bs), dtype=torch.float64, device=dev)
     v = torch.empty(n_blocks * bs, dtype=torch.float64, device=dev)
     st = _lib.stream_ptr()
     if mode == "fd":
